@@ -1,0 +1,345 @@
+"""Benchmark of the PBDR training step (BASELINE.json metric: train images/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One process per GPU (torchrun for N > 1).  A step = forward + backward of a
+batch of views + Adam (Alg. 1) on a synthetic aerial scene
+of the configuration's shape (data: synthetic, random-init Gaussians).
+Prints ONE JSON line on rank 0 (contract in the task statement):
+  value      images/s over the timed K steps, inputs resident in HBM
+  e2e        images/s through the public API with the step's ground-truth
+             images copied H2D from pinned host memory and the losses read back
+  roofline   dominant kernel: algorithmic bytes / CUDA-event duration vs the
+             measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline  the CPU oracle's training step on this host (bounded sample)
+--impl reference times the CPU oracle alone (the reference package has no
+renderer) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1]: 1M Gaussians, 1080p, batch 4, 1 GPU
+    "c2": dict(seed=1, n_points=1_000_000, grid=(1, 1), n_views=8, altitude=50.0, image_size=(1920, 1080),
+               batch=4, G=2048, desc="synthetic 3DGS aerial scene, 1M Gaussians, 1080p cameras, batch 4"),
+    # configs[0]: CPU-oracle-sized case
+    "c1": dict(seed=0, n_points=10_000, grid=(2, 2), n_views=8, altitude=50.0, image_size=(128, 128),
+               batch=1, G=2048, desc="synthetic 3DGS scene, 10K Gaussians, 8 cameras at 128x128, batch 1"),
+}
+METRIC = "train images/s (fwd+bwd) at 1/2/4/8 B200, % HBM roofline; comm bytes/step"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        try:
+            rows = [ln.split(",") for ln in open(self.path).read().strip().splitlines() if ln.strip()]
+        except Exception:
+            return out
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower() == "active":
+                    reasons.add(nm)
+        if sm:
+            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(smax), reasons=sorted(reasons), samples=len(sm))
+        return out
+
+
+def build_scene(cfg, rank=0, world=1):
+    from paper_2512_20017_b200 import scenes
+    from paper_2512_20017_b200.culling import zorder_group
+
+    ds = scenes.generate_aerial_scene(cfg["seed"], cfg["n_points"], cfg["grid"], cfg["n_views"], cfg["altitude"],
+                                      cfg["image_size"])
+    g = zorder_group(ds.cloud, G=cfg["G"])
+    spacing = scenes.mean_spacing(cfg["altitude"], cfg["grid"], cfg["n_points"])
+    params = scenes.init_gaussians(g.sorted_cloud, cfg["seed"], spacing)
+    W, H = cfg["image_size"]
+    gt = scenes.synthetic_gt(cfg["seed"], cfg["n_views"], W, H)
+    return ds, g, params, gt
+
+
+def schedule(n_views, batch, steps, seed=9):
+    """Batches as in run_training_sim (simulator.py:350-358): per epoch a
+    SeedSequence([seed, 2, e]) permutation of the views, partial batch dropped."""
+    out, e = [], 0
+    while len(out) < steps:
+        order = np.random.default_rng(np.random.SeedSequence([seed, 2, e])).permutation(n_views)
+        for i in range(n_views // batch):
+            out.append([int(v) for v in order[i * batch:(i + 1) * batch]])
+        e += 1
+    return out[:steps]
+
+
+def kernel_bytes(stage, last, S, B):
+    """Algorithmic (compulsory) bytes of one launch of a stage."""
+    I, V, slots = last["n_inst"], last["n_rows"], last["n_slots"]
+    npx = slots * last["H"] * last["W"]
+    if stage == "raster_fwd":   # instance list (4 B) + gathered splat (36 B); image 12 + T 4 + n 4 B/px + gt 3 B/px
+        return 40 * I + 23 * npx
+    if stage == "raster_bwd":   # same reads + image/gt re-read + 9 f32 atomics per splat
+        return 40 * I + 23 * npx + 36 * V
+    if stage == "project":      # 240 B params per visible point (once) + mask + 48 B per row
+        return 240 * last["n_visible_points"] + 4 * S + 48 * V
+    if stage == "project_bwd_adam":  # params/m/v read+write (60 f32 each) + mask + 36 B G_SP per row
+        return 6 * 240 * S + 4 * S + 36 * V
+    if stage == "cull":
+        return 16 * S + 4 * S
+    return None
+
+
+def run_ours(args, cfg):
+    import torch
+
+    from paper_2512_20017_b200 import _native as nat
+    from paper_2512_20017_b200 import scenes
+    from paper_2512_20017_b200.trainer import AdamConfig, SplatTrainer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    t0 = time.time()
+    ds, g, params, gt = build_scene(cfg)
+    setup_s = time.time() - t0
+    W, H = cfg["image_size"]
+    B = cfg["batch"]
+    tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt,
+                      adam=AdamConfig(scenes.lr_table(cfg["altitude"])))
+    sched = schedule(cfg["n_views"], B, args.warmup + 2 * args.steps + 2)
+    for i in range(args.warmup):
+        tr.step(sched[i])
+    torch.cuda.synchronize()
+    # ---- timed region: device-resident inputs
+    tr.timers = {}
+    lc0 = nat.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    inst, rows = [], []
+    with ClockSampler(local) as clk:
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        start.record()
+        for i in range(args.steps):
+            tr.step(sched[args.warmup + i])
+            inst.append(tr.last["n_inst"])
+            rows.append(tr.last["n_rows"])
+        end.record()
+        torch.cuda.synchronize()
+    launches = nat.launch_count() - lc0
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    stage_ms = {k: float(np.mean([s.elapsed_time(e) for s, e in v])) for k, v in tr.timers.items()}
+    tr.timers = None
+    ms_per_step = ms / args.steps
+    images = B * world * args.steps
+    value = images / (ms / 1000.0)
+    # ---- e2e: public API with pinned host ground truth, loss read back
+    pinned = torch.from_numpy(gt).pin_memory()
+    e2e_sched = sched[args.warmup + args.steps: args.warmup + 2 * args.steps]
+    gt_dev = torch.empty((B, H, W, 3), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    t_e2e0 = time.perf_counter()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record()
+    loss_host = None
+    for b in e2e_sched:
+        gt_dev.copy_(pinned[b], non_blocking=True)
+        losses = tr.step(b, gt_batch=gt_dev)
+        loss_host = losses.cpu()
+    e_end.record()
+    torch.cuda.synchronize()
+    e2e_ms = e_start.elapsed_time(e_end)
+    e2e_wall = (time.perf_counter() - t_e2e0) * 1000.0
+    e2e_value = B * world * len(e2e_sched) / (max(e2e_ms, e2e_wall) / 1000.0)
+    # ---- roofline of the dominant kernel
+    peak, peak_kind = _peaks()
+    last = dict(tr.last, H=H, W=W, n_visible_points=int(tr.last.get("n_visible_points", tr.S)))
+    dom = max(stage_ms, key=stage_ms.get) if stage_ms else None
+    roof = None
+    if dom:
+        nbytes = kernel_bytes(dom, dict(last, n_inst=int(np.mean(inst)), n_rows=int(np.mean(rows))), tr.S, B)
+        ach = nbytes / (stage_ms[dom] / 1000.0) / 1e9 if nbytes else None
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": (ach / peak) if ach else None, "traffic": None, "peak_kind": peak_kind,
+                "bytes_per_launch": nbytes, "ms_per_launch": stage_ms[dom]}
+    stages = {}
+    for k, v in stage_ms.items():
+        nb = kernel_bytes(k, dict(last, n_inst=int(np.mean(inst)), n_rows=int(np.mean(rows))), tr.S, B)
+        stages[k] = {"ms": round(v, 4), "share": round(v / ms_per_step, 4),
+                     "gbs": round(nb / (v / 1000.0) / 1e9, 1) if nb else None}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, ds, g, params, gt, steps=1)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "n_points": cfg["n_points"], "image": list(cfg["image_size"]),
+                       "global_batch": B * world, "views": cfg["n_views"], "group_size": cfg["G"],
+                       "parallelism": f"points+images x{world}",
+                       "l2": "inputs larger than L2 (params+Adam state %.0f MB)" % (3 * tr.params.numel() * 4 / 1e6)},
+            "e2e": {"value": round(e2e_value, 3), "unit": "images/s", "h2d_bytes_per_step": B * H * W * 3,
+                    "d2h_bytes_per_step": 4 * B},
+            "roofline": roof,
+            "stages": stages,
+            "instances_per_step": int(np.mean(inst)), "splat_rows_per_step": int(np.mean(rows)),
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "setup_s": round(setup_s, 1),
+            "final_loss": None if loss_host is None else [round(float(x), 5) for x in loss_host],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_baseline(cfg, ds, g, params, gt, steps=1, warmup=0):
+    """CPU oracle training step on this host, bounded sample: 1 view of the
+    configuration per step, all host threads."""
+    from oracle import py_oracle
+    from paper_2512_20017_b200 import scenes
+    from paper_2512_20017_b200.culling import batch_planes
+    from paper_2512_20017_b200.trainer import camera_bytes
+
+    p = np.ascontiguousarray(params.copy())
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+    lr = scenes.lr_table(cfg["altitude"])
+    views = [ds.views[i % len(ds.views)] for i in range(steps + warmup)]
+    for k in range(warmup):
+        py_oracle.train_step(p, m, v, batch_planes([views[k]], 1), camera_bytes([views[k]]), gt[views[k].id:views[k].id + 1],
+                             3, lr, 0.9, 0.999, 1e-15, k + 1)
+    t0 = time.perf_counter()
+    for k in range(warmup, warmup + steps):
+        vv = views[k]
+        py_oracle.train_step(p, m, v, batch_planes([vv], 1), camera_bytes([vv]), gt[vv.id:vv.id + 1], 3, lr, 0.9,
+                             0.999, 1e-15, k + 1)
+    dt = time.perf_counter() - t0
+    return {"value": round(steps / dt, 5), "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{steps} step(s) x 1 view of the same scene ({cfg['n_points']} Gaussians, "
+                      f"{cfg['image_size'][0]}x{cfg['image_size'][1]}), oracle/splat_oracle.c OpenMP",
+            "seconds": round(dt, 2)}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ds, g, params, gt = build_scene_host(cfg)
+    cpu = cpu_baseline(cfg, ds, g, params, gt, steps=args.steps, warmup=min(args.warmup, 1))
+    line = {"metric": METRIC, "impl": "reference", "value": cpu["value"], "unit": "images/s",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1000.0 / cpu["value"], 2), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "n_points": cfg["n_points"], "image": list(cfg["image_size"]),
+                       "global_batch": cfg["batch"]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": cpu["value"], "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def build_scene_host(cfg):
+    """Scene on the host only (reference arm: no GPU involvement)."""
+    from oracle import py_oracle
+    from paper_2512_20017_b200 import scenes
+
+    ds = scenes.generate_aerial_scene(cfg["seed"], cfg["n_points"], cfg["grid"], cfg["n_views"], cfg["altitude"],
+                                      cfg["image_size"])
+    perm, gb, aabb = py_oracle.zorder_layout(ds.cloud.positions, cfg["G"])
+    sorted_cloud = scenes.PointCloud(ds.cloud.positions[perm])
+    params = scenes.init_gaussians(sorted_cloud, cfg["seed"],
+                                   scenes.mean_spacing(cfg["altitude"], cfg["grid"], cfg["n_points"]))
+    W, H = cfg["image_size"]
+    return ds, None, params, scenes.synthetic_gt(cfg["seed"], cfg["n_views"], W, H)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,283 @@
+/*
+ * splat_b200.h — C ABI of the B200-native point-based differentiable
+ * rendering (PBDR) training step (Algorithm 1 of arxiv 2512.20017,
+ * PAPER.md:465-518).
+ *
+ * Every entry point is a stateless, asynchronous launch on the caller's
+ * CUDA stream.  All pointers are DEVICE pointers unless the parameter name
+ * ends in `_host`.  The caller owns all memory (torch tensors on the Python
+ * side); the library never allocates.  Return value: 0 on success, otherwise
+ * a bs_status code whose meaning maps 1:1 onto the reference's exception
+ * classes (pkg/src/splatsched/errors.py:8-51); the message is available
+ * from bs_last_error() (thread-local).
+ *
+ * Interfaces replaced (reference file:line, /root/reference/pkg/src/splatsched):
+ *   bs_cull_count      visibility.py:237-252 cull_points, 263-276 cull_group,
+ *                      283-292 _candidate_indices, 308-358 build_access_matrix,
+ *                      partition.py:65-97 build_bipartite_graph (edge mode),
+ *                      PAPER.md:474-483 pts_culling + C[v]_k (mask mode)
+ *   bs_bbox            scene.py:109-112 PointCloud.bbox
+ *   bs_morton_codes    visibility.py:33-62 _quantize/_interleave3/morton_codes
+ *   bs_radix_sort_*    visibility.py:122 np.argsort(kind="stable")
+ *   bs_group_aabb      visibility.py:127-133 (group AABBs of zorder_group)
+ *   bs_scan_counts     (row layout of SP[v]_k)
+ *   bs_project_fwd     PAPER.md:418,452 pts_splatting (3DGS, 11-element SP,
+ *                      PAPER.md:1192-1200)
+ *   bs_bin_*           PAPER.md:264 "sorts ... splats by their distance"
+ *   bs_raster_fwd      PAPER.md:264,494 image_render forward
+ *   bs_l1_loss         PAPER.md:495 loss_fn
+ *   bs_raster_bwd      PAPER.md:503 image_render.backward
+ *   bs_project_bwd     PAPER.md:513-514 pts_splatting.backward
+ *   bs_adam_step       PAPER.md:517 AdamUpdate
+ *   bs_project_bwd_adam  PAPER.md:511-517 (lines 23-27 of Alg. 1 fused)
+ */
+#ifndef SPLAT_B200_H
+#define SPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py:8-51) ------------------------------------ */
+enum {
+  BS_OK = 0,
+  BS_ERR_PARAMETER = 1,     /* ParameterError     errors.py:12-13 */
+  BS_ERR_CONFIGURATION = 2, /* ConfigurationError errors.py:16-17 */
+  BS_ERR_CONSISTENCY = 3,   /* ConsistencyError   errors.py:20-21 */
+  BS_ERR_CONSTRAINT = 4,    /* ConstraintError    errors.py:24-25 */
+  BS_ERR_CUDA = 5,          /* CUDA runtime failure (no reference analogue) */
+  BS_ERR_CAPACITY = 6       /* caller buffer too small (ParameterError) */
+};
+
+const char* bs_last_error(void);
+int32_t bs_abi_version(void);
+/* Number of kernel launches issued by this library since load (for the
+ * bench's gpu_launches claim). */
+int64_t bs_launch_count(void);
+
+/* ---- parameter layout --------------------------------------------------
+ * A shard of S points is stored as BS_PARAM_PLANES planes of float4, plane
+ * p at float offset p*S*4:
+ *   plane 0  : mean.x mean.y mean.z opacity_logit
+ *   plane 1  : log_scale.x log_scale.y log_scale.z 0      (2DGS: .z unused)
+ *   plane 2  : quat.w quat.x quat.y quat.z
+ *   plane 3+ : SH coefficients, flat index f = 3*k + channel (k = 0..15),
+ *              plane 3 + f/4, lane f%4
+ * 59 live floats per point ("59 attributes") + 1 pad. */
+#define BS_PARAM_PLANES 15
+#define BS_PARAM_FLOATS 60
+/* splat-state row (SP): 12 floats, 48 B; the 11 elements of PAPER.md
+ * Table tab:states-3dgs + 1 pad:
+ *   0 u  1 v  2 opacity  3 conic_a  4 conic_b  5 conic_c
+ *   6 r  7 g  8 b        9 depth    10 radius  11 pad (0) */
+#define BS_SP_FLOATS 12
+/* gradient row (G_SP): 9 floats (d u, d v, d opacity, d conic a/b/c, d rgb) */
+#define BS_GSP_FLOATS 9
+#define BS_TILE 16
+
+/* Camera of one view, float32, as consumed by the projection and raster
+ * kernels.  Convention of CameraView (scene.py:126-131): +x right, +y down,
+ * +z forward; rot_cw = rotation^T maps world to camera; pixel x of a
+ * camera-frame point q is fx*q.x/q.z + cx (test_visibility.py:204-215). */
+typedef struct {
+  float rot_cw[9]; /* row-major world->camera rotation */
+  float pos[3];    /* camera centre, world */
+  float fx, fy, cx, cy;
+  float lim_x, lim_y; /* 1.3 * tan(fov/2): EWA Jacobian clamp */
+  float near_plane, far_plane;
+  int32_t width, height;
+} bs_camera;
+
+/* ---- K0: culling / access counts --------------------------------------- */
+enum {
+  BS_CULL_ACCESS_EXACT = 0,  /* out0: int64 [B*P*P, n_gpus] (build_access_matrix EXACT) */
+  BS_CULL_ACCESS_GROUP = 1,  /* out0: int64 [B*P*P, n_gpus] (GROUP_APPROX) */
+  BS_CULL_EDGES = 2,         /* out0: int32 [n_groups, B] per-(group,view) counts */
+  BS_CULL_MASK = 3           /* out0: uint32 [n] view bitmask (B<=32),
+                                out1: int32 [n_groups, B] counts,
+                                out2: int64 [B*P*P] per-patch counts (may be NULL) */
+};
+
+typedef struct {
+  int32_t mode;
+  int32_t n_views;    /* B */
+  int32_t P;          /* patch factor >= 1 */
+  int32_t n_gpus;     /* columns of the access matrix (ACCESS modes) */
+  int32_t temporal;   /* 1: also test presence[i,0] <= t <= presence[i,1] in f32 */
+  int32_t pos_stride; /* floats between consecutive positions: 3 or 4 */
+} bs_cull_desc;
+
+/* planes: float64 [B][2 + 2*(P+1)][4]: near, far, x-edges c=0..P,
+ *   y-edges r=0..P, each (nx, ny, nz, offset) exactly as numpy computes
+ *   them in frustum_from_view (visibility.py:168-217).  Patch (r,c) of a
+ *   view holds p iff near>=0, far>=0, xe[c]>=0, xe[c+1]<0, ye[r]>=0,
+ *   ye[r+1]<0 with d = fma(z,nz,fma(y,ny,x*nx)) + offset in f64.
+ * group_begin: int32 [n_groups+1] point offsets; group_aabb: float32
+ *   [n_groups][2][3] (min; max) or NULL (no AABB early-out; ACCESS_GROUP
+ *   requires it).  point_gpu: int32 [n] or NULL (all points -> column 0).
+ * presence: float32 [n][2] or NULL; view_times: float32 [B] or NULL. */
+int32_t bs_cull_count(const bs_cull_desc* desc_host, const float* positions,
+                      int64_t n_points, const float* presence,
+                      const int32_t* group_begin, const float* group_aabb,
+                      int32_t n_groups, const double* planes,
+                      const float* view_times, const int32_t* point_gpu,
+                      void* out0, void* out1, void* out2, void* stream);
+
+/* ---- Morton codes / grouping ------------------------------------------ */
+/* bbox_out: float32 [2][3] (min; max) of positions (exact reduction). */
+int32_t bs_bbox(const float* positions, int64_t n, int32_t pos_stride,
+                float* bbox_out, void* workspace, size_t ws_bytes,
+                void* stream);
+size_t bs_bbox_workspace(int64_t n);
+/* codes[i] = interleave(clip(floor((p - min)/extent*(2^b-1)))) in f64. */
+int32_t bs_morton_codes(const float* positions, int64_t n, int32_t pos_stride,
+                        const float* bbox, int32_t bits_per_axis,
+                        uint64_t* codes, void* stream);
+/* AABB of each group of G consecutive points (last group may be short). */
+int32_t bs_group_aabb(const float* positions, int64_t n, int32_t pos_stride,
+                      int32_t G, float* aabb_out, void* stream);
+/* out[i, :] = in[idx[i], :] for rows of `row_floats` floats (float4-aligned
+ * plane layout aware: in/out are plane-major with n_in / n_out rows). */
+int32_t bs_gather_planes(const float* in, int64_t n_in, const int64_t* idx,
+                         int64_t n_out, int32_t n_planes, float* out,
+                         void* stream);
+
+/* ---- radix sort (stable LSD, 8-bit digits) ----------------------------- */
+/* Sorts (keys, vals) by bits [begin_bit, end_bit).  n is read from
+ * n_dev (device int64) when non-NULL, else n_host.  Result is in keys/vals;
+ * keys_alt/vals_alt are scratch of the same capacity. */
+size_t bs_radix_sort_workspace(int64_t capacity);
+int32_t bs_radix_sort_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt,
+                          uint32_t* vals_alt, int64_t n_host,
+                          const int64_t* n_dev, int32_t begin_bit,
+                          int32_t end_bit, void* workspace, size_t ws_bytes,
+                          void* stream);
+int32_t bs_radix_sort_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt,
+                          uint32_t* vals_alt, int64_t n_host,
+                          const int64_t* n_dev, int32_t begin_bit,
+                          int32_t end_bit, void* workspace, size_t ws_bytes,
+                          void* stream);
+
+/* ---- row layout of the splat state ------------------------------------ */
+/* counts: int32 [n_groups][B] (from BS_CULL_MASK).  view_order: int32 [B]
+ * host array (NULL = identity); rows are laid out view-major in this order.
+ * Outputs: base: int32 [n_groups][B] first row of (group, view) relative to
+ * the view's first row; view_rows: int64 [B] visible points per view;
+ * view_row0: int64 [B] first row of each view. */
+int32_t bs_scan_counts(const int32_t* counts, int32_t n_groups,
+                       int32_t n_views, const int32_t* view_order_host,
+                       int32_t* base, int64_t* view_rows, int64_t* view_row0,
+                       void* stream);
+
+/* ---- K1: projection (pts_splatting) ------------------------------------ */
+typedef struct {
+  int32_t n_views;
+  int32_t sh_degree; /* 0..3 */
+  int32_t tiles_x_max, tiles_y_max;
+} bs_proj_desc;
+int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
+                       int64_t n_points, const uint32_t* vis_mask,
+                       const int32_t* group_begin, int32_t n_groups,
+                       const int32_t* base, const int64_t* view_row0,
+                       const bs_camera* cams, float* sp_rows, void* stream);
+
+/* ---- K2: tile binning ------------------------------------------------- */
+/* Rows [seg_row0[s], seg_row0[s+1]) belong to render slot seg_slot[s].
+ * Step 1: depth keys ((slot<<32)|f32bits(depth)) for every row. */
+int32_t bs_bin_depth_keys(const float* sp_rows, int64_t n_rows,
+                          const int64_t* seg_row0, const int32_t* seg_slot,
+                          int32_t n_segs, uint64_t* keys, uint32_t* vals,
+                          void* stream);
+/* Step 2: per depth-sorted row, number of tiles (reads sp row radius/uv);
+ * writes int64 inclusive prefix counts into offsets [n_rows] and the total
+ * into total_dev[0]. */
+int32_t bs_bin_count(const float* sp_rows, const uint32_t* sorted_rows,
+                     int64_t n_rows, const uint64_t* sorted_keys,
+                     const bs_camera* slot_cams, int64_t* offsets,
+                     int64_t* total_dev, void* workspace, size_t ws_bytes,
+                     void* stream);
+size_t bs_bin_count_workspace(int64_t n_rows);
+/* Step 3: emit (slot*tiles_per_slot + tile, row) instances in depth order. */
+int32_t bs_bin_emit(const float* sp_rows, const uint32_t* sorted_rows,
+                    int64_t n_rows, const uint64_t* sorted_keys,
+                    const bs_camera* slot_cams, int32_t tiles_per_slot,
+                    const int64_t* offsets, uint32_t* inst_keys,
+                    uint32_t* inst_rows, void* stream);
+/* Step 4: ranges int32 [n_slots*tiles_per_slot][2] = [start, end). */
+int32_t bs_tile_ranges(const uint32_t* inst_keys, const int64_t* n_dev,
+                       int64_t n_host, int32_t n_buckets, int32_t* ranges,
+                       void* stream);
+
+/* ---- K3/L/K4: rasterisation ------------------------------------------- */
+typedef struct {
+  int32_t n_slots;
+  int32_t tiles_per_slot; /* bucket stride (max tiles_x*tiles_y) */
+  int32_t width, height;  /* common image size of all slots */
+  float bg[3];
+  int32_t loss_fused;     /* 1: gt given, fwd writes L1 partials per tile */
+} bs_raster_desc;
+/* image: f32 [n_slots][H][W][3]; final_T: f32 [n_slots][H][W];
+ * n_contrib: int32 [n_slots][H][W] (range-relative end of the blend);
+ * gt: u8 [*][H][W][3] or NULL, image of slot s at gt_slot_view[s] (NULL =
+ * identity); loss_tiles: f32 [n_slots][tiles]. */
+int32_t bs_raster_fwd(const bs_raster_desc* desc_host, const float* sp_rows,
+                      const uint32_t* inst_rows, const int32_t* ranges,
+                      float* image, float* final_T, int32_t* n_contrib,
+                      const uint8_t* gt, const int32_t* gt_slot_view,
+                      float* loss_tiles, void* stream);
+/* mean-L1 loss per slot: loss[s] = mean|img - gt/255|; grad = d loss/d img
+ * (grad may be NULL).  The fused training step instead reduces the per-tile
+ * partials of bs_raster_fwd with bs_reduce_loss_tiles. */
+int32_t bs_l1_loss(const float* image, const uint8_t* gt, int32_t n_slots,
+                   int32_t height, int32_t width, float* loss, float* grad,
+                   void* workspace, size_t ws_bytes, void* stream);
+size_t bs_l1_loss_workspace(int32_t n_slots);
+int32_t bs_reduce_loss_tiles(const float* loss_tiles, int32_t n_slots,
+                             int32_t tiles_per_slot, int32_t height,
+                             int32_t width, float* loss, void* stream);
+/* dL/dimage either given (grad_image f32 [n_slots][H][W][3]) or, when NULL,
+ * the mean-L1 gradient recomputed from image and gt.  g_sp: f32 [n_rows][9]
+ * accumulated with atomics (caller zeroes it). */
+int32_t bs_raster_bwd(const bs_raster_desc* desc_host, const float* sp_rows,
+                      const uint32_t* inst_rows, const int32_t* ranges,
+                      const float* image, const float* final_T,
+                      const int32_t* n_contrib, const float* grad_image,
+                      const uint8_t* gt, const int32_t* gt_slot_view,
+                      float* g_sp, void* stream);
+
+/* ---- K1b + K5 ---------------------------------------------------------- */
+/* grad_params: plane layout like params, ACCUMULATED (caller zeroes). */
+int32_t bs_project_bwd(const bs_proj_desc* desc_host, const float* params,
+                       int64_t n_points, const uint32_t* vis_mask,
+                       const int32_t* group_begin, int32_t n_groups,
+                       const int32_t* base, const int64_t* view_row0,
+                       const bs_camera* cams, const float* g_sp,
+                       float* grad_params, void* stream);
+
+typedef struct {
+  float lr[BS_PARAM_FLOATS]; /* per (plane, lane) learning rate */
+  float beta1, beta2, eps;
+  int32_t step;       /* 1-based step count for bias correction */
+  int32_t selective;  /* 1: skip points with vis_mask == 0 */
+} bs_adam_desc;
+int32_t bs_adam_step(const bs_adam_desc* desc_host, float* params,
+                     const float* grads, float* exp_avg, float* exp_avg_sq,
+                     int64_t n_points, const uint32_t* vis_mask, void* stream);
+/* Fused: projection backward over all views of each point followed by the
+ * Adam update of that point; no grad_params round trip through HBM. */
+int32_t bs_project_bwd_adam(const bs_proj_desc* pdesc_host,
+                            const bs_adam_desc* adesc_host, float* params,
+                            float* exp_avg, float* exp_avg_sq,
+                            int64_t n_points, const uint32_t* vis_mask,
+                            const int32_t* group_begin, int32_t n_groups,
+                            const int32_t* base, const int64_t* view_row0,
+                            const bs_camera* cams, const float* g_sp,
+                            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLAT_B200_H */

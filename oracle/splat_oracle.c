@@ -1,0 +1,735 @@
+/*
+ * CPU oracle of the PBDR training-step hot path (test infrastructure; see
+ * splat_oracle.h).  Build: gcc -O2 -fopenmp -ffp-contract=off (no FMA
+ * contraction: every float op rounds separately, so the projection below
+ * performs exactly the op sequence of the sm_100a kernel and reproduces its
+ * splat state bit-for-bit).
+ *
+ * Reference citations (/root/reference):
+ *   culling / access counts  pkg/src/splatsched/visibility.py:153-161,
+ *                            237-252, 263-292, 308-358
+ *   Morton codes             visibility.py:33-62
+ *   training step            PAPER.md:465-518 (Alg. 1), rendering outline
+ *                            PAPER.md:264, splat state PAPER.md:1192-1200
+ */
+#include "splat_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define TILE 16
+#define SPF 12
+#define GSPF 9
+
+/* ------------------------------------------------------------------------ */
+/* culling (visibility.py)                                                  */
+
+/* p @ planes[:, :3].T + planes[:, 3] as OpenBLAS evaluates it for >= 2 rows
+ * (visibility.py:155-156; order measured in SURVEY.md §0.6). */
+static double pdist(const double* pl, double x, double y, double z) {
+  return fma(z, pl[2], fma(y, pl[1], x * pl[0])) + pl[3];
+}
+
+/* plane pointer of a view block: 0 near, 1 far, 2+c x-edge c, 3+P+r y-edge r */
+static const double* vplane(const double* vp, int k) { return vp + 4 * k; }
+
+/* cull_group (visibility.py:263-276) for patch (r, c); 1 = OUTSIDE. */
+static int group_outside(const double* vp, int P, int r, int c, const float* box) {
+  const double* pl[6] = {vplane(vp, 0), vplane(vp, 1), vplane(vp, 2 + c), vplane(vp, 2 + c + 1),
+                         vplane(vp, 3 + P + r), vplane(vp, 3 + P + r + 1)};
+  const int neg[6] = {0, 0, 0, 1, 0, 1};
+  for (int k = 0; k < 6; ++k) {
+    int all = 1;
+    for (int i = 0; i < 2 && all; ++i)
+      for (int j = 0; j < 2 && all; ++j)
+        for (int l = 0; l < 2 && all; ++l) {
+          const double d = pdist(pl[k], (double)box[3 * i + 0], (double)box[3 * j + 1], (double)box[3 * l + 2]);
+          /* the exclusive plane is the negation: -d < 0  <=>  d > 0 */
+          all = neg[k] ? (d > 0.0) : (d < 0.0);
+        }
+    if (all) return 1;
+  }
+  return 0;
+}
+
+/* Frustum.contains for patch (r, c) (visibility.py:158-161). */
+static int in_patch(const double* vp, int P, int r, int c, double x, double y, double z) {
+  if (!(pdist(vplane(vp, 0), x, y, z) >= 0.0)) return 0;
+  if (!(pdist(vplane(vp, 1), x, y, z) >= 0.0)) return 0;
+  if (!(pdist(vplane(vp, 2 + c), x, y, z) >= 0.0)) return 0;
+  if (!(-pdist(vplane(vp, 2 + c + 1), x, y, z) > 0.0)) return 0;
+  if (!(pdist(vplane(vp, 3 + P + r), x, y, z) >= 0.0)) return 0;
+  if (!(-pdist(vplane(vp, 3 + P + r + 1), x, y, z) > 0.0)) return 0;
+  return 1;
+}
+
+void or_access_matrix(const float* pos, int64_t n, const int32_t* gb, const float* aabb, int32_t ng,
+                      const double* planes, int32_t B, int32_t P, const int32_t* point_gpu, int32_t N, int32_t mode,
+                      const float* presence, const float* view_times, int64_t* out) {
+  (void)n;
+  const int npl = 2 + 2 * (P + 1);
+  memset(out, 0, sizeof(int64_t) * (size_t)B * P * P * N);
+  for (int v = 0; v < B; ++v) {
+    const double* vp = planes + (size_t)v * npl * 4;
+    for (int r = 0; r < P; ++r)
+      for (int c = 0; c < P; ++c) {
+        int64_t* row = out + ((size_t)v * P * P + r * P + c) * N;
+        for (int g = 0; g < ng; ++g) {
+          if (aabb && group_outside(vp, P, r, c, aabb + 6 * (size_t)g)) continue; /* _candidate_indices */
+          for (int i = gb[g]; i < gb[g + 1]; ++i) {
+            int ok = 1;
+            if (mode == 0) {
+              ok = in_patch(vp, P, r, c, pos[3 * (size_t)i], pos[3 * (size_t)i + 1], pos[3 * (size_t)i + 2]);
+              if (ok && presence) {
+                const float t = view_times[v]; /* f32 compare (visibility.py:251) */
+                ok = (presence[2 * (size_t)i] <= t) && (t <= presence[2 * (size_t)i + 1]);
+              }
+            }
+            if (ok) row[point_gpu ? point_gpu[i] : 0] += 1;
+          }
+        }
+      }
+  }
+}
+
+void or_visibility_mask(const float* pos, int64_t n, const int32_t* gb, const float* aabb, int32_t ng,
+                        const double* planes, int32_t B, uint32_t* mask) {
+  memset(mask, 0, sizeof(uint32_t) * (size_t)n);
+  const int npl = 6;
+  for (int v = 0; v < B; ++v) {
+    const double* vp = planes + (size_t)v * npl * 4;
+    for (int g = 0; g < ng; ++g) {
+      if (aabb && group_outside(vp, 1, 0, 0, aabb + 6 * (size_t)g)) continue;
+      for (int i = gb[g]; i < gb[g + 1]; ++i)
+        if (in_patch(vp, 1, 0, 0, pos[3 * (size_t)i], pos[3 * (size_t)i + 1], pos[3 * (size_t)i + 2]))
+          mask[i] |= 1u << v;
+    }
+  }
+}
+
+/* _quantize + _interleave3 (visibility.py:33-52) */
+void or_morton(const float* pos, int64_t n, const float* bbox, int32_t bits, uint64_t* codes) {
+  const double scale = (double)((1ull << bits) - 1);
+  double mn[3], ext[3];
+  for (int k = 0; k < 3; ++k) {
+    mn[k] = (double)bbox[k];
+    ext[k] = (double)bbox[3 + k] - mn[k];
+    if (ext[k] == 0.0) ext[k] = 1.0;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t q[3];
+    for (int k = 0; k < 3; ++k) {
+      double t = floor(((double)pos[3 * i + k] - mn[k]) / ext[k] * scale);
+      if (t < 0) t = 0;
+      if (t > scale) t = scale;
+      q[k] = (uint64_t)t;
+    }
+    uint64_t code = 0;
+    for (int b = 0; b < bits; ++b) {
+      code |= ((q[0] >> b) & 1ull) << (3 * b);
+      code |= ((q[1] >> b) & 1ull) << (3 * b + 1);
+      code |= ((q[2] >> b) & 1ull) << (3 * b + 2);
+    }
+    codes[i] = code;
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* projection (pts_splatting) -- same op sequence as csrc/splat_math.cuh     */
+
+static const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+static const float C2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                            -1.0925484305920792f, 0.5462742152960396f};
+static const float C3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
+                            0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
+                            -0.5900435899266435f};
+
+typedef union {
+  float f;
+  uint32_t u;
+} fbits;
+
+float or_det_expf(float x) {
+  x = fminf(fmaxf(x, -80.0f), 80.0f);
+  const float n = rintf(x * 0x1.715476p+0f);
+  float r = x - n * 0x1.62e400p-1f;
+  r = r - n * 0x1.7f7d1cp-20f;
+  float p = 0x1.6c16c2p-10f;
+  p = p * r + 0x1.111112p-7f;
+  p = p * r + 0x1.555556p-5f;
+  p = p * r + 0x1.555556p-3f;
+  p = p * r + 0x1.000000p-1f;
+  p = p * r + 1.0f;
+  p = p * r + 1.0f;
+  fbits s;
+  s.u = (uint32_t)((int)n + 127) << 23;
+  return p * s.f;
+}
+
+typedef struct {
+  float p[3], op, ls[3], q[4], sh[48];
+} opoint;
+
+typedef struct {
+  float d[3], qc[3], s[3], qn[4], qnorm, Rq[9], Sc[9];
+  float J00, J02, J11, J12, tx, ty;
+  int clamp_x, clamp_y;
+  float a, b, c, det, conic[3], radius, u, v, depth, len, dir[3], Y[16], col_raw[3], col[3], opac;
+  int valid;
+} oproj;
+
+static void load_opoint(const float* params, int64_t S, int64_t i, opoint* pt) {
+  const float* p0 = params + 4 * i;
+  const float* p1 = params + 4 * (S + i);
+  const float* p2 = params + 4 * (2 * S + i);
+  for (int k = 0; k < 3; ++k) pt->p[k] = p0[k];
+  pt->op = p0[3];
+  for (int k = 0; k < 3; ++k) pt->ls[k] = p1[k];
+  for (int k = 0; k < 4; ++k) pt->q[k] = p2[k];
+  for (int f = 0; f < 48; ++f) pt->sh[f] = params[4 * ((3 + f / 4) * S + i) + (f % 4)];
+}
+
+static void sh_basis(const float* dir, int n_sh, float* Y) {
+  const float x = dir[0], y = dir[1], z = dir[2];
+  for (int k = 0; k < 16; ++k) Y[k] = 0.f;
+  Y[0] = C0;
+  if (n_sh > 1) {
+    Y[1] = -C1 * y;
+    Y[2] = C1 * z;
+    Y[3] = -C1 * x;
+  }
+  if (n_sh > 4) {
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    Y[4] = C2[0] * xy;
+    Y[5] = C2[1] * yz;
+    Y[6] = C2[2] * ((2.f * zz - xx) - yy);
+    Y[7] = C2[3] * xz;
+    Y[8] = C2[4] * (xx - yy);
+    if (n_sh > 9) {
+      Y[9] = (C3[0] * y) * (3.f * xx - yy);
+      Y[10] = (C3[1] * xy) * z;
+      Y[11] = (C3[2] * y) * ((4.f * zz - xx) - yy);
+      Y[12] = (C3[3] * z) * ((2.f * zz - 3.f * xx) - 3.f * yy);
+      Y[13] = (C3[4] * x) * ((4.f * zz - xx) - yy);
+      Y[14] = (C3[5] * z) * (xx - yy);
+      Y[15] = (C3[6] * x) * (xx - 3.f * yy);
+    }
+  }
+}
+
+static void proj_fwd(const opoint* pt, const or_camera* c, int n_sh, oproj* f) {
+  for (int k = 0; k < 3; ++k) f->d[k] = pt->p[k] - c->pos[k];
+  for (int k = 0; k < 3; ++k)
+    f->qc[k] = (c->rot_cw[3 * k] * f->d[0] + c->rot_cw[3 * k + 1] * f->d[1]) + c->rot_cw[3 * k + 2] * f->d[2];
+  const float z = f->qc[2];
+  for (int k = 0; k < 3; ++k) f->s[k] = or_det_expf(pt->ls[k]);
+  const float nn = ((pt->q[0] * pt->q[0] + pt->q[1] * pt->q[1]) + pt->q[2] * pt->q[2]) + pt->q[3] * pt->q[3];
+  f->qnorm = sqrtf(nn);
+  for (int k = 0; k < 4; ++k) f->qn[k] = pt->q[k] / f->qnorm;
+  const float w = f->qn[0], x = f->qn[1], y = f->qn[2], zq = f->qn[3];
+  const float xx = x * x, yy = y * y, zz = zq * zq, xy = x * y, xz = x * zq, yz = y * zq;
+  const float wx = w * x, wy = w * y, wz = w * zq;
+  float* R = f->Rq;
+  R[0] = 1.f - 2.f * (yy + zz);
+  R[1] = 2.f * (xy - wz);
+  R[2] = 2.f * (xz + wy);
+  R[3] = 2.f * (xy + wz);
+  R[4] = 1.f - 2.f * (xx + zz);
+  R[5] = 2.f * (yz - wx);
+  R[6] = 2.f * (xz - wy);
+  R[7] = 2.f * (yz + wx);
+  R[8] = 1.f - 2.f * (xx + yy);
+  float M[9], Sg[9], T[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) M[3 * i + j] = R[3 * i + j] * f->s[j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = i; j < 3; ++j) {
+      const float v = (M[3 * i] * M[3 * j] + M[3 * i + 1] * M[3 * j + 1]) + M[3 * i + 2] * M[3 * j + 2];
+      Sg[3 * i + j] = v;
+      Sg[3 * j + i] = v;
+    }
+  const float* W = c->rot_cw;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) T[3 * i + j] = (W[3 * i] * Sg[j] + W[3 * i + 1] * Sg[3 + j]) + W[3 * i + 2] * Sg[6 + j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = i; j < 3; ++j) {
+      const float v = (T[3 * i] * W[3 * j] + T[3 * i + 1] * W[3 * j + 1]) + T[3 * i + 2] * W[3 * j + 2];
+      f->Sc[3 * i + j] = v;
+      f->Sc[3 * j + i] = v;
+    }
+  const float* Sc = f->Sc;
+  const float xr = f->qc[0] / z, yr = f->qc[1] / z;
+  f->clamp_x = (xr < -c->lim_x) || (xr > c->lim_x);
+  f->clamp_y = (yr < -c->lim_y) || (yr > c->lim_y);
+  f->tx = fminf(c->lim_x, fmaxf(-c->lim_x, xr)) * z;
+  f->ty = fminf(c->lim_y, fmaxf(-c->lim_y, yr)) * z;
+  const float z2 = z * z;
+  f->J00 = c->fx / z;
+  f->J11 = c->fy / z;
+  f->J02 = -((c->fx * f->tx) / z2);
+  f->J12 = -((c->fy * f->ty) / z2);
+  float U0[3], U1[3];
+  for (int j = 0; j < 3; ++j) {
+    U0[j] = f->J00 * Sc[j] + f->J02 * Sc[6 + j];
+    U1[j] = f->J11 * Sc[3 + j] + f->J12 * Sc[6 + j];
+  }
+  f->a = (U0[0] * f->J00 + U0[2] * f->J02) + 0.3f;
+  f->b = U0[1] * f->J11 + U0[2] * f->J12;
+  f->c = (U1[1] * f->J11 + U1[2] * f->J12) + 0.3f;
+  f->det = f->a * f->c - f->b * f->b;
+  f->valid = f->det > 0.f;
+  if (f->valid) {
+    f->conic[0] = f->c / f->det;
+    f->conic[1] = (-f->b) / f->det;
+    f->conic[2] = f->a / f->det;
+    const float mid = 0.5f * (f->a + f->c);
+    const float disc = fmaxf(0.1f, mid * mid - f->det);
+    const float l1 = mid + sqrtf(disc);
+    f->radius = ceilf(3.f * sqrtf(l1));
+  } else {
+    f->conic[0] = f->conic[1] = f->conic[2] = 0.f;
+    f->radius = 0.f;
+  }
+  f->u = c->fx * xr + c->cx;
+  f->v = c->fy * yr + c->cy;
+  f->depth = z;
+  f->len = sqrtf((f->d[0] * f->d[0] + f->d[1] * f->d[1]) + f->d[2] * f->d[2]);
+  for (int k = 0; k < 3; ++k) f->dir[k] = f->d[k] / f->len;
+  sh_basis(f->dir, n_sh, f->Y);
+  for (int ch = 0; ch < 3; ++ch) {
+    float acc = f->Y[0] * pt->sh[ch];
+    for (int k = 1; k < n_sh; ++k) acc = acc + f->Y[k] * pt->sh[3 * k + ch];
+    f->col_raw[ch] = acc + 0.5f;
+    f->col[ch] = fmaxf(f->col_raw[ch], 0.f);
+  }
+  f->opac = 1.f / (1.f + or_det_expf(-pt->op));
+}
+
+void or_project(const float* params, int64_t S, const int64_t* idx, int64_t m, const or_camera* c, int32_t sh_degree,
+                float* sp) {
+  const int n_sh = (sh_degree + 1) * (sh_degree + 1);
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < m; ++k) {
+    opoint pt;
+    oproj f;
+    load_opoint(params, S, idx[k], &pt);
+    proj_fwd(&pt, c, n_sh, &f);
+    float* r = sp + k * SPF;
+    r[0] = f.u;
+    r[1] = f.v;
+    r[2] = f.opac;
+    r[3] = f.conic[0];
+    r[4] = f.conic[1];
+    r[5] = f.conic[2];
+    r[6] = f.col[0];
+    r[7] = f.col[1];
+    r[8] = f.col[2];
+    r[9] = f.depth;
+    r[10] = f.valid ? f.radius : 0.f;
+    r[11] = 0.f;
+  }
+}
+
+/* Analytic backward of proj_fwd (chain rule written out independently of the
+ * CUDA file; checked against float64 autograd in tests). */
+static void proj_bwd(const opoint* pt, const or_camera* c, int n_sh, const oproj* f, const float* gsp, float* g) {
+  if (!f->valid) return;
+  float dc[3];
+  for (int ch = 0; ch < 3; ++ch) dc[ch] = f->col_raw[ch] >= 0.f ? gsp[6 + ch] : 0.f;
+  float wk[16] = {0};
+  for (int k = 0; k < n_sh; ++k)
+    for (int ch = 0; ch < 3; ++ch) {
+      g[12 + 3 * k + ch] += f->Y[k] * dc[ch];
+      wk[k] += dc[ch] * pt->sh[3 * k + ch];
+    }
+  /* gradient of sum_k wk[k] Y_k(dir) w.r.t. dir */
+  const float x = f->dir[0], y = f->dir[1], z = f->dir[2];
+  float gd[3] = {0, 0, 0};
+  if (n_sh > 1) {
+    gd[1] -= C1 * wk[1];
+    gd[2] += C1 * wk[2];
+    gd[0] -= C1 * wk[3];
+  }
+  if (n_sh > 4) {
+    gd[0] += C2[0] * y * wk[4];
+    gd[1] += C2[0] * x * wk[4];
+    gd[1] += C2[1] * z * wk[5];
+    gd[2] += C2[1] * y * wk[5];
+    gd[0] -= 2.f * C2[2] * x * wk[6];
+    gd[1] -= 2.f * C2[2] * y * wk[6];
+    gd[2] += 4.f * C2[2] * z * wk[6];
+    gd[0] += C2[3] * z * wk[7];
+    gd[2] += C2[3] * x * wk[7];
+    gd[0] += 2.f * C2[4] * x * wk[8];
+    gd[1] -= 2.f * C2[4] * y * wk[8];
+  }
+  if (n_sh > 9) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    /* Y9 = C3_0 (3 x^2 y - y^3) */
+    gd[0] += C3[0] * 6.f * x * y * wk[9];
+    gd[1] += C3[0] * 3.f * (xx - yy) * wk[9];
+    /* Y10 = C3_1 x y z */
+    gd[0] += C3[1] * y * z * wk[10];
+    gd[1] += C3[1] * x * z * wk[10];
+    gd[2] += C3[1] * x * y * wk[10];
+    /* Y11 = C3_2 (4 y z^2 - x^2 y - y^3) */
+    gd[0] += C3[2] * (-2.f * x * y) * wk[11];
+    gd[1] += C3[2] * (4.f * zz - xx - 3.f * yy) * wk[11];
+    gd[2] += C3[2] * (8.f * y * z) * wk[11];
+    /* Y12 = C3_3 (2 z^3 - 3 x^2 z - 3 y^2 z) */
+    gd[0] += C3[3] * (-6.f * x * z) * wk[12];
+    gd[1] += C3[3] * (-6.f * y * z) * wk[12];
+    gd[2] += C3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * wk[12];
+    /* Y13 = C3_4 (4 x z^2 - x^3 - x y^2) */
+    gd[0] += C3[4] * (4.f * zz - 3.f * xx - yy) * wk[13];
+    gd[1] += C3[4] * (-2.f * x * y) * wk[13];
+    gd[2] += C3[4] * (8.f * x * z) * wk[13];
+    /* Y14 = C3_5 (x^2 z - y^2 z) */
+    gd[0] += C3[5] * (2.f * x * z) * wk[14];
+    gd[1] += C3[5] * (-2.f * y * z) * wk[14];
+    gd[2] += C3[5] * (xx - yy) * wk[14];
+    /* Y15 = C3_6 (x^3 - 3 x y^2) */
+    gd[0] += C3[6] * 3.f * (xx - yy) * wk[15];
+    gd[1] += C3[6] * (-6.f * x * y) * wk[15];
+  }
+  const float dd = x * gd[0] + y * gd[1] + z * gd[2];
+  float gp[3];
+  for (int k = 0; k < 3; ++k) gp[k] = (gd[k] - f->dir[k] * dd) / f->len;
+  g[3] += gsp[2] * f->opac * (1.f - f->opac);
+  const float zc = f->qc[2];
+  float gq[3];
+  gq[0] = gsp[0] * c->fx / zc;
+  gq[1] = gsp[1] * c->fy / zc;
+  gq[2] = -(gsp[0] * c->fx * f->qc[0] + gsp[1] * c->fy * f->qc[1]) / (zc * zc);
+  /* conic = inv(cov2d): d conic / d (a, b, c) */
+  const float A = gsp[3], Bg = gsp[4], Cg = gsp[5];
+  const float a = f->a, b = f->b, cc = f->c, det2 = f->det * f->det;
+  const float ga = (-cc * cc * A + b * cc * Bg - b * b * Cg) / det2;
+  const float gb = (2.f * b * cc * A - (a * cc + b * b) * Bg + 2.f * a * b * Cg) / det2;
+  const float gc = (-b * b * A + a * b * Bg - a * a * Cg) / det2;
+  /* cov2d = J Sc J^T with J = [[J00, 0, J02], [0, J11, J12]] */
+  const float J[2][3] = {{f->J00, 0.f, f->J02}, {0.f, f->J11, f->J12}};
+  const float Gm[2][2] = {{ga, 0.5f * gb}, {0.5f * gb, gc}};
+  float gSc[9] = {0};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      for (int r = 0; r < 2; ++r)
+        for (int s = 0; s < 2; ++s) gSc[3 * i + j] += J[r][i] * Gm[r][s] * J[s][j];
+  float gJ[2][3] = {{0}};
+  for (int r = 0; r < 2; ++r)
+    for (int k = 0; k < 3; ++k)
+      for (int s = 0; s < 2; ++s)
+        for (int m = 0; m < 3; ++m) gJ[r][k] += 2.f * Gm[r][s] * J[s][m] * f->Sc[3 * m + k];
+  const float iz2 = 1.f / (zc * zc), iz3 = iz2 / zc;
+  gq[2] += -c->fx * iz2 * gJ[0][0] - c->fy * iz2 * gJ[1][1];
+  if (!f->clamp_x) {
+    gq[0] += -c->fx * iz2 * gJ[0][2];
+    gq[2] += 2.f * c->fx * f->qc[0] * iz3 * gJ[0][2];
+  } else {
+    gq[2] += c->fx * f->tx * iz3 * gJ[0][2];
+  }
+  if (!f->clamp_y) {
+    gq[1] += -c->fy * iz2 * gJ[1][2];
+    gq[2] += 2.f * c->fy * f->qc[1] * iz3 * gJ[1][2];
+  } else {
+    gq[2] += c->fy * f->ty * iz3 * gJ[1][2];
+  }
+  const float* W = c->rot_cw;
+  for (int k = 0; k < 3; ++k) g[k] += gp[k] + W[k] * gq[0] + W[3 + k] * gq[1] + W[6 + k] * gq[2];
+  /* Sc = W Sg W^T */
+  float gSg[9] = {0};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      for (int r = 0; r < 3; ++r)
+        for (int s = 0; s < 3; ++s) gSg[3 * i + j] += W[3 * r + i] * gSc[3 * r + s] * W[3 * s + j];
+  /* Sg = M M^T, M = R diag(s) */
+  float M[9], gM[9] = {0};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) M[3 * i + j] = f->Rq[3 * i + j] * f->s[j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      for (int k = 0; k < 3; ++k) gM[3 * i + j] += (gSg[3 * i + k] + gSg[3 * k + i]) * M[3 * k + j];
+  float G[9];
+  for (int j = 0; j < 3; ++j) {
+    float gs = 0.f;
+    for (int i = 0; i < 3; ++i) {
+      gs += f->Rq[3 * i + j] * gM[3 * i + j];
+      G[3 * i + j] = gM[3 * i + j] * f->s[j];
+    }
+    g[4 + j] += gs * f->s[j];
+  }
+  const float w = f->qn[0], qx = f->qn[1], qy = f->qn[2], qz = f->qn[3];
+  float gqn[4];
+  gqn[0] = 2.f * (-qz * G[1] + qy * G[2] + qz * G[3] - qx * G[5] - qy * G[6] + qx * G[7]);
+  gqn[1] = 2.f * (qy * G[1] + qz * G[2] + qy * G[3] - 2.f * qx * G[4] - w * G[5] + qz * G[6] + w * G[7] - 2.f * qx * G[8]);
+  gqn[2] = 2.f * (-2.f * qy * G[0] + qx * G[1] + w * G[2] + qx * G[3] + qz * G[5] - w * G[6] + qz * G[7] - 2.f * qy * G[8]);
+  gqn[3] = 2.f * (-2.f * qz * G[0] - w * G[1] + qx * G[2] + w * G[3] - 2.f * qz * G[4] + qy * G[5] + qx * G[6] + qy * G[7]);
+  const float dq = w * gqn[0] + qx * gqn[1] + qy * gqn[2] + qz * gqn[3];
+  for (int k = 0; k < 4; ++k) g[8 + k] += (gqn[k] - f->qn[k] * dq) / f->qnorm;
+}
+
+void or_project_bwd(const float* params, int64_t S, const int64_t* idx, int64_t m, const or_camera* c,
+                    int32_t sh_degree, const float* gsp, float* grad_params) {
+  const int n_sh = (sh_degree + 1) * (sh_degree + 1);
+  for (int64_t k = 0; k < m; ++k) {
+    opoint pt;
+    oproj f;
+    float g[60] = {0};
+    const int64_t i = idx[k];
+    load_opoint(params, S, i, &pt);
+    proj_fwd(&pt, c, n_sh, &f);
+    proj_bwd(&pt, c, n_sh, &f, gsp + k * GSPF, g);
+    for (int p = 0; p < 15; ++p)
+      for (int l = 0; l < 4; ++l) grad_params[4 * (p * S + i) + l] += g[4 * p + l];
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* binning + rasterisation                                                   */
+
+typedef struct {
+  uint32_t tile, depth_bits, row;
+} oinst;
+
+static int inst_cmp(const void* pa, const void* pb) {
+  const oinst* a = (const oinst*)pa;
+  const oinst* b = (const oinst*)pb;
+  if (a->tile != b->tile) return a->tile < b->tile ? -1 : 1;
+  if (a->depth_bits != b->depth_bits) return a->depth_bits < b->depth_bits ? -1 : 1;
+  return a->row < b->row ? -1 : (a->row > b->row);
+}
+
+/* tiles whose span meets [u - r, u + r] (same f32 ops as csrc/bin.cu) */
+static int tile_rect(const float* row, int W, int H, int* x0, int* x1, int* y0, int* y1) {
+  const float u = row[0], v = row[1], r = row[10];
+  if (!(r > 0.f)) return 0;
+  const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
+  *x0 = (int)fminf(fmaxf(floorf((u - r) * 0.0625f), 0.f), (float)tx);
+  *x1 = (int)fminf(fmaxf(floorf((u + r) * 0.0625f) + 1.f, 0.f), (float)tx);
+  *y0 = (int)fminf(fmaxf(floorf((v - r) * 0.0625f), 0.f), (float)ty);
+  *y1 = (int)fminf(fmaxf(floorf((v + r) * 0.0625f) + 1.f, 0.f), (float)ty);
+  if (*x1 <= *x0 || *y1 <= *y0) return 0;
+  return (*x1 - *x0) * (*y1 - *y0);
+}
+
+static oinst* bin_view(const float* sp, int64_t m, int W, int H, int64_t* n_out, int32_t* ranges) {
+  const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
+  int64_t total = 0;
+  int x0, x1, y0, y1;
+  for (int64_t k = 0; k < m; ++k) total += tile_rect(sp + k * SPF, W, H, &x0, &x1, &y0, &y1);
+  oinst* inst = (oinst*)malloc(sizeof(oinst) * (size_t)(total > 0 ? total : 1));
+  int64_t o = 0;
+  for (int64_t k = 0; k < m; ++k) {
+    const float* r = sp + k * SPF;
+    if (!tile_rect(r, W, H, &x0, &x1, &y0, &y1)) continue;
+    fbits db;
+    db.f = r[9];
+    for (int y = y0; y < y1; ++y)
+      for (int x = x0; x < x1; ++x) {
+        inst[o].tile = (uint32_t)(y * tx + x);
+        inst[o].depth_bits = db.u;
+        inst[o].row = (uint32_t)k;
+        ++o;
+      }
+  }
+  qsort(inst, (size_t)total, sizeof(oinst), inst_cmp);
+  for (int t = 0; t < tx * ty; ++t) ranges[2 * t] = ranges[2 * t + 1] = 0;
+  for (int64_t i = 0; i < total; ++i) {
+    const uint32_t t = inst[i].tile;
+    if (i == 0 || inst[i - 1].tile != t) ranges[2 * t] = (int32_t)i;
+    if (i == total - 1 || inst[i + 1].tile != t) ranges[2 * t + 1] = (int32_t)(i + 1);
+  }
+  *n_out = total;
+  return inst;
+}
+
+static float splat_power(const float* r, float px, float py, float* dx, float* dy) {
+  *dx = r[0] - px;
+  *dy = r[1] - py;
+  const float q = fmaf(r[3], (*dx) * (*dx), r[5] * ((*dy) * (*dy)));
+  return fmaf(-0.5f, q, -(r[4] * ((*dx) * (*dy))));
+}
+
+int32_t or_render(const float* sp, int64_t m, int32_t W, int32_t H, const float* bg, float* image, float* final_T,
+                  int32_t* n_contrib, uint32_t* tile_lists, int64_t* n_inst, int32_t* tile_ranges) {
+  const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
+  int32_t* ranges = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)tx * ty);
+  int64_t total = 0;
+  oinst* inst = bin_view(sp, m, W, H, &total, ranges);
+  if (tile_lists) {
+    if (*n_inst < total) {
+      *n_inst = total;
+      free(inst);
+      free(ranges);
+      return 1;
+    }
+    for (int64_t i = 0; i < total; ++i) tile_lists[i] = inst[i].row;
+    memcpy(tile_ranges, ranges, sizeof(int32_t) * 2 * (size_t)tx * ty);
+  }
+  if (n_inst) *n_inst = total;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int t = 0; t < tx * ty; ++t) {
+    const int bx = t % tx, by = t / tx;
+    for (int ly = 0; ly < TILE; ++ly)
+      for (int lx = 0; lx < TILE; ++lx) {
+        const int px = bx * TILE + lx, py = by * TILE + ly;
+        if (px >= W || py >= H) continue;
+        const float pxf = (float)px + 0.5f, pyf = (float)py + 0.5f;
+        float T = 1.f, C[3] = {0, 0, 0};
+        int contrib = 0;
+        for (int i = ranges[2 * t]; i < ranges[2 * t + 1]; ++i) {
+          const float* r = sp + (int64_t)inst[i].row * SPF;
+          float dx, dy;
+          const float power = splat_power(r, pxf, pyf, &dx, &dy);
+          if (power > 0.f) continue;
+          const float alpha = fminf(0.99f, r[2] * expf(power));
+          if (alpha < 1.f / 255.f) continue;
+          const float nT = T * (1.f - alpha);
+          if (nT < 1e-4f) break;
+          const float w = alpha * T;
+          for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(r[6 + ch], w, C[ch]);
+          T = nT;
+          contrib = i + 1 - ranges[2 * t];
+        }
+        const int64_t pix = (int64_t)py * W + px;
+        for (int ch = 0; ch < 3; ++ch) image[3 * pix + ch] = C[ch] + T * bg[ch];
+        final_T[pix] = T;
+        n_contrib[pix] = contrib;
+      }
+  }
+  free(inst);
+  free(ranges);
+  return 0;
+}
+
+int32_t or_render_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const float* bg, const float* final_T,
+                      const int32_t* n_contrib, const float* grad_image, float* gsp) {
+  const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
+  int32_t* ranges = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)tx * ty);
+  int64_t total = 0;
+  oinst* inst = bin_view(sp, m, W, H, &total, ranges);
+  memset(gsp, 0, sizeof(float) * GSPF * (size_t)m);
+  /* serial over tiles: gradient sums are order-sensitive only at fp32 level */
+  for (int t = 0; t < tx * ty; ++t) {
+    const int bx = t % tx, by = t / tx;
+    for (int ly = 0; ly < TILE; ++ly)
+      for (int lx = 0; lx < TILE; ++lx) {
+        const int px = bx * TILE + lx, py = by * TILE + ly;
+        if (px >= W || py >= H) continue;
+        const int64_t pix = (int64_t)py * W + px;
+        const float pxf = (float)px + 0.5f, pyf = (float)py + 0.5f;
+        const float* dC = grad_image + 3 * pix;
+        const float T_final = final_T[pix];
+        const float bgdot = bg[0] * dC[0] + bg[1] * dC[1] + bg[2] * dC[2];
+        float T = T_final, acc[3] = {0, 0, 0}, last_alpha = 0.f, lc[3] = {0, 0, 0};
+        const int r0 = ranges[2 * t];
+        for (int i = r0 + n_contrib[pix] - 1; i >= r0; --i) {
+          const int64_t row = inst[i].row;
+          const float* r = sp + row * SPF;
+          float dx, dy;
+          const float power = splat_power(r, pxf, pyf, &dx, &dy);
+          if (power > 0.f) continue;
+          const float ex = expf(power);
+          const float raw = r[2] * ex;
+          const float alpha = fminf(0.99f, raw);
+          if (alpha < 1.f / 255.f) continue;
+          const float ra = 1.f / (1.f - alpha);
+          T = T * ra;
+          float* g = gsp + row * GSPF;
+          const float fac = alpha * T;
+          for (int ch = 0; ch < 3; ++ch) g[6 + ch] += fac * dC[ch];
+          for (int ch = 0; ch < 3; ++ch) acc[ch] = last_alpha * lc[ch] + (1.f - last_alpha) * acc[ch];
+          last_alpha = alpha;
+          for (int ch = 0; ch < 3; ++ch) lc[ch] = r[6 + ch];
+          float dL_da = 0.f;
+          for (int ch = 0; ch < 3; ++ch) dL_da += (r[6 + ch] - acc[ch]) * dC[ch];
+          dL_da = T * dL_da - T_final * ra * bgdot;
+          if (raw > 0.99f) continue; /* clamped alpha: no gradient to opacity/geometry */
+          const float dpow = dL_da * alpha;
+          g[2] += dL_da * ex;
+          g[3] += -0.5f * dx * dx * dpow;
+          g[4] += -dx * dy * dpow;
+          g[5] += -0.5f * dy * dy * dpow;
+          g[0] += -(r[3] * dx + r[4] * dy) * dpow;
+          g[1] += -(r[4] * dx + r[5] * dy) * dpow;
+        }
+      }
+  }
+  free(inst);
+  free(ranges);
+  return 0;
+}
+
+double or_l1_loss(const float* image, const uint8_t* gt, int64_t n, float* grad) {
+  double s = 0.0;
+  const float inv = (float)(1.0 / (double)n);
+  for (int64_t i = 0; i < n; ++i) {
+    const float d = image[i] - gt[i] * (1.f / 255.f);
+    s += fabsf(d);
+    if (grad) grad[i] = (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) * inv;
+  }
+  return s / (double)n;
+}
+
+/* torch.optim.Adam single-tensor arithmetic */
+void or_adam(float* p, const float* g, float* m, float* v, int64_t n, const float* lr60, int64_t S, float beta1,
+             float beta2, float eps, int32_t step) {
+  const double bc1 = 1.0 - pow((double)beta1, (double)step);
+  const double bc2 = 1.0 - pow((double)beta2, (double)step);
+  const float scale = (float)(1.0 / bc1), bc2s = (float)sqrt(bc2);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t plane = (t / 4) / S;
+    const int lane = (int)(t % 4);
+    m[t] = m[t] + (1.f - beta1) * (g[t] - m[t]);
+    v[t] = beta2 * v[t] + (1.f - beta2) * g[t] * g[t];
+    const float denom = sqrtf(v[t]) / bc2s + eps;
+    p[t] = p[t] - (lr60[4 * plane + lane] * scale) * m[t] / denom;
+  }
+}
+
+double or_train_step(float* params, float* exp_avg, float* exp_avg_sq, int64_t S, const double* planes,
+                     const or_camera* cams, int32_t B, const uint8_t* gt, int32_t sh_degree, const float* lr60,
+                     float beta1, float beta2, float eps, int32_t step, int32_t n_threads) {
+  (void)n_threads;
+  const int64_t NP = 60 * S;
+  float* grads = (float*)calloc((size_t)NP, sizeof(float));
+  float* pos = (float*)malloc(sizeof(float) * 3 * (size_t)S);
+  for (int64_t i = 0; i < S; ++i)
+    for (int k = 0; k < 3; ++k) pos[3 * i + k] = params[4 * i + k];
+  double loss = 0.0;
+  for (int v = 0; v < B; ++v) {
+    const or_camera* c = cams + v;
+    const double* vp = planes + (size_t)v * 24;
+    int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)(S > 0 ? S : 1));
+    int64_t m = 0;
+    for (int64_t i = 0; i < S; ++i)
+      if (in_patch(vp, 1, 0, 0, pos[3 * i], pos[3 * i + 1], pos[3 * i + 2])) idx[m++] = i;
+    float* sp = (float*)malloc(sizeof(float) * SPF * (size_t)(m > 0 ? m : 1));
+    or_project(params, S, idx, m, c, sh_degree, sp);
+    const int W = c->width, H = c->height;
+    const int64_t npx = (int64_t)W * H;
+    float* img = (float*)malloc(sizeof(float) * 3 * (size_t)npx);
+    float* fT = (float*)malloc(sizeof(float) * (size_t)npx);
+    int32_t* nc = (int32_t*)malloc(sizeof(int32_t) * (size_t)npx);
+    float* gimg = (float*)malloc(sizeof(float) * 3 * (size_t)npx);
+    const float bg[3] = {0, 0, 0};
+    or_render(sp, m, W, H, bg, img, fT, nc, NULL, NULL, NULL);
+    loss += or_l1_loss(img, gt + (size_t)v * 3 * npx, 3 * npx, gimg);
+    float* gsp = (float*)malloc(sizeof(float) * GSPF * (size_t)(m > 0 ? m : 1));
+    or_render_bwd(sp, m, W, H, bg, fT, nc, gimg, gsp);
+    or_project_bwd(params, S, idx, m, c, sh_degree, gsp, grads);
+    free(idx);
+    free(sp);
+    free(img);
+    free(fT);
+    free(nc);
+    free(gimg);
+    free(gsp);
+  }
+  or_adam(params, grads, exp_avg, exp_avg_sq, NP, lr60, S, beta1, beta2, eps, step);
+  free(grads);
+  free(pos);
+  return loss;
+}

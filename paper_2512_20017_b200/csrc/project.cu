@@ -1,0 +1,404 @@
+// K1 projection (pts_splatting), K1b projection backward, K5 Adam, and the
+// fused K1b+K5 per-point kernel (Alg. 1 lines 23-27).
+//
+// Row layout: the splat state of view v is a contiguous run of rows in the
+// order of ascending local point index; runs are concatenated in the
+// caller's view order (destination order for the all-to-all).
+// The row of (point i in group g, view v) is
+//     view_row0[v] + base[g][v] + #{visible points of v in g before i}
+// recomputed identically by every per-point kernel with warp ballots, so no
+// per-(view, point) index table is ever materialised.
+#include "splat_math.cuh"
+
+namespace bs {
+namespace {
+
+constexpr int kProjThreads = 256;
+constexpr int kProjWarps = kProjThreads / 32;
+constexpr int kMaxViews = 32;
+
+// Per-round in-group ranks of the set view bits of every thread.
+struct RowRanker {
+  uint32_t* s_bal;  // [kProjWarps][kMaxViews]
+  int* s_run;       // [kMaxViews]
+
+  // Call with all threads of the CTA.  Returns nothing; rows are obtained by
+  // row_of() for set bits until the next advance().
+  __device__ void round(uint32_t mask, int B) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int v = 0; v < B; ++v) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (mask >> v) & 1u);
+      if (lane == 0) s_bal[w * kMaxViews + v] = bal;
+    }
+    __syncthreads();
+  }
+  __device__ int row_offset(int v) const {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int pre = s_run[v];
+    for (int j = 0; j < w; ++j) pre += __popc(s_bal[j * kMaxViews + v]);
+    return pre + __popc(s_bal[w * kMaxViews + v] & ((1u << lane) - 1u));
+  }
+  __device__ void advance(int B) {
+    __syncthreads();
+    if (threadIdx.x < B) {
+      int add = 0;
+      for (int j = 0; j < kProjWarps; ++j) add += __popc(s_bal[j * kMaxViews + threadIdx.x]);
+      s_run[threadIdx.x] += add;
+    }
+    __syncthreads();
+  }
+};
+
+struct ProjArgs {
+  int B, n_sh;
+  const float4* params;
+  int64_t S;
+  const uint32_t* mask;
+  const int32_t* group_begin;
+  const int32_t* base;  // [ng][B]
+  const int64_t* view_row0;
+  const bs_camera* cams;
+};
+
+__global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, float* __restrict__ sp) {
+  __shared__ uint32_t s_bal[kProjWarps * kMaxViews];
+  __shared__ int s_run[kMaxViews];
+  __shared__ bs_camera s_cam[kMaxViews];
+  __shared__ int64_t s_row0[kMaxViews];
+  const int g = blockIdx.x, B = a.B;
+  if (threadIdx.x < B) {
+    s_run[threadIdx.x] = 0;
+    s_cam[threadIdx.x] = a.cams[threadIdx.x];
+    s_row0[threadIdx.x] = a.view_row0[threadIdx.x] + a.base[(size_t)g * B + threadIdx.x];
+  }
+  __syncthreads();
+  RowRanker rk{s_bal, s_run};
+  const int begin = a.group_begin[g], end = a.group_begin[g + 1];
+  for (int b0 = begin; b0 < end; b0 += kProjThreads) {
+    const int i = b0 + threadIdx.x;
+    const uint32_t mask = i < end ? a.mask[i] : 0u;
+    rk.round(mask, B);
+    if (mask) {
+      PointIn pt;
+      load_point(a.params, a.S, i, a.n_sh, pt);
+      uint32_t m = mask;
+      while (m) {
+        const int v = __ffs(m) - 1;
+        m &= m - 1;
+        ProjFwd f;
+        project_forward(pt, s_cam[v], a.n_sh, f);
+        const int64_t row = s_row0[v] + rk.row_offset(v);
+        write_sp_row(sp + row * BS_SP_FLOATS, f);
+      }
+    }
+    rk.advance(B);
+  }
+}
+
+// Accumulate the parameter gradient of one point over all its views.
+__device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camera* s_cam, const int64_t* s_row0,
+                                               const RowRanker& rk, uint32_t mask, const PointIn& pt,
+                                               const float* __restrict__ gsp, PointGrad& gr) {
+  uint32_t m = mask;
+  while (m) {
+    const int v = __ffs(m) - 1;
+    m &= m - 1;
+    const int64_t row = s_row0[v] + rk.row_offset(v);
+    float gs[9];
+    const float* src = gsp + row * BS_GSP_FLOATS;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) gs[k] = src[k];
+    ProjFwd f;
+    project_forward(pt, s_cam[v], a.n_sh, f);
+    project_backward(pt, s_cam[v], a.n_sh, f, gs, gr);
+  }
+}
+
+__global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, const float* __restrict__ gsp,
+                                                                   float4* __restrict__ gparams) {
+  __shared__ uint32_t s_bal[kProjWarps * kMaxViews];
+  __shared__ int s_run[kMaxViews];
+  __shared__ bs_camera s_cam[kMaxViews];
+  __shared__ int64_t s_row0[kMaxViews];
+  const int g = blockIdx.x, B = a.B;
+  if (threadIdx.x < B) {
+    s_run[threadIdx.x] = 0;
+    s_cam[threadIdx.x] = a.cams[threadIdx.x];
+    s_row0[threadIdx.x] = a.view_row0[threadIdx.x] + a.base[(size_t)g * B + threadIdx.x];
+  }
+  __syncthreads();
+  RowRanker rk{s_bal, s_run};
+  const int begin = a.group_begin[g], end = a.group_begin[g + 1];
+  for (int b0 = begin; b0 < end; b0 += kProjThreads) {
+    const int i = b0 + threadIdx.x;
+    const uint32_t mask = i < end ? a.mask[i] : 0u;
+    rk.round(mask, B);
+    if (mask) {
+      PointIn pt;
+      load_point(a.params, a.S, i, a.n_sh, pt);
+      PointGrad gr;
+#pragma unroll
+      for (int k = 0; k < 60; ++k) gr.g[k] = 0.f;
+      point_backward(a, s_cam, s_row0, rk, mask, pt, gsp, gr);
+#pragma unroll
+      for (int p = 0; p < BS_PARAM_PLANES; ++p) {
+        float4 acc = gparams[p * a.S + i];
+        acc.x += gr.g[4 * p];
+        acc.y += gr.g[4 * p + 1];
+        acc.z += gr.g[4 * p + 2];
+        acc.w += gr.g[4 * p + 3];
+        gparams[p * a.S + i] = acc;
+      }
+    }
+    rk.advance(B);
+  }
+}
+
+struct AdamConsts {
+  float lr[BS_PARAM_FLOATS];
+  float beta1, beta2, eps, step_size_scale, bc2_sqrt;
+  int selective;
+};
+
+// torch.optim.Adam (foreach=False) arithmetic on one float4 of a plane.
+__device__ __forceinline__ void adam4(float4& p, float4 g, float4& m, float4& v, const AdamConsts& c, int plane) {
+  float* pp = &p.x;
+  float* gg = &g.x;
+  float* mm = &m.x;
+  float* vv = &v.x;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    mm[k] = mm[k] + (1.f - c.beta1) * (gg[k] - mm[k]);
+    vv[k] = c.beta2 * vv[k] + (1.f - c.beta2) * gg[k] * gg[k];
+    const float denom = sqrtf(vv[k]) / c.bc2_sqrt + c.eps;
+    const float step = c.lr[4 * plane + k] * c.step_size_scale;
+    pp[k] = pp[k] - step * mm[k] / denom;
+  }
+}
+
+__global__ void __launch_bounds__(256) adam_kernel(AdamConsts c, float4* __restrict__ params,
+                                                   const float4* __restrict__ grads, float4* __restrict__ m,
+                                                   float4* __restrict__ v, int64_t S,
+                                                   const uint32_t* __restrict__ mask) {
+  const int64_t total = S * BS_PARAM_PLANES;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int plane = (int)(t / S);
+    const int64_t i = t - plane * S;
+    if (c.selective && mask && mask[i] == 0u) continue;
+    float4 p = params[t], mm = m[t], vv = v[t];
+    adam4(p, grads[t], mm, vv, c, plane);
+    params[t] = p;
+    m[t] = mm;
+    v[t] = vv;
+  }
+}
+
+__global__ void __launch_bounds__(kProjThreads) project_bwd_adam_kernel(ProjArgs a, AdamConsts c,
+                                                                        const float* __restrict__ gsp,
+                                                                        float4* params,
+                                                                        float4* __restrict__ m,
+                                                                        float4* __restrict__ v) {
+  __shared__ uint32_t s_bal[kProjWarps * kMaxViews];
+  __shared__ int s_run[kMaxViews];
+  __shared__ bs_camera s_cam[kMaxViews];
+  __shared__ int64_t s_row0[kMaxViews];
+  const int g = blockIdx.x, B = a.B;
+  if (threadIdx.x < B) {
+    s_run[threadIdx.x] = 0;
+    s_cam[threadIdx.x] = a.cams[threadIdx.x];
+    s_row0[threadIdx.x] = a.view_row0[threadIdx.x] + a.base[(size_t)g * B + threadIdx.x];
+  }
+  __syncthreads();
+  RowRanker rk{s_bal, s_run};
+  const int begin = a.group_begin[g], end = a.group_begin[g + 1];
+  for (int b0 = begin; b0 < end; b0 += kProjThreads) {
+    const int i = b0 + threadIdx.x;
+    const bool ok = i < end;
+    const uint32_t mask = ok ? a.mask[i] : 0u;
+    rk.round(mask, B);
+    if (ok && !(c.selective && mask == 0u)) {
+      PointGrad gr;
+#pragma unroll
+      for (int k = 0; k < 60; ++k) gr.g[k] = 0.f;
+      if (mask) {
+        PointIn pt;
+        load_point(a.params, a.S, i, a.n_sh, pt);
+        point_backward(a, s_cam, s_row0, rk, mask, pt, gsp, gr);
+      }
+#pragma unroll
+      for (int p = 0; p < BS_PARAM_PLANES; ++p) {
+        const int64_t t = p * a.S + i;
+        float4 pp = params[t], mm = m[t], vv = v[t];
+        adam4(pp, make_float4(gr.g[4 * p], gr.g[4 * p + 1], gr.g[4 * p + 2], gr.g[4 * p + 3]), mm, vv, c, p);
+        params[t] = pp;
+        m[t] = mm;
+        v[t] = vv;
+      }
+    }
+    rk.advance(B);
+  }
+}
+
+// ---- row layout ------------------------------------------------------------
+
+__global__ void __launch_bounds__(1024) scan_counts_kernel(const int32_t* __restrict__ counts, int ng, int B,
+                                                           int32_t* __restrict__ base, int64_t* __restrict__ rows) {
+  __shared__ int s_w[32];
+  const int v = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  int carry = 0;
+  for (int b0 = 0; b0 < ng; b0 += 1024) {
+    const int gi = b0 + tid;
+    const int x0 = gi < ng ? counts[(size_t)gi * B + v] : 0;
+    int x = x0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int t = s_w[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      s_w[lane] = t;
+    }
+    __syncthreads();
+    if (gi < ng) base[(size_t)gi * B + v] = carry + (w ? s_w[w - 1] : 0) + x - x0;
+    const int tot = s_w[31];
+    __syncthreads();
+    carry += tot;
+  }
+  if (tid == 0) rows[v] = carry;
+}
+
+struct ViewOrder {
+  int order[kMaxViews];
+};
+
+__global__ void view_row0_kernel(const int64_t* __restrict__ rows, ViewOrder o, int B, int64_t* __restrict__ row0) {
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int k = 0; k < B; ++k) {
+      row0[o.order[k]] = acc;
+      acc += rows[o.order[k]];
+    }
+  }
+}
+
+int32_t check_proj(const bs_proj_desc* d) {
+  BS_REQUIRE(d != nullptr, BS_ERR_PARAMETER, "null projection descriptor");
+  BS_REQUIRE(d->n_views >= 1 && d->n_views <= kMaxViews, BS_ERR_PARAMETER, "projection supports 1..32 views");
+  BS_REQUIRE(d->sh_degree >= 0 && d->sh_degree <= 3, BS_ERR_PARAMETER, "sh_degree must be in [0, 3]");
+  return BS_OK;
+}
+
+AdamConsts make_adam(const bs_adam_desc* d) {
+  AdamConsts c;
+  for (int k = 0; k < BS_PARAM_FLOATS; ++k) c.lr[k] = d->lr[k];
+  c.beta1 = d->beta1;
+  c.beta2 = d->beta2;
+  c.eps = d->eps;
+  const double bc1 = 1.0 - pow((double)d->beta1, (double)d->step);
+  const double bc2 = 1.0 - pow((double)d->beta2, (double)d->step);
+  c.step_size_scale = (float)(1.0 / bc1);
+  c.bc2_sqrt = (float)sqrt(bc2);
+  c.selective = d->selective;
+  return c;
+}
+
+}  // namespace
+}  // namespace bs
+
+using namespace bs;
+
+extern "C" int32_t bs_scan_counts(const int32_t* counts, int32_t n_groups, int32_t n_views,
+                                  const int32_t* view_order_host, int32_t* base, int64_t* view_rows,
+                                  int64_t* view_row0, void* stream) {
+  BS_REQUIRE(n_views >= 1 && n_views <= kMaxViews, BS_ERR_PARAMETER, "scan_counts supports 1..32 views");
+  ViewOrder o;
+  bool seen[kMaxViews] = {false};
+  for (int k = 0; k < n_views; ++k) {
+    const int v = view_order_host ? view_order_host[k] : k;
+    BS_REQUIRE(v >= 0 && v < n_views && !seen[v], BS_ERR_PARAMETER, "view_order must be a permutation");
+    seen[v] = true;
+    o.order[k] = v;
+  }
+  cudaStream_t s = as_stream(stream);
+  if (n_groups > 0) {
+    scan_counts_kernel<<<n_views, 1024, 0, s>>>(counts, n_groups, n_views, base, view_rows);
+    BS_LAUNCH_CHECK("scan_counts_kernel");
+  } else {
+    cudaMemsetAsync(view_rows, 0, sizeof(int64_t) * n_views, s);
+  }
+  view_row0_kernel<<<1, 32, 0, s>>>(view_rows, o, n_views, view_row0);
+  BS_LAUNCH_CHECK("view_row0_kernel");
+  return BS_OK;
+}
+
+extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, int64_t n_points,
+                                  const uint32_t* vis_mask, const int32_t* group_begin, int32_t n_groups,
+                                  const int32_t* base, const int64_t* view_row0, const bs_camera* cams,
+                                  float* sp_rows, void* stream) {
+  int32_t st = check_proj(d);
+  if (st) return st;
+  if (n_groups == 0) return BS_OK;
+  const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
+  ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
+             view_row0, cams};
+  project_fwd_kernel<<<n_groups, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
+  BS_LAUNCH_CHECK("project_fwd_kernel");
+  return BS_OK;
+}
+
+extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, int64_t n_points,
+                                  const uint32_t* vis_mask, const int32_t* group_begin, int32_t n_groups,
+                                  const int32_t* base, const int64_t* view_row0, const bs_camera* cams,
+                                  const float* g_sp, float* grad_params, void* stream) {
+  int32_t st = check_proj(d);
+  if (st) return st;
+  if (n_groups == 0) return BS_OK;
+  const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
+  ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
+             view_row0, cams};
+  project_bwd_kernel<<<n_groups, kProjThreads, 0, as_stream(stream)>>>(a, g_sp,
+                                                                       reinterpret_cast<float4*>(grad_params));
+  BS_LAUNCH_CHECK("project_bwd_kernel");
+  return BS_OK;
+}
+
+extern "C" int32_t bs_adam_step(const bs_adam_desc* d, float* params, const float* grads, float* exp_avg,
+                                float* exp_avg_sq, int64_t n_points, const uint32_t* vis_mask, void* stream) {
+  BS_REQUIRE(d != nullptr && d->step >= 1, BS_ERR_PARAMETER, "adam: step must be >= 1");
+  BS_REQUIRE(!d->selective || vis_mask, BS_ERR_PARAMETER, "selective adam needs the visibility mask");
+  if (n_points == 0) return BS_OK;
+  AdamConsts c = make_adam(d);
+  adam_kernel<<<grid_for(n_points * BS_PARAM_PLANES, 256), 256, 0, as_stream(stream)>>>(
+      c, reinterpret_cast<float4*>(params), reinterpret_cast<const float4*>(grads),
+      reinterpret_cast<float4*>(exp_avg), reinterpret_cast<float4*>(exp_avg_sq), n_points, vis_mask);
+  BS_LAUNCH_CHECK("adam_kernel");
+  return BS_OK;
+}
+
+extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_desc* ad, float* params,
+                                       float* exp_avg, float* exp_avg_sq, int64_t n_points,
+                                       const uint32_t* vis_mask, const int32_t* group_begin, int32_t n_groups,
+                                       const int32_t* base, const int64_t* view_row0, const bs_camera* cams,
+                                       const float* g_sp, void* stream) {
+  int32_t st = check_proj(pd);
+  if (st) return st;
+  BS_REQUIRE(ad != nullptr && ad->step >= 1, BS_ERR_PARAMETER, "adam: step must be >= 1");
+  if (n_groups == 0) return BS_OK;
+  const int n_sh = (pd->sh_degree + 1) * (pd->sh_degree + 1);
+  ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
+             view_row0, cams};
+  AdamConsts c = make_adam(ad);
+  project_bwd_adam_kernel<<<n_groups, kProjThreads, 0, as_stream(stream)>>>(
+      a, c, g_sp, reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(exp_avg),
+      reinterpret_cast<float4*>(exp_avg_sq));
+  BS_LAUNCH_CHECK("project_bwd_adam_kernel");
+  return BS_OK;
+}

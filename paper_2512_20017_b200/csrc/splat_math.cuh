@@ -1,0 +1,421 @@
+// 3DGS projection math (pts_splatting) and its
+// analytic backward (pts_splatting.backward).
+//
+// Forward: every arithmetic op is an explicit round-to-nearest intrinsic
+// (bs::fmul/fadd/...), so the splat state is bit-identical to the CPU
+// oracle (oracle/splat_oracle.c, same op sequence, -ffp-contract=off).
+// Backward: ordinary float arithmetic (contraction allowed); compared to the
+// oracle within the fp32 tolerance stated in tests/test_gpu_parity.py.
+//
+// Conventions (builder-chosen standard 3DGS, frozen here):
+//   EWA dilation 0.3 px^2, Jacobian clamp |x/z| <= 1.3 tan(fov/2),
+//   radius = ceil(3 sqrt(lambda_max)), SH degree <= 3 with colour
+//   max(sum + 0.5, 0), opacity = sigmoid(logit), scale = exp(log_scale).
+#pragma once
+#include "common.cuh"
+
+namespace bs {
+
+constexpr float kSH_C0 = 0.28209479177387814f;
+constexpr float kSH_C1 = 0.4886025119029199f;
+constexpr float kSH_C2_0 = 1.0925484305920792f;
+constexpr float kSH_C2_1 = -1.0925484305920792f;
+constexpr float kSH_C2_2 = 0.31539156525252005f;
+constexpr float kSH_C2_3 = -1.0925484305920792f;
+constexpr float kSH_C2_4 = 0.5462742152960396f;
+constexpr float kSH_C3_0 = -0.5900435899266435f;
+constexpr float kSH_C3_1 = 2.890611442640554f;
+constexpr float kSH_C3_2 = -0.4570457994644658f;
+constexpr float kSH_C3_3 = 0.3731763325901154f;
+constexpr float kSH_C3_4 = -0.4570457994644658f;
+constexpr float kSH_C3_5 = 1.445305721320277f;
+constexpr float kSH_C3_6 = -0.5900435899266435f;
+constexpr float kDilation = 0.3f;
+
+struct PointIn {
+  float p[3];
+  float op_logit;
+  float ls[3];
+  float q[4];
+  float sh[48];
+};
+
+struct ProjFwd {
+  float d[3];      // p - campos
+  float qc[3];     // camera-frame position
+  float s[3];      // scales
+  float qn[4];     // normalised quaternion
+  float qnorm;
+  float Rq[9];     // rotation of the quaternion
+  float Sc[6];     // camera-frame covariance (00 01 02 11 12 22)
+  float J00, J02, J11, J12;
+  bool clamp_x, clamp_y;
+  float tx, ty;
+  float a, b, c, det;  // dilated 2D covariance
+  float conic[3];
+  float radius;
+  float u, v, depth;
+  float len, dir[3];
+  float Y[16];
+  float col_raw[3], col[3];
+  float opac;
+  bool valid;
+};
+
+__device__ __forceinline__ void load_point(const float4* __restrict__ params, int64_t S, int64_t i,
+                                           int n_sh, PointIn& pt) {
+  const float4 a = params[i];
+  const float4 b = params[S + i];
+  const float4 q = params[2 * S + i];
+  pt.p[0] = a.x; pt.p[1] = a.y; pt.p[2] = a.z; pt.op_logit = a.w;
+  pt.ls[0] = b.x; pt.ls[1] = b.y; pt.ls[2] = b.z;
+  pt.q[0] = q.x; pt.q[1] = q.y; pt.q[2] = q.z; pt.q[3] = q.w;
+  const int planes = (3 * n_sh + 3) / 4;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    if (k < planes) {
+      const float4 t = params[(3 + k) * S + i];
+      pt.sh[4 * k] = t.x; pt.sh[4 * k + 1] = t.y; pt.sh[4 * k + 2] = t.z; pt.sh[4 * k + 3] = t.w;
+    } else {
+      pt.sh[4 * k] = pt.sh[4 * k + 1] = pt.sh[4 * k + 2] = pt.sh[4 * k + 3] = 0.f;
+    }
+  }
+}
+
+__device__ __forceinline__ void sh_basis(const float dir[3], int n_sh, float Y[16]) {
+  const float x = dir[0], y = dir[1], z = dir[2];
+  Y[0] = kSH_C0;
+#pragma unroll
+  for (int k = 1; k < 16; ++k) Y[k] = 0.f;
+  if (n_sh > 1) {
+    Y[1] = fmul(-kSH_C1, y);
+    Y[2] = fmul(kSH_C1, z);
+    Y[3] = fmul(-kSH_C1, x);
+  }
+  if (n_sh > 4) {
+    const float xx = fmul(x, x), yy = fmul(y, y), zz = fmul(z, z);
+    const float xy = fmul(x, y), yz = fmul(y, z), xz = fmul(x, z);
+    Y[4] = fmul(kSH_C2_0, xy);
+    Y[5] = fmul(kSH_C2_1, yz);
+    Y[6] = fmul(kSH_C2_2, fsub(fsub(fmul(2.f, zz), xx), yy));
+    Y[7] = fmul(kSH_C2_3, xz);
+    Y[8] = fmul(kSH_C2_4, fsub(xx, yy));
+    if (n_sh > 9) {
+      Y[9] = fmul(fmul(kSH_C3_0, y), fsub(fmul(3.f, xx), yy));
+      Y[10] = fmul(fmul(kSH_C3_1, xy), z);
+      Y[11] = fmul(fmul(kSH_C3_2, y), fsub(fsub(fmul(4.f, zz), xx), yy));
+      Y[12] = fmul(fmul(kSH_C3_3, z), fsub(fsub(fmul(2.f, zz), fmul(3.f, xx)), fmul(3.f, yy)));
+      Y[13] = fmul(fmul(kSH_C3_4, x), fsub(fsub(fmul(4.f, zz), xx), yy));
+      Y[14] = fmul(fmul(kSH_C3_5, z), fsub(xx, yy));
+      Y[15] = fmul(fmul(kSH_C3_6, x), fsub(xx, fmul(3.f, yy)));
+    }
+  }
+}
+
+__device__ __forceinline__ void project_forward(const PointIn& pt, const bs_camera& c, int n_sh, ProjFwd& f) {
+  // camera frame: q = Rcw (p - pos)
+#pragma unroll
+  for (int k = 0; k < 3; ++k) f.d[k] = fsub(pt.p[k], c.pos[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    f.qc[k] = fadd(fadd(fmul(c.rot_cw[3 * k], f.d[0]), fmul(c.rot_cw[3 * k + 1], f.d[1])),
+                   fmul(c.rot_cw[3 * k + 2], f.d[2]));
+  const float z = f.qc[2];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) f.s[k] = det_expf(pt.ls[k]);
+  const float nn = fadd(fadd(fadd(fmul(pt.q[0], pt.q[0]), fmul(pt.q[1], pt.q[1])), fmul(pt.q[2], pt.q[2])),
+                        fmul(pt.q[3], pt.q[3]));
+  f.qnorm = fsqrt(nn);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) f.qn[k] = fdiv(pt.q[k], f.qnorm);
+  const float w = f.qn[0], x = f.qn[1], y = f.qn[2], zq = f.qn[3];
+  const float xx = fmul(x, x), yy = fmul(y, y), zz = fmul(zq, zq);
+  const float xy = fmul(x, y), xz = fmul(x, zq), yz = fmul(y, zq);
+  const float wx = fmul(w, x), wy = fmul(w, y), wz = fmul(w, zq);
+  f.Rq[0] = fsub(1.f, fmul(2.f, fadd(yy, zz)));
+  f.Rq[1] = fmul(2.f, fsub(xy, wz));
+  f.Rq[2] = fmul(2.f, fadd(xz, wy));
+  f.Rq[3] = fmul(2.f, fadd(xy, wz));
+  f.Rq[4] = fsub(1.f, fmul(2.f, fadd(xx, zz)));
+  f.Rq[5] = fmul(2.f, fsub(yz, wx));
+  f.Rq[6] = fmul(2.f, fsub(xz, wy));
+  f.Rq[7] = fmul(2.f, fadd(yz, wx));
+  f.Rq[8] = fsub(1.f, fmul(2.f, fadd(xx, yy)));
+  float M[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) M[3 * i + j] = fmul(f.Rq[3 * i + j], f.s[j]);
+  float Sg[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) {
+      const float v = fadd(fadd(fmul(M[3 * i], M[3 * j]), fmul(M[3 * i + 1], M[3 * j + 1])),
+                           fmul(M[3 * i + 2], M[3 * j + 2]));
+      Sg[3 * i + j] = v;
+      Sg[3 * j + i] = v;
+    }
+  // Sc = W Sg W^T
+  const float* W = c.rot_cw;
+  float T[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      T[3 * i + j] = fadd(fadd(fmul(W[3 * i], Sg[j]), fmul(W[3 * i + 1], Sg[3 + j])), fmul(W[3 * i + 2], Sg[6 + j]));
+  float Sc[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) {
+      const float v =
+          fadd(fadd(fmul(T[3 * i], W[3 * j]), fmul(T[3 * i + 1], W[3 * j + 1])), fmul(T[3 * i + 2], W[3 * j + 2]));
+      Sc[3 * i + j] = v;
+      Sc[3 * j + i] = v;
+    }
+  f.Sc[0] = Sc[0]; f.Sc[1] = Sc[1]; f.Sc[2] = Sc[2]; f.Sc[3] = Sc[4]; f.Sc[4] = Sc[5]; f.Sc[5] = Sc[8];
+  // EWA Jacobian with the usual clamp of x/z, y/z
+  const float xr = fdiv(f.qc[0], z), yr = fdiv(f.qc[1], z);
+  f.clamp_x = (xr < -c.lim_x) || (xr > c.lim_x);
+  f.clamp_y = (yr < -c.lim_y) || (yr > c.lim_y);
+  f.tx = fmul(fminf(c.lim_x, fmaxf(-c.lim_x, xr)), z);
+  f.ty = fmul(fminf(c.lim_y, fmaxf(-c.lim_y, yr)), z);
+  const float z2 = fmul(z, z);
+  f.J00 = fdiv(c.fx, z);
+  f.J11 = fdiv(c.fy, z);
+  f.J02 = -fdiv(fmul(c.fx, f.tx), z2);
+  f.J12 = -fdiv(fmul(c.fy, f.ty), z2);
+  float U0[3], U1[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    U0[j] = fadd(fmul(f.J00, Sc[j]), fmul(f.J02, Sc[6 + j]));
+    U1[j] = fadd(fmul(f.J11, Sc[3 + j]), fmul(f.J12, Sc[6 + j]));
+  }
+  f.a = fadd(fadd(fmul(U0[0], f.J00), fmul(U0[2], f.J02)), kDilation);
+  f.b = fadd(fmul(U0[1], f.J11), fmul(U0[2], f.J12));
+  f.c = fadd(fadd(fmul(U1[1], f.J11), fmul(U1[2], f.J12)), kDilation);
+  f.det = fsub(fmul(f.a, f.c), fmul(f.b, f.b));
+  f.valid = f.det > 0.f;
+  if (f.valid) {
+    f.conic[0] = fdiv(f.c, f.det);
+    f.conic[1] = fdiv(-f.b, f.det);
+    f.conic[2] = fdiv(f.a, f.det);
+    const float mid = fmul(0.5f, fadd(f.a, f.c));
+    const float disc = fmaxf(0.1f, fsub(fmul(mid, mid), f.det));
+    const float l1 = fadd(mid, fsqrt(disc));
+    f.radius = ceilf(fmul(3.f, fsqrt(l1)));
+  } else {
+    f.conic[0] = f.conic[1] = f.conic[2] = 0.f;
+    f.radius = 0.f;
+  }
+  f.u = fadd(fmul(c.fx, xr), c.cx);
+  f.v = fadd(fmul(c.fy, yr), c.cy);
+  f.depth = z;
+  // view-dependent colour
+  f.len = fsqrt(fadd(fadd(fmul(f.d[0], f.d[0]), fmul(f.d[1], f.d[1])), fmul(f.d[2], f.d[2])));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) f.dir[k] = fdiv(f.d[k], f.len);
+  sh_basis(f.dir, n_sh, f.Y);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float acc = fmul(f.Y[0], pt.sh[ch]);
+#pragma unroll
+    for (int k = 1; k < 16; ++k)
+      if (k < n_sh) acc = fadd(acc, fmul(f.Y[k], pt.sh[3 * k + ch]));
+    f.col_raw[ch] = fadd(acc, 0.5f);
+    f.col[ch] = fmaxf(f.col_raw[ch], 0.f);
+  }
+  f.opac = det_sigmoid(pt.op_logit);
+}
+
+__device__ __forceinline__ void write_sp_row(float* __restrict__ row, const ProjFwd& f) {
+  float4* r4 = reinterpret_cast<float4*>(row);
+  r4[0] = make_float4(f.u, f.v, f.opac, f.conic[0]);
+  r4[1] = make_float4(f.conic[1], f.conic[2], f.col[0], f.col[1]);
+  r4[2] = make_float4(f.col[2], f.depth, f.valid ? f.radius : 0.f, 0.f);
+}
+
+// Gradient of the 60-float parameter row of one point (plane layout order:
+// mean xyz, opacity logit, log scales xyz, pad, quat wxyz, sh[48]).
+struct PointGrad {
+  float g[60];
+};
+
+// dY_k/d(dir) accumulated against per-coefficient weights wk[k] = sum_ch dc*sh.
+__device__ __forceinline__ void sh_dir_grad(const float dir[3], int n_sh, const float* wk, float gd[3]) {
+  const float x = dir[0], y = dir[1], z = dir[2];
+  gd[0] = gd[1] = gd[2] = 0.f;
+  if (n_sh > 1) {
+    gd[1] += -kSH_C1 * wk[1];
+    gd[2] += kSH_C1 * wk[2];
+    gd[0] += -kSH_C1 * wk[3];
+  }
+  if (n_sh > 4) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    gd[0] += kSH_C2_0 * y * wk[4];
+    gd[1] += kSH_C2_0 * x * wk[4];
+    gd[1] += kSH_C2_1 * z * wk[5];
+    gd[2] += kSH_C2_1 * y * wk[5];
+    gd[0] += -2.f * kSH_C2_2 * x * wk[6];
+    gd[1] += -2.f * kSH_C2_2 * y * wk[6];
+    gd[2] += 4.f * kSH_C2_2 * z * wk[6];
+    gd[0] += kSH_C2_3 * z * wk[7];
+    gd[2] += kSH_C2_3 * x * wk[7];
+    gd[0] += 2.f * kSH_C2_4 * x * wk[8];
+    gd[1] += -2.f * kSH_C2_4 * y * wk[8];
+    if (n_sh > 9) {
+      gd[0] += kSH_C3_0 * 6.f * x * y * wk[9];
+      gd[1] += kSH_C3_0 * (3.f * xx - 3.f * yy) * wk[9];
+      gd[0] += kSH_C3_1 * y * z * wk[10];
+      gd[1] += kSH_C3_1 * x * z * wk[10];
+      gd[2] += kSH_C3_1 * x * y * wk[10];
+      gd[0] += kSH_C3_2 * (-2.f * x * y) * wk[11];
+      gd[1] += kSH_C3_2 * (4.f * zz - xx - 3.f * yy) * wk[11];
+      gd[2] += kSH_C3_2 * 8.f * y * z * wk[11];
+      gd[0] += kSH_C3_3 * (-6.f * x * z) * wk[12];
+      gd[1] += kSH_C3_3 * (-6.f * y * z) * wk[12];
+      gd[2] += kSH_C3_3 * (6.f * zz - 3.f * xx - 3.f * yy) * wk[12];
+      gd[0] += kSH_C3_4 * (4.f * zz - 3.f * xx - yy) * wk[13];
+      gd[1] += kSH_C3_4 * (-2.f * x * y) * wk[13];
+      gd[2] += kSH_C3_4 * 8.f * x * z * wk[13];
+      gd[0] += kSH_C3_5 * 2.f * x * z * wk[14];
+      gd[1] += kSH_C3_5 * (-2.f * y * z) * wk[14];
+      gd[2] += kSH_C3_5 * (xx - yy) * wk[14];
+      gd[0] += kSH_C3_6 * (3.f * xx - 3.f * yy) * wk[15];
+      gd[1] += kSH_C3_6 * (-6.f * x * y) * wk[15];
+    }
+  }
+}
+
+// Accumulate d L / d params of one (point, view) pair into gr.
+// gsp = (du, dv, dopac, dA, dB, dC, dr, dg, db).
+__device__ __forceinline__ void project_backward(const PointIn& pt, const bs_camera& c, int n_sh,
+                                                 const ProjFwd& f, const float gsp[9], PointGrad& gr) {
+  if (!f.valid) return;
+  // ---- colour -> sh, dir
+  float dc[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) dc[ch] = f.col_raw[ch] >= 0.f ? gsp[6 + ch] : 0.f;
+  float wk[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) wk[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (k >= n_sh) break;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      gr.g[12 + 3 * k + ch] += f.Y[k] * dc[ch];
+      wk[k] += dc[ch] * pt.sh[3 * k + ch];
+    }
+  }
+  float gdir[3];
+  sh_dir_grad(f.dir, n_sh, wk, gdir);
+  const float dd = f.dir[0] * gdir[0] + f.dir[1] * gdir[1] + f.dir[2] * gdir[2];
+  float gp[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) gp[k] = (gdir[k] - f.dir[k] * dd) / f.len;
+  // ---- opacity
+  gr.g[3] += gsp[2] * f.opac * (1.f - f.opac);
+  // ---- means2d -> camera point
+  const float z = f.qc[2], iz = 1.f / z, iz2 = iz * iz;
+  float gq[3];
+  gq[0] = gsp[0] * c.fx * iz;
+  gq[1] = gsp[1] * c.fy * iz;
+  gq[2] = -(gsp[0] * c.fx * f.qc[0] + gsp[1] * c.fy * f.qc[1]) * iz2;
+  // ---- conic -> dilated 2D covariance
+  const float A = gsp[3], Bg = gsp[4], Cg = gsp[5];
+  const float a = f.a, b = f.b, cc = f.c;
+  const float id2 = 1.f / (f.det * f.det);
+  const float ga = (-cc * cc * A + b * cc * Bg - b * b * Cg) * id2;
+  const float gb = (2.f * b * cc * A - (a * cc + b * b) * Bg + 2.f * a * b * Cg) * id2;
+  const float gc = (-b * b * A + a * b * Bg - a * a * Cg) * id2;
+  // ---- cov2d = J Sc J^T
+  const float J0[3] = {f.J00, 0.f, f.J02};
+  const float J1[3] = {0.f, f.J11, f.J12};
+  const float Sc[9] = {f.Sc[0], f.Sc[1], f.Sc[2], f.Sc[1], f.Sc[3], f.Sc[4], f.Sc[2], f.Sc[4], f.Sc[5]};
+  float gSc[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      gSc[3 * i + j] = ga * J0[i] * J0[j] + 0.5f * gb * (J0[i] * J1[j] + J1[i] * J0[j]) + gc * J1[i] * J1[j];
+  float GJ0[3], GJ1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    GJ0[k] = ga * J0[k] + 0.5f * gb * J1[k];
+    GJ1[k] = 0.5f * gb * J0[k] + gc * J1[k];
+  }
+  // g_J = 2 (Gm J) Sc
+  float gJ00 = 0.f, gJ02 = 0.f, gJ11 = 0.f, gJ12 = 0.f;
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    gJ00 += 2.f * GJ0[m] * Sc[3 * m + 0];
+    gJ02 += 2.f * GJ0[m] * Sc[3 * m + 2];
+    gJ11 += 2.f * GJ1[m] * Sc[3 * m + 1];
+    gJ12 += 2.f * GJ1[m] * Sc[3 * m + 2];
+  }
+  // ---- J -> camera point
+  gq[2] += -c.fx * iz2 * gJ00 - c.fy * iz2 * gJ11;
+  if (!f.clamp_x) {
+    gq[0] += -c.fx * iz2 * gJ02;
+    gq[2] += 2.f * c.fx * f.qc[0] * iz2 * iz * gJ02;
+  } else {
+    gq[2] += c.fx * f.tx * iz2 * iz * gJ02;
+  }
+  if (!f.clamp_y) {
+    gq[1] += -c.fy * iz2 * gJ12;
+    gq[2] += 2.f * c.fy * f.qc[1] * iz2 * iz * gJ12;
+  } else {
+    gq[2] += c.fy * f.ty * iz2 * iz * gJ12;
+  }
+  // ---- camera point -> world mean: g_p += W^T g_q
+  const float* W = c.rot_cw;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) gp[k] += W[k] * gq[0] + W[3 + k] * gq[1] + W[6 + k] * gq[2];
+  gr.g[0] += gp[0];
+  gr.g[1] += gp[1];
+  gr.g[2] += gp[2];
+  // ---- Sc = W Sg W^T  ->  g_Sg = W^T g_Sc W
+  float tmp[9], gSg[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) tmp[3 * i + j] = W[i] * gSc[j] + W[3 + i] * gSc[3 + j] + W[6 + i] * gSc[6 + j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) gSg[3 * i + j] = tmp[3 * i] * W[j] + tmp[3 * i + 1] * W[3 + j] + tmp[3 * i + 2] * W[6 + j];
+  // ---- Sg = M M^T, M = Rq S  ->  g_M = 2 g_Sg M
+  float M[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) M[3 * i + j] = f.Rq[3 * i + j] * f.s[j];
+  float gM[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      gM[3 * i + j] = 2.f * (gSg[3 * i] * M[j] + gSg[3 * i + 1] * M[3 + j] + gSg[3 * i + 2] * M[6 + j]);
+  float G[9];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float gs = f.Rq[j] * gM[j] + f.Rq[3 + j] * gM[3 + j] + f.Rq[6 + j] * gM[6 + j];
+    gr.g[4 + j] += gs * f.s[j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) G[3 * i + j] = gM[3 * i + j] * f.s[j];
+  }
+  // ---- rotation -> normalised quaternion -> raw quaternion
+  const float w = f.qn[0], x = f.qn[1], y = f.qn[2], zq = f.qn[3];
+  float gqn[4];
+  gqn[0] = 2.f * (-zq * G[1] + y * G[2] + zq * G[3] - x * G[5] - y * G[6] + x * G[7]);
+  gqn[1] = 2.f * (y * G[1] + zq * G[2] + y * G[3] - 2.f * x * G[4] - w * G[5] + zq * G[6] + w * G[7] - 2.f * x * G[8]);
+  gqn[2] = 2.f * (-2.f * y * G[0] + x * G[1] + w * G[2] + x * G[3] + zq * G[5] - w * G[6] + zq * G[7] - 2.f * y * G[8]);
+  gqn[3] = 2.f * (-2.f * zq * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.f * zq * G[4] + y * G[5] + x * G[6] + y * G[7]);
+  const float dq = w * gqn[0] + x * gqn[1] + y * gqn[2] + zq * gqn[3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) gr.g[8 + k] += (gqn[k] - f.qn[k] * dq) / f.qnorm;
+}
+
+}  // namespace bs

@@ -1,0 +1,261 @@
+"""Per-rank executor of one PBDR training step (Algorithm 1).
+
+One process per GPU.  Rank k holds a shard PC_k of the Z-ordered point cloud
+(whole point groups, ascending global index) in the plane-major parameter
+layout of include/splat_b200.h plus its Adam moments.  A step over a batch
+of views runs, all on the GPU through the C ABI:
+
+  K0  bs_cull_count(MASK)        pts_culling for every batch view (line 3)
+      -> C[v]_k per view          (line 4)
+  [N>1] all_gather C -> A; host hierarchical_place -> W   (lines 6-8)
+      bs_scan_counts             SP row layout in destination order
+  K1  bs_project_fwd             pts_splatting (line 5) straight into the
+                                 all-to-all send layout
+  [N>1] all_to_all_single SP     (line 9)
+  K2  depth keys + radix sort + tile count/emit + radix sort + ranges
+  K3  bs_raster_fwd (+ fused mean-L1 loss partials)     (lines 11-15)
+  K4  bs_raster_bwd (L1 gradient recomputed in-kernel)  (lines 17-19)
+  [N>1] reverse all_to_all_single G_SP                  (line 21)
+  K1b+K5 bs_project_bwd_adam      (lines 22-27), fused per point
+
+There is no CPU path: every kernel call raises if the library or the GPU is
+missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .culling import view_plane_block
+from .scenes import CameraView
+
+_CAM_BYTES = ctypes.sizeof(nat.Camera)
+
+
+def camera_struct(view: CameraView) -> nat.Camera:
+    fx, fy, cx, cy = view.intrinsics()
+    c = nat.Camera()
+    rot_cw = np.asarray(view.rotation, dtype=np.float64).T.astype(np.float32).reshape(9)
+    for k in range(9):
+        c.rot_cw[k] = float(rot_cw[k])
+    for k in range(3):
+        c.pos[k] = float(np.float32(view.position[k]))
+    c.fx, c.fy, c.cx, c.cy = fx, fy, cx, cy
+    c.lim_x = 1.3 * math.tan(view.fov_x / 2.0)
+    c.lim_y = 1.3 * math.tan(view.fov_y / 2.0)
+    c.near_plane, c.far_plane = view.near, view.far
+    c.width, c.height = view.width, view.height
+    return c
+
+
+def camera_bytes(views) -> np.ndarray:
+    buf = bytearray()
+    for v in views:
+        buf += bytes(camera_struct(v))
+    return np.frombuffer(bytes(buf), dtype=np.uint8).reshape(len(views), _CAM_BYTES).copy()
+
+
+@dataclass
+class AdamConfig:
+    lr: np.ndarray  # (60,) per-lane learning rates
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-15
+    selective: bool = False
+
+
+class _Grow:
+    """Grow-only cache of device buffers keyed by name."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.bufs = {}
+
+    def get(self, name, n, dtype):
+        b = self.bufs.get(name)
+        if b is None or b.numel() < n or b.dtype != dtype:
+            cap = max(int(n * 1.25) + 1024, 1024)
+            b = torch.empty(cap, dtype=dtype, device=self.dev)
+            self.bufs[name] = b
+        return b[:n]
+
+
+def _bits_for(n: int) -> int:
+    return max(1, int(math.ceil(math.log2(max(n, 2)))))
+
+
+class SplatTrainer:
+    """Rank-local state + one training step.  `params` is the plane-major
+    [15, S, 4] float32 shard (ascending global point index); `group_begin`
+    (int32, n_groups+1) and `aabb` (float32, n_groups x 6) describe its point
+    groups; `views` are all dataset views (the batch picks from them);
+    `gt` is u8 [n_views, H, W, 3] (device-resident ground truth)."""
+
+    def __init__(self, params: np.ndarray, group_begin: np.ndarray, aabb: np.ndarray, views, gt=None,
+                 sh_degree: int = 3, adam: AdamConfig | None = None, device=None, comm=None,
+                 bg=(0.0, 0.0, 0.0)):
+        nat.load()
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.S = int(params.shape[1])
+        self.params = torch.as_tensor(np.ascontiguousarray(params, dtype=np.float32), device=self.dev)
+        self.exp_avg = torch.zeros_like(self.params)
+        self.exp_avg_sq = torch.zeros_like(self.params)
+        self.group_begin = torch.as_tensor(np.asarray(group_begin, dtype=np.int32), device=self.dev)
+        self.aabb = torch.as_tensor(np.ascontiguousarray(aabb, dtype=np.float32).reshape(-1, 6), device=self.dev)
+        self.n_groups = len(group_begin) - 1
+        self.views = list(views)
+        self.W, self.H = self.views[0].width, self.views[0].height
+        if any((v.width, v.height) != (self.W, self.H) for v in self.views):
+            raise ValueError("all views of a trainer must share one image size")
+        self.tiles_x = (self.W + nat.TILE - 1) // nat.TILE
+        self.tiles_y = (self.H + nat.TILE - 1) // nat.TILE
+        self.tiles = self.tiles_x * self.tiles_y
+        self.planes_all = torch.as_tensor(np.stack([view_plane_block(v, 1) for v in self.views]), device=self.dev)
+        self.cams_all = torch.as_tensor(camera_bytes(self.views), device=self.dev)
+        self.gt = None if gt is None else torch.as_tensor(gt, device=self.dev)
+        self.sh_degree = sh_degree
+        self.adam = adam if adam is not None else AdamConfig(np.full(60, 1e-3, dtype=np.float32))
+        self.step_count = 0
+        self.comm = comm
+        self.bg = bg
+        self.buf = _Grow(self.dev)
+        self.timers = None  # optional {stage: [(start_evt, end_evt), ...]}
+        self.last = {}
+
+    # ------------------------------------------------------------------ utils
+    def _t(self, name):
+        """Context manager recording CUDA events around a stage (if enabled)."""
+        trainer = self
+
+        class _T:
+            def __enter__(self_):
+                if trainer.timers is not None:
+                    self_.s = torch.cuda.Event(enable_timing=True)
+                    self_.s.record()
+                return self_
+
+            def __exit__(self_, *exc):
+                if trainer.timers is not None:
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record()
+                    trainer.timers.setdefault(name, []).append((self_.s, e))
+                return False
+
+        return _T()
+
+    # ------------------------------------------------------------------ step
+    def step(self, batch_ids, gt_batch: torch.Tensor | None = None):
+        """One training step over `batch_ids` (indices into self.views).
+        Returns the per-view mean-L1 losses as a device tensor [B]."""
+        B = len(batch_ids)
+        if not (1 <= B <= 32):
+            raise ValueError("batch must hold 1..32 views")
+        dev, S, st = self.dev, self.S, nat.stream_handle()
+        bidx = torch.as_tensor(np.asarray(batch_ids, dtype=np.int64), device=dev)
+        planes = self.planes_all.index_select(0, bidx).contiguous()
+        cams = self.cams_all.index_select(0, bidx).contiguous()
+        # ---- K0: culling -> visibility masks + per-(group, view) counts
+        mask = self.buf.get("mask", S, torch.int32)
+        counts = self.buf.get("counts", self.n_groups * B, torch.int32)
+        with self._t("cull"):
+            desc = nat.CullDesc(nat.CULL_MASK, B, 1, 1, 0, 4)
+            nat.call("bs_cull_count", desc, nat.ptr(self.params), S, None, nat.ptr(self.group_begin),
+                     nat.ptr(self.aabb), self.n_groups, nat.ptr(planes), None, None, nat.ptr(mask),
+                     nat.ptr(counts), None, st)
+        base = self.buf.get("base", self.n_groups * B, torch.int32)
+        view_rows = self.buf.get("view_rows", B, torch.int64)
+        view_row0 = self.buf.get("view_row0", B, torch.int64)
+        order = np.arange(B, dtype=np.int32)
+        nat.call("bs_scan_counts", nat.ptr(counts), self.n_groups, B, order.ctypes.data, nat.ptr(base),
+                 nat.ptr(view_rows), nat.ptr(view_row0), st)
+        rows_host = view_rows.cpu().numpy()  # C[v]_k (sync 1: sizes the splat buffers)
+        n_rows = int(rows_host.sum())
+        self.last["rows_per_view"] = rows_host.copy()
+        # ---- K1: projection into SP rows
+        sp = self.buf.get("sp", max(n_rows, 1) * nat.SP_FLOATS, torch.float32)
+        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y)
+        with self._t("project"):
+            nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask), nat.ptr(self.group_begin),
+                     self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(sp), st)
+        # ---- render every batch view locally (N = 1: W[v] = k for all v)
+        slot_cams = cams
+        seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(rows_host)[:-1]]).astype(np.int64), device=dev)
+        seg_slot = torch.arange(B, dtype=torch.int32, device=dev)
+        losses, gsp = self._render_and_backward(sp, n_rows, seg_row0, seg_slot, B, slot_cams, bidx, gt_batch)
+        # ---- K1b + K5: projection backward fused with Adam
+        self.step_count += 1
+        ad = nat.AdamDesc()
+        for k in range(60):
+            ad.lr[k] = float(self.adam.lr[k])
+        ad.beta1, ad.beta2, ad.eps = self.adam.beta1, self.adam.beta2, self.adam.eps
+        ad.step, ad.selective = self.step_count, 1 if self.adam.selective else 0
+        with self._t("project_bwd_adam"):
+            nat.call("bs_project_bwd_adam", pdesc, ad, nat.ptr(self.params), nat.ptr(self.exp_avg),
+                     nat.ptr(self.exp_avg_sq), S, nat.ptr(mask), nat.ptr(self.group_begin), self.n_groups,
+                     nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
+        return losses
+
+    def _render_and_backward(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, gt_views, gt_batch):
+        dev, st = self.dev, nat.stream_handle()
+        lib = nat.load()
+        # ---- K2: binning
+        with self._t("bin"):
+            keys = self.buf.get("dkeys", max(n_rows, 1), torch.int64)
+            vals = self.buf.get("dvals", max(n_rows, 1), torch.int32)
+            nat.call("bs_bin_depth_keys", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot),
+                     len(seg_slot), nat.ptr(keys), nat.ptr(vals), st)
+            ka = self.buf.get("dkeys_alt", max(n_rows, 1), torch.int64)
+            va = self.buf.get("dvals_alt", max(n_rows, 1), torch.int32)
+            ws = self.buf.get("sort_ws", lib.bs_radix_sort_workspace(max(n_rows, 1)), torch.uint8)
+            nat.call("bs_radix_sort_u64", nat.ptr(keys), nat.ptr(vals), nat.ptr(ka), nat.ptr(va), n_rows, None, 0,
+                     32 + _bits_for(n_slots), nat.ptr(ws), ws.numel(), st)
+            offsets = self.buf.get("offsets", max(n_rows, 1), torch.int64)
+            total = self.buf.get("total", 1, torch.int64)
+            cws = self.buf.get("count_ws", lib.bs_bin_count_workspace(max(n_rows, 1)), torch.uint8)
+            nat.call("bs_bin_count", nat.ptr(sp), nat.ptr(vals), n_rows, nat.ptr(keys), nat.ptr(slot_cams),
+                     nat.ptr(offsets), nat.ptr(total), nat.ptr(cws), cws.numel(), st)
+            n_inst = int(total.item())  # sync 2: sizes the instance buffers
+            ikeys = self.buf.get("ikeys", max(n_inst, 1), torch.int32)
+            irows = self.buf.get("irows", max(n_inst, 1), torch.int32)
+            nat.call("bs_bin_emit", nat.ptr(sp), nat.ptr(vals), n_rows, nat.ptr(keys), nat.ptr(slot_cams),
+                     self.tiles, nat.ptr(offsets), nat.ptr(ikeys), nat.ptr(irows), st)
+            ika = self.buf.get("ikeys_alt", max(n_inst, 1), torch.int32)
+            ira = self.buf.get("irows_alt", max(n_inst, 1), torch.int32)
+            ws2 = self.buf.get("sort_ws2", lib.bs_radix_sort_workspace(max(n_inst, 1)), torch.uint8)
+            nat.call("bs_radix_sort_u32", nat.ptr(ikeys), nat.ptr(irows), nat.ptr(ika), nat.ptr(ira), n_inst, None,
+                     0, _bits_for(n_slots * self.tiles), nat.ptr(ws2), ws2.numel(), st)
+            ranges = self.buf.get("ranges", n_slots * self.tiles * 2, torch.int32)
+            nat.call("bs_tile_ranges", nat.ptr(ikeys), None, n_inst, n_slots * self.tiles, nat.ptr(ranges), st)
+        self.last.update(n_rows=n_rows, n_inst=n_inst, n_slots=n_slots)
+        # ---- K3: forward + fused L1 partials
+        npx = self.H * self.W
+        image = self.buf.get("image", n_slots * npx * 3, torch.float32)
+        final_T = self.buf.get("final_T", n_slots * npx, torch.float32)
+        n_contrib = self.buf.get("n_contrib", n_slots * npx, torch.int32)
+        loss_tiles = self.buf.get("loss_tiles", n_slots * self.tiles, torch.float32)
+        rdesc = nat.RasterDesc(n_slots, self.tiles, self.W, self.H, (ctypes.c_float * 3)(*self.bg), 1)
+        if gt_batch is not None:
+            gt, gt_map = gt_batch, None
+        else:
+            gt = self.gt
+            gt_map = gt_views.to(torch.int32)
+        with self._t("raster_fwd"):
+            nat.call("bs_raster_fwd", rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
+                     nat.ptr(final_T), nat.ptr(n_contrib), nat.ptr(gt), nat.ptr(gt_map), nat.ptr(loss_tiles), st)
+        losses = self.buf.get("losses", n_slots, torch.float32)
+        nat.call("bs_reduce_loss_tiles", nat.ptr(loss_tiles), n_slots, self.tiles, self.H, self.W, nat.ptr(losses), st)
+        # ---- K4: backward
+        gsp = self.buf.get("gsp", max(n_rows, 1) * nat.GSP_FLOATS, torch.float32)
+        gsp.zero_()
+        with self._t("raster_bwd"):
+            nat.call("bs_raster_bwd", rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
+                     nat.ptr(final_T), nat.ptr(n_contrib), None, nat.ptr(gt), nat.ptr(gt_map), nat.ptr(gsp), st)
+        self.last.update(image=image, final_T=final_T, n_contrib=n_contrib, ranges=ranges, irows=irows,
+                         sp=sp, gsp=gsp)
+        return losses, gsp

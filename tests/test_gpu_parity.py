@@ -1,0 +1,332 @@
+"""GPU parity: sm_100a kernels (through the C ABI) vs the reference's golden
+vectors and the CPU oracle.
+
+Tolerances (fp32 half; integer half is bit-exact):
+  * splat state (projection forward): bit-exact (same IEEE op sequence)
+  * tile keys / per-tile sorted lists / ranges / visibility / A: bit-exact
+  * rendered image: max-abs <= 1e-4 (image range [0, ~1]); the only
+    differences are __expf vs libm expf inside alpha
+  * G_SP and parameter gradients: max-abs <= 1e-4 x max|g| per component
+    (absorbs atomic-order nondeterminism of the backward kernel)
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2512_20017_b200 import _native as nat
+from paper_2512_20017_b200 import scenes
+from paper_2512_20017_b200.culling import (EXACT, GROUP_APPROX, batch_planes, build_access_matrix, morton_codes,
+                                           radix_sort_u64, zorder_group)
+from paper_2512_20017_b200.trainer import AdamConfig, SplatTrainer, camera_bytes
+
+from _scene import c1_setup, oracle_view_pipeline
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_REL = 1e-4
+
+
+def _aerial_golden_scene():
+    return scenes.generate_aerial_scene(seed=3, n_points=6000, grid=(2, 3), n_views=10, altitude=20,
+                                        image_size=(96, 64))
+
+
+def _street_golden_scene():
+    wps = [(0, 0, 0), (60, 0, 0), (60, 50, 0), (120, 50, 0)]
+    return scenes.generate_street_scene(seed=4, n_points=3000, trajectory_waypoints=wps, n_views=12,
+                                        image_size=(80, 60), duration=5.0)
+
+
+# ---------------------------------------------------------------- integer half
+
+
+def test_morton_codes_match_reference(golden, cuda):
+    for bits in (1, 4, 10, 21):
+        got = morton_codes(golden["morton_pts"], golden["morton_bbox"], bits)
+        assert np.array_equal(got, golden[f"morton_codes_b{bits}"]), bits
+    flat = golden["morton_flat_pts"]
+    got = morton_codes(flat, np.stack([flat.min(0), flat.max(0)]), 21)
+    assert np.array_equal(got, golden["morton_flat_codes"])
+
+
+@pytest.mark.parametrize("dtype", ["u64", "u32"])
+@pytest.mark.parametrize("n", [0, 1, 7, 4096, 4097, 100_003, 1_000_000])
+def test_radix_sort_stable(cuda, n, dtype):
+    rng = np.random.default_rng(n + (1 if dtype == "u64" else 2))
+    if dtype == "u64":
+        keys = rng.integers(0, 2**40, n, dtype=np.uint64) & np.uint64(0xFFFF0000FF)  # many duplicates
+        kt = torch.as_tensor(keys.view(np.int64), device=cuda).clone()
+    else:
+        keys = rng.integers(0, 3000, n).astype(np.uint32)
+        kt = torch.as_tensor(keys.view(np.int32), device=cuda).clone()
+    vals = torch.arange(n, dtype=torch.int32, device=cuda)
+    if dtype == "u64":
+        radix_sort_u64(kt, vals, 0, 40)
+        got_keys = kt.cpu().numpy().view(np.uint64)
+    else:
+        ka, va = torch.empty_like(kt), torch.empty_like(vals)
+        ws = torch.empty(nat.load().bs_radix_sort_workspace(max(n, 1)), dtype=torch.uint8, device=cuda)
+        nat.call("bs_radix_sort_u32", nat.ptr(kt), nat.ptr(vals), nat.ptr(ka), nat.ptr(va), n, None, 0, 12,
+                 nat.ptr(ws), ws.numel(), nat.stream_handle())
+        got_keys = kt.cpu().numpy().view(np.uint32)
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(vals.cpu().numpy(), order)
+    assert np.array_equal(got_keys, keys[order])
+
+
+def test_zorder_group_matches_reference(golden, cuda):
+    ds = _aerial_golden_scene()
+    assert np.array_equal(ds.cloud.positions, golden["aerial_positions"])
+    g = zorder_group(ds.cloud, G=128)
+    assert np.array_equal(g.permutation, golden["aerial_perm"])
+    assert np.array_equal(np.stack([gr.aabb for gr in g.groups]), golden["aerial_aabb"])
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_access_matrix_matches_reference(golden, cuda, P):
+    ds = _aerial_golden_scene()
+    g = zorder_group(ds.cloud, G=128)
+    pg = golden["aerial_point_gpu"]
+    assert np.array_equal(build_access_matrix(g, pg, ds.views, P=P, granularity=EXACT), golden[f"access_exact_P{P}"])
+    assert np.array_equal(build_access_matrix(g, pg, ds.views, P=P, granularity=GROUP_APPROX),
+                          golden[f"access_group_P{P}"])
+
+
+def test_access_matrix_temporal_matches_reference(golden, cuda):
+    st = _street_golden_scene()
+    g = zorder_group(st.cloud, G=64)
+    assert np.array_equal(g.permutation, golden["street_perm"])
+    pg = golden["street_point_gpu"]
+    assert np.array_equal(build_access_matrix(g, pg, st.views, P=2, temporal=True),
+                          golden["street_access_temporal_P2"])
+    assert np.array_equal(build_access_matrix(g, pg, st.views, P=1), golden["street_access_spatial_P1"])
+
+
+def test_visibility_mask_matches_reference(golden, cuda):
+    ds = _aerial_golden_scene()
+    g = zorder_group(ds.cloud, G=128)
+    pos, gb, aabb, _ = g.device_arrays(cuda)
+    planes = torch.as_tensor(batch_planes(ds.views, 1), device=cuda)
+    B = len(ds.views)
+    mask = torch.empty(len(pos), dtype=torch.int32, device=cuda)
+    counts = torch.empty(g.n_groups * B, dtype=torch.int32, device=cuda)
+    patch = torch.empty(B, dtype=torch.int64, device=cuda)
+    nat.call("bs_cull_count", nat.CullDesc(nat.CULL_MASK, B, 1, 1, 0, 3), nat.ptr(pos), len(pos), None,
+             nat.ptr(gb), nat.ptr(aabb), g.n_groups, nat.ptr(planes), None, None, nat.ptr(mask), nat.ptr(counts),
+             nat.ptr(patch), nat.stream_handle())
+    m = mask.cpu().numpy().view(np.uint32)
+    assert np.array_equal(m, golden["aerial_vis_mask"])
+    per_view = counts.cpu().numpy().reshape(g.n_groups, B).sum(0)
+    assert np.array_equal(per_view, golden["access_exact_P1"].sum(1))
+    assert np.array_equal(patch.cpu().numpy(), golden["access_exact_P1"].sum(1))
+
+
+# ---------------------------------------------------------------- float half
+
+
+@pytest.fixture(scope="module")
+def c1(cuda):
+    ds, params, gb, aabb, gt = c1_setup()
+    return ds, params, gb, aabb, gt
+
+
+def _trainer(c1, **kw):
+    ds, params, gb, aabb, gt = c1
+    return SplatTrainer(params, gb, aabb, ds.views, gt=gt, sh_degree=3, **kw)
+
+
+def test_projection_bitexact_and_binning(c1, cuda):
+    from oracle import py_oracle
+
+    ds, params, gb, aabb, gt = c1
+    tr = _trainer(c1)
+    batch = [0, 3, 5]
+    tr.step(batch)
+    torch.cuda.synchronize()
+    sp = tr.last["sp"][: tr.last["n_rows"] * 12].cpu().numpy().reshape(-1, 12)
+    rows = tr.last["rows_per_view"]
+    row0 = np.concatenate([[0], np.cumsum(rows)])
+    ranges = tr.last["ranges"].cpu().numpy().reshape(len(batch), -1, 2)
+    irows = tr.last["irows"][: tr.last["n_inst"]].cpu().numpy()
+    for s, v in enumerate(batch):
+        ref = oracle_view_pipeline(params, gb, aabb, ds.views[v], camera_bytes([ds.views[v]]), gt[v])
+        assert rows[s] == len(ref["idx"])
+        mine = sp[row0[s]:row0[s + 1]]
+        assert np.array_equal(mine.view(np.uint32), ref["sp"].view(np.uint32)), f"view {v}: SP not bit-exact"
+        # per-tile depth-sorted lists (rows relative to the view's run)
+        rr = ranges[s]
+        assert np.array_equal(rr[:, 1] - rr[:, 0], ref["ranges"][:, 1] - ref["ranges"][:, 0])
+        for t in range(rr.shape[0]):
+            a = irows[rr[t, 0]:rr[t, 1]] - row0[s]
+            b = ref["lists"][ref["ranges"][t, 0]:ref["ranges"][t, 1]]
+            assert np.array_equal(a, b), f"view {v} tile {t}"
+
+
+def test_render_forward_and_backward_tolerance(c1, cuda):
+    ds, params, gb, aabb, gt = c1
+    tr = _trainer(c1)
+    batch = [1, 6]
+    losses = tr.step(batch).cpu().numpy()
+    n = tr.last["n_rows"]
+    H, W = tr.H, tr.W
+    img = tr.last["image"][: len(batch) * H * W * 3].cpu().numpy().reshape(len(batch), H, W, 3)
+    gsp = tr.last["gsp"][: n * 9].cpu().numpy().reshape(-1, 9)
+    rows = tr.last["rows_per_view"]
+    row0 = np.concatenate([[0], np.cumsum(rows)])
+    for s, v in enumerate(batch):
+        ref = oracle_view_pipeline(params, gb, aabb, ds.views[v], camera_bytes([ds.views[v]]), gt[v])
+        assert np.abs(img[s] - ref["img"]).max() <= IMG_TOL
+        assert abs(losses[s] - ref["loss"]) <= 1e-5
+        g = gsp[row0[s]:row0[s + 1]]
+        scale = np.abs(ref["gsp"]).max(axis=0) + 1e-30
+        err = (np.abs(g - ref["gsp"]) / scale).max(axis=0)
+        assert (err <= GRAD_REL).all(), err
+
+
+def test_projection_backward_tolerance(c1, cuda):
+    from oracle import py_oracle
+
+    ds, params, gb, aabb, gt = c1
+    tr = _trainer(c1)
+    batch = [2, 4, 7]
+    tr.step(batch)
+    # gradient of the same step through bs_project_bwd (separate kernel)
+    st = nat.stream_handle()
+    B = len(batch)
+    planes = tr.planes_all.index_select(0, torch.as_tensor(batch, device=cuda)).contiguous()
+    cams = tr.cams_all.index_select(0, torch.as_tensor(batch, device=cuda)).contiguous()
+    prm = torch.as_tensor(params, device=cuda)
+    mask = torch.empty(tr.S, dtype=torch.int32, device=cuda)
+    counts = torch.empty(tr.n_groups * B, dtype=torch.int32, device=cuda)
+    nat.call("bs_cull_count", nat.CullDesc(nat.CULL_MASK, B, 1, 1, 0, 4), nat.ptr(prm), tr.S, None,
+             nat.ptr(tr.group_begin), nat.ptr(tr.aabb), tr.n_groups, nat.ptr(planes), None, None, nat.ptr(mask),
+             nat.ptr(counts), None, st)
+    base = torch.empty_like(counts)
+    vr = torch.empty(B, dtype=torch.int64, device=cuda)
+    v0 = torch.empty(B, dtype=torch.int64, device=cuda)
+    nat.call("bs_scan_counts", nat.ptr(counts), tr.n_groups, B, None, nat.ptr(base), nat.ptr(vr), nat.ptr(v0), st)
+    n = int(vr.sum().item())
+    gsp = torch.as_tensor(np.random.default_rng(1).normal(0, 1e-3, (n, 9)).astype(np.float32), device=cuda)
+    grad = torch.zeros_like(prm)
+    nat.call("bs_project_bwd", nat.ProjDesc(B, 3, 0, 0), nat.ptr(prm), tr.S, nat.ptr(mask), nat.ptr(tr.group_begin),
+             tr.n_groups, nat.ptr(base), nat.ptr(v0), nat.ptr(cams), nat.ptr(gsp), nat.ptr(grad), st)
+    g_gpu = grad.cpu().numpy()
+    g_ref = np.zeros_like(params)
+    m = mask.cpu().numpy().view(np.uint32)
+    row = 0
+    gs = gsp.cpu().numpy()
+    for s, v in enumerate(batch):
+        idx = np.flatnonzero((m >> s) & 1).astype(np.int64)
+        py_oracle.project_bwd(params, idx, camera_bytes([ds.views[v]]), 3, gs[row:row + len(idx)], g_ref)
+        row += len(idx)
+    scale = np.abs(g_ref).reshape(15, -1, 4).max(axis=1) + 1e-30  # per (plane, lane)
+    err = (np.abs(g_gpu - g_ref).max(axis=1) / scale)
+    assert (err <= GRAD_REL).all(), err.max()
+
+
+def test_adam_matches_torch(cuda):
+    rng = np.random.default_rng(3)
+    S = 1000
+    p0 = rng.normal(0, 1, (15, S, 4)).astype(np.float32)
+    lr = rng.uniform(1e-4, 1e-2, 60).astype(np.float32)
+    p = torch.as_tensor(p0, device=cuda).clone()
+    m = torch.zeros_like(p)
+    v = torch.zeros_like(p)
+    ref = torch.nn.Parameter(torch.as_tensor(p0).clone().reshape(15, S, 4))
+    groups = [{"params": [], "lr": 0.0}]
+    # torch reference with per-lane lr: run one Adam per lane column
+    refs = []
+    for k in range(60):
+        t = torch.nn.Parameter(torch.as_tensor(p0[k // 4, :, k % 4]).clone())
+        refs.append((t, torch.optim.Adam([t], lr=float(lr[k]), betas=(0.9, 0.999), eps=1e-15)))
+    for step in range(1, 4):
+        g = rng.normal(0, 1e-2, (15, S, 4)).astype(np.float32)
+        d = nat.AdamDesc()
+        for k in range(60):
+            d.lr[k] = float(lr[k])
+        d.beta1, d.beta2, d.eps, d.step, d.selective = 0.9, 0.999, 1e-15, step, 0
+        gt = torch.as_tensor(g, device=cuda)
+        nat.call("bs_adam_step", d, nat.ptr(p), nat.ptr(gt), nat.ptr(m), nat.ptr(v), S, None, nat.stream_handle())
+        for k, (t, opt) in enumerate(refs):
+            t.grad = torch.as_tensor(g[k // 4, :, k % 4])
+            opt.step()
+    got = p.cpu().numpy()
+    for k, (t, _) in enumerate(refs):
+        np.testing.assert_allclose(got[k // 4, :, k % 4], t.detach().numpy(), rtol=1e-5, atol=1e-7)
+    del ref, groups
+
+
+def test_train_step_matches_oracle(c1, cuda):
+    from oracle import py_oracle
+
+    ds, params, gb, aabb, gt = c1
+    lr = scenes.lr_table(50.0)
+    tr = _trainer(c1, adam=AdamConfig(lr))
+    batch = [0, 2, 5, 7]
+    losses = tr.step(batch).cpu().numpy()
+    after = tr.params.cpu().numpy()
+    # oracle: gradients of the same batch, then Adam step 1
+    g_ref = np.zeros_like(params)
+    ref_losses = []
+    for v in batch:
+        r = oracle_view_pipeline(params, gb, aabb, ds.views[v], camera_bytes([ds.views[v]]), gt[v])
+        g_ref += r["gparams"]
+        ref_losses.append(r["loss"])
+    np.testing.assert_allclose(losses, ref_losses, rtol=1e-5)
+    p = params.copy()
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+    py_oracle.adam(p, g_ref, m, v, lr, 0.9, 0.999, 1e-15, 1)
+    # step 1 of Adam moves each scalar by ~lr*sign(g): compare within 2*lr where
+    # |g| is at the noise floor, tightly elsewhere
+    diff = np.abs(after - p)
+    lr_full = np.broadcast_to(lr.reshape(15, 1, 4), p.shape)
+    gscale = np.abs(g_ref).reshape(15, -1, 4).max(axis=1, keepdims=True)
+    tiny = np.abs(g_ref) <= 1e-3 * gscale
+    assert (diff[~tiny] <= 1e-3 * lr_full[~tiny] + 1e-7).mean() > 0.999
+    assert (diff <= 2.0 * lr_full + 1e-6).all()
+
+
+# ---------------------------------------------------------------- full size (C2) properties
+
+
+def test_c2_scale_properties(cuda):
+    """1M Gaussians, 1080p, batch 4: sortedness of every per-tile list by
+    (bucket, depth, row), instance conservation, image/transmittance ranges,
+    loss = mean|img - gt| recomputed, deterministic forward."""
+    ds = scenes.generate_aerial_scene(1, 1_000_000, (1, 1), 8, 50.0, (1920, 1080))
+    g = zorder_group(ds.cloud, G=2048)
+    params = scenes.init_gaussians(g.sorted_cloud, 1, scenes.mean_spacing(50.0, (1, 1), 1_000_000))
+    gt = scenes.synthetic_gt(1, 8, 1920, 1080)
+    gb = g.group_begin()
+    tr = SplatTrainer(params, gb, g.aabbs.reshape(-1, 6), ds.views, gt=gt)
+    batch = [0, 3, 4, 7]
+    losses = tr.step(batch).cpu().numpy()
+    n, I = tr.last["n_rows"], tr.last["n_inst"]
+    sp = tr.last["sp"][: n * 12].view(n, 12)
+    irows = tr.last["irows"][:I].long()
+    ranges = tr.last["ranges"].view(-1, 2)
+    assert I > n  # every visible splat covers >= 1 tile
+    # bucket of every instance from the ranges
+    lens = (ranges[:, 1] - ranges[:, 0]).clamp(min=0)
+    assert int(lens.sum()) == I
+    bucket = torch.repeat_interleave(torch.arange(len(ranges), device=cuda), lens)
+    depth = sp[irows, 9]
+    b0, b1 = bucket[:-1], bucket[1:]
+    d0, d1 = depth[:-1], depth[1:]
+    r0, r1 = irows[:-1], irows[1:]
+    ok = (b0 < b1) | ((b0 == b1) & ((d0 < d1) | ((d0 == d1) & (r0 < r1))))
+    assert bool(ok.all())
+    img = tr.last["image"][: 4 * 1080 * 1920 * 3].view(4, 1080, 1920, 3)
+    T = tr.last["final_T"][: 4 * 1080 * 1920]
+    assert float(T.min()) >= 0.0 and float(T.max()) <= 1.0
+    assert float(img.min()) >= 0.0
+    gtb = torch.as_tensor(gt[batch], device=cuda).float() / 255.0
+    ref_loss = (img - gtb).abs().mean(dim=(1, 2, 3)).cpu().numpy()
+    np.testing.assert_allclose(losses, ref_loss, rtol=1e-4)
+    assert np.isfinite(tr.last["gsp"][: n * 9].cpu().numpy()).all()
+    assert np.isfinite(tr.params.cpu().numpy()).all()
