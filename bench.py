@@ -173,6 +173,10 @@ def run_ours(args, cfg):
     tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt,
                       adam=AdamConfig(scenes.lr_table(cfg["altitude"])))
     sched = schedule(cfg["n_views"], B, args.warmup + 2 * args.steps + 2)
+    # clocks are sampled from the start of the warm-up to the end of the timed
+    # region (nvidia-smi needs ~0.5 s to start streaming)
+    clk = ClockSampler(local).__enter__()
+    time.sleep(1.0)
     for i in range(args.warmup):
         tr.step(sched[i])
     torch.cuda.synchronize()
@@ -181,18 +185,21 @@ def run_ours(args, cfg):
     lc0 = nat.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     inst, rows = [], []
-    with ClockSampler(local) as clk:
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        start.record()
-        for i in range(args.steps):
-            tr.step(sched[args.warmup + i])
-            inst.append(tr.last["n_inst"])
-            rows.append(tr.last["n_rows"])
-        end.record()
-        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    start.record()
+    for i in range(args.steps):
+        tr.step(sched[args.warmup + i])
+        inst.append(tr.last["n_inst"])
+        rows.append(tr.last["n_rows"])
+    end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk.__exit__(None, None, None)
     launches = nat.launch_count() - lc0
+    tr.last["n_visible_points"] = int((tr.buf.bufs["mask"][: tr.S] != 0).sum().item())
     ms = start.elapsed_time(end)
     if world > 1:
         t = torch.tensor([ms], device="cuda")

@@ -29,8 +29,7 @@ def build(force: bool = False) -> str:
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB):
-            build()
+        build()
         _lib = C.CDLL(_LIB)
         P, I32, I64, F, D = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_double
         sig = {
@@ -45,6 +44,7 @@ def lib():
             "or_l1_loss": (D, [P, P, I64, P]),
             "or_adam": (None, [P, P, P, P, I64, P, I64, F, F, F, I32]),
             "or_train_step": (D, [P, P, P, I64, P, P, I32, P, I32, P, F, F, F, I32, I32]),
+            "or_plane_distances": (None, [P, I64, P, I32, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -83,6 +83,15 @@ def visibility_mask(positions, group_begin, aabb, planes, B):
     pl = _c(planes, np.float64)
     out = np.zeros(len(pos), dtype=np.uint32)
     lib().or_visibility_mask(_p(pos), len(pos), _p(gb), _p(ab), len(gb) - 1, _p(pl), B, _p(out))
+    return out
+
+
+def plane_distances(points, planes):
+    """fma(z, c, fma(y, b, x*a)) + d for every (point, plane) -- the kernels' order."""
+    pts = _c(points, np.float64)
+    pl = _c(planes, np.float64)
+    out = np.zeros((len(pts), len(pl)), dtype=np.float64)
+    lib().or_plane_distances(_p(pts), len(pts), _p(pl), len(pl), _p(out))
     return out
 
 

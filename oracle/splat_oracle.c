@@ -31,6 +31,12 @@ static double pdist(const double* pl, double x, double y, double z) {
   return fma(z, pl[2], fma(y, pl[1], x * pl[0])) + pl[3];
 }
 
+/* d[i][k] for n points against m planes (exposed for the BLAS-order check) */
+void or_plane_distances(const double* pts, int64_t n, const double* planes, int32_t m, double* out) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < m; ++k) out[i * m + k] = pdist(planes + 4 * k, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+}
+
 /* plane pointer of a view block: 0 near, 1 far, 2+c x-edge c, 3+P+r y-edge r */
 static const double* vplane(const double* vp, int k) { return vp + 4 * k; }
 

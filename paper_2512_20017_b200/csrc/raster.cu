@@ -32,11 +32,12 @@ struct RastArgs {
 };
 
 // Bit-identical in both kernels (explicit round-to-nearest intrinsics).
+// a = (u, v, conic_a, conic_b), cconic = conic_c.
 __device__ __forceinline__ float splat_power(float4 a, float cconic, float px, float py, float& dx, float& dy) {
   dx = __fsub_rn(a.x, px);
   dy = __fsub_rn(a.y, py);
-  const float q = __fmaf_rn(a.w, __fmul_rn(dx, dx), __fmul_rn(cconic, __fmul_rn(dy, dy)));
-  return __fmaf_rn(-0.5f, q, -__fmul_rn(a.z, __fmul_rn(dx, dy)));
+  const float q = __fmaf_rn(a.z, __fmul_rn(dx, dx), __fmul_rn(cconic, __fmul_rn(dy, dy)));
+  return __fmaf_rn(-0.5f, q, -__fmul_rn(a.w, __fmul_rn(dx, dy)));
 }
 
 // smem staging: sa = (u, v, A, B), sb = (C, opacity, r, g), sc = b

@@ -1,0 +1,50 @@
+"""CPU checks of the C ABI: the in-tree library loads without a GPU and
+exports every entry point include/splat_b200.h declares; the ctypes table
+matches the header."""
+
+import ctypes
+import os
+import re
+
+from paper_2512_20017_b200 import _native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "splat_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    assert "bs_cull_count" in names and "bs_raster_bwd" in names and "bs_project_bwd_adam" in names
+    assert len(names) >= 25
+
+
+def test_library_exports_every_declared_symbol():
+    assert os.path.exists(_native.lib_path()), "run __graft_entry__.build() first"
+    lib = ctypes.CDLL(_native.lib_path())
+    missing = [n for n in _declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_ctypes_table_covers_header():
+    assert sorted(_native.EXPORTED) == _declared()
+
+
+def test_struct_sizes_match_header_layout():
+    # bs_camera: 9+3+4+2+2 floats + 2 int32 = 22 * 4 bytes
+    assert ctypes.sizeof(_native.Camera) == 88
+    assert ctypes.sizeof(_native.AdamDesc) == 4 * (60 + 3 + 2)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import pytest
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(_native.NativeError if hasattr(_native, "NativeError") else Exception):
+        _native.load(require_cuda=True)
