@@ -2,24 +2,35 @@
 // loss (loss_fn) and K4 backward (image_render.backward,
 // PAPER.md:503).
 //
-// One CTA of 256 threads per 16x16 tile; one pixel per thread (pixel centre
-// (x + 0.5, y + 0.5)).  Splats of the tile's depth-sorted instance range are
-// staged through shared memory in batches of 256 (one gathered SP row per
-// thread), then every thread blends the batch front to back:
+// One CTA of 128 threads per 16x16 tile.  Warp w owns the 8x8 quadrant
+// (w & 1, w >> 1) of the tile and every thread two vertically adjacent
+// pixels of it, so each staged splat is read from shared memory once per
+// two pixels.  Splats of the tile's depth-sorted instance range are staged
+// in batches of 128 (one gathered SP row per thread); at staging time every
+// splat gets a 4-bit mask of the quadrants its alpha >= 1/255 footprint
+// can reach (exact ellipse bounding box of o * exp(power) = 1/255, padded by
+// 1%), and each warp walks only its own splats, compacted with ballots, in
+// depth order.  Per pixel (centre (x + 0.5, y + 0.5)):
 //   power = -0.5 (A dx^2 + C dy^2) - B dx dy,  dx = u - px
 //   alpha = min(0.99, opacity * exp(power)); skipped if power > 0 or
 //   alpha < 1/255; the pixel stops before the splat that would bring its
 //   transmittance below 1e-4 (standard 3DGS conventions).
-// The CTA leaves the loop when every pixel is done (__syncthreads_count).
-// The backward kernel walks the same range back to front, reconstructing
-// T by division, and reduces each splat's 9 gradient terms over the warp
-// (shuffles) before one atomicAdd per term per warp.
+// The quadrant masks only drop (warp, splat) pairs whose every alpha is
+// below 1/255, so the blend is the same as walking the whole list.
+//
+// Backward walks the same range back to front (T recovered by division).
+// Per splat, each thread sums its two pixels' 9 gradient terms, the warp
+// reduce-scatters the 9 sums in 12 shuffles, the warp partials meet in
+// shared memory, and one thread per splat issues the 9 atomicAdds -- one
+// atomic set per (tile, splat) pair.
 #include "common.cuh"
 
 namespace bs {
 namespace {
 
-constexpr int kRastThreads = BS_TILE * BS_TILE;  // 256
+constexpr int kThreads = 128;
+constexpr int kWarps = kThreads / 32;
+constexpr int kBatch = kThreads;
 constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kAlphaMax = 0.99f;
 constexpr float kTMin = 1e-4f;
@@ -40,15 +51,39 @@ __device__ __forceinline__ float splat_power(float4 a, float cconic, float px, f
   return __fmaf_rn(-0.5f, q, -__fmul_rn(a.w, __fmul_rn(dx, dy)));
 }
 
-// smem staging: sa = (u, v, A, B), sb = (C, opacity, r, g), sc = b
+// smem staging: a = (u, v, A, B), b = (C, opacity, r, g), c = b-channel,
+// m = quadrant mask
 struct SplatSmem {
-  float4 a[kRastThreads];
-  float4 b[kRastThreads];
-  float c[kRastThreads];
-  uint32_t row[kRastThreads];
+  float4 a[kBatch];
+  float4 b[kBatch];
+  float c[kBatch];
+  uint32_t row[kBatch];
+  uint32_t m[kBatch];
 };
 
-__device__ __forceinline__ void stage_splat(SplatSmem& s, int j, const float* __restrict__ sp, uint32_t row) {
+// Quadrants (bit w for quadrant (w & 1, w >> 1)) of tile (tx, ty) whose
+// pixel centres can see alpha >= 1/255 from this splat.
+__device__ __forceinline__ uint32_t quadrant_mask(float u, float v, float A, float B, float C, float o, int tx,
+                                                  int ty) {
+  const float L = 2.f * __logf(255.f * o);  // q(d) <= L  <=>  o exp(-q/2) >= 1/255
+  const float detq = A * C - B * B;
+  if (!(L > 0.f) || !(detq > 0.f)) return 0u;
+  const float hx = sqrtf(L * C / detq) * 1.01f + 1e-3f;
+  const float hy = sqrtf(L * A / detq) * 1.01f + 1e-3f;
+  uint32_t m = 0;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const float x0 = (float)(tx * BS_TILE + (w & 1) * 8) + 0.5f, x1 = x0 + 7.f;
+    const float y0 = (float)(ty * BS_TILE + (w >> 1) * 8) + 0.5f, y1 = y0 + 7.f;
+    const float ex = fabsf(u - fminf(fmaxf(u, x0), x1));
+    const float ey = fabsf(v - fminf(fmaxf(v, y0), y1));
+    if (ex <= hx && ey <= hy) m |= 1u << w;
+  }
+  return m;
+}
+
+__device__ __forceinline__ void stage_splat(SplatSmem& s, int j, const float* __restrict__ sp, uint32_t row, int tx,
+                                            int ty) {
   const float4* r4 = reinterpret_cast<const float4*>(sp + (int64_t)row * BS_SP_FLOATS);
   const float4 p0 = __ldg(r4);      // u v opac A
   const float4 p1 = __ldg(r4 + 1);  // B C r g
@@ -57,81 +92,323 @@ __device__ __forceinline__ void stage_splat(SplatSmem& s, int j, const float* __
   s.b[j] = make_float4(p1.y, p0.z, p1.z, p1.w);
   s.c[j] = b;
   s.row[j] = row;
+  s.m[j] = quadrant_mask(p0.x, p0.y, p0.w, p1.x, p1.y, p0.z, tx, ty);
 }
 
-__global__ void __launch_bounds__(kRastThreads) raster_fwd_kernel(RastArgs a, const float* __restrict__ sp,
-                                                                  const uint32_t* __restrict__ inst_rows,
-                                                                  const int2* __restrict__ ranges,
-                                                                  float* __restrict__ image,
-                                                                  float* __restrict__ final_T,
-                                                                  int32_t* __restrict__ n_contrib,
-                                                                  const uint8_t* __restrict__ gt,
-                                                                  const int32_t* __restrict__ gt_view,
-                                                                  float* __restrict__ loss_tiles) {
+struct PixelFwd {
+  float T, c0, c1, c2;
+  int contrib;
+  bool done;
+};
+
+__device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float4& sb, float cb, float pxf, float pyf,
+                                      int rel) {
+  float dx, dy;
+  const float power = splat_power(sa, sb.x, pxf, pyf, dx, dy);
+  if (power > 0.f) return;
+  const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, __expf(power)));
+  if (alpha < kAlphaMin) return;
+  const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
+  if (nT < kTMin) {
+    p.done = true;
+    return;
+  }
+  const float w = __fmul_rn(alpha, p.T);
+  p.c0 = __fmaf_rn(sb.z, w, p.c0);
+  p.c1 = __fmaf_rn(sb.w, w, p.c1);
+  p.c2 = __fmaf_rn(cb, w, p.c2);
+  p.T = nT;
+  p.contrib = rel + 1;
+}
+
+// Pixel coordinates of thread `t`: quadrant of its warp, two rows.
+__device__ __forceinline__ void thread_pixels(int tile_x, int tile_y, int& px, int& py0) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  px = tile_x * BS_TILE + (w & 1) * 8 + (lane & 7);
+  py0 = tile_y * BS_TILE + (w >> 1) * 8 + 2 * (lane >> 3);
+}
+
+__global__ void __launch_bounds__(kThreads) raster_fwd_kernel(RastArgs a, const float* __restrict__ sp,
+                                                              const uint32_t* __restrict__ inst_rows,
+                                                              const int2* __restrict__ ranges,
+                                                              float* __restrict__ image, float* __restrict__ final_T,
+                                                              int32_t* __restrict__ n_contrib,
+                                                              const uint8_t* __restrict__ gt,
+                                                              const int32_t* __restrict__ gt_view,
+                                                              float* __restrict__ loss_tiles) {
   __shared__ SplatSmem s;
-  __shared__ float s_red[kRastThreads / 32];
+  __shared__ float s_red[kWarps];
   const int slot = blockIdx.z;
   const int tile = blockIdx.y * a.tiles_x + blockIdx.x;
-  const int px = blockIdx.x * BS_TILE + (threadIdx.x % BS_TILE);
-  const int py = blockIdx.y * BS_TILE + (threadIdx.x / BS_TILE);
-  const bool inside = px < a.W && py < a.H;
-  const float pxf = (float)px + 0.5f, pyf = (float)py + 0.5f;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int px, py0;
+  thread_pixels(blockIdx.x, blockIdx.y, px, py0);
+  const float pxf = (float)px + 0.5f;
+  const float pyf[2] = {(float)py0 + 0.5f, (float)py0 + 1.5f};
+  const bool in_x = px < a.W;
+  const bool inside[2] = {in_x && py0 < a.H, in_x && py0 + 1 < a.H};
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
-  float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-  int contrib = 0;
-  bool done = !inside;
-  for (int b0 = rg.x; b0 < rg.y; b0 += kRastThreads) {
-    if (__syncthreads_count(done) == kRastThreads) break;
+  PixelFwd p[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) p[k] = PixelFwd{1.f, 0.f, 0.f, 0.f, 0, !inside[k]};
+  for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
+    if (__syncthreads_count(p[0].done && p[1].done) == kThreads) break;
     const int idx = b0 + threadIdx.x;
-    if (idx < rg.y) stage_splat(s, threadIdx.x, sp, inst_rows[idx]);
+    if (idx < rg.y) stage_splat(s, threadIdx.x, sp, inst_rows[idx], blockIdx.x, blockIdx.y);
     __syncthreads();
-    const int nb = min(kRastThreads, rg.y - b0);
-    for (int j = 0; j < nb && !done; ++j) {
-      const float4 sa = s.a[j];
-      const float4 sb = s.b[j];
-      float dx, dy;
-      const float power = splat_power(sa, sb.x, pxf, pyf, dx, dy);
-      if (power > 0.f) continue;
-      const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, __expf(power)));
-      if (alpha < kAlphaMin) continue;
-      const float nT = __fmul_rn(T, __fsub_rn(1.f, alpha));
-      if (nT < kTMin) {
-        done = true;
-        break;
+    const int nb = min(kBatch, rg.y - b0);
+    for (int c0 = 0; c0 < nb; c0 += 32) {
+      if (__all_sync(0xffffffffu, p[0].done && p[1].done)) break;
+      const int jj = c0 + lane;
+      uint32_t bits = __ballot_sync(0xffffffffu, jj < nb && ((s.m[jj] >> w) & 1u));
+      while (bits) {
+        const int j = c0 + __ffs(bits) - 1;
+        bits &= bits - 1;
+        const float4 sa = s.a[j];
+        const float4 sb = s.b[j];
+        const float cb = s.c[j];
+        const int rel = b0 + j - rg.x;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          if (!p[k].done) blend(p[k], sa, sb, cb, pxf, pyf[k], rel);
       }
-      const float w = __fmul_rn(alpha, T);
-      C0 = __fmaf_rn(sb.z, w, C0);
-      C1 = __fmaf_rn(sb.w, w, C1);
-      C2 = __fmaf_rn(s.c[j], w, C2);
-      T = nT;
-      contrib = b0 + j + 1 - rg.x;
     }
   }
   float l = 0.f;
-  if (inside) {
-    const int64_t pix = ((int64_t)slot * a.H + py) * a.W + px;
-    const float o0 = C0 + T * a.bg[0], o1 = C1 + T * a.bg[1], o2 = C2 + T * a.bg[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (!inside[k]) continue;
+    const int64_t pix = ((int64_t)slot * a.H + py0 + k) * a.W + px;
+    const float o0 = p[k].c0 + p[k].T * a.bg[0], o1 = p[k].c1 + p[k].T * a.bg[1], o2 = p[k].c2 + p[k].T * a.bg[2];
     image[3 * pix] = o0;
     image[3 * pix + 1] = o1;
     image[3 * pix + 2] = o2;
-    final_T[pix] = T;
-    n_contrib[pix] = contrib;
+    final_T[pix] = p[k].T;
+    n_contrib[pix] = p[k].contrib;
     if (a.loss_fused) {
       const int gv = gt_view ? gt_view[slot] : slot;
-      const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py) * a.W + px);
-      const float g0 = gp[0] * (1.f / 255.f), g1 = gp[1] * (1.f / 255.f), g2 = gp[2] * (1.f / 255.f);
-      l = fabsf(o0 - g0) + fabsf(o1 - g1) + fabsf(o2 - g2);
+      const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py0 + k) * a.W + px);
+      l += fabsf(o0 - gp[0] * (1.f / 255.f)) + fabsf(o1 - gp[1] * (1.f / 255.f)) + fabsf(o2 - gp[2] * (1.f / 255.f));
     }
   }
   if (a.loss_fused) {
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = l;
+    if (lane == 0) s_red[w] = l;
     __syncthreads();
     if (threadIdx.x == 0) {
       float t = 0.f;
-      for (int k = 0; k < kRastThreads / 32; ++k) t += s_red[k];
+      for (int k = 0; k < kWarps; ++k) t += s_red[k];
       loss_tiles[(int64_t)slot * a.tiles_per_slot + tile] = t;
     }
+  }
+}
+
+// Reduce-scatter of 9 per-lane values over the warp in 12 shuffles.  Returns
+// the full warp sum of value `out_idx` in lanes where out_idx >= 0 (even
+// lanes; every index 0..8 appears in exactly one even lane).
+__device__ __forceinline__ float warp_reduce9(const float v[9], int& out_idx) {
+  const int lane = threadIdx.x & 31;
+  // step 1 (xor 16): lower half keeps values 0..4, upper half 5..8 (+pad)
+  const bool u16 = lane & 16;
+  float a[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const float hi = i < 4 ? v[5 + i] : 0.f;
+    const float send = u16 ? v[i] : hi;
+    const float mine = u16 ? hi : v[i];
+    a[i] = mine + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  // step 2 (xor 8): positions 0..2 | 3..4
+  const bool u8 = lane & 8;
+  float b[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float hi = i < 2 ? a[3 + i] : 0.f;
+    const float send = u8 ? a[i] : hi;
+    const float mine = u8 ? hi : a[i];
+    b[i] = mine + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  // step 3 (xor 4): positions 0..1 | 2
+  const bool u4 = lane & 4;
+  float c[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float hi = i < 1 ? b[2 + i] : 0.f;
+    const float send = u4 ? b[i] : hi;
+    const float mine = u4 ? hi : b[i];
+    c[i] = mine + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  // step 4 (xor 2): position 0 | 1
+  const bool u2 = lane & 2;
+  const float send = u2 ? c[0] : c[1];
+  const float mine = u2 ? c[1] : c[0];
+  float d = mine + __shfl_xor_sync(0xffffffffu, send, 2);
+  d += __shfl_xor_sync(0xffffffffu, d, 1);
+  // lane bits (b4 b3 b2 b1) -> value index (see the split sequence above)
+  constexpr uint64_t kMap = 0xFFF8F765FF43F210ull;  // nibble per (lane >> 1); F = none
+  const int nib = (int)((kMap >> (4 * (lane >> 1))) & 0xF);
+  out_idx = ((lane & 1) == 0 && nib != 0xF) ? nib : -1;
+  return d;
+}
+
+struct PixelBwd {
+  float T, T_final, dC0, dC1, dC2, acc0, acc1, acc2, last_alpha, lc0, lc1, lc2, bgdot;
+  int n;
+  bool inside;
+};
+
+// Gradient contribution of one splat at one pixel, added into g[9].
+__device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const float4& sb, float cb, float pxf,
+                                           float pyf, float g[9]) {
+  float dx, dy;
+  const float power = splat_power(sa, sb.x, pxf, pyf, dx, dy);
+  if (power > 0.f) return false;
+  const float ex = __expf(power);
+  const float raw = __fmul_rn(sb.y, ex);
+  const float alpha = fminf(kAlphaMax, raw);
+  if (alpha < kAlphaMin) return false;
+  const float ra = 1.f / (1.f - alpha);
+  p.T = p.T * ra;
+  const float fac = alpha * p.T;
+  g[6] += fac * p.dC0;
+  g[7] += fac * p.dC1;
+  g[8] += fac * p.dC2;
+  p.acc0 = p.last_alpha * p.lc0 + (1.f - p.last_alpha) * p.acc0;
+  p.acc1 = p.last_alpha * p.lc1 + (1.f - p.last_alpha) * p.acc1;
+  p.acc2 = p.last_alpha * p.lc2 + (1.f - p.last_alpha) * p.acc2;
+  p.last_alpha = alpha;
+  p.lc0 = sb.z;
+  p.lc1 = sb.w;
+  p.lc2 = cb;
+  float dL_dalpha = p.T * ((sb.z - p.acc0) * p.dC0 + (sb.w - p.acc1) * p.dC1 + (cb - p.acc2) * p.dC2);
+  dL_dalpha -= p.T_final * ra * p.bgdot;
+  if (raw > kAlphaMax) return true;  // clamped: colour gradient only
+  const float dpow = dL_dalpha * alpha;
+  g[2] += dL_dalpha * ex;
+  g[3] += -0.5f * dx * dx * dpow;
+  g[4] += -dx * dy * dpow;
+  g[5] += -0.5f * dy * dy * dpow;
+  g[0] += -(sa.z * dx + sa.w * dy) * dpow;
+  g[1] += -(sa.w * dx + sb.x * dy) * dpow;
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads) raster_bwd_kernel(
+    RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
+    const float* __restrict__ image, const float* __restrict__ final_T, const int32_t* __restrict__ n_contrib,
+    const float* __restrict__ grad_image, const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view,
+    float* __restrict__ g_sp) {
+  __shared__ SplatSmem s;
+  __shared__ float s_part[kWarps][kBatch][9];
+  __shared__ int s_max[kWarps];
+  const int slot = blockIdx.z;
+  const int tile = blockIdx.y * a.tiles_x + blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int px, py0;
+  thread_pixels(blockIdx.x, blockIdx.y, px, py0);
+  const float pxf = (float)px + 0.5f;
+  const float pyf[2] = {(float)py0 + 0.5f, (float)py0 + 1.5f};
+  const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
+
+  PixelBwd p[2];
+  int mx = 0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    PixelBwd& q = p[k];
+    q.inside = px < a.W && py0 + k < a.H;
+    q.T = 1.f;
+    q.n = 0;
+    q.dC0 = q.dC1 = q.dC2 = 0.f;
+    if (q.inside) {
+      const int64_t pix = ((int64_t)slot * a.H + py0 + k) * a.W + px;
+      q.T = final_T[pix];
+      q.n = n_contrib[pix];
+      if (grad_image) {
+        q.dC0 = grad_image[3 * pix];
+        q.dC1 = grad_image[3 * pix + 1];
+        q.dC2 = grad_image[3 * pix + 2];
+      } else {
+        const int gv = gt_view ? gt_view[slot] : slot;
+        const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py0 + k) * a.W + px);
+        const float d0 = image[3 * pix] - gp[0] * (1.f / 255.f);
+        const float d1 = image[3 * pix + 1] - gp[1] * (1.f / 255.f);
+        const float d2 = image[3 * pix + 2] - gp[2] * (1.f / 255.f);
+        q.dC0 = (d0 > 0.f ? 1.f : (d0 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+        q.dC1 = (d1 > 0.f ? 1.f : (d1 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+        q.dC2 = (d2 > 0.f ? 1.f : (d2 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+      }
+    }
+    q.T_final = q.T;
+    q.bgdot = a.bg[0] * q.dC0 + a.bg[1] * q.dC1 + a.bg[2] * q.dC2;
+    q.acc0 = q.acc1 = q.acc2 = q.last_alpha = q.lc0 = q.lc1 = q.lc2 = 0.f;
+    mx = max(mx, q.n);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) s_max[w] = mx;
+  __syncthreads();
+  int tile_n = 0;
+#pragma unroll
+  for (int k = 0; k < kWarps; ++k) tile_n = max(tile_n, s_max[k]);
+  const int warp_n = mx;  // deepest contributor of this warp's pixels
+
+  for (int bend = rg.x + tile_n; bend > rg.x; bend -= kBatch) {
+    const int nb = min(kBatch, bend - rg.x);
+    if ((int)threadIdx.x < nb)
+      stage_splat(s, threadIdx.x, sp, inst_rows[bend - 1 - threadIdx.x], blockIdx.x, blockIdx.y);
+    __syncthreads();
+    // splats are staged back to front: increasing j walks towards the camera
+    for (int c0 = 0; c0 < nb; c0 += 32) {
+      const int jj = c0 + lane;
+      uint32_t bits = __ballot_sync(0xffffffffu, jj < nb && ((s.m[jj] >> w) & 1u));
+      while (bits) {
+        const int j = c0 + __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int rel = bend - 1 - j - rg.x;  // range-relative index of this splat
+        float g[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) g[k] = 0.f;
+        bool any = false;
+        if (rel < warp_n) {
+          const float4 sa = s.a[j];
+          const float4 sb = s.b[j];
+          const float cb = s.c[j];
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            if (p[k].inside && rel < p[k].n) any |= pixel_grad(p[k], sa, sb, cb, pxf, pyf[k], g);
+        }
+        int idx;
+        float r = 0.f;
+        if (__any_sync(0xffffffffu, any)) {
+          r = warp_reduce9(g, idx);
+        } else {
+          idx = ((lane & 1) == 0 && lane < 18) ? (lane >> 1) : -1;  // zero this warp's slot
+        }
+        if (idx >= 0) s_part[w][j][idx] = r;
+      }
+    }
+    __syncthreads();
+    // one atomic set per (tile, splat) with a nonzero gradient
+    for (int j = threadIdx.x; j < nb; j += kThreads) {
+      const uint32_t m = s.m[j];
+      if (!m) continue;
+      float t[9];
+      bool nz = false;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        float acc = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < kWarps; ++ww)
+          if ((m >> ww) & 1u) acc += s_part[ww][j][k];
+        t[k] = acc;
+        nz |= acc != 0.f;
+      }
+      if (nz) {
+        float* dst = g_sp + (int64_t)s.row[j] * BS_GSP_FLOATS;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) atomicAdd(dst + k, t[k]);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -139,119 +416,6 @@ __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-
-__global__ void __launch_bounds__(kRastThreads) raster_bwd_kernel(
-    RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
-    const float* __restrict__ image, const float* __restrict__ final_T, const int32_t* __restrict__ n_contrib,
-    const float* __restrict__ grad_image, const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view,
-    float* __restrict__ g_sp) {
-  __shared__ SplatSmem s;
-  __shared__ int s_max[kRastThreads / 32];
-  const int slot = blockIdx.z;
-  const int tile = blockIdx.y * a.tiles_x + blockIdx.x;
-  const int px = blockIdx.x * BS_TILE + (threadIdx.x % BS_TILE);
-  const int py = blockIdx.y * BS_TILE + (threadIdx.x / BS_TILE);
-  const bool inside = px < a.W && py < a.H;
-  const float pxf = (float)px + 0.5f, pyf = (float)py + 0.5f;
-  const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
-  const int lane = threadIdx.x & 31;
-
-  float T = 1.f, dC0 = 0.f, dC1 = 0.f, dC2 = 0.f;
-  int my_n = 0;
-  if (inside) {
-    const int64_t pix = ((int64_t)slot * a.H + py) * a.W + px;
-    T = final_T[pix];
-    my_n = n_contrib[pix];
-    if (grad_image) {
-      dC0 = grad_image[3 * pix];
-      dC1 = grad_image[3 * pix + 1];
-      dC2 = grad_image[3 * pix + 2];
-    } else {
-      const int gv = gt_view ? gt_view[slot] : slot;
-      const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py) * a.W + px);
-      const float d0 = image[3 * pix] - gp[0] * (1.f / 255.f);
-      const float d1 = image[3 * pix + 1] - gp[1] * (1.f / 255.f);
-      const float d2 = image[3 * pix + 2] - gp[2] * (1.f / 255.f);
-      dC0 = (d0 > 0.f ? 1.f : (d0 < 0.f ? -1.f : 0.f)) * a.inv_norm;
-      dC1 = (d1 > 0.f ? 1.f : (d1 < 0.f ? -1.f : 0.f)) * a.inv_norm;
-      dC2 = (d2 > 0.f ? 1.f : (d2 < 0.f ? -1.f : 0.f)) * a.inv_norm;
-    }
-  }
-  // deepest contributing splat over the tile
-  int mx = my_n;
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) s_max[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  int tile_n = 0;
-  for (int k = 0; k < kRastThreads / 32; ++k) tile_n = max(tile_n, s_max[k]);
-  const float T_final = T;
-  const float bgdot = a.bg[0] * dC0 + a.bg[1] * dC1 + a.bg[2] * dC2;
-  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;          // colour behind the current splat
-  float last_alpha = 0.f, lc0 = 0.f, lc1 = 0.f, lc2 = 0.f;
-  const int end = rg.x + tile_n;
-  for (int bend = end; bend > rg.x; bend -= kRastThreads) {
-    const int bstart = max(rg.x, bend - kRastThreads);
-    const int nb = bend - bstart;
-    __syncthreads();
-    if ((int)threadIdx.x < nb) stage_splat(s, threadIdx.x, sp, inst_rows[bend - 1 - threadIdx.x]);
-    __syncthreads();
-    for (int j = 0; j < nb; ++j) {
-      const int rel = bend - 1 - j - rg.x;  // range-relative index of this splat
-      bool valid = inside && rel < my_n;
-      float g[9];
-      const float4 sa = s.a[j];
-      const float4 sb = s.b[j];
-      const float cb = s.c[j];
-      float dx = 0.f, dy = 0.f, power = 0.f, alpha = 0.f, ex = 0.f;
-      if (valid) {
-        power = splat_power(sa, sb.x, pxf, pyf, dx, dy);
-        valid = power <= 0.f;
-        if (valid) {
-          ex = __expf(power);
-          const float raw = __fmul_rn(sb.y, ex);
-          alpha = fminf(kAlphaMax, raw);
-          valid = alpha >= kAlphaMin;
-          if (valid) {
-            const float ra = 1.f / (1.f - alpha);
-            T = T * ra;
-            const float fac = alpha * T;
-            g[6] = fac * dC0;
-            g[7] = fac * dC1;
-            g[8] = fac * dC2;
-            acc0 = last_alpha * lc0 + (1.f - last_alpha) * acc0;
-            acc1 = last_alpha * lc1 + (1.f - last_alpha) * acc1;
-            acc2 = last_alpha * lc2 + (1.f - last_alpha) * acc2;
-            last_alpha = alpha;
-            lc0 = sb.z;
-            lc1 = sb.w;
-            lc2 = cb;
-            float dL_dalpha = T * ((sb.z - acc0) * dC0 + (sb.w - acc1) * dC1 + (cb - acc2) * dC2);
-            dL_dalpha -= T_final * ra * bgdot;
-            const bool clamped = raw > kAlphaMax;
-            const float dL_dpow = clamped ? 0.f : dL_dalpha * alpha;
-            g[2] = clamped ? 0.f : dL_dalpha * ex;
-            g[3] = -0.5f * dx * dx * dL_dpow;
-            g[4] = -dx * dy * dL_dpow;
-            g[5] = -0.5f * dy * dy * dL_dpow;
-            g[0] = -(sa.z * dx + sa.w * dy) * dL_dpow;
-            g[1] = -(sa.w * dx + sb.x * dy) * dL_dpow;
-          }
-        }
-      }
-      if (!__any_sync(0xffffffffu, valid)) continue;
-      if (!valid)
-#pragma unroll
-        for (int k = 0; k < 9; ++k) g[k] = 0.f;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) g[k] = warp_sum(g[k]);
-      if (lane == 0) {
-        float* dst = g_sp + (int64_t)s.row[j] * BS_GSP_FLOATS;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) atomicAdd(dst + k, g[k]);
-      }
-    }
-  }
 }
 
 __global__ void l1_loss_kernel(const float* __restrict__ img, const uint8_t* __restrict__ gt, int n_slots,
@@ -327,9 +491,9 @@ extern "C" int32_t bs_raster_fwd(const bs_raster_desc* d, const float* sp_rows, 
   if (st) return st;
   BS_REQUIRE(!a.loss_fused || (gt && loss_tiles), BS_ERR_PARAMETER, "fused loss needs gt and loss_tiles");
   const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
-  raster_fwd_kernel<<<grid, kRastThreads, 0, as_stream(stream)>>>(a, sp_rows, inst_rows,
-                                                                  reinterpret_cast<const int2*>(ranges), image,
-                                                                  final_T, n_contrib, gt, gt_slot_view, loss_tiles);
+  raster_fwd_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(a, sp_rows, inst_rows,
+                                                              reinterpret_cast<const int2*>(ranges), image, final_T,
+                                                              n_contrib, gt, gt_slot_view, loss_tiles);
   BS_LAUNCH_CHECK("raster_fwd_kernel");
   return BS_OK;
 }
@@ -343,9 +507,9 @@ extern "C" int32_t bs_raster_bwd(const bs_raster_desc* d, const float* sp_rows, 
   if (st) return st;
   BS_REQUIRE(grad_image || (image && gt), BS_ERR_PARAMETER, "raster_bwd needs grad_image or (image, gt)");
   const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
-  raster_bwd_kernel<<<grid, kRastThreads, 0, as_stream(stream)>>>(a, sp_rows, inst_rows,
-                                                                  reinterpret_cast<const int2*>(ranges), image,
-                                                                  final_T, n_contrib, grad_image, gt, gt_slot_view, g_sp);
+  raster_bwd_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(a, sp_rows, inst_rows,
+                                                              reinterpret_cast<const int2*>(ranges), image, final_T,
+                                                              n_contrib, grad_image, gt, gt_slot_view, g_sp);
   BS_LAUNCH_CHECK("raster_bwd_kernel");
   return BS_OK;
 }

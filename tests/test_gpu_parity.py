@@ -330,3 +330,38 @@ def test_c2_scale_properties(cuda):
     np.testing.assert_allclose(losses, ref_loss, rtol=1e-4)
     assert np.isfinite(tr.last["gsp"][: n * 9].cpu().numpy()).all()
     assert np.isfinite(tr.params.cpu().numpy()).all()
+
+
+# ---------------------------------------------------------------- graph + simulation on the GPU
+
+
+def test_bipartite_graph_matches_reference(golden, cuda):
+    from paper_2512_20017_b200.sharding import build_bipartite_graph
+
+    ds = _aerial_golden_scene()
+    g = zorder_group(ds.cloud, G=128)
+    graph = build_bipartite_graph(g, ds)
+    assert np.array_equal(graph.group_weights, golden["graph_group_weights"])
+    assert np.array_equal(graph.edge_groups, golden["graph_edge_groups"])
+    assert np.array_equal(graph.edge_views, golden["graph_edge_views"])
+    assert np.array_equal(graph.edge_weights, golden["graph_edge_weights"])
+
+
+def test_training_sim_report_matches_reference(golden, cuda):
+    """run_training_sim with GPU-built access matrices: byte-identical JSON."""
+    import json
+
+    from paper_2512_20017_b200 import accounting as acc
+    from paper_2512_20017_b200.assign import CostCoefficients
+
+    ds = _aerial_golden_scene()
+    topo = acc.ClusterTopology(machines=2, gpus_per_machine=2, inter_bandwidth=25e9, intra_bandwidth=300e9)
+    inter = CostCoefficients(p=4.0)
+    intra = CostCoefficients(alpha=0.0, beta=0.1, gamma=0.1, delta=1.0, p=4.0)
+    kw = dict(epochs=1, batch_size=4, P=2, seed=9)
+    loc = acc.LocalityAwareStrategy(group_size=128, seed=5, inter_coeffs=inter, intra_coeffs=intra)
+    rep_r = acc.run_training_sim(ds, topo, acc.RandomStrategy(seed=5), **kw)
+    rep_l = acc.run_training_sim(ds, topo, loc, **kw)
+    assert json.dumps(rep_r.to_json(), sort_keys=True).encode() == golden["sim_random_json"].tobytes()
+    assert json.dumps(rep_l.to_json(), sort_keys=True).encode() == golden["sim_locality_json"].tobytes()
+    assert acc.comm_reduction(rep_r, rep_l) == golden["sim_reduction"][0]
