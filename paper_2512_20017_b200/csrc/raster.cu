@@ -2,35 +2,35 @@
 // loss (loss_fn) and K4 backward (image_render.backward,
 // PAPER.md:503).
 //
-// One CTA of 128 threads per 16x16 tile.  Warp w owns the 8x8 quadrant
-// (w & 1, w >> 1) of the tile and every thread two vertically adjacent
-// pixels of it, so each staged splat is read from shared memory once per
-// two pixels.  Splats of the tile's depth-sorted instance range are staged
-// in batches of 128 (one gathered SP row per thread); at staging time every
-// splat gets a 4-bit mask of the quadrants its alpha >= 1/255 footprint
-// can reach (exact ellipse bounding box of o * exp(power) = 1/255, padded by
-// 1%), and each warp walks only its own splats, compacted with ballots, in
-// depth order.  Per pixel (centre (x + 0.5, y + 0.5)):
+// One CTA of 4 warps per 16x16 tile; warp w owns the 8x8 quadrant
+// (w & 1, w >> 1) and every lane two vertically adjacent pixels of it.  The
+// warps of a tile never synchronise with each other: each walks the tile's
+// depth-sorted instance range in chunks of 32 on its own, gathering one SP
+// row per lane (the next chunk is prefetched into registers while the
+// current one is blended), keeps only the splats whose alpha >= 1/255
+// footprint can reach its quadrant (exact bounding box of the ellipse
+// o * exp(power) = 1/255, padded by 1%), compacts them with a ballot into
+// warp-private shared memory and blends them in depth order.  Per pixel
+// (centre (x + 0.5, y + 0.5)):
 //   power = -0.5 (A dx^2 + C dy^2) - B dx dy,  dx = u - px
 //   alpha = min(0.99, opacity * exp(power)); skipped if power > 0 or
-//   alpha < 1/255; the pixel stops before the splat that would bring its
+//   alpha < 1/255; a pixel stops before the splat that would bring its
 //   transmittance below 1e-4 (standard 3DGS conventions).
-// The quadrant masks only drop (warp, splat) pairs whose every alpha is
-// below 1/255, so the blend is the same as walking the whole list.
+// The footprint filter only drops splats whose every alpha at the quadrant
+// is below 1/255, so the blend equals walking the whole list.
 //
-// Backward walks the same range back to front (T recovered by division).
-// Per splat, each thread sums its two pixels' 9 gradient terms, the warp
-// reduce-scatters the 9 sums in 12 shuffles, the warp partials meet in
-// shared memory, and one thread per splat issues the 9 atomicAdds -- one
-// atomic set per (tile, splat) pair.
+// Backward: each warp walks its own range back to front from the deepest
+// contributor of its pixels (T recovered by division); per splat each lane
+// sums its two pixels' 9 gradient terms, the warp reduce-scatters the 9
+// sums in 12 shuffles and 9 lanes issue the atomicAdds (one RED instruction
+// per (quadrant, splat) pair).
 #include "common.cuh"
 
 namespace bs {
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kWarps = kThreads / 32;
-constexpr int kBatch = kThreads;
+constexpr int kWarps = 4;
+constexpr int kThreads = 32 * kWarps;
 constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kAlphaMax = 0.99f;
 constexpr float kTMin = 1e-4f;
@@ -51,48 +51,69 @@ __device__ __forceinline__ float splat_power(float4 a, float cconic, float px, f
   return __fmaf_rn(-0.5f, q, -__fmul_rn(a.w, __fmul_rn(dx, dy)));
 }
 
-// smem staging: a = (u, v, A, B), b = (C, opacity, r, g), c = b-channel,
-// m = quadrant mask
-struct SplatSmem {
-  float4 a[kBatch];
-  float4 b[kBatch];
-  float c[kBatch];
-  uint32_t row[kBatch];
-  uint32_t m[kBatch];
+// Warp-private staging: a = (u, v, A, B), b = (C, opacity, r, g), c = b-channel
+struct WarpSmem {
+  float4 a[32];
+  float4 b[32];
+  float c[32];
+  uint32_t row[32];
 };
 
-// Quadrants (bit w for quadrant (w & 1, w >> 1)) of tile (tx, ty) whose
-// pixel centres can see alpha >= 1/255 from this splat.
-__device__ __forceinline__ uint32_t quadrant_mask(float u, float v, float A, float B, float C, float o, int tx,
-                                                  int ty) {
-  const float L = 2.f * __logf(255.f * o);  // q(d) <= L  <=>  o exp(-q/2) >= 1/255
-  const float detq = A * C - B * B;
-  if (!(L > 0.f) || !(detq > 0.f)) return 0u;
-  const float hx = sqrtf(L * C / detq) * 1.01f + 1e-3f;
-  const float hy = sqrtf(L * A / detq) * 1.01f + 1e-3f;
-  uint32_t m = 0;
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    const float x0 = (float)(tx * BS_TILE + (w & 1) * 8) + 0.5f, x1 = x0 + 7.f;
-    const float y0 = (float)(ty * BS_TILE + (w >> 1) * 8) + 0.5f, y1 = y0 + 7.f;
-    const float ex = fabsf(u - fminf(fmaxf(u, x0), x1));
-    const float ey = fabsf(v - fminf(fmaxf(v, y0), y1));
-    if (ex <= hx && ey <= hy) m |= 1u << w;
+// One gathered splat (register prefetch of the next chunk).
+struct Splat {
+  float4 p0, p1;  // (u v opac A), (B C r g)
+  float b;
+  uint32_t row;
+  bool ok;
+};
+
+__device__ __forceinline__ void fetch_splat(Splat& f, const float* __restrict__ sp,
+                                            const uint32_t* __restrict__ inst_rows, int idx, bool ok) {
+  f.ok = ok;
+  if (ok) {
+    f.row = __ldg(inst_rows + idx);
+    const float4* r4 = reinterpret_cast<const float4*>(sp + (int64_t)f.row * BS_SP_FLOATS);
+    f.p0 = __ldg(r4);
+    f.p1 = __ldg(r4 + 1);
+    f.b = __ldg(sp + (int64_t)f.row * BS_SP_FLOATS + 8);
   }
-  return m;
 }
 
-__device__ __forceinline__ void stage_splat(SplatSmem& s, int j, const float* __restrict__ sp, uint32_t row, int tx,
-                                            int ty) {
-  const float4* r4 = reinterpret_cast<const float4*>(sp + (int64_t)row * BS_SP_FLOATS);
-  const float4 p0 = __ldg(r4);      // u v opac A
-  const float4 p1 = __ldg(r4 + 1);  // B C r g
-  const float b = __ldg(sp + (int64_t)row * BS_SP_FLOATS + 8);
-  s.a[j] = make_float4(p0.x, p0.y, p0.w, p1.x);
-  s.b[j] = make_float4(p1.y, p0.z, p1.z, p1.w);
-  s.c[j] = b;
-  s.row[j] = row;
-  s.m[j] = quadrant_mask(p0.x, p0.y, p0.w, p1.x, p1.y, p0.z, tx, ty);
+// Can this splat reach alpha >= 1/255 at a pixel centre of [x0,x1] x [y0,y1]?
+__device__ __forceinline__ bool reaches(const Splat& f, float x0, float x1, float y0, float y1) {
+  if (!f.ok) return false;
+  const float u = f.p0.x, v = f.p0.y, A = f.p0.w, B = f.p1.x, C = f.p1.y, o = f.p0.z;
+  const float L = 2.f * __logf(255.f * o);  // q(d) <= L  <=>  o exp(-q/2) >= 1/255
+  const float detq = A * C - B * B;
+  if (!(L > 0.f) || !(detq > 0.f)) return false;
+  const float hx = sqrtf(L * C / detq) * 1.01f + 1e-3f;
+  const float hy = sqrtf(L * A / detq) * 1.01f + 1e-3f;
+  return fabsf(u - fminf(fmaxf(u, x0), x1)) <= hx && fabsf(v - fminf(fmaxf(v, y0), y1)) <= hy;
+}
+
+__device__ __forceinline__ void stage(WarpSmem& s, int lane, const Splat& f) {
+  s.a[lane] = make_float4(f.p0.x, f.p0.y, f.p0.w, f.p1.x);
+  s.b[lane] = make_float4(f.p1.y, f.p0.z, f.p1.z, f.p1.w);
+  s.c[lane] = f.b;
+  s.row[lane] = f.row;
+}
+
+struct Quad {
+  int px, py0;          // lane's pixels: (px, py0), (px, py0 + 1)
+  float x0, x1, y0, y1;  // pixel-centre extent of the warp's quadrant
+};
+
+__device__ __forceinline__ Quad quad_of(int tile_x, int tile_y) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Quad q;
+  const int qx = tile_x * BS_TILE + (w & 1) * 8, qy = tile_y * BS_TILE + (w >> 1) * 8;
+  q.px = qx + (lane & 7);
+  q.py0 = qy + 2 * (lane >> 3);
+  q.x0 = (float)qx + 0.5f;
+  q.x1 = q.x0 + 7.f;
+  q.y0 = (float)qy + 0.5f;
+  q.y1 = q.y0 + 7.f;
+  return q;
 }
 
 struct PixelFwd {
@@ -121,13 +142,6 @@ __device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float
   p.contrib = rel + 1;
 }
 
-// Pixel coordinates of thread `t`: quadrant of its warp, two rows.
-__device__ __forceinline__ void thread_pixels(int tile_x, int tile_y, int& px, int& py0) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  px = tile_x * BS_TILE + (w & 1) * 8 + (lane & 7);
-  py0 = tile_y * BS_TILE + (w >> 1) * 8 + 2 * (lane >> 3);
-}
-
 __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(RastArgs a, const float* __restrict__ sp,
                                                               const uint32_t* __restrict__ inst_rows,
                                                               const int2* __restrict__ ranges,
@@ -136,58 +150,55 @@ __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(RastArgs a, const 
                                                               const uint8_t* __restrict__ gt,
                                                               const int32_t* __restrict__ gt_view,
                                                               float* __restrict__ loss_tiles) {
-  __shared__ SplatSmem s;
+  __shared__ WarpSmem smem[kWarps];
   __shared__ float s_red[kWarps];
   const int slot = blockIdx.z;
   const int tile = blockIdx.y * a.tiles_x + blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int px, py0;
-  thread_pixels(blockIdx.x, blockIdx.y, px, py0);
-  const float pxf = (float)px + 0.5f;
-  const float pyf[2] = {(float)py0 + 0.5f, (float)py0 + 1.5f};
-  const bool in_x = px < a.W;
-  const bool inside[2] = {in_x && py0 < a.H, in_x && py0 + 1 < a.H};
+  WarpSmem& s = smem[w];
+  const Quad q = quad_of(blockIdx.x, blockIdx.y);
+  const float pxf = (float)q.px + 0.5f;
+  const float pyf0 = (float)q.py0 + 0.5f, pyf1 = (float)q.py0 + 1.5f;
+  const bool in_x = q.px < a.W;
+  const bool in0 = in_x && q.py0 < a.H, in1 = in_x && q.py0 + 1 < a.H;
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
-  PixelFwd p[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) p[k] = PixelFwd{1.f, 0.f, 0.f, 0.f, 0, !inside[k]};
-  for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
-    if (__syncthreads_count(p[0].done && p[1].done) == kThreads) break;
-    const int idx = b0 + threadIdx.x;
-    if (idx < rg.y) stage_splat(s, threadIdx.x, sp, inst_rows[idx], blockIdx.x, blockIdx.y);
-    __syncthreads();
-    const int nb = min(kBatch, rg.y - b0);
-    for (int c0 = 0; c0 < nb; c0 += 32) {
-      if (__all_sync(0xffffffffu, p[0].done && p[1].done)) break;
-      const int jj = c0 + lane;
-      uint32_t bits = __ballot_sync(0xffffffffu, jj < nb && ((s.m[jj] >> w) & 1u));
-      while (bits) {
-        const int j = c0 + __ffs(bits) - 1;
-        bits &= bits - 1;
-        const float4 sa = s.a[j];
-        const float4 sb = s.b[j];
-        const float cb = s.c[j];
-        const int rel = b0 + j - rg.x;
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-          if (!p[k].done) blend(p[k], sa, sb, cb, pxf, pyf[k], rel);
-      }
+  PixelFwd p0{1.f, 0.f, 0.f, 0.f, 0, !in0}, p1{1.f, 0.f, 0.f, 0.f, 0, !in1};
+  Splat f;
+  fetch_splat(f, sp, inst_rows, rg.x + lane, rg.x + lane < rg.y);
+  for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
+    if (__all_sync(0xffffffffu, p0.done && p1.done)) break;
+    const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
+    uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if (keep) stage(s, lane, f);
+    fetch_splat(f, sp, inst_rows, b0 + 32 + lane, b0 + 32 + lane < rg.y);
+    __syncwarp();
+    while (bits) {
+      const int j = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const float4 sa = s.a[j];
+      const float4 sb = s.b[j];
+      const float cb = s.c[j];
+      const int rel = b0 + j - rg.x;
+      if (!p0.done) blend(p0, sa, sb, cb, pxf, pyf0, rel);
+      if (!p1.done) blend(p1, sa, sb, cb, pxf, pyf1, rel);
     }
+    __syncwarp();
   }
   float l = 0.f;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-    if (!inside[k]) continue;
-    const int64_t pix = ((int64_t)slot * a.H + py0 + k) * a.W + px;
-    const float o0 = p[k].c0 + p[k].T * a.bg[0], o1 = p[k].c1 + p[k].T * a.bg[1], o2 = p[k].c2 + p[k].T * a.bg[2];
+    const PixelFwd& p = k ? p1 : p0;
+    if (!(k ? in1 : in0)) continue;
+    const int64_t pix = ((int64_t)slot * a.H + q.py0 + k) * a.W + q.px;
+    const float o0 = p.c0 + p.T * a.bg[0], o1 = p.c1 + p.T * a.bg[1], o2 = p.c2 + p.T * a.bg[2];
     image[3 * pix] = o0;
     image[3 * pix + 1] = o1;
     image[3 * pix + 2] = o2;
-    final_T[pix] = p[k].T;
-    n_contrib[pix] = p[k].contrib;
+    final_T[pix] = p.T;
+    n_contrib[pix] = p.contrib;
     if (a.loss_fused) {
       const int gv = gt_view ? gt_view[slot] : slot;
-      const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py0 + k) * a.W + px);
+      const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + q.py0 + k) * a.W + q.px);
       l += fabsf(o0 - gp[0] * (1.f / 255.f)) + fabsf(o1 - gp[1] * (1.f / 255.f)) + fabsf(o2 - gp[2] * (1.f / 255.f));
     }
   }
@@ -254,7 +265,6 @@ __device__ __forceinline__ float warp_reduce9(const float v[9], int& out_idx) {
 struct PixelBwd {
   float T, T_final, dC0, dC1, dC2, acc0, acc1, acc2, last_alpha, lc0, lc1, lc2, bgdot;
   int n;
-  bool inside;
 };
 
 // Gradient contribution of one splat at one pixel, added into g[9].
@@ -267,7 +277,7 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
   const float raw = __fmul_rn(sb.y, ex);
   const float alpha = fminf(kAlphaMax, raw);
   if (alpha < kAlphaMin) return false;
-  const float ra = 1.f / (1.f - alpha);
+  const float ra = __fdividef(1.f, 1.f - alpha);  // alpha <= 0.99: fast reciprocal is safe
   p.T = p.T * ra;
   const float fac = alpha * p.T;
   g[6] += fac * p.dC0;
@@ -293,122 +303,89 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
   return true;
 }
 
-__global__ void __launch_bounds__(kThreads) raster_bwd_kernel(
+__device__ __forceinline__ void init_pixel_bwd(PixelBwd& q, const RastArgs& a, int slot, int px, int py, bool inside,
+                                               const float* __restrict__ image, const float* __restrict__ final_T,
+                                               const int32_t* __restrict__ n_contrib,
+                                               const float* __restrict__ grad_image, const uint8_t* __restrict__ gt,
+                                               const int32_t* __restrict__ gt_view) {
+  q.T = 1.f;
+  q.n = 0;
+  q.dC0 = q.dC1 = q.dC2 = 0.f;
+  if (inside) {
+    const int64_t pix = ((int64_t)slot * a.H + py) * a.W + px;
+    q.T = final_T[pix];
+    q.n = n_contrib[pix];
+    if (grad_image) {
+      q.dC0 = grad_image[3 * pix];
+      q.dC1 = grad_image[3 * pix + 1];
+      q.dC2 = grad_image[3 * pix + 2];
+    } else {
+      const int gv = gt_view ? gt_view[slot] : slot;
+      const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py) * a.W + px);
+      const float d0 = image[3 * pix] - gp[0] * (1.f / 255.f);
+      const float d1 = image[3 * pix + 1] - gp[1] * (1.f / 255.f);
+      const float d2 = image[3 * pix + 2] - gp[2] * (1.f / 255.f);
+      q.dC0 = (d0 > 0.f ? 1.f : (d0 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+      q.dC1 = (d1 > 0.f ? 1.f : (d1 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+      q.dC2 = (d2 > 0.f ? 1.f : (d2 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+    }
+  }
+  q.T_final = q.T;
+  q.bgdot = a.bg[0] * q.dC0 + a.bg[1] * q.dC1 + a.bg[2] * q.dC2;
+  q.acc0 = q.acc1 = q.acc2 = q.last_alpha = q.lc0 = q.lc1 = q.lc2 = 0.f;
+}
+
+__global__ void __launch_bounds__(kThreads, 6) raster_bwd_kernel(
     RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
     const float* __restrict__ image, const float* __restrict__ final_T, const int32_t* __restrict__ n_contrib,
     const float* __restrict__ grad_image, const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view,
     float* __restrict__ g_sp) {
-  __shared__ SplatSmem s;
-  __shared__ float s_part[kWarps][kBatch][9];
-  __shared__ int s_max[kWarps];
+  __shared__ WarpSmem smem[kWarps];
   const int slot = blockIdx.z;
   const int tile = blockIdx.y * a.tiles_x + blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int px, py0;
-  thread_pixels(blockIdx.x, blockIdx.y, px, py0);
-  const float pxf = (float)px + 0.5f;
-  const float pyf[2] = {(float)py0 + 0.5f, (float)py0 + 1.5f};
+  WarpSmem& s = smem[w];
+  const Quad q = quad_of(blockIdx.x, blockIdx.y);
+  const float pxf = (float)q.px + 0.5f;
+  const float pyf0 = (float)q.py0 + 0.5f, pyf1 = (float)q.py0 + 1.5f;
+  const bool in_x = q.px < a.W;
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
-
-  PixelBwd p[2];
-  int mx = 0;
+  PixelBwd p0, p1;
+  init_pixel_bwd(p0, a, slot, q.px, q.py0, in_x && q.py0 < a.H, image, final_T, n_contrib, grad_image, gt, gt_view);
+  init_pixel_bwd(p1, a, slot, q.px, q.py0 + 1, in_x && q.py0 + 1 < a.H, image, final_T, n_contrib, grad_image, gt,
+                 gt_view);
+  int warp_n = max(p0.n, p1.n);  // deepest contributor of this warp's pixels
+  for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
+  const int end = rg.x + warp_n;
+  Splat f;
+  fetch_splat(f, sp, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
+  // chunks back to front; within a chunk lane j holds instance cend - 1 - j
+  for (int cend = end; cend > rg.x; cend -= 32) {
+    const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
+    uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if (keep) stage(s, lane, f);
+    fetch_splat(f, sp, inst_rows, cend - 33 - lane, cend - 33 - lane >= rg.x);
+    __syncwarp();
+    while (bits) {
+      const int j = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int rel = cend - 1 - j - rg.x;  // range-relative index of this splat
+      float g[9];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    PixelBwd& q = p[k];
-    q.inside = px < a.W && py0 + k < a.H;
-    q.T = 1.f;
-    q.n = 0;
-    q.dC0 = q.dC1 = q.dC2 = 0.f;
-    if (q.inside) {
-      const int64_t pix = ((int64_t)slot * a.H + py0 + k) * a.W + px;
-      q.T = final_T[pix];
-      q.n = n_contrib[pix];
-      if (grad_image) {
-        q.dC0 = grad_image[3 * pix];
-        q.dC1 = grad_image[3 * pix + 1];
-        q.dC2 = grad_image[3 * pix + 2];
-      } else {
-        const int gv = gt_view ? gt_view[slot] : slot;
-        const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py0 + k) * a.W + px);
-        const float d0 = image[3 * pix] - gp[0] * (1.f / 255.f);
-        const float d1 = image[3 * pix + 1] - gp[1] * (1.f / 255.f);
-        const float d2 = image[3 * pix + 2] - gp[2] * (1.f / 255.f);
-        q.dC0 = (d0 > 0.f ? 1.f : (d0 < 0.f ? -1.f : 0.f)) * a.inv_norm;
-        q.dC1 = (d1 > 0.f ? 1.f : (d1 < 0.f ? -1.f : 0.f)) * a.inv_norm;
-        q.dC2 = (d2 > 0.f ? 1.f : (d2 < 0.f ? -1.f : 0.f)) * a.inv_norm;
-      }
-    }
-    q.T_final = q.T;
-    q.bgdot = a.bg[0] * q.dC0 + a.bg[1] * q.dC1 + a.bg[2] * q.dC2;
-    q.acc0 = q.acc1 = q.acc2 = q.last_alpha = q.lc0 = q.lc1 = q.lc2 = 0.f;
-    mx = max(mx, q.n);
-  }
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) s_max[w] = mx;
-  __syncthreads();
-  int tile_n = 0;
-#pragma unroll
-  for (int k = 0; k < kWarps; ++k) tile_n = max(tile_n, s_max[k]);
-  const int warp_n = mx;  // deepest contributor of this warp's pixels
-
-  for (int bend = rg.x + tile_n; bend > rg.x; bend -= kBatch) {
-    const int nb = min(kBatch, bend - rg.x);
-    if ((int)threadIdx.x < nb)
-      stage_splat(s, threadIdx.x, sp, inst_rows[bend - 1 - threadIdx.x], blockIdx.x, blockIdx.y);
-    __syncthreads();
-    // splats are staged back to front: increasing j walks towards the camera
-    for (int c0 = 0; c0 < nb; c0 += 32) {
-      const int jj = c0 + lane;
-      uint32_t bits = __ballot_sync(0xffffffffu, jj < nb && ((s.m[jj] >> w) & 1u));
-      while (bits) {
-        const int j = c0 + __ffs(bits) - 1;
-        bits &= bits - 1;
-        const int rel = bend - 1 - j - rg.x;  // range-relative index of this splat
-        float g[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) g[k] = 0.f;
-        bool any = false;
-        if (rel < warp_n) {
-          const float4 sa = s.a[j];
-          const float4 sb = s.b[j];
-          const float cb = s.c[j];
-#pragma unroll
-          for (int k = 0; k < 2; ++k)
-            if (p[k].inside && rel < p[k].n) any |= pixel_grad(p[k], sa, sb, cb, pxf, pyf[k], g);
-        }
+      for (int k = 0; k < 9; ++k) g[k] = 0.f;
+      const float4 sa = s.a[j];
+      const float4 sb = s.b[j];
+      const float cb = s.c[j];
+      bool any = false;
+      if (rel < p0.n) any |= pixel_grad(p0, sa, sb, cb, pxf, pyf0, g);
+      if (rel < p1.n) any |= pixel_grad(p1, sa, sb, cb, pxf, pyf1, g);
+      if (__any_sync(0xffffffffu, any)) {
         int idx;
-        float r = 0.f;
-        if (__any_sync(0xffffffffu, any)) {
-          r = warp_reduce9(g, idx);
-        } else {
-          idx = ((lane & 1) == 0 && lane < 18) ? (lane >> 1) : -1;  // zero this warp's slot
-        }
-        if (idx >= 0) s_part[w][j][idx] = r;
+        const float r = warp_reduce9(g, idx);
+        if (idx >= 0) atomicAdd(g_sp + (int64_t)s.row[j] * BS_GSP_FLOATS + idx, r);
       }
     }
-    __syncthreads();
-    // one atomic set per (tile, splat) with a nonzero gradient
-    for (int j = threadIdx.x; j < nb; j += kThreads) {
-      const uint32_t m = s.m[j];
-      if (!m) continue;
-      float t[9];
-      bool nz = false;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        float acc = 0.f;
-#pragma unroll
-        for (int ww = 0; ww < kWarps; ++ww)
-          if ((m >> ww) & 1u) acc += s_part[ww][j][k];
-        t[k] = acc;
-        nz |= acc != 0.f;
-      }
-      if (nz) {
-        float* dst = g_sp + (int64_t)s.row[j] * BS_GSP_FLOATS;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) atomicAdd(dst + k, t[k]);
-      }
-    }
-    __syncthreads();
+    __syncwarp();
   }
 }
 

@@ -33,6 +33,7 @@ import torch
 
 from . import _native as nat
 from .culling import view_plane_block
+from .exchange import layout_for
 from .scenes import CameraView
 
 _CAM_BYTES = ctypes.sizeof(nat.Camera)
@@ -174,20 +175,50 @@ class SplatTrainer:
         order = np.arange(B, dtype=np.int32)
         nat.call("bs_scan_counts", nat.ptr(counts), self.n_groups, B, order.ctypes.data, nat.ptr(base),
                  nat.ptr(view_rows), nat.ptr(view_row0), st)
-        rows_host = view_rows.cpu().numpy()  # C[v]_k (sync 1: sizes the splat buffers)
+        lay = None
+        if self.comm is None:
+            rows_host = view_rows.cpu().numpy()  # C[v]_k (sync 1: sizes the splat buffers)
+        else:
+            # A <- all-gather C[.]_k ; W <- AssignImages(A)  (Alg. 1 lines 6-8)
+            with self._t("assign"):
+                A = self.comm.gather_access(view_rows)
+                W = self.comm.assign(A)
+                lay = layout_for(A, W, self.comm.rank)
+                rows_host = A[:, self.comm.rank].copy()
+                row0 = np.zeros(B, dtype=np.int64)
+                row0[lay.order] = np.concatenate([[0], np.cumsum(rows_host[lay.order])[:-1]])
+                view_row0.copy_(torch.as_tensor(row0))
+            self.last.update(A=A, W=W, layout=lay)
         n_rows = int(rows_host.sum())
         self.last["rows_per_view"] = rows_host.copy()
-        # ---- K1: projection into SP rows
+        # ---- K1: projection into SP rows (send layout)
         sp = self.buf.get("sp", max(n_rows, 1) * nat.SP_FLOATS, torch.float32)
         pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y)
         with self._t("project"):
             nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask), nat.ptr(self.group_begin),
                      self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(sp), st)
-        # ---- render every batch view locally (N = 1: W[v] = k for all v)
-        slot_cams = cams
-        seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(rows_host)[:-1]]).astype(np.int64), device=dev)
-        seg_slot = torch.arange(B, dtype=torch.int32, device=dev)
-        losses, gsp = self._render_and_backward(sp, n_rows, seg_row0, seg_slot, B, slot_cams, bidx, gt_batch)
+        if lay is None:
+            # every batch view is rendered here (N = 1: W[v] = k for all v)
+            seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(rows_host)[:-1]]).astype(np.int64),
+                                       device=dev)
+            seg_slot = torch.arange(B, dtype=torch.int32, device=dev)
+            losses, gsp = self._render_and_backward(sp, n_rows, seg_row0, seg_slot, B, cams, bidx, gt_batch)
+        else:
+            # SP all-to-all to the rendering ranks (line 9), render, G_SP back (line 21)
+            with self._t("a2a_fwd"):
+                sp_recv = self.comm.forward(sp[: n_rows * nat.SP_FLOATS], lay, nat.SP_FLOATS)
+            mine = torch.as_tensor(lay.my_views, device=dev)
+            seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(lay.seg_rows)[:-1]]).astype(np.int64),
+                                       device=dev)
+            seg_slot = torch.as_tensor(lay.seg_slot, device=dev)
+            gt_slots = None
+            if gt_batch is not None:
+                gt_slots = gt_batch.index_select(0, mine).contiguous()
+            losses, gsp_recv = self._render_and_backward(sp_recv.reshape(-1), lay.n_recv, seg_row0, seg_slot,
+                                                         len(lay.my_views), cams.index_select(0, mine).contiguous(),
+                                                         bidx.index_select(0, mine), gt_slots)
+            with self._t("a2a_bwd"):
+                gsp = self.comm.backward(gsp_recv[: lay.n_recv * nat.GSP_FLOATS], lay, nat.GSP_FLOATS).reshape(-1)
         # ---- K1b + K5: projection backward fused with Adam
         self.step_count += 1
         ad = nat.AdamDesc()
