@@ -72,7 +72,9 @@ int64_t bs_launch_count(void);
 /* splat-state row (SP): 12 floats, 48 B; the 11 elements of PAPER.md
  * Table tab:states-3dgs + 1 pad:
  *   0 u  1 v  2 opacity  3 conic_a  4 conic_b  5 conic_c
- *   6 r  7 g  8 b        9 depth    10 radius  11 pad (0) */
+ *   6 r  7 g  8 b        9 depth    10 radius_x  11 radius_y
+ * (the paper's single "radii" element is stored per axis: the tight box of
+ * the 3-sigma ellipse, gsplat >= 1.0 convention) */
 #define BS_SP_FLOATS 12
 /* gradient row (G_SP): 9 floats (d u, d v, d opacity, d conic a/b/c, d rgb) */
 #define BS_GSP_FLOATS 9
@@ -210,6 +212,38 @@ int32_t bs_bin_emit(const float* sp_rows, const uint32_t* sorted_rows,
 int32_t bs_tile_ranges(const uint32_t* inst_keys, const int64_t* n_dev,
                        int64_t n_host, int32_t n_buckets, int32_t* ranges,
                        void* stream);
+
+/* ---- K2, bucket pipeline (used by the training step) --------------------
+ * Same per-tile lists as the pipeline above (ascending depth, ties by row),
+ * without full-length radix passes:
+ *   count   -> bucket_counts int32 [n_buckets] (zeroed inside)
+ *   offsets -> ranges int32 [n_buckets][2], cursor int32 [n_buckets],
+ *              stats int64 [2] = {total instances, largest bucket}
+ *   scatter -> inst_keys u64 [total] = (f32bits(depth) << 32) | row, grouped
+ *              by bucket (unordered inside)
+ *   sort    -> inst_rows u32 [total]: per bucket, rows in key order; buckets
+ *              with more than smem_cap (<= bs_bin_tiles_max_sort()) keys are
+ *              skipped -- sort that slice with bs_radix_sort_u64 and take
+ *              bs_keys_low32. */
+int32_t bs_bin_tiles_count(const float* sp_rows, int64_t n_rows,
+                           const int64_t* seg_row0, const int32_t* seg_slot,
+                           int32_t n_segs, const bs_camera* slot_cams,
+                           int32_t tiles_per_slot, int32_t n_buckets,
+                           int32_t* bucket_counts, void* stream);
+int32_t bs_bin_tiles_offsets(const int32_t* bucket_counts, int32_t n_buckets,
+                             int32_t* ranges, int32_t* cursor, int64_t* stats,
+                             void* stream);
+int32_t bs_bin_tiles_scatter(const float* sp_rows, int64_t n_rows,
+                             const int64_t* seg_row0, const int32_t* seg_slot,
+                             int32_t n_segs, const bs_camera* slot_cams,
+                             int32_t tiles_per_slot, int32_t* cursor,
+                             uint64_t* inst_keys, void* stream);
+int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* ranges,
+                          int32_t n_buckets, int32_t smem_cap,
+                          uint32_t* inst_rows, void* stream);
+int32_t bs_bin_tiles_max_sort(void);
+int32_t bs_keys_low32(const uint64_t* keys, int64_t n, uint32_t* out,
+                      void* stream);
 
 /* ---- K3/L/K4: rasterisation ------------------------------------------- */
 typedef struct {

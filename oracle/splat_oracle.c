@@ -181,7 +181,7 @@ typedef struct {
   float d[3], qc[3], s[3], qn[4], qnorm, Rq[9], Sc[9];
   float J00, J02, J11, J12, tx, ty;
   int clamp_x, clamp_y;
-  float a, b, c, det, conic[3], radius, u, v, depth, len, dir[3], Y[16], col_raw[3], col[3], opac;
+  float a, b, c, det, conic[3], radius_x, radius_y, u, v, depth, len, dir[3], Y[16], col_raw[3], col[3], opac;
   int valid;
 } oproj;
 
@@ -289,13 +289,11 @@ static void proj_fwd(const opoint* pt, const or_camera* c, int n_sh, oproj* f) {
     f->conic[0] = f->c / f->det;
     f->conic[1] = (-f->b) / f->det;
     f->conic[2] = f->a / f->det;
-    const float mid = 0.5f * (f->a + f->c);
-    const float disc = fmaxf(0.1f, mid * mid - f->det);
-    const float l1 = mid + sqrtf(disc);
-    f->radius = ceilf(3.f * sqrtf(l1));
+    f->radius_x = ceilf(3.f * sqrtf(f->a));
+    f->radius_y = ceilf(3.f * sqrtf(f->c));
   } else {
     f->conic[0] = f->conic[1] = f->conic[2] = 0.f;
-    f->radius = 0.f;
+    f->radius_x = f->radius_y = 0.f;
   }
   f->u = c->fx * xr + c->cx;
   f->v = c->fy * yr + c->cy;
@@ -332,8 +330,8 @@ void or_project(const float* params, int64_t S, const int64_t* idx, int64_t m, c
     r[7] = f.col[1];
     r[8] = f.col[2];
     r[9] = f.depth;
-    r[10] = f.valid ? f.radius : 0.f;
-    r[11] = 0.f;
+    r[10] = f.valid ? f.radius_x : 0.f;
+    r[11] = f.valid ? f.radius_y : 0.f;
   }
 }
 
@@ -508,13 +506,13 @@ static int inst_cmp(const void* pa, const void* pb) {
 
 /* tiles whose span meets [u - r, u + r] (same f32 ops as csrc/bin.cu) */
 static int tile_rect(const float* row, int W, int H, int* x0, int* x1, int* y0, int* y1) {
-  const float u = row[0], v = row[1], r = row[10];
-  if (!(r > 0.f)) return 0;
+  const float u = row[0], v = row[1], rx = row[10], ry = row[11];
+  if (!(rx > 0.f) || !(ry > 0.f)) return 0;
   const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
-  *x0 = (int)fminf(fmaxf(floorf((u - r) * 0.0625f), 0.f), (float)tx);
-  *x1 = (int)fminf(fmaxf(floorf((u + r) * 0.0625f) + 1.f, 0.f), (float)tx);
-  *y0 = (int)fminf(fmaxf(floorf((v - r) * 0.0625f), 0.f), (float)ty);
-  *y1 = (int)fminf(fmaxf(floorf((v + r) * 0.0625f) + 1.f, 0.f), (float)ty);
+  *x0 = (int)fminf(fmaxf(floorf((u - rx) * 0.0625f), 0.f), (float)tx);
+  *x1 = (int)fminf(fmaxf(floorf((u + rx) * 0.0625f) + 1.f, 0.f), (float)tx);
+  *y0 = (int)fminf(fmaxf(floorf((v - ry) * 0.0625f), 0.f), (float)ty);
+  *y1 = (int)fminf(fmaxf(floorf((v + ry) * 0.0625f) + 1.f, 0.f), (float)ty);
   if (*x1 <= *x0 || *y1 <= *y0) return 0;
   return (*x1 - *x0) * (*y1 - *y0);
 }

@@ -12,30 +12,13 @@
 //     on the 64-bit key ((slot, tile) << 32 | depth).
 //  6. bs_tile_ranges    : [start, end) of every bucket.
 //
-// Tile rectangle of a splat (integer-exact on host and device):
-//   x0 = clamp(floor((u - r) / 16), 0, tiles_x), x1 = clamp(floor((u + r) / 16) + 1, 0, tiles_x)
-// (and the same in y): the tiles whose pixel span meets [u - r, u + r].
-#include "common.cuh"
+// Tile rectangles: tile.cuh.  The training step uses the bucket + per-tile
+// sort pipeline of bin_tiles.cu; this radix-sort pipeline is kept as an
+// alternative ABI (and cross-check) producing the identical lists.
+#include "tile.cuh"
 
 namespace bs {
 namespace {
-
-__device__ __forceinline__ int tile_rect(const float* __restrict__ row, int W, int H, int& x0, int& x1, int& y0,
-                                         int& y1) {
-  const float u = row[0], v = row[1], r = row[10];
-  if (!(r > 0.f)) {
-    x0 = x1 = y0 = y1 = 0;
-    return 0;
-  }
-  const int tx = (W + BS_TILE - 1) / BS_TILE, ty = (H + BS_TILE - 1) / BS_TILE;
-  const float inv = 1.0f / BS_TILE;  // exact power of two
-  x0 = (int)fminf(fmaxf(floorf(fmul(fsub(u, r), inv)), 0.f), (float)tx);
-  x1 = (int)fminf(fmaxf(fadd(floorf(fmul(fadd(u, r), inv)), 1.f), 0.f), (float)tx);
-  y0 = (int)fminf(fmaxf(floorf(fmul(fsub(v, r), inv)), 0.f), (float)ty);
-  y1 = (int)fminf(fmaxf(fadd(floorf(fmul(fadd(v, r), inv)), 1.f), 0.f), (float)ty);
-  if (x1 <= x0 || y1 <= y0) return 0;
-  return (x1 - x0) * (y1 - y0);
-}
 
 __global__ void depth_keys_kernel(const float* __restrict__ sp, int64_t n, const int64_t* __restrict__ seg_row0,
                                   const int32_t* __restrict__ seg_slot, int n_segs, uint64_t* __restrict__ keys,

@@ -9,7 +9,8 @@
 //
 // Conventions (builder-chosen standard 3DGS, frozen here):
 //   EWA dilation 0.3 px^2, Jacobian clamp |x/z| <= 1.3 tan(fov/2),
-//   radius = ceil(3 sqrt(lambda_max)), SH degree <= 3 with colour
+//   radii = ceil(3 sqrt(cov2d_xx)), ceil(3 sqrt(cov2d_yy)) (per-axis 3-sigma
+//   box, the gsplat >= 1.0 convention), SH degree <= 3 with colour
 //   max(sum + 0.5, 0), opacity = sigmoid(logit), scale = exp(log_scale).
 #pragma once
 #include "common.cuh"
@@ -53,7 +54,7 @@ struct ProjFwd {
   float tx, ty;
   float a, b, c, det;  // dilated 2D covariance
   float conic[3];
-  float radius;
+  float radius_x, radius_y;
   float u, v, depth;
   float len, dir[3];
   float Y[16];
@@ -201,13 +202,12 @@ __device__ __forceinline__ void project_forward(const PointIn& pt, const bs_came
     f.conic[0] = fdiv(f.c, f.det);
     f.conic[1] = fdiv(-f.b, f.det);
     f.conic[2] = fdiv(f.a, f.det);
-    const float mid = fmul(0.5f, fadd(f.a, f.c));
-    const float disc = fmaxf(0.1f, fsub(fmul(mid, mid), f.det));
-    const float l1 = fadd(mid, fsqrt(disc));
-    f.radius = ceilf(fmul(3.f, fsqrt(l1)));
+    // per-axis 3-sigma extents = the tight bounding box of the 3-sigma ellipse
+    f.radius_x = ceilf(fmul(3.f, fsqrt(f.a)));
+    f.radius_y = ceilf(fmul(3.f, fsqrt(f.c)));
   } else {
     f.conic[0] = f.conic[1] = f.conic[2] = 0.f;
-    f.radius = 0.f;
+    f.radius_x = f.radius_y = 0.f;
   }
   f.u = fadd(fmul(c.fx, xr), c.cx);
   f.v = fadd(fmul(c.fy, yr), c.cy);
@@ -233,7 +233,7 @@ __device__ __forceinline__ void write_sp_row(float* __restrict__ row, const Proj
   float4* r4 = reinterpret_cast<float4*>(row);
   r4[0] = make_float4(f.u, f.v, f.opac, f.conic[0]);
   r4[1] = make_float4(f.conic[1], f.conic[2], f.col[0], f.col[1]);
-  r4[2] = make_float4(f.col[2], f.depth, f.valid ? f.radius : 0.f, 0.f);
+  r4[2] = make_float4(f.col[2], f.depth, f.valid ? f.radius_x : 0.f, f.valid ? f.radius_y : 0.f);
 }
 
 // Gradient of the 60-float parameter row of one point (plane layout order:

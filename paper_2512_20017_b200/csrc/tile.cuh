@@ -1,0 +1,39 @@
+// Tile geometry shared by the binning kernels.
+#pragma once
+#include "common.cuh"
+
+namespace bs {
+
+// Tile rectangle of a splat (integer-exact on host and device), per-axis
+// radii rx = sp[10], ry = sp[11]:
+//   x0 = clamp(floor((u - rx) / 16), 0, tiles_x), x1 = clamp(floor((u + rx) / 16) + 1, 0, tiles_x)
+// (and the same in y with ry): the tiles whose pixel span meets the box.
+__device__ __forceinline__ int tile_rect(const float* __restrict__ row, int W, int H, int& x0, int& x1, int& y0,
+                                         int& y1) {
+  const float u = row[0], v = row[1], rx = row[10], ry = row[11];
+  if (!(rx > 0.f) || !(ry > 0.f)) {
+    x0 = x1 = y0 = y1 = 0;
+    return 0;
+  }
+  const int tx = (W + BS_TILE - 1) / BS_TILE, ty = (H + BS_TILE - 1) / BS_TILE;
+  const float inv = 1.0f / BS_TILE;  // exact power of two
+  x0 = (int)fminf(fmaxf(floorf(fmul(fsub(u, rx), inv)), 0.f), (float)tx);
+  x1 = (int)fminf(fmaxf(fadd(floorf(fmul(fadd(u, rx), inv)), 1.f), 0.f), (float)tx);
+  y0 = (int)fminf(fmaxf(floorf(fmul(fsub(v, ry), inv)), 0.f), (float)ty);
+  y1 = (int)fminf(fmaxf(fadd(floorf(fmul(fadd(v, ry), inv)), 1.f), 0.f), (float)ty);
+  if (x1 <= x0 || y1 <= y0) return 0;
+  return (x1 - x0) * (y1 - y0);
+}
+
+// Segment (render slot run) of row r: last s with seg_row0[s] <= r.
+__device__ __forceinline__ int segment_of(const int64_t* __restrict__ seg_row0, int n_segs, int64_t r) {
+  int lo = 0, hi = n_segs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (seg_row0[mid] <= r) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+}  // namespace bs

@@ -128,6 +128,8 @@ class SplatTrainer:
         self.buf = _Grow(self.dev)
         self.timers = None  # optional {stage: [(start_evt, end_evt), ...]}
         self.last = {}
+        self.binning = "bucket"  # or "radix" (identical lists, see csrc/bin_tiles.cu)
+        self.sort_cap = 4096     # bucket sizes sorted in shared memory
 
     # ------------------------------------------------------------------ utils
     def _t(self, name):
@@ -232,37 +234,78 @@ class SplatTrainer:
                      nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
         return losses
 
+    def _bin_buckets(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams):
+        """Bucket pipeline (csrc/bin_tiles.cu): atomics into (slot, tile)
+        buckets, then a shared-memory sort of every bucket by (depth, row)."""
+        st, lib = nat.stream_handle(), nat.load()
+        nb = n_slots * self.tiles
+        counts = self.buf.get("bucket_counts", nb, torch.int32)
+        nat.call("bs_bin_tiles_count", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
+                 nat.ptr(slot_cams), self.tiles, nb, nat.ptr(counts), st)
+        ranges = self.buf.get("ranges", nb * 2, torch.int32)
+        cursor = self.buf.get("cursor", nb, torch.int32)
+        stats = self.buf.get("bin_stats", 2, torch.int64)
+        nat.call("bs_bin_tiles_offsets", nat.ptr(counts), nb, nat.ptr(ranges), nat.ptr(cursor), nat.ptr(stats), st)
+        n_inst, biggest = (int(x) for x in stats.cpu().tolist())  # sync 2: sizes the instance buffers
+        keys = self.buf.get("inst_keys", max(n_inst, 1), torch.int64)
+        irows = self.buf.get("irows", max(n_inst, 1), torch.int32)
+        nat.call("bs_bin_tiles_scatter", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
+                 nat.ptr(slot_cams), self.tiles, nat.ptr(cursor), nat.ptr(keys), st)
+        cap = min(self.sort_cap, lib.bs_bin_tiles_max_sort())
+        nat.call("bs_bin_tiles_sort", nat.ptr(keys), nat.ptr(ranges), nb, cap, nat.ptr(irows), st)
+        if biggest > cap:  # rare: buckets beyond the shared-memory sort
+            rg = ranges.view(-1, 2).cpu().numpy()
+            for b in np.flatnonzero(rg[:, 1] - rg[:, 0] > cap):
+                s0, s1 = int(rg[b, 0]), int(rg[b, 1])
+                k = keys[s0:s1]
+                v = torch.empty(s1 - s0, dtype=torch.int32, device=self.dev)
+                from .culling import radix_sort_u64
+                radix_sort_u64(k, v, 0, 64)
+                nat.call("bs_keys_low32", nat.ptr(k), s1 - s0, nat.ptr(irows[s0:s1]), st)
+        self.last["largest_bucket"] = biggest
+        return n_inst, irows, ranges
+
+    def _bin_radix(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams):
+        """Radix pipeline (csrc/bin.cu + sort.cu): stable depth sort of the rows,
+        tile emission in depth order, stable tile sort, ranges."""
+        st, lib = nat.stream_handle(), nat.load()
+        keys = self.buf.get("dkeys", max(n_rows, 1), torch.int64)
+        vals = self.buf.get("dvals", max(n_rows, 1), torch.int32)
+        nat.call("bs_bin_depth_keys", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot),
+                 len(seg_slot), nat.ptr(keys), nat.ptr(vals), st)
+        ka = self.buf.get("dkeys_alt", max(n_rows, 1), torch.int64)
+        va = self.buf.get("dvals_alt", max(n_rows, 1), torch.int32)
+        ws = self.buf.get("sort_ws", lib.bs_radix_sort_workspace(max(n_rows, 1)), torch.uint8)
+        nat.call("bs_radix_sort_u64", nat.ptr(keys), nat.ptr(vals), nat.ptr(ka), nat.ptr(va), n_rows, None, 0,
+                 32 + _bits_for(n_slots), nat.ptr(ws), ws.numel(), st)
+        offsets = self.buf.get("offsets", max(n_rows, 1), torch.int64)
+        total = self.buf.get("total", 1, torch.int64)
+        cws = self.buf.get("count_ws", lib.bs_bin_count_workspace(max(n_rows, 1)), torch.uint8)
+        nat.call("bs_bin_count", nat.ptr(sp), nat.ptr(vals), n_rows, nat.ptr(keys), nat.ptr(slot_cams),
+                 nat.ptr(offsets), nat.ptr(total), nat.ptr(cws), cws.numel(), st)
+        n_inst = int(total.item())  # sync 2: sizes the instance buffers
+        ikeys = self.buf.get("ikeys", max(n_inst, 1), torch.int32)
+        irows = self.buf.get("irows", max(n_inst, 1), torch.int32)
+        nat.call("bs_bin_emit", nat.ptr(sp), nat.ptr(vals), n_rows, nat.ptr(keys), nat.ptr(slot_cams),
+                 self.tiles, nat.ptr(offsets), nat.ptr(ikeys), nat.ptr(irows), st)
+        ika = self.buf.get("ikeys_alt", max(n_inst, 1), torch.int32)
+        ira = self.buf.get("irows_alt", max(n_inst, 1), torch.int32)
+        ws2 = self.buf.get("sort_ws2", lib.bs_radix_sort_workspace(max(n_inst, 1)), torch.uint8)
+        nat.call("bs_radix_sort_u32", nat.ptr(ikeys), nat.ptr(irows), nat.ptr(ika), nat.ptr(ira), n_inst, None,
+                 0, _bits_for(n_slots * self.tiles), nat.ptr(ws2), ws2.numel(), st)
+        ranges = self.buf.get("ranges", n_slots * self.tiles * 2, torch.int32)
+        nat.call("bs_tile_ranges", nat.ptr(ikeys), None, n_inst, n_slots * self.tiles, nat.ptr(ranges), st)
+        return n_inst, irows, ranges
+
     def _render_and_backward(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, gt_views, gt_batch):
         dev, st = self.dev, nat.stream_handle()
         lib = nat.load()
         # ---- K2: binning
         with self._t("bin"):
-            keys = self.buf.get("dkeys", max(n_rows, 1), torch.int64)
-            vals = self.buf.get("dvals", max(n_rows, 1), torch.int32)
-            nat.call("bs_bin_depth_keys", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot),
-                     len(seg_slot), nat.ptr(keys), nat.ptr(vals), st)
-            ka = self.buf.get("dkeys_alt", max(n_rows, 1), torch.int64)
-            va = self.buf.get("dvals_alt", max(n_rows, 1), torch.int32)
-            ws = self.buf.get("sort_ws", lib.bs_radix_sort_workspace(max(n_rows, 1)), torch.uint8)
-            nat.call("bs_radix_sort_u64", nat.ptr(keys), nat.ptr(vals), nat.ptr(ka), nat.ptr(va), n_rows, None, 0,
-                     32 + _bits_for(n_slots), nat.ptr(ws), ws.numel(), st)
-            offsets = self.buf.get("offsets", max(n_rows, 1), torch.int64)
-            total = self.buf.get("total", 1, torch.int64)
-            cws = self.buf.get("count_ws", lib.bs_bin_count_workspace(max(n_rows, 1)), torch.uint8)
-            nat.call("bs_bin_count", nat.ptr(sp), nat.ptr(vals), n_rows, nat.ptr(keys), nat.ptr(slot_cams),
-                     nat.ptr(offsets), nat.ptr(total), nat.ptr(cws), cws.numel(), st)
-            n_inst = int(total.item())  # sync 2: sizes the instance buffers
-            ikeys = self.buf.get("ikeys", max(n_inst, 1), torch.int32)
-            irows = self.buf.get("irows", max(n_inst, 1), torch.int32)
-            nat.call("bs_bin_emit", nat.ptr(sp), nat.ptr(vals), n_rows, nat.ptr(keys), nat.ptr(slot_cams),
-                     self.tiles, nat.ptr(offsets), nat.ptr(ikeys), nat.ptr(irows), st)
-            ika = self.buf.get("ikeys_alt", max(n_inst, 1), torch.int32)
-            ira = self.buf.get("irows_alt", max(n_inst, 1), torch.int32)
-            ws2 = self.buf.get("sort_ws2", lib.bs_radix_sort_workspace(max(n_inst, 1)), torch.uint8)
-            nat.call("bs_radix_sort_u32", nat.ptr(ikeys), nat.ptr(irows), nat.ptr(ika), nat.ptr(ira), n_inst, None,
-                     0, _bits_for(n_slots * self.tiles), nat.ptr(ws2), ws2.numel(), st)
-            ranges = self.buf.get("ranges", n_slots * self.tiles * 2, torch.int32)
-            nat.call("bs_tile_ranges", nat.ptr(ikeys), None, n_inst, n_slots * self.tiles, nat.ptr(ranges), st)
+            if self.binning == "radix":
+                n_inst, irows, ranges = self._bin_radix(sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams)
+            else:
+                n_inst, irows, ranges = self._bin_buckets(sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams)
         self.last.update(n_rows=n_rows, n_inst=n_inst, n_slots=n_slots)
         # ---- K3: forward + fused L1 partials
         npx = self.H * self.W

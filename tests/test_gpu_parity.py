@@ -365,3 +365,21 @@ def test_training_sim_report_matches_reference(golden, cuda):
     assert json.dumps(rep_r.to_json(), sort_keys=True).encode() == golden["sim_random_json"].tobytes()
     assert json.dumps(rep_l.to_json(), sort_keys=True).encode() == golden["sim_locality_json"].tobytes()
     assert acc.comm_reduction(rep_r, rep_l) == golden["sim_reduction"][0]
+
+
+def test_binning_pipelines_agree_and_large_bucket_fallback(c1, cuda):
+    """Bucket pipeline (default), radix pipeline and the large-bucket
+    fallback (tiny shared-memory capacity) give identical per-tile lists."""
+    outs = []
+    for mode, cap in (("bucket", 4096), ("radix", 4096), ("bucket", 8)):
+        tr = _trainer(c1)
+        tr.binning, tr.sort_cap = mode, cap
+        tr.step([0, 3, 5])
+        torch.cuda.synchronize()
+        n = tr.last["n_inst"]
+        outs.append((tr.last["ranges"].cpu().numpy().copy(), tr.last["irows"][:n].cpu().numpy().copy(),
+                     tr.last["image"][: 3 * 128 * 128 * 3].cpu().numpy().copy()))
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0])
+        assert np.array_equal(o[1], outs[0][1])
+        assert np.array_equal(o[2], outs[0][2])
