@@ -54,39 +54,42 @@ __global__ void __launch_bounds__(1024) offsets_kernel(const int32_t* __restrict
   __shared__ int64_t s_w[32];
   __shared__ int s_mx[32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  int64_t carry = 0;
+  // each thread owns a contiguous run of buckets: one block-wide scan total
+  const int per = (nb + 1023) / 1024;
+  const int b_lo = min(nb, tid * per), b_hi = min(nb, b_lo + per);
+  int64_t local = 0;
   int mx = 0;
-  for (int b0 = 0; b0 < nb; b0 += 1024) {
-    const int i = b0 + tid;
-    const int64_t v = i < nb ? counts[i] : 0;
-    mx = max(mx, (int)v);
-    int64_t x = v;
+  for (int i = b_lo; i < b_hi; ++i) {
+    const int v = counts[i];
+    local += v;
+    mx = max(mx, v);
+  }
+  int64_t x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t t = s_w[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
     }
-    if (lane == 31) s_w[w] = x;
-    __syncthreads();
-    if (w == 0) {
-      int64_t t = s_w[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
-        if (lane >= o) t += y;
-      }
-      s_w[lane] = t;
-    }
-    __syncthreads();
-    const int64_t start = carry + (w ? s_w[w - 1] : 0) + x - v;
-    if (i < nb) {
-      ranges[i] = make_int2((int)start, (int)(start + v));
-      cursor[i] = (int)start;
-    }
-    const int64_t tot = s_w[31];
-    __syncthreads();
-    carry += tot;
+    s_w[lane] = t;
   }
+  __syncthreads();
+  int64_t start = (w ? s_w[w - 1] : 0) + x - local;
+  for (int i = b_lo; i < b_hi; ++i) {
+    const int v = counts[i];
+    ranges[i] = make_int2((int)start, (int)(start + v));
+    cursor[i] = (int)start;
+    start += v;
+  }
+  const int64_t carry = s_w[31];
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (lane == 0) s_mx[w] = mx;
   __syncthreads();
@@ -113,13 +116,58 @@ __global__ void scatter_tiles_kernel(BinGeom g, int32_t* __restrict__ cursor, ui
   }
 }
 
+// Small buckets (n <= kWarpCap): one warp per bucket, bitonic network over
+// the padded power of two in warp-private shared memory, every lane owning
+// whole compare-exchange pairs (no idle half, only __syncwarp).
+constexpr int kWarpCap = 1024;
+constexpr int kSortWarpsPerCta = 8;
+
+__global__ void __launch_bounds__(32 * kSortWarpsPerCta) sort_tiles_warp_kernel(const uint64_t* __restrict__ keys,
+                                                                                 const int2* __restrict__ ranges,
+                                                                                 int nb, int cap,
+                                                                                 uint32_t* __restrict__ rows) {
+  extern __shared__ uint64_t s_all[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kSortWarpsPerCta + w;
+  if (b >= nb) return;
+  const int2 rg = ranges[b];
+  const int n = rg.y - rg.x;
+  if (n <= 0 || n > cap || n > kWarpCap) return;
+  if (n == 1) {
+    if (lane == 0) rows[rg.x] = (uint32_t)keys[rg.x];
+    return;
+  }
+  uint64_t* s = s_all + w * kWarpCap;
+  int m = 2;
+  while (m < n) m <<= 1;
+  for (int i = lane; i < m; i += 32) s[i] = i < n ? keys[rg.x + i] : ~0ull;
+  __syncwarp();
+  const int half = m >> 1;
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int p = lane; p < half; p += 32) {
+        const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));  // bit log2(j) of i is 0
+        const int ixj = i | j;
+        const uint64_t a = s[i], c = s[ixj];
+        if ((a > c) == ((i & k) == 0)) {
+          s[i] = c;
+          s[ixj] = a;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  for (int i = lane; i < n; i += 32) rows[rg.x + i] = (uint32_t)s[i];
+}
+
+// Buckets with kWarpCap < n <= cap: one CTA each.
 __global__ void __launch_bounds__(kSortThreads) sort_tiles_kernel(const uint64_t* __restrict__ keys,
                                                                   const int2* __restrict__ ranges, int cap,
                                                                   uint32_t* __restrict__ rows) {
   __shared__ uint64_t s[kSortCap];
   const int2 rg = ranges[blockIdx.x];
   const int n = rg.y - rg.x;
-  if (n <= 0 || n > cap) return;
+  if (n <= kWarpCap || n > cap) return;
   if (n == 1) {
     if (threadIdx.x == 0) rows[rg.x] = (uint32_t)keys[rg.x];
     return;
@@ -198,9 +246,17 @@ extern "C" int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* r
   BS_REQUIRE(smem_cap >= 1 && smem_cap <= kSortCap, BS_ERR_PARAMETER, "bin: smem_cap must be in [1, %d]",
              kSortCap);
   if (n_buckets == 0) return BS_OK;
-  sort_tiles_kernel<<<n_buckets, kSortThreads, 0, as_stream(stream)>>>(inst_keys, reinterpret_cast<const int2*>(ranges),
-                                                                       smem_cap, inst_rows);
-  BS_LAUNCH_CHECK("sort_tiles_kernel");
+  cudaStream_t s = as_stream(stream);
+  const size_t wsmem = sizeof(uint64_t) * kWarpCap * kSortWarpsPerCta;
+  cudaFuncSetAttribute(sort_tiles_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
+  sort_tiles_warp_kernel<<<(n_buckets + kSortWarpsPerCta - 1) / kSortWarpsPerCta, 32 * kSortWarpsPerCta, wsmem, s>>>(
+      inst_keys, reinterpret_cast<const int2*>(ranges), n_buckets, smem_cap, inst_rows);
+  BS_LAUNCH_CHECK("sort_tiles_warp_kernel");
+  if (smem_cap > kWarpCap) {
+    sort_tiles_kernel<<<n_buckets, kSortThreads, 0, s>>>(inst_keys, reinterpret_cast<const int2*>(ranges), smem_cap,
+                                                         inst_rows);
+    BS_LAUNCH_CHECK("sort_tiles_kernel");
+  }
   return BS_OK;
 }
 

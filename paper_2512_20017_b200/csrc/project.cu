@@ -95,10 +95,12 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
   }
 }
 
-// Accumulate the parameter gradient of one point over all its views.
+// Accumulate the parameter gradient of one point over all its views:
+// geometry (12 floats) into g, SH coefficients through sh_add.
+template <class SH, class ShAdd>
 __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camera* s_cam, const int64_t* s_row0,
-                                               const RowRanker& rk, uint32_t mask, const PointIn& pt,
-                                               const float* __restrict__ gsp, PointGrad& gr) {
+                                               const RowRanker& rk, uint32_t mask, const PointIn& pt, const SH& sh,
+                                               const float* __restrict__ gsp, float* g, ShAdd sh_add) {
   uint32_t m = mask;
   while (m) {
     const int v = __ffs(m) - 1;
@@ -109,8 +111,8 @@ __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camer
 #pragma unroll
     for (int k = 0; k < 9; ++k) gs[k] = src[k];
     ProjFwd f;
-    project_forward(pt, s_cam[v], a.n_sh, f);
-    project_backward(pt, s_cam[v], a.n_sh, f, gs, gr);
+    project_forward_t(pt, sh, s_cam[v], a.n_sh, f);
+    project_backward_t(pt, sh, s_cam[v], a.n_sh, f, gs, g, sh_add);
   }
 }
 
@@ -139,7 +141,8 @@ __global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, c
       PointGrad gr;
 #pragma unroll
       for (int k = 0; k < 60; ++k) gr.g[k] = 0.f;
-      point_backward(a, s_cam, s_row0, rk, mask, pt, gsp, gr);
+      point_backward(a, s_cam, s_row0, rk, mask, pt, ShRegs{pt.sh}, gsp, gr.g,
+                     [&](int f, float v) { gr.g[12 + f] += v; });
 #pragma unroll
       for (int p = 0; p < BS_PARAM_PLANES; ++p) {
         float4 acc = gparams[p * a.S + i];
@@ -193,11 +196,12 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamConsts c, float4* __restr
   }
 }
 
-__global__ void __launch_bounds__(kProjThreads) project_bwd_adam_kernel(ProjArgs a, AdamConsts c,
-                                                                        const float* __restrict__ gsp,
-                                                                        float4* params,
-                                                                        float4* __restrict__ m,
-                                                                        float4* __restrict__ v) {
+__global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjArgs a, AdamConsts c,
+                                                                           const float* __restrict__ gsp,
+                                                                           float4* params,
+                                                                           float4* __restrict__ m,
+                                                                           float4* __restrict__ v) {
+  extern __shared__ float s_gsh[];  // [48][kProjThreads]
   __shared__ uint32_t s_bal[kProjWarps * kMaxViews];
   __shared__ int s_run[kMaxViews];
   __shared__ bs_camera s_cam[kMaxViews];
@@ -217,19 +221,30 @@ __global__ void __launch_bounds__(kProjThreads) project_bwd_adam_kernel(ProjArgs
     const uint32_t mask = ok ? a.mask[i] : 0u;
     rk.round(mask, B);
     if (ok && !(c.selective && mask == 0u)) {
-      PointGrad gr;
+      // geometry gradient in registers, the 48 SH gradients in this thread's
+      // shared-memory column (keeps the register peak below the
+      // 2-CTAs-per-SM budget)
+      float g12[12];
 #pragma unroll
-      for (int k = 0; k < 60; ++k) gr.g[k] = 0.f;
+      for (int k = 0; k < 12; ++k) g12[k] = 0.f;
+      float* my_sh = s_gsh + threadIdx.x;
+#pragma unroll
+      for (int f = 0; f < 48; ++f) my_sh[f * kProjThreads] = 0.f;
       if (mask) {
         PointIn pt;
-        load_point(a.params, a.S, i, a.n_sh, pt);
-        point_backward(a, s_cam, s_row0, rk, mask, pt, gsp, gr);
+        load_point(a.params, a.S, i, 0, pt);  // geometry planes only; SH read from L1 on use
+        const ShPlanes sh{reinterpret_cast<const float*>(a.params), a.S, i};
+        point_backward(a, s_cam, s_row0, rk, mask, pt, sh, gsp, g12,
+                       [&](int f, float val) { my_sh[f * kProjThreads] += val; });
       }
 #pragma unroll
       for (int p = 0; p < BS_PARAM_PLANES; ++p) {
         const int64_t t = p * a.S + i;
         float4 pp = params[t], mm = m[t], vv = v[t];
-        adam4(pp, make_float4(gr.g[4 * p], gr.g[4 * p + 1], gr.g[4 * p + 2], gr.g[4 * p + 3]), mm, vv, c, p);
+        const float4 gg = p < 3 ? make_float4(g12[4 * p], g12[4 * p + 1], g12[4 * p + 2], g12[4 * p + 3])
+                                : make_float4(my_sh[(4 * p - 12) * kProjThreads], my_sh[(4 * p - 11) * kProjThreads],
+                                              my_sh[(4 * p - 10) * kProjThreads], my_sh[(4 * p - 9) * kProjThreads]);
+        adam4(pp, gg, mm, vv, c, p);
         params[t] = pp;
         m[t] = mm;
         v[t] = vv;
@@ -396,7 +411,9 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams};
   AdamConsts c = make_adam(ad);
-  project_bwd_adam_kernel<<<n_groups, kProjThreads, 0, as_stream(stream)>>>(
+  const size_t smem = sizeof(float) * 48 * kProjThreads;
+  cudaFuncSetAttribute(project_bwd_adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  project_bwd_adam_kernel<<<n_groups, kProjThreads, smem, as_stream(stream)>>>(
       a, c, g_sp, reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(exp_avg),
       reinterpret_cast<float4*>(exp_avg_sq));
   BS_LAUNCH_CHECK("project_bwd_adam_kernel");

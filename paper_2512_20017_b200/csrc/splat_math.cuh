@@ -113,7 +113,31 @@ __device__ __forceinline__ void sh_basis(const float dir[3], int n_sh, float Y[1
   }
 }
 
+// SH coefficient accessors: from the registers of a loaded point, or straight
+// from the plane-major parameters (L1-resident) to keep 48 registers free.
+struct ShRegs {
+  const float* sh;
+  __device__ __forceinline__ float operator()(int f) const { return sh[f]; }
+};
+struct ShPlanes {
+  const float* params;  // plane-major float4 planes as floats
+  int64_t S, i;
+  __device__ __forceinline__ float operator()(int f) const {
+    return __ldg(params + ((int64_t)(3 + (f >> 2)) * S + i) * 4 + (f & 3));
+  }
+};
+
+template <class SH>
+__device__ __forceinline__ void project_forward_t(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
+                                                  ProjFwd& f);
+
 __device__ __forceinline__ void project_forward(const PointIn& pt, const bs_camera& c, int n_sh, ProjFwd& f) {
+  project_forward_t(pt, ShRegs{pt.sh}, c, n_sh, f);
+}
+
+template <class SH>
+__device__ __forceinline__ void project_forward_t(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
+                                                  ProjFwd& f) {
   // camera frame: q = Rcw (p - pos)
 #pragma unroll
   for (int k = 0; k < 3; ++k) f.d[k] = fsub(pt.p[k], c.pos[k]);
@@ -219,10 +243,10 @@ __device__ __forceinline__ void project_forward(const PointIn& pt, const bs_came
   sh_basis(f.dir, n_sh, f.Y);
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
-    float acc = fmul(f.Y[0], pt.sh[ch]);
+    float acc = fmul(f.Y[0], sh(ch));
 #pragma unroll
     for (int k = 1; k < 16; ++k)
-      if (k < n_sh) acc = fadd(acc, fmul(f.Y[k], pt.sh[3 * k + ch]));
+      if (k < n_sh) acc = fadd(acc, fmul(f.Y[k], sh(3 * k + ch)));
     f.col_raw[ch] = fadd(acc, 0.5f);
     f.col[ch] = fmaxf(f.col_raw[ch], 0.f);
   }
@@ -288,10 +312,23 @@ __device__ __forceinline__ void sh_dir_grad(const float dir[3], int n_sh, const 
   }
 }
 
-// Accumulate d L / d params of one (point, view) pair into gr.
+// Accumulate d L / d params of one (point, view) pair: the 12 geometry
+// floats (plane 0..2 order) into g, the SH coefficient gradients through
+// sh_add(flat index f = 3k + channel, value).
 // gsp = (du, dv, dopac, dA, dB, dC, dr, dg, db).
+template <class SH, class ShAdd>
+__device__ __forceinline__ void project_backward_t(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
+                                                   const ProjFwd& f, const float gsp[9], float* g, ShAdd sh_add);
+
+template <class ShAdd>
 __device__ __forceinline__ void project_backward(const PointIn& pt, const bs_camera& c, int n_sh,
-                                                 const ProjFwd& f, const float gsp[9], PointGrad& gr) {
+                                                 const ProjFwd& f, const float gsp[9], float* g, ShAdd sh_add) {
+  project_backward_t(pt, ShRegs{pt.sh}, c, n_sh, f, gsp, g, sh_add);
+}
+
+template <class SH, class ShAdd>
+__device__ __forceinline__ void project_backward_t(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
+                                                   const ProjFwd& f, const float gsp[9], float* g, ShAdd sh_add) {
   if (!f.valid) return;
   // ---- colour -> sh, dir
   float dc[3];
@@ -305,8 +342,8 @@ __device__ __forceinline__ void project_backward(const PointIn& pt, const bs_cam
     if (k >= n_sh) break;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      gr.g[12 + 3 * k + ch] += f.Y[k] * dc[ch];
-      wk[k] += dc[ch] * pt.sh[3 * k + ch];
+      sh_add(3 * k + ch, f.Y[k] * dc[ch]);
+      wk[k] += dc[ch] * sh(3 * k + ch);
     }
   }
   float gdir[3];
@@ -316,7 +353,7 @@ __device__ __forceinline__ void project_backward(const PointIn& pt, const bs_cam
 #pragma unroll
   for (int k = 0; k < 3; ++k) gp[k] = (gdir[k] - f.dir[k] * dd) / f.len;
   // ---- opacity
-  gr.g[3] += gsp[2] * f.opac * (1.f - f.opac);
+  g[3] += gsp[2] * f.opac * (1.f - f.opac);
   // ---- means2d -> camera point
   const float z = f.qc[2], iz = 1.f / z, iz2 = iz * iz;
   float gq[3];
@@ -373,9 +410,9 @@ __device__ __forceinline__ void project_backward(const PointIn& pt, const bs_cam
   const float* W = c.rot_cw;
 #pragma unroll
   for (int k = 0; k < 3; ++k) gp[k] += W[k] * gq[0] + W[3 + k] * gq[1] + W[6 + k] * gq[2];
-  gr.g[0] += gp[0];
-  gr.g[1] += gp[1];
-  gr.g[2] += gp[2];
+  g[0] += gp[0];
+  g[1] += gp[1];
+  g[2] += gp[2];
   // ---- Sc = W Sg W^T  ->  g_Sg = W^T g_Sc W
   float tmp[9], gSg[9];
 #pragma unroll
@@ -402,7 +439,7 @@ __device__ __forceinline__ void project_backward(const PointIn& pt, const bs_cam
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
     const float gs = f.Rq[j] * gM[j] + f.Rq[3 + j] * gM[3 + j] + f.Rq[6 + j] * gM[6 + j];
-    gr.g[4 + j] += gs * f.s[j];
+    g[4 + j] += gs * f.s[j];
 #pragma unroll
     for (int i = 0; i < 3; ++i) G[3 * i + j] = gM[3 * i + j] * f.s[j];
   }
@@ -415,7 +452,7 @@ __device__ __forceinline__ void project_backward(const PointIn& pt, const bs_cam
   gqn[3] = 2.f * (-2.f * zq * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.f * zq * G[4] + y * G[5] + x * G[6] + y * G[7]);
   const float dq = w * gqn[0] + x * gqn[1] + y * gqn[2] + zq * gqn[3];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) gr.g[8 + k] += (gqn[k] - f.qn[k] * dq) / f.qnorm;
+  for (int k = 0; k < 4; ++k) g[8 + k] += (gqn[k] - f.qn[k] * dq) / f.qnorm;
 }
 
 }  // namespace bs

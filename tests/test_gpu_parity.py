@@ -383,3 +383,24 @@ def test_binning_pipelines_agree_and_large_bucket_fallback(c1, cuda):
         assert np.array_equal(o[0], outs[0][0])
         assert np.array_equal(o[1], outs[0][1])
         assert np.array_equal(o[2], outs[0][2])
+
+
+def test_c2_bucket_and_radix_binning_identical(cuda):
+    """At full C2 size the bucket pipeline (warp/CTA shared-memory sorts and
+    the large-bucket fallback) reproduces the radix pipeline's lists."""
+    ds = scenes.generate_aerial_scene(1, 1_000_000, (1, 1), 8, 50.0, (1920, 1080))
+    g = zorder_group(ds.cloud, G=2048)
+    params = scenes.init_gaussians(g.sorted_cloud, 1, scenes.mean_spacing(50.0, (1, 1), 1_000_000))
+    gt = scenes.synthetic_gt(1, 8, 1920, 1080)
+    res = []
+    for mode, cap in (("bucket", 4096), ("radix", 4096), ("bucket", 600)):
+        tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt)
+        tr.binning, tr.sort_cap = mode, cap
+        tr.step([2, 5])
+        torch.cuda.synchronize()
+        n = tr.last["n_inst"]
+        res.append((tr.last["ranges"].cpu().numpy().copy(), tr.last["irows"][:n].cpu().numpy().copy(),
+                    tr.last.get("largest_bucket")))
+        del tr
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(res[0][0], res[2][0]) and np.array_equal(res[0][1], res[2][1])
