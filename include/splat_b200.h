@@ -232,7 +232,8 @@ int32_t bs_bin_tiles_count(const float* sp_rows, int64_t n_rows,
                            int32_t* bucket_counts, void* stream);
 int32_t bs_bin_tiles_offsets(const int32_t* bucket_counts, int32_t n_buckets,
                              int32_t* ranges, int32_t* cursor, int64_t* stats,
-                             void* stream);
+                             void* workspace, size_t ws_bytes, void* stream);
+size_t bs_bin_tiles_offsets_workspace(int32_t n_buckets);
 int32_t bs_bin_tiles_scatter(const float* sp_rows, int64_t n_rows,
                              const int64_t* seg_row0, const int32_t* seg_slot,
                              int32_t n_segs, const bs_camera* slot_cams,
@@ -252,6 +253,7 @@ typedef struct {
   int32_t width, height;  /* common image size of all slots */
   float bg[3];
   int32_t loss_fused;     /* 1: gt given, fwd writes L1 partials per tile */
+  int32_t pixels_per_lane;/* 1: 8x4 pixel region per warp, 2 (default, 0): 8x8 */
 } bs_raster_desc;
 /* image: f32 [n_slots][H][W][3]; final_T: f32 [n_slots][H][W];
  * n_contrib: int32 [n_slots][H][W] (range-relative end of the blend);

@@ -55,7 +55,7 @@ class ProjDesc(C.Structure):
 class RasterDesc(C.Structure):
     _fields_ = [("n_slots", C.c_int32), ("tiles_per_slot", C.c_int32),
                 ("width", C.c_int32), ("height", C.c_int32),
-                ("bg", C.c_float * 3), ("loss_fused", C.c_int32)]
+                ("bg", C.c_float * 3), ("loss_fused", C.c_int32), ("pixels_per_lane", C.c_int32)]
 
 
 class AdamDesc(C.Structure):
@@ -90,7 +90,8 @@ _SIGS = {
     "bs_bin_emit": (_I32, [_P, _P, _I64, _P, _P, _I32, _P, _P, _P, _P]),
     "bs_tile_ranges": (_I32, [_P, _P, _I64, _I32, _P, _P]),
     "bs_bin_tiles_count": (_I32, [_P, _I64, _P, _P, _I32, _P, _I32, _I32, _P, _P]),
-    "bs_bin_tiles_offsets": (_I32, [_P, _I32, _P, _P, _P, _P]),
+    "bs_bin_tiles_offsets": (_I32, [_P, _I32, _P, _P, _P, _P, _SZ, _P]),
+    "bs_bin_tiles_offsets_workspace": (_SZ, [_I32]),
     "bs_bin_tiles_scatter": (_I32, [_P, _I64, _P, _P, _I32, _P, _I32, _P, _P, _P]),
     "bs_bin_tiles_sort": (_I32, [_P, _P, _I32, _I32, _P, _P]),
     "bs_bin_tiles_max_sort": (_I32, []),

@@ -48,23 +48,13 @@ __global__ void count_tiles_kernel(BinGeom g, int32_t* __restrict__ counts) {
   }
 }
 
-__global__ void __launch_bounds__(1024) offsets_kernel(const int32_t* __restrict__ counts, int nb,
-                                                       int2* __restrict__ ranges, int32_t* __restrict__ cursor,
-                                                       int64_t* __restrict__ stats) {
-  __shared__ int64_t s_w[32];
-  __shared__ int s_mx[32];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  // each thread owns a contiguous run of buckets: one block-wide scan total
-  const int per = (nb + 1023) / 1024;
-  const int b_lo = min(nb, tid * per), b_hi = min(nb, b_lo + per);
-  int64_t local = 0;
-  int mx = 0;
-  for (int i = b_lo; i < b_hi; ++i) {
-    const int v = counts[i];
-    local += v;
-    mx = max(mx, v);
-  }
-  int64_t x = local;
+// Bucket offsets: 3-phase scan (per-block sums, scan of the block sums,
+// block-local scan + offset), every access coalesced.
+constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ int64_t block_exscan(int64_t v, int64_t* s_w, int64_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -73,7 +63,7 @@ __global__ void __launch_bounds__(1024) offsets_kernel(const int32_t* __restrict
   if (lane == 31) s_w[w] = x;
   __syncthreads();
   if (w == 0) {
-    int64_t t = s_w[lane];
+    int64_t t = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
@@ -82,22 +72,67 @@ __global__ void __launch_bounds__(1024) offsets_kernel(const int32_t* __restrict
     s_w[lane] = t;
   }
   __syncthreads();
-  int64_t start = (w ? s_w[w - 1] : 0) + x - local;
-  for (int i = b_lo; i < b_hi; ++i) {
-    const int v = counts[i];
-    ranges[i] = make_int2((int)start, (int)(start + v));
-    cursor[i] = (int)start;
-    start += v;
-  }
-  const int64_t carry = s_w[31];
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) s_mx[w] = mx;
+  if (total) *total = s_w[(blockDim.x >> 5) - 1];
+  return (w ? s_w[w - 1] : 0) + x - v;
+}
+
+__global__ void __launch_bounds__(kScanBlock) bucket_sums_kernel(const int32_t* __restrict__ counts, int nb,
+                                                                  int64_t* __restrict__ part, int* __restrict__ pmax) {
+  __shared__ int64_t s_w[32];
+  __shared__ int s_m[32];
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  const int v = i < nb ? counts[i] : 0;
+  int64_t tot;
+  block_exscan(v, s_w, &tot);
+  int m = v;
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
   __syncthreads();
-  if (tid == 0) {
-    int m = 0;
-    for (int k = 0; k < 32; ++k) m = max(m, s_mx[k]);
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < 32; ++k) m = max(m, s_m[k]);
+    part[blockIdx.x] = tot;
+    pmax[blockIdx.x] = max(m, s_m[0]);
+  }
+}
+
+__global__ void __launch_bounds__(kScanBlock) bucket_parts_kernel(int64_t* __restrict__ part,
+                                                                   const int* __restrict__ pmax, int np,
+                                                                   int64_t* __restrict__ stats) {
+  __shared__ int64_t s_w[32];
+  __shared__ int s_m[32];
+  int64_t carry = 0;
+  int m = 0;
+  for (int b0 = 0; b0 < np; b0 += kScanBlock) {
+    const int i = b0 + threadIdx.x;
+    const int64_t v = i < np ? part[i] : 0;
+    if (i < np) m = max(m, pmax[i]);
+    int64_t tot;
+    const int64_t ex = block_exscan(v, s_w, &tot);
+    if (i < np) part[i] = carry + ex;
+    __syncthreads();
+    carry += tot;
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 32; ++k) m = max(m, s_m[k]);
     stats[0] = carry;
     stats[1] = m;
+  }
+}
+
+__global__ void __launch_bounds__(kScanBlock) bucket_ranges_kernel(const int32_t* __restrict__ counts, int nb,
+                                                                    const int64_t* __restrict__ part,
+                                                                    int2* __restrict__ ranges,
+                                                                    int32_t* __restrict__ cursor) {
+  __shared__ int64_t s_w[32];
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  const int v = i < nb ? counts[i] : 0;
+  const int64_t start = part[blockIdx.x] + block_exscan(v, s_w, nullptr);
+  if (i < nb) {
+    ranges[i] = make_int2((int)start, (int)(start + v));
+    cursor[i] = (int)start;
   }
 }
 
@@ -220,12 +255,28 @@ extern "C" int32_t bs_bin_tiles_count(const float* sp_rows, int64_t n_rows, cons
   return BS_OK;
 }
 
+extern "C" size_t bs_bin_tiles_offsets_workspace(int32_t n_buckets) {
+  const size_t np = (size_t)(n_buckets + kScanBlock - 1) / kScanBlock;
+  return (sizeof(int64_t) + sizeof(int)) * (np > 0 ? np : 1);
+}
+
 extern "C" int32_t bs_bin_tiles_offsets(const int32_t* bucket_counts, int32_t n_buckets, int32_t* ranges,
-                                        int32_t* cursor, int64_t* stats, void* stream) {
+                                        int32_t* cursor, int64_t* stats, void* workspace, size_t ws_bytes,
+                                        void* stream) {
   BS_REQUIRE(n_buckets >= 1, BS_ERR_PARAMETER, "bin: bad bucket count");
-  offsets_kernel<<<1, 1024, 0, as_stream(stream)>>>(bucket_counts, n_buckets, reinterpret_cast<int2*>(ranges),
-                                                    cursor, stats);
-  BS_LAUNCH_CHECK("offsets_kernel");
+  cudaStream_t s = as_stream(stream);
+  const int np = (n_buckets + kScanBlock - 1) / kScanBlock;
+  BS_REQUIRE(ws_bytes >= bs_bin_tiles_offsets_workspace(n_buckets), BS_ERR_CAPACITY,
+             "bin offsets workspace too small");
+  int64_t* part = static_cast<int64_t*>(workspace);
+  int* pmax = reinterpret_cast<int*>(part + np);
+  bucket_sums_kernel<<<np, kScanBlock, 0, s>>>(bucket_counts, n_buckets, part, pmax);
+  BS_LAUNCH_CHECK("bucket_sums_kernel");
+  bucket_parts_kernel<<<1, kScanBlock, 0, s>>>(part, pmax, np, stats);
+  BS_LAUNCH_CHECK("bucket_parts_kernel");
+  bucket_ranges_kernel<<<np, kScanBlock, 0, s>>>(bucket_counts, n_buckets, part, reinterpret_cast<int2*>(ranges),
+                                                 cursor);
+  BS_LAUNCH_CHECK("bucket_ranges_kernel");
   return BS_OK;
 }
 

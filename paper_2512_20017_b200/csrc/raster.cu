@@ -29,8 +29,6 @@
 namespace bs {
 namespace {
 
-constexpr int kWarps = 4;
-constexpr int kThreads = 32 * kWarps;
 constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kAlphaMax = 0.99f;
 constexpr float kTMin = 1e-4f;
@@ -98,23 +96,26 @@ __device__ __forceinline__ void stage(WarpSmem& s, int lane, const Splat& f) {
   s.row[lane] = f.row;
 }
 
-struct Quad {
-  int px, py0;          // lane's pixels: (px, py0), (px, py0 + 1)
-  float x0, x1, y0, y1;  // pixel-centre extent of the warp's quadrant
+// Pixel region of a warp: 8 x (4 * PPL) pixels, PPL vertically adjacent
+// pixels per lane; a 16x16 tile holds 8 / PPL such regions (one per warp).
+template <int PPL>
+struct Region {
+  static constexpr int kH = 4 * PPL;
+  static constexpr int kWarps = (BS_TILE * BS_TILE) / (32 * PPL);
+  static constexpr int kThreads = 32 * kWarps;
+  int px, py0;           // lane's pixels: (px, py0 + k), k < PPL
+  float x0, x1, y0, y1;  // pixel-centre extent of the warp's region
+  __device__ __forceinline__ Region(int tile_x, int tile_y) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rx = tile_x * BS_TILE + (w & 1) * 8, ry = tile_y * BS_TILE + (w >> 1) * kH;
+    px = rx + (lane & 7);
+    py0 = ry + PPL * (lane >> 3);
+    x0 = (float)rx + 0.5f;
+    x1 = x0 + 7.f;
+    y0 = (float)ry + 0.5f;
+    y1 = y0 + (float)(kH - 1);
+  }
 };
-
-__device__ __forceinline__ Quad quad_of(int tile_x, int tile_y) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  Quad q;
-  const int qx = tile_x * BS_TILE + (w & 1) * 8, qy = tile_y * BS_TILE + (w >> 1) * 8;
-  q.px = qx + (lane & 7);
-  q.py0 = qy + 2 * (lane >> 3);
-  q.x0 = (float)qx + 0.5f;
-  q.x1 = q.x0 + 7.f;
-  q.y0 = (float)qy + 0.5f;
-  q.y1 = q.y0 + 7.f;
-  return q;
-}
 
 struct PixelFwd {
   float T, c0, c1, c2;
@@ -142,31 +143,36 @@ __device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float
   p.contrib = rel + 1;
 }
 
-__global__ void __launch_bounds__(kThreads) raster_fwd_kernel(RastArgs a, const float* __restrict__ sp,
-                                                              const uint32_t* __restrict__ inst_rows,
-                                                              const int2* __restrict__ ranges,
-                                                              float* __restrict__ image, float* __restrict__ final_T,
-                                                              int32_t* __restrict__ n_contrib,
-                                                              const uint8_t* __restrict__ gt,
-                                                              const int32_t* __restrict__ gt_view,
-                                                              float* __restrict__ loss_tiles) {
-  __shared__ WarpSmem smem[kWarps];
-  __shared__ float s_red[kWarps];
+template <int PPL>
+__device__ __forceinline__ bool all_done(const PixelFwd (&p)[PPL]) {
+  bool d = true;
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) d = d && p[k].done;
+  return d;
+}
+
+template <int PPL>
+__global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
+    RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
+    float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
+    const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view, float* __restrict__ loss_tiles) {
+  constexpr int kW = Region<PPL>::kWarps;
+  __shared__ WarpSmem smem[kW];
+  __shared__ float s_red[kW];
   const int slot = blockIdx.z;
   const int tile = blockIdx.y * a.tiles_x + blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem& s = smem[w];
-  const Quad q = quad_of(blockIdx.x, blockIdx.y);
+  const Region<PPL> q(blockIdx.x, blockIdx.y);
   const float pxf = (float)q.px + 0.5f;
-  const float pyf0 = (float)q.py0 + 0.5f, pyf1 = (float)q.py0 + 1.5f;
-  const bool in_x = q.px < a.W;
-  const bool in0 = in_x && q.py0 < a.H, in1 = in_x && q.py0 + 1 < a.H;
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
-  PixelFwd p0{1.f, 0.f, 0.f, 0.f, 0, !in0}, p1{1.f, 0.f, 0.f, 0.f, 0, !in1};
+  PixelFwd p[PPL];
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) p[k] = PixelFwd{1.f, 0.f, 0.f, 0.f, 0, !(q.px < a.W && q.py0 + k < a.H)};
   Splat f;
   fetch_splat(f, sp, inst_rows, rg.x + lane, rg.x + lane < rg.y);
   for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
-    if (__all_sync(0xffffffffu, p0.done && p1.done)) break;
+    if (__all_sync(0xffffffffu, all_done<PPL>(p))) break;
     const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
     if (keep) stage(s, lane, f);
@@ -179,23 +185,23 @@ __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(RastArgs a, const 
       const float4 sb = s.b[j];
       const float cb = s.c[j];
       const int rel = b0 + j - rg.x;
-      if (!p0.done) blend(p0, sa, sb, cb, pxf, pyf0, rel);
-      if (!p1.done) blend(p1, sa, sb, cb, pxf, pyf1, rel);
+#pragma unroll
+      for (int k = 0; k < PPL; ++k)
+        if (!p[k].done) blend(p[k], sa, sb, cb, pxf, (float)(q.py0 + k) + 0.5f, rel);
     }
     __syncwarp();
   }
   float l = 0.f;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const PixelFwd& p = k ? p1 : p0;
-    if (!(k ? in1 : in0)) continue;
+  for (int k = 0; k < PPL; ++k) {
+    if (!(q.px < a.W && q.py0 + k < a.H)) continue;
     const int64_t pix = ((int64_t)slot * a.H + q.py0 + k) * a.W + q.px;
-    const float o0 = p.c0 + p.T * a.bg[0], o1 = p.c1 + p.T * a.bg[1], o2 = p.c2 + p.T * a.bg[2];
+    const float o0 = p[k].c0 + p[k].T * a.bg[0], o1 = p[k].c1 + p[k].T * a.bg[1], o2 = p[k].c2 + p[k].T * a.bg[2];
     image[3 * pix] = o0;
     image[3 * pix + 1] = o1;
     image[3 * pix + 2] = o2;
-    final_T[pix] = p.T;
-    n_contrib[pix] = p.contrib;
+    final_T[pix] = p[k].T;
+    n_contrib[pix] = p[k].contrib;
     if (a.loss_fused) {
       const int gv = gt_view ? gt_view[slot] : slot;
       const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + q.py0 + k) * a.W + q.px);
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(RastArgs a, const 
     __syncthreads();
     if (threadIdx.x == 0) {
       float t = 0.f;
-      for (int k = 0; k < kWarps; ++k) t += s_red[k];
+      for (int k = 0; k < kW; ++k) t += s_red[k];
       loss_tiles[(int64_t)slot * a.tiles_per_slot + tile] = t;
     }
   }
@@ -335,28 +341,31 @@ __device__ __forceinline__ void init_pixel_bwd(PixelBwd& q, const RastArgs& a, i
   q.acc0 = q.acc1 = q.acc2 = q.last_alpha = q.lc0 = q.lc1 = q.lc2 = 0.f;
 }
 
-__global__ void __launch_bounds__(kThreads, 6) raster_bwd_kernel(
+template <int PPL>
+__global__ void __launch_bounds__(Region<PPL>::kThreads, 768 / Region<PPL>::kThreads) raster_bwd_kernel(
     RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
     const float* __restrict__ image, const float* __restrict__ final_T, const int32_t* __restrict__ n_contrib,
     const float* __restrict__ grad_image, const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view,
     float* __restrict__ g_sp) {
-  __shared__ WarpSmem smem[kWarps];
+  constexpr int kW = Region<PPL>::kWarps;
+  __shared__ WarpSmem smem[kW];
   const int slot = blockIdx.z;
   const int tile = blockIdx.y * a.tiles_x + blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem& s = smem[w];
-  const Quad q = quad_of(blockIdx.x, blockIdx.y);
+  const Region<PPL> q(blockIdx.x, blockIdx.y);
   const float pxf = (float)q.px + 0.5f;
-  const float pyf0 = (float)q.py0 + 0.5f, pyf1 = (float)q.py0 + 1.5f;
-  const bool in_x = q.px < a.W;
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
-  PixelBwd p0, p1;
-  init_pixel_bwd(p0, a, slot, q.px, q.py0, in_x && q.py0 < a.H, image, final_T, n_contrib, grad_image, gt, gt_view);
-  init_pixel_bwd(p1, a, slot, q.px, q.py0 + 1, in_x && q.py0 + 1 < a.H, image, final_T, n_contrib, grad_image, gt,
-                 gt_view);
-  int warp_n = max(p0.n, p1.n);  // deepest contributor of this warp's pixels
+  PixelBwd p[PPL];
+  int warp_n = 0;
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) {
+    init_pixel_bwd(p[k], a, slot, q.px, q.py0 + k, q.px < a.W && q.py0 + k < a.H, image, final_T, n_contrib,
+                   grad_image, gt, gt_view);
+    warp_n = max(warp_n, p[k].n);
+  }
   for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
-  const int end = rg.x + warp_n;
+  const int end = rg.x + warp_n;  // deepest contributor of this warp's pixels
   Splat f;
   fetch_splat(f, sp, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
   // chunks back to front; within a chunk lane j holds instance cend - 1 - j
@@ -377,8 +386,9 @@ __global__ void __launch_bounds__(kThreads, 6) raster_bwd_kernel(
       const float4 sb = s.b[j];
       const float cb = s.c[j];
       bool any = false;
-      if (rel < p0.n) any |= pixel_grad(p0, sa, sb, cb, pxf, pyf0, g);
-      if (rel < p1.n) any |= pixel_grad(p1, sa, sb, cb, pxf, pyf1, g);
+#pragma unroll
+      for (int k = 0; k < PPL; ++k)
+        if (rel < p[k].n) any |= pixel_grad(p[k], sa, sb, cb, pxf, (float)(q.py0 + k) + 0.5f, g);
       if (__any_sync(0xffffffffu, any)) {
         int idx;
         const float r = warp_reduce9(g, idx);
@@ -468,9 +478,14 @@ extern "C" int32_t bs_raster_fwd(const bs_raster_desc* d, const float* sp_rows, 
   if (st) return st;
   BS_REQUIRE(!a.loss_fused || (gt && loss_tiles), BS_ERR_PARAMETER, "fused loss needs gt and loss_tiles");
   const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
-  raster_fwd_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(a, sp_rows, inst_rows,
-                                                              reinterpret_cast<const int2*>(ranges), image, final_T,
-                                                              n_contrib, gt, gt_slot_view, loss_tiles);
+  if (d->pixels_per_lane == 1)
+    raster_fwd_kernel<1><<<grid, Region<1>::kThreads, 0, as_stream(stream)>>>(
+        a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image, final_T, n_contrib, gt, gt_slot_view,
+        loss_tiles);
+  else
+    raster_fwd_kernel<2><<<grid, Region<2>::kThreads, 0, as_stream(stream)>>>(
+        a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image, final_T, n_contrib, gt, gt_slot_view,
+        loss_tiles);
   BS_LAUNCH_CHECK("raster_fwd_kernel");
   return BS_OK;
 }
@@ -484,9 +499,14 @@ extern "C" int32_t bs_raster_bwd(const bs_raster_desc* d, const float* sp_rows, 
   if (st) return st;
   BS_REQUIRE(grad_image || (image && gt), BS_ERR_PARAMETER, "raster_bwd needs grad_image or (image, gt)");
   const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
-  raster_bwd_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(a, sp_rows, inst_rows,
-                                                              reinterpret_cast<const int2*>(ranges), image, final_T,
-                                                              n_contrib, grad_image, gt, gt_slot_view, g_sp);
+  if (d->pixels_per_lane == 1)
+    raster_bwd_kernel<1><<<grid, Region<1>::kThreads, 0, as_stream(stream)>>>(
+        a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image, final_T, n_contrib, grad_image, gt,
+        gt_slot_view, g_sp);
+  else
+    raster_bwd_kernel<2><<<grid, Region<2>::kThreads, 0, as_stream(stream)>>>(
+        a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image, final_T, n_contrib, grad_image, gt,
+        gt_slot_view, g_sp);
   BS_LAUNCH_CHECK("raster_bwd_kernel");
   return BS_OK;
 }

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -130,6 +131,8 @@ class SplatTrainer:
         self.last = {}
         self.binning = "bucket"  # or "radix" (identical lists, see csrc/bin_tiles.cu)
         self.sort_cap = 4096     # bucket sizes sorted in shared memory
+        # raster work split: pixels per lane (2 -> 8x8 region per warp, 1 -> 8x4)
+        self.pixels_per_lane = int(os.environ.get("BS_RASTER_PPL", "2"))
 
     # ------------------------------------------------------------------ utils
     def _t(self, name):
@@ -245,7 +248,9 @@ class SplatTrainer:
         ranges = self.buf.get("ranges", nb * 2, torch.int32)
         cursor = self.buf.get("cursor", nb, torch.int32)
         stats = self.buf.get("bin_stats", 2, torch.int64)
-        nat.call("bs_bin_tiles_offsets", nat.ptr(counts), nb, nat.ptr(ranges), nat.ptr(cursor), nat.ptr(stats), st)
+        ows = self.buf.get("offsets_ws", lib.bs_bin_tiles_offsets_workspace(nb), torch.uint8)
+        nat.call("bs_bin_tiles_offsets", nat.ptr(counts), nb, nat.ptr(ranges), nat.ptr(cursor), nat.ptr(stats),
+                 nat.ptr(ows), ows.numel(), st)
         n_inst, biggest = (int(x) for x in stats.cpu().tolist())  # sync 2: sizes the instance buffers
         keys = self.buf.get("inst_keys", max(n_inst, 1), torch.int64)
         irows = self.buf.get("irows", max(n_inst, 1), torch.int32)
@@ -313,7 +318,8 @@ class SplatTrainer:
         final_T = self.buf.get("final_T", n_slots * npx, torch.float32)
         n_contrib = self.buf.get("n_contrib", n_slots * npx, torch.int32)
         loss_tiles = self.buf.get("loss_tiles", n_slots * self.tiles, torch.float32)
-        rdesc = nat.RasterDesc(n_slots, self.tiles, self.W, self.H, (ctypes.c_float * 3)(*self.bg), 1)
+        rdesc = nat.RasterDesc(n_slots, self.tiles, self.W, self.H, (ctypes.c_float * 3)(*self.bg), 1,
+                               self.pixels_per_lane)
         if gt_batch is not None:
             gt, gt_map = gt_batch, None
         else:
