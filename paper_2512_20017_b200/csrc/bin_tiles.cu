@@ -151,17 +151,75 @@ __global__ void scatter_tiles_kernel(BinGeom g, int32_t* __restrict__ cursor, ui
   }
 }
 
-// Small buckets (n <= kWarpCap): one warp per bucket, bitonic network over
-// the padded power of two in warp-private shared memory, every lane owning
-// whole compare-exchange pairs (no idle half, only __syncwarp).
+// Small buckets (n <= kWarpCap): one warp per bucket, bitonic network held
+// entirely in registers.  Lane l owns elements [l*E, l*E + E) of the padded
+// power of two M = 32*E; partners closer than E are exchanged inside the
+// lane, farther ones with __shfl_xor (same register slot, lane ^ j/E).  The
+// network is fully unrolled per E, so there is no shared memory traffic and
+// no dependent-load chain.
 constexpr int kWarpCap = 1024;
 constexpr int kSortWarpsPerCta = 8;
+
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, m);
+  const uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(v >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+template <int E>
+__device__ __forceinline__ void warp_bitonic(uint64_t (&x)[E], int lane) {
+  constexpr int M = 32 * E;
+#pragma unroll
+  for (int k = 2; k <= M; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+        const int lj = j / E;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const bool asc = ((lane * E + e) & k) == 0;
+          const uint64_t o = shfl_xor_u64(x[e], lj);
+          const bool take_min = lower == asc;
+          x[e] = (take_min == (o < x[e])) ? o : x[e];
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if ((e & j) == 0) {
+            const bool asc = ((lane * E + e) & k) == 0;
+            const uint64_t a = x[e], b = x[e | j];
+            const bool sw = asc ? (a > b) : (a < b);
+            x[e] = sw ? b : a;
+            x[e | j] = sw ? a : b;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void sort_bucket_regs(const uint64_t* __restrict__ keys, int start, int n,
+                                                 uint32_t* __restrict__ rows, int lane) {
+  uint64_t x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane * E + e;
+    x[e] = i < n ? keys[start + i] : ~0ull;
+  }
+  warp_bitonic<E>(x, lane);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane * E + e;
+    if (i < n) rows[start + i] = (uint32_t)x[e];
+  }
+}
 
 __global__ void __launch_bounds__(32 * kSortWarpsPerCta) sort_tiles_warp_kernel(const uint64_t* __restrict__ keys,
                                                                                  const int2* __restrict__ ranges,
                                                                                  int nb, int cap,
                                                                                  uint32_t* __restrict__ rows) {
-  extern __shared__ uint64_t s_all[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * kSortWarpsPerCta + w;
   if (b >= nb) return;
@@ -172,27 +230,12 @@ __global__ void __launch_bounds__(32 * kSortWarpsPerCta) sort_tiles_warp_kernel(
     if (lane == 0) rows[rg.x] = (uint32_t)keys[rg.x];
     return;
   }
-  uint64_t* s = s_all + w * kWarpCap;
-  int m = 2;
-  while (m < n) m <<= 1;
-  for (int i = lane; i < m; i += 32) s[i] = i < n ? keys[rg.x + i] : ~0ull;
-  __syncwarp();
-  const int half = m >> 1;
-  for (int k = 2; k <= m; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int p = lane; p < half; p += 32) {
-        const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));  // bit log2(j) of i is 0
-        const int ixj = i | j;
-        const uint64_t a = s[i], c = s[ixj];
-        if ((a > c) == ((i & k) == 0)) {
-          s[i] = c;
-          s[ixj] = a;
-        }
-      }
-      __syncwarp();
-    }
-  }
-  for (int i = lane; i < n; i += 32) rows[rg.x + i] = (uint32_t)s[i];
+  if (n <= 32) sort_bucket_regs<1>(keys, rg.x, n, rows, lane);
+  else if (n <= 64) sort_bucket_regs<2>(keys, rg.x, n, rows, lane);
+  else if (n <= 128) sort_bucket_regs<4>(keys, rg.x, n, rows, lane);
+  else if (n <= 256) sort_bucket_regs<8>(keys, rg.x, n, rows, lane);
+  else if (n <= 512) sort_bucket_regs<16>(keys, rg.x, n, rows, lane);
+  else sort_bucket_regs<32>(keys, rg.x, n, rows, lane);
 }
 
 // Buckets with kWarpCap < n <= cap: one CTA each.
@@ -298,9 +341,7 @@ extern "C" int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* r
              kSortCap);
   if (n_buckets == 0) return BS_OK;
   cudaStream_t s = as_stream(stream);
-  const size_t wsmem = sizeof(uint64_t) * kWarpCap * kSortWarpsPerCta;
-  cudaFuncSetAttribute(sort_tiles_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
-  sort_tiles_warp_kernel<<<(n_buckets + kSortWarpsPerCta - 1) / kSortWarpsPerCta, 32 * kSortWarpsPerCta, wsmem, s>>>(
+  sort_tiles_warp_kernel<<<(n_buckets + kSortWarpsPerCta - 1) / kSortWarpsPerCta, 32 * kSortWarpsPerCta, 0, s>>>(
       inst_keys, reinterpret_cast<const int2*>(ranges), n_buckets, smem_cap, inst_rows);
   BS_LAUNCH_CHECK("sort_tiles_warp_kernel");
   if (smem_cap > kWarpCap) {

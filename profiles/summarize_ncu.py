@@ -64,7 +64,7 @@ def full(path: str) -> dict:
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1.0, "usecond": 1e3,
-             "msecond": 1e6, "second": 1e9}
+             "msecond": 1e6, "second": 1e9, "ns": 1.0, "us": 1e3, "ms": 1e6, "s": 1e9}
     out = {}
     for r in rows[2:]:
         name = _short(r[hdr.index("Kernel Name")])
