@@ -133,6 +133,68 @@ def schedule(n_views, batch, steps, seed=9):
     return out[:steps]
 
 
+def weak_scaled(cfg, world):
+    """N ranks: N aerial cells side by side (grid (1, N)), N x the points,
+    views and batch -- per-rank work fixed (weak scaling)."""
+    c = dict(cfg)
+    rows, cols = cfg["grid"]
+    c.update(n_points=cfg["n_points"] * world, grid=(rows, cols * world), n_views=cfg["n_views"] * world,
+             desc=cfg["desc"] + f" per rank, x{world} ranks (grid {rows}x{cols * world})")
+    return c
+
+
+def shard_for_rank(ds, g, params, world, rank):
+    """Points-to-rank map of the paper's offline placement: GPU-built
+    bipartite visibility graph -> hierarchical_partition(graph, N, 1)
+    (deterministic, identical on every rank); returns this rank's shard."""
+    from paper_2512_20017_b200.sharding import build_bipartite_graph, hierarchical_partition
+
+    t0 = time.time()
+    graph = build_bipartite_graph(g, ds)
+    t1 = time.time()
+    part = hierarchical_partition(graph, world, 1, eps=0.05, seed=5)
+    t2 = time.time()
+    owner = part.flat_gpus()
+    mine = np.flatnonzero(owner == rank)
+    sizes = np.array([g.groups[k].size for k in mine], dtype=np.int64)
+    pts = np.concatenate([np.arange(g.groups[k].begin, g.groups[k].end) for k in mine])
+    gb = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    aabb = g.aabbs.reshape(-1, 6)[mine]
+    info = {"groups": int(g.n_groups), "graph_edges": int(len(graph.edge_weights)),
+            "graph_build_s": round(t1 - t0, 2), "partition_s": round(t2 - t1, 2),
+            "points_per_rank": [int(x) for x in part.per_gpu_weights()], "owner": owner}
+    return np.ascontiguousarray(params[:, pts, :]), gb, aabb, info
+
+
+def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps):
+    """All-to-all bytes per step: moved by NCCL (summed over ranks),
+    A-predicted (account_iteration on topology (N, 1)), and the same
+    accounting for the RandomStrategy baseline on the same batches."""
+    import torch
+
+    from paper_2512_20017_b200.accounting import (ClusterTopology, account_iteration, random_placement,
+                                                  random_point_gpus)
+    from paper_2512_20017_b200.culling import build_access_matrix
+
+    t = torch.tensor([comm.bytes_fwd, comm.bytes_bwd], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t)
+    fwd, bwd = (float(x) / steps for x in t.tolist())
+    topo = ClusterTopology(world, 1, 25e9, 300e9)
+    pred = np.mean([account_iteration(A, __import__("paper_2512_20017_b200").PlacementSolution(W, world), topo, 48)
+                    .send_inter.sum() for A, W in step_AW]) * 48
+    rnd_pg = random_point_gpus(len(ds.cloud), world,
+                               np.random.default_rng(np.random.SeedSequence([5, 17])))[g.permutation]
+    rnd = []
+    for it, b in enumerate(batches):
+        A = build_access_matrix(g, rnd_pg, [ds.views[v] for v in b], 1)
+        sol = random_placement(len(b), world, np.random.default_rng(np.random.SeedSequence([5, 3, it])))
+        rnd.append(account_iteration(A, sol, topo, 48).send_inter.sum() * 48)
+    rnd = float(np.mean(rnd))
+    return {"fwd_bytes_per_step": fwd, "bwd_bytes_per_step": bwd, "fwd_bytes_predicted": float(pred),
+            "random_fwd_bytes_per_step": rnd, "reduction_vs_random_pct": 100.0 * (1.0 - fwd / rnd) if rnd else None,
+            "row_bytes": {"fwd": 48, "bwd": 36}}
+
+
 def kernel_bytes(stage, last, S, B):
     """Algorithmic (compulsory) bytes of one launch of a stage."""
     I, V, slots = last["n_inst"], last["n_rows"], last["n_slots"]
@@ -161,17 +223,25 @@ def run_ours(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    comm, part_info = None, {}
     if world > 1:
         import torch.distributed as dist
 
+        from paper_2512_20017_b200.exchange import SplatExchange
+
         dist.init_process_group("nccl")
+        cfg = weak_scaled(cfg, world)
     t0 = time.time()
     ds, g, params, gt = build_scene(cfg)
+    gb, aabb = g.group_begin(), g.aabbs.reshape(-1, 6)
+    if world > 1:
+        params, gb, aabb, part_info = shard_for_rank(ds, g, params, world, rank)
+        comm = SplatExchange()
     setup_s = time.time() - t0
     W, H = cfg["image_size"]
-    B = cfg["batch"]
-    tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt,
-                      adam=AdamConfig(scenes.lr_table(cfg["altitude"])))
+    B = cfg["batch"] * world
+    tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt, adam=AdamConfig(scenes.lr_table(cfg["altitude"])),
+                      comm=comm)
     sched = schedule(cfg["n_views"], B, args.warmup + 2 * args.steps + 2)
     # clocks are sampled from the start of the warm-up to the end of the timed
     # region (nvidia-smi needs ~0.5 s to start streaming)
@@ -188,11 +258,16 @@ def run_ours(args, cfg):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    step_AW = []
+    if comm is not None:
+        comm.bytes_fwd = comm.bytes_bwd = 0
     start.record()
     for i in range(args.steps):
         tr.step(sched[args.warmup + i])
         inst.append(tr.last["n_inst"])
         rows.append(tr.last["n_rows"])
+        if comm is not None:
+            step_AW.append((tr.last["A"], tr.last["W"]))
     end.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -208,8 +283,12 @@ def run_ours(args, cfg):
     stage_ms = {k: float(np.mean([s.elapsed_time(e) for s, e in v])) for k, v in tr.timers.items()}
     tr.timers = None
     ms_per_step = ms / args.steps
-    images = B * world * args.steps
+    images = B * args.steps
     value = images / (ms / 1000.0)
+    comm_report = None
+    if comm is not None:
+        comm_report = comm_bytes_report(comm, step_AW, sched[args.warmup:args.warmup + args.steps], ds, g,
+                                        world, rank, args.steps)
     # ---- e2e: public API with pinned host ground truth, loss read back
     # the step's ground-truth images are copied from pinned host memory on a
     # side stream, double-buffered: step i+1's upload overlaps step i
@@ -248,7 +327,11 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     e2e_ms = e_start.elapsed_time(e_end)
     e2e_wall = (time.perf_counter() - t_e2e0) * 1000.0
-    e2e_value = B * world * len(e2e_sched) / (max(e2e_ms, e2e_wall) / 1000.0)
+    if world > 1:
+        t = torch.tensor([e2e_ms, e2e_wall], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms, e2e_wall = (float(x) for x in t.tolist())
+    e2e_value = B * len(e2e_sched) / (max(e2e_ms, e2e_wall) / 1000.0)
     # ---- roofline of the dominant kernel
     peak, peak_kind = _peaks()
     last = dict(tr.last, H=H, W=W, n_visible_points=int(tr.last.get("n_visible_points", tr.S)))
@@ -266,7 +349,7 @@ def run_ours(args, cfg):
         stages[k] = {"ms": round(v, 4), "share": round(v / ms_per_step, 4),
                      "gbs": round(nb / (v / 1000.0) / 1e9, 1) if nb else None}
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, ds, g, params, gt, steps=1)
     if rank == 0:
         line = {
@@ -274,11 +357,13 @@ def run_ours(args, cfg):
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["desc"], "n_points": cfg["n_points"], "image": list(cfg["image_size"]),
-                       "global_batch": B * world, "views": cfg["n_views"], "group_size": cfg["G"],
+                       "global_batch": B, "views": cfg["n_views"], "group_size": cfg["G"],
                        "parallelism": f"points+images x{world}",
-                       "l2": "inputs larger than L2 (params+Adam state %.0f MB)" % (3 * tr.params.numel() * 4 / 1e6)},
-            "e2e": {"value": round(e2e_value, 3), "unit": "images/s", "h2d_bytes_per_step": B * H * W * 3,
+                       "l2": "inputs larger than L2 (params+Adam state %.0f MB/rank)" % (3 * tr.params.numel() * 4 / 1e6)},
+            "e2e": {"value": round(e2e_value, 3), "unit": "images/s", "h2d_bytes_per_step": B * H * W * 3 * world,
                     "d2h_bytes_per_step": 4 * B},
+            "comm": comm_report,
+            "partition": {k: v for k, v in part_info.items() if k != "owner"} or None,
             "roofline": roof,
             "stages": stages,
             "instances_per_step": int(np.mean(inst)), "splat_rows_per_step": int(np.mean(rows)),

@@ -1,0 +1,238 @@
+// 2D Gaussian splatting (2DGS, surfel ray-splat intersection; PAPER.md:
+// 773-777, state table) -- projection, its analytic
+// backward, and the per-pixel evaluation shared by the raster kernels.
+//
+// A point is an oriented disk: centre p, tangent axes R(q)[:,0]*s_u and
+// R(q)[:,1]*s_v (s = exp(log_scale.xy)), normal R(q)[:,2].  With camera-frame
+// columns c0 = K Rcw t_u, c1 = K Rcw t_v, c2 = K Rcw (p - campos) the
+// homogeneous image of the local point (u, v) is M (u, v, 1)^T, M = [c0 c1 c2]
+// ("ray transform", stored row-major -- the KWH matrix of the state table).
+// For a pixel centre (x, y) the ray meets the disk at
+//   h_x = M_row0 - x M_row2,  h_y = M_row1 - y M_row2,  zeta = h_x x h_y,
+//   (u, v) = (zeta.x, zeta.y) / zeta.z,
+// and, with the screen-space low-pass of 2DGS (sigma_f = 1/sqrt 2 px),
+//   power = -0.5 min(u^2 + v^2, 2 |mean2d - pixel|^2).
+// mean2d = c2.xy / c2.z (projected centre); per-axis radii bound the image of
+// the 3-sigma disk u^2 + v^2 = 9 (exact bounding box of that conic from its
+// dual C* = M diag(9, 9, -1) M^T), measured from mean2d.
+//
+// Forward: explicit round-to-nearest ops (bit-identical to the CPU oracle).
+#pragma once
+#include "splat_math.cuh"
+
+namespace bs {
+
+// SP row of a 2DGS splat (24 floats, 96 B):
+//   0 u  1 v  2 opacity  3..11 M (row-major)  12 r 13 g 14 b  15 depth
+//   16 radius_x  17 radius_y  18..20 normal (camera frame)  21..23 pad
+constexpr int kSP2 = 24;
+// G_SP row of a 2DGS splat (15 floats): d u, d v, d M[9], d opacity, d rgb
+constexpr int kGSP2 = 15;
+
+struct Proj2D {
+  float d[3], qc[3], s[2], qn[4], qnorm, Rq[9], Rc[9];
+  float c0[3], c1[3], c2[3];  // M columns
+  float u, v, depth, radius_x, radius_y, normal[3];
+  float len, dir[3], Y[16], col_raw[3], col[3], opac;
+  bool valid;
+};
+
+__device__ __forceinline__ void kmul(const bs_camera& c, const float x[3], float out[3]) {
+  out[0] = fadd(fmul(c.fx, x[0]), fmul(c.cx, x[2]));
+  out[1] = fadd(fmul(c.fy, x[1]), fmul(c.cy, x[2]));
+  out[2] = x[2];
+}
+
+template <class SH>
+__device__ __forceinline__ void project2d_forward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
+                                                  Proj2D& f) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) f.d[k] = fsub(pt.p[k], c.pos[k]);
+  const float* W = c.rot_cw;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    f.qc[k] = fadd(fadd(fmul(W[3 * k], f.d[0]), fmul(W[3 * k + 1], f.d[1])), fmul(W[3 * k + 2], f.d[2]));
+  f.s[0] = det_expf(pt.ls[0]);
+  f.s[1] = det_expf(pt.ls[1]);
+  const float nn = fadd(fadd(fadd(fmul(pt.q[0], pt.q[0]), fmul(pt.q[1], pt.q[1])), fmul(pt.q[2], pt.q[2])),
+                        fmul(pt.q[3], pt.q[3]));
+  f.qnorm = fsqrt(nn);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) f.qn[k] = fdiv(pt.q[k], f.qnorm);
+  const float w = f.qn[0], x = f.qn[1], y = f.qn[2], zq = f.qn[3];
+  const float xx = fmul(x, x), yy = fmul(y, y), zz = fmul(zq, zq);
+  const float xy = fmul(x, y), xz = fmul(x, zq), yz = fmul(y, zq);
+  const float wx = fmul(w, x), wy = fmul(w, y), wz = fmul(w, zq);
+  f.Rq[0] = fsub(1.f, fmul(2.f, fadd(yy, zz)));
+  f.Rq[1] = fmul(2.f, fsub(xy, wz));
+  f.Rq[2] = fmul(2.f, fadd(xz, wy));
+  f.Rq[3] = fmul(2.f, fadd(xy, wz));
+  f.Rq[4] = fsub(1.f, fmul(2.f, fadd(xx, zz)));
+  f.Rq[5] = fmul(2.f, fsub(yz, wx));
+  f.Rq[6] = fmul(2.f, fsub(xz, wy));
+  f.Rq[7] = fmul(2.f, fadd(yz, wx));
+  f.Rq[8] = fsub(1.f, fmul(2.f, fadd(xx, yy)));
+  // Rc = Rcw Rq
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      f.Rc[3 * i + j] =
+          fadd(fadd(fmul(W[3 * i], f.Rq[j]), fmul(W[3 * i + 1], f.Rq[3 + j])), fmul(W[3 * i + 2], f.Rq[6 + j]));
+  float tu[3], tv[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    tu[i] = fmul(f.Rc[3 * i], f.s[0]);
+    tv[i] = fmul(f.Rc[3 * i + 1], f.s[1]);
+  }
+  kmul(c, tu, f.c0);
+  kmul(c, tv, f.c1);
+  kmul(c, f.qc, f.c2);
+  const float z = f.qc[2];
+  f.depth = z;
+  f.u = fdiv(f.c2[0], f.c2[2]);
+  f.v = fdiv(f.c2[1], f.c2[2]);
+  // dual conic of the 3-sigma disk: C*_ij = 9 (c0_i c0_j + c1_i c1_j) - c2_i c2_j
+  const float c22 = fsub(fmul(9.f, fadd(fmul(f.c0[2], f.c0[2]), fmul(f.c1[2], f.c1[2]))), fmul(f.c2[2], f.c2[2]));
+  const float c02 = fsub(fmul(9.f, fadd(fmul(f.c0[0], f.c0[2]), fmul(f.c1[0], f.c1[2]))), fmul(f.c2[0], f.c2[2]));
+  const float c12 = fsub(fmul(9.f, fadd(fmul(f.c0[1], f.c0[2]), fmul(f.c1[1], f.c1[2]))), fmul(f.c2[1], f.c2[2]));
+  const float c00 = fsub(fmul(9.f, fadd(fmul(f.c0[0], f.c0[0]), fmul(f.c1[0], f.c1[0]))), fmul(f.c2[0], f.c2[0]));
+  const float c11 = fsub(fmul(9.f, fadd(fmul(f.c0[1], f.c0[1]), fmul(f.c1[1], f.c1[1]))), fmul(f.c2[1], f.c2[1]));
+  f.valid = c22 < 0.f;  // the 3-sigma disk images to a bounded ellipse
+  f.radius_x = f.radius_y = 0.f;
+  if (f.valid) {
+    const float bx = fdiv(c02, c22), by = fdiv(c12, c22);
+    const float ex = fsub(fmul(bx, bx), fdiv(c00, c22));
+    const float ey = fsub(fmul(by, by), fdiv(c11, c22));
+    f.valid = ex >= 0.f && ey >= 0.f;
+    if (f.valid) {
+      f.radius_x = ceilf(fadd(fabsf(fsub(bx, f.u)), fsqrt(ex)));
+      f.radius_y = ceilf(fadd(fabsf(fsub(by, f.v)), fsqrt(ey)));
+    }
+  }
+  // camera-frame normal, oriented towards the camera
+  float n0 = f.Rc[2], n1 = f.Rc[5], n2 = f.Rc[8];
+  const float facing = fadd(fadd(fmul(n0, f.qc[0]), fmul(n1, f.qc[1])), fmul(n2, f.qc[2]));
+  if (facing > 0.f) {
+    n0 = -n0;
+    n1 = -n1;
+    n2 = -n2;
+  }
+  f.normal[0] = n0;
+  f.normal[1] = n1;
+  f.normal[2] = n2;
+  // view-dependent colour and opacity (as 3DGS)
+  f.len = fsqrt(fadd(fadd(fmul(f.d[0], f.d[0]), fmul(f.d[1], f.d[1])), fmul(f.d[2], f.d[2])));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) f.dir[k] = fdiv(f.d[k], f.len);
+  sh_basis(f.dir, n_sh, f.Y);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float acc = fmul(f.Y[0], sh(ch));
+#pragma unroll
+    for (int k = 1; k < 16; ++k)
+      if (k < n_sh) acc = fadd(acc, fmul(f.Y[k], sh(3 * k + ch)));
+    f.col_raw[ch] = fadd(acc, 0.5f);
+    f.col[ch] = fmaxf(f.col_raw[ch], 0.f);
+  }
+  f.opac = det_sigmoid(pt.op_logit);
+}
+
+__device__ __forceinline__ void write_sp2_row(float* __restrict__ row, const Proj2D& f) {
+  float4* r4 = reinterpret_cast<float4*>(row);
+  // rows of M: (c0.x c1.x c2.x) (c0.y c1.y c2.y) (c0.z c1.z c2.z)
+  r4[0] = make_float4(f.u, f.v, f.opac, f.c0[0]);
+  r4[1] = make_float4(f.c1[0], f.c2[0], f.c0[1], f.c1[1]);
+  r4[2] = make_float4(f.c2[1], f.c0[2], f.c1[2], f.c2[2]);
+  r4[3] = make_float4(f.col[0], f.col[1], f.col[2], f.depth);
+  r4[4] = make_float4(f.valid ? f.radius_x : 0.f, f.valid ? f.radius_y : 0.f, f.normal[0], f.normal[1]);
+  r4[5] = make_float4(f.normal[2], 0.f, 0.f, 0.f);
+}
+
+// Accumulate the parameter gradient of one (point, view) pair.
+// gsp = (du, dv, dM[9] row-major, dopacity, dr, dg, db).
+template <class SH, class ShAdd>
+__device__ __forceinline__ void project2d_backward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
+                                                   const Proj2D& f, const float gsp[15], float* g, ShAdd sh_add) {
+  if (!f.valid) return;
+  // ---- colour -> sh, dir (as 3DGS)
+  float dc[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) dc[ch] = f.col_raw[ch] >= 0.f ? gsp[12 + ch] : 0.f;
+  float wk[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) wk[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (k >= n_sh) break;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      sh_add(3 * k + ch, f.Y[k] * dc[ch]);
+      wk[k] += dc[ch] * sh(3 * k + ch);
+    }
+  }
+  float gdir[3];
+  sh_dir_grad(f.dir, n_sh, wk, gdir);
+  const float dd = f.dir[0] * gdir[0] + f.dir[1] * gdir[1] + f.dir[2] * gdir[2];
+  float gp[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) gp[k] = (gdir[k] - f.dir[k] * dd) / f.len;
+  // ---- opacity
+  g[3] += gsp[11] * f.opac * (1.f - f.opac);
+  // ---- M rows -> columns c0, c1, c2; mean2d = c2.xy / c2.z
+  const float* gm = gsp + 2;  // row-major 3x3
+  float gc0[3] = {gm[0], gm[3], gm[6]};
+  float gc1[3] = {gm[1], gm[4], gm[7]};
+  float gc2[3] = {gm[2], gm[5], gm[8]};
+  const float iz = 1.f / f.c2[2];
+  gc2[0] += gsp[0] * iz;
+  gc2[1] += gsp[1] * iz;
+  gc2[2] += -(gsp[0] * f.c2[0] + gsp[1] * f.c2[1]) * iz * iz;
+  // c = K x  ->  dL/dx = (fx gc.x, fy gc.y, cx gc.x + cy gc.y + gc.z)
+  auto kback = [&](const float gcv[3], float gx[3]) {
+    gx[0] = c.fx * gcv[0];
+    gx[1] = c.fy * gcv[1];
+    gx[2] = c.cx * gcv[0] + c.cy * gcv[1] + gcv[2];
+  };
+  float gtu[3], gtv[3], gq[3];
+  kback(gc0, gtu);
+  kback(gc1, gtv);
+  kback(gc2, gq);
+  // ---- q = Rcw (p - campos)
+  const float* W = c.rot_cw;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) gp[k] += W[k] * gq[0] + W[3 + k] * gq[1] + W[6 + k] * gq[2];
+  g[0] += gp[0];
+  g[1] += gp[1];
+  g[2] += gp[2];
+  // ---- tu = Rc[:,0] s_u, tv = Rc[:,1] s_v
+  float gs0 = 0.f, gs1 = 0.f;
+  float gRc[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    gs0 += f.Rc[3 * i] * gtu[i];
+    gs1 += f.Rc[3 * i + 1] * gtv[i];
+    gRc[3 * i] = gtu[i] * f.s[0];
+    gRc[3 * i + 1] = gtv[i] * f.s[1];
+    gRc[3 * i + 2] = 0.f;  // the normal column carries no loss gradient
+  }
+  g[4] += gs0 * f.s[0];
+  g[5] += gs1 * f.s[1];
+  // ---- Rc = Rcw Rq  ->  dL/dRq = Rcw^T dL/dRc
+  float G[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) G[3 * i + j] = W[i] * gRc[j] + W[3 + i] * gRc[3 + j] + W[6 + i] * gRc[6 + j];
+  const float w = f.qn[0], x = f.qn[1], y = f.qn[2], zq = f.qn[3];
+  float gqn[4];
+  gqn[0] = 2.f * (-zq * G[1] + y * G[2] + zq * G[3] - x * G[5] - y * G[6] + x * G[7]);
+  gqn[1] = 2.f * (y * G[1] + zq * G[2] + y * G[3] - 2.f * x * G[4] - w * G[5] + zq * G[6] + w * G[7] - 2.f * x * G[8]);
+  gqn[2] = 2.f * (-2.f * y * G[0] + x * G[1] + w * G[2] + x * G[3] + zq * G[5] - w * G[6] + zq * G[7] - 2.f * y * G[8]);
+  gqn[3] = 2.f * (-2.f * zq * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.f * zq * G[4] + y * G[5] + x * G[6] + y * G[7]);
+  const float dq = w * gqn[0] + x * gqn[1] + y * gqn[2] + zq * gqn[3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) g[8 + k] += (gqn[k] - f.qn[k] * dq) / f.qnorm;
+}
+
+}  // namespace bs

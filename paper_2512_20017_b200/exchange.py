@@ -81,11 +81,17 @@ class SplatExchange:
                                                                                     delta=1.0, p=4.0)
         self.bytes_fwd = 0
         self.bytes_bwd = 0
+        # gloo (CPU tests, several ranks sharing one GPU) moves host tensors only
+        self.host_staging = dist.get_backend(group) == "gloo"
+
+    def _stage(self, t: torch.Tensor) -> torch.Tensor:
+        return t.cpu() if self.host_staging else t
 
     def gather_access(self, col: torch.Tensor) -> np.ndarray:
         """All-gather C[.]_k (int64 [B]) -> A int64 [B, N] on the host."""
-        out = torch.empty(self.world * col.numel(), dtype=col.dtype, device=col.device)
-        dist.all_gather_into_tensor(out, col.contiguous(), group=self.group)
+        src = self._stage(col.contiguous())
+        out = torch.empty(self.world * col.numel(), dtype=col.dtype, device=src.device)
+        dist.all_gather_into_tensor(out, src, group=self.group)
         return out.view(self.world, -1).t().cpu().numpy().astype(np.int64)
 
     def assign(self, A: np.ndarray) -> np.ndarray:
@@ -94,10 +100,11 @@ class SplatExchange:
         return hierarchical_place(A, N, 1, self.inter, self.intra).assignment
 
     def _a2a(self, send: torch.Tensor, send_rows, recv_rows, width: int) -> torch.Tensor:
-        recv = torch.empty((int(sum(recv_rows)), width), dtype=send.dtype, device=send.device)
-        dist.all_to_all_single(recv, send.view(-1, width), output_split_sizes=list(recv_rows),
-                               input_split_sizes=list(send_rows), group=self.group)
-        return recv
+        src = self._stage(send.view(-1, width))
+        recv = torch.empty((int(sum(recv_rows)), width), dtype=send.dtype, device=src.device)
+        dist.all_to_all_single(recv, src, output_split_sizes=list(recv_rows), input_split_sizes=list(send_rows),
+                               group=self.group)
+        return recv.to(send.device) if self.host_staging else recv
 
     def forward(self, sp_send: torch.Tensor, lay: StepLayout, width: int) -> torch.Tensor:
         """Splat state rows to the ranks that render them (line 9)."""

@@ -1,0 +1,108 @@
+"""Two ranks of the full GPU training step (SplatTrainer + SplatExchange)
+sharing cuda:0 over gloo (host-staged all-to-all), against the single-rank
+step on the whole scene: every rendered view and every updated parameter
+must agree (the points-to-rank partition is the paper's offline placement,
+the image-to-rank assignment hierarchical_place on the all-gathered A)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+BATCH = [0, 2, 5, 7]
+
+
+def _setup():
+    from paper_2512_20017_b200 import scenes
+    from paper_2512_20017_b200.culling import zorder_group
+
+    ds = scenes.generate_aerial_scene(0, 20_000, (1, 2), 8, 50.0, (160, 96))
+    g = zorder_group(ds.cloud, G=256)
+    params = scenes.init_gaussians(g.sorted_cloud, 0, scenes.mean_spacing(50.0, (1, 2), 20_000))
+    gt = scenes.synthetic_gt(0, 8, 160, 96)
+    return ds, g, params, gt
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_2512_20017_b200 import scenes
+    from paper_2512_20017_b200.exchange import SplatExchange
+    from paper_2512_20017_b200.sharding import build_bipartite_graph, hierarchical_partition
+    from paper_2512_20017_b200.trainer import AdamConfig, SplatTrainer
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ds, g, params, gt = _setup()
+        part = hierarchical_partition(build_bipartite_graph(g, ds), world, 1, eps=0.05, seed=5)
+        mine = np.flatnonzero(part.flat_gpus() == rank)
+        pts = np.concatenate([np.arange(g.groups[k].begin, g.groups[k].end) for k in mine])
+        sizes = [g.groups[k].size for k in mine]
+        gb = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+        tr = SplatTrainer(np.ascontiguousarray(params[:, pts, :]), gb, g.aabbs.reshape(-1, 6)[mine], ds.views,
+                          gt=gt, adam=AdamConfig(scenes.lr_table(50.0)), comm=SplatExchange())
+        losses = tr.step(BATCH).cpu().numpy()
+        lay = tr.last["layout"]
+        n = len(lay.my_views)
+        img = tr.last["image"][: n * 96 * 160 * 3].cpu().numpy().reshape(n, 96, 160, 3)
+        q.put((rank, pts, tr.params.cpu().numpy(), [BATCH[v] for v in lay.my_views], img, losses,
+               tr.last["A"], tr.last["W"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_two_ranks_match_single_rank(cuda):
+    import torch.multiprocessing as mp
+
+    from paper_2512_20017_b200 import scenes
+    from paper_2512_20017_b200.trainer import AdamConfig, SplatTrainer
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        item = q.get(timeout=600)
+        res[item[0]] = item
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    # single rank over the whole scene
+    ds, g, params, gt = _setup()
+    lr = scenes.lr_table(50.0)
+    tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt, adam=AdamConfig(lr))
+    losses = tr.step(BATCH).cpu().numpy()
+    img_ref = tr.last["image"][: len(BATCH) * 96 * 160 * 3].cpu().numpy().reshape(len(BATCH), 96, 160, 3)
+    after_ref = tr.params.cpu().numpy()
+    A = res[0][6]
+    assert np.array_equal(A, res[1][6]) and np.array_equal(res[0][7], res[1][7])
+    assert np.array_equal(A.sum(axis=1), tr.last["rows_per_view"])  # the same visible sets
+    assert sorted(res[0][3] + res[1][3]) == sorted(BATCH)
+    for r in (0, 1):
+        for slot, v in enumerate(res[r][3]):
+            k = BATCH.index(v)
+            assert np.abs(res[r][4][slot] - img_ref[k]).max() <= 1e-6, f"view {v}"
+            assert abs(res[r][5][slot] - losses[k]) <= 1e-6
+        pts, after = res[r][1], res[r][2]
+        ref = after_ref[:, pts, :]
+        lr_full = np.broadcast_to(lr.reshape(15, 1, 4), ref.shape)
+        diff = np.abs(after - ref)
+        assert (diff <= 1e-3 * lr_full + 1e-7).mean() > 0.999
+        assert (diff <= 2.0 * lr_full + 1e-6).all()
