@@ -175,10 +175,18 @@ int32_t bs_scan_counts(const int32_t* counts, int32_t n_groups,
                        void* stream);
 
 /* ---- K1: projection (pts_splatting) ------------------------------------ */
+enum { BS_MODEL_3DGS = 0, BS_MODEL_2DGS = 1 };
+/* 2DGS splat-state row (BS_SP2_FLOATS = 24 floats, 96 B): the 20 elements of
+ * PAPER.md Table tab:states-2dgs -- 0 u 1 v 2 opacity 3..11 ray transform M
+ * (row-major KWH) 12..14 rgb 15 depth 16 radius_x 17 radius_y 18..20 normal
+ * -- + 3 pad.  G_SP row: 15 floats (d u, d v, d M[9], d opacity, d rgb). */
+#define BS_SP2_FLOATS 24
+#define BS_GSP2_FLOATS 15
 typedef struct {
   int32_t n_views;
   int32_t sh_degree; /* 0..3 */
   int32_t tiles_x_max, tiles_y_max;
+  int32_t model;     /* BS_MODEL_3DGS (default) or BS_MODEL_2DGS */
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,
@@ -229,7 +237,7 @@ int32_t bs_bin_tiles_count(const float* sp_rows, int64_t n_rows,
                            const int64_t* seg_row0, const int32_t* seg_slot,
                            int32_t n_segs, const bs_camera* slot_cams,
                            int32_t tiles_per_slot, int32_t n_buckets,
-                           int32_t* bucket_counts, void* stream);
+                           int32_t* bucket_counts, int32_t model, void* stream);
 int32_t bs_bin_tiles_offsets(const int32_t* bucket_counts, int32_t n_buckets,
                              int32_t* ranges, int32_t* cursor, int64_t* stats,
                              void* workspace, size_t ws_bytes, void* stream);
@@ -238,7 +246,7 @@ int32_t bs_bin_tiles_scatter(const float* sp_rows, int64_t n_rows,
                              const int64_t* seg_row0, const int32_t* seg_slot,
                              int32_t n_segs, const bs_camera* slot_cams,
                              int32_t tiles_per_slot, int32_t* cursor,
-                             uint64_t* inst_keys, void* stream);
+                             uint64_t* inst_keys, int32_t model, void* stream);
 int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* ranges,
                           int32_t n_buckets, int32_t smem_cap,
                           uint32_t* inst_rows, void* stream);
@@ -283,6 +291,22 @@ int32_t bs_raster_bwd(const bs_raster_desc* desc_host, const float* sp_rows,
                       const int32_t* n_contrib, const float* grad_image,
                       const uint8_t* gt, const int32_t* gt_slot_view,
                       float* g_sp, void* stream);
+
+/* 2DGS (surfel) variants: same arguments, BS_SP2_FLOATS rows in, BS_GSP2_FLOATS
+ * gradient rows out (config 3; reference: the 2DGS state of PAPER.md:1217-1226,
+ * the paper's 2DGS renderer is gsplat's and absent from /root/reference).  Pixel weight exp(-0.5 min(u^2+v^2,
+ * 2|mean2d - pixel|^2)) with (u, v) the ray-splat intersection. */
+int32_t bs_raster2d_fwd(const bs_raster_desc* desc_host, const float* sp_rows,
+                        const uint32_t* inst_rows, const int32_t* ranges,
+                        float* image, float* final_T, int32_t* n_contrib,
+                        const uint8_t* gt, const int32_t* gt_slot_view,
+                        float* loss_tiles, void* stream);
+int32_t bs_raster2d_bwd(const bs_raster_desc* desc_host, const float* sp_rows,
+                        const uint32_t* inst_rows, const int32_t* ranges,
+                        const float* image, const float* final_T,
+                        const int32_t* n_contrib, const float* grad_image,
+                        const uint8_t* gt, const int32_t* gt_slot_view,
+                        float* g_sp, void* stream);
 
 /* ---- K1b + K5 ---------------------------------------------------------- */
 /* grad_params: plane layout like params, ACCUMULATED (caller zeroes). */

@@ -45,6 +45,11 @@ def lib():
             "or_adam": (None, [P, P, P, P, I64, P, I64, F, F, F, I32]),
             "or_train_step": (D, [P, P, P, I64, P, P, I32, P, I32, P, F, F, F, I32, I32]),
             "or_plane_distances": (None, [P, I64, P, I32, P]),
+            "or_project2d": (None, [P, I64, P, I64, P, I32, P]),
+            "or_project2d_bwd": (None, [P, I64, P, I64, P, I32, P, P]),
+            "or_render2d": (I32, [P, I64, I32, I32, P, P, P, P, P, P, P]),
+            "or_render2d_bwd": (I32, [P, I64, I32, I32, P, P, P, P, P]),
+            "or_train_step_model": (D, [P, P, P, I64, P, P, I32, P, I32, P, F, F, F, I32, I32, I32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -107,28 +112,36 @@ def det_expf(x: float) -> float:
     return lib().or_det_expf(float(x))
 
 
-def project(params, idx, cam_bytes, sh_degree):
+# row widths per model: 3DGS SP 12 / G_SP 9, 2DGS SP 24 / G_SP 15 (include/splat_b200.h)
+_WIDTH = {"3dgs": (12, 9, ""), "2dgs": (24, 15, "2d")}
+
+
+def project(params, idx, cam_bytes, sh_degree, model="3dgs"):
+    spf, _, sfx = _WIDTH[model]
     prm = _c(params, np.float32)
     S = prm.shape[1]
     ix = _c(idx, np.int64)
     cam = _c(cam_bytes, np.uint8)
-    out = np.zeros((len(ix), 12), dtype=np.float32)
-    lib().or_project(_p(prm), S, _p(ix), len(ix), _p(cam), sh_degree, _p(out))
+    out = np.zeros((len(ix), spf), dtype=np.float32)
+    getattr(lib(), "or_project" + sfx)(_p(prm), S, _p(ix), len(ix), _p(cam), sh_degree, _p(out))
     return out
 
 
-def project_bwd(params, idx, cam_bytes, sh_degree, gsp, grad=None):
+def project_bwd(params, idx, cam_bytes, sh_degree, gsp, grad=None, model="3dgs"):
+    _, _, sfx = _WIDTH[model]
     prm = _c(params, np.float32)
     S = prm.shape[1]
     ix = _c(idx, np.int64)
     cam = _c(cam_bytes, np.uint8)
     g = _c(gsp, np.float32)
     out = np.zeros_like(prm) if grad is None else grad
-    lib().or_project_bwd(_p(prm), S, _p(ix), len(ix), _p(cam), sh_degree, _p(g), _p(out))
+    getattr(lib(), "or_project" + sfx + "_bwd")(_p(prm), S, _p(ix), len(ix), _p(cam), sh_degree, _p(g), _p(out))
     return out
 
 
-def render(sp, W, H, bg=(0.0, 0.0, 0.0), want_lists=False):
+def render(sp, W, H, bg=(0.0, 0.0, 0.0), want_lists=False, model="3dgs"):
+    _, _, sfx = _WIDTH[model]
+    fn = getattr(lib(), "or_render" + sfx)
     s = _c(sp, np.float32)
     bgv = _c(bg, np.float32)
     img = np.zeros((H, W, 3), dtype=np.float32)
@@ -136,23 +149,25 @@ def render(sp, W, H, bg=(0.0, 0.0, 0.0), want_lists=False):
     nc = np.zeros((H, W), dtype=np.int32)
     tx, ty = (W + 15) // 16, (H + 15) // 16
     if not want_lists:
-        lib().or_render(_p(s), len(s), W, H, _p(bgv), _p(img), _p(T), _p(nc), None, None, None)
+        fn(_p(s), len(s), W, H, _p(bgv), _p(img), _p(T), _p(nc), None, None, None)
         return img, T, nc
     n = C.c_int64(0)
     ranges = np.zeros((tx * ty, 2), dtype=np.int32)
-    lib().or_render(_p(s), len(s), W, H, _p(bgv), _p(img), _p(T), _p(nc), None, C.byref(n), None)
+    fn(_p(s), len(s), W, H, _p(bgv), _p(img), _p(T), _p(nc), None, C.byref(n), None)
     lists = np.zeros(max(n.value, 1), dtype=np.uint32)
-    rc = lib().or_render(_p(s), len(s), W, H, _p(bgv), _p(img), _p(T), _p(nc), _p(lists), C.byref(n), _p(ranges))
+    rc = fn(_p(s), len(s), W, H, _p(bgv), _p(img), _p(T), _p(nc), _p(lists), C.byref(n), _p(ranges))
     assert rc == 0
     return img, T, nc, lists[: n.value], ranges
 
 
-def render_bwd(sp, W, H, final_T, n_contrib, grad_image, bg=(0.0, 0.0, 0.0)):
+def render_bwd(sp, W, H, final_T, n_contrib, grad_image, bg=(0.0, 0.0, 0.0), model="3dgs"):
+    _, gspf, sfx = _WIDTH[model]
     s = _c(sp, np.float32)
     bgv = _c(bg, np.float32)
-    out = np.zeros((len(s), 9), dtype=np.float32)
-    lib().or_render_bwd(_p(s), len(s), W, H, _p(bgv), _p(_c(final_T, np.float32)), _p(_c(n_contrib, np.int32)),
-                        _p(_c(grad_image, np.float32)), _p(out))
+    out = np.zeros((len(s), gspf), dtype=np.float32)
+    getattr(lib(), "or_render" + sfx + "_bwd")(_p(s), len(s), W, H, _p(bgv), _p(_c(final_T, np.float32)),
+                                               _p(_c(n_contrib, np.int32)), _p(_c(grad_image, np.float32)),
+                                               _p(out))
     return out
 
 
@@ -170,13 +185,15 @@ def adam(params, grads, m, v, lr60, beta1, beta2, eps, step):
                   beta1, beta2, eps, step)
 
 
-def train_step(params, m, v, planes, cam_bytes, gt, sh_degree, lr60, beta1, beta2, eps, step, threads=0):
+def train_step(params, m, v, planes, cam_bytes, gt, sh_degree, lr60, beta1, beta2, eps, step, threads=0,
+               model="3dgs"):
     """In-place CPU training step over len(cam_bytes) views; returns summed loss."""
     S = params.shape[1]
     B = len(cam_bytes)
-    return lib().or_train_step(_p(params), _p(m), _p(v), S, _p(_c(planes, np.float64)),
-                               _p(_c(cam_bytes, np.uint8)), B, _p(_c(gt, np.uint8)), sh_degree,
-                               _p(_c(lr60, np.float32)), beta1, beta2, eps, step, threads)
+    return lib().or_train_step_model(_p(params), _p(m), _p(v), S, _p(_c(planes, np.float64)),
+                                     _p(_c(cam_bytes, np.uint8)), B, _p(_c(gt, np.uint8)), sh_degree,
+                                     _p(_c(lr60, np.float32)), beta1, beta2, eps, step, threads,
+                                     1 if model == "2dgs" else 0)
 
 
 def zorder_layout(positions, G):

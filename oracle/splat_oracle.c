@@ -505,8 +505,8 @@ static int inst_cmp(const void* pa, const void* pb) {
 }
 
 /* tiles whose span meets [u - r, u + r] (same f32 ops as csrc/bin.cu) */
-static int tile_rect(const float* row, int W, int H, int* x0, int* x1, int* y0, int* y1) {
-  const float u = row[0], v = row[1], rx = row[10], ry = row[11];
+static int tile_rect_at(const float* row, int rad, int W, int H, int* x0, int* x1, int* y0, int* y1) {
+  const float u = row[0], v = row[1], rx = row[rad], ry = row[rad + 1];
   if (!(rx > 0.f) || !(ry > 0.f)) return 0;
   const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
   *x0 = (int)fminf(fmaxf(floorf((u - rx) * 0.0625f), 0.f), (float)tx);
@@ -517,18 +517,25 @@ static int tile_rect(const float* row, int W, int H, int* x0, int* x1, int* y0, 
   return (*x1 - *x0) * (*y1 - *y0);
 }
 
-static oinst* bin_view(const float* sp, int64_t m, int W, int H, int64_t* n_out, int32_t* ranges) {
+/* row geometry: 3DGS rows {12 floats, radii at 10, depth at 9}, 2DGS {24, 16, 15} */
+typedef struct {
+  int stride, rad, depth;
+} olayout;
+static const olayout LAY3 = {SPF, 10, 9};
+static const olayout LAY2 = {24, 16, 15};
+
+static oinst* bin_view_l(const float* sp, int64_t m, int W, int H, olayout L, int64_t* n_out, int32_t* ranges) {
   const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
   int64_t total = 0;
   int x0, x1, y0, y1;
-  for (int64_t k = 0; k < m; ++k) total += tile_rect(sp + k * SPF, W, H, &x0, &x1, &y0, &y1);
+  for (int64_t k = 0; k < m; ++k) total += tile_rect_at(sp + k * L.stride, L.rad, W, H, &x0, &x1, &y0, &y1);
   oinst* inst = (oinst*)malloc(sizeof(oinst) * (size_t)(total > 0 ? total : 1));
   int64_t o = 0;
   for (int64_t k = 0; k < m; ++k) {
-    const float* r = sp + k * SPF;
-    if (!tile_rect(r, W, H, &x0, &x1, &y0, &y1)) continue;
+    const float* r = sp + k * L.stride;
+    if (!tile_rect_at(r, L.rad, W, H, &x0, &x1, &y0, &y1)) continue;
     fbits db;
-    db.f = r[9];
+    db.f = r[L.depth];
     for (int y = y0; y < y1; ++y)
       for (int x = x0; x < x1; ++x) {
         inst[o].tile = (uint32_t)(y * tx + x);
@@ -546,6 +553,10 @@ static oinst* bin_view(const float* sp, int64_t m, int W, int H, int64_t* n_out,
   }
   *n_out = total;
   return inst;
+}
+
+static oinst* bin_view(const float* sp, int64_t m, int W, int H, int64_t* n_out, int32_t* ranges) {
+  return bin_view_l(sp, m, W, H, LAY3, n_out, ranges);
 }
 
 static float splat_power(const float* r, float px, float py, float* dx, float* dy) {
@@ -696,6 +707,411 @@ void or_adam(float* p, const float* g, float* m, float* v, int64_t n, const floa
 double or_train_step(float* params, float* exp_avg, float* exp_avg_sq, int64_t S, const double* planes,
                      const or_camera* cams, int32_t B, const uint8_t* gt, int32_t sh_degree, const float* lr60,
                      float beta1, float beta2, float eps, int32_t step, int32_t n_threads) {
+  return or_train_step_model(params, exp_avg, exp_avg_sq, S, planes, cams, B, gt, sh_degree, lr60, beta1, beta2, eps,
+                             step, n_threads, 0);
+}
+
+/* ------------------------------------------------------------------------ */
+/* 2DGS (surfel) variant: PAPER.md:773-777 and the 20-element state of       */
+/* PAPER.md:1217-1226.  Rows: SP2F = 24 floats                               */
+/*   u v opac M[9] (row-major ray transform) r g b depth rx ry normal[3] pad  */
+/* and G_SP2F = 15 floats (du dv dM[9] dopac dr dg db).  The paper's 2DGS    */
+/* kernels (gsplat) are not in /root/reference: parity for this half is      */
+/* pinned by the float64 autograd restatement in tests/test_oracle_2d.py.    */
+
+#define SP2F 24
+#define GSP2F 15
+
+typedef struct {
+  float d[3], qc[3], s[2], qn[4], qnorm, Rq[9], Rc[9];
+  float c0[3], c1[3], c2[3];
+  float u, v, depth, radius_x, radius_y, normal[3];
+  float len, dir[3], Y[16], col_raw[3], col[3], opac;
+  int valid;
+} oproj2;
+
+/* homogeneous image of a camera-frame vector: K x (no division) */
+static void kapply(const or_camera* c, const float* x, float* out) {
+  out[0] = c->fx * x[0] + c->cx * x[2];
+  out[1] = c->fy * x[1] + c->cy * x[2];
+  out[2] = x[2];
+}
+
+static void quat_rot(const float* qn, float* R) {
+  const float w = qn[0], x = qn[1], y = qn[2], z = qn[3];
+  const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, xz = x * z, yz = y * z;
+  const float wx = w * x, wy = w * y, wz = w * z;
+  R[0] = 1.f - 2.f * (yy + zz);
+  R[1] = 2.f * (xy - wz);
+  R[2] = 2.f * (xz + wy);
+  R[3] = 2.f * (xy + wz);
+  R[4] = 1.f - 2.f * (xx + zz);
+  R[5] = 2.f * (yz - wx);
+  R[6] = 2.f * (xz - wy);
+  R[7] = 2.f * (yz + wx);
+  R[8] = 1.f - 2.f * (xx + yy);
+}
+
+static void proj2_fwd(const opoint* pt, const or_camera* c, int n_sh, oproj2* f) {
+  const float* W = c->rot_cw;
+  for (int k = 0; k < 3; ++k) f->d[k] = pt->p[k] - c->pos[k];
+  for (int k = 0; k < 3; ++k) f->qc[k] = (W[3 * k] * f->d[0] + W[3 * k + 1] * f->d[1]) + W[3 * k + 2] * f->d[2];
+  f->s[0] = or_det_expf(pt->ls[0]);
+  f->s[1] = or_det_expf(pt->ls[1]);
+  const float nn = ((pt->q[0] * pt->q[0] + pt->q[1] * pt->q[1]) + pt->q[2] * pt->q[2]) + pt->q[3] * pt->q[3];
+  f->qnorm = sqrtf(nn);
+  for (int k = 0; k < 4; ++k) f->qn[k] = pt->q[k] / f->qnorm;
+  quat_rot(f->qn, f->Rq);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      f->Rc[3 * i + j] = (W[3 * i] * f->Rq[j] + W[3 * i + 1] * f->Rq[3 + j]) + W[3 * i + 2] * f->Rq[6 + j];
+  float tu[3], tv[3];
+  for (int i = 0; i < 3; ++i) {
+    tu[i] = f->Rc[3 * i] * f->s[0];
+    tv[i] = f->Rc[3 * i + 1] * f->s[1];
+  }
+  kapply(c, tu, f->c0);
+  kapply(c, tv, f->c1);
+  kapply(c, f->qc, f->c2);
+  f->depth = f->qc[2];
+  f->u = f->c2[0] / f->c2[2];
+  f->v = f->c2[1] / f->c2[2];
+  /* bounding box of the image of the disk u^2 + v^2 <= 9 (dual conic) */
+  const float* a = f->c0;
+  const float* b = f->c1;
+  const float* e = f->c2;
+  const float d22 = 9.f * (a[2] * a[2] + b[2] * b[2]) - e[2] * e[2];
+  const float d02 = 9.f * (a[0] * a[2] + b[0] * b[2]) - e[0] * e[2];
+  const float d12 = 9.f * (a[1] * a[2] + b[1] * b[2]) - e[1] * e[2];
+  const float d00 = 9.f * (a[0] * a[0] + b[0] * b[0]) - e[0] * e[0];
+  const float d11 = 9.f * (a[1] * a[1] + b[1] * b[1]) - e[1] * e[1];
+  f->valid = d22 < 0.f;
+  f->radius_x = f->radius_y = 0.f;
+  if (f->valid) {
+    const float bx = d02 / d22, by = d12 / d22;
+    const float ex = bx * bx - d00 / d22, ey = by * by - d11 / d22;
+    f->valid = ex >= 0.f && ey >= 0.f;
+    if (f->valid) {
+      f->radius_x = ceilf(fabsf(bx - f->u) + sqrtf(ex));
+      f->radius_y = ceilf(fabsf(by - f->v) + sqrtf(ey));
+    }
+  }
+  float n[3] = {f->Rc[2], f->Rc[5], f->Rc[8]};
+  const float facing = (n[0] * f->qc[0] + n[1] * f->qc[1]) + n[2] * f->qc[2];
+  for (int k = 0; k < 3; ++k) f->normal[k] = facing > 0.f ? -n[k] : n[k];
+  f->len = sqrtf((f->d[0] * f->d[0] + f->d[1] * f->d[1]) + f->d[2] * f->d[2]);
+  for (int k = 0; k < 3; ++k) f->dir[k] = f->d[k] / f->len;
+  sh_basis(f->dir, n_sh, f->Y);
+  for (int ch = 0; ch < 3; ++ch) {
+    float acc = f->Y[0] * pt->sh[ch];
+    for (int k = 1; k < n_sh; ++k) acc = acc + f->Y[k] * pt->sh[3 * k + ch];
+    f->col_raw[ch] = acc + 0.5f;
+    f->col[ch] = fmaxf(f->col_raw[ch], 0.f);
+  }
+  f->opac = 1.f / (1.f + or_det_expf(-pt->op));
+}
+
+void or_project2d(const float* params, int64_t S, const int64_t* idx, int64_t m, const or_camera* c,
+                  int32_t sh_degree, float* sp) {
+  const int n_sh = (sh_degree + 1) * (sh_degree + 1);
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < m; ++k) {
+    opoint pt;
+    oproj2 f;
+    load_opoint(params, S, idx[k], &pt);
+    proj2_fwd(&pt, c, n_sh, &f);
+    float* r = sp + k * SP2F;
+    r[0] = f.u;
+    r[1] = f.v;
+    r[2] = f.opac;
+    for (int i = 0; i < 3; ++i) {
+      r[3 + 3 * i + 0] = f.c0[i];
+      r[3 + 3 * i + 1] = f.c1[i];
+      r[3 + 3 * i + 2] = f.c2[i];
+    }
+    for (int ch = 0; ch < 3; ++ch) r[12 + ch] = f.col[ch];
+    r[15] = f.depth;
+    r[16] = f.valid ? f.radius_x : 0.f;
+    r[17] = f.valid ? f.radius_y : 0.f;
+    for (int k2 = 0; k2 < 3; ++k2) r[18 + k2] = f.normal[k2];
+    r[21] = r[22] = r[23] = 0.f;
+  }
+}
+
+/* gradient of sum_k wk[k] Y_k(dir) w.r.t. dir (same basis as sh_basis) */
+static void sh_dir_grad_o(const float* dir, int n_sh, const float* wk, float* gd) {
+  const float x = dir[0], y = dir[1], z = dir[2];
+  gd[0] = gd[1] = gd[2] = 0.f;
+  if (n_sh > 1) {
+    gd[1] -= C1 * wk[1];
+    gd[2] += C1 * wk[2];
+    gd[0] -= C1 * wk[3];
+  }
+  if (n_sh > 4) {
+    gd[0] += C2[0] * y * wk[4];
+    gd[1] += C2[0] * x * wk[4];
+    gd[1] += C2[1] * z * wk[5];
+    gd[2] += C2[1] * y * wk[5];
+    gd[0] -= 2.f * C2[2] * x * wk[6];
+    gd[1] -= 2.f * C2[2] * y * wk[6];
+    gd[2] += 4.f * C2[2] * z * wk[6];
+    gd[0] += C2[3] * z * wk[7];
+    gd[2] += C2[3] * x * wk[7];
+    gd[0] += 2.f * C2[4] * x * wk[8];
+    gd[1] -= 2.f * C2[4] * y * wk[8];
+  }
+  if (n_sh > 9) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    gd[0] += C3[0] * 6.f * x * y * wk[9];
+    gd[1] += C3[0] * 3.f * (xx - yy) * wk[9];
+    gd[0] += C3[1] * y * z * wk[10];
+    gd[1] += C3[1] * x * z * wk[10];
+    gd[2] += C3[1] * x * y * wk[10];
+    gd[0] += C3[2] * (-2.f * x * y) * wk[11];
+    gd[1] += C3[2] * (4.f * zz - xx - 3.f * yy) * wk[11];
+    gd[2] += C3[2] * (8.f * y * z) * wk[11];
+    gd[0] += C3[3] * (-6.f * x * z) * wk[12];
+    gd[1] += C3[3] * (-6.f * y * z) * wk[12];
+    gd[2] += C3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * wk[12];
+    gd[0] += C3[4] * (4.f * zz - 3.f * xx - yy) * wk[13];
+    gd[1] += C3[4] * (-2.f * x * y) * wk[13];
+    gd[2] += C3[4] * (8.f * x * z) * wk[13];
+    gd[0] += C3[5] * (2.f * x * z) * wk[14];
+    gd[1] += C3[5] * (-2.f * y * z) * wk[14];
+    gd[2] += C3[5] * (xx - yy) * wk[14];
+    gd[0] += C3[6] * 3.f * (xx - yy) * wk[15];
+    gd[1] += C3[6] * (-6.f * x * y) * wk[15];
+  }
+}
+
+static void proj2_bwd(const opoint* pt, const or_camera* c, int n_sh, const oproj2* f, const float* gsp, float* g) {
+  if (!f->valid) return;
+  float dc[3], wk[16] = {0}, gd[3];
+  for (int ch = 0; ch < 3; ++ch) dc[ch] = f->col_raw[ch] >= 0.f ? gsp[12 + ch] : 0.f;
+  for (int k = 0; k < n_sh; ++k)
+    for (int ch = 0; ch < 3; ++ch) {
+      g[12 + 3 * k + ch] += f->Y[k] * dc[ch];
+      wk[k] += dc[ch] * pt->sh[3 * k + ch];
+    }
+  sh_dir_grad_o(f->dir, n_sh, wk, gd);
+  const float dd = f->dir[0] * gd[0] + f->dir[1] * gd[1] + f->dir[2] * gd[2];
+  float gpos[3];
+  for (int k = 0; k < 3; ++k) gpos[k] = (gd[k] - f->dir[k] * dd) / f->len;
+  g[3] += gsp[11] * f->opac * (1.f - f->opac);
+  /* M = [c0 c1 c2] (columns); dL/dc_j = column j of dL/dM, plus the mean2d term on c2 */
+  float gcol[3][3];
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < 3; ++i) gcol[j][i] = gsp[2 + 3 * i + j];
+  const float z = f->c2[2];
+  gcol[2][0] += gsp[0] / z;
+  gcol[2][1] += gsp[1] / z;
+  gcol[2][2] -= (gsp[0] * f->c2[0] + gsp[1] * f->c2[1]) / (z * z);
+  /* back through K: x -> (fx x0 + cx x2, fy x1 + cy x2, x2) */
+  float gx[3][3];
+  for (int j = 0; j < 3; ++j) {
+    gx[j][0] = c->fx * gcol[j][0];
+    gx[j][1] = c->fy * gcol[j][1];
+    gx[j][2] = c->cx * gcol[j][0] + c->cy * gcol[j][1] + gcol[j][2];
+  }
+  /* qc = W (p - campos): dL/dp = W^T dL/dqc */
+  const float* W = c->rot_cw;
+  for (int k = 0; k < 3; ++k) g[k] += gpos[k] + W[k] * gx[2][0] + W[3 + k] * gx[2][1] + W[6 + k] * gx[2][2];
+  /* t_u = Rc[:,0] s_u, t_v = Rc[:,1] s_v */
+  float gRc[9] = {0};
+  float gsu = 0.f, gsv = 0.f;
+  for (int i = 0; i < 3; ++i) {
+    gsu += gx[0][i] * f->Rc[3 * i];
+    gsv += gx[1][i] * f->Rc[3 * i + 1];
+    gRc[3 * i] = gx[0][i] * f->s[0];
+    gRc[3 * i + 1] = gx[1][i] * f->s[1];
+  }
+  g[4] += gsu * f->s[0];
+  g[5] += gsv * f->s[1];
+  /* Rc = W Rq: dL/dRq = W^T dL/dRc */
+  float G[9] = {0};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      for (int r = 0; r < 3; ++r) G[3 * i + j] += W[3 * r + i] * gRc[3 * r + j];
+  const float w = f->qn[0], qx = f->qn[1], qy = f->qn[2], qz = f->qn[3];
+  float gqn[4];
+  gqn[0] = 2.f * (-qz * G[1] + qy * G[2] + qz * G[3] - qx * G[5] - qy * G[6] + qx * G[7]);
+  gqn[1] = 2.f * (qy * G[1] + qz * G[2] + qy * G[3] - 2.f * qx * G[4] - w * G[5] + qz * G[6] + w * G[7] - 2.f * qx * G[8]);
+  gqn[2] = 2.f * (-2.f * qy * G[0] + qx * G[1] + w * G[2] + qx * G[3] + qz * G[5] - w * G[6] + qz * G[7] - 2.f * qy * G[8]);
+  gqn[3] = 2.f * (-2.f * qz * G[0] - w * G[1] + qx * G[2] + w * G[3] - 2.f * qz * G[4] + qy * G[5] + qx * G[6] + qy * G[7]);
+  const float dq = w * gqn[0] + qx * gqn[1] + qy * gqn[2] + qz * gqn[3];
+  for (int k = 0; k < 4; ++k) g[8 + k] += (gqn[k] - f->qn[k] * dq) / f->qnorm;
+}
+
+void or_project2d_bwd(const float* params, int64_t S, const int64_t* idx, int64_t m, const or_camera* c,
+                      int32_t sh_degree, const float* gsp, float* grad_params) {
+  const int n_sh = (sh_degree + 1) * (sh_degree + 1);
+  for (int64_t k = 0; k < m; ++k) {
+    opoint pt;
+    oproj2 f;
+    float g[60] = {0};
+    const int64_t i = idx[k];
+    load_opoint(params, S, i, &pt);
+    proj2_fwd(&pt, c, n_sh, &f);
+    proj2_bwd(&pt, c, n_sh, &f, gsp + k * GSP2F, g);
+    for (int p = 0; p < 15; ++p)
+      for (int l = 0; l < 4; ++l) grad_params[4 * (p * S + i) + l] += g[4 * p + l];
+  }
+}
+
+/* ray-splat intersection of pixel centre (px, py) with a 2DGS row */
+typedef struct {
+  float hx[3], hy[3], z[3], u, v, g3, dx, dy, g2, power;
+  int ok;
+} oeval2;
+
+static void eval2_o(const float* r, float px, float py, oeval2* e) {
+  const float* M = r + 3;
+  for (int k = 0; k < 3; ++k) {
+    e->hx[k] = M[k] - px * M[6 + k];
+    e->hy[k] = M[3 + k] - py * M[6 + k];
+  }
+  e->z[0] = e->hx[1] * e->hy[2] - e->hx[2] * e->hy[1];
+  e->z[1] = e->hx[2] * e->hy[0] - e->hx[0] * e->hy[2];
+  e->z[2] = e->hx[0] * e->hy[1] - e->hx[1] * e->hy[0];
+  e->ok = e->z[2] != 0.f;
+  if (!e->ok) return;
+  e->u = e->z[0] / e->z[2];
+  e->v = e->z[1] / e->z[2];
+  e->g3 = e->u * e->u + e->v * e->v;
+  e->dx = r[0] - px;
+  e->dy = r[1] - py;
+  e->g2 = 2.f * (e->dx * e->dx + e->dy * e->dy);
+  e->power = -0.5f * fminf(e->g3, e->g2);
+}
+
+int32_t or_render2d(const float* sp, int64_t m, int32_t W, int32_t H, const float* bg, float* image, float* final_T,
+                    int32_t* n_contrib, uint32_t* tile_lists, int64_t* n_inst, int32_t* tile_ranges) {
+  const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
+  int32_t* ranges = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)tx * ty);
+  int64_t total = 0;
+  oinst* inst = bin_view_l(sp, m, W, H, LAY2, &total, ranges);
+  if (tile_lists) {
+    if (*n_inst < total) {
+      *n_inst = total;
+      free(inst);
+      free(ranges);
+      return 1;
+    }
+    for (int64_t i = 0; i < total; ++i) tile_lists[i] = inst[i].row;
+    memcpy(tile_ranges, ranges, sizeof(int32_t) * 2 * (size_t)tx * ty);
+  }
+  if (n_inst) *n_inst = total;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int t = 0; t < tx * ty; ++t) {
+    const int bx = t % tx, by = t / tx;
+    for (int ly = 0; ly < TILE; ++ly)
+      for (int lx = 0; lx < TILE; ++lx) {
+        const int px = bx * TILE + lx, py = by * TILE + ly;
+        if (px >= W || py >= H) continue;
+        const float pxf = (float)px + 0.5f, pyf = (float)py + 0.5f;
+        float T = 1.f, C[3] = {0, 0, 0};
+        int contrib = 0;
+        for (int i = ranges[2 * t]; i < ranges[2 * t + 1]; ++i) {
+          const float* r = sp + (int64_t)inst[i].row * SP2F;
+          oeval2 e;
+          eval2_o(r, pxf, pyf, &e);
+          if (!e.ok || e.power > 0.f) continue;
+          const float alpha = fminf(0.99f, r[2] * expf(e.power));
+          if (alpha < 1.f / 255.f) continue;
+          const float nT = T * (1.f - alpha);
+          if (nT < 1e-4f) break;
+          const float w = alpha * T;
+          for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(r[12 + ch], w, C[ch]);
+          T = nT;
+          contrib = i + 1 - ranges[2 * t];
+        }
+        const int64_t pix = (int64_t)py * W + px;
+        for (int ch = 0; ch < 3; ++ch) image[3 * pix + ch] = C[ch] + T * bg[ch];
+        final_T[pix] = T;
+        n_contrib[pix] = contrib;
+      }
+  }
+  free(inst);
+  free(ranges);
+  return 0;
+}
+
+int32_t or_render2d_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const float* bg, const float* final_T,
+                        const int32_t* n_contrib, const float* grad_image, float* gsp) {
+  const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
+  int32_t* ranges = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)tx * ty);
+  int64_t total = 0;
+  oinst* inst = bin_view_l(sp, m, W, H, LAY2, &total, ranges);
+  memset(gsp, 0, sizeof(float) * GSP2F * (size_t)m);
+  for (int t = 0; t < tx * ty; ++t) {
+    const int bx = t % tx, by = t / tx;
+    for (int ly = 0; ly < TILE; ++ly)
+      for (int lx = 0; lx < TILE; ++lx) {
+        const int px = bx * TILE + lx, py = by * TILE + ly;
+        if (px >= W || py >= H) continue;
+        const int64_t pix = (int64_t)py * W + px;
+        const float pxf = (float)px + 0.5f, pyf = (float)py + 0.5f;
+        const float* dC = grad_image + 3 * pix;
+        const float T_final = final_T[pix];
+        const float bgdot = bg[0] * dC[0] + bg[1] * dC[1] + bg[2] * dC[2];
+        float T = T_final, acc[3] = {0, 0, 0}, last_alpha = 0.f, lc[3] = {0, 0, 0};
+        const int r0 = ranges[2 * t];
+        for (int i = r0 + n_contrib[pix] - 1; i >= r0; --i) {
+          const int64_t row = inst[i].row;
+          const float* r = sp + row * SP2F;
+          oeval2 e;
+          eval2_o(r, pxf, pyf, &e);
+          if (!e.ok || e.power > 0.f) continue;
+          const float ex = expf(e.power);
+          const float raw = r[2] * ex;
+          const float alpha = fminf(0.99f, raw);
+          if (alpha < 1.f / 255.f) continue;
+          const float ra = 1.f / (1.f - alpha);
+          T = T * ra;
+          float* g = gsp + row * GSP2F;
+          const float fac = alpha * T;
+          for (int ch = 0; ch < 3; ++ch) g[12 + ch] += fac * dC[ch];
+          for (int ch = 0; ch < 3; ++ch) acc[ch] = last_alpha * lc[ch] + (1.f - last_alpha) * acc[ch];
+          last_alpha = alpha;
+          for (int ch = 0; ch < 3; ++ch) lc[ch] = r[12 + ch];
+          float dL_da = 0.f;
+          for (int ch = 0; ch < 3; ++ch) dL_da += (r[12 + ch] - acc[ch]) * dC[ch];
+          dL_da = T * dL_da - T_final * ra * bgdot;
+          if (raw > 0.99f) continue;
+          const float dpow = dL_da * alpha;
+          g[11] += dL_da * ex;
+          if (e.g3 <= e.g2) {
+            /* power = -(u^2 + v^2) / 2, (u, v) = zeta.xy / zeta.z, zeta = hx x hy */
+            const float gu = -e.u * dpow, gv = -e.v * dpow;
+            const float gz[3] = {gu / e.z[2], gv / e.z[2], -(gu * e.z[0] + gv * e.z[1]) / (e.z[2] * e.z[2])};
+            float ghx[3], ghy[3];
+            ghx[0] = e.hy[1] * gz[2] - e.hy[2] * gz[1];
+            ghx[1] = e.hy[2] * gz[0] - e.hy[0] * gz[2];
+            ghx[2] = e.hy[0] * gz[1] - e.hy[1] * gz[0];
+            ghy[0] = gz[1] * e.hx[2] - gz[2] * e.hx[1];
+            ghy[1] = gz[2] * e.hx[0] - gz[0] * e.hx[2];
+            ghy[2] = gz[0] * e.hx[1] - gz[1] * e.hx[0];
+            for (int k = 0; k < 3; ++k) {
+              g[2 + k] += ghx[k];
+              g[5 + k] += ghy[k];
+              g[8 + k] -= pxf * ghx[k] + pyf * ghy[k];
+            }
+          } else {
+            /* low-pass branch: power = -(dx^2 + dy^2) */
+            g[0] += -2.f * e.dx * dpow;
+            g[1] += -2.f * e.dy * dpow;
+          }
+        }
+      }
+  }
+  free(inst);
+  free(ranges);
+  return 0;
+}
+
+double or_train_step_model(float* params, float* exp_avg, float* exp_avg_sq, int64_t S, const double* planes,
+                           const or_camera* cams, int32_t B, const uint8_t* gt, int32_t sh_degree, const float* lr60,
+                           float beta1, float beta2, float eps, int32_t step, int32_t n_threads, int32_t model) {
   (void)n_threads;
   const int64_t NP = 60 * S;
   float* grads = (float*)calloc((size_t)NP, sizeof(float));
@@ -710,8 +1126,12 @@ double or_train_step(float* params, float* exp_avg, float* exp_avg_sq, int64_t S
     int64_t m = 0;
     for (int64_t i = 0; i < S; ++i)
       if (in_patch(vp, 1, 0, 0, pos[3 * i], pos[3 * i + 1], pos[3 * i + 2])) idx[m++] = i;
-    float* sp = (float*)malloc(sizeof(float) * SPF * (size_t)(m > 0 ? m : 1));
-    or_project(params, S, idx, m, c, sh_degree, sp);
+    const int spf = model ? SP2F : SPF, gspf = model ? GSP2F : GSPF;
+    float* sp = (float*)malloc(sizeof(float) * spf * (size_t)(m > 0 ? m : 1));
+    if (model)
+      or_project2d(params, S, idx, m, c, sh_degree, sp);
+    else
+      or_project(params, S, idx, m, c, sh_degree, sp);
     const int W = c->width, H = c->height;
     const int64_t npx = (int64_t)W * H;
     float* img = (float*)malloc(sizeof(float) * 3 * (size_t)npx);
@@ -719,11 +1139,19 @@ double or_train_step(float* params, float* exp_avg, float* exp_avg_sq, int64_t S
     int32_t* nc = (int32_t*)malloc(sizeof(int32_t) * (size_t)npx);
     float* gimg = (float*)malloc(sizeof(float) * 3 * (size_t)npx);
     const float bg[3] = {0, 0, 0};
-    or_render(sp, m, W, H, bg, img, fT, nc, NULL, NULL, NULL);
+    if (model)
+      or_render2d(sp, m, W, H, bg, img, fT, nc, NULL, NULL, NULL);
+    else
+      or_render(sp, m, W, H, bg, img, fT, nc, NULL, NULL, NULL);
     loss += or_l1_loss(img, gt + (size_t)v * 3 * npx, 3 * npx, gimg);
-    float* gsp = (float*)malloc(sizeof(float) * GSPF * (size_t)(m > 0 ? m : 1));
-    or_render_bwd(sp, m, W, H, bg, fT, nc, gimg, gsp);
-    or_project_bwd(params, S, idx, m, c, sh_degree, gsp, grads);
+    float* gsp = (float*)malloc(sizeof(float) * gspf * (size_t)(m > 0 ? m : 1));
+    if (model) {
+      or_render2d_bwd(sp, m, W, H, bg, fT, nc, gimg, gsp);
+      or_project2d_bwd(params, S, idx, m, c, sh_degree, gsp, grads);
+    } else {
+      or_render_bwd(sp, m, W, H, bg, fT, nc, gimg, gsp);
+      or_project_bwd(params, S, idx, m, c, sh_degree, gsp, grads);
+    }
     free(idx);
     free(sp);
     free(img);
@@ -737,3 +1165,4 @@ double or_train_step(float* params, float* exp_avg, float* exp_avg_sq, int64_t S
   free(pos);
   return loss;
 }
+

@@ -78,4 +78,28 @@ double or_train_step(float* params, float* exp_avg, float* exp_avg_sq,
                      int32_t B, const uint8_t* gt, int32_t sh_degree,
                      const float* lr60, float beta1, float beta2, float eps,
                      int32_t step, int32_t n_threads);
+
+/* 2DGS (surfel) variants: rows [m][24] / gradient rows [m][15]
+ * (include/splat_b200.h BS_SP2_FLOATS / BS_GSP2_FLOATS). */
+void or_project2d(const float* params, int64_t S, const int64_t* idx, int64_t m,
+                  const or_camera* c, int32_t sh_degree, float* sp);
+void or_project2d_bwd(const float* params, int64_t S, const int64_t* idx,
+                      int64_t m, const or_camera* c, int32_t sh_degree,
+                      const float* gsp, float* grad_params);
+int32_t or_render2d(const float* sp, int64_t m, int32_t W, int32_t H,
+                    const float* bg, float* image, float* final_T,
+                    int32_t* n_contrib, uint32_t* tile_lists, int64_t* n_inst,
+                    int32_t* tile_ranges);
+int32_t or_render2d_bwd(const float* sp, int64_t m, int32_t W, int32_t H,
+                        const float* bg, const float* final_T,
+                        const int32_t* n_contrib, const float* grad_image,
+                        float* gsp);
+/* or_train_step for model 0 (3DGS) or 1 (2DGS). */
+double or_train_step_model(float* params, float* exp_avg, float* exp_avg_sq,
+                           int64_t S, const double* planes,
+                           const or_camera* cams, int32_t B, const uint8_t* gt,
+                           int32_t sh_degree, const float* lr60, float beta1,
+                           float beta2, float eps, int32_t step,
+                           int32_t n_threads, int32_t model);
+
 #endif

@@ -47,9 +47,15 @@ class CullDesc(C.Structure):
                 ("n_gpus", C.c_int32), ("temporal", C.c_int32), ("pos_stride", C.c_int32)]
 
 
+MODEL_3DGS = 0
+MODEL_2DGS = 1
+SP2_FLOATS = 24
+GSP2_FLOATS = 15
+
+
 class ProjDesc(C.Structure):
     _fields_ = [("n_views", C.c_int32), ("sh_degree", C.c_int32),
-                ("tiles_x_max", C.c_int32), ("tiles_y_max", C.c_int32)]
+                ("tiles_x_max", C.c_int32), ("tiles_y_max", C.c_int32), ("model", C.c_int32)]
 
 
 class RasterDesc(C.Structure):
@@ -89,10 +95,10 @@ _SIGS = {
     "bs_bin_count": (_I32, [_P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "bs_bin_emit": (_I32, [_P, _P, _I64, _P, _P, _I32, _P, _P, _P, _P]),
     "bs_tile_ranges": (_I32, [_P, _P, _I64, _I32, _P, _P]),
-    "bs_bin_tiles_count": (_I32, [_P, _I64, _P, _P, _I32, _P, _I32, _I32, _P, _P]),
+    "bs_bin_tiles_count": (_I32, [_P, _I64, _P, _P, _I32, _P, _I32, _I32, _P, _I32, _P]),
     "bs_bin_tiles_offsets": (_I32, [_P, _I32, _P, _P, _P, _P, _SZ, _P]),
     "bs_bin_tiles_offsets_workspace": (_SZ, [_I32]),
-    "bs_bin_tiles_scatter": (_I32, [_P, _I64, _P, _P, _I32, _P, _I32, _P, _P, _P]),
+    "bs_bin_tiles_scatter": (_I32, [_P, _I64, _P, _P, _I32, _P, _I32, _P, _P, _I32, _P]),
     "bs_bin_tiles_sort": (_I32, [_P, _P, _I32, _I32, _P, _P]),
     "bs_bin_tiles_max_sort": (_I32, []),
     "bs_keys_low32": (_I32, [_P, _I64, _P, _P]),
@@ -101,6 +107,8 @@ _SIGS = {
     "bs_l1_loss": (_I32, [_P, _P, _I32, _I32, _I32, _P, _P, _P, _SZ, _P]),
     "bs_reduce_loss_tiles": (_I32, [_P, _I32, _I32, _I32, _I32, _P, _P]),
     "bs_raster_bwd": (_I32, [C.POINTER(RasterDesc), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "bs_raster2d_fwd": (_I32, [C.POINTER(RasterDesc), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "bs_raster2d_bwd": (_I32, [C.POINTER(RasterDesc), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bs_project_bwd": (_I32, [C.POINTER(ProjDesc), _P, _I64, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),
     "bs_adam_step": (_I32, [C.POINTER(AdamDesc), _P, _P, _P, _P, _I64, _P, _P]),
     "bs_project_bwd_adam": (_I32, [C.POINTER(ProjDesc), C.POINTER(AdamDesc), _P, _P, _P, _I64, _P, _P,

@@ -33,6 +33,7 @@ struct BinGeom {
   int n_segs;
   const bs_camera* cams;
   int tiles_per_slot;
+  SpLayout lay;
 };
 
 __global__ void count_tiles_kernel(BinGeom g, int32_t* __restrict__ counts) {
@@ -40,7 +41,7 @@ __global__ void count_tiles_kernel(BinGeom g, int32_t* __restrict__ counts) {
     const int slot = g.seg_slot[segment_of(g.seg_row0, g.n_segs, r)];
     const int W = g.cams[slot].width, H = g.cams[slot].height;
     int x0, x1, y0, y1;
-    if (!tile_rect(g.sp + r * BS_SP_FLOATS, W, H, x0, x1, y0, y1)) continue;
+    if (!tile_rect_at(g.sp + r * g.lay.stride, g.lay.rad_off, W, H, x0, x1, y0, y1)) continue;
     const int tx = (W + BS_TILE - 1) / BS_TILE;
     int32_t* base = counts + (int64_t)slot * g.tiles_per_slot;
     for (int y = y0; y < y1; ++y)
@@ -140,11 +141,11 @@ __global__ void scatter_tiles_kernel(BinGeom g, int32_t* __restrict__ cursor, ui
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < g.n; r += (int64_t)gridDim.x * blockDim.x) {
     const int slot = g.seg_slot[segment_of(g.seg_row0, g.n_segs, r)];
     const int W = g.cams[slot].width, H = g.cams[slot].height;
-    const float* row = g.sp + r * BS_SP_FLOATS;
+    const float* row = g.sp + r * g.lay.stride;
     int x0, x1, y0, y1;
-    if (!tile_rect(row, W, H, x0, x1, y0, y1)) continue;
+    if (!tile_rect_at(row, g.lay.rad_off, W, H, x0, x1, y0, y1)) continue;
     const int tx = (W + BS_TILE - 1) / BS_TILE;
-    const uint64_t key = ((uint64_t)__float_as_uint(row[9]) << 32) | (uint64_t)(uint32_t)r;
+    const uint64_t key = ((uint64_t)__float_as_uint(row[g.lay.depth_off]) << 32) | (uint64_t)(uint32_t)r;
     int32_t* base = cursor + (int64_t)slot * g.tiles_per_slot;
     for (int y = y0; y < y1; ++y)
       for (int x = x0; x < x1; ++x) keys[atomicAdd(base + y * tx + x, 1)] = key;
@@ -285,14 +286,14 @@ using namespace bs;
 extern "C" int32_t bs_bin_tiles_count(const float* sp_rows, int64_t n_rows, const int64_t* seg_row0,
                                       const int32_t* seg_slot, int32_t n_segs, const bs_camera* slot_cams,
                                       int32_t tiles_per_slot, int32_t n_buckets, int32_t* bucket_counts,
-                                      void* stream) {
+                                      int32_t model, void* stream) {
   BS_REQUIRE(n_segs >= 1 && n_buckets >= 1, BS_ERR_PARAMETER, "bin: bad segment/bucket counts");
   BS_REQUIRE(n_rows < (1ll << 32), BS_ERR_PARAMETER, "bin: too many rows for 32-bit row ids");
   cudaStream_t s = as_stream(stream);
   if (cudaMemsetAsync(bucket_counts, 0, sizeof(int32_t) * (size_t)n_buckets, s) != cudaSuccess)
     return set_error(BS_ERR_CUDA, "bin: memset failed");
   if (n_rows == 0) return BS_OK;
-  BinGeom g{sp_rows, n_rows, seg_row0, seg_slot, n_segs, slot_cams, tiles_per_slot};
+  BinGeom g{sp_rows, n_rows, seg_row0, seg_slot, n_segs, slot_cams, tiles_per_slot, sp_layout(model)};
   count_tiles_kernel<<<grid_for(n_rows, 256), 256, 0, s>>>(g, bucket_counts);
   BS_LAUNCH_CHECK("count_tiles_kernel");
   return BS_OK;
@@ -326,10 +327,10 @@ extern "C" int32_t bs_bin_tiles_offsets(const int32_t* bucket_counts, int32_t n_
 extern "C" int32_t bs_bin_tiles_scatter(const float* sp_rows, int64_t n_rows, const int64_t* seg_row0,
                                         const int32_t* seg_slot, int32_t n_segs, const bs_camera* slot_cams,
                                         int32_t tiles_per_slot, int32_t* cursor, uint64_t* inst_keys,
-                                        void* stream) {
+                                        int32_t model, void* stream) {
   BS_REQUIRE(n_segs >= 1, BS_ERR_PARAMETER, "bin: need at least one segment");
   if (n_rows == 0) return BS_OK;
-  BinGeom g{sp_rows, n_rows, seg_row0, seg_slot, n_segs, slot_cams, tiles_per_slot};
+  BinGeom g{sp_rows, n_rows, seg_row0, seg_slot, n_segs, slot_cams, tiles_per_slot, sp_layout(model)};
   scatter_tiles_kernel<<<grid_for(n_rows, 256), 256, 0, as_stream(stream)>>>(g, cursor, inst_keys);
   BS_LAUNCH_CHECK("scatter_tiles_kernel");
   return BS_OK;

@@ -8,7 +8,7 @@
 //     view_row0[v] + base[g][v] + #{visible points of v in g before i}
 // recomputed identically by every per-point kernel with warp ballots, so no
 // per-(view, point) index table is ever materialised.
-#include "splat_math.cuh"
+#include "splat2d_math.cuh"
 
 namespace bs {
 namespace {
@@ -60,6 +60,39 @@ struct ProjArgs {
   const bs_camera* cams;
 };
 
+// Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
+// 24-float SP rows, splat2d_math.cuh).
+struct Model3 {
+  using F = ProjFwd;
+  static constexpr int kSP = BS_SP_FLOATS, kGSP = BS_GSP_FLOATS;
+  template <class SH>
+  __device__ static void forward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh, F& f) {
+    project_forward_t(pt, sh, c, n_sh, f);
+  }
+  __device__ static void write(float* row, const F& f) { write_sp_row(row, f); }
+  template <class SH, class A>
+  __device__ static void backward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh, const F& f,
+                                  const float* gs, float* g, A add) {
+    project_backward_t(pt, sh, c, n_sh, f, gs, g, add);
+  }
+};
+
+struct Model2 {
+  using F = Proj2D;
+  static constexpr int kSP = kSP2, kGSP = kGSP2;
+  template <class SH>
+  __device__ static void forward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh, F& f) {
+    project2d_forward(pt, sh, c, n_sh, f);
+  }
+  __device__ static void write(float* row, const F& f) { write_sp2_row(row, f); }
+  template <class SH, class A>
+  __device__ static void backward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh, const F& f,
+                                  const float* gs, float* g, A add) {
+    project2d_backward(pt, sh, c, n_sh, f, gs, g, add);
+  }
+};
+
+template <class M>
 __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, float* __restrict__ sp) {
   __shared__ uint32_t s_bal[kProjWarps * kMaxViews];
   __shared__ int s_run[kMaxViews];
@@ -85,10 +118,10 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
       while (m) {
         const int v = __ffs(m) - 1;
         m &= m - 1;
-        ProjFwd f;
-        project_forward(pt, s_cam[v], a.n_sh, f);
+        typename M::F f;
+        M::forward(pt, ShRegs{pt.sh}, s_cam[v], a.n_sh, f);
         const int64_t row = s_row0[v] + rk.row_offset(v);
-        write_sp_row(sp + row * BS_SP_FLOATS, f);
+        M::write(sp + row * M::kSP, f);
       }
     }
     rk.advance(B);
@@ -97,7 +130,7 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
 
 // Accumulate the parameter gradient of one point over all its views:
 // geometry (12 floats) into g, SH coefficients through sh_add.
-template <class SH, class ShAdd>
+template <class M, class SH, class ShAdd>
 __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camera* s_cam, const int64_t* s_row0,
                                                const RowRanker& rk, uint32_t mask, const PointIn& pt, const SH& sh,
                                                const float* __restrict__ gsp, float* g, ShAdd sh_add) {
@@ -106,16 +139,17 @@ __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camer
     const int v = __ffs(m) - 1;
     m &= m - 1;
     const int64_t row = s_row0[v] + rk.row_offset(v);
-    float gs[9];
-    const float* src = gsp + row * BS_GSP_FLOATS;
+    float gs[M::kGSP];
+    const float* src = gsp + row * M::kGSP;
 #pragma unroll
-    for (int k = 0; k < 9; ++k) gs[k] = src[k];
-    ProjFwd f;
-    project_forward_t(pt, sh, s_cam[v], a.n_sh, f);
-    project_backward_t(pt, sh, s_cam[v], a.n_sh, f, gs, g, sh_add);
+    for (int k = 0; k < M::kGSP; ++k) gs[k] = src[k];
+    typename M::F f;
+    M::forward(pt, sh, s_cam[v], a.n_sh, f);
+    M::backward(pt, sh, s_cam[v], a.n_sh, f, gs, g, sh_add);
   }
 }
 
+template <class M>
 __global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, const float* __restrict__ gsp,
                                                                    float4* __restrict__ gparams) {
   __shared__ uint32_t s_bal[kProjWarps * kMaxViews];
@@ -141,8 +175,8 @@ __global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, c
       PointGrad gr;
 #pragma unroll
       for (int k = 0; k < 60; ++k) gr.g[k] = 0.f;
-      point_backward(a, s_cam, s_row0, rk, mask, pt, ShRegs{pt.sh}, gsp, gr.g,
-                     [&](int f, float v) { gr.g[12 + f] += v; });
+      point_backward<M>(a, s_cam, s_row0, rk, mask, pt, ShRegs{pt.sh}, gsp, gr.g,
+                        [&](int f, float v) { gr.g[12 + f] += v; });
 #pragma unroll
       for (int p = 0; p < BS_PARAM_PLANES; ++p) {
         float4 acc = gparams[p * a.S + i];
@@ -196,6 +230,7 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamConsts c, float4* __restr
   }
 }
 
+template <class M>
 __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjArgs a, AdamConsts c,
                                                                            const float* __restrict__ gsp,
                                                                            float4* params,
@@ -234,7 +269,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
         PointIn pt;
         load_point(a.params, a.S, i, 0, pt);  // geometry planes only; SH read from L1 on use
         const ShPlanes sh{reinterpret_cast<const float*>(a.params), a.S, i};
-        point_backward(a, s_cam, s_row0, rk, mask, pt, sh, gsp, g12,
+        point_backward<M>(a, s_cam, s_row0, rk, mask, pt, sh, gsp, g12,
                        [&](int f, float val) { my_sh[f * kProjThreads] += val; });
       }
 #pragma unroll
@@ -364,7 +399,10 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams};
-  project_fwd_kernel<<<n_groups, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
+  if (d->model == BS_MODEL_2DGS)
+    project_fwd_kernel<Model2><<<n_groups, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
+  else
+    project_fwd_kernel<Model3><<<n_groups, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
   BS_LAUNCH_CHECK("project_fwd_kernel");
   return BS_OK;
 }
@@ -379,8 +417,12 @@ extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, in
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams};
-  project_bwd_kernel<<<n_groups, kProjThreads, 0, as_stream(stream)>>>(a, g_sp,
-                                                                       reinterpret_cast<float4*>(grad_params));
+  if (d->model == BS_MODEL_2DGS)
+    project_bwd_kernel<Model2><<<n_groups, kProjThreads, 0, as_stream(stream)>>>(
+        a, g_sp, reinterpret_cast<float4*>(grad_params));
+  else
+    project_bwd_kernel<Model3><<<n_groups, kProjThreads, 0, as_stream(stream)>>>(
+        a, g_sp, reinterpret_cast<float4*>(grad_params));
   BS_LAUNCH_CHECK("project_bwd_kernel");
   return BS_OK;
 }
@@ -412,10 +454,14 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
              view_row0, cams};
   AdamConsts c = make_adam(ad);
   const size_t smem = sizeof(float) * 48 * kProjThreads;
-  cudaFuncSetAttribute(project_bwd_adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  project_bwd_adam_kernel<<<n_groups, kProjThreads, smem, as_stream(stream)>>>(
-      a, c, g_sp, reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(exp_avg),
-      reinterpret_cast<float4*>(exp_avg_sq));
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<n_groups, kProjThreads, smem, as_stream(stream)>>>(a, c, g_sp, reinterpret_cast<float4*>(params),
+                                                             reinterpret_cast<float4*>(exp_avg),
+                                                             reinterpret_cast<float4*>(exp_avg_sq));
+  };
+  if (pd->model == BS_MODEL_2DGS) launch(project_bwd_adam_kernel<Model2>);
+  else launch(project_bwd_adam_kernel<Model3>);
   BS_LAUNCH_CHECK("project_bwd_adam_kernel");
   return BS_OK;
 }

@@ -1,0 +1,435 @@
+// 2DGS rasterisation (surfel ray-splat intersection, splat2d_math.cuh):
+// forward alpha compositing + fused mean-L1 partials, and the backward.
+// Same execution scheme as the 3DGS kernels (raster.cu, 1 pixel per lane):
+// 16x16 tiles, 8 independent warps per tile each owning an 8x4 pixel
+// region, chunks of 32 gathered instances with a register prefetch, a
+// per-warp footprint filter, ballot compaction into warp-private shared
+// memory.  Per pixel (centre x + 0.5, y + 0.5):
+//   h_x = M_row0 - x M_row2, h_y = M_row1 - y M_row2, zeta = h_x x h_y,
+//   (u, v) = zeta.xy / zeta.z,  g3 = u^2 + v^2,  g2 = 2 |mean2d - pixel|^2,
+//   alpha = min(0.99, opacity exp(-0.5 min(g3, g2))) -- same skip / stop
+// rules as 3DGS.  Footprint filter: alpha >= 1/255 needs min(g3, g2) <= L,
+// L = 2 ln(255 o): the union of the bounding box of the image of the disk
+// u^2 + v^2 <= L (dual conic; unbounded -> keep) and the circle
+// |mean2d - pixel| <= sqrt(L / 2), padded by 1%.
+// Backward: 15 gradient terms per splat, reduce-scattered over the warp in
+// 16 shuffles, one RED per term per (region, splat).
+#include "splat2d_math.cuh"
+
+namespace bs {
+namespace {
+
+constexpr int kW2 = 8;  // warps per 16x16 tile (8x4 region each)
+constexpr int kT2 = 32 * kW2;
+constexpr float kAMin = 1.0f / 255.0f;
+constexpr float kAMax = 0.99f;
+constexpr float kTStop = 1e-4f;
+
+struct R2Args {
+  int n_slots, tiles_per_slot, W, H, tiles_x;
+  float bg[3];
+  int loss_fused;
+  float inv_norm;
+};
+
+// staged splat: a = (u, v, opac, M0), b = (M1..M4), c = (M5..M8), d = (r, g, b, -)
+struct Warp2 {
+  float4 a[32], b[32], c[32], d[32];
+  uint32_t row[32];
+};
+
+struct Splat2 {
+  float4 p[4];  // SP floats 0..15
+  uint32_t row;
+  bool ok;
+};
+
+__device__ __forceinline__ void fetch2(Splat2& f, const float* __restrict__ sp, const uint32_t* __restrict__ rows,
+                                       int idx, bool ok) {
+  f.ok = ok;
+  if (ok) {
+    f.row = __ldg(rows + idx);
+    const float4* r4 = reinterpret_cast<const float4*>(sp + (int64_t)f.row * kSP2);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) f.p[k] = __ldg(r4 + k);
+  }
+}
+
+// M rows from the staged layout: r0 = (M0, M1, M2), r1 = (M3, M4, M5), r2 = (M6, M7, M8)
+__device__ __forceinline__ void m_rows(const float4& a, const float4& b, const float4& c, float r0[3], float r1[3],
+                                       float r2[3]) {
+  r0[0] = a.w; r0[1] = b.x; r0[2] = b.y;
+  r1[0] = b.z; r1[1] = b.w; r1[2] = c.x;
+  r2[0] = c.y; r2[1] = c.z; r2[2] = c.w;
+}
+
+__device__ __forceinline__ bool reaches2(const Splat2& f, float x0, float x1, float y0, float y1) {
+  if (!f.ok) return false;
+  const float4 a = make_float4(f.p[0].x, f.p[0].y, f.p[0].z, f.p[0].w);
+  const float4 b = f.p[1], c = f.p[2];
+  const float o = a.z;
+  const float L = 2.f * __logf(255.f * o);
+  if (!(L > 0.f)) return false;
+  // low-pass circle around mean2d
+  const float rc = sqrtf(0.5f * L) * 1.01f + 1e-3f;
+  const float ecx = fabsf(a.x - fminf(fmaxf(a.x, x0), x1)), ecy = fabsf(a.y - fminf(fmaxf(a.y, y0), y1));
+  if (ecx <= rc && ecy <= rc) return true;
+  // image of the disk u^2 + v^2 <= L
+  float r0[3], r1[3], r2[3];
+  m_rows(a, b, c, r0, r1, r2);
+  // columns: c0 = (r0[0], r1[0], r2[0]), c1 = (r0[1], r1[1], r2[1]), c2 = (r0[2], r1[2], r2[2])
+  const float C22 = L * (r2[0] * r2[0] + r2[1] * r2[1]) - r2[2] * r2[2];
+  if (!(C22 < 0.f)) return true;  // unbounded image: keep (conservative)
+  const float C02 = L * (r0[0] * r2[0] + r0[1] * r2[1]) - r0[2] * r2[2];
+  const float C12 = L * (r1[0] * r2[0] + r1[1] * r2[1]) - r1[2] * r2[2];
+  const float C00 = L * (r0[0] * r0[0] + r0[1] * r0[1]) - r0[2] * r0[2];
+  const float C11 = L * (r1[0] * r1[0] + r1[1] * r1[1]) - r1[2] * r1[2];
+  const float bx = C02 / C22, by = C12 / C22;
+  const float hx = sqrtf(fmaxf(bx * bx - C00 / C22, 0.f)) * 1.01f + 1e-3f;
+  const float hy = sqrtf(fmaxf(by * by - C11 / C22, 0.f)) * 1.01f + 1e-3f;
+  return fabsf(bx - fminf(fmaxf(bx, x0), x1)) <= hx && fabsf(by - fminf(fmaxf(by, y0), y1)) <= hy;
+}
+
+__device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f) {
+  s.a[lane] = f.p[0];
+  s.b[lane] = f.p[1];
+  s.c[lane] = f.p[2];
+  s.d[lane] = f.p[3];  // (r, g, b, depth)
+  s.row[lane] = f.row;
+}
+
+struct Eval2 {
+  float hx[3], hy[3], z[3], u, v, g3, dx, dy, g2, power;
+  bool ok;
+};
+
+// Bit-identical in forward and backward (explicit round-to-nearest ops).
+__device__ __forceinline__ void eval2(const float4& a, const float4& b, const float4& c, float px, float py,
+                                      Eval2& e) {
+  float r0[3], r1[3], r2[3];
+  m_rows(a, b, c, r0, r1, r2);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    e.hx[k] = __fsub_rn(r0[k], __fmul_rn(px, r2[k]));
+    e.hy[k] = __fsub_rn(r1[k], __fmul_rn(py, r2[k]));
+  }
+  e.z[0] = __fsub_rn(__fmul_rn(e.hx[1], e.hy[2]), __fmul_rn(e.hx[2], e.hy[1]));
+  e.z[1] = __fsub_rn(__fmul_rn(e.hx[2], e.hy[0]), __fmul_rn(e.hx[0], e.hy[2]));
+  e.z[2] = __fsub_rn(__fmul_rn(e.hx[0], e.hy[1]), __fmul_rn(e.hx[1], e.hy[0]));
+  e.ok = e.z[2] != 0.f;
+  if (!e.ok) return;
+  e.u = __fdiv_rn(e.z[0], e.z[2]);
+  e.v = __fdiv_rn(e.z[1], e.z[2]);
+  e.g3 = __fadd_rn(__fmul_rn(e.u, e.u), __fmul_rn(e.v, e.v));
+  e.dx = __fsub_rn(a.x, px);
+  e.dy = __fsub_rn(a.y, py);
+  e.g2 = __fmul_rn(2.f, __fadd_rn(__fmul_rn(e.dx, e.dx), __fmul_rn(e.dy, e.dy)));
+  e.power = __fmul_rn(-0.5f, fminf(e.g3, e.g2));
+}
+
+struct Px2 {
+  float T, c0, c1, c2;
+  int contrib;
+  bool done;
+};
+
+__global__ void __launch_bounds__(kT2) raster2d_fwd_kernel(R2Args a, const float* __restrict__ sp,
+                                                            const uint32_t* __restrict__ inst_rows,
+                                                            const int2* __restrict__ ranges, float* __restrict__ image,
+                                                            float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
+                                                            const uint8_t* __restrict__ gt,
+                                                            const int32_t* __restrict__ gt_view,
+                                                            float* __restrict__ loss_tiles) {
+  __shared__ Warp2 smem[kW2];
+  __shared__ float s_red[kW2];
+  const int slot = blockIdx.z, tile = blockIdx.y * a.tiles_x + blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Warp2& s = smem[w];
+  const int rx = blockIdx.x * BS_TILE + (w & 1) * 8, ry = blockIdx.y * BS_TILE + (w >> 1) * 4;
+  const int px = rx + (lane & 7), py = ry + (lane >> 3);
+  const float x0 = rx + 0.5f, x1 = x0 + 7.f, y0 = ry + 0.5f, y1 = y0 + 3.f;
+  const float pxf = px + 0.5f, pyf = py + 0.5f;
+  const bool inside = px < a.W && py < a.H;
+  const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
+  Px2 p{1.f, 0.f, 0.f, 0.f, 0, !inside};
+  Splat2 f;
+  fetch2(f, sp, inst_rows, rg.x + lane, rg.x + lane < rg.y);
+  for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
+    if (__all_sync(0xffffffffu, p.done)) break;
+    const bool keep = reaches2(f, x0, x1, y0, y1);
+    uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if (keep) stage2(s, lane, f);
+    fetch2(f, sp, inst_rows, b0 + 32 + lane, b0 + 32 + lane < rg.y);
+    __syncwarp();
+    while (bits) {
+      const int j = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (p.done) continue;
+      Eval2 e;
+      const float4 sa = s.a[j];
+      eval2(sa, s.b[j], s.c[j], pxf, pyf, e);
+      if (!e.ok || e.power > 0.f) continue;
+      const float alpha = fminf(kAMax, __fmul_rn(sa.z, __expf(e.power)));
+      if (alpha < kAMin) continue;
+      const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
+      if (nT < kTStop) {
+        p.done = true;
+        continue;
+      }
+      const float wgt = __fmul_rn(alpha, p.T);
+      const float4 col = s.d[j];
+      p.c0 = __fmaf_rn(col.x, wgt, p.c0);
+      p.c1 = __fmaf_rn(col.y, wgt, p.c1);
+      p.c2 = __fmaf_rn(col.z, wgt, p.c2);
+      p.T = nT;
+      p.contrib = b0 + j + 1 - rg.x;
+    }
+    __syncwarp();
+  }
+  float l = 0.f;
+  if (inside) {
+    const int64_t pix = ((int64_t)slot * a.H + py) * a.W + px;
+    const float o0 = p.c0 + p.T * a.bg[0], o1 = p.c1 + p.T * a.bg[1], o2 = p.c2 + p.T * a.bg[2];
+    image[3 * pix] = o0;
+    image[3 * pix + 1] = o1;
+    image[3 * pix + 2] = o2;
+    final_T[pix] = p.T;
+    n_contrib[pix] = p.contrib;
+    if (a.loss_fused) {
+      const int gv = gt_view ? gt_view[slot] : slot;
+      const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py) * a.W + px);
+      l = fabsf(o0 - gp[0] * (1.f / 255.f)) + fabsf(o1 - gp[1] * (1.f / 255.f)) + fabsf(o2 - gp[2] * (1.f / 255.f));
+    }
+  }
+  if (a.loss_fused) {
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) s_red[w] = l;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int k = 0; k < kW2; ++k) t += s_red[k];
+      loss_tiles[(int64_t)slot * a.tiles_per_slot + tile] = t;
+    }
+  }
+}
+
+// Reduce-scatter of 16 per-lane values (index 15 padding) in 16 shuffles;
+// even lane L ends with the warp sum of value L >> 1.
+__device__ __forceinline__ float warp_reduce16(float v[16]) {
+  const int lane = threadIdx.x & 31;
+  float a[8], b[4], c[2];
+  const bool u16 = lane & 16;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float send = u16 ? v[i] : v[8 + i];
+    const float mine = u16 ? v[8 + i] : v[i];
+    a[i] = mine + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  const bool u8 = lane & 8;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = u8 ? a[i] : a[4 + i];
+    const float mine = u8 ? a[4 + i] : a[i];
+    b[i] = mine + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const bool u4 = lane & 4;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = u4 ? b[i] : b[2 + i];
+    const float mine = u4 ? b[2 + i] : b[i];
+    c[i] = mine + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  const bool u2 = lane & 2;
+  const float send = u2 ? c[0] : c[1];
+  const float mine = u2 ? c[1] : c[0];
+  float d = mine + __shfl_xor_sync(0xffffffffu, send, 2);
+  return d + __shfl_xor_sync(0xffffffffu, d, 1);
+}
+
+struct PxB2 {
+  float T, T_final, dC0, dC1, dC2, acc0, acc1, acc2, last_alpha, lc0, lc1, lc2, bgdot;
+  int n;
+};
+
+__global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
+    R2Args a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
+    const float* __restrict__ image, const float* __restrict__ final_T, const int32_t* __restrict__ n_contrib,
+    const float* __restrict__ grad_image, const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view,
+    float* __restrict__ g_sp) {
+  __shared__ Warp2 smem[kW2];
+  const int slot = blockIdx.z, tile = blockIdx.y * a.tiles_x + blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Warp2& s = smem[w];
+  const int rx = blockIdx.x * BS_TILE + (w & 1) * 8, ry = blockIdx.y * BS_TILE + (w >> 1) * 4;
+  const int px = rx + (lane & 7), py = ry + (lane >> 3);
+  const float x0 = rx + 0.5f, x1 = x0 + 7.f, y0 = ry + 0.5f, y1 = y0 + 3.f;
+  const float pxf = px + 0.5f, pyf = py + 0.5f;
+  const bool inside = px < a.W && py < a.H;
+  const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
+  PxB2 q;
+  q.T = 1.f;
+  q.n = 0;
+  q.dC0 = q.dC1 = q.dC2 = 0.f;
+  if (inside) {
+    const int64_t pix = ((int64_t)slot * a.H + py) * a.W + px;
+    q.T = final_T[pix];
+    q.n = n_contrib[pix];
+    if (grad_image) {
+      q.dC0 = grad_image[3 * pix];
+      q.dC1 = grad_image[3 * pix + 1];
+      q.dC2 = grad_image[3 * pix + 2];
+    } else {
+      const int gv = gt_view ? gt_view[slot] : slot;
+      const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py) * a.W + px);
+      const float d0 = image[3 * pix] - gp[0] * (1.f / 255.f);
+      const float d1 = image[3 * pix + 1] - gp[1] * (1.f / 255.f);
+      const float d2 = image[3 * pix + 2] - gp[2] * (1.f / 255.f);
+      q.dC0 = (d0 > 0.f ? 1.f : (d0 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+      q.dC1 = (d1 > 0.f ? 1.f : (d1 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+      q.dC2 = (d2 > 0.f ? 1.f : (d2 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+    }
+  }
+  q.T_final = q.T;
+  q.bgdot = a.bg[0] * q.dC0 + a.bg[1] * q.dC1 + a.bg[2] * q.dC2;
+  q.acc0 = q.acc1 = q.acc2 = q.last_alpha = q.lc0 = q.lc1 = q.lc2 = 0.f;
+  int warp_n = q.n;
+  for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
+  const int end = rg.x + warp_n;
+  Splat2 f;
+  fetch2(f, sp, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
+  for (int cend = end; cend > rg.x; cend -= 32) {
+    const bool keep = reaches2(f, x0, x1, y0, y1);
+    uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if (keep) stage2(s, lane, f);
+    fetch2(f, sp, inst_rows, cend - 33 - lane, cend - 33 - lane >= rg.x);
+    __syncwarp();
+    while (bits) {
+      const int j = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int rel = cend - 1 - j - rg.x;
+      float g[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) g[k] = 0.f;
+      bool any = false;
+      if (rel < q.n) {
+        const float4 sa = s.a[j];
+        Eval2 e;
+        eval2(sa, s.b[j], s.c[j], pxf, pyf, e);
+        if (e.ok && e.power <= 0.f) {
+          const float ex = __expf(e.power);
+          const float raw = __fmul_rn(sa.z, ex);
+          const float alpha = fminf(kAMax, raw);
+          if (alpha >= kAMin) {
+            any = true;
+            const float4 col = s.d[j];
+            const float ra = __fdividef(1.f, 1.f - alpha);
+            q.T = q.T * ra;
+            const float fac = alpha * q.T;
+            g[12] = fac * q.dC0;
+            g[13] = fac * q.dC1;
+            g[14] = fac * q.dC2;
+            q.acc0 = q.last_alpha * q.lc0 + (1.f - q.last_alpha) * q.acc0;
+            q.acc1 = q.last_alpha * q.lc1 + (1.f - q.last_alpha) * q.acc1;
+            q.acc2 = q.last_alpha * q.lc2 + (1.f - q.last_alpha) * q.acc2;
+            q.last_alpha = alpha;
+            q.lc0 = col.x;
+            q.lc1 = col.y;
+            q.lc2 = col.z;
+            float dLda = q.T * ((col.x - q.acc0) * q.dC0 + (col.y - q.acc1) * q.dC1 + (col.z - q.acc2) * q.dC2);
+            dLda -= q.T_final * ra * q.bgdot;
+            if (raw <= kAMax) {
+              const float dpow = dLda * alpha;
+              g[11] = dLda * ex;
+              if (e.g3 <= e.g2) {
+                // power = -0.5 (u^2 + v^2)
+                const float gu = -e.u * dpow, gv = -e.v * dpow;
+                const float iz = 1.f / e.z[2];
+                const float gz0 = gu * iz, gz1 = gv * iz, gz2 = -(gu * e.z[0] + gv * e.z[1]) * iz * iz;
+                // zeta = hx x hy: d/dhx = hy x gz, d/dhy = gz x hx
+                const float ghx0 = e.hy[1] * gz2 - e.hy[2] * gz1;
+                const float ghx1 = e.hy[2] * gz0 - e.hy[0] * gz2;
+                const float ghx2 = e.hy[0] * gz1 - e.hy[1] * gz0;
+                const float ghy0 = gz1 * e.hx[2] - gz2 * e.hx[1];
+                const float ghy1 = gz2 * e.hx[0] - gz0 * e.hx[2];
+                const float ghy2 = gz0 * e.hx[1] - gz1 * e.hx[0];
+                g[2] = ghx0;
+                g[3] = ghx1;
+                g[4] = ghx2;
+                g[5] = ghy0;
+                g[6] = ghy1;
+                g[7] = ghy2;
+                g[8] = -(pxf * ghx0 + pyf * ghy0);
+                g[9] = -(pxf * ghx1 + pyf * ghy1);
+                g[10] = -(pxf * ghx2 + pyf * ghy2);
+              } else {
+                // power = -(dx^2 + dy^2), dx = u - px
+                g[0] = -2.f * e.dx * dpow;
+                g[1] = -2.f * e.dy * dpow;
+              }
+            }
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, any)) {
+        const float r = warp_reduce16(g);
+        const int idx = lane >> 1;
+        if ((lane & 1) == 0 && idx < kGSP2) atomicAdd(g_sp + (int64_t)s.row[j] * kGSP2 + idx, r);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+int32_t make_r2(const bs_raster_desc* d, R2Args& a) {
+  BS_REQUIRE(d != nullptr, BS_ERR_PARAMETER, "null raster descriptor");
+  BS_REQUIRE(d->width >= 1 && d->height >= 1, BS_ERR_PARAMETER, "image size must be >= 1 pixel");
+  BS_REQUIRE(d->n_slots >= 1 && d->n_slots <= 65535, BS_ERR_PARAMETER, "bad slot count");
+  a.n_slots = d->n_slots;
+  a.W = d->width;
+  a.H = d->height;
+  a.tiles_x = (d->width + BS_TILE - 1) / BS_TILE;
+  const int tiles_y = (d->height + BS_TILE - 1) / BS_TILE;
+  BS_REQUIRE(d->tiles_per_slot >= a.tiles_x * tiles_y, BS_ERR_PARAMETER, "tiles_per_slot too small");
+  a.tiles_per_slot = d->tiles_per_slot;
+  a.bg[0] = d->bg[0];
+  a.bg[1] = d->bg[1];
+  a.bg[2] = d->bg[2];
+  a.loss_fused = d->loss_fused;
+  a.inv_norm = (float)(1.0 / (3.0 * (double)d->width * (double)d->height));
+  return BS_OK;
+}
+
+}  // namespace
+}  // namespace bs
+
+using namespace bs;
+
+extern "C" int32_t bs_raster2d_fwd(const bs_raster_desc* d, const float* sp_rows, const uint32_t* inst_rows,
+                                   const int32_t* ranges, float* image, float* final_T, int32_t* n_contrib,
+                                   const uint8_t* gt, const int32_t* gt_slot_view, float* loss_tiles, void* stream) {
+  R2Args a;
+  int32_t st = make_r2(d, a);
+  if (st) return st;
+  BS_REQUIRE(!a.loss_fused || (gt && loss_tiles), BS_ERR_PARAMETER, "fused loss needs gt and loss_tiles");
+  const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
+  raster2d_fwd_kernel<<<grid, kT2, 0, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges),
+                                                          image, final_T, n_contrib, gt, gt_slot_view, loss_tiles);
+  BS_LAUNCH_CHECK("raster2d_fwd_kernel");
+  return BS_OK;
+}
+
+extern "C" int32_t bs_raster2d_bwd(const bs_raster_desc* d, const float* sp_rows, const uint32_t* inst_rows,
+                                   const int32_t* ranges, const float* image, const float* final_T,
+                                   const int32_t* n_contrib, const float* grad_image, const uint8_t* gt,
+                                   const int32_t* gt_slot_view, float* g_sp, void* stream) {
+  R2Args a;
+  int32_t st = make_r2(d, a);
+  if (st) return st;
+  BS_REQUIRE(grad_image || (image && gt), BS_ERR_PARAMETER, "raster_bwd needs grad_image or (image, gt)");
+  const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
+  raster2d_bwd_kernel<<<grid, kT2, 0, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges),
+                                                          image, final_T, n_contrib, grad_image, gt, gt_slot_view,
+                                                          g_sp);
+  BS_LAUNCH_CHECK("raster2d_bwd_kernel");
+  return BS_OK;
+}

@@ -101,8 +101,16 @@ class SplatTrainer:
 
     def __init__(self, params: np.ndarray, group_begin: np.ndarray, aabb: np.ndarray, views, gt=None,
                  sh_degree: int = 3, adam: AdamConfig | None = None, device=None, comm=None,
-                 bg=(0.0, 0.0, 0.0)):
+                 bg=(0.0, 0.0, 0.0), model: str = "3dgs"):
         nat.load()
+        if model not in ("3dgs", "2dgs"):
+            raise ValueError(f"unknown splat model {model!r} (3dgs | 2dgs)")
+        self.model = model
+        self.model_id = nat.MODEL_2DGS if model == "2dgs" else nat.MODEL_3DGS
+        self.sp_floats = nat.SP2_FLOATS if model == "2dgs" else nat.SP_FLOATS
+        self.gsp_floats = nat.GSP2_FLOATS if model == "2dgs" else nat.GSP_FLOATS
+        self._raster = ("bs_raster2d_fwd", "bs_raster2d_bwd") if model == "2dgs" else ("bs_raster_fwd",
+                                                                                      "bs_raster_bwd")
         self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.S = int(params.shape[1])
         self.params = torch.as_tensor(np.ascontiguousarray(params, dtype=np.float32), device=self.dev)
@@ -198,8 +206,8 @@ class SplatTrainer:
         n_rows = int(rows_host.sum())
         self.last["rows_per_view"] = rows_host.copy()
         # ---- K1: projection into SP rows (send layout)
-        sp = self.buf.get("sp", max(n_rows, 1) * nat.SP_FLOATS, torch.float32)
-        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y)
+        sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
+        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id)
         with self._t("project"):
             nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask), nat.ptr(self.group_begin),
                      self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(sp), st)
@@ -212,7 +220,7 @@ class SplatTrainer:
         else:
             # SP all-to-all to the rendering ranks (line 9), render, G_SP back (line 21)
             with self._t("a2a_fwd"):
-                sp_recv = self.comm.forward(sp[: n_rows * nat.SP_FLOATS], lay, nat.SP_FLOATS)
+                sp_recv = self.comm.forward(sp[: n_rows * self.sp_floats], lay, self.sp_floats)
             mine = torch.as_tensor(lay.my_views, device=dev)
             seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(lay.seg_rows)[:-1]]).astype(np.int64),
                                        device=dev)
@@ -224,7 +232,8 @@ class SplatTrainer:
                                                          len(lay.my_views), cams.index_select(0, mine).contiguous(),
                                                          bidx.index_select(0, mine), gt_slots)
             with self._t("a2a_bwd"):
-                gsp = self.comm.backward(gsp_recv[: lay.n_recv * nat.GSP_FLOATS], lay, nat.GSP_FLOATS).reshape(-1)
+                gsp = self.comm.backward(gsp_recv[: lay.n_recv * self.gsp_floats], lay,
+                                         self.gsp_floats).reshape(-1)
         # ---- K1b + K5: projection backward fused with Adam
         self.step_count += 1
         ad = nat.AdamDesc()
@@ -245,7 +254,7 @@ class SplatTrainer:
         nb = n_slots * self.tiles
         counts = self.buf.get("bucket_counts", nb, torch.int32)
         nat.call("bs_bin_tiles_count", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
-                 nat.ptr(slot_cams), self.tiles, nb, nat.ptr(counts), st)
+                 nat.ptr(slot_cams), self.tiles, nb, nat.ptr(counts), self.model_id, st)
         ranges = self.buf.get("ranges", nb * 2, torch.int32)
         cursor = self.buf.get("cursor", nb, torch.int32)
         stats = self.buf.get("bin_stats", 2, torch.int64)
@@ -256,7 +265,7 @@ class SplatTrainer:
         keys = self.buf.get("inst_keys", max(n_inst, 1), torch.int64)
         irows = self.buf.get("irows", max(n_inst, 1), torch.int32)
         nat.call("bs_bin_tiles_scatter", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
-                 nat.ptr(slot_cams), self.tiles, nat.ptr(cursor), nat.ptr(keys), st)
+                 nat.ptr(slot_cams), self.tiles, nat.ptr(cursor), nat.ptr(keys), self.model_id, st)
         cap = min(self.sort_cap, lib.bs_bin_tiles_max_sort())
         nat.call("bs_bin_tiles_sort", nat.ptr(keys), nat.ptr(ranges), nb, cap, nat.ptr(irows), st)
         if biggest > cap:  # rare: buckets beyond the shared-memory sort
@@ -309,6 +318,8 @@ class SplatTrainer:
         # ---- K2: binning
         with self._t("bin"):
             if self.binning == "radix":
+                if self.model != "3dgs":
+                    raise ValueError("the radix binning pipeline reads 3DGS rows only; use binning='bucket'")
                 n_inst, irows, ranges = self._bin_radix(sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams)
             else:
                 n_inst, irows, ranges = self._bin_buckets(sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams)
@@ -327,15 +338,15 @@ class SplatTrainer:
             gt = self.gt
             gt_map = gt_views.to(torch.int32)
         with self._t("raster_fwd"):
-            nat.call("bs_raster_fwd", rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
+            nat.call(self._raster[0], rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
                      nat.ptr(final_T), nat.ptr(n_contrib), nat.ptr(gt), nat.ptr(gt_map), nat.ptr(loss_tiles), st)
         losses = self.buf.get("losses", n_slots, torch.float32)
         nat.call("bs_reduce_loss_tiles", nat.ptr(loss_tiles), n_slots, self.tiles, self.H, self.W, nat.ptr(losses), st)
         # ---- K4: backward
-        gsp = self.buf.get("gsp", max(n_rows, 1) * nat.GSP_FLOATS, torch.float32)
+        gsp = self.buf.get("gsp", max(n_rows, 1) * self.gsp_floats, torch.float32)
         gsp.zero_()
         with self._t("raster_bwd"):
-            nat.call("bs_raster_bwd", rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
+            nat.call(self._raster[1], rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
                      nat.ptr(final_T), nat.ptr(n_contrib), None, nat.ptr(gt), nat.ptr(gt_map), nat.ptr(gsp), st)
         self.last.update(image=image, final_T=final_T, n_contrib=n_contrib, ranges=ranges, irows=irows,
                          sp=sp, gsp=gsp)
