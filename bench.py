@@ -39,6 +39,10 @@ CONFIGS = {
     # configs[0]: CPU-oracle-sized case
     "c1": dict(seed=0, n_points=10_000, grid=(2, 2), n_views=8, altitude=50.0, image_size=(128, 128),
                batch=1, G=2048, desc="synthetic 3DGS scene, 10K Gaussians, 8 cameras at 128x128, batch 1"),
+    # configs[2]: 2DGS (surfels), 2M points, 1080p, batch 4
+    "c3": dict(seed=2, n_points=2_000_000, grid=(1, 1), n_views=8, altitude=50.0, image_size=(1920, 1080),
+               batch=4, G=2048, model="2dgs",
+               desc="synthetic 2DGS aerial scene, 2M surfels, 1080p cameras, batch 4"),
 }
 METRIC = "train images/s (fwd+bwd) at 1/2/4/8 B200, % HBM roofline; comm bytes/step"
 
@@ -166,7 +170,7 @@ def shard_for_rank(ds, g, params, world, rank):
     return np.ascontiguousarray(params[:, pts, :]), gb, aabb, info
 
 
-def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps):
+def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps, row_bytes=48, grad_bytes=36):
     """All-to-all bytes per step: moved by NCCL (summed over ranks),
     A-predicted (account_iteration on topology (N, 1)), and the same
     accounting for the RandomStrategy baseline on the same batches."""
@@ -180,26 +184,27 @@ def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps):
     torch.distributed.all_reduce(t)
     fwd, bwd = (float(x) / steps for x in t.tolist())
     topo = ClusterTopology(world, 1, 25e9, 300e9)
-    pred = np.mean([account_iteration(A, __import__("paper_2512_20017_b200").PlacementSolution(W, world), topo, 48)
-                    .send_inter.sum() for A, W in step_AW]) * 48
+    pred = np.mean([account_iteration(A, __import__("paper_2512_20017_b200").PlacementSolution(W, world), topo,
+                                      row_bytes).send_inter.sum() for A, W in step_AW]) * row_bytes
     rnd_pg = random_point_gpus(len(ds.cloud), world,
                                np.random.default_rng(np.random.SeedSequence([5, 17])))[g.permutation]
     rnd = []
     for it, b in enumerate(batches):
         A = build_access_matrix(g, rnd_pg, [ds.views[v] for v in b], 1)
         sol = random_placement(len(b), world, np.random.default_rng(np.random.SeedSequence([5, 3, it])))
-        rnd.append(account_iteration(A, sol, topo, 48).send_inter.sum() * 48)
+        rnd.append(account_iteration(A, sol, topo, row_bytes).send_inter.sum() * row_bytes)
     rnd = float(np.mean(rnd))
     return {"fwd_bytes_per_step": fwd, "bwd_bytes_per_step": bwd, "fwd_bytes_predicted": float(pred),
             "random_fwd_bytes_per_step": rnd, "reduction_vs_random_pct": 100.0 * (1.0 - fwd / rnd) if rnd else None,
-            "row_bytes": {"fwd": 48, "bwd": 36}}
+            "row_bytes": {"fwd": row_bytes, "bwd": grad_bytes}}
 
 
 _STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_kernel",
+                 "raster2d_bwd": "raster2d_bwd_kernel", "raster2d_fwd": "raster2d_fwd_kernel",
                  "project_bwd_adam": "project_bwd_adam_kernel", "project": "project_fwd_kernel", "cull": "cull_kernel"}
 
 
-def kernel_traffic(stage):
+def kernel_traffic(stage, model="3dgs"):
     """DRAM bytes (read + write) of one launch of the stage's kernel from the
     committed ncu --set full summary of the same configuration, or None."""
     path = os.path.join(ROOT, "profiles", "r1_kernel_traffic.json")
@@ -207,25 +212,30 @@ def kernel_traffic(stage):
         table = json.load(open(path))
     except Exception:
         return None
-    prefix = _STAGE_KERNEL.get(stage, stage)
+    key = stage.replace("raster_", "raster2d_") if model == "2dgs" and stage.startswith("raster_") else stage
+    prefix = _STAGE_KERNEL.get(key, key)
     for k, v in table.items():
         if k.startswith(prefix):
             return v.get("dram_traffic_bytes")
     return None
 
 
-def kernel_bytes(stage, last, S, B):
-    """Algorithmic (compulsory) bytes of one launch of a stage."""
+def kernel_bytes(stage, last, S, B, model="3dgs"):
+    """Algorithmic (compulsory) bytes of one launch of a stage.
+    Per instance: list entry 4 B + the splat fields the rasteriser gathers
+    (3DGS 36 B: mean, opacity, conic, rgb; 2DGS 64 B: mean, opacity, M, rgb, depth);
+    per row: SP write (48 / 96 B) and G_SP (36 / 60 B)."""
     I, V, slots = last["n_inst"], last["n_rows"], last["n_slots"]
     npx = slots * last["H"] * last["W"]
-    if stage == "raster_fwd":   # instance list (4 B) + gathered splat (36 B); image 12 + T 4 + n 4 B/px + gt 3 B/px
-        return 40 * I + 23 * npx
-    if stage == "raster_bwd":   # same reads + image/gt re-read + 9 f32 atomics per splat
-        return 40 * I + 23 * npx + 36 * V
-    if stage == "project":      # 240 B params per visible point (once) + mask + 48 B per row
-        return 240 * last["n_visible_points"] + 4 * S + 48 * V
-    if stage == "project_bwd_adam":  # params/m/v read+write (60 f32 each) + mask + 36 B G_SP per row
-        return 6 * 240 * S + 4 * S + 36 * V
+    per_inst, sp_row, gsp_row = (68, 96, 60) if model == "2dgs" else (40, 48, 36)
+    if stage == "raster_fwd":   # instance list + gathered splat; image 12 + T 4 + n 4 B/px + gt 3 B/px
+        return per_inst * I + 23 * npx
+    if stage == "raster_bwd":   # same reads + image/gt re-read + one f32 atomic per G_SP term per splat
+        return per_inst * I + 23 * npx + gsp_row * V
+    if stage == "project":      # 240 B params per visible point (once) + mask + SP row
+        return 240 * last["n_visible_points"] + 4 * S + sp_row * V
+    if stage == "project_bwd_adam":  # params/m/v read+write (60 f32 each) + mask + G_SP per row
+        return 6 * 240 * S + 4 * S + gsp_row * V
     if stage == "cull":
         return 16 * S + 4 * S
     return None
@@ -259,8 +269,9 @@ def run_ours(args, cfg):
     setup_s = time.time() - t0
     W, H = cfg["image_size"]
     B = cfg["batch"] * world
+    model = cfg.get("model", "3dgs")
     tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt, adam=AdamConfig(scenes.lr_table(cfg["altitude"])),
-                      comm=comm)
+                      comm=comm, model=model)
     sched = schedule(cfg["n_views"], B, args.warmup + 2 * args.steps + 2)
     # clocks are sampled from the start of the warm-up to the end of the timed
     # region (nvidia-smi needs ~0.5 s to start streaming)
@@ -307,7 +318,8 @@ def run_ours(args, cfg):
     comm_report = None
     if comm is not None:
         comm_report = comm_bytes_report(comm, step_AW, sched[args.warmup:args.warmup + args.steps], ds, g,
-                                        world, rank, args.steps)
+                                        world, rank, args.steps, row_bytes=4 * tr.sp_floats,
+                                        grad_bytes=4 * tr.gsp_floats)
     # ---- e2e: public API with pinned host ground truth, loss read back
     # the step's ground-truth images are copied from pinned host memory on a
     # side stream, double-buffered: step i+1's upload overlaps step i
@@ -357,16 +369,17 @@ def run_ours(args, cfg):
     dom = max(stage_ms, key=stage_ms.get) if stage_ms else None
     roof = None
     if dom:
-        nbytes = kernel_bytes(dom, dict(last, n_inst=int(np.mean(inst)), n_rows=int(np.mean(rows))), tr.S, B)
+        nbytes = kernel_bytes(dom, dict(last, n_inst=int(np.mean(inst)), n_rows=int(np.mean(rows))), tr.S, B,
+                              model)
         ach = nbytes / (stage_ms[dom] / 1000.0) / 1e9 if nbytes else None
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": kernel_traffic(dom), "peak_kind": peak_kind,
+                "frac": (ach / peak) if ach else None, "traffic": kernel_traffic(dom, model), "peak_kind": peak_kind,
                 "bytes_per_launch": nbytes, "ms_per_launch": stage_ms[dom],
                 "note": "raster kernels are FP32/issue-bound (ncu: issue slots ~80-90% busy), not HBM-bound; "
                         "traffic = ncu dram read+write bytes of one launch (profiles/r1_kernel_traffic.json)"}
     stages = {}
     for k, v in stage_ms.items():
-        nb = kernel_bytes(k, dict(last, n_inst=int(np.mean(inst)), n_rows=int(np.mean(rows))), tr.S, B)
+        nb = kernel_bytes(k, dict(last, n_inst=int(np.mean(inst)), n_rows=int(np.mean(rows))), tr.S, B, model)
         stages[k] = {"ms": round(v, 4), "share": round(v / ms_per_step, 4),
                      "gbs": round(nb / (v / 1000.0) / 1e9, 1) if nb else None}
     cpu = None
@@ -377,8 +390,8 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": round(value, 3), "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "n_points": cfg["n_points"], "image": list(cfg["image_size"]),
-                       "global_batch": B, "views": cfg["n_views"], "group_size": cfg["G"],
+            "config": {"workload": cfg["desc"], "primitive": model, "n_points": cfg["n_points"],
+                       "image": list(cfg["image_size"]), "global_batch": B, "views": cfg["n_views"], "group_size": cfg["G"],
                        "parallelism": f"points+images x{world}",
                        "l2": "inputs larger than L2 (params+Adam state %.0f MB/rank)" % (3 * tr.params.numel() * 4 / 1e6)},
             "e2e": {"value": round(e2e_value, 3), "unit": "images/s", "h2d_bytes_per_step": B * H * W * 3 * world,
@@ -411,15 +424,16 @@ def cpu_baseline(cfg, ds, g, params, gt, steps=1, warmup=0):
     m = np.zeros_like(p)
     v = np.zeros_like(p)
     lr = scenes.lr_table(cfg["altitude"])
+    model = cfg.get("model", "3dgs")
     views = [ds.views[i % len(ds.views)] for i in range(steps + warmup)]
     for k in range(warmup):
-        py_oracle.train_step(p, m, v, batch_planes([views[k]], 1), camera_bytes([views[k]]), gt[views[k].id:views[k].id + 1],
-                             3, lr, 0.9, 0.999, 1e-15, k + 1)
+        py_oracle.train_step(p, m, v, batch_planes([views[k]], 1), camera_bytes([views[k]]),
+                             gt[views[k].id:views[k].id + 1], 3, lr, 0.9, 0.999, 1e-15, k + 1, model=model)
     t0 = time.perf_counter()
     for k in range(warmup, warmup + steps):
         vv = views[k]
         py_oracle.train_step(p, m, v, batch_planes([vv], 1), camera_bytes([vv]), gt[vv.id:vv.id + 1], 3, lr, 0.9,
-                             0.999, 1e-15, k + 1)
+                             0.999, 1e-15, k + 1, model=model)
     dt = time.perf_counter() - t0
     return {"value": round(steps / dt, 5), "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"{steps} step(s) x 1 view of the same scene ({cfg['n_points']} Gaussians, "
@@ -437,8 +451,8 @@ def run_reference(args, cfg):
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1000.0 / cpu["value"], 2), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "n_points": cfg["n_points"], "image": list(cfg["image_size"]),
-                       "global_batch": cfg["batch"]},
+            "config": {"workload": cfg["desc"], "primitive": cfg.get("model", "3dgs"), "n_points": cfg["n_points"],
+                       "image": list(cfg["image_size"]), "global_batch": cfg["batch"]},
             "cpu_baseline": cpu,
             "e2e": {"value": cpu["value"], "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
