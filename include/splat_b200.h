@@ -187,6 +187,9 @@ typedef struct {
   int32_t sh_degree; /* 0..3 */
   int32_t tiles_x_max, tiles_y_max;
   int32_t model;     /* BS_MODEL_3DGS (default) or BS_MODEL_2DGS */
+  int32_t max_group_points; /* largest group size; > 0 lets the per-point
+                               kernels split a group over several CTAs (one
+                               per 256 points), 0 = one CTA per group */
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,

@@ -1,0 +1,50 @@
+"""K2 tile binning through the bucket pipeline (csrc/bin_tiles.cu), shared by
+the training-step executor (trainer.py) and the UDF wrappers (udf.py).
+
+The lists equal a stable depth sort of the splat rows followed by a stable
+sort by (slot, tile) ("sorts ... splats by their distance"):
+per tile ascending depth, ties in row order."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+
+def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, model_id=nat.MODEL_3DGS,
+                sort_cap=4096):
+    """Atomics into (slot, tile) buckets, then a shared-memory sort of every
+    bucket by (depth, row); buckets larger than the in-SM sort go through the
+    device radix sort.  `buf` is a grow-only buffer cache with
+    get(name, n, dtype).  Returns (n_inst, inst_rows, ranges, largest bucket)."""
+    st, lib = nat.stream_handle(), nat.load()
+    nb = n_slots * tiles
+    counts = buf.get("bucket_counts", nb, torch.int32)
+    nat.call("bs_bin_tiles_count", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
+             nat.ptr(slot_cams), tiles, nb, nat.ptr(counts), model_id, st)
+    ranges = buf.get("ranges", nb * 2, torch.int32)
+    cursor = buf.get("cursor", nb, torch.int32)
+    stats = buf.get("bin_stats", 2, torch.int64)
+    ows = buf.get("offsets_ws", lib.bs_bin_tiles_offsets_workspace(nb), torch.uint8)
+    nat.call("bs_bin_tiles_offsets", nat.ptr(counts), nb, nat.ptr(ranges), nat.ptr(cursor), nat.ptr(stats),
+             nat.ptr(ows), ows.numel(), st)
+    n_inst, biggest = (int(x) for x in stats.cpu().tolist())  # sizes the instance buffers
+    keys = buf.get("inst_keys", max(n_inst, 1), torch.int64)
+    irows = buf.get("irows", max(n_inst, 1), torch.int32)
+    nat.call("bs_bin_tiles_scatter", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
+             nat.ptr(slot_cams), tiles, nat.ptr(cursor), nat.ptr(keys), model_id, st)
+    cap = min(sort_cap, lib.bs_bin_tiles_max_sort())
+    nat.call("bs_bin_tiles_sort", nat.ptr(keys), nat.ptr(ranges), nb, cap, nat.ptr(irows), st)
+    if biggest > cap:  # rare: buckets beyond the shared-memory sort
+        from .culling import radix_sort_u64
+
+        rg = ranges.view(-1, 2).cpu().numpy()
+        for b in np.flatnonzero(rg[:, 1] - rg[:, 0] > cap):
+            s0, s1 = int(rg[b, 0]), int(rg[b, 1])
+            k = keys[s0:s1]
+            v = torch.empty(s1 - s0, dtype=torch.int32, device=keys.device)
+            radix_sort_u64(k, v, 0, 64)
+            nat.call("bs_keys_low32", nat.ptr(k), s1 - s0, nat.ptr(irows[s0:s1]), st)
+    return n_inst, irows, ranges, biggest

@@ -49,6 +49,28 @@ struct RowRanker {
   }
 };
 
+// Point range of this CTA.  gridDim.y == 1: the whole group g.  Otherwise
+// chunk blockIdx.y (kProjThreads points) of g, with the ranker's running
+// per-view counts advanced over the group's earlier chunks first.  Returns
+// false (uniformly over the CTA) when the chunk lies past the group's end.
+__device__ __forceinline__ bool chunk_range(const int32_t* __restrict__ group_begin, const uint32_t* __restrict__ mask,
+                                            RowRanker& rk, int g, int B, int& lo, int& hi) {
+  const int begin = group_begin[g], end = group_begin[g + 1];
+  if (gridDim.y == 1) {
+    lo = begin;
+    hi = end;
+    return true;
+  }
+  lo = begin + (int)blockIdx.y * kProjThreads;
+  if (lo >= end) return false;
+  hi = min(end, lo + kProjThreads);
+  for (int b = begin; b < lo; b += kProjThreads) {
+    rk.round(mask[b + threadIdx.x], B);
+    rk.advance(B);
+  }
+  return true;
+}
+
 struct ProjArgs {
   int B, n_sh;
   const float4* params;
@@ -106,8 +128,9 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
   }
   __syncthreads();
   RowRanker rk{s_bal, s_run};
-  const int begin = a.group_begin[g], end = a.group_begin[g + 1];
-  for (int b0 = begin; b0 < end; b0 += kProjThreads) {
+  int lo, end;
+  if (!chunk_range(a.group_begin, a.mask, rk, g, B, lo, end)) return;
+  for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const uint32_t mask = i < end ? a.mask[i] : 0u;
     rk.round(mask, B);
@@ -164,8 +187,9 @@ __global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, c
   }
   __syncthreads();
   RowRanker rk{s_bal, s_run};
-  const int begin = a.group_begin[g], end = a.group_begin[g + 1];
-  for (int b0 = begin; b0 < end; b0 += kProjThreads) {
+  int lo, end;
+  if (!chunk_range(a.group_begin, a.mask, rk, g, B, lo, end)) return;
+  for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const uint32_t mask = i < end ? a.mask[i] : 0u;
     rk.round(mask, B);
@@ -249,8 +273,9 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
   }
   __syncthreads();
   RowRanker rk{s_bal, s_run};
-  const int begin = a.group_begin[g], end = a.group_begin[g + 1];
-  for (int b0 = begin; b0 < end; b0 += kProjThreads) {
+  int lo, end;
+  if (!chunk_range(a.group_begin, a.mask, rk, g, B, lo, end)) return;
+  for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const bool ok = i < end;
     const uint32_t mask = ok ? a.mask[i] : 0u;
@@ -272,17 +297,30 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
         point_backward<M>(a, s_cam, s_row0, rk, mask, pt, sh, gsp, g12,
                        [&](int f, float val) { my_sh[f * kProjThreads] += val; });
       }
+      // Adam over the 15 planes, 3 planes per batch: all 15 loads of a batch
+      // are issued before its first store (memory-level parallelism)
 #pragma unroll
-      for (int p = 0; p < BS_PARAM_PLANES; ++p) {
-        const int64_t t = p * a.S + i;
-        float4 pp = params[t], mm = m[t], vv = v[t];
-        const float4 gg = p < 3 ? make_float4(g12[4 * p], g12[4 * p + 1], g12[4 * p + 2], g12[4 * p + 3])
-                                : make_float4(my_sh[(4 * p - 12) * kProjThreads], my_sh[(4 * p - 11) * kProjThreads],
-                                              my_sh[(4 * p - 10) * kProjThreads], my_sh[(4 * p - 9) * kProjThreads]);
-        adam4(pp, gg, mm, vv, c, p);
-        params[t] = pp;
-        m[t] = mm;
-        v[t] = vv;
+      for (int p0 = 0; p0 < BS_PARAM_PLANES; p0 += 3) {
+        float4 pp[3], mm[3], vv[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int64_t t = (p0 + k) * a.S + i;
+          pp[k] = params[t];
+          mm[k] = m[t];
+          vv[k] = v[t];
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int p = p0 + k;
+          const int64_t t = p * a.S + i;
+          const float4 gg = p < 3 ? make_float4(g12[4 * p], g12[4 * p + 1], g12[4 * p + 2], g12[4 * p + 3])
+                                  : make_float4(my_sh[(4 * p - 12) * kProjThreads], my_sh[(4 * p - 11) * kProjThreads],
+                                                my_sh[(4 * p - 10) * kProjThreads], my_sh[(4 * p - 9) * kProjThreads]);
+          adam4(pp[k], gg, mm[k], vv[k], c, p);
+          params[t] = pp[k];
+          m[t] = mm[k];
+          v[t] = vv[k];
+        }
       }
     }
     rk.advance(B);
@@ -343,7 +381,14 @@ int32_t check_proj(const bs_proj_desc* d) {
   BS_REQUIRE(d != nullptr, BS_ERR_PARAMETER, "null projection descriptor");
   BS_REQUIRE(d->n_views >= 1 && d->n_views <= kMaxViews, BS_ERR_PARAMETER, "projection supports 1..32 views");
   BS_REQUIRE(d->sh_degree >= 0 && d->sh_degree <= 3, BS_ERR_PARAMETER, "sh_degree must be in [0, 3]");
+  BS_REQUIRE(d->max_group_points >= 0 && d->max_group_points <= (1 << 24), BS_ERR_PARAMETER,
+             "max_group_points must be in [0, 2^24]");
   return BS_OK;
+}
+
+dim3 proj_grid(const bs_proj_desc* d, int n_groups) {
+  const int chunks = d->max_group_points > 0 ? (d->max_group_points + kProjThreads - 1) / kProjThreads : 1;
+  return dim3(n_groups, chunks);
 }
 
 AdamConsts make_adam(const bs_adam_desc* d) {
@@ -399,10 +444,11 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams};
+  const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
-    project_fwd_kernel<Model2><<<n_groups, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
+    project_fwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
   else
-    project_fwd_kernel<Model3><<<n_groups, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
+    project_fwd_kernel<Model3><<<grid, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
   BS_LAUNCH_CHECK("project_fwd_kernel");
   return BS_OK;
 }
@@ -417,11 +463,12 @@ extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, in
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams};
+  const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
-    project_bwd_kernel<Model2><<<n_groups, kProjThreads, 0, as_stream(stream)>>>(
+    project_bwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(
         a, g_sp, reinterpret_cast<float4*>(grad_params));
   else
-    project_bwd_kernel<Model3><<<n_groups, kProjThreads, 0, as_stream(stream)>>>(
+    project_bwd_kernel<Model3><<<grid, kProjThreads, 0, as_stream(stream)>>>(
         a, g_sp, reinterpret_cast<float4*>(grad_params));
   BS_LAUNCH_CHECK("project_bwd_kernel");
   return BS_OK;
@@ -456,7 +503,7 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   const size_t smem = sizeof(float) * 48 * kProjThreads;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<n_groups, kProjThreads, smem, as_stream(stream)>>>(a, c, g_sp, reinterpret_cast<float4*>(params),
+    kern<<<proj_grid(pd, n_groups), kProjThreads, smem, as_stream(stream)>>>(a, c, g_sp, reinterpret_cast<float4*>(params),
                                                              reinterpret_cast<float4*>(exp_avg),
                                                              reinterpret_cast<float4*>(exp_avg_sq));
   };

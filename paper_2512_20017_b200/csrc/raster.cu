@@ -2,13 +2,13 @@
 // loss (loss_fn) and K4 backward (image_render.backward,
 // PAPER.md:503).
 //
-// One CTA of 4 warps per 16x16 tile; warp w owns the 8x8 quadrant
-// (w & 1, w >> 1) and every lane two vertically adjacent pixels of it.  The
-// warps of a tile never synchronise with each other: each walks the tile's
+// One CTA per 16x16 tile.  With PPL pixels per lane (default 1) a warp owns
+// an 8 x 4*PPL pixel region and a tile holds 8 / PPL such warps.  The warps
+// of a tile never synchronise with each other: each walks the tile's
 // depth-sorted instance range in chunks of 32 on its own, gathering one SP
 // row per lane (the next chunk is prefetched into registers while the
 // current one is blended), keeps only the splats whose alpha >= 1/255
-// footprint can reach its quadrant (exact bounding box of the ellipse
+// footprint can reach its region (exact bounding box of the ellipse
 // o * exp(power) = 1/255, padded by 1%), compacts them with a ballot into
 // warp-private shared memory and blends them in depth order.  Per pixel
 // (centre (x + 0.5, y + 0.5)):
@@ -16,14 +16,17 @@
 //   alpha = min(0.99, opacity * exp(power)); skipped if power > 0 or
 //   alpha < 1/255; a pixel stops before the splat that would bring its
 //   transmittance below 1e-4 (standard 3DGS conventions).
-// The footprint filter only drops splats whose every alpha at the quadrant
+// The conic is staged pre-scaled by -log2(e)/2 (B by -log2(e)) so the
+// exponent is one ex2.approx; forward and backward evaluate alpha with the
+// same instructions, so their skip / stop decisions agree exactly.
+// The footprint filter only drops splats whose every alpha at the region
 // is below 1/255, so the blend equals walking the whole list.
 //
 // Backward: each warp walks its own range back to front from the deepest
-// contributor of its pixels (T recovered by division); per splat each lane
-// sums its two pixels' 9 gradient terms, the warp reduce-scatters the 9
-// sums in 12 shuffles and 9 lanes issue the atomicAdds (one RED instruction
-// per (quadrant, splat) pair).
+// contributor of its pixels (T recovered by division).  Per splat the lanes
+// that contribute are counted with a ballot: up to kSparseLanes of them add
+// their 9 gradient terms with direct REDs; otherwise the warp reduce-scatters
+// the 9 sums in 12 shuffles and 9 lanes issue one RED each.
 #include "common.cuh"
 
 namespace bs {
@@ -32,6 +35,15 @@ namespace {
 constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kAlphaMax = 0.99f;
 constexpr float kTMin = 1e-4f;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr int kSparseLanes = 3;  // contributing lanes handled with direct REDs
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 struct RastArgs {
   int n_slots, tiles_per_slot, W, H, tiles_x;
@@ -40,16 +52,16 @@ struct RastArgs {
   float inv_norm;  // 1 / (H * W * 3)
 };
 
-// Bit-identical in both kernels (explicit round-to-nearest intrinsics).
-// a = (u, v, conic_a, conic_b), cconic = conic_c.
-__device__ __forceinline__ float splat_power(float4 a, float cconic, float px, float py, float& dx, float& dy) {
+// log2(e) * power at a pixel from the pre-scaled conic
+// a = (u, v, kA, kB), kc: kA = -log2(e) A / 2, kB = -log2(e) B, kc = -log2(e) C / 2.
+// Explicit round-to-nearest intrinsics: identical in both kernels.
+__device__ __forceinline__ float splat_power2(float4 a, float kc, float px, float py, float& dx, float& dy) {
   dx = __fsub_rn(a.x, px);
   dy = __fsub_rn(a.y, py);
-  const float q = __fmaf_rn(a.z, __fmul_rn(dx, dx), __fmul_rn(cconic, __fmul_rn(dy, dy)));
-  return __fmaf_rn(-0.5f, q, -__fmul_rn(a.w, __fmul_rn(dx, dy)));
+  return __fmaf_rn(a.z, __fmul_rn(dx, dx), __fmaf_rn(kc, __fmul_rn(dy, dy), __fmul_rn(a.w, __fmul_rn(dx, dy))));
 }
 
-// Warp-private staging: a = (u, v, A, B), b = (C, opacity, r, g), c = b-channel
+// Warp-private staging: a = (u, v, kA, kB), b = (kC, opacity, r, g), c = b-channel
 struct WarpSmem {
   float4 a[32];
   float4 b[32];
@@ -90,8 +102,8 @@ __device__ __forceinline__ bool reaches(const Splat& f, float x0, float x1, floa
 }
 
 __device__ __forceinline__ void stage(WarpSmem& s, int lane, const Splat& f) {
-  s.a[lane] = make_float4(f.p0.x, f.p0.y, f.p0.w, f.p1.x);
-  s.b[lane] = make_float4(f.p1.y, f.p0.z, f.p1.z, f.p1.w);
+  s.a[lane] = make_float4(f.p0.x, f.p0.y, f.p0.w * (-0.5f * kLog2e), f.p1.x * -kLog2e);
+  s.b[lane] = make_float4(f.p1.y * (-0.5f * kLog2e), f.p0.z, f.p1.z, f.p1.w);
   s.c[lane] = f.b;
   s.row[lane] = f.row;
 }
@@ -126,9 +138,9 @@ struct PixelFwd {
 __device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float4& sb, float cb, float pxf, float pyf,
                                       int rel) {
   float dx, dy;
-  const float power = splat_power(sa, sb.x, pxf, pyf, dx, dy);
-  if (power > 0.f) return;
-  const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, __expf(power)));
+  const float power2 = splat_power2(sa, sb.x, pxf, pyf, dx, dy);
+  if (power2 > 0.f) return;
+  const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, ex2_approx(power2)));
   if (alpha < kAlphaMin) return;
   const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
   if (nT < kTMin) {
@@ -273,22 +285,21 @@ struct PixelBwd {
   int n;
 };
 
-// Gradient contribution of one splat at one pixel, added into g[9].
+// Gradient contribution of one splat at one pixel.  kAssign: writes all 9
+// terms of g when it returns true (g untouched otherwise); else adds into g.
+template <bool kAssign>
 __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const float4& sb, float cb, float pxf,
                                            float pyf, float g[9]) {
   float dx, dy;
-  const float power = splat_power(sa, sb.x, pxf, pyf, dx, dy);
-  if (power > 0.f) return false;
-  const float ex = __expf(power);
+  const float power2 = splat_power2(sa, sb.x, pxf, pyf, dx, dy);
+  if (power2 > 0.f) return false;
+  const float ex = ex2_approx(power2);
   const float raw = __fmul_rn(sb.y, ex);
   const float alpha = fminf(kAlphaMax, raw);
   if (alpha < kAlphaMin) return false;
   const float ra = __fdividef(1.f, 1.f - alpha);  // alpha <= 0.99: fast reciprocal is safe
   p.T = p.T * ra;
   const float fac = alpha * p.T;
-  g[6] += fac * p.dC0;
-  g[7] += fac * p.dC1;
-  g[8] += fac * p.dC2;
   p.acc0 = p.last_alpha * p.lc0 + (1.f - p.last_alpha) * p.acc0;
   p.acc1 = p.last_alpha * p.lc1 + (1.f - p.last_alpha) * p.acc1;
   p.acc2 = p.last_alpha * p.lc2 + (1.f - p.last_alpha) * p.acc2;
@@ -298,14 +309,22 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
   p.lc2 = cb;
   float dL_dalpha = p.T * ((sb.z - p.acc0) * p.dC0 + (sb.w - p.acc1) * p.dC1 + (cb - p.acc2) * p.dC2);
   dL_dalpha -= p.T_final * ra * p.bgdot;
-  if (raw > kAlphaMax) return true;  // clamped: colour gradient only
-  const float dpow = dL_dalpha * alpha;
-  g[2] += dL_dalpha * ex;
-  g[3] += -0.5f * dx * dx * dpow;
-  g[4] += -dx * dy * dpow;
-  g[5] += -0.5f * dy * dy * dpow;
-  g[0] += -(sa.z * dx + sa.w * dy) * dpow;
-  g[1] += -(sa.w * dx + sb.x * dy) * dpow;
+  // clamped alpha (raw > 0.99): colour gradient only
+  const float dpow = raw > kAlphaMax ? 0.f : dL_dalpha * alpha;  // dL / d power
+  // d power / d(u, v) = -(A dx + B dy, B dx + C dy) = (2 kA dx + kB dy, kB dx + 2 kC dy) ln 2
+  const float dpl = dpow * kLn2;
+  float t[9];
+  t[0] = (2.f * sa.z * dx + sa.w * dy) * dpl;
+  t[1] = (sa.w * dx + 2.f * sb.x * dy) * dpl;
+  t[2] = raw > kAlphaMax ? 0.f : dL_dalpha * ex;
+  t[3] = -0.5f * dx * dx * dpow;
+  t[4] = -dx * dy * dpow;
+  t[5] = -0.5f * dy * dy * dpow;
+  t[6] = fac * p.dC0;
+  t[7] = fac * p.dC1;
+  t[8] = fac * p.dC2;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) g[k] = kAssign ? t[k] : g[k] + t[k];
   return true;
 }
 
@@ -342,7 +361,7 @@ __device__ __forceinline__ void init_pixel_bwd(PixelBwd& q, const RastArgs& a, i
 }
 
 template <int PPL>
-__global__ void __launch_bounds__(Region<PPL>::kThreads, 768 / Region<PPL>::kThreads) raster_bwd_kernel(
+__global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768) / Region<PPL>::kThreads) raster_bwd_kernel(
     RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
     const float* __restrict__ image, const float* __restrict__ final_T, const int32_t* __restrict__ n_contrib,
     const float* __restrict__ grad_image, const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view,
@@ -380,19 +399,33 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, 768 / Region<PPL>::kThr
       bits &= bits - 1;
       const int rel = cend - 1 - j - rg.x;  // range-relative index of this splat
       float g[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) g[k] = 0.f;
       const float4 sa = s.a[j];
       const float4 sb = s.b[j];
       const float cb = s.c[j];
       bool any = false;
+      if constexpr (PPL == 1) {
+        if (rel < p[0].n) any = pixel_grad<true>(p[0], sa, sb, cb, pxf, (float)q.py0 + 0.5f, g);
+      } else {
 #pragma unroll
-      for (int k = 0; k < PPL; ++k)
-        if (rel < p[k].n) any |= pixel_grad(p[k], sa, sb, cb, pxf, (float)(q.py0 + k) + 0.5f, g);
-      if (__any_sync(0xffffffffu, any)) {
+        for (int k = 0; k < 9; ++k) g[k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < PPL; ++k)
+          if (rel < p[k].n) any |= pixel_grad<false>(p[k], sa, sb, cb, pxf, (float)(q.py0 + k) + 0.5f, g);
+      }
+      const uint32_t who = __ballot_sync(0xffffffffu, any);
+      if (who == 0u) continue;
+      float* dst = g_sp + (int64_t)s.row[j] * BS_GSP_FLOATS;
+      if (__popc(who) <= kSparseLanes) {
+        if (any) {
+#pragma unroll
+          for (int k = 0; k < 9; ++k) atomicAdd(dst + k, g[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) g[k] = any ? g[k] : 0.f;
         int idx;
         const float r = warp_reduce9(g, idx);
-        if (idx >= 0) atomicAdd(g_sp + (int64_t)s.row[j] * BS_GSP_FLOATS + idx, r);
+        if (idx >= 0) atomicAdd(dst + idx, r);
       }
     }
     __syncwarp();

@@ -12,8 +12,10 @@
 // L = 2 ln(255 o): the union of the bounding box of the image of the disk
 // u^2 + v^2 <= L (dual conic; unbounded -> keep) and the circle
 // |mean2d - pixel| <= sqrt(L / 2), padded by 1%.
-// Backward: 15 gradient terms per splat, reduce-scattered over the warp in
-// 16 shuffles, one RED per term per (region, splat).
+// Backward: 15 gradient terms per splat; up to 3 contributing lanes add them
+// with direct REDs, otherwise they are reduce-scattered over the warp in 16
+// shuffles and one RED per term is issued per (region, splat).  exp is one
+// ex2.approx in both kernels (identical skip / stop decisions).
 #include "splat2d_math.cuh"
 
 namespace bs {
@@ -24,6 +26,14 @@ constexpr int kT2 = 32 * kW2;
 constexpr float kAMin = 1.0f / 255.0f;
 constexpr float kAMax = 0.99f;
 constexpr float kTStop = 1e-4f;
+constexpr float kLog2e2 = 1.4426950408889634f;
+constexpr int kSparse2 = 3;  // contributing lanes handled with direct REDs
+
+__device__ __forceinline__ float ex2a(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 struct R2Args {
   int n_slots, tiles_per_slot, W, H, tiles_x;
@@ -169,7 +179,7 @@ __global__ void __launch_bounds__(kT2) raster2d_fwd_kernel(R2Args a, const float
       const float4 sa = s.a[j];
       eval2(sa, s.b[j], s.c[j], pxf, pyf, e);
       if (!e.ok || e.power > 0.f) continue;
-      const float alpha = fminf(kAMax, __fmul_rn(sa.z, __expf(e.power)));
+      const float alpha = fminf(kAMax, __fmul_rn(sa.z, ex2a(__fmul_rn(e.power, kLog2e2))));
       if (alpha < kAMin) continue;
       const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
       if (nT < kTStop) {
@@ -316,7 +326,7 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
         Eval2 e;
         eval2(sa, s.b[j], s.c[j], pxf, pyf, e);
         if (e.ok && e.power <= 0.f) {
-          const float ex = __expf(e.power);
+          const float ex = ex2a(__fmul_rn(e.power, kLog2e2));
           const float raw = __fmul_rn(sa.z, ex);
           const float alpha = fminf(kAMax, raw);
           if (alpha >= kAMin) {
@@ -370,10 +380,18 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
           }
         }
       }
-      if (__any_sync(0xffffffffu, any)) {
+      const uint32_t who = __ballot_sync(0xffffffffu, any);
+      if (who == 0u) continue;
+      float* dst = g_sp + (int64_t)s.row[j] * kGSP2;
+      if (__popc(who) <= kSparse2) {
+        if (any) {
+#pragma unroll
+          for (int k = 0; k < kGSP2; ++k) atomicAdd(dst + k, g[k]);
+        }
+      } else {
         const float r = warp_reduce16(g);
         const int idx = lane >> 1;
-        if ((lane & 1) == 0 && idx < kGSP2) atomicAdd(g_sp + (int64_t)s.row[j] * kGSP2 + idx, r);
+        if ((lane & 1) == 0 && idx < kGSP2) atomicAdd(dst + idx, r);
       }
     }
     __syncwarp();

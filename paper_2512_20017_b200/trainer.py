@@ -33,6 +33,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from .binning import bin_buckets
 from .culling import view_plane_block
 from .exchange import layout_for
 from .scenes import CameraView
@@ -119,6 +120,8 @@ class SplatTrainer:
         self.group_begin = torch.as_tensor(np.asarray(group_begin, dtype=np.int32), device=self.dev)
         self.aabb = torch.as_tensor(np.ascontiguousarray(aabb, dtype=np.float32).reshape(-1, 6), device=self.dev)
         self.n_groups = len(group_begin) - 1
+        gsz = np.diff(np.asarray(group_begin, dtype=np.int64))
+        self.max_group = int(gsz.max()) if len(gsz) else 0  # per-point kernels: one CTA per 256 points
         self.views = list(views)
         self.W, self.H = self.views[0].width, self.views[0].height
         if any((v.width, v.height) != (self.W, self.H) for v in self.views):
@@ -207,7 +210,7 @@ class SplatTrainer:
         self.last["rows_per_view"] = rows_host.copy()
         # ---- K1: projection into SP rows (send layout)
         sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
-        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id)
+        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group)
         with self._t("project"):
             nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask), nat.ptr(self.group_begin),
                      self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(sp), st)
@@ -248,35 +251,9 @@ class SplatTrainer:
         return losses
 
     def _bin_buckets(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams):
-        """Bucket pipeline (csrc/bin_tiles.cu): atomics into (slot, tile)
-        buckets, then a shared-memory sort of every bucket by (depth, row)."""
-        st, lib = nat.stream_handle(), nat.load()
-        nb = n_slots * self.tiles
-        counts = self.buf.get("bucket_counts", nb, torch.int32)
-        nat.call("bs_bin_tiles_count", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
-                 nat.ptr(slot_cams), self.tiles, nb, nat.ptr(counts), self.model_id, st)
-        ranges = self.buf.get("ranges", nb * 2, torch.int32)
-        cursor = self.buf.get("cursor", nb, torch.int32)
-        stats = self.buf.get("bin_stats", 2, torch.int64)
-        ows = self.buf.get("offsets_ws", lib.bs_bin_tiles_offsets_workspace(nb), torch.uint8)
-        nat.call("bs_bin_tiles_offsets", nat.ptr(counts), nb, nat.ptr(ranges), nat.ptr(cursor), nat.ptr(stats),
-                 nat.ptr(ows), ows.numel(), st)
-        n_inst, biggest = (int(x) for x in stats.cpu().tolist())  # sync 2: sizes the instance buffers
-        keys = self.buf.get("inst_keys", max(n_inst, 1), torch.int64)
-        irows = self.buf.get("irows", max(n_inst, 1), torch.int32)
-        nat.call("bs_bin_tiles_scatter", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
-                 nat.ptr(slot_cams), self.tiles, nat.ptr(cursor), nat.ptr(keys), self.model_id, st)
-        cap = min(self.sort_cap, lib.bs_bin_tiles_max_sort())
-        nat.call("bs_bin_tiles_sort", nat.ptr(keys), nat.ptr(ranges), nb, cap, nat.ptr(irows), st)
-        if biggest > cap:  # rare: buckets beyond the shared-memory sort
-            rg = ranges.view(-1, 2).cpu().numpy()
-            for b in np.flatnonzero(rg[:, 1] - rg[:, 0] > cap):
-                s0, s1 = int(rg[b, 0]), int(rg[b, 1])
-                k = keys[s0:s1]
-                v = torch.empty(s1 - s0, dtype=torch.int32, device=self.dev)
-                from .culling import radix_sort_u64
-                radix_sort_u64(k, v, 0, 64)
-                nat.call("bs_keys_low32", nat.ptr(k), s1 - s0, nat.ptr(irows[s0:s1]), st)
+        """Bucket pipeline (csrc/bin_tiles.cu), see binning.bin_buckets."""
+        n_inst, irows, ranges, biggest = bin_buckets(self.buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams,
+                                                     self.tiles, self.model_id, self.sort_cap)
         self.last["largest_bucket"] = biggest
         return n_inst, irows, ranges
 
