@@ -78,6 +78,7 @@ def build_oracle(force: bool = False, verbose: bool = False) -> str:
 if __name__ == "__main__":
     v = "-v" in sys.argv
     f = "-f" in sys.argv
-    print(build_native(force=f, verbose=v))
+    # BS_NVCC_EXTRA: extra nvcc flags for tuning experiments (e.g. -DBS_SPARSE_LANES=5)
+    print(build_native(force=f, verbose=v, extra_flags=os.environ.get("BS_NVCC_EXTRA", "").split()))
     if os.path.exists(os.path.join(ORACLE_DIR, "splat_oracle.c")):
         print(build_oracle(force=f, verbose=v))

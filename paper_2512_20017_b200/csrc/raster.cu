@@ -24,7 +24,7 @@
 //
 // Backward: each warp walks its own range back to front from the deepest
 // contributor of its pixels (T recovered by division).  Per splat the lanes
-// that contribute are counted with a ballot: up to kSparseLanes of them add
+// that contribute are counted with a ballot: up to kSparseLanes (6) of them add
 // their 9 gradient terms with direct REDs; otherwise the warp reduce-scatters
 // the 9 sums in 12 shuffles and 9 lanes issue one RED each.
 #include "common.cuh"
@@ -37,7 +37,10 @@ constexpr float kAlphaMax = 0.99f;
 constexpr float kTMin = 1e-4f;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr int kSparseLanes = 3;  // contributing lanes handled with direct REDs
+#ifndef BS_SPARSE_LANES
+#define BS_SPARSE_LANES 6  // swept on B200 (C2): 0 3.15, 2 3.08, 3 3.01, 4 2.97, 5 2.92, 6 2.91, 8 2.94 ms
+#endif
+constexpr int kSparseLanes = BS_SPARSE_LANES;  // contributing lanes handled with direct REDs
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float r;

@@ -12,7 +12,7 @@
 // L = 2 ln(255 o): the union of the bounding box of the image of the disk
 // u^2 + v^2 <= L (dual conic; unbounded -> keep) and the circle
 // |mean2d - pixel| <= sqrt(L / 2), padded by 1%.
-// Backward: 15 gradient terms per splat; up to 3 contributing lanes add them
+// Backward: 15 gradient terms per splat; up to 5 contributing lanes add them
 // with direct REDs, otherwise they are reduce-scattered over the warp in 16
 // shuffles and one RED per term is issued per (region, splat).  exp is one
 // ex2.approx in both kernels (identical skip / stop decisions).
@@ -27,7 +27,10 @@ constexpr float kAMin = 1.0f / 255.0f;
 constexpr float kAMax = 0.99f;
 constexpr float kTStop = 1e-4f;
 constexpr float kLog2e2 = 1.4426950408889634f;
-constexpr int kSparse2 = 3;  // contributing lanes handled with direct REDs
+#ifndef BS_SPARSE2_LANES
+#define BS_SPARSE2_LANES 5  // swept on B200 (C3): 0 7.59, 2 7.55, 3 7.45, 5 7.36, 8 7.65 ms
+#endif
+constexpr int kSparse2 = BS_SPARSE2_LANES;  // contributing lanes handled with direct REDs
 
 __device__ __forceinline__ float ex2a(float x) {
   float r;
