@@ -84,34 +84,43 @@ struct ProjArgs {
 
 // Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
 // 24-float SP rows, splat2d_math.cuh).
+// Per point: pre() once (view-independent work), forward()/backward() per
+// view, finish() once to push the accumulated view-independent gradient
+// (Acc) through the scales and the quaternion.
 struct Model3 {
   using F = ProjFwd;
-  static constexpr int kSP = BS_SP_FLOATS, kGSP = BS_GSP_FLOATS;
+  using Pre = PointPre;
+  static constexpr int kSP = BS_SP_FLOATS, kGSP = BS_GSP_FLOATS, kAcc = 6;
+  __device__ static void pre(const PointIn& pt, Pre& r) { point_pre(pt, r); }
   template <class SH>
-  __device__ static void forward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh, F& f) {
-    project_forward_t(pt, sh, c, n_sh, f);
+  __device__ static void forward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh, F& f) {
+    project_forward_t(pt, r, sh, c, n_sh, f);
   }
   __device__ static void write(float* row, const F& f) { write_sp_row(row, f); }
   template <class SH, class A>
-  __device__ static void backward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh, const F& f,
-                                  const float* gs, float* g, A add) {
-    project_backward_t(pt, sh, c, n_sh, f, gs, g, add);
+  __device__ static void backward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh,
+                                  const F& f, const float* gs, float* g, float* acc, A add) {
+    project_backward_t(pt, r, sh, c, n_sh, f, gs, g, acc, add);
   }
+  __device__ static void finish(const PointIn& pt, const float* acc, float* g) { point_pre_backward(pt, acc, g); }
 };
 
 struct Model2 {
   using F = Proj2D;
-  static constexpr int kSP = kSP2, kGSP = kGSP2;
+  using Pre = Pre2D;
+  static constexpr int kSP = kSP2, kGSP = kGSP2, kAcc = 9;
+  __device__ static void pre(const PointIn& pt, Pre& r) { point_pre2(pt, r); }
   template <class SH>
-  __device__ static void forward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh, F& f) {
-    project2d_forward(pt, sh, c, n_sh, f);
+  __device__ static void forward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh, F& f) {
+    project2d_forward(pt, r, sh, c, n_sh, f);
   }
   __device__ static void write(float* row, const F& f) { write_sp2_row(row, f); }
   template <class SH, class A>
-  __device__ static void backward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh, const F& f,
-                                  const float* gs, float* g, A add) {
-    project2d_backward(pt, sh, c, n_sh, f, gs, g, add);
+  __device__ static void backward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh,
+                                  const F& f, const float* gs, float* g, float* acc, A add) {
+    project2d_backward(pt, r, sh, c, n_sh, f, gs, g, acc, add);
   }
+  __device__ static void finish(const PointIn& pt, const float* acc, float* g) { point_pre2_backward(pt, acc, g); }
 };
 
 template <class M>
@@ -137,12 +146,14 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
     if (mask) {
       PointIn pt;
       load_point(a.params, a.S, i, a.n_sh, pt);
+      typename M::Pre pre;
+      M::pre(pt, pre);
       uint32_t m = mask;
       while (m) {
         const int v = __ffs(m) - 1;
         m &= m - 1;
         typename M::F f;
-        M::forward(pt, ShRegs{pt.sh}, s_cam[v], a.n_sh, f);
+        M::forward(pt, pre, ShRegs{pt.sh}, s_cam[v], a.n_sh, f);
         const int64_t row = s_row0[v] + rk.row_offset(v);
         M::write(sp + row * M::kSP, f);
       }
@@ -157,6 +168,11 @@ template <class M, class SH, class ShAdd>
 __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camera* s_cam, const int64_t* s_row0,
                                                const RowRanker& rk, uint32_t mask, const PointIn& pt, const SH& sh,
                                                const float* __restrict__ gsp, float* g, ShAdd sh_add) {
+  typename M::Pre pre;
+  M::pre(pt, pre);
+  float acc[M::kAcc];
+#pragma unroll
+  for (int k = 0; k < M::kAcc; ++k) acc[k] = 0.f;
   uint32_t m = mask;
   while (m) {
     const int v = __ffs(m) - 1;
@@ -167,9 +183,10 @@ __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camer
 #pragma unroll
     for (int k = 0; k < M::kGSP; ++k) gs[k] = src[k];
     typename M::F f;
-    M::forward(pt, sh, s_cam[v], a.n_sh, f);
-    M::backward(pt, sh, s_cam[v], a.n_sh, f, gs, g, sh_add);
+    M::forward(pt, pre, sh, s_cam[v], a.n_sh, f);
+    M::backward(pt, pre, sh, s_cam[v], a.n_sh, f, gs, g, acc, sh_add);
   }
+  M::finish(pt, acc, g);
 }
 
 template <class M>

@@ -29,8 +29,34 @@ constexpr int kSP2 = 24;
 // G_SP row of a 2DGS splat (15 floats): d u, d v, d M[9], d opacity, d rgb
 constexpr int kGSP2 = 15;
 
+// View-independent part of a surfel projection (once per point): rotation of
+// the quaternion, the two tangent scales, activated opacity.
+struct Pre2D {
+  float Rq[9], s[2], opac;
+};
+
+__device__ __forceinline__ void point_pre2(const PointIn& pt, Pre2D& r) {
+  QuatFrame q;
+  quat_frame(pt, 2, q);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) r.Rq[k] = q.Rq[k];
+  r.s[0] = q.s[0];
+  r.s[1] = q.s[1];
+  r.opac = det_sigmoid(pt.op_logit);
+}
+
+// dL/dRq accumulated over views (G, row-major) -> quaternion (g[8..11]).
+__device__ __forceinline__ void point_pre2_backward(const PointIn& pt, const float G[9], float* g) {
+  QuatFrame q;
+  quat_frame(pt, 2, q);
+  float gq[4];
+  quat_backward(q, G, gq);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) g[8 + k] += gq[k];
+}
+
 struct Proj2D {
-  float d[3], qc[3], s[2], qn[4], qnorm, Rq[9], Rc[9];
+  float d[3], qc[3], Rc[9];
   float c0[3], c1[3], c2[3];  // M columns
   float u, v, depth, radius_x, radius_y, normal[3];
   float len, dir[3], Y[16], col_raw[3], col[3], opac;
@@ -44,46 +70,26 @@ __device__ __forceinline__ void kmul(const bs_camera& c, const float x[3], float
 }
 
 template <class SH>
-__device__ __forceinline__ void project2d_forward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
-                                                  Proj2D& f) {
+__device__ __forceinline__ void project2d_forward(const PointIn& pt, const Pre2D& pre, const SH& sh,
+                                                  const bs_camera& c, int n_sh, Proj2D& f) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) f.d[k] = fsub(pt.p[k], c.pos[k]);
   const float* W = c.rot_cw;
 #pragma unroll
   for (int k = 0; k < 3; ++k)
     f.qc[k] = fadd(fadd(fmul(W[3 * k], f.d[0]), fmul(W[3 * k + 1], f.d[1])), fmul(W[3 * k + 2], f.d[2]));
-  f.s[0] = det_expf(pt.ls[0]);
-  f.s[1] = det_expf(pt.ls[1]);
-  const float nn = fadd(fadd(fadd(fmul(pt.q[0], pt.q[0]), fmul(pt.q[1], pt.q[1])), fmul(pt.q[2], pt.q[2])),
-                        fmul(pt.q[3], pt.q[3]));
-  f.qnorm = fsqrt(nn);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) f.qn[k] = fdiv(pt.q[k], f.qnorm);
-  const float w = f.qn[0], x = f.qn[1], y = f.qn[2], zq = f.qn[3];
-  const float xx = fmul(x, x), yy = fmul(y, y), zz = fmul(zq, zq);
-  const float xy = fmul(x, y), xz = fmul(x, zq), yz = fmul(y, zq);
-  const float wx = fmul(w, x), wy = fmul(w, y), wz = fmul(w, zq);
-  f.Rq[0] = fsub(1.f, fmul(2.f, fadd(yy, zz)));
-  f.Rq[1] = fmul(2.f, fsub(xy, wz));
-  f.Rq[2] = fmul(2.f, fadd(xz, wy));
-  f.Rq[3] = fmul(2.f, fadd(xy, wz));
-  f.Rq[4] = fsub(1.f, fmul(2.f, fadd(xx, zz)));
-  f.Rq[5] = fmul(2.f, fsub(yz, wx));
-  f.Rq[6] = fmul(2.f, fsub(xz, wy));
-  f.Rq[7] = fmul(2.f, fadd(yz, wx));
-  f.Rq[8] = fsub(1.f, fmul(2.f, fadd(xx, yy)));
   // Rc = Rcw Rq
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j)
       f.Rc[3 * i + j] =
-          fadd(fadd(fmul(W[3 * i], f.Rq[j]), fmul(W[3 * i + 1], f.Rq[3 + j])), fmul(W[3 * i + 2], f.Rq[6 + j]));
+          fadd(fadd(fmul(W[3 * i], pre.Rq[j]), fmul(W[3 * i + 1], pre.Rq[3 + j])), fmul(W[3 * i + 2], pre.Rq[6 + j]));
   float tu[3], tv[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    tu[i] = fmul(f.Rc[3 * i], f.s[0]);
-    tv[i] = fmul(f.Rc[3 * i + 1], f.s[1]);
+    tu[i] = fmul(f.Rc[3 * i], pre.s[0]);
+    tv[i] = fmul(f.Rc[3 * i + 1], pre.s[1]);
   }
   kmul(c, tu, f.c0);
   kmul(c, tv, f.c1);
@@ -135,7 +141,7 @@ __device__ __forceinline__ void project2d_forward(const PointIn& pt, const SH& s
     f.col_raw[ch] = fadd(acc, 0.5f);
     f.col[ch] = fmaxf(f.col_raw[ch], 0.f);
   }
-  f.opac = det_sigmoid(pt.op_logit);
+  f.opac = pre.opac;
 }
 
 __device__ __forceinline__ void write_sp2_row(float* __restrict__ row, const Proj2D& f) {
@@ -151,9 +157,11 @@ __device__ __forceinline__ void write_sp2_row(float* __restrict__ row, const Pro
 
 // Accumulate the parameter gradient of one (point, view) pair.
 // gsp = (du, dv, dM[9] row-major, dopacity, dr, dg, db).
+// GR accumulates dL/dRq (row-major) for point_pre2_backward.
 template <class SH, class ShAdd>
-__device__ __forceinline__ void project2d_backward(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
-                                                   const Proj2D& f, const float gsp[15], float* g, ShAdd sh_add) {
+__device__ __forceinline__ void project2d_backward(const PointIn& pt, const Pre2D& pre, const SH& sh,
+                                                   const bs_camera& c, int n_sh, const Proj2D& f,
+                                                   const float gsp[15], float* g, float GR[9], ShAdd sh_add) {
   if (!f.valid) return;
   // ---- colour -> sh, dir (as 3DGS)
   float dc[3];
@@ -178,7 +186,7 @@ __device__ __forceinline__ void project2d_backward(const PointIn& pt, const SH& 
 #pragma unroll
   for (int k = 0; k < 3; ++k) gp[k] = (gdir[k] - f.dir[k] * dd) / f.len;
   // ---- opacity
-  g[3] += gsp[11] * f.opac * (1.f - f.opac);
+  g[3] += gsp[11] * pre.opac * (1.f - pre.opac);
   // ---- M rows -> columns c0, c1, c2; mean2d = c2.xy / c2.z
   const float* gm = gsp + 2;  // row-major 3x3
   float gc0[3] = {gm[0], gm[3], gm[6]};
@@ -212,27 +220,17 @@ __device__ __forceinline__ void project2d_backward(const PointIn& pt, const SH& 
   for (int i = 0; i < 3; ++i) {
     gs0 += f.Rc[3 * i] * gtu[i];
     gs1 += f.Rc[3 * i + 1] * gtv[i];
-    gRc[3 * i] = gtu[i] * f.s[0];
-    gRc[3 * i + 1] = gtv[i] * f.s[1];
+    gRc[3 * i] = gtu[i] * pre.s[0];
+    gRc[3 * i + 1] = gtv[i] * pre.s[1];
     gRc[3 * i + 2] = 0.f;  // the normal column carries no loss gradient
   }
-  g[4] += gs0 * f.s[0];
-  g[5] += gs1 * f.s[1];
+  g[4] += gs0 * pre.s[0];
+  g[5] += gs1 * pre.s[1];
   // ---- Rc = Rcw Rq  ->  dL/dRq = Rcw^T dL/dRc
-  float G[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) G[3 * i + j] = W[i] * gRc[j] + W[3 + i] * gRc[3 + j] + W[6 + i] * gRc[6 + j];
-  const float w = f.qn[0], x = f.qn[1], y = f.qn[2], zq = f.qn[3];
-  float gqn[4];
-  gqn[0] = 2.f * (-zq * G[1] + y * G[2] + zq * G[3] - x * G[5] - y * G[6] + x * G[7]);
-  gqn[1] = 2.f * (y * G[1] + zq * G[2] + y * G[3] - 2.f * x * G[4] - w * G[5] + zq * G[6] + w * G[7] - 2.f * x * G[8]);
-  gqn[2] = 2.f * (-2.f * y * G[0] + x * G[1] + w * G[2] + x * G[3] + zq * G[5] - w * G[6] + zq * G[7] - 2.f * y * G[8]);
-  gqn[3] = 2.f * (-2.f * zq * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.f * zq * G[4] + y * G[5] + x * G[6] + y * G[7]);
-  const float dq = w * gqn[0] + x * gqn[1] + y * gqn[2] + zq * gqn[3];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) g[8 + k] += (gqn[k] - f.qn[k] * dq) / f.qnorm;
+    for (int j = 0; j < 3; ++j) GR[3 * i + j] += W[i] * gRc[j] + W[3 + i] * gRc[3 + j] + W[6 + i] * gRc[6 + j];
 }
 
 }  // namespace bs

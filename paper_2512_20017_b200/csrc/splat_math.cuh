@@ -44,10 +44,6 @@ struct PointIn {
 struct ProjFwd {
   float d[3];      // p - campos
   float qc[3];     // camera-frame position
-  float s[3];      // scales
-  float qn[4];     // normalised quaternion
-  float qnorm;
-  float Rq[9];     // rotation of the quaternion
   float Sc[6];     // camera-frame covariance (00 01 02 11 12 22)
   float J00, J02, J11, J12;
   bool clamp_x, clamp_y;
@@ -127,17 +123,108 @@ struct ShPlanes {
   }
 };
 
-template <class SH>
-__device__ __forceinline__ void project_forward_t(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
-                                                  ProjFwd& f);
+// Scales, normalised quaternion and its rotation matrix of a point (shared by
+// the 3DGS and 2DGS models; explicit round-to-nearest ops).
+struct QuatFrame {
+  float s[3], qn[4], qnorm, Rq[9];
+};
 
-__device__ __forceinline__ void project_forward(const PointIn& pt, const bs_camera& c, int n_sh, ProjFwd& f) {
-  project_forward_t(pt, ShRegs{pt.sh}, c, n_sh, f);
+__device__ __forceinline__ void quat_frame(const PointIn& pt, int n_scales, QuatFrame& r) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) r.s[k] = k < n_scales ? det_expf(pt.ls[k]) : 0.f;
+  const float nn = fadd(fadd(fadd(fmul(pt.q[0], pt.q[0]), fmul(pt.q[1], pt.q[1])), fmul(pt.q[2], pt.q[2])),
+                        fmul(pt.q[3], pt.q[3]));
+  r.qnorm = fsqrt(nn);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) r.qn[k] = fdiv(pt.q[k], r.qnorm);
+  const float w = r.qn[0], x = r.qn[1], y = r.qn[2], zq = r.qn[3];
+  const float xx = fmul(x, x), yy = fmul(y, y), zz = fmul(zq, zq);
+  const float xy = fmul(x, y), xz = fmul(x, zq), yz = fmul(y, zq);
+  const float wx = fmul(w, x), wy = fmul(w, y), wz = fmul(w, zq);
+  r.Rq[0] = fsub(1.f, fmul(2.f, fadd(yy, zz)));
+  r.Rq[1] = fmul(2.f, fsub(xy, wz));
+  r.Rq[2] = fmul(2.f, fadd(xz, wy));
+  r.Rq[3] = fmul(2.f, fadd(xy, wz));
+  r.Rq[4] = fsub(1.f, fmul(2.f, fadd(xx, zz)));
+  r.Rq[5] = fmul(2.f, fsub(yz, wx));
+  r.Rq[6] = fmul(2.f, fsub(xz, wy));
+  r.Rq[7] = fmul(2.f, fadd(yz, wx));
+  r.Rq[8] = fsub(1.f, fmul(2.f, fadd(xx, yy)));
+}
+
+// dL/d(raw quaternion) from dL/dRq (G, row-major), through the normalisation.
+__device__ __forceinline__ void quat_backward(const QuatFrame& r, const float G[9], float gq[4]) {
+  const float w = r.qn[0], x = r.qn[1], y = r.qn[2], zq = r.qn[3];
+  float gqn[4];
+  gqn[0] = 2.f * (-zq * G[1] + y * G[2] + zq * G[3] - x * G[5] - y * G[6] + x * G[7]);
+  gqn[1] = 2.f * (y * G[1] + zq * G[2] + y * G[3] - 2.f * x * G[4] - w * G[5] + zq * G[6] + w * G[7] - 2.f * x * G[8]);
+  gqn[2] = 2.f * (-2.f * y * G[0] + x * G[1] + w * G[2] + x * G[3] + zq * G[5] - w * G[6] + zq * G[7] - 2.f * y * G[8]);
+  gqn[3] = 2.f * (-2.f * zq * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.f * zq * G[4] + y * G[5] + x * G[6] + y * G[7]);
+  const float dq = w * gqn[0] + x * gqn[1] + y * gqn[2] + zq * gqn[3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) gq[k] = (gqn[k] - r.qn[k] * dq) / r.qnorm;
+}
+
+// View-independent part of a 3DGS projection, computed once per point and
+// reused for all its views: world covariance Sg = (Rq S)(Rq S)^T (00 01 02 11
+// 12 22) and the activated opacity.
+struct PointPre {
+  float Sg[6];
+  float opac;
+};
+
+__device__ __forceinline__ void point_pre(const PointIn& pt, PointPre& r) {
+  QuatFrame q;
+  quat_frame(pt, 3, q);
+  float M[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) M[3 * i + j] = fmul(q.Rq[3 * i + j], q.s[j]);
+  int k = 0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j)
+      r.Sg[k++] = fadd(fadd(fmul(M[3 * i], M[3 * j]), fmul(M[3 * i + 1], M[3 * j + 1])), fmul(M[3 * i + 2], M[3 * j + 2]));
+  r.opac = det_sigmoid(pt.op_logit);
+}
+
+// Gradient of the view-independent part: dL/dSg (accumulated over views,
+// 6 unique entries) -> log scales (g[4..6]) and quaternion (g[8..11]).
+__device__ __forceinline__ void point_pre_backward(const PointIn& pt, const float gS[6], float* g) {
+  QuatFrame q;
+  quat_frame(pt, 3, q);
+  const float gSg[9] = {gS[0], gS[1], gS[2], gS[1], gS[3], gS[4], gS[2], gS[4], gS[5]};
+  float M[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) M[3 * i + j] = q.Rq[3 * i + j] * q.s[j];
+  // Sg = M M^T, M = Rq S  ->  g_M = 2 g_Sg M
+  float gM[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      gM[3 * i + j] = 2.f * (gSg[3 * i] * M[j] + gSg[3 * i + 1] * M[3 + j] + gSg[3 * i + 2] * M[6 + j]);
+  float G[9];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float gs = q.Rq[j] * gM[j] + q.Rq[3 + j] * gM[3 + j] + q.Rq[6 + j] * gM[6 + j];
+    g[4 + j] += gs * q.s[j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) G[3 * i + j] = gM[3 * i + j] * q.s[j];
+  }
+  float gq[4];
+  quat_backward(q, G, gq);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) g[8 + k] += gq[k];
 }
 
 template <class SH>
-__device__ __forceinline__ void project_forward_t(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
-                                                  ProjFwd& f) {
+__device__ __forceinline__ void project_forward_t(const PointIn& pt, const PointPre& pre, const SH& sh,
+                                                  const bs_camera& c, int n_sh, ProjFwd& f) {
   // camera frame: q = Rcw (p - pos)
 #pragma unroll
   for (int k = 0; k < 3; ++k) f.d[k] = fsub(pt.p[k], c.pos[k]);
@@ -146,41 +233,8 @@ __device__ __forceinline__ void project_forward_t(const PointIn& pt, const SH& s
     f.qc[k] = fadd(fadd(fmul(c.rot_cw[3 * k], f.d[0]), fmul(c.rot_cw[3 * k + 1], f.d[1])),
                    fmul(c.rot_cw[3 * k + 2], f.d[2]));
   const float z = f.qc[2];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) f.s[k] = det_expf(pt.ls[k]);
-  const float nn = fadd(fadd(fadd(fmul(pt.q[0], pt.q[0]), fmul(pt.q[1], pt.q[1])), fmul(pt.q[2], pt.q[2])),
-                        fmul(pt.q[3], pt.q[3]));
-  f.qnorm = fsqrt(nn);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) f.qn[k] = fdiv(pt.q[k], f.qnorm);
-  const float w = f.qn[0], x = f.qn[1], y = f.qn[2], zq = f.qn[3];
-  const float xx = fmul(x, x), yy = fmul(y, y), zz = fmul(zq, zq);
-  const float xy = fmul(x, y), xz = fmul(x, zq), yz = fmul(y, zq);
-  const float wx = fmul(w, x), wy = fmul(w, y), wz = fmul(w, zq);
-  f.Rq[0] = fsub(1.f, fmul(2.f, fadd(yy, zz)));
-  f.Rq[1] = fmul(2.f, fsub(xy, wz));
-  f.Rq[2] = fmul(2.f, fadd(xz, wy));
-  f.Rq[3] = fmul(2.f, fadd(xy, wz));
-  f.Rq[4] = fsub(1.f, fmul(2.f, fadd(xx, zz)));
-  f.Rq[5] = fmul(2.f, fsub(yz, wx));
-  f.Rq[6] = fmul(2.f, fsub(xz, wy));
-  f.Rq[7] = fmul(2.f, fadd(yz, wx));
-  f.Rq[8] = fsub(1.f, fmul(2.f, fadd(xx, yy)));
-  float M[9];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) M[3 * i + j] = fmul(f.Rq[3 * i + j], f.s[j]);
-  float Sg[9];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = i; j < 3; ++j) {
-      const float v = fadd(fadd(fmul(M[3 * i], M[3 * j]), fmul(M[3 * i + 1], M[3 * j + 1])),
-                           fmul(M[3 * i + 2], M[3 * j + 2]));
-      Sg[3 * i + j] = v;
-      Sg[3 * j + i] = v;
-    }
+  const float Sg[9] = {pre.Sg[0], pre.Sg[1], pre.Sg[2], pre.Sg[1], pre.Sg[3], pre.Sg[4],
+                       pre.Sg[2], pre.Sg[4], pre.Sg[5]};
   // Sc = W Sg W^T
   const float* W = c.rot_cw;
   float T[9];
@@ -250,7 +304,7 @@ __device__ __forceinline__ void project_forward_t(const PointIn& pt, const SH& s
     f.col_raw[ch] = fadd(acc, 0.5f);
     f.col[ch] = fmaxf(f.col_raw[ch], 0.f);
   }
-  f.opac = det_sigmoid(pt.op_logit);
+  f.opac = pre.opac;
 }
 
 __device__ __forceinline__ void write_sp_row(float* __restrict__ row, const ProjFwd& f) {
@@ -316,19 +370,11 @@ __device__ __forceinline__ void sh_dir_grad(const float dir[3], int n_sh, const 
 // floats (plane 0..2 order) into g, the SH coefficient gradients through
 // sh_add(flat index f = 3k + channel, value).
 // gsp = (du, dv, dopac, dA, dB, dC, dr, dg, db).
+// gS accumulates dL/dSg (6 unique entries) for point_pre_backward.
 template <class SH, class ShAdd>
-__device__ __forceinline__ void project_backward_t(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
-                                                   const ProjFwd& f, const float gsp[9], float* g, ShAdd sh_add);
-
-template <class ShAdd>
-__device__ __forceinline__ void project_backward(const PointIn& pt, const bs_camera& c, int n_sh,
-                                                 const ProjFwd& f, const float gsp[9], float* g, ShAdd sh_add) {
-  project_backward_t(pt, ShRegs{pt.sh}, c, n_sh, f, gsp, g, sh_add);
-}
-
-template <class SH, class ShAdd>
-__device__ __forceinline__ void project_backward_t(const PointIn& pt, const SH& sh, const bs_camera& c, int n_sh,
-                                                   const ProjFwd& f, const float gsp[9], float* g, ShAdd sh_add) {
+__device__ __forceinline__ void project_backward_t(const PointIn& pt, const PointPre& pre, const SH& sh,
+                                                   const bs_camera& c, int n_sh, const ProjFwd& f,
+                                                   const float gsp[9], float* g, float gS[6], ShAdd sh_add) {
   if (!f.valid) return;
   // ---- colour -> sh, dir
   float dc[3];
@@ -353,7 +399,7 @@ __device__ __forceinline__ void project_backward_t(const PointIn& pt, const SH& 
 #pragma unroll
   for (int k = 0; k < 3; ++k) gp[k] = (gdir[k] - f.dir[k] * dd) / f.len;
   // ---- opacity
-  g[3] += gsp[2] * f.opac * (1.f - f.opac);
+  g[3] += gsp[2] * pre.opac * (1.f - pre.opac);
   // ---- means2d -> camera point
   const float z = f.qc[2], iz = 1.f / z, iz2 = iz * iz;
   float gq[3];
@@ -423,36 +469,12 @@ __device__ __forceinline__ void project_backward_t(const PointIn& pt, const SH& 
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) gSg[3 * i + j] = tmp[3 * i] * W[j] + tmp[3 * i + 1] * W[3 + j] + tmp[3 * i + 2] * W[6 + j];
-  // ---- Sg = M M^T, M = Rq S  ->  g_M = 2 g_Sg M
-  float M[9];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) M[3 * i + j] = f.Rq[3 * i + j] * f.s[j];
-  float gM[9];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-      gM[3 * i + j] = 2.f * (gSg[3 * i] * M[j] + gSg[3 * i + 1] * M[3 + j] + gSg[3 * i + 2] * M[6 + j]);
-  float G[9];
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const float gs = f.Rq[j] * gM[j] + f.Rq[3 + j] * gM[3 + j] + f.Rq[6 + j] * gM[6 + j];
-    g[4 + j] += gs * f.s[j];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) G[3 * i + j] = gM[3 * i + j] * f.s[j];
-  }
-  // ---- rotation -> normalised quaternion -> raw quaternion
-  const float w = f.qn[0], x = f.qn[1], y = f.qn[2], zq = f.qn[3];
-  float gqn[4];
-  gqn[0] = 2.f * (-zq * G[1] + y * G[2] + zq * G[3] - x * G[5] - y * G[6] + x * G[7]);
-  gqn[1] = 2.f * (y * G[1] + zq * G[2] + y * G[3] - 2.f * x * G[4] - w * G[5] + zq * G[6] + w * G[7] - 2.f * x * G[8]);
-  gqn[2] = 2.f * (-2.f * y * G[0] + x * G[1] + w * G[2] + x * G[3] + zq * G[5] - w * G[6] + zq * G[7] - 2.f * y * G[8]);
-  gqn[3] = 2.f * (-2.f * zq * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.f * zq * G[4] + y * G[5] + x * G[6] + y * G[7]);
-  const float dq = w * gqn[0] + x * gqn[1] + y * gqn[2] + zq * gqn[3];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) g[8 + k] += (gqn[k] - f.qn[k] * dq) / f.qnorm;
+  gS[0] += gSg[0];
+  gS[1] += gSg[1];
+  gS[2] += gSg[2];
+  gS[3] += gSg[4];
+  gS[4] += gSg[5];
+  gS[5] += gSg[8];
 }
 
 }  // namespace bs
