@@ -2,7 +2,7 @@
 // view-dependent splats by their distance to the camera plane").
 //
 //  1. bs_bin_tiles_count   per (row, covered tile): atomicAdd on the
-//                          (slot, tile) bucket counter
+//                          (slot, tile) bucket counter, warp-aggregated
 //  2. bs_bin_tiles_offsets one-CTA exclusive scan -> ranges [start, end),
 //                          scatter cursors, total and largest bucket
 //  3. bs_bin_tiles_scatter per (row, tile): key = (f32bits(depth) << 32) | row
@@ -36,16 +36,48 @@ struct BinGeom {
   SpLayout lay;
 };
 
-__global__ void count_tiles_kernel(BinGeom g, int32_t* __restrict__ counts) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < g.n; r += (int64_t)gridDim.x * blockDim.x) {
-    const int slot = g.seg_slot[segment_of(g.seg_row0, g.n_segs, r)];
+// Rows of a warp are consecutive points of one Z-ordered shard, so their
+// tiles coincide often: every round each lane takes its next covered tile,
+// lanes with equal buckets are grouped with __match_any_sync and only the
+// group leader touches the counter (warp-aggregated atomics).
+struct RowTiles {
+  int slot, x0, x1, y1, tx, x, y;
+  bool left;  // tiles remain
+  __device__ __forceinline__ void init(const BinGeom& g, int64_t r) {
+    left = false;
+    if (r >= g.n) return;
+    slot = g.seg_slot[segment_of(g.seg_row0, g.n_segs, r)];
     const int W = g.cams[slot].width, H = g.cams[slot].height;
-    int x0, x1, y0, y1;
-    if (!tile_rect_at(g.sp + r * g.lay.stride, g.lay.rad_off, W, H, x0, x1, y0, y1)) continue;
-    const int tx = (W + BS_TILE - 1) / BS_TILE;
-    int32_t* base = counts + (int64_t)slot * g.tiles_per_slot;
-    for (int y = y0; y < y1; ++y)
-      for (int x = x0; x < x1; ++x) atomicAdd(base + y * tx + x, 1);
+    int y0;
+    if (!tile_rect_at(g.sp + r * g.lay.stride, g.lay.rad_off, W, H, x0, x1, y0, y1)) return;
+    tx = (W + BS_TILE - 1) / BS_TILE;
+    x = x0;
+    y = y0;
+    left = true;
+  }
+  // bucket of the current tile (or -1), then advance
+  __device__ __forceinline__ int next(int tiles_per_slot) {
+    if (!left) return -1;
+    const int b = slot * tiles_per_slot + y * tx + x;
+    if (++x == x1) {
+      x = x0;
+      left = ++y < y1;
+    }
+    return b;
+  }
+};
+
+__global__ void count_tiles_kernel(BinGeom g, int32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; r0 < g.n; r0 += stride) {
+    RowTiles t;
+    t.init(g, r0 + lane);
+    while (__any_sync(0xffffffffu, t.left)) {
+      const int b = t.next(g.tiles_per_slot);
+      const uint32_t peers = __match_any_sync(0xffffffffu, b);
+      if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(counts + b, __popc(peers));
+    }
   }
 }
 
@@ -138,17 +170,25 @@ __global__ void __launch_bounds__(kScanBlock) bucket_ranges_kernel(const int32_t
 }
 
 __global__ void scatter_tiles_kernel(BinGeom g, int32_t* __restrict__ cursor, uint64_t* __restrict__ keys) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < g.n; r += (int64_t)gridDim.x * blockDim.x) {
-    const int slot = g.seg_slot[segment_of(g.seg_row0, g.n_segs, r)];
-    const int W = g.cams[slot].width, H = g.cams[slot].height;
-    const float* row = g.sp + r * g.lay.stride;
-    int x0, x1, y0, y1;
-    if (!tile_rect_at(row, g.lay.rad_off, W, H, x0, x1, y0, y1)) continue;
-    const int tx = (W + BS_TILE - 1) / BS_TILE;
-    const uint64_t key = ((uint64_t)__float_as_uint(row[g.lay.depth_off]) << 32) | (uint64_t)(uint32_t)r;
-    int32_t* base = cursor + (int64_t)slot * g.tiles_per_slot;
-    for (int y = y0; y < y1; ++y)
-      for (int x = x0; x < x1; ++x) keys[atomicAdd(base + y * tx + x, 1)] = key;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; r0 < g.n; r0 += stride) {
+    const int64_t r = r0 + lane;
+    RowTiles t;
+    t.init(g, r);
+    const uint64_t key =
+        t.left ? ((uint64_t)__float_as_uint(g.sp[r * g.lay.stride + g.lay.depth_off]) << 32) | (uint64_t)(uint32_t)r
+               : 0ull;
+    while (__any_sync(0xffffffffu, t.left)) {
+      const int b = t.next(g.tiles_per_slot);
+      const uint32_t peers = __match_any_sync(0xffffffffu, b);
+      const int leader = __ffs(peers) - 1;
+      int pos = 0;
+      if (b >= 0 && lane == leader) pos = atomicAdd(cursor + b, __popc(peers));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (b >= 0) keys[pos + __popc(peers & lt)] = key;
+    }
   }
 }
 
@@ -217,26 +257,35 @@ __device__ __forceinline__ void sort_bucket_regs(const uint64_t* __restrict__ ke
   }
 }
 
+// One launch per size class (n <= 256, <= 512, <= 1024) so that each class
+// is compiled with the registers of its own largest network (the 1024-key
+// network needs 64 key registers per lane; the common 257..512 class half of
+// that), instead of the whole kernel paying for the largest one.
+template <int EMAX>
 __global__ void __launch_bounds__(32 * kSortWarpsPerCta) sort_tiles_warp_kernel(const uint64_t* __restrict__ keys,
                                                                                  const int2* __restrict__ ranges,
                                                                                  int nb, int cap,
                                                                                  uint32_t* __restrict__ rows) {
+  constexpr int kLo = EMAX <= 8 ? 0 : 16 * EMAX;  // exclusive lower bound of the class
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * kSortWarpsPerCta + w;
   if (b >= nb) return;
   const int2 rg = ranges[b];
   const int n = rg.y - rg.x;
-  if (n <= 0 || n > cap || n > kWarpCap) return;
-  if (n == 1) {
-    if (lane == 0) rows[rg.x] = (uint32_t)keys[rg.x];
-    return;
+  if (n <= kLo || n > 32 * EMAX || n > cap) return;
+  if constexpr (EMAX <= 8) {
+    if (n <= 0) return;
+    if (n == 1) {
+      if (lane == 0) rows[rg.x] = (uint32_t)keys[rg.x];
+      return;
+    }
+    if (n <= 32) sort_bucket_regs<1>(keys, rg.x, n, rows, lane);
+    else if (n <= 64) sort_bucket_regs<2>(keys, rg.x, n, rows, lane);
+    else if (n <= 128) sort_bucket_regs<4>(keys, rg.x, n, rows, lane);
+    else sort_bucket_regs<8>(keys, rg.x, n, rows, lane);
+  } else {
+    sort_bucket_regs<EMAX>(keys, rg.x, n, rows, lane);
   }
-  if (n <= 32) sort_bucket_regs<1>(keys, rg.x, n, rows, lane);
-  else if (n <= 64) sort_bucket_regs<2>(keys, rg.x, n, rows, lane);
-  else if (n <= 128) sort_bucket_regs<4>(keys, rg.x, n, rows, lane);
-  else if (n <= 256) sort_bucket_regs<8>(keys, rg.x, n, rows, lane);
-  else if (n <= 512) sort_bucket_regs<16>(keys, rg.x, n, rows, lane);
-  else sort_bucket_regs<32>(keys, rg.x, n, rows, lane);
 }
 
 // Buckets with kWarpCap < n <= cap: one CTA each.
@@ -342,9 +391,14 @@ extern "C" int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* r
              kSortCap);
   if (n_buckets == 0) return BS_OK;
   cudaStream_t s = as_stream(stream);
-  sort_tiles_warp_kernel<<<(n_buckets + kSortWarpsPerCta - 1) / kSortWarpsPerCta, 32 * kSortWarpsPerCta, 0, s>>>(
-      inst_keys, reinterpret_cast<const int2*>(ranges), n_buckets, smem_cap, inst_rows);
-  BS_LAUNCH_CHECK("sort_tiles_warp_kernel");
+  const int grid = (n_buckets + kSortWarpsPerCta - 1) / kSortWarpsPerCta;
+  const int2* rg = reinterpret_cast<const int2*>(ranges);
+  sort_tiles_warp_kernel<8><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+  BS_LAUNCH_CHECK("sort_tiles_warp_kernel<8>");
+  sort_tiles_warp_kernel<16><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+  BS_LAUNCH_CHECK("sort_tiles_warp_kernel<16>");
+  sort_tiles_warp_kernel<32><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+  BS_LAUNCH_CHECK("sort_tiles_warp_kernel<32>");
   if (smem_cap > kWarpCap) {
     sort_tiles_kernel<<<n_buckets, kSortThreads, 0, s>>>(inst_keys, reinterpret_cast<const int2*>(ranges), smem_cap,
                                                          inst_rows);

@@ -102,7 +102,7 @@ class SplatTrainer:
 
     def __init__(self, params: np.ndarray, group_begin: np.ndarray, aabb: np.ndarray, views, gt=None,
                  sh_degree: int = 3, adam: AdamConfig | None = None, device=None, comm=None,
-                 bg=(0.0, 0.0, 0.0), model: str = "3dgs"):
+                 bg=(0.0, 0.0, 0.0), model: str = "3dgs", presence: np.ndarray | None = None):
         nat.load()
         if model not in ("3dgs", "2dgs"):
             raise ValueError(f"unknown splat model {model!r} (3dgs | 2dgs)")
@@ -131,6 +131,22 @@ class SplatTrainer:
         self.tiles = self.tiles_x * self.tiles_y
         self.planes_all = torch.as_tensor(np.stack([view_plane_block(v, 1) for v in self.views]), device=self.dev)
         self.cams_all = torch.as_tensor(camera_bytes(self.views), device=self.dev)
+        # 4DGS spatio-temporal culling (visibility.py:244-252):
+        # point i is a candidate for view v iff presence[i, 0] <= t_v <= presence[i, 1] (f32)
+        self.presence = self.view_times = None
+        if presence is not None:
+            pres = np.ascontiguousarray(presence, dtype=np.float32)
+            if pres.shape != (self.S, 2):
+                from .status import ParameterError
+
+                raise ParameterError("presence must be float32 [S, 2] aligned with the shard")
+            if any(v.time is None for v in self.views):
+                from .status import ConfigurationError
+
+                raise ConfigurationError("temporal culling needs a timestamp on every view")
+            self.presence = torch.as_tensor(pres, device=self.dev)
+            self.view_times = torch.as_tensor(np.array([v.time for v in self.views], dtype=np.float32),
+                                              device=self.dev)
         self.gt = None if gt is None else torch.as_tensor(gt, device=self.dev)
         self.sh_degree = sh_degree
         self.adam = adam if adam is not None else AdamConfig(np.full(60, 1e-3, dtype=np.float32))
@@ -182,10 +198,12 @@ class SplatTrainer:
         mask = self.buf.get("mask", S, torch.int32)
         counts = self.buf.get("counts", self.n_groups * B, torch.int32)
         with self._t("cull"):
-            desc = nat.CullDesc(nat.CULL_MASK, B, 1, 1, 0, 4)
-            nat.call("bs_cull_count", desc, nat.ptr(self.params), S, None, nat.ptr(self.group_begin),
-                     nat.ptr(self.aabb), self.n_groups, nat.ptr(planes), None, None, nat.ptr(mask),
-                     nat.ptr(counts), None, st)
+            temporal = self.presence is not None
+            times = self.view_times.index_select(0, bidx).contiguous() if temporal else None
+            desc = nat.CullDesc(nat.CULL_MASK, B, 1, 1, 1 if temporal else 0, 4)
+            nat.call("bs_cull_count", desc, nat.ptr(self.params), S, nat.ptr(self.presence),
+                     nat.ptr(self.group_begin), nat.ptr(self.aabb), self.n_groups, nat.ptr(planes), nat.ptr(times),
+                     None, nat.ptr(mask), nat.ptr(counts), None, st)
         base = self.buf.get("base", self.n_groups * B, torch.int32)
         view_rows = self.buf.get("view_rows", B, torch.int64)
         view_row0 = self.buf.get("view_row0", B, torch.int64)

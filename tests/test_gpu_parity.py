@@ -412,3 +412,30 @@ def test_c2_bucket_and_radix_binning_identical(cuda):
     assert np.array_equal(_norm_ranges(res[0][0]), _norm_ranges(res[1][0]))
     assert np.array_equal(res[0][1], res[1][1])
     assert np.array_equal(_norm_ranges(res[0][0]), _norm_ranges(res[2][0])) and np.array_equal(res[0][1], res[2][1])
+
+
+def test_train_step_temporal_culling_4dgs(cuda):
+    """4DGS profile: the step's culling also applies the
+    presence intervals (visibility.py:244-252, f32 compare); the rows it
+    projects equal the host cull_points(view_time, presence) sets."""
+    from paper_2512_20017_b200.culling import cull_points, frustum_from_view
+
+    st = _street_golden_scene()
+    g = zorder_group(st.cloud, G=64)
+    pres = st.cloud.timestamps[g.permutation]
+    params = scenes.init_gaussians(g.sorted_cloud, 4, 0.5)
+    W, H = st.views[0].width, st.views[0].height
+    gt = scenes.synthetic_gt(4, len(st.views), W, H)
+    tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), st.views, gt=gt, presence=pres)
+    batch = [1, 4, 7, 10]
+    tr.step(batch)
+    torch.cuda.synchronize()
+    rows = tr.last["rows_per_view"]
+    mask = tr.buf.bufs["mask"][: tr.S].cpu().numpy().view(np.uint32)
+    pos = g.sorted_cloud.positions
+    for s, v in enumerate(batch):
+        view = st.views[v]
+        ref = cull_points(frustum_from_view(view), pos, np.float32(view.time), pres)
+        assert np.array_equal(((mask >> s) & 1).astype(bool), ref), f"view {v}"
+        assert rows[s] == ref.sum()
+    assert 0 < rows.sum() < len(batch) * tr.S  # the time test actually removes points
