@@ -37,6 +37,7 @@ def lib():
             "or_visibility_mask": (None, [P, I64, P, P, I32, P, I32, P]),
             "or_morton": (None, [P, I64, P, I32, P]),
             "or_det_expf": (F, [F]),
+            "or_det_logf": (F, [F]),
             "or_project": (None, [P, I64, P, I64, P, I32, P]),
             "or_project_bwd": (None, [P, I64, P, I64, P, I32, P, P]),
             "or_render": (I32, [P, I64, I32, I32, P, P, P, P, P, P, P]),
@@ -110,6 +111,10 @@ def morton(positions, bbox, bits):
 
 def det_expf(x: float) -> float:
     return lib().or_det_expf(float(x))
+
+
+def det_logf(x: float) -> float:
+    return lib().or_det_logf(float(x))
 
 
 # row widths per model: 3DGS SP 12 / G_SP 9, 2DGS SP 24 / G_SP 15 (include/splat_b200.h)

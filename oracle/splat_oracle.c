@@ -173,6 +173,31 @@ float or_det_expf(float x) {
   return p * s.f;
 }
 
+/* ln(x), same op sequence as csrc/common.cuh det_logf */
+float or_det_logf(float x) {
+  if (!(x >= 1.17549435e-38f)) return -87.5f;
+  fbits b;
+  b.f = x;
+  int e = (int)(b.u >> 23) - 127;
+  fbits mb;
+  mb.u = (b.u & 0x7fffffu) | 0x3f800000u;
+  float m = mb.f;
+  if (m > 1.41421356f) {
+    m = m * 0.5f;
+    e += 1;
+  }
+  const float s = (m - 1.0f) / (m + 1.0f);
+  const float s2 = s * s;
+  float p = 0x1.c71c72p-4f;
+  p = p * s2 + 0x1.249250p-3f;
+  p = p * s2 + 0x1.99999ap-3f;
+  p = p * s2 + 0x1.555556p-2f;
+  p = p * s2 + 1.0f;
+  const float lnm = (2.0f * s) * p;
+  const float fe = (float)e;
+  return fe * 0x1.62e400p-1f + (lnm + fe * 0x1.7f7d1cp-20f);
+}
+
 typedef struct {
   float p[3], op, ls[3], q[4], sh[48];
 } opoint;
@@ -289,8 +314,11 @@ static void proj_fwd(const opoint* pt, const or_camera* c, int n_sh, oproj* f) {
     f->conic[0] = f->c / f->det;
     f->conic[1] = (-f->b) / f->det;
     f->conic[2] = f->a / f->det;
-    f->radius_x = ceilf(3.f * sqrtf(f->a));
-    f->radius_y = ceilf(3.f * sqrtf(f->c));
+    /* support box: q <= k, k = min(9, 2 ln(255 o)) (csrc/common.cuh support_k) */
+    const float o = 1.f / (1.f + or_det_expf(-pt->op));
+    const float k = fminf(9.0f, 2.0f * or_det_logf(255.0f * o));
+    f->radius_x = k > 0.f ? sqrtf(k * f->a) : 0.f;
+    f->radius_y = k > 0.f ? sqrtf(k * f->c) : 0.f;
   } else {
     f->conic[0] = f->conic[1] = f->conic[2] = 0.f;
     f->radius_x = f->radius_y = 0.f;
@@ -597,7 +625,7 @@ int32_t or_render(const float* sp, int64_t m, int32_t W, int32_t H, const float*
           const float* r = sp + (int64_t)inst[i].row * SPF;
           float dx, dy;
           const float power = splat_power(r, pxf, pyf, &dx, &dy);
-          if (power > 0.f) continue;
+          if (power > 0.f || power < -4.5f) continue; /* q > 9: outside the 3-sigma ellipse */
           const float alpha = fminf(0.99f, r[2] * expf(power));
           if (alpha < 1.f / 255.f) continue;
           const float nT = T * (1.f - alpha);
@@ -644,7 +672,7 @@ int32_t or_render_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const fl
           const float* r = sp + row * SPF;
           float dx, dy;
           const float power = splat_power(r, pxf, pyf, &dx, &dy);
-          if (power > 0.f) continue;
+          if (power > 0.f || power < -4.5f) continue; /* q > 9: outside the 3-sigma ellipse */
           const float ex = expf(power);
           const float raw = r[2] * ex;
           const float alpha = fminf(0.99f, raw);

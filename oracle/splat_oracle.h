@@ -39,6 +39,7 @@ void or_visibility_mask(const float* pos, int64_t n, const int32_t* group_begin,
 void or_morton(const float* pos, int64_t n, const float* bbox, int32_t bits,
                uint64_t* codes);
 float or_det_expf(float x);
+float or_det_logf(float x);
 
 /* params: plane layout [15][S][4].  Projects points idx[0..m) for camera c
  * into sp rows [m][12]. */

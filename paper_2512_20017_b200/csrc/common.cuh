@@ -80,6 +80,38 @@ __device__ __forceinline__ float det_expf(float x) {
   return fmul(p, __int_as_float(e << 23));
 }
 
+// ln(x) for normal x > 0: x = m 2^e with m in [sqrt(1/2), sqrt(2)),
+// ln m = 2 atanh(s), s = (m - 1) / (m + 1), odd series to s^9 (|s| <= 0.172,
+// truncation < 1e-9).  Exact IEEE ops only (host oracle: or_det_logf).
+// Non-positive or subnormal input returns -87.5 (below ln(FLT_MIN)).
+__device__ __forceinline__ float det_logf(float x) {
+  if (!(x >= 1.17549435e-38f)) return -87.5f;
+  const uint32_t ix = __float_as_uint(x);
+  int e = (int)(ix >> 23) - 127;
+  float m = __uint_as_float((ix & 0x7fffffu) | 0x3f800000u);
+  if (m > 1.41421356f) {
+    m = fmul(m, 0.5f);
+    e += 1;
+  }
+  const float s = fdiv(fsub(m, 1.0f), fadd(m, 1.0f));
+  const float s2 = fmul(s, s);
+  float p = 0x1.c71c72p-4f;              // 1/9
+  p = fadd(fmul(p, s2), 0x1.249250p-3f);  // 1/7
+  p = fadd(fmul(p, s2), 0x1.99999ap-3f);  // 1/5
+  p = fadd(fmul(p, s2), 0x1.555556p-2f);  // 1/3
+  p = fadd(fmul(p, s2), 1.0f);
+  const float lnm = fmul(fmul(2.0f, s), p);
+  const float fe = (float)e;
+  return fadd(fmul(fe, 0x1.62e400p-1f), fadd(lnm, fmul(fe, 0x1.7f7d1cp-20f)));
+}
+
+// Squared Mahalanobis extent of a 3DGS splat's support: the blend keeps a
+// pair iff q <= 9 (3-sigma ellipse) and alpha = o exp(-q/2) >= 1/255, i.e.
+// q <= min(9, 2 ln(255 o)).  <= 0: the splat can never contribute.
+__device__ __forceinline__ float support_k(float opac) {
+  return fminf(9.0f, fmul(2.0f, det_logf(fmul(255.0f, opac))));
+}
+
 __device__ __forceinline__ float det_sigmoid(float x) {
   return fdiv(1.0f, fadd(1.0f, det_expf(-x)));
 }

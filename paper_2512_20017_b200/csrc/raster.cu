@@ -7,20 +7,20 @@
 // of a tile never synchronise with each other: each walks the tile's
 // depth-sorted instance range in chunks of 32 on its own, gathering one SP
 // row per lane (the next chunk is prefetched into registers while the
-// current one is blended), keeps only the splats whose alpha >= 1/255
-// footprint can reach its region (exact bounding box of the ellipse
-// o * exp(power) = 1/255, padded by 1%), compacts them with a ballot into
-// warp-private shared memory and blends them in depth order.  Per pixel
-// (centre (x + 0.5, y + 0.5)):
-//   power = -0.5 (A dx^2 + C dy^2) - B dx dy,  dx = u - px
-//   alpha = min(0.99, opacity * exp(power)); skipped if power > 0 or
-//   alpha < 1/255; a pixel stops before the splat that would bring its
-//   transmittance below 1e-4 (standard 3DGS conventions).
+// current one is blended), keeps only the splats whose support box (the
+// projection's per-axis extents sp[10], sp[11]) can reach its region,
+// compacts them with a ballot into warp-private shared memory and blends
+// them in depth order.  Per pixel (centre (x + 0.5, y + 0.5)):
+//   power = -0.5 q = -0.5 (A dx^2 + C dy^2) - B dx dy,  dx = u - px
+//   alpha = min(0.99, opacity * exp(power)); skipped if power > 0, q > 9
+//   (outside the 3-sigma ellipse) or alpha < 1/255; a pixel stops before the
+//   splat that would bring its transmittance below 1e-4 (standard 3DGS
+//   conventions).
 // The conic is staged pre-scaled by -log2(e)/2 (B by -log2(e)) so the
 // exponent is one ex2.approx; forward and backward evaluate alpha with the
 // same instructions, so their skip / stop decisions agree exactly.
-// The footprint filter only drops splats whose every alpha at the region
-// is below 1/255, so the blend equals walking the whole list.
+// The support filter only drops splats that are skipped at every pixel of
+// the region, so the blend equals walking the whole list.
 //
 // Backward: each warp walks its own range back to front from the deepest
 // contributor of its pixels (T recovered by division).  Per splat the lanes
@@ -37,6 +37,7 @@ constexpr float kAlphaMax = 0.99f;
 constexpr float kTMin = 1e-4f;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kP2Min = -4.5f * kLog2e;  // q > 9 (outside the 3-sigma ellipse): no contribution
 #ifndef BS_SPARSE_LANES
 #define BS_SPARSE_LANES 6  // swept on B200 (C2): 0 3.15, 2 3.08, 3 3.01, 4 2.97, 5 2.92, 6 2.91, 8 2.94 ms
 #endif
@@ -76,6 +77,7 @@ struct WarpSmem {
 struct Splat {
   float4 p0, p1;  // (u v opac A), (B C r g)
   float b;
+  float2 h;       // support half-widths (hx, hy) = sp[10], sp[11]
   uint32_t row;
   bool ok;
 };
@@ -89,19 +91,19 @@ __device__ __forceinline__ void fetch_splat(Splat& f, const float* __restrict__ 
     f.p0 = __ldg(r4);
     f.p1 = __ldg(r4 + 1);
     f.b = __ldg(sp + (int64_t)f.row * BS_SP_FLOATS + 8);
+    f.h = __ldg(reinterpret_cast<const float2*>(sp + (int64_t)f.row * BS_SP_FLOATS + 10));
   }
 }
 
-// Can this splat reach alpha >= 1/255 at a pixel centre of [x0,x1] x [y0,y1]?
+// Can this splat's support (the box of half-widths hx = sp[10], hy = sp[11]
+// around (u, v), written by the projection; 0 = never contributes) reach a
+// pixel centre of [x0,x1] x [y0,y1]?  Padded by 1e-3 px + 1e-4 relative so
+// pairs on the box edge are left to the per-pixel test.
 __device__ __forceinline__ bool reaches(const Splat& f, float x0, float x1, float y0, float y1) {
-  if (!f.ok) return false;
-  const float u = f.p0.x, v = f.p0.y, A = f.p0.w, B = f.p1.x, C = f.p1.y, o = f.p0.z;
-  const float L = 2.f * __logf(255.f * o);  // q(d) <= L  <=>  o exp(-q/2) >= 1/255
-  const float detq = A * C - B * B;
-  if (!(L > 0.f) || !(detq > 0.f)) return false;
-  const float hx = sqrtf(L * C / detq) * 1.01f + 1e-3f;
-  const float hy = sqrtf(L * A / detq) * 1.01f + 1e-3f;
-  return fabsf(u - fminf(fmaxf(u, x0), x1)) <= hx && fabsf(v - fminf(fmaxf(v, y0), y1)) <= hy;
+  const float u = f.p0.x, v = f.p0.y, hx = f.h.x, hy = f.h.y;
+  if (!f.ok || !(hx > 0.f)) return false;
+  return fabsf(u - fminf(fmaxf(u, x0), x1)) <= fmaf(hx, 1.0001f, 1e-3f) &&
+         fabsf(v - fminf(fmaxf(v, y0), y1)) <= fmaf(hy, 1.0001f, 1e-3f);
 }
 
 __device__ __forceinline__ void stage(WarpSmem& s, int lane, const Splat& f) {
@@ -142,7 +144,7 @@ __device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float
                                       int rel) {
   float dx, dy;
   const float power2 = splat_power2(sa, sb.x, pxf, pyf, dx, dy);
-  if (power2 > 0.f) return;
+  if (power2 > 0.f || power2 < kP2Min) return;
   const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, ex2_approx(power2)));
   if (alpha < kAlphaMin) return;
   const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
@@ -295,7 +297,7 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
                                            float pyf, float g[9]) {
   float dx, dy;
   const float power2 = splat_power2(sa, sb.x, pxf, pyf, dx, dy);
-  if (power2 > 0.f) return false;
+  if (power2 > 0.f || power2 < kP2Min) return false;
   const float ex = ex2_approx(power2);
   const float raw = __fmul_rn(sb.y, ex);
   const float alpha = fminf(kAlphaMax, raw);

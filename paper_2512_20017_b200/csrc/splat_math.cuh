@@ -9,8 +9,10 @@
 //
 // Conventions (builder-chosen standard 3DGS, frozen here):
 //   EWA dilation 0.3 px^2, Jacobian clamp |x/z| <= 1.3 tan(fov/2),
-//   radii = ceil(3 sqrt(cov2d_xx)), ceil(3 sqrt(cov2d_yy)) (per-axis 3-sigma
-//   box, the gsplat >= 1.0 convention), SH degree <= 3 with colour
+//   support of a splat = {q <= 9} (3-sigma ellipse) intersected with
+//   {alpha >= 1/255}; radii = float half-widths sqrt(k cov2d_xx),
+//   sqrt(k cov2d_yy), k = min(9, 2 ln(255 o)): the tight bounding box of the
+//   support (opacity-aware; 0 when o < 1/255), SH degree <= 3 with colour
 //   max(sum + 0.5, 0), opacity = sigmoid(logit), scale = exp(log_scale).
 #pragma once
 #include "common.cuh"
@@ -280,9 +282,11 @@ __device__ __forceinline__ void project_forward_t(const PointIn& pt, const Point
     f.conic[0] = fdiv(f.c, f.det);
     f.conic[1] = fdiv(-f.b, f.det);
     f.conic[2] = fdiv(f.a, f.det);
-    // per-axis 3-sigma extents = the tight bounding box of the 3-sigma ellipse
-    f.radius_x = ceilf(fmul(3.f, fsqrt(f.a)));
-    f.radius_y = ceilf(fmul(3.f, fsqrt(f.c)));
+    // per-axis extents = the tight bounding box of the support ellipse
+    // q <= k, k = min(9, 2 ln(255 o)) (half-widths sqrt(k cov_xx), sqrt(k cov_yy))
+    const float k = support_k(pre.opac);
+    f.radius_x = k > 0.f ? fsqrt(fmul(k, f.a)) : 0.f;
+    f.radius_y = k > 0.f ? fsqrt(fmul(k, f.c)) : 0.f;
   } else {
     f.conic[0] = f.conic[1] = f.conic[2] = 0.f;
     f.radius_x = f.radius_y = 0.f;

@@ -135,6 +135,18 @@ def test_det_expf_accuracy():
     assert (np.abs(got - ref) / ref).max() < 5e-7
 
 
+def test_det_logf_accuracy():
+    """Deterministic ln used for the opacity-aware support extents
+    k = min(9, 2 ln(255 o)) (csrc/common.cuh det_logf)."""
+    xs = np.concatenate([np.geomspace(1e-30, 1e30, 3001), np.linspace(0.5, 2.0, 2001),
+                         255.0 * np.linspace(1e-4, 1.0, 2001)]).astype(np.float32)
+    got = np.array([py_oracle.det_logf(x) for x in xs], dtype=np.float64)
+    ref = np.log(xs.astype(np.float64))
+    err = np.abs(got - ref) / np.maximum(np.abs(ref), 1.0)
+    assert err.max() < 3e-7
+    assert py_oracle.det_logf(0.0) == -87.5 and py_oracle.det_logf(-1.0) == -87.5
+
+
 # ---------------------------------------------------------------- float half: oracle vs f64 autograd
 
 
@@ -222,7 +234,7 @@ def test_oracle_gradients_match_float64_autograd():
             A, Bc, Cc = conic[ci, 0], conic[ci, 1], conic[ci, 2]
             power = -0.5 * (A * dx * dx + Cc * dy * dy) - Bc * dx * dy
             alpha = (opac[ci] * torch.exp(power)).clamp(max=0.99)
-            keep = (power.detach() <= 0) & (alpha.detach() >= 1.0 / 255.0)
+            keep = (power.detach() <= 0) & (power.detach() >= -4.5) & (alpha.detach() >= 1.0 / 255.0)
             alpha = alpha[keep]
             cc = col[ci][keep]
             T = torch.cumprod(torch.cat([torch.ones(1, dtype=torch.float64), 1 - alpha[:-1]]), 0)
