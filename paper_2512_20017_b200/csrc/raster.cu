@@ -286,13 +286,22 @@ __device__ __forceinline__ float warp_reduce9(const float v[9], int& out_idx) {
 }
 
 struct PixelBwd {
-  float T, T_final, dC0, dC1, dC2, acc0, acc1, acc2, last_alpha, lc0, lc1, lc2, bgdot;
+  float T, T_final, dC0, dC1, dC2, acc0, acc1, acc2, bgdot;
   int n;
 };
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // Gradient contribution of one splat at one pixel.  kAssign: writes all 9
 // terms of g when it returns true (g untouched otherwise); else adds into g.
-template <bool kAssign>
+// acc = colour blended behind this splat, normalised by the transmittance
+// in front of it: acc' = acc + alpha (c - acc) after the splat.  kBg: the
+// background is not black (adds its transmittance term to dL/dalpha).
+template <bool kAssign, bool kBg>
 __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const float4& sb, float cb, float pxf,
                                            float pyf, float g[9]) {
   float dx, dy;
@@ -302,18 +311,15 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
   const float raw = __fmul_rn(sb.y, ex);
   const float alpha = fminf(kAlphaMax, raw);
   if (alpha < kAlphaMin) return false;
-  const float ra = __fdividef(1.f, 1.f - alpha);  // alpha <= 0.99: fast reciprocal is safe
+  const float ra = rcp_approx(1.f - alpha);  // alpha <= 0.99
   p.T = p.T * ra;
   const float fac = alpha * p.T;
-  p.acc0 = p.last_alpha * p.lc0 + (1.f - p.last_alpha) * p.acc0;
-  p.acc1 = p.last_alpha * p.lc1 + (1.f - p.last_alpha) * p.acc1;
-  p.acc2 = p.last_alpha * p.lc2 + (1.f - p.last_alpha) * p.acc2;
-  p.last_alpha = alpha;
-  p.lc0 = sb.z;
-  p.lc1 = sb.w;
-  p.lc2 = cb;
-  float dL_dalpha = p.T * ((sb.z - p.acc0) * p.dC0 + (sb.w - p.acc1) * p.dC1 + (cb - p.acc2) * p.dC2);
-  dL_dalpha -= p.T_final * ra * p.bgdot;
+  const float e0 = sb.z - p.acc0, e1 = sb.w - p.acc1, e2 = cb - p.acc2;
+  float dL_dalpha = p.T * (e0 * p.dC0 + e1 * p.dC1 + e2 * p.dC2);
+  if (kBg) dL_dalpha -= p.T_final * ra * p.bgdot;
+  p.acc0 = fmaf(alpha, e0, p.acc0);
+  p.acc1 = fmaf(alpha, e1, p.acc1);
+  p.acc2 = fmaf(alpha, e2, p.acc2);
   // clamped alpha (raw > 0.99): colour gradient only
   const float dpow = raw > kAlphaMax ? 0.f : dL_dalpha * alpha;  // dL / d power
   // d power / d(u, v) = -(A dx + B dy, B dx + C dy) = (2 kA dx + kB dy, kB dx + 2 kC dy) ln 2
@@ -322,9 +328,10 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
   t[0] = (2.f * sa.z * dx + sa.w * dy) * dpl;
   t[1] = (sa.w * dx + 2.f * sb.x * dy) * dpl;
   t[2] = raw > kAlphaMax ? 0.f : dL_dalpha * ex;
-  t[3] = -0.5f * dx * dx * dpow;
-  t[4] = -dx * dy * dpow;
-  t[5] = -0.5f * dy * dy * dpow;
+  const float hdx = -0.5f * dpow * dx;
+  t[3] = hdx * dx;
+  t[4] = 2.f * hdx * dy;
+  t[5] = -0.5f * dpow * dy * dy;
   t[6] = fac * p.dC0;
   t[7] = fac * p.dC1;
   t[8] = fac * p.dC2;
@@ -362,10 +369,10 @@ __device__ __forceinline__ void init_pixel_bwd(PixelBwd& q, const RastArgs& a, i
   }
   q.T_final = q.T;
   q.bgdot = a.bg[0] * q.dC0 + a.bg[1] * q.dC1 + a.bg[2] * q.dC2;
-  q.acc0 = q.acc1 = q.acc2 = q.last_alpha = q.lc0 = q.lc1 = q.lc2 = 0.f;
+  q.acc0 = q.acc1 = q.acc2 = 0.f;
 }
 
-template <int PPL>
+template <int PPL, bool kBg>
 __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768) / Region<PPL>::kThreads) raster_bwd_kernel(
     RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
     const float* __restrict__ image, const float* __restrict__ final_T, const int32_t* __restrict__ n_contrib,
@@ -409,13 +416,13 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
       const float cb = s.c[j];
       bool any = false;
       if constexpr (PPL == 1) {
-        if (rel < p[0].n) any = pixel_grad<true>(p[0], sa, sb, cb, pxf, (float)q.py0 + 0.5f, g);
+        if (rel < p[0].n) any = pixel_grad<true, kBg>(p[0], sa, sb, cb, pxf, (float)q.py0 + 0.5f, g);
       } else {
 #pragma unroll
         for (int k = 0; k < 9; ++k) g[k] = 0.f;
 #pragma unroll
         for (int k = 0; k < PPL; ++k)
-          if (rel < p[k].n) any |= pixel_grad<false>(p[k], sa, sb, cb, pxf, (float)(q.py0 + k) + 0.5f, g);
+          if (rel < p[k].n) any |= pixel_grad<false, kBg>(p[k], sa, sb, cb, pxf, (float)(q.py0 + k) + 0.5f, g);
       }
       const uint32_t who = __ballot_sync(0xffffffffu, any);
       if (who == 0u) continue;
@@ -537,14 +544,15 @@ extern "C" int32_t bs_raster_bwd(const bs_raster_desc* d, const float* sp_rows, 
   if (st) return st;
   BS_REQUIRE(grad_image || (image && gt), BS_ERR_PARAMETER, "raster_bwd needs grad_image or (image, gt)");
   const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
+  const bool bg = a.bg[0] != 0.f || a.bg[1] != 0.f || a.bg[2] != 0.f;
+  auto launch = [&](auto kern, int threads) {
+    kern<<<grid, threads, 0, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image,
+                                                  final_T, n_contrib, grad_image, gt, gt_slot_view, g_sp);
+  };
   if (d->pixels_per_lane == 1)
-    raster_bwd_kernel<1><<<grid, Region<1>::kThreads, 0, as_stream(stream)>>>(
-        a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image, final_T, n_contrib, grad_image, gt,
-        gt_slot_view, g_sp);
+    bg ? launch(raster_bwd_kernel<1, true>, Region<1>::kThreads) : launch(raster_bwd_kernel<1, false>, Region<1>::kThreads);
   else
-    raster_bwd_kernel<2><<<grid, Region<2>::kThreads, 0, as_stream(stream)>>>(
-        a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image, final_T, n_contrib, grad_image, gt,
-        gt_slot_view, g_sp);
+    bg ? launch(raster_bwd_kernel<2, true>, Region<2>::kThreads) : launch(raster_bwd_kernel<2, false>, Region<2>::kThreads);
   BS_LAUNCH_CHECK("raster_bwd_kernel");
   return BS_OK;
 }

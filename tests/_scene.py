@@ -31,7 +31,7 @@ def c1_setup(G: int = 256, **over):
     return ds, params, gb, aabb, gt
 
 
-def oracle_view_pipeline(params, gb, aabb, view, cam_bytes, gt_img, sh_degree=3, model="3dgs"):
+def oracle_view_pipeline(params, gb, aabb, view, cam_bytes, gt_img, sh_degree=3, model="3dgs", bg=(0.0, 0.0, 0.0)):
     """Oracle forward + backward of one view; returns dict of intermediates."""
     from oracle import py_oracle
 
@@ -40,9 +40,9 @@ def oracle_view_pipeline(params, gb, aabb, view, cam_bytes, gt_img, sh_degree=3,
     mask = py_oracle.visibility_mask(pos, gb, aabb, planes, 1)
     idx = np.flatnonzero(mask & 1).astype(np.int64)
     sp = py_oracle.project(params, idx, cam_bytes, sh_degree, model=model)
-    img, T, nc, lists, ranges = py_oracle.render(sp, view.width, view.height, want_lists=True, model=model)
+    img, T, nc, lists, ranges = py_oracle.render(sp, view.width, view.height, bg=bg, want_lists=True, model=model)
     loss, gimg = py_oracle.l1_loss(img, gt_img)
-    gsp = py_oracle.render_bwd(sp, view.width, view.height, T, nc, gimg, model=model)
+    gsp = py_oracle.render_bwd(sp, view.width, view.height, T, nc, gimg, bg=bg, model=model)
     gparams = py_oracle.project_bwd(params, idx, cam_bytes, sh_degree, gsp, model=model)
     return dict(mask=mask, idx=idx, sp=sp, img=img, T=T, nc=nc, lists=lists, ranges=ranges, loss=loss, gimg=gimg,
                 gsp=gsp, gparams=gparams)

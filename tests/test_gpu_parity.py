@@ -173,9 +173,10 @@ def test_projection_bitexact_and_binning(c1, cuda):
             assert np.array_equal(a, b), f"view {v} tile {t}"
 
 
-def test_render_forward_and_backward_tolerance(c1, cuda):
+@pytest.mark.parametrize("bg", [(0.0, 0.0, 0.0), (0.2, 0.5, 0.9)])
+def test_render_forward_and_backward_tolerance(c1, cuda, bg):
     ds, params, gb, aabb, gt = c1
-    tr = _trainer(c1)
+    tr = _trainer(c1, bg=bg)
     batch = [1, 6]
     losses = tr.step(batch).cpu().numpy()
     n = tr.last["n_rows"]
@@ -185,7 +186,7 @@ def test_render_forward_and_backward_tolerance(c1, cuda):
     rows = tr.last["rows_per_view"]
     row0 = np.concatenate([[0], np.cumsum(rows)])
     for s, v in enumerate(batch):
-        ref = oracle_view_pipeline(params, gb, aabb, ds.views[v], camera_bytes([ds.views[v]]), gt[v])
+        ref = oracle_view_pipeline(params, gb, aabb, ds.views[v], camera_bytes([ds.views[v]]), gt[v], bg=bg)
         assert np.abs(img[s] - ref["img"]).max() <= IMG_TOL
         assert abs(losses[s] - ref["loss"]) <= 1e-5
         g = gsp[row0[s]:row0[s + 1]]
