@@ -73,10 +73,18 @@ int64_t bs_launch_count(void);
  * Table tab:states-3dgs + 1 pad:
  *   0 u  1 v  2 opacity  3 conic_a  4 conic_b  5 conic_c
  *   6 r  7 g  8 b        9 depth    10 radius_x  11 radius_y
- * (the paper's single "radii" element is stored per axis: the tight box of
- * the 3-sigma ellipse, gsplat >= 1.0 convention) */
+ * (the paper's single "radii" element is stored per axis as float
+ * half-widths: the tight box of the splat's support q <= min(9, 2 ln(255 o)),
+ * i.e. the 3-sigma ellipse cut by alpha >= 1/255; 0 = never contributes) */
 #define BS_SP_FLOATS 12
-/* gradient row (G_SP): 9 floats (d u, d v, d opacity, d conic a/b/c, d rgb) */
+/* gradient row (G_SP): 9 floats as written by bs_raster_bwd -- moments of
+ * dL/dpower over the pixels (power = -q/2, dx = u - px, dy = v - py):
+ *   0 sum dpow dx  1 sum dpow dy  2 dL/dopacity  3 sum dpow dx^2
+ *   4 sum dpow dx dy  5 sum dpow dy^2  6..8 dL/drgb
+ * The projection backward, which has the conic (A, B, C), turns them into
+ * dL/du = -(A m0 + B m1), dL/dv = -(B m0 + C m1), dL/dA = -m3/2,
+ * dL/dB = -m4, dL/dC = -m5/2 (bs_proj_desc.gsp_form = 1 accepts plain
+ * dL/dSP instead: d u, d v, d opacity, d conic a/b/c, d rgb). */
 #define BS_GSP_FLOATS 9
 #define BS_TILE 16
 
@@ -190,6 +198,9 @@ typedef struct {
   int32_t max_group_points; /* largest group size; > 0 lets the per-point
                                kernels split a group over several CTAs (one
                                per 256 points), 0 = one CTA per group */
+  int32_t gsp_form;  /* 3DGS G_SP rows given to the projection backward:
+                        0 = raster moments (bs_raster_bwd output, default),
+                        1 = plain dL/dSP (d u, d v, d opacity, d conic, d rgb) */
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,

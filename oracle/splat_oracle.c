@@ -365,8 +365,16 @@ void or_project(const float* params, int64_t S, const int64_t* idx, int64_t m, c
 
 /* Analytic backward of proj_fwd (chain rule written out independently of the
  * CUDA file; checked against float64 autograd in tests). */
-static void proj_bwd(const opoint* pt, const or_camera* c, int n_sh, const oproj* f, const float* gsp, float* g) {
+static void proj_bwd(const opoint* pt, const or_camera* c, int n_sh, const oproj* f, const float* gsp_m, float* g) {
   if (!f->valid) return;
+  /* G_SP moments -> dL/d(u, v, opacity, conic, rgb) with this view's conic */
+  float gsp[9];
+  for (int k = 0; k < 9; ++k) gsp[k] = gsp_m[k];
+  gsp[0] = -(f->conic[0] * gsp_m[0] + f->conic[1] * gsp_m[1]);
+  gsp[1] = -(f->conic[1] * gsp_m[0] + f->conic[2] * gsp_m[1]);
+  gsp[3] = -0.5f * gsp_m[3];
+  gsp[4] = -gsp_m[4];
+  gsp[5] = -0.5f * gsp_m[5];
   float dc[3];
   for (int ch = 0; ch < 3; ++ch) dc[ch] = f->col_raw[ch] >= 0.f ? gsp[6 + ch] : 0.f;
   float wk[16] = {0};
@@ -689,13 +697,14 @@ int32_t or_render_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const fl
           for (int ch = 0; ch < 3; ++ch) dL_da += (r[6 + ch] - acc[ch]) * dC[ch];
           dL_da = T * dL_da - T_final * ra * bgdot;
           if (raw > 0.99f) continue; /* clamped alpha: no gradient to opacity/geometry */
+          /* G_SP: moments of dpow = dL/dpower (include/splat_b200.h) */
           const float dpow = dL_da * alpha;
           g[2] += dL_da * ex;
-          g[3] += -0.5f * dx * dx * dpow;
-          g[4] += -dx * dy * dpow;
-          g[5] += -0.5f * dy * dy * dpow;
-          g[0] += -(r[3] * dx + r[4] * dy) * dpow;
-          g[1] += -(r[4] * dx + r[5] * dy) * dpow;
+          g[0] += dpow * dx;
+          g[1] += dpow * dy;
+          g[3] += dpow * dx * dx;
+          g[4] += dpow * dx * dy;
+          g[5] += dpow * dy * dy;
         }
       }
   }

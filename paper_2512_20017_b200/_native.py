@@ -56,7 +56,7 @@ GSP2_FLOATS = 15
 class ProjDesc(C.Structure):
     _fields_ = [("n_views", C.c_int32), ("sh_degree", C.c_int32),
                 ("tiles_x_max", C.c_int32), ("tiles_y_max", C.c_int32), ("model", C.c_int32),
-                ("max_group_points", C.c_int32)]
+                ("max_group_points", C.c_int32), ("gsp_form", C.c_int32)]
 
 
 class RasterDesc(C.Structure):

@@ -80,6 +80,7 @@ struct ProjArgs {
   const int32_t* base;  // [ng][B]
   const int64_t* view_row0;
   const bs_camera* cams;
+  int gsp_standard;  // 3DGS G_SP rows: 0 = raster moments (default), 1 = dL/dSP
 };
 
 // Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
@@ -103,6 +104,8 @@ struct Model3 {
     project_backward_t(pt, r, sh, c, n_sh, f, gs, g, acc, add);
   }
   __device__ static void finish(const PointIn& pt, const float* acc, float* g) { point_pre_backward(pt, acc, g); }
+  // raster moments (M1..M5 of dL/dpower) -> dL/d(u, v, conic a, b, c)
+  __device__ static void from_moments(const F& f, float* gs) { gsp_from_moments(f.conic, gs); }
 };
 
 struct Model2 {
@@ -121,6 +124,7 @@ struct Model2 {
     project2d_backward(pt, r, sh, c, n_sh, f, gs, g, acc, add);
   }
   __device__ static void finish(const PointIn& pt, const float* acc, float* g) { point_pre2_backward(pt, acc, g); }
+  __device__ static void from_moments(const F&, float*) {}
 };
 
 template <class M>
@@ -184,6 +188,7 @@ __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camer
     for (int k = 0; k < M::kGSP; ++k) gs[k] = src[k];
     typename M::F f;
     M::forward(pt, pre, sh, s_cam[v], a.n_sh, f);
+    if (!a.gsp_standard) M::from_moments(f, gs);
     M::backward(pt, pre, sh, s_cam[v], a.n_sh, f, gs, g, acc, sh_add);
   }
   M::finish(pt, acc, g);
@@ -470,7 +475,7 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
   if (n_groups == 0) return BS_OK;
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams};
+             view_row0, cams, d->gsp_form};
   const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
     project_fwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
@@ -489,7 +494,7 @@ extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, in
   if (n_groups == 0) return BS_OK;
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams};
+             view_row0, cams, d->gsp_form};
   const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
     project_bwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(
@@ -525,7 +530,7 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   if (n_groups == 0) return BS_OK;
   const int n_sh = (pd->sh_degree + 1) * (pd->sh_degree + 1);
   ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams};
+             view_row0, cams, pd->gsp_form};
   AdamConsts c = make_adam(ad);
   const size_t smem = sizeof(float) * 48 * kProjThreads;
   auto launch = [&](auto kern) {

@@ -36,7 +36,6 @@ constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kAlphaMax = 0.99f;
 constexpr float kTMin = 1e-4f;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kP2Min = -4.5f * kLog2e;  // q > 9 (outside the 3-sigma ellipse): no contribution
 #ifndef BS_SPARSE_LANES
 #define BS_SPARSE_LANES 6  // swept on B200 (C2): 0 3.15, 2 3.08, 3 3.01, 4 2.97, 5 2.92, 6 2.91, 8 2.94 ms
@@ -46,6 +45,12 @@ constexpr int kSparseLanes = BS_SPARSE_LANES;  // contributing lanes handled wit
 __device__ __forceinline__ float ex2_approx(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 
@@ -290,12 +295,6 @@ struct PixelBwd {
   int n;
 };
 
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-
 // Gradient contribution of one splat at one pixel.  kAssign: writes all 9
 // terms of g when it returns true (g untouched otherwise); else adds into g.
 // acc = colour blended behind this splat, normalised by the transmittance
@@ -320,18 +319,17 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
   p.acc0 = fmaf(alpha, e0, p.acc0);
   p.acc1 = fmaf(alpha, e1, p.acc1);
   p.acc2 = fmaf(alpha, e2, p.acc2);
-  // clamped alpha (raw > 0.99): colour gradient only
+  // clamped alpha (raw > 0.99): colour gradient only.  G_SP carries the
+  // moments of dL/dpower (power = -q/2) over the pixels; the projection
+  // backward applies the conic (include/splat_b200.h, G_SP row).
   const float dpow = raw > kAlphaMax ? 0.f : dL_dalpha * alpha;  // dL / d power
-  // d power / d(u, v) = -(A dx + B dy, B dx + C dy) = (2 kA dx + kB dy, kB dx + 2 kC dy) ln 2
-  const float dpl = dpow * kLn2;
   float t[9];
-  t[0] = (2.f * sa.z * dx + sa.w * dy) * dpl;
-  t[1] = (sa.w * dx + 2.f * sb.x * dy) * dpl;
+  t[0] = dpow * dx;
+  t[1] = dpow * dy;
   t[2] = raw > kAlphaMax ? 0.f : dL_dalpha * ex;
-  const float hdx = -0.5f * dpow * dx;
-  t[3] = hdx * dx;
-  t[4] = 2.f * hdx * dy;
-  t[5] = -0.5f * dpow * dy * dy;
+  t[3] = t[0] * dx;
+  t[4] = t[0] * dy;
+  t[5] = t[1] * dy;
   t[6] = fac * p.dC0;
   t[7] = fac * p.dC1;
   t[8] = fac * p.dC2;

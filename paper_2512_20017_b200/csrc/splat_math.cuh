@@ -318,6 +318,20 @@ __device__ __forceinline__ void write_sp_row(float* __restrict__ row, const Proj
   r4[2] = make_float4(f.col[2], f.depth, f.valid ? f.radius_x : 0.f, f.valid ? f.radius_y : 0.f);
 }
 
+// G_SP rows from the rasteriser hold moments of dL/dpower over the pixels,
+// power = -q/2, d = (u - px, v - py): M1 = sum dpow dx, M2 = sum dpow dy,
+// M3..M5 = sum dpow (dx^2, dx dy, dy^2).  With conic (A, B, C):
+// dL/du = -(A M1 + B M2), dL/dv = -(B M1 + C M2), dL/dA = -M3/2,
+// dL/dB = -M4, dL/dC = -M5/2 (entries 2, 6..8 are already dL/dSP).
+__device__ __forceinline__ void gsp_from_moments(const float conic[3], float* gs) {
+  const float m1 = gs[0], m2 = gs[1];
+  gs[0] = -(conic[0] * m1 + conic[1] * m2);
+  gs[1] = -(conic[1] * m1 + conic[2] * m2);
+  gs[3] = -0.5f * gs[3];
+  gs[4] = -gs[4];
+  gs[5] = -0.5f * gs[5];
+}
+
 // Gradient of the 60-float parameter row of one point (plane layout order:
 // mean xyz, opacity logit, log scales xyz, pad, quat wxyz, sh[48]).
 struct PointGrad {

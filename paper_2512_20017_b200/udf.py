@@ -162,7 +162,7 @@ class _ProjectFn(torch.autograd.Function):
         else:
             gsp = g[:, :nat.GSP_FLOATS].contiguous()
         grad = torch.zeros_like(planes)
-        desc = nat.ProjDesc(1, ctx.sh_degree, 0, 0, ctx.model_id, _CHUNK)
+        desc = nat.ProjDesc(1, ctx.sh_degree, 0, 0, ctx.model_id, _CHUNK, 1)  # gsp_form 1: plain dL/dSP
         nat.call("bs_project_bwd", desc, nat.ptr(planes), V, nat.ptr(mask), nat.ptr(gb), ctx.ng, nat.ptr(base),
                  nat.ptr(row0), nat.ptr(cam), nat.ptr(gsp), nat.ptr(grad), nat.stream_handle())
         return grad, None, None, None, None
@@ -243,7 +243,16 @@ class _RenderFn(torch.autograd.Function):
             grad_rows[:, 2] = g_sp[:, 11]
             grad_rows[:, 12:15] = g_sp[:, 12:15]
         else:
-            grad_rows[:, :gw] = g_sp
+            # G_SP moments of dL/dpower (include/splat_b200.h) -> dL/d(u, v, conic)
+            A, Bc, Cc = rows[:, 3], rows[:, 4], rows[:, 5]
+            m1, m2 = g_sp[:, 0], g_sp[:, 1]
+            grad_rows[:, 0] = -(A * m1 + Bc * m2)
+            grad_rows[:, 1] = -(Bc * m1 + Cc * m2)
+            grad_rows[:, 2] = g_sp[:, 2]
+            grad_rows[:, 3] = -0.5 * g_sp[:, 3]
+            grad_rows[:, 4] = -g_sp[:, 4]
+            grad_rows[:, 5] = -0.5 * g_sp[:, 5]
+            grad_rows[:, 6:9] = g_sp[:, 6:9]
         return grad_rows, None, None, None, None, None
 
 
