@@ -1,0 +1,36 @@
+/* Host-side native library of the B200 PBDR training path (libsplat_host.so).
+ *
+ * C ABI (plain pointers and sizes), no CUDA: the offline and online
+ * scheduling algorithms of the reference that run on the host between GPU
+ * steps, re-implemented in C++ so they scale to the BASELINE configs.
+ *
+ * Status codes follow include/splat_b200.h (0 OK, 1 ParameterError). */
+#ifndef SPLAT_HOST_H
+#define SPLAT_HOST_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BS_HOST_OK 0
+#define BS_HOST_ERR_PARAMETER 1
+
+/* One run of the multilevel k-way partitioner -- replaces Multilevel.run of
+ * /root/reference/pkg/src/splatsched/partition.py:104-434 (called by
+ * partition_graph, partition.py:398-434, once per seed run).  Graph: n
+ * vertices with balance weights, n_edges undirected edges (eu[e], ev[e],
+ * ew[e]); parts >= 2; eps = balance slack.  pcg_state: numpy PCG64 state of
+ * np.random.default_rng(SeedSequence([seed, run])) as
+ * {state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger}.  Output:
+ * labels int64[n], identical to the reference's for integer weights. */
+int32_t bs_partition_multilevel(int64_t n, const double* balance, int64_t n_edges, const int64_t* eu,
+                                const int64_t* ev, const double* ew, int32_t parts, double eps,
+                                const uint64_t* pcg_state, int64_t* labels);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPLAT_HOST_H */

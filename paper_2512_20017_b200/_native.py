@@ -142,6 +142,40 @@ def load(require_cuda: bool = True):
     return _lib
 
 
+_HOST_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsplat_host.so")
+_host = None
+_HOST_SIGS = {
+    "bs_partition_multilevel": (_I32, [_I64, _P, _I64, _P, _P, _P, _I32, C.c_double, _P, _P]),
+}
+HOST_EXPORTED = tuple(_HOST_SIGS)
+
+
+def host_lib_path() -> str:
+    return _HOST_PATH
+
+
+def load_host():
+    """Host-side scheduling library (include/splat_host.h; C++, no CUDA)."""
+    global _host
+    with _lock:
+        if _host is None:
+            if not os.path.exists(_HOST_PATH):
+                raise NativeError(f"host library not built: {_HOST_PATH} (run __graft_entry__.build())")
+            lib = C.CDLL(_HOST_PATH)
+            for name, (res, args) in _HOST_SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _host = lib
+    return _host
+
+
+def host_call(name: str, *args) -> None:
+    st = getattr(load_host(), name)(*args)
+    if st != 0:
+        raise_for_status(st, f"{name} rejected its arguments")
+
+
 def call(name: str, *args) -> None:
     """Invoke a bs_* entry point and map a nonzero status to an exception."""
     lib = load()

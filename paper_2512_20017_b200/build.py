@@ -14,6 +14,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libsplat_b200.so")
+HOST_LIB = os.path.join(LIBDIR, "libsplat_host.so")
+HOST_SOURCES = ["host/partition.cpp"]
 ORACLE_DIR = os.path.join(ROOT, "oracle")
 ORACLE_LIB = os.path.join(ORACLE_DIR, "build", "libsplat_oracle.so")
 
@@ -64,6 +66,16 @@ def build_native(force: bool = False, verbose: bool = False, extra_flags=()) -> 
     return LIB
 
 
+def build_host(force: bool = False, verbose: bool = False) -> str:
+    """Compile the host-side scheduling library (C++, no CUDA) in-tree."""
+    os.makedirs(LIBDIR, exist_ok=True)
+    srcs = [os.path.join(CSRC, s) for s in HOST_SOURCES]
+    hdr = os.path.join(ROOT, "include", "splat_host.h")
+    if force or not _newer(HOST_LIB, srcs + [hdr]):
+        _run(["g++", "-O3", "-std=c++17", "-fPIC", "-shared", "-fopenmp", "-Wall", "-o", HOST_LIB, *srcs], verbose)
+    return HOST_LIB
+
+
 def build_oracle(force: bool = False, verbose: bool = False) -> str:
     """Compile the CPU oracle (test infrastructure only) with gcc."""
     src = os.path.join(ORACLE_DIR, "splat_oracle.c")
@@ -80,5 +92,6 @@ if __name__ == "__main__":
     f = "-f" in sys.argv
     # BS_NVCC_EXTRA: extra nvcc flags for tuning experiments (e.g. -DBS_SPARSE_LANES=5)
     print(build_native(force=f, verbose=v, extra_flags=os.environ.get("BS_NVCC_EXTRA", "").split()))
+    print(build_host(force=f, verbose=v))
     if os.path.exists(os.path.join(ORACLE_DIR, "splat_oracle.c")):
         print(build_oracle(force=f, verbose=v))
