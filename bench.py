@@ -180,7 +180,8 @@ def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps, row_byt
                                                   random_point_gpus)
     from paper_2512_20017_b200.culling import build_access_matrix
 
-    t = torch.tensor([comm.bytes_fwd, comm.bytes_bwd], dtype=torch.float64, device="cuda")
+    dev = "cpu" if comm.host_staging else "cuda"
+    t = torch.tensor([comm.bytes_fwd, comm.bytes_bwd], dtype=torch.float64, device=dev)
     torch.distributed.all_reduce(t)
     fwd, bwd = (float(x) / steps for x in t.tolist())
     topo = ClusterTopology(world, 1, 25e9, 300e9)
@@ -241,6 +242,16 @@ def kernel_bytes(stage, last, S, B, model="3dgs"):
     return None
 
 
+def _max_over_ranks(vals):
+    import torch
+    import torch.distributed as dist
+
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
 def run_ours(args, cfg):
     import torch
 
@@ -251,14 +262,15 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % torch.cuda.device_count())
     comm, part_info = None, {}
     if world > 1:
         import torch.distributed as dist
 
         from paper_2512_20017_b200.exchange import SplatExchange
 
-        dist.init_process_group("nccl")
+        # BS_DIST_BACKEND=gloo: several ranks sharing one GPU (plumbing tests)
+        dist.init_process_group(os.environ.get("BS_DIST_BACKEND", "nccl"))
         cfg = weak_scaled(cfg, world)
     t0 = time.time()
     ds, g, params, gt = build_scene(cfg)
@@ -277,8 +289,9 @@ def run_ours(args, cfg):
     # region (nvidia-smi needs ~0.5 s to start streaming)
     clk = ClockSampler(local).__enter__()
     time.sleep(1.0)
+    nxt = (lambda i: sched[i + 1]) if comm is not None else (lambda i: None)  # async placement (N > 1)
     for i in range(args.warmup):
-        tr.step(sched[i])
+        tr.step(sched[i], next_batch=nxt(i))
     torch.cuda.synchronize()
     # ---- timed region: device-resident inputs
     tr.timers = {}
@@ -292,8 +305,11 @@ def run_ours(args, cfg):
     if comm is not None:
         comm.bytes_fwd = comm.bytes_bwd = 0
     start.record()
+    if comm is not None:
+        comm.place_ms.clear()
+        comm.wait_ms.clear()
     for i in range(args.steps):
-        tr.step(sched[args.warmup + i])
+        tr.step(sched[args.warmup + i], next_batch=nxt(args.warmup + i))
         inst.append(tr.last["n_inst"])
         rows.append(tr.last["n_rows"])
         if comm is not None:
@@ -307,16 +323,17 @@ def run_ours(args, cfg):
     tr.last["n_visible_points"] = int((tr.buf.bufs["mask"][: tr.S] != 0).sum().item())
     ms = start.elapsed_time(end)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _max_over_ranks([ms])[0]
     stage_ms = {k: float(np.mean([s.elapsed_time(e) for s, e in v])) for k, v in tr.timers.items()}
     tr.timers = None
     ms_per_step = ms / args.steps
     images = B * args.steps
     value = images / (ms / 1000.0)
     comm_report = None
+    placement = None
     if comm is not None:
+        placement = {"async": True, "stale_steps": 1, "host_place_ms": round(float(np.mean(comm.place_ms)), 3),
+                     "step_wait_ms": round(float(np.mean(comm.wait_ms)), 3) if comm.wait_ms else None}
         comm_report = comm_bytes_report(comm, step_AW, sched[args.warmup:args.warmup + args.steps], ds, g,
                                         world, rank, args.steps, row_bytes=4 * tr.sp_floats,
                                         grad_bytes=4 * tr.gsp_floats)
@@ -349,7 +366,8 @@ def run_ours(args, cfg):
         if i + 1 < len(e2e_sched):
             upload(i + 1)
         torch.cuda.current_stream().wait_event(ready[i % 2])
-        losses = tr.step(b, gt_batch=gt_bufs[i % 2])
+        losses = tr.step(b, gt_batch=gt_bufs[i % 2],
+                         next_batch=e2e_sched[i + 1] if comm is not None and i + 1 < len(e2e_sched) else None)
         ev = torch.cuda.Event()
         ev.record()
         freed[i % 2] = ev
@@ -359,9 +377,7 @@ def run_ours(args, cfg):
     e2e_ms = e_start.elapsed_time(e_end)
     e2e_wall = (time.perf_counter() - t_e2e0) * 1000.0
     if world > 1:
-        t = torch.tensor([e2e_ms, e2e_wall], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms, e2e_wall = (float(x) for x in t.tolist())
+        e2e_ms, e2e_wall = _max_over_ranks([e2e_ms, e2e_wall])
     e2e_value = B * len(e2e_sched) / (max(e2e_ms, e2e_wall) / 1000.0)
     # ---- roofline of the dominant kernel
     peak, peak_kind = _peaks()
@@ -397,6 +413,7 @@ def run_ours(args, cfg):
             "e2e": {"value": round(e2e_value, 3), "unit": "images/s", "h2d_bytes_per_step": B * H * W * 3 * world,
                     "d2h_bytes_per_step": 4 * B},
             "comm": comm_report,
+            "placement": placement,
             "partition": {k: v for k, v in part_info.items() if k != "owner"} or None,
             "roofline": roof,
             "stages": stages,

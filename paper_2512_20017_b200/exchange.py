@@ -17,10 +17,21 @@ sources, so they land in the send layout where the projection backward
 finds them by the same row index.  Split sizes follow from A alone; no
 extra size exchange is needed.  With P = 1 the rows moved are exactly the
 A-predicted transfers of account_iteration (simulator.py:134-183).
+
+Asynchronous online placement:
+with `prefetch`, the access counts of the NEXT batch (culled on the GPU at
+the start of the current step, i.e. before its Adam update: stale by one
+step, the staleness simulator.py:40-45 models) are all-gathered
+asynchronously and a host thread computes its W while the GPU runs the
+current step.  The next step still all-gathers its fresh counts, which fix
+the split sizes; only W comes from the stale matrix, so the exchange stays
+exact and the placement leaves the critical path.
 """
 
 from __future__ import annotations
 
+import concurrent.futures as cf
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -83,6 +94,11 @@ class SplatExchange:
         self.bytes_bwd = 0
         # gloo (CPU tests, several ranks sharing one GPU) moves host tensors only
         self.host_staging = dist.get_backend(group) == "gloo"
+        self._pool = cf.ThreadPoolExecutor(max_workers=1, thread_name_prefix="placement")
+        self._ahead = None       # (key, future of W)
+        self.place_ms = []       # host placement time per W (ms)
+        self.wait_ms = []        # time the step waited for a prefetched W (ms)
+        self.prefetched = 0
 
     def _stage(self, t: torch.Tensor) -> torch.Tensor:
         return t.cpu() if self.host_staging else t
@@ -94,10 +110,54 @@ class SplatExchange:
         dist.all_gather_into_tensor(out, src, group=self.group)
         return out.view(self.world, -1).t().cpu().numpy().astype(np.int64)
 
-    def assign(self, A: np.ndarray) -> np.ndarray:
-        """W <- AssignImages(A): hierarchical_place on a one-box topology (N, 1)."""
+    def _place(self, A: np.ndarray) -> np.ndarray:
+        t = time.perf_counter()
         B, N = A.shape
-        return hierarchical_place(A, N, 1, self.inter, self.intra).assignment
+        W = hierarchical_place(A, N, 1, self.inter, self.intra).assignment
+        self.place_ms.append(1e3 * (time.perf_counter() - t))
+        return W
+
+    def assign(self, A: np.ndarray, key=None) -> np.ndarray:
+        """W <- AssignImages(A): hierarchical_place on a one-box topology
+        (N, 1); the W prefetched for `key` (stale by one step) when there is one."""
+        if key is not None and self._ahead is not None and self._ahead[0] == key:
+            fut = self._ahead[1]
+            self._ahead = None
+            t = time.perf_counter()
+            W = fut.result()
+            self.wait_ms.append(1e3 * (time.perf_counter() - t))
+            self.prefetched += 1
+            return W
+        self._ahead = None
+        return self._place(A)
+
+    def prefetch(self, col_next: torch.Tensor, key) -> None:
+        """Start the all-gather of the next batch's counts and its placement
+        on the host thread (collective issued here, in program order)."""
+        src = self._stage(col_next.contiguous())
+        out = torch.empty(self.world * col_next.numel(), dtype=col_next.dtype, device=src.device)
+        work = dist.all_gather_into_tensor(out, src, group=self.group, async_op=True)
+        if out.is_cuda:
+            work.wait()  # stream-ordered: later work on this stream sees the result
+            host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+            host.copy_(out, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+
+            def ready():
+                ev.synchronize()
+                return host
+        else:
+            def ready():
+                work.wait()
+                return out
+        world = self.world
+
+        def job():
+            A = ready().view(world, -1).t().numpy().astype(np.int64)
+            return self._place(A)
+
+        self._ahead = (key, self._pool.submit(job))
 
     def _a2a(self, send: torch.Tensor, send_rows, recv_rows, width: int) -> torch.Tensor:
         src = self._stage(send.view(-1, width))

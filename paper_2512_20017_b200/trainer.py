@@ -184,32 +184,48 @@ class SplatTrainer:
         return _T()
 
     # ------------------------------------------------------------------ step
-    def step(self, batch_ids, gt_batch: torch.Tensor | None = None):
+    def _cull_counts(self, batch_ids, mask, counts, base, view_rows, view_row0, st):
+        B = len(batch_ids)
+        bidx = torch.as_tensor(np.asarray(batch_ids, dtype=np.int64), device=self.dev)
+        planes = self.planes_all.index_select(0, bidx).contiguous()
+        temporal = self.presence is not None
+        times = self.view_times.index_select(0, bidx).contiguous() if temporal else None
+        desc = nat.CullDesc(nat.CULL_MASK, B, 1, 1, 1 if temporal else 0, 4)
+        nat.call("bs_cull_count", desc, nat.ptr(self.params), self.S, nat.ptr(self.presence),
+                 nat.ptr(self.group_begin), nat.ptr(self.aabb), self.n_groups, nat.ptr(planes), nat.ptr(times),
+                 None, nat.ptr(mask), nat.ptr(counts), None, st)
+        order = np.arange(B, dtype=np.int32)
+        nat.call("bs_scan_counts", nat.ptr(counts), self.n_groups, B, order.ctypes.data, nat.ptr(base),
+                 nat.ptr(view_rows), nat.ptr(view_row0), st)
+
+    def step(self, batch_ids, gt_batch: torch.Tensor | None = None, next_batch=None):
         """One training step over `batch_ids` (indices into self.views).
-        Returns the per-view mean-L1 losses as a device tensor [B]."""
+        Returns the per-view mean-L1 losses as a device tensor [B].
+        With several ranks, `next_batch` (the same on every rank) starts the
+        asynchronous placement of the following step (exchange.py)."""
         B = len(batch_ids)
         if not (1 <= B <= 32):
             raise ValueError("batch must hold 1..32 views")
         dev, S, st = self.dev, self.S, nat.stream_handle()
         bidx = torch.as_tensor(np.asarray(batch_ids, dtype=np.int64), device=dev)
-        planes = self.planes_all.index_select(0, bidx).contiguous()
         cams = self.cams_all.index_select(0, bidx).contiguous()
         # ---- K0: culling -> visibility masks + per-(group, view) counts
         mask = self.buf.get("mask", S, torch.int32)
         counts = self.buf.get("counts", self.n_groups * B, torch.int32)
-        with self._t("cull"):
-            temporal = self.presence is not None
-            times = self.view_times.index_select(0, bidx).contiguous() if temporal else None
-            desc = nat.CullDesc(nat.CULL_MASK, B, 1, 1, 1 if temporal else 0, 4)
-            nat.call("bs_cull_count", desc, nat.ptr(self.params), S, nat.ptr(self.presence),
-                     nat.ptr(self.group_begin), nat.ptr(self.aabb), self.n_groups, nat.ptr(planes), nat.ptr(times),
-                     None, nat.ptr(mask), nat.ptr(counts), None, st)
         base = self.buf.get("base", self.n_groups * B, torch.int32)
         view_rows = self.buf.get("view_rows", B, torch.int64)
         view_row0 = self.buf.get("view_row0", B, torch.int64)
-        order = np.arange(B, dtype=np.int32)
-        nat.call("bs_scan_counts", nat.ptr(counts), self.n_groups, B, order.ctypes.data, nat.ptr(base),
-                 nat.ptr(view_rows), nat.ptr(view_row0), st)
+        with self._t("cull"):
+            self._cull_counts(batch_ids, mask, counts, base, view_rows, view_row0, st)
+        if self.comm is not None and next_batch is not None:
+            # counts of the next batch on the pre-update positions -> async W
+            Bn = len(next_batch)
+            nb = self.buf
+            self._cull_counts(next_batch, nb.get("mask_next", S, torch.int32),
+                              nb.get("counts_next", self.n_groups * Bn, torch.int32),
+                              nb.get("base_next", self.n_groups * Bn, torch.int32),
+                              nb.get("view_rows_next", Bn, torch.int64), nb.get("view_row0_next", Bn, torch.int64), st)
+            self.comm.prefetch(nb.get("view_rows_next", Bn, torch.int64), tuple(int(v) for v in next_batch))
         lay = None
         if self.comm is None:
             rows_host = view_rows.cpu().numpy()  # C[v]_k (sync 1: sizes the splat buffers)
@@ -217,7 +233,7 @@ class SplatTrainer:
             # A <- all-gather C[.]_k ; W <- AssignImages(A)  (Alg. 1 lines 6-8)
             with self._t("assign"):
                 A = self.comm.gather_access(view_rows)
-                W = self.comm.assign(A)
+                W = self.comm.assign(A, key=tuple(int(v) for v in batch_ids))
                 lay = layout_for(A, W, self.comm.rank)
                 rows_host = A[:, self.comm.rank].copy()
                 row0 = np.zeros(B, dtype=np.int64)

@@ -146,3 +146,50 @@ def test_two_rank_exchange_matches_single_process():
     tr = account_iteration(A, PlacementSolution(W, world), ClusterTopology(world, 1, 1e9, 1e9), 48)
     assert sum(res[r][6] for r in range(world)) == int(tr.send_inter.sum()) * 48
     assert sum(res[r][7] for r in range(world)) == int(tr.recv_inter.sum()) * 36
+
+
+def _prefetch_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ex = SplatExchange()
+        rng = np.random.default_rng(100 + rank)
+        stale = torch.as_tensor(rng.integers(0, 5000, 8), dtype=torch.int64)
+        fresh = stale + torch.as_tensor(rng.integers(0, 50, 8), dtype=torch.int64)
+        ex.prefetch(stale, key=(1, 2, 3, 4, 5, 6, 7, 8))      # issued during step t
+        A = ex.gather_access(fresh)                          # step t+1: fresh counts
+        W = ex.assign(A, key=(1, 2, 3, 4, 5, 6, 7, 8))        # the prefetched (stale) W
+        A_stale = torch.empty(world * 8, dtype=torch.int64)
+        dist.all_gather_into_tensor(A_stale, stale)
+        out_q.put((rank, A, W, A_stale.view(world, -1).t().numpy(), ex.prefetched, ex.assign(A, key=None)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_async_placement():
+    """prefetch(): the W of the next batch is computed on a host thread from
+    the stale all-gathered counts; identical on every rank."""
+    from paper_2512_20017_b200.assign import CostCoefficients, hierarchical_place
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_prefetch_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        item = q.get(timeout=300)
+        res[item[0]] = item
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    _, A, W, A_stale, n_pref, W_fresh = res[0]
+    assert n_pref == 1
+    assert np.array_equal(W, res[1][2]) and np.array_equal(A, res[1][1])
+    inter = CostCoefficients(p=4.0)
+    intra = CostCoefficients(alpha=0.0, beta=0.1, gamma=0.1, delta=1.0, p=4.0)
+    assert np.array_equal(W, hierarchical_place(A_stale, world, 1, inter, intra).assignment)
+    assert np.array_equal(W_fresh, hierarchical_place(A, world, 1, inter, intra).assignment)
+    assert np.bincount(W, minlength=world).tolist() == [4, 4]
