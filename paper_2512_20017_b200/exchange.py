@@ -95,7 +95,7 @@ class SplatExchange:
         # gloo (CPU tests, several ranks sharing one GPU) moves host tensors only
         self.host_staging = dist.get_backend(group) == "gloo"
         self._pool = cf.ThreadPoolExecutor(max_workers=1, thread_name_prefix="placement")
-        self._ahead = None       # (key, future of W)
+        self._ahead = {}         # batch key -> future of its W
         self.place_ms = []       # host placement time per W (ms)
         self.wait_ms = []        # time the step waited for a prefetched W (ms)
         self.prefetched = 0
@@ -120,15 +120,13 @@ class SplatExchange:
     def assign(self, A: np.ndarray, key=None) -> np.ndarray:
         """W <- AssignImages(A): hierarchical_place on a one-box topology
         (N, 1); the W prefetched for `key` (stale by one step) when there is one."""
-        if key is not None and self._ahead is not None and self._ahead[0] == key:
-            fut = self._ahead[1]
-            self._ahead = None
+        fut = self._ahead.pop(key, None) if key is not None else None
+        if fut is not None:
             t = time.perf_counter()
             W = fut.result()
             self.wait_ms.append(1e3 * (time.perf_counter() - t))
             self.prefetched += 1
             return W
-        self._ahead = None
         return self._place(A)
 
     def prefetch(self, col_next: torch.Tensor, key) -> None:
@@ -157,7 +155,9 @@ class SplatExchange:
             A = ready().view(world, -1).t().numpy().astype(np.int64)
             return self._place(A)
 
-        self._ahead = (key, self._pool.submit(job))
+        for stale in list(self._ahead)[:-1]:  # keep at most two pending batches
+            self._ahead.pop(stale)
+        self._ahead[key] = self._pool.submit(job)
 
     def _a2a(self, send: torch.Tensor, send_rows, recv_rows, width: int) -> torch.Tensor:
         src = self._stage(send.view(-1, width))
