@@ -38,6 +38,12 @@ __device__ __forceinline__ float ex2a(float x) {
   return r;
 }
 
+__device__ __forceinline__ float rcpa(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 struct R2Args {
   int n_slots, tiles_per_slot, W, H, tiles_x;
   float bg[3];
@@ -84,7 +90,7 @@ __device__ __forceinline__ bool reaches2(const Splat2& f, float x0, float x1, fl
   const float L = 2.f * __logf(255.f * o);
   if (!(L > 0.f)) return false;
   // low-pass circle around mean2d
-  const float rc = sqrtf(0.5f * L) * 1.01f + 1e-3f;
+  const float rc = __fsqrt_rz(0.5f * L) * 1.01f + 1e-3f;
   const float ecx = fabsf(a.x - fminf(fmaxf(a.x, x0), x1)), ecy = fabsf(a.y - fminf(fmaxf(a.y, y0), y1));
   if (ecx <= rc && ecy <= rc) return true;
   // image of the disk u^2 + v^2 <= L
@@ -97,9 +103,10 @@ __device__ __forceinline__ bool reaches2(const Splat2& f, float x0, float x1, fl
   const float C12 = L * (r1[0] * r2[0] + r1[1] * r2[1]) - r1[2] * r2[2];
   const float C00 = L * (r0[0] * r0[0] + r0[1] * r0[1]) - r0[2] * r0[2];
   const float C11 = L * (r1[0] * r1[0] + r1[1] * r1[1]) - r1[2] * r1[2];
-  const float bx = C02 / C22, by = C12 / C22;
-  const float hx = sqrtf(fmaxf(bx * bx - C00 / C22, 0.f)) * 1.01f + 1e-3f;
-  const float hy = sqrtf(fmaxf(by * by - C11 / C22, 0.f)) * 1.01f + 1e-3f;
+  const float i22 = rcpa(C22);  // approximate: absorbed by the 1% padding
+  const float bx = C02 * i22, by = C12 * i22;
+  const float hx = __fsqrt_rz(fmaxf(bx * bx - C00 * i22, 0.f)) * 1.01f + 1e-3f;
+  const float hy = __fsqrt_rz(fmaxf(by * by - C11 * i22, 0.f)) * 1.01f + 1e-3f;
   return fabsf(bx - fminf(fmaxf(bx, x0), x1)) <= hx && fabsf(by - fminf(fmaxf(by, y0), y1)) <= hy;
 }
 
@@ -112,7 +119,7 @@ __device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f) {
 }
 
 struct Eval2 {
-  float hx[3], hy[3], z[3], u, v, g3, dx, dy, g2, power;
+  float hx[3], hy[3], z[3], iz, u, v, g3, dx, dy, g2, power;
   bool ok;
 };
 
@@ -131,8 +138,9 @@ __device__ __forceinline__ void eval2(const float4& a, const float4& b, const fl
   e.z[2] = __fsub_rn(__fmul_rn(e.hx[0], e.hy[1]), __fmul_rn(e.hx[1], e.hy[0]));
   e.ok = e.z[2] != 0.f;
   if (!e.ok) return;
-  e.u = __fdiv_rn(e.z[0], e.z[2]);
-  e.v = __fdiv_rn(e.z[1], e.z[2]);
+  e.iz = rcpa(e.z[2]);  // one approximate reciprocal (both kernels evaluate it identically)
+  e.u = __fmul_rn(e.z[0], e.iz);
+  e.v = __fmul_rn(e.z[1], e.iz);
   e.g3 = __fadd_rn(__fmul_rn(e.u, e.u), __fmul_rn(e.v, e.v));
   e.dx = __fsub_rn(a.x, px);
   e.dy = __fsub_rn(a.y, py);
@@ -260,10 +268,11 @@ __device__ __forceinline__ float warp_reduce16(float v[16]) {
 }
 
 struct PxB2 {
-  float T, T_final, dC0, dC1, dC2, acc0, acc1, acc2, last_alpha, lc0, lc1, lc2, bgdot;
+  float T, T_final, dC0, dC1, dC2, acc0, acc1, acc2, bgdot;
   int n;
 };
 
+template <bool kBg>
 __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
     R2Args a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
     const float* __restrict__ image, const float* __restrict__ final_T, const int32_t* __restrict__ n_contrib,
@@ -304,7 +313,7 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
   }
   q.T_final = q.T;
   q.bgdot = a.bg[0] * q.dC0 + a.bg[1] * q.dC1 + a.bg[2] * q.dC2;
-  q.acc0 = q.acc1 = q.acc2 = q.last_alpha = q.lc0 = q.lc1 = q.lc2 = 0.f;
+  q.acc0 = q.acc1 = q.acc2 = 0.f;
   int warp_n = q.n;
   for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
   const int end = rg.x + warp_n;
@@ -335,28 +344,26 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
           if (alpha >= kAMin) {
             any = true;
             const float4 col = s.d[j];
-            const float ra = __fdividef(1.f, 1.f - alpha);
+            const float ra = rcpa(1.f - alpha);  // alpha <= 0.99
             q.T = q.T * ra;
             const float fac = alpha * q.T;
             g[12] = fac * q.dC0;
             g[13] = fac * q.dC1;
             g[14] = fac * q.dC2;
-            q.acc0 = q.last_alpha * q.lc0 + (1.f - q.last_alpha) * q.acc0;
-            q.acc1 = q.last_alpha * q.lc1 + (1.f - q.last_alpha) * q.acc1;
-            q.acc2 = q.last_alpha * q.lc2 + (1.f - q.last_alpha) * q.acc2;
-            q.last_alpha = alpha;
-            q.lc0 = col.x;
-            q.lc1 = col.y;
-            q.lc2 = col.z;
-            float dLda = q.T * ((col.x - q.acc0) * q.dC0 + (col.y - q.acc1) * q.dC1 + (col.z - q.acc2) * q.dC2);
-            dLda -= q.T_final * ra * q.bgdot;
+            // acc = colour behind this splat (normalised); acc' = acc + alpha (c - acc)
+            const float e0 = col.x - q.acc0, e1 = col.y - q.acc1, e2 = col.z - q.acc2;
+            float dLda = q.T * (e0 * q.dC0 + e1 * q.dC1 + e2 * q.dC2);
+            if (kBg) dLda -= q.T_final * ra * q.bgdot;
+            q.acc0 = fmaf(alpha, e0, q.acc0);
+            q.acc1 = fmaf(alpha, e1, q.acc1);
+            q.acc2 = fmaf(alpha, e2, q.acc2);
             if (raw <= kAMax) {
               const float dpow = dLda * alpha;
               g[11] = dLda * ex;
               if (e.g3 <= e.g2) {
                 // power = -0.5 (u^2 + v^2)
                 const float gu = -e.u * dpow, gv = -e.v * dpow;
-                const float iz = 1.f / e.z[2];
+                const float iz = e.iz;
                 const float gz0 = gu * iz, gz1 = gv * iz, gz2 = -(gu * e.z[0] + gv * e.z[1]) * iz * iz;
                 // zeta = hx x hy: d/dhx = hy x gz, d/dhy = gz x hx
                 const float ghx0 = e.hy[1] * gz2 - e.hy[2] * gz1;
@@ -448,9 +455,10 @@ extern "C" int32_t bs_raster2d_bwd(const bs_raster_desc* d, const float* sp_rows
   if (st) return st;
   BS_REQUIRE(grad_image || (image && gt), BS_ERR_PARAMETER, "raster_bwd needs grad_image or (image, gt)");
   const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
-  raster2d_bwd_kernel<<<grid, kT2, 0, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges),
-                                                          image, final_T, n_contrib, grad_image, gt, gt_slot_view,
-                                                          g_sp);
+  const bool bg = a.bg[0] != 0.f || a.bg[1] != 0.f || a.bg[2] != 0.f;
+  auto kern = bg ? raster2d_bwd_kernel<true> : raster2d_bwd_kernel<false>;
+  kern<<<grid, kT2, 0, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image,
+                                            final_T, n_contrib, grad_image, gt, gt_slot_view, g_sp);
   BS_LAUNCH_CHECK("raster2d_bwd_kernel");
   return BS_OK;
 }

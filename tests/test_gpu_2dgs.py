@@ -33,9 +33,10 @@ def _trainer(c1, **kw):
     return SplatTrainer(params, gb, aabb, ds.views, gt=gt, sh_degree=3, model="2dgs", **kw)
 
 
-def _ref(c1, v):
+def _ref(c1, v, bg=(0.0, 0.0, 0.0)):
     ds, params, gb, aabb, gt = c1
-    return oracle_view_pipeline(params, gb, aabb, ds.views[v], camera_bytes([ds.views[v]]), gt[v], model="2dgs")
+    return oracle_view_pipeline(params, gb, aabb, ds.views[v], camera_bytes([ds.views[v]]), gt[v], model="2dgs",
+                                bg=bg)
 
 
 def test_projection2d_bitexact_and_binning(c1, cuda):
@@ -61,8 +62,9 @@ def test_projection2d_bitexact_and_binning(c1, cuda):
             assert np.array_equal(a, b), f"view {v} tile {t}"
 
 
-def test_render2d_forward_and_backward_tolerance(c1, cuda):
-    tr = _trainer(c1)
+@pytest.mark.parametrize("bg", [(0.0, 0.0, 0.0), (0.3, 0.1, 0.7)])
+def test_render2d_forward_and_backward_tolerance(c1, cuda, bg):
+    tr = _trainer(c1, bg=bg)
     batch = [1, 6]
     losses = tr.step(batch).cpu().numpy()
     n = tr.last["n_rows"]
@@ -72,7 +74,7 @@ def test_render2d_forward_and_backward_tolerance(c1, cuda):
     rows = tr.last["rows_per_view"]
     row0 = np.concatenate([[0], np.cumsum(rows)])
     for s, v in enumerate(batch):
-        ref = _ref(c1, v)
+        ref = _ref(c1, v, bg)
         assert ref["img"].max() > 0.05  # the surfels actually cover pixels
         assert np.abs(img[s] - ref["img"]).max() <= IMG_TOL
         assert abs(losses[s] - ref["loss"]) <= 1e-5
