@@ -61,16 +61,51 @@ struct RastArgs {
   float inv_norm;  // 1 / (H * W * 3)
 };
 
-// log2(e) * power at a pixel from the pre-scaled conic
-// a = (u, v, kA, kB), kc: kA = -log2(e) A / 2, kB = -log2(e) B, kc = -log2(e) C / 2.
-// Explicit round-to-nearest intrinsics: identical in both kernels.
-__device__ __forceinline__ float splat_power2(float4 a, float kc, float px, float py, float& dx, float& dy) {
-  dx = __fsub_rn(a.x, px);
-  dy = __fsub_rn(a.y, py);
-  return __fmaf_rn(a.z, __fmul_rn(dx, dx), __fmaf_rn(kc, __fmul_rn(dy, dy), __fmul_rn(a.w, __fmul_rn(dx, dy))));
+// Packed FP32 pairs (sm_100 FADD2 / FMUL2 / FFMA2: one issue slot for two
+// lanes' worth of FP32 work; a scalar operand is broadcast for free).
+struct F2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ F2 f2(float a, float b) {
+  F2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 unf2(F2 x) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(x.v));
+  return r;
+}
+__device__ __forceinline__ F2 add2(F2 a, F2 b) {
+  F2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
+  F2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+  F2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+__device__ __forceinline__ F2 bcast(float s) { return f2(s, s); }
+
+// log2(e) * power at a pixel from the pre-scaled conic:
+// uv = (u, v), k = (kA, kC), kb: kA = -log2(e) A / 2, kC = -log2(e) C / 2,
+// kb = -log2(e) B; npx = -(px, py).  d = (dx, dy) = uv - pixel.
+//   power2 = fma(kb, dx dy, kA dx^2) + kC dy^2
+// Explicit round-to-nearest ops in a fixed order: identical in both kernels.
+__device__ __forceinline__ float splat_power2(F2 uv, F2 k, float kb, F2 npx, F2& d) {
+  d = add2(uv, npx);
+  const float2 dd = unf2(d);
+  const float2 t = unf2(mul2(mul2(d, d), k));
+  return __fadd_rn(__fmaf_rn(kb, __fmul_rn(dd.x, dd.y), t.x), t.y);
 }
 
-// Warp-private staging: a = (u, v, kA, kB), b = (kC, opacity, r, g), c = b-channel
+// Warp-private staging: a = (u, v, kA, kC), b = (kB, opacity, r, g), c = b-channel
 struct WarpSmem {
   float4 a[32];
   float4 b[32];
@@ -112,8 +147,8 @@ __device__ __forceinline__ bool reaches(const Splat& f, float x0, float x1, floa
 }
 
 __device__ __forceinline__ void stage(WarpSmem& s, int lane, const Splat& f) {
-  s.a[lane] = make_float4(f.p0.x, f.p0.y, f.p0.w * (-0.5f * kLog2e), f.p1.x * -kLog2e);
-  s.b[lane] = make_float4(f.p1.y * (-0.5f * kLog2e), f.p0.z, f.p1.z, f.p1.w);
+  s.a[lane] = make_float4(f.p0.x, f.p0.y, f.p0.w * (-0.5f * kLog2e), f.p1.y * (-0.5f * kLog2e));
+  s.b[lane] = make_float4(f.p1.x * -kLog2e, f.p0.z, f.p1.z, f.p1.w);
   s.c[lane] = f.b;
   s.row[lane] = f.row;
 }
@@ -140,15 +175,15 @@ struct Region {
 };
 
 struct PixelFwd {
-  float T, c0, c1, c2;
+  F2 c01;  // (r, g) accumulated
+  float T, c2;
   int contrib;
   bool done;
 };
 
-__device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float4& sb, float cb, float pxf, float pyf,
-                                      int rel) {
-  float dx, dy;
-  const float power2 = splat_power2(sa, sb.x, pxf, pyf, dx, dy);
+__device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float4& sb, float cb, F2 npx, int rel) {
+  F2 d;
+  const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
   if (power2 > 0.f || power2 < kP2Min) return;
   const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, ex2_approx(power2)));
   if (alpha < kAlphaMin) return;
@@ -158,8 +193,7 @@ __device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float
     return;
   }
   const float w = __fmul_rn(alpha, p.T);
-  p.c0 = __fmaf_rn(sb.z, w, p.c0);
-  p.c1 = __fmaf_rn(sb.w, w, p.c1);
+  p.c01 = fma2(f2(sb.z, sb.w), bcast(w), p.c01);
   p.c2 = __fmaf_rn(cb, w, p.c2);
   p.T = nT;
   p.contrib = rel + 1;
@@ -190,7 +224,7 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
   PixelFwd p[PPL];
 #pragma unroll
-  for (int k = 0; k < PPL; ++k) p[k] = PixelFwd{1.f, 0.f, 0.f, 0.f, 0, !(q.px < a.W && q.py0 + k < a.H)};
+  for (int k = 0; k < PPL; ++k) p[k] = PixelFwd{f2(0.f, 0.f), 1.f, 0.f, 0, !(q.px < a.W && q.py0 + k < a.H)};
   Splat f;
   fetch_splat(f, sp, inst_rows, rg.x + lane, rg.x + lane < rg.y);
   for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
@@ -209,7 +243,7 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
       const int rel = b0 + j - rg.x;
 #pragma unroll
       for (int k = 0; k < PPL; ++k)
-        if (!p[k].done) blend(p[k], sa, sb, cb, pxf, (float)(q.py0 + k) + 0.5f, rel);
+        if (!p[k].done) blend(p[k], sa, sb, cb, f2(-pxf, -((float)(q.py0 + k) + 0.5f)), rel);
     }
     __syncwarp();
   }
@@ -218,7 +252,8 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
   for (int k = 0; k < PPL; ++k) {
     if (!(q.px < a.W && q.py0 + k < a.H)) continue;
     const int64_t pix = ((int64_t)slot * a.H + q.py0 + k) * a.W + q.px;
-    const float o0 = p[k].c0 + p[k].T * a.bg[0], o1 = p[k].c1 + p[k].T * a.bg[1], o2 = p[k].c2 + p[k].T * a.bg[2];
+    const float2 c01 = unf2(p[k].c01);
+    const float o0 = c01.x + p[k].T * a.bg[0], o1 = c01.y + p[k].T * a.bg[1], o2 = p[k].c2 + p[k].T * a.bg[2];
     image[3 * pix] = o0;
     image[3 * pix + 1] = o1;
     image[3 * pix + 2] = o2;
@@ -291,7 +326,9 @@ __device__ __forceinline__ float warp_reduce9(const float v[9], int& out_idx) {
 }
 
 struct PixelBwd {
-  float T, T_final, dC0, dC1, dC2, acc0, acc1, acc2, bgdot;
+  float2 acc01;  // colour behind the current splat (r, g), normalised
+  F2 dC01;       // dL/dC (r, g)
+  float T, T_final, dC2, acc2, bgdot;
   int n;
 };
 
@@ -301,10 +338,10 @@ struct PixelBwd {
 // in front of it: acc' = acc + alpha (c - acc) after the splat.  kBg: the
 // background is not black (adds its transmittance term to dL/dalpha).
 template <bool kAssign, bool kBg>
-__device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const float4& sb, float cb, float pxf,
-                                           float pyf, float g[9]) {
-  float dx, dy;
-  const float power2 = splat_power2(sa, sb.x, pxf, pyf, dx, dy);
+__device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const float4& sb, float cb, F2 npx,
+                                           float g[9]) {
+  F2 d;
+  const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
   if (power2 > 0.f || power2 < kP2Min) return false;
   const float ex = ex2_approx(power2);
   const float raw = __fmul_rn(sb.y, ex);
@@ -313,25 +350,29 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
   const float ra = rcp_approx(1.f - alpha);  // alpha <= 0.99
   p.T = p.T * ra;
   const float fac = alpha * p.T;
-  const float e0 = sb.z - p.acc0, e1 = sb.w - p.acc1, e2 = cb - p.acc2;
-  float dL_dalpha = p.T * (e0 * p.dC0 + e1 * p.dC1 + e2 * p.dC2);
+  const F2 e01 = add2(f2(sb.z, sb.w), f2(-p.acc01.x, -p.acc01.y));
+  const float e2 = cb - p.acc2;
+  const float2 ed = unf2(mul2(e01, p.dC01));
+  float dL_dalpha = p.T * fmaf(e2, p.dC2, ed.x + ed.y);
   if (kBg) dL_dalpha -= p.T_final * ra * p.bgdot;
-  p.acc0 = fmaf(alpha, e0, p.acc0);
-  p.acc1 = fmaf(alpha, e1, p.acc1);
+  p.acc01 = unf2(fma2(bcast(alpha), e01, f2(p.acc01.x, p.acc01.y)));
   p.acc2 = fmaf(alpha, e2, p.acc2);
   // clamped alpha (raw > 0.99): colour gradient only.  G_SP carries the
   // moments of dL/dpower (power = -q/2) over the pixels; the projection
   // backward applies the conic (include/splat_b200.h, G_SP row).
   const float dpow = raw > kAlphaMax ? 0.f : dL_dalpha * alpha;  // dL / d power
+  const float2 t01 = unf2(mul2(bcast(dpow), d));     // dpow (dx, dy)
+  const float2 t34 = unf2(mul2(bcast(t01.x), d));    // dpow dx (dx, dy)
+  const float2 t67 = unf2(mul2(bcast(fac), p.dC01));
   float t[9];
-  t[0] = dpow * dx;
-  t[1] = dpow * dy;
+  t[0] = t01.x;
+  t[1] = t01.y;
   t[2] = raw > kAlphaMax ? 0.f : dL_dalpha * ex;
-  t[3] = t[0] * dx;
-  t[4] = t[0] * dy;
-  t[5] = t[1] * dy;
-  t[6] = fac * p.dC0;
-  t[7] = fac * p.dC1;
+  t[3] = t34.x;
+  t[4] = t34.y;
+  t[5] = t01.y * unf2(d).y;
+  t[6] = t67.x;
+  t[7] = t67.y;
   t[8] = fac * p.dC2;
 #pragma unroll
   for (int k = 0; k < 9; ++k) g[k] = kAssign ? t[k] : g[k] + t[k];
@@ -345,14 +386,15 @@ __device__ __forceinline__ void init_pixel_bwd(PixelBwd& q, const RastArgs& a, i
                                                const int32_t* __restrict__ gt_view) {
   q.T = 1.f;
   q.n = 0;
-  q.dC0 = q.dC1 = q.dC2 = 0.f;
+  float dC0 = 0.f, dC1 = 0.f;
+  q.dC2 = 0.f;
   if (inside) {
     const int64_t pix = ((int64_t)slot * a.H + py) * a.W + px;
     q.T = final_T[pix];
     q.n = n_contrib[pix];
     if (grad_image) {
-      q.dC0 = grad_image[3 * pix];
-      q.dC1 = grad_image[3 * pix + 1];
+      dC0 = grad_image[3 * pix];
+      dC1 = grad_image[3 * pix + 1];
       q.dC2 = grad_image[3 * pix + 2];
     } else {
       const int gv = gt_view ? gt_view[slot] : slot;
@@ -360,14 +402,16 @@ __device__ __forceinline__ void init_pixel_bwd(PixelBwd& q, const RastArgs& a, i
       const float d0 = image[3 * pix] - gp[0] * (1.f / 255.f);
       const float d1 = image[3 * pix + 1] - gp[1] * (1.f / 255.f);
       const float d2 = image[3 * pix + 2] - gp[2] * (1.f / 255.f);
-      q.dC0 = (d0 > 0.f ? 1.f : (d0 < 0.f ? -1.f : 0.f)) * a.inv_norm;
-      q.dC1 = (d1 > 0.f ? 1.f : (d1 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+      dC0 = (d0 > 0.f ? 1.f : (d0 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+      dC1 = (d1 > 0.f ? 1.f : (d1 < 0.f ? -1.f : 0.f)) * a.inv_norm;
       q.dC2 = (d2 > 0.f ? 1.f : (d2 < 0.f ? -1.f : 0.f)) * a.inv_norm;
     }
   }
   q.T_final = q.T;
-  q.bgdot = a.bg[0] * q.dC0 + a.bg[1] * q.dC1 + a.bg[2] * q.dC2;
-  q.acc0 = q.acc1 = q.acc2 = 0.f;
+  q.dC01 = f2(dC0, dC1);
+  q.bgdot = a.bg[0] * dC0 + a.bg[1] * dC1 + a.bg[2] * q.dC2;
+  q.acc01 = make_float2(0.f, 0.f);
+  q.acc2 = 0.f;
 }
 
 template <int PPL, bool kBg>
@@ -414,13 +458,13 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
       const float cb = s.c[j];
       bool any = false;
       if constexpr (PPL == 1) {
-        if (rel < p[0].n) any = pixel_grad<true, kBg>(p[0], sa, sb, cb, pxf, (float)q.py0 + 0.5f, g);
+        if (rel < p[0].n) any = pixel_grad<true, kBg>(p[0], sa, sb, cb, f2(-pxf, -((float)q.py0 + 0.5f)), g);
       } else {
 #pragma unroll
         for (int k = 0; k < 9; ++k) g[k] = 0.f;
 #pragma unroll
         for (int k = 0; k < PPL; ++k)
-          if (rel < p[k].n) any |= pixel_grad<false, kBg>(p[k], sa, sb, cb, pxf, (float)(q.py0 + k) + 0.5f, g);
+          if (rel < p[k].n) any |= pixel_grad<false, kBg>(p[k], sa, sb, cb, f2(-pxf, -((float)(q.py0 + k) + 0.5f)), g);
       }
       const uint32_t who = __ballot_sync(0xffffffffu, any);
       if (who == 0u) continue;
