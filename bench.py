@@ -360,6 +360,9 @@ def run_ours(args, cfg):
     t_e2e0 = time.perf_counter()
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_start.record()
+    # per-step losses land in pinned host memory by an asynchronous D2H copy
+    # (read back every step without stalling the launch queue)
+    loss_pinned = [torch.empty(B, dtype=torch.float32, pin_memory=True) for _ in range(len(e2e_sched))]
     loss_host = None
     upload(0)
     for i, b in enumerate(e2e_sched):
@@ -371,10 +374,11 @@ def run_ours(args, cfg):
         ev = torch.cuda.Event()
         ev.record()
         freed[i % 2] = ev
-        loss_host = losses.cpu()
+        loss_pinned[i][: losses.numel()].copy_(losses, non_blocking=True)
     e_end.record()
     torch.cuda.synchronize()
     e2e_ms = e_start.elapsed_time(e_end)
+    loss_host = loss_pinned[-1] if loss_pinned else None
     e2e_wall = (time.perf_counter() - t_e2e0) * 1000.0
     if world > 1:
         e2e_ms, e2e_wall = _max_over_ranks([e2e_ms, e2e_wall])

@@ -14,11 +14,13 @@ from . import _native as nat
 
 
 def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, model_id=nat.MODEL_3DGS,
-                sort_cap=4096):
+                sort_cap=4096, before_sync=None):
     """Atomics into (slot, tile) buckets, then a shared-memory sort of every
     bucket by (depth, row); buckets larger than the in-SM sort go through the
     device radix sort.  `buf` is a grow-only buffer cache with
-    get(name, n, dtype).  Returns (n_inst, inst_rows, ranges, largest bucket)."""
+    get(name, n, dtype).  `before_sync` (optional) queues independent GPU work
+    ahead of the host read of the instance count, which it then overlaps.
+    Returns (n_inst, inst_rows, ranges, largest bucket)."""
     st, lib = nat.stream_handle(), nat.load()
     nb = n_slots * tiles
     counts = buf.get("bucket_counts", nb, torch.int32)
@@ -30,6 +32,8 @@ def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, 
     ows = buf.get("offsets_ws", lib.bs_bin_tiles_offsets_workspace(nb), torch.uint8)
     nat.call("bs_bin_tiles_offsets", nat.ptr(counts), nb, nat.ptr(ranges), nat.ptr(cursor), nat.ptr(stats),
              nat.ptr(ows), ows.numel(), st)
+    if before_sync is not None:
+        before_sync()
     n_inst, biggest = (int(x) for x in stats.cpu().tolist())  # sizes the instance buffers
     keys = buf.get("inst_keys", max(n_inst, 1), torch.int64)
     irows = buf.get("irows", max(n_inst, 1), torch.int32)

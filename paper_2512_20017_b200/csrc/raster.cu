@@ -621,7 +621,7 @@ extern "C" int32_t bs_reduce_loss_tiles(const float* loss_tiles, int32_t n_slots
                                         int32_t height, int32_t width, float* loss, void* stream) {
   BS_REQUIRE(n_slots >= 1, BS_ERR_PARAMETER, "bad slot count");
   const float inv_norm = (float)(1.0 / (3.0 * (double)height * (double)width));
-  reduce_partials_kernel<<<n_slots, 256, 0, as_stream(stream)>>>(loss_tiles, n_slots, tiles_per_slot, inv_norm,
+  reduce_partials_kernel<<<n_slots, 1024, 0, as_stream(stream)>>>(loss_tiles, n_slots, tiles_per_slot, inv_norm,
                                                                  loss);
   BS_LAUNCH_CHECK("reduce_partials_kernel");
   return BS_OK;

@@ -161,6 +161,15 @@ class SplatTrainer:
         # raster work split: pixels per lane (1 -> 8x4 region per warp, 2 -> 8x8);
         # 1 measured faster on B200 (C2: bwd 3.30 vs 3.52 ms, fwd 1.22 vs 1.24 ms)
         self.pixels_per_lane = int(os.environ.get("BS_RASTER_PPL", "1"))
+        # batch indices reach the GPU by asynchronous copies from a pinned ring
+        self._ids_pin = [torch.empty(64, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        self._ids_ev = [None, None]
+        self._ids_k = 0
+        # N = 1: the splat buffer is sized for every point in every batch view
+        # when that fits this budget, so the projection is launched before the
+        # host reads the row counts (the read then overlaps the projection)
+        self.sp_capacity_bytes = 2 << 30
+        self._rows_pin = torch.empty(32, dtype=torch.int64, pin_memory=True)
 
     # ------------------------------------------------------------------ utils
     def _t(self, name):
@@ -184,9 +193,26 @@ class SplatTrainer:
         return _T()
 
     # ------------------------------------------------------------------ step
-    def _cull_counts(self, batch_ids, mask, counts, base, view_rows, view_row0, st):
+    def _device_ids(self, ids, name):
+        """Batch indices on the device through a pinned, event-guarded ring
+        (a pageable copy would stall the host until the GPU caught up)."""
+        k = self._ids_k = (self._ids_k + 1) % 2
+        if self._ids_ev[k] is not None:
+            self._ids_ev[k].synchronize()
+        n = len(ids)
+        pin = self._ids_pin[k]
+        pin[:n] = torch.as_tensor(np.asarray(ids, dtype=np.int64))
+        dst = self.buf.get(name, 64, torch.int64)[:n]
+        dst.copy_(pin[:n], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ids_ev[k] = ev
+        return dst
+
+    def _cull_counts(self, batch_ids, mask, counts, base, view_rows, view_row0, st, bidx=None):
         B = len(batch_ids)
-        bidx = torch.as_tensor(np.asarray(batch_ids, dtype=np.int64), device=self.dev)
+        if bidx is None:
+            bidx = self._device_ids(batch_ids, "bidx_cull")
         planes = self.planes_all.index_select(0, bidx).contiguous()
         temporal = self.presence is not None
         times = self.view_times.index_select(0, bidx).contiguous() if temporal else None
@@ -207,7 +233,7 @@ class SplatTrainer:
         if not (1 <= B <= 32):
             raise ValueError("batch must hold 1..32 views")
         dev, S, st = self.dev, self.S, nat.stream_handle()
-        bidx = torch.as_tensor(np.asarray(batch_ids, dtype=np.int64), device=dev)
+        bidx = self._device_ids(batch_ids, "bidx")
         cams = self.cams_all.index_select(0, bidx).contiguous()
         # ---- K0: culling -> visibility masks + per-(group, view) counts
         mask = self.buf.get("mask", S, torch.int32)
@@ -216,7 +242,7 @@ class SplatTrainer:
         view_rows = self.buf.get("view_rows", B, torch.int64)
         view_row0 = self.buf.get("view_row0", B, torch.int64)
         with self._t("cull"):
-            self._cull_counts(batch_ids, mask, counts, base, view_rows, view_row0, st)
+            self._cull_counts(batch_ids, mask, counts, base, view_rows, view_row0, st, bidx)
         if self.comm is not None and next_batch is not None:
             # counts of the next batch on the pre-update positions -> async W
             Bn = len(next_batch)
@@ -227,8 +253,27 @@ class SplatTrainer:
                               nb.get("view_rows_next", Bn, torch.int64), nb.get("view_row0_next", Bn, torch.int64), st)
             self.comm.prefetch(nb.get("view_rows_next", Bn, torch.int64), tuple(int(v) for v in next_batch))
         lay = None
-        if self.comm is None:
-            rows_host = view_rows.cpu().numpy()  # C[v]_k (sync 1: sizes the splat buffers)
+        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group)
+        early = self.comm is None and S * B * self.sp_floats * 4 <= self.sp_capacity_bytes
+        if early:
+            # the row counts start towards the host before the projection is
+            # queued, so the host resumes while the projection still runs
+            rows_pin = self._rows_pin[:B]
+            rows_pin.copy_(view_rows, non_blocking=True)
+            rows_ready = torch.cuda.Event()
+            rows_ready.record()
+            # ---- K1 first (rows land at view_row0 from the scan), then the
+            # row counts are read while the projection runs
+            sp = self.buf.get("sp", max(S * B, 1) * self.sp_floats, torch.float32)
+            with self._t("project"):
+                nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask),
+                         nat.ptr(self.group_begin), self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams),
+                         nat.ptr(sp), st)
+        if early:
+            rows_ready.synchronize()  # C[v]_k (sync 1: sizes the render buffers)
+            rows_host = rows_pin.numpy().copy()
+        elif self.comm is None:
+            rows_host = view_rows.cpu().numpy()
         else:
             # A <- all-gather C[.]_k ; W <- AssignImages(A)  (Alg. 1 lines 6-8)
             with self._t("assign"):
@@ -242,17 +287,18 @@ class SplatTrainer:
             self.last.update(A=A, W=W, layout=lay)
         n_rows = int(rows_host.sum())
         self.last["rows_per_view"] = rows_host.copy()
-        # ---- K1: projection into SP rows (send layout)
-        sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
-        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group)
-        with self._t("project"):
-            nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask), nat.ptr(self.group_begin),
-                     self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(sp), st)
+        if not early:
+            # ---- K1: projection into SP rows (send layout)
+            sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
+            with self._t("project"):
+                nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask),
+                         nat.ptr(self.group_begin), self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams),
+                         nat.ptr(sp), st)
         if lay is None:
-            # every batch view is rendered here (N = 1: W[v] = k for all v)
-            seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(rows_host)[:-1]]).astype(np.int64),
-                                       device=dev)
-            seg_slot = torch.arange(B, dtype=torch.int32, device=dev)
+            # every batch view is rendered here (N = 1: W[v] = k for all v):
+            # one segment per view, starting at the scan's view_row0
+            seg_row0 = view_row0
+            seg_slot = self._slot_ids(B)
             losses, gsp = self._render_and_backward(sp, n_rows, seg_row0, seg_slot, B, cams, bidx, gt_batch)
         else:
             # SP all-to-all to the rendering ranks (line 9), render, G_SP back (line 21)
@@ -284,10 +330,17 @@ class SplatTrainer:
                      nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
         return losses
 
-    def _bin_buckets(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams):
+    def _slot_ids(self, B):
+        t = self.buf.bufs.get("slot_ids")
+        if t is None or t.numel() < 32:
+            t = torch.arange(32, dtype=torch.int32, device=self.dev)
+            self.buf.bufs["slot_ids"] = t
+        return t[:B]
+
+    def _bin_buckets(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, before_sync=None):
         """Bucket pipeline (csrc/bin_tiles.cu), see binning.bin_buckets."""
         n_inst, irows, ranges, biggest = bin_buckets(self.buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams,
-                                                     self.tiles, self.model_id, self.sort_cap)
+                                                     self.tiles, self.model_id, self.sort_cap, before_sync)
         self.last["largest_bucket"] = biggest
         return n_inst, irows, ranges
 
@@ -326,14 +379,18 @@ class SplatTrainer:
     def _render_and_backward(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, gt_views, gt_batch):
         dev, st = self.dev, nat.stream_handle()
         lib = nat.load()
+        gsp = self.buf.get("gsp", max(n_rows, 1) * self.gsp_floats, torch.float32)
         # ---- K2: binning
         with self._t("bin"):
             if self.binning == "radix":
                 if self.model != "3dgs":
                     raise ValueError("the radix binning pipeline reads 3DGS rows only; use binning='bucket'")
+                gsp.zero_()
                 n_inst, irows, ranges = self._bin_radix(sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams)
             else:
-                n_inst, irows, ranges = self._bin_buckets(sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams)
+                # the G_SP accumulator is cleared while the host reads the instance count
+                n_inst, irows, ranges = self._bin_buckets(sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams,
+                                                          before_sync=gsp.zero_)
         self.last.update(n_rows=n_rows, n_inst=n_inst, n_slots=n_slots)
         # ---- K3: forward + fused L1 partials
         npx = self.H * self.W
@@ -354,8 +411,6 @@ class SplatTrainer:
         losses = self.buf.get("losses", n_slots, torch.float32)
         nat.call("bs_reduce_loss_tiles", nat.ptr(loss_tiles), n_slots, self.tiles, self.H, self.W, nat.ptr(losses), st)
         # ---- K4: backward
-        gsp = self.buf.get("gsp", max(n_rows, 1) * self.gsp_floats, torch.float32)
-        gsp.zero_()
         with self._t("raster_bwd"):
             nat.call(self._raster[1], rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
                      nat.ptr(final_T), nat.ptr(n_contrib), None, nat.ptr(gt), nat.ptr(gt_map), nat.ptr(gsp), st)
