@@ -48,3 +48,23 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(_native.NativeError if hasattr(_native, "NativeError") else Exception):
         _native.load(require_cuda=True)
+
+
+def _declared_host():
+    src = open(os.path.join(ROOT, "include", "splat_host.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_host_library_exports_every_declared_symbol():
+    assert os.path.exists(_native.host_lib_path()), "run __graft_entry__.build() first"
+    lib = ctypes.CDLL(_native.host_lib_path())
+    names = _declared_host()
+    assert "bs_partition_multilevel" in names
+    assert not [n for n in names if not hasattr(lib, n)]
+    assert sorted(_native.HOST_EXPORTED) == names
+
+
+def test_proj_desc_layout():
+    # bs_proj_desc: 7 int32 (n_views, sh_degree, tiles_x_max, tiles_y_max, model, max_group_points, gsp_form)
+    assert ctypes.sizeof(_native.ProjDesc) == 28
