@@ -336,7 +336,7 @@ def run_ours(args, cfg):
                      "step_wait_ms": round(float(np.mean(comm.wait_ms)), 3) if comm.wait_ms else None}
         comm_report = comm_bytes_report(comm, step_AW, sched[args.warmup:args.warmup + args.steps], ds, g,
                                         world, rank, args.steps, row_bytes=4 * tr.sp_floats,
-                                        grad_bytes=4 * tr.gsp_floats)
+                                        grad_bytes=4 * tr.gsp_wire_floats)
     # ---- e2e: public API with pinned host ground truth, loss read back
     # the step's ground-truth images are copied from pinned host memory on a
     # side stream, double-buffered: step i+1's upload overlaps step i

@@ -77,7 +77,8 @@ int64_t bs_launch_count(void);
  * half-widths: the tight box of the splat's support q <= min(9, 2 ln(255 o)),
  * i.e. the 3-sigma ellipse cut by alpha >= 1/255; 0 = never contributes) */
 #define BS_SP_FLOATS 12
-/* gradient row (G_SP): 9 floats as written by bs_raster_bwd -- moments of
+/* gradient row (G_SP): 12 floats (48 B, 16-byte aligned so the rasteriser
+ * adds with 128-bit REDs), 9 used + 3 pad, as written by bs_raster_bwd -- moments of
  * dL/dpower over the pixels (power = -q/2, dx = u - px, dy = v - py):
  *   0 sum dpow dx  1 sum dpow dy  2 dL/dopacity  3 sum dpow dx^2
  *   4 sum dpow dx dy  5 sum dpow dy^2  6..8 dL/drgb
@@ -85,7 +86,7 @@ int64_t bs_launch_count(void);
  * dL/du = -(A m0 + B m1), dL/dv = -(B m0 + C m1), dL/dA = -m3/2,
  * dL/dB = -m4, dL/dC = -m5/2 (bs_proj_desc.gsp_form = 1 accepts plain
  * dL/dSP instead: d u, d v, d opacity, d conic a/b/c, d rgb). */
-#define BS_GSP_FLOATS 9
+#define BS_GSP_FLOATS 12
 #define BS_TILE 16
 
 /* Camera of one view, float32, as consumed by the projection and raster

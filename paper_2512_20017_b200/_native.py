@@ -22,7 +22,7 @@ _lib = None
 PARAM_PLANES = 15
 PARAM_FLOATS = 60
 SP_FLOATS = 12
-GSP_FLOATS = 9
+GSP_FLOATS = 12
 TILE = 16
 
 CULL_ACCESS_EXACT = 0

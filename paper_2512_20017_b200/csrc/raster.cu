@@ -24,9 +24,10 @@
 //
 // Backward: each warp walks its own range back to front from the deepest
 // contributor of its pixels (T recovered by division).  Per splat the lanes
-// that contribute are counted with a ballot: up to kSparseLanes (6) of them add
-// their 9 gradient terms with direct REDs; otherwise the warp reduce-scatters
-// the 9 sums in 12 shuffles and 9 lanes issue one RED each.
+// that contribute are counted with a ballot: up to kSparseLanes (12) of them
+// add their 9 gradient terms with direct REDs (two 128-bit + one 32-bit RED
+// into the 16-byte aligned G_SP row); otherwise the warp reduce-scatters the
+// 9 sums in 12 shuffles and 9 lanes issue one RED each.
 #include "common.cuh"
 
 namespace bs {
@@ -38,7 +39,8 @@ constexpr float kTMin = 1e-4f;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kP2Min = -4.5f * kLog2e;  // q > 9 (outside the 3-sigma ellipse): no contribution
 #ifndef BS_SPARSE_LANES
-#define BS_SPARSE_LANES 6  // swept on B200 (C2): 0 3.15, 2 3.08, 3 3.01, 4 2.97, 5 2.92, 6 2.91, 8 2.94 ms
+// swept on B200 (C2, 128-bit REDs): 6 2.18, 8 2.11, 10 2.07, 12 2.06, 16 2.15, 32 3.25 ms
+#define BS_SPARSE_LANES 12
 #endif
 constexpr int kSparseLanes = BS_SPARSE_LANES;  // contributing lanes handled with direct REDs
 
@@ -471,8 +473,15 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
       float* dst = g_sp + (int64_t)s.row[j] * BS_GSP_FLOATS;
       if (__popc(who) <= kSparseLanes) {
         if (any) {
+#if BS_GSP_FLOATS == 12
+          // 16-byte aligned rows: two 128-bit REDs + one scalar
+          atomicAdd(reinterpret_cast<float4*>(dst), make_float4(g[0], g[1], g[2], g[3]));
+          atomicAdd(reinterpret_cast<float4*>(dst + 4), make_float4(g[4], g[5], g[6], g[7]));
+          atomicAdd(dst + 8, g[8]);
+#else
 #pragma unroll
           for (int k = 0; k < 9; ++k) atomicAdd(dst + k, g[k]);
+#endif
         }
       } else {
 #pragma unroll

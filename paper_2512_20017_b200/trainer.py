@@ -110,6 +110,7 @@ class SplatTrainer:
         self.model_id = nat.MODEL_2DGS if model == "2dgs" else nat.MODEL_3DGS
         self.sp_floats = nat.SP2_FLOATS if model == "2dgs" else nat.SP_FLOATS
         self.gsp_floats = nat.GSP2_FLOATS if model == "2dgs" else nat.GSP_FLOATS
+        self.gsp_wire_floats = nat.GSP2_FLOATS if model == "2dgs" else 9  # floats of a G_SP row that carry data
         self._raster = ("bs_raster2d_fwd", "bs_raster2d_bwd") if model == "2dgs" else ("bs_raster_fwd",
                                                                                       "bs_raster_bwd")
         self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
@@ -315,8 +316,17 @@ class SplatTrainer:
                                                          len(lay.my_views), cams.index_select(0, mine).contiguous(),
                                                          bidx.index_select(0, mine), gt_slots)
             with self._t("a2a_bwd"):
-                gsp = self.comm.backward(gsp_recv[: lay.n_recv * self.gsp_floats], lay,
-                                         self.gsp_floats).reshape(-1)
+                # only the used floats of a G_SP row travel (3DGS: 9 of the 12)
+                wire = self.gsp_wire_floats
+                g = gsp_recv[: lay.n_recv * self.gsp_floats].view(-1, self.gsp_floats)
+                back = self.comm.backward(g[:, :wire].contiguous().reshape(-1), lay, wire).view(-1, wire)
+                if wire != self.gsp_floats:
+                    full = self.buf.get("gsp_home", max(back.shape[0], 1) * self.gsp_floats, torch.float32)
+                    full = full[: back.shape[0] * self.gsp_floats].view(-1, self.gsp_floats)
+                    full.zero_()
+                    full[:, :wire] = back
+                    back = full
+                gsp = back.reshape(-1)
         # ---- K1b + K5: projection backward fused with Adam
         self.step_count += 1
         ad = nat.AdamDesc()

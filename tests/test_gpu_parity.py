@@ -182,7 +182,9 @@ def test_render_forward_and_backward_tolerance(c1, cuda, bg):
     n = tr.last["n_rows"]
     H, W = tr.H, tr.W
     img = tr.last["image"][: len(batch) * H * W * 3].cpu().numpy().reshape(len(batch), H, W, 3)
-    gsp = tr.last["gsp"][: n * 9].cpu().numpy().reshape(-1, 9)
+    gsp = tr.last["gsp"][: n * 12].cpu().numpy().reshape(-1, 12)
+    assert not gsp[:, 9:].any()  # row padding stays zero
+    gsp = gsp[:, :9]
     rows = tr.last["rows_per_view"]
     row0 = np.concatenate([[0], np.cumsum(rows)])
     for s, v in enumerate(batch):
@@ -218,7 +220,9 @@ def test_projection_backward_tolerance(c1, cuda):
     v0 = torch.empty(B, dtype=torch.int64, device=cuda)
     nat.call("bs_scan_counts", nat.ptr(counts), tr.n_groups, B, None, nat.ptr(base), nat.ptr(vr), nat.ptr(v0), st)
     n = int(vr.sum().item())
-    gsp = torch.as_tensor(np.random.default_rng(1).normal(0, 1e-3, (n, 9)).astype(np.float32), device=cuda)
+    g9 = np.random.default_rng(1).normal(0, 1e-3, (n, 9)).astype(np.float32)
+    gsp = torch.zeros((n, nat.GSP_FLOATS), dtype=torch.float32, device=cuda)  # 16-byte aligned rows, 3 pad
+    gsp[:, :9] = torch.as_tensor(g9, device=cuda)
     grad = torch.zeros_like(prm)
     nat.call("bs_project_bwd", nat.ProjDesc(B, 3, 0, 0), nat.ptr(prm), tr.S, nat.ptr(mask), nat.ptr(tr.group_begin),
              tr.n_groups, nat.ptr(base), nat.ptr(v0), nat.ptr(cams), nat.ptr(gsp), nat.ptr(grad), st)
@@ -226,7 +230,7 @@ def test_projection_backward_tolerance(c1, cuda):
     g_ref = np.zeros_like(params)
     m = mask.cpu().numpy().view(np.uint32)
     row = 0
-    gs = gsp.cpu().numpy()
+    gs = g9
     for s, v in enumerate(batch):
         idx = np.flatnonzero((m >> s) & 1).astype(np.int64)
         py_oracle.project_bwd(params, idx, camera_bytes([ds.views[v]]), 3, gs[row:row + len(idx)], g_ref)
@@ -336,7 +340,7 @@ def test_c2_scale_properties(cuda):
     gtb = torch.as_tensor(gt[batch], device=cuda).float() / 255.0
     ref_loss = (img - gtb).abs().mean(dim=(1, 2, 3)).cpu().numpy()
     np.testing.assert_allclose(losses, ref_loss, rtol=1e-4)
-    assert np.isfinite(tr.last["gsp"][: n * 9].cpu().numpy()).all()
+    assert np.isfinite(tr.last["gsp"][: n * 12].cpu().numpy()).all()
     assert np.isfinite(tr.params.cpu().numpy()).all()
 
 

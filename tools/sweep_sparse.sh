@@ -1,0 +1,6 @@
+# sweep of the direct-RED threshold of the 3DGS raster backward (C2)
+for L in ${LANES:-6 10 14 20}; do
+  BS_NVCC_EXTRA="-DBS_SPARSE_LANES=$L" python -m paper_2512_20017_b200.build -f > /dev/null 2>&1
+  timeout 300 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/sweep_$L.json 2>/dev/null
+  python -c "import json; d=json.load(open('gpurun_out/sweep_$L.json')); print('lanes $L', d['value'], {k:v['ms'] for k,v in d['stages'].items() if 'raster' in k})"
+done
