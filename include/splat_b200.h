@@ -188,9 +188,10 @@ enum { BS_MODEL_3DGS = 0, BS_MODEL_2DGS = 1 };
 /* 2DGS splat-state row (BS_SP2_FLOATS = 24 floats, 96 B): the 20 elements of
  * PAPER.md Table tab:states-2dgs -- 0 u 1 v 2 opacity 3..11 ray transform M
  * (row-major KWH) 12..14 rgb 15 depth 16 radius_x 17 radius_y 18..20 normal
- * -- + 3 pad.  G_SP row: 15 floats (d u, d v, d M[9], d opacity, d rgb). */
+ * -- + 3 pad.  G_SP row: 16 floats (64-byte aligned for 128-bit REDs):
+ * d u, d v, d M[9], d opacity, d rgb, pad. */
 #define BS_SP2_FLOATS 24
-#define BS_GSP2_FLOATS 15
+#define BS_GSP2_FLOATS 16
 typedef struct {
   int32_t n_views;
   int32_t sh_degree; /* 0..3 */

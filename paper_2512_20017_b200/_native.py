@@ -50,7 +50,7 @@ class CullDesc(C.Structure):
 MODEL_3DGS = 0
 MODEL_2DGS = 1
 SP2_FLOATS = 24
-GSP2_FLOATS = 15
+GSP2_FLOATS = 16
 
 
 class ProjDesc(C.Structure):

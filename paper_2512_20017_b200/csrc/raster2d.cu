@@ -12,8 +12,8 @@
 // L = 2 ln(255 o): the union of the bounding box of the image of the disk
 // u^2 + v^2 <= L (dual conic; unbounded -> keep) and the circle
 // |mean2d - pixel| <= sqrt(L / 2), padded by 1%.
-// Backward: 15 gradient terms per splat; up to 5 contributing lanes add them
-// with direct REDs, otherwise they are reduce-scattered over the warp in 16
+// Backward: 15 gradient terms per splat; up to 12 contributing lanes add them
+// with four 128-bit REDs each (64-byte aligned G_SP rows), otherwise they are reduce-scattered over the warp in 16
 // shuffles and one RED per term is issued per (region, splat).  exp is one
 // ex2.approx in both kernels (identical skip / stop decisions).
 #include "splat2d_math.cuh"
@@ -28,7 +28,7 @@ constexpr float kAMax = 0.99f;
 constexpr float kTStop = 1e-4f;
 constexpr float kLog2e2 = 1.4426950408889634f;
 #ifndef BS_SPARSE2_LANES
-#define BS_SPARSE2_LANES 5  // swept on B200 (C3): 0 7.59, 2 7.55, 3 7.45, 5 7.36, 8 7.65 ms
+#define BS_SPARSE2_LANES 12  // swept on B200 (C3, 128-bit REDs): 5 5.74, 8 5.53, 12 5.38, 16 5.41 ms
 #endif
 constexpr int kSparse2 = BS_SPARSE2_LANES;  // contributing lanes handled with direct REDs
 
@@ -395,13 +395,15 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
       float* dst = g_sp + (int64_t)s.row[j] * kGSP2;
       if (__popc(who) <= kSparse2) {
         if (any) {
+          // 64-byte aligned rows: four 128-bit REDs (the 16th float is padding, g[15] = 0)
 #pragma unroll
-          for (int k = 0; k < kGSP2; ++k) atomicAdd(dst + k, g[k]);
+          for (int k = 0; k < 16; k += 4)
+            atomicAdd(reinterpret_cast<float4*>(dst + k), make_float4(g[k], g[k + 1], g[k + 2], g[k + 3]));
         }
       } else {
         const float r = warp_reduce16(g);
         const int idx = lane >> 1;
-        if ((lane & 1) == 0 && idx < kGSP2) atomicAdd(dst + idx, r);
+        if ((lane & 1) == 0 && idx < kGSP2Used) atomicAdd(dst + idx, r);
       }
     }
     __syncwarp();

@@ -26,8 +26,10 @@ namespace bs {
 //   0 u  1 v  2 opacity  3..11 M (row-major)  12 r 13 g 14 b  15 depth
 //   16 radius_x  17 radius_y  18..20 normal (camera frame)  21..23 pad
 constexpr int kSP2 = 24;
-// G_SP row of a 2DGS splat (15 floats): d u, d v, d M[9], d opacity, d rgb
-constexpr int kGSP2 = 15;
+// G_SP row of a 2DGS splat (16 floats, 64-byte aligned; 15 used): d u, d v,
+// d M[9], d opacity, d rgb, pad
+constexpr int kGSP2 = 16;
+constexpr int kGSP2Used = 15;
 
 // View-independent part of a surfel projection (once per point): rotation of
 // the quaternion, the two tangent scales, activated opacity.

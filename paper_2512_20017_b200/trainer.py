@@ -110,7 +110,7 @@ class SplatTrainer:
         self.model_id = nat.MODEL_2DGS if model == "2dgs" else nat.MODEL_3DGS
         self.sp_floats = nat.SP2_FLOATS if model == "2dgs" else nat.SP_FLOATS
         self.gsp_floats = nat.GSP2_FLOATS if model == "2dgs" else nat.GSP_FLOATS
-        self.gsp_wire_floats = nat.GSP2_FLOATS if model == "2dgs" else 9  # floats of a G_SP row that carry data
+        self.gsp_wire_floats = 15 if model == "2dgs" else 9  # floats of a G_SP row that carry data
         self._raster = ("bs_raster2d_fwd", "bs_raster2d_bwd") if model == "2dgs" else ("bs_raster_fwd",
                                                                                       "bs_raster_bwd")
         self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)

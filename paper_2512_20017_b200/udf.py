@@ -158,7 +158,8 @@ class _ProjectFn(torch.autograd.Function):
         g = grad_sp.float()
         if ctx.model_id == nat.MODEL_2DGS:
             # SP2 (u v opac M9 rgb ...) -> G_SP2 (du dv dM9 dopac drgb)
-            gsp = torch.cat([g[:, 0:2], g[:, 3:12], g[:, 2:3], g[:, 12:15]], 1).contiguous()
+            gsp = torch.cat([g[:, 0:2], g[:, 3:12], g[:, 2:3], g[:, 12:15], torch.zeros_like(g[:, :1])],
+                            1).contiguous()  # 16-float rows (include/splat_b200.h)
         else:
             gsp = g[:, :nat.GSP_FLOATS].contiguous()
         grad = torch.zeros_like(planes)

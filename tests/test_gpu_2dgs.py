@@ -70,7 +70,9 @@ def test_render2d_forward_and_backward_tolerance(c1, cuda, bg):
     n = tr.last["n_rows"]
     H, W = tr.H, tr.W
     img = tr.last["image"][: len(batch) * H * W * 3].cpu().numpy().reshape(len(batch), H, W, 3)
-    gsp = tr.last["gsp"][: n * 15].cpu().numpy().reshape(-1, 15)
+    gsp = tr.last["gsp"][: n * 16].cpu().numpy().reshape(-1, 16)
+    assert not gsp[:, 15].any()  # row padding stays zero
+    gsp = gsp[:, :15]
     rows = tr.last["rows_per_view"]
     row0 = np.concatenate([[0], np.cumsum(rows)])
     for s, v in enumerate(batch):
@@ -106,7 +108,9 @@ def test_projection2d_backward_tolerance(c1, cuda):
     v0 = torch.empty(B, dtype=torch.int64, device=cuda)
     nat.call("bs_scan_counts", nat.ptr(counts), tr.n_groups, B, None, nat.ptr(base), nat.ptr(vr), nat.ptr(v0), st)
     n = int(vr.sum().item())
-    gsp = torch.as_tensor(np.random.default_rng(1).normal(0, 1e-3, (n, 15)).astype(np.float32), device=cuda)
+    g15 = np.random.default_rng(1).normal(0, 1e-3, (n, 15)).astype(np.float32)
+    gsp = torch.zeros((n, nat.GSP2_FLOATS), dtype=torch.float32, device=cuda)  # 64-byte aligned rows
+    gsp[:, :15] = torch.as_tensor(g15, device=cuda)
     grad = torch.zeros_like(prm)
     nat.call("bs_project_bwd", nat.ProjDesc(B, 3, 0, 0, nat.MODEL_2DGS), nat.ptr(prm), tr.S, nat.ptr(mask),
              nat.ptr(tr.group_begin), tr.n_groups, nat.ptr(base), nat.ptr(v0), nat.ptr(cams), nat.ptr(gsp),
@@ -115,7 +119,7 @@ def test_projection2d_backward_tolerance(c1, cuda):
     g_ref = np.zeros_like(params)
     m = mask.cpu().numpy().view(np.uint32)
     row = 0
-    gs = gsp.cpu().numpy()
+    gs = g15
     for s, v in enumerate(batch):
         idx = np.flatnonzero((m >> s) & 1).astype(np.int64)
         py_oracle.project_bwd(params, idx, camera_bytes([ds.views[v]]), 3, gs[row:row + len(idx)], g_ref,
