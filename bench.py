@@ -225,7 +225,7 @@ def kernel_bytes(stage, last, S, B, model="3dgs"):
     """Algorithmic (compulsory) bytes of one launch of a stage.
     Per instance: list entry 4 B + the splat fields the rasteriser gathers
     (3DGS 36 B: mean, opacity, conic, rgb; 2DGS 64 B: mean, opacity, M, rgb, depth);
-    per row: SP write (48 / 96 B) and G_SP (36 / 60 B)."""
+    per row: SP write (48 / 96 B) and the used G_SP floats (36 / 60 B)."""
     I, V, slots = last["n_inst"], last["n_rows"], last["n_slots"]
     npx = slots * last["H"] * last["W"]
     per_inst, sp_row, gsp_row = (68, 96, 60) if model == "2dgs" else (40, 48, 36)
