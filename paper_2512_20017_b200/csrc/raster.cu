@@ -124,17 +124,27 @@ struct Splat {
   bool ok;
 };
 
-__device__ __forceinline__ void fetch_splat(Splat& f, const float* __restrict__ sp,
-                                            const uint32_t* __restrict__ inst_rows, int idx, bool ok) {
+__device__ __forceinline__ void fetch_row_data(Splat& f, const float* __restrict__ sp, uint32_t row, bool ok) {
   f.ok = ok;
   if (ok) {
-    f.row = __ldg(inst_rows + idx);
-    const float4* r4 = reinterpret_cast<const float4*>(sp + (int64_t)f.row * BS_SP_FLOATS);
+    f.row = row;
+    const float4* r4 = reinterpret_cast<const float4*>(sp + (int64_t)row * BS_SP_FLOATS);
     f.p0 = __ldg(r4);
     f.p1 = __ldg(r4 + 1);
-    f.b = __ldg(sp + (int64_t)f.row * BS_SP_FLOATS + 8);
-    f.h = __ldg(reinterpret_cast<const float2*>(sp + (int64_t)f.row * BS_SP_FLOATS + 10));
+    f.b = __ldg(sp + (int64_t)row * BS_SP_FLOATS + 8);
+    f.h = __ldg(reinterpret_cast<const float2*>(sp + (int64_t)row * BS_SP_FLOATS + 10));
   }
+}
+
+__device__ __forceinline__ void fetch_splat(Splat& f, const float* __restrict__ sp,
+                                            const uint32_t* __restrict__ inst_rows, int idx, bool ok) {
+  fetch_row_data(f, sp, ok ? __ldg(inst_rows + idx) : 0u, ok);
+}
+
+// Row index of instance idx (prefetched one chunk ahead of its SP row so the
+// two dependent gathers never sit back to back).
+__device__ __forceinline__ uint32_t fetch_row(const uint32_t* __restrict__ inst_rows, int idx, bool ok) {
+  return ok ? __ldg(inst_rows + idx) : 0u;
 }
 
 // Can this splat's support (the box of half-widths hx = sp[10], hy = sp[11]
@@ -229,12 +239,14 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
   for (int k = 0; k < PPL; ++k) p[k] = PixelFwd{f2(0.f, 0.f), 1.f, 0.f, 0, !(q.px < a.W && q.py0 + k < a.H)};
   Splat f;
   fetch_splat(f, sp, inst_rows, rg.x + lane, rg.x + lane < rg.y);
+  uint32_t row_next = fetch_row(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
   for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
     if (__all_sync(0xffffffffu, all_done<PPL>(p))) break;
     const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
     if (keep) stage(s, lane, f);
-    fetch_splat(f, sp, inst_rows, b0 + 32 + lane, b0 + 32 + lane < rg.y);
+    fetch_row_data(f, sp, row_next, b0 + 32 + lane < rg.y);
+    row_next = fetch_row(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
     __syncwarp();
     while (bits) {
       const int j = __ffs(bits) - 1;
@@ -443,12 +455,14 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
   const int end = rg.x + warp_n;  // deepest contributor of this warp's pixels
   Splat f;
   fetch_splat(f, sp, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
+  uint32_t row_next = fetch_row(inst_rows, end - 33 - lane, end - 33 - lane >= rg.x);
   // chunks back to front; within a chunk lane j holds instance cend - 1 - j
   for (int cend = end; cend > rg.x; cend -= 32) {
     const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
     if (keep) stage(s, lane, f);
-    fetch_splat(f, sp, inst_rows, cend - 33 - lane, cend - 33 - lane >= rg.x);
+    fetch_row_data(f, sp, row_next, cend - 33 - lane >= rg.x);
+    row_next = fetch_row(inst_rows, cend - 65 - lane, cend - 65 - lane >= rg.x);
     __syncwarp();
     while (bits) {
       const int j = __ffs(bits) - 1;
