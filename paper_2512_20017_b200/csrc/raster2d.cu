@@ -63,15 +63,24 @@ struct Splat2 {
   bool ok;
 };
 
-__device__ __forceinline__ void fetch2(Splat2& f, const float* __restrict__ sp, const uint32_t* __restrict__ rows,
-                                       int idx, bool ok) {
+__device__ __forceinline__ void fetch2_row(Splat2& f, const float* __restrict__ sp, uint32_t row, bool ok) {
   f.ok = ok;
   if (ok) {
-    f.row = __ldg(rows + idx);
-    const float4* r4 = reinterpret_cast<const float4*>(sp + (int64_t)f.row * kSP2);
+    f.row = row;
+    const float4* r4 = reinterpret_cast<const float4*>(sp + (int64_t)row * kSP2);
 #pragma unroll
     for (int k = 0; k < 4; ++k) f.p[k] = __ldg(r4 + k);
   }
+}
+
+__device__ __forceinline__ void fetch2(Splat2& f, const float* __restrict__ sp, const uint32_t* __restrict__ rows,
+                                       int idx, bool ok) {
+  fetch2_row(f, sp, ok ? __ldg(rows + idx) : 0u, ok);
+}
+
+// row index prefetched one chunk ahead of its SP row (no back-to-back dependent gathers)
+__device__ __forceinline__ uint32_t row2(const uint32_t* __restrict__ rows, int idx, bool ok) {
+  return ok ? __ldg(rows + idx) : 0u;
 }
 
 // M rows from the staged layout: r0 = (M0, M1, M2), r1 = (M3, M4, M5), r2 = (M6, M7, M8)
@@ -175,12 +184,14 @@ __global__ void __launch_bounds__(kT2) raster2d_fwd_kernel(R2Args a, const float
   Px2 p{1.f, 0.f, 0.f, 0.f, 0, !inside};
   Splat2 f;
   fetch2(f, sp, inst_rows, rg.x + lane, rg.x + lane < rg.y);
+  uint32_t row_next = row2(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
   for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
     if (__all_sync(0xffffffffu, p.done)) break;
     const bool keep = reaches2(f, x0, x1, y0, y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
     if (keep) stage2(s, lane, f);
-    fetch2(f, sp, inst_rows, b0 + 32 + lane, b0 + 32 + lane < rg.y);
+    fetch2_row(f, sp, row_next, b0 + 32 + lane < rg.y);
+    row_next = row2(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
     __syncwarp();
     while (bits) {
       const int j = __ffs(bits) - 1;
@@ -319,11 +330,13 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
   const int end = rg.x + warp_n;
   Splat2 f;
   fetch2(f, sp, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
+  uint32_t row_next = row2(inst_rows, end - 33 - lane, end - 33 - lane >= rg.x);
   for (int cend = end; cend > rg.x; cend -= 32) {
     const bool keep = reaches2(f, x0, x1, y0, y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
     if (keep) stage2(s, lane, f);
-    fetch2(f, sp, inst_rows, cend - 33 - lane, cend - 33 - lane >= rg.x);
+    fetch2_row(f, sp, row_next, cend - 33 - lane >= rg.x);
+    row_next = row2(inst_rows, cend - 65 - lane, cend - 65 - lane >= rg.x);
     __syncwarp();
     while (bits) {
       const int j = __ffs(bits) - 1;
