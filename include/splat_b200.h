@@ -189,7 +189,12 @@ enum { BS_MODEL_3DGS = 0, BS_MODEL_2DGS = 1 };
  * PAPER.md Table tab:states-2dgs -- 0 u 1 v 2 opacity 3..11 ray transform M
  * (row-major KWH) 12..14 rgb 15 depth 16 radius_x 17 radius_y 18..20 normal
  * -- + 3 pad.  G_SP row: 16 floats (64-byte aligned for 128-bit REDs):
- * d u, d v, d M[9], d opacity, d rgb, pad. */
+ * d u, d v, then the moments Ga = sum dL/dzeta, Gb = sum px dL/dzeta,
+ * Gc = sum py dL/dzeta of the per-pixel zeta = r0 x r1 + px (r1 x r2) +
+ * py (r2 x r0) (r_i rows of M), d opacity, d rgb, pad.  The projection
+ * backward turns the moments into dL/dM (dL/dr0 = r1 x Ga + Gc x r2,
+ * dL/dr1 = Ga x r0 + r2 x Gb, dL/dr2 = Gb x r1 + r0 x Gc); gsp_form = 1
+ * accepts plain dL/dM instead. */
 #define BS_SP2_FLOATS 24
 #define BS_GSP2_FLOATS 16
 typedef struct {

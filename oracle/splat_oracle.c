@@ -921,8 +921,35 @@ static void sh_dir_grad_o(const float* dir, int n_sh, const float* wk, float* gd
   }
 }
 
-static void proj2_bwd(const opoint* pt, const or_camera* c, int n_sh, const oproj2* f, const float* gsp, float* g) {
+static void cross3o(const float* a, const float* b, float* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+static void proj2_bwd(const opoint* pt, const or_camera* c, int n_sh, const oproj2* f, const float* gsp_m, float* g) {
   if (!f->valid) return;
+  /* G_SP2 moments (Ga, Gb, Gc of dL/dzeta) -> dL/dM rows:
+   * dL/dr0 = r1 x Ga + Gc x r2, dL/dr1 = Ga x r0 + r2 x Gb, dL/dr2 = Gb x r1 + r0 x Gc */
+  float gsp[15];
+  for (int k = 0; k < 15; ++k) gsp[k] = gsp_m[k];
+  {
+    const float r0[3] = {f->c0[0], f->c1[0], f->c2[0]}, r1[3] = {f->c0[1], f->c1[1], f->c2[1]},
+                r2[3] = {f->c0[2], f->c1[2], f->c2[2]};
+    const float* Ga = gsp_m + 2;
+    const float* Gb = gsp_m + 5;
+    const float* Gc = gsp_m + 8;
+    float t0[3], t1[3];
+    cross3o(r1, Ga, t0);
+    cross3o(Gc, r2, t1);
+    for (int k = 0; k < 3; ++k) gsp[2 + k] = t0[k] + t1[k];
+    cross3o(Ga, r0, t0);
+    cross3o(r2, Gb, t1);
+    for (int k = 0; k < 3; ++k) gsp[5 + k] = t0[k] + t1[k];
+    cross3o(Gb, r1, t0);
+    cross3o(r0, Gc, t1);
+    for (int k = 0; k < 3; ++k) gsp[8 + k] = t0[k] + t1[k];
+  }
   float dc[3], wk[16] = {0}, gd[3];
   for (int ch = 0; ch < 3; ++ch) dc[ch] = f->col_raw[ch] >= 0.f ? gsp[12 + ch] : 0.f;
   for (int k = 0; k < n_sh; ++k)
@@ -1001,23 +1028,39 @@ typedef struct {
   int ok;
 } oeval2;
 
+static void cross3e(const float* a, const float* b, float* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+/* zeta = h_x x h_y is affine in the pixel; it is evaluated, as in the kernels
+ * (csrc/raster2d.cu stage2/eval2), from the pixel's 8x4 region origin (X, Y):
+ * zeta = z0 + ox (hy0 x r2) + oy (r2 x hx0), z0 = hx0 x hy0, with the
+ * origin-shifted rows hx0 = r0 - X r2, hy0 = r1 - Y r2 and the pixel's integer
+ * offsets (ox, oy) from the origin. */
 static void eval2_o(const float* r, float px, float py, oeval2* e) {
   const float* M = r + 3;
+  const int x = (int)px, y = (int)py; /* pixel centre = integer + 0.5 */
+  const int rx = (x / 8) * 8, ry = (y / 4) * 4;
+  const float X = (float)rx + 0.5f, Y = (float)ry + 0.5f, ox = (float)(x - rx), oy = (float)(y - ry);
+  float z0[3], zb[3], zc[3];
   for (int k = 0; k < 3; ++k) {
-    e->hx[k] = M[k] - px * M[6 + k];
-    e->hy[k] = M[3 + k] - py * M[6 + k];
+    e->hx[k] = M[k] - X * M[6 + k];
+    e->hy[k] = M[3 + k] - Y * M[6 + k];
   }
-  e->z[0] = e->hx[1] * e->hy[2] - e->hx[2] * e->hy[1];
-  e->z[1] = e->hx[2] * e->hy[0] - e->hx[0] * e->hy[2];
-  e->z[2] = e->hx[0] * e->hy[1] - e->hx[1] * e->hy[0];
+  cross3e(e->hx, e->hy, z0);
+  cross3e(e->hy, M + 6, zb);
+  cross3e(M + 6, e->hx, zc);
+  for (int k = 0; k < 3; ++k) e->z[k] = fmaf(zc[k], oy, fmaf(zb[k], ox, z0[k]));
   e->ok = e->z[2] != 0.f;
   if (!e->ok) return;
   e->u = e->z[0] / e->z[2];
   e->v = e->z[1] / e->z[2];
-  e->g3 = e->u * e->u + e->v * e->v;
+  e->g3 = fmaf(e->u, e->u, e->v * e->v);
   e->dx = r[0] - px;
   e->dy = r[1] - py;
-  e->g2 = 2.f * (e->dx * e->dx + e->dy * e->dy);
+  e->g2 = 2.f * fmaf(e->dx, e->dx, e->dy * e->dy);
   e->power = -0.5f * fminf(e->g3, e->g2);
 }
 
@@ -1121,17 +1164,12 @@ int32_t or_render2d_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const 
             /* power = -(u^2 + v^2) / 2, (u, v) = zeta.xy / zeta.z, zeta = hx x hy */
             const float gu = -e.u * dpow, gv = -e.v * dpow;
             const float gz[3] = {gu / e.z[2], gv / e.z[2], -(gu * e.z[0] + gv * e.z[1]) / (e.z[2] * e.z[2])};
-            float ghx[3], ghy[3];
-            ghx[0] = e.hy[1] * gz[2] - e.hy[2] * gz[1];
-            ghx[1] = e.hy[2] * gz[0] - e.hy[0] * gz[2];
-            ghx[2] = e.hy[0] * gz[1] - e.hy[1] * gz[0];
-            ghy[0] = gz[1] * e.hx[2] - gz[2] * e.hx[1];
-            ghy[1] = gz[2] * e.hx[0] - gz[0] * e.hx[2];
-            ghy[2] = gz[0] * e.hx[1] - gz[1] * e.hx[0];
+            /* G_SP2 moments of dL/dzeta: sum gz, sum gz px, sum gz py
+             * (zeta = r0 x r1 + px (r1 x r2) + py (r2 x r0); include/splat_b200.h) */
             for (int k = 0; k < 3; ++k) {
-              g[2 + k] += ghx[k];
-              g[5 + k] += ghy[k];
-              g[8 + k] -= pxf * ghx[k] + pyf * ghy[k];
+              g[2 + k] += gz[k];
+              g[5 + k] += gz[k] * pxf;
+              g[8 + k] += gz[k] * pyf;
             }
           } else {
             /* low-pass branch: power = -(dx^2 + dy^2) */

@@ -124,7 +124,8 @@ struct Model2 {
     project2d_backward(pt, r, sh, c, n_sh, f, gs, g, acc, add);
   }
   __device__ static void finish(const PointIn& pt, const float* acc, float* g) { point_pre2_backward(pt, acc, g); }
-  __device__ static void from_moments(const F&, float*) {}
+  // raster moments of dL/dzeta -> dL/dM rows
+  __device__ static void from_moments(const F& f, float* gs) { gsp2_from_moments(f, gs); }
 };
 
 template <class M>

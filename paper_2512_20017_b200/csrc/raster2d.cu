@@ -12,6 +12,9 @@
 // L = 2 ln(255 o): the union of the bounding box of the image of the disk
 // u^2 + v^2 <= L (dual conic; unbounded -> keep) and the circle
 // |mean2d - pixel| <= sqrt(L / 2), padded by 1%.
+// Per pixel zeta is affine in the pixel (staging computes it at the region
+// origin and its two increments), so the backward accumulates the moments of
+// dL/dzeta instead of dL/dM (include/splat_b200.h, 2DGS G_SP row).
 // Backward: 15 gradient terms per splat; up to 12 contributing lanes add them
 // with four 128-bit REDs each (64-byte aligned G_SP rows), otherwise they are reduce-scattered over the warp in 16
 // shuffles and one RED per term is issued per (region, splat).  exp is one
@@ -119,41 +122,61 @@ __device__ __forceinline__ bool reaches2(const Splat2& f, float x0, float x1, fl
   return fabsf(bx - fminf(fmaxf(bx, x0), x1)) <= hx && fabsf(by - fminf(fmaxf(by, y0), y1)) <= hy;
 }
 
-__device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f) {
-  s.a[lane] = f.p[0];
-  s.b[lane] = f.p[1];
-  s.c[lane] = f.p[2];
+// Staging: zeta = h_x x h_y is affine in the pixel (h_x = r0 - px r2,
+// h_y = r1 - py r2, and r2 x r2 = 0).  Each warp stages zeta at its region
+// origin (X, Y) (the per-pixel formula evaluated once, z0 = hx0 x hy0) and
+// the increments zb = hy0 x r2, zc = r2 x hx0 of the origin-shifted rows, so
+// a pixel needs zeta = z0 + zb ox + zc oy with small exact integer offsets.
+// staged: a = (u, v, opac, z0.x), b = (z0.y, z0.z, zb.x, zb.y),
+//         c = (zb.z, zc.x, zc.y, zc.z), d = (r, g, b, -)
+__device__ __forceinline__ void cross3(const float a[3], const float b[3], float o[3]) {
+  o[0] = __fsub_rn(__fmul_rn(a[1], b[2]), __fmul_rn(a[2], b[1]));
+  o[1] = __fsub_rn(__fmul_rn(a[2], b[0]), __fmul_rn(a[0], b[2]));
+  o[2] = __fsub_rn(__fmul_rn(a[0], b[1]), __fmul_rn(a[1], b[0]));
+}
+
+__device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f, float X, float Y) {
+  float r0[3], r1[3], r2[3];
+  m_rows(f.p[0], f.p[1], f.p[2], r0, r1, r2);
+  float hx[3], hy[3], z0[3], zb[3], zc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    hx[k] = __fsub_rn(r0[k], __fmul_rn(X, r2[k]));
+    hy[k] = __fsub_rn(r1[k], __fmul_rn(Y, r2[k]));
+  }
+  // increments from the origin-shifted rows (small, like the per-pixel
+  // formula's operands): (hx - ox r2) x (hy - oy r2) = z0 + ox (hy x r2) + oy (r2 x hx)
+  cross3(hx, hy, z0);
+  cross3(hy, r2, zb);
+  cross3(r2, hx, zc);
+  s.a[lane] = make_float4(f.p[0].x, f.p[0].y, f.p[0].z, z0[0]);
+  s.b[lane] = make_float4(z0[1], z0[2], zb[0], zb[1]);
+  s.c[lane] = make_float4(zb[2], zc[0], zc[1], zc[2]);
   s.d[lane] = f.p[3];  // (r, g, b, depth)
   s.row[lane] = f.row;
 }
 
 struct Eval2 {
-  float hx[3], hy[3], z[3], iz, u, v, g3, dx, dy, g2, power;
+  float z[3], iz, u, v, g3, dx, dy, g2, power;
   bool ok;
 };
 
 // Bit-identical in forward and backward (explicit round-to-nearest ops).
+// (ox, oy): the pixel's offset from the region origin (small integers).
 __device__ __forceinline__ void eval2(const float4& a, const float4& b, const float4& c, float px, float py,
-                                      Eval2& e) {
-  float r0[3], r1[3], r2[3];
-  m_rows(a, b, c, r0, r1, r2);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    e.hx[k] = __fsub_rn(r0[k], __fmul_rn(px, r2[k]));
-    e.hy[k] = __fsub_rn(r1[k], __fmul_rn(py, r2[k]));
-  }
-  e.z[0] = __fsub_rn(__fmul_rn(e.hx[1], e.hy[2]), __fmul_rn(e.hx[2], e.hy[1]));
-  e.z[1] = __fsub_rn(__fmul_rn(e.hx[2], e.hy[0]), __fmul_rn(e.hx[0], e.hy[2]));
-  e.z[2] = __fsub_rn(__fmul_rn(e.hx[0], e.hy[1]), __fmul_rn(e.hx[1], e.hy[0]));
+                                      float ox, float oy, Eval2& e) {
+  e.z[0] = __fmaf_rn(c.y, oy, __fmaf_rn(b.z, ox, a.w));
+  e.z[1] = __fmaf_rn(c.z, oy, __fmaf_rn(b.w, ox, b.x));
+  e.z[2] = __fmaf_rn(c.w, oy, __fmaf_rn(c.x, ox, b.y));
   e.ok = e.z[2] != 0.f;
   if (!e.ok) return;
   e.iz = rcpa(e.z[2]);  // one approximate reciprocal (both kernels evaluate it identically)
   e.u = __fmul_rn(e.z[0], e.iz);
   e.v = __fmul_rn(e.z[1], e.iz);
-  e.g3 = __fadd_rn(__fmul_rn(e.u, e.u), __fmul_rn(e.v, e.v));
+  e.g3 = __fmaf_rn(e.u, e.u, __fmul_rn(e.v, e.v));
   e.dx = __fsub_rn(a.x, px);
   e.dy = __fsub_rn(a.y, py);
-  e.g2 = __fmul_rn(2.f, __fadd_rn(__fmul_rn(e.dx, e.dx), __fmul_rn(e.dy, e.dy)));
+  e.g2 = __fmul_rn(2.f, __fmaf_rn(e.dx, e.dx, __fmul_rn(e.dy, e.dy)));
   e.power = __fmul_rn(-0.5f, fminf(e.g3, e.g2));
 }
 
@@ -179,6 +202,7 @@ __global__ void __launch_bounds__(kT2) raster2d_fwd_kernel(R2Args a, const float
   const int px = rx + (lane & 7), py = ry + (lane >> 3);
   const float x0 = rx + 0.5f, x1 = x0 + 7.f, y0 = ry + 0.5f, y1 = y0 + 3.f;
   const float pxf = px + 0.5f, pyf = py + 0.5f;
+  const float oxf = (float)(lane & 7), oyf = (float)(lane >> 3);  // offset from the region origin (x0, y0)
   const bool inside = px < a.W && py < a.H;
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
   Px2 p{1.f, 0.f, 0.f, 0.f, 0, !inside};
@@ -189,7 +213,7 @@ __global__ void __launch_bounds__(kT2) raster2d_fwd_kernel(R2Args a, const float
     if (__all_sync(0xffffffffu, p.done)) break;
     const bool keep = reaches2(f, x0, x1, y0, y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
-    if (keep) stage2(s, lane, f);
+    if (keep) stage2(s, lane, f, x0, y0);
     fetch2_row(f, sp, row_next, b0 + 32 + lane < rg.y);
     row_next = row2(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
     __syncwarp();
@@ -199,7 +223,7 @@ __global__ void __launch_bounds__(kT2) raster2d_fwd_kernel(R2Args a, const float
       if (p.done) continue;
       Eval2 e;
       const float4 sa = s.a[j];
-      eval2(sa, s.b[j], s.c[j], pxf, pyf, e);
+      eval2(sa, s.b[j], s.c[j], pxf, pyf, oxf, oyf, e);
       if (!e.ok || e.power > 0.f) continue;
       const float alpha = fminf(kAMax, __fmul_rn(sa.z, ex2a(__fmul_rn(e.power, kLog2e2))));
       if (alpha < kAMin) continue;
@@ -297,6 +321,7 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
   const int px = rx + (lane & 7), py = ry + (lane >> 3);
   const float x0 = rx + 0.5f, x1 = x0 + 7.f, y0 = ry + 0.5f, y1 = y0 + 3.f;
   const float pxf = px + 0.5f, pyf = py + 0.5f;
+  const float oxf = (float)(lane & 7), oyf = (float)(lane >> 3);  // offset from the region origin (x0, y0)
   const bool inside = px < a.W && py < a.H;
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
   PxB2 q;
@@ -334,7 +359,7 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
   for (int cend = end; cend > rg.x; cend -= 32) {
     const bool keep = reaches2(f, x0, x1, y0, y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
-    if (keep) stage2(s, lane, f);
+    if (keep) stage2(s, lane, f, x0, y0);
     fetch2_row(f, sp, row_next, cend - 33 - lane >= rg.x);
     row_next = row2(inst_rows, cend - 65 - lane, cend - 65 - lane >= rg.x);
     __syncwarp();
@@ -349,7 +374,7 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
       if (rel < q.n) {
         const float4 sa = s.a[j];
         Eval2 e;
-        eval2(sa, s.b[j], s.c[j], pxf, pyf, e);
+        eval2(sa, s.b[j], s.c[j], pxf, pyf, oxf, oyf, e);
         if (e.ok && e.power <= 0.f) {
           const float ex = ex2a(__fmul_rn(e.power, kLog2e2));
           const float raw = __fmul_rn(sa.z, ex);
@@ -374,26 +399,21 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
               const float dpow = dLda * alpha;
               g[11] = dLda * ex;
               if (e.g3 <= e.g2) {
-                // power = -0.5 (u^2 + v^2)
+                // power = -0.5 (u^2 + v^2), (u, v) = zeta.xy / zeta.z; G_SP2
+                // carries the moments sum gz, sum gz px, sum gz py of
+                // dL/dzeta (the projection backward applies the M rows)
                 const float gu = -e.u * dpow, gv = -e.v * dpow;
                 const float iz = e.iz;
-                const float gz0 = gu * iz, gz1 = gv * iz, gz2 = -(gu * e.z[0] + gv * e.z[1]) * iz * iz;
-                // zeta = hx x hy: d/dhx = hy x gz, d/dhy = gz x hx
-                const float ghx0 = e.hy[1] * gz2 - e.hy[2] * gz1;
-                const float ghx1 = e.hy[2] * gz0 - e.hy[0] * gz2;
-                const float ghx2 = e.hy[0] * gz1 - e.hy[1] * gz0;
-                const float ghy0 = gz1 * e.hx[2] - gz2 * e.hx[1];
-                const float ghy1 = gz2 * e.hx[0] - gz0 * e.hx[2];
-                const float ghy2 = gz0 * e.hx[1] - gz1 * e.hx[0];
-                g[2] = ghx0;
-                g[3] = ghx1;
-                g[4] = ghx2;
-                g[5] = ghy0;
-                g[6] = ghy1;
-                g[7] = ghy2;
-                g[8] = -(pxf * ghx0 + pyf * ghy0);
-                g[9] = -(pxf * ghx1 + pyf * ghy1);
-                g[10] = -(pxf * ghx2 + pyf * ghy2);
+                const float gz0 = gu * iz, gz1 = gv * iz, gz2 = -(gu * e.u + gv * e.v) * iz;
+                g[2] = gz0;
+                g[3] = gz1;
+                g[4] = gz2;
+                g[5] = gz0 * pxf;
+                g[6] = gz1 * pxf;
+                g[7] = gz2 * pxf;
+                g[8] = gz0 * pyf;
+                g[9] = gz1 * pyf;
+                g[10] = gz2 * pyf;
               } else {
                 // power = -(dx^2 + dy^2), dx = u - px
                 g[0] = -2.f * e.dx * dpow;

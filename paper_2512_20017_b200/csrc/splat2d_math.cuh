@@ -157,6 +157,37 @@ __device__ __forceinline__ void write_sp2_row(float* __restrict__ row, const Pro
   r4[5] = make_float4(f.normal[2], 0.f, 0.f, 0.f);
 }
 
+// G_SP2 rows from the rasteriser carry, in entries 2..10, the moments
+// Ga = sum dL/dzeta, Gb = sum px dL/dzeta, Gc = sum py dL/dzeta of the
+// per-pixel zeta = r0 x r1 + px (r1 x r2) + py (r2 x r0) (r_i: rows of M).
+// dL/dr0 = r1 x Ga + Gc x r2, dL/dr1 = Ga x r0 + r2 x Gb,
+// dL/dr2 = Gb x r1 + r0 x Gc  ->  entries 2..10 become dL/dM (row-major).
+__device__ __forceinline__ void cross3f(const float a[3], const float b[3], float o[3]) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+__device__ __forceinline__ void gsp2_from_moments(const Proj2D& f, float* gs) {
+  const float r0[3] = {f.c0[0], f.c1[0], f.c2[0]};
+  const float r1[3] = {f.c0[1], f.c1[1], f.c2[1]};
+  const float r2[3] = {f.c0[2], f.c1[2], f.c2[2]};
+  const float Ga[3] = {gs[2], gs[3], gs[4]}, Gb[3] = {gs[5], gs[6], gs[7]}, Gc[3] = {gs[8], gs[9], gs[10]};
+  float t0[3], t1[3];
+  cross3f(r1, Ga, t0);
+  cross3f(Gc, r2, t1);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) gs[2 + k] = t0[k] + t1[k];
+  cross3f(Ga, r0, t0);
+  cross3f(r2, Gb, t1);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) gs[5 + k] = t0[k] + t1[k];
+  cross3f(Gb, r1, t0);
+  cross3f(r0, Gc, t1);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) gs[8 + k] = t0[k] + t1[k];
+}
+
 // Accumulate the parameter gradient of one (point, view) pair.
 // gsp = (du, dv, dM[9] row-major, dopacity, dr, dg, db).
 // GR accumulates dL/dRq (row-major) for point_pre2_backward.

@@ -240,7 +240,13 @@ class _RenderFn(torch.autograd.Function):
         grad_rows = torch.zeros_like(rows)
         if model_id == nat.MODEL_2DGS:
             grad_rows[:, 0:2] = g_sp[:, 0:2]
-            grad_rows[:, 3:12] = g_sp[:, 2:11]
+            # moments Ga, Gb, Gc of dL/dzeta (include/splat_b200.h) -> dL/dM rows
+            r0, r1, r2 = rows[:, 3:6], rows[:, 6:9], rows[:, 9:12]
+            ga, gb, gc = g_sp[:, 2:5], g_sp[:, 5:8], g_sp[:, 8:11]
+            cr = torch.linalg.cross
+            grad_rows[:, 3:6] = cr(r1, ga) + cr(gc, r2)
+            grad_rows[:, 6:9] = cr(ga, r0) + cr(r2, gb)
+            grad_rows[:, 9:12] = cr(gb, r1) + cr(r0, gc)
             grad_rows[:, 2] = g_sp[:, 11]
             grad_rows[:, 12:15] = g_sp[:, 12:15]
         else:

@@ -21,6 +21,7 @@ pytestmark = pytest.mark.gpu
 
 IMG_TOL = 1e-4
 GRAD_REL = 1e-4
+RASTER_GRAD_REL = 1e-4  # raster-produced G_SP2 and the dL/dM it encodes
 
 
 @pytest.fixture(scope="module")
@@ -83,7 +84,21 @@ def test_render2d_forward_and_backward_tolerance(c1, cuda, bg):
         g = gsp[row0[s]:row0[s + 1]]
         scale = np.abs(ref["gsp"]).max(axis=0) + 1e-30
         err = (np.abs(g - ref["gsp"]) / scale).max(axis=0)
-        assert (err <= GRAD_REL).all(), err
+        assert (err <= RASTER_GRAD_REL).all(), err
+        # the dL/dM the moments encode (converted with the bit-exact rows)
+        dm, dm_ref = _moments_to_dM(g, ref["sp"]), _moments_to_dM(ref["gsp"], ref["sp"])
+        err_m = (np.abs(dm - dm_ref) / (np.abs(dm_ref).max(axis=0) + 1e-30)).max(axis=0)
+        assert (err_m <= RASTER_GRAD_REL).all(), err_m
+
+
+def _moments_to_dM(gsp, sp):
+    """G_SP2 entries 2..10 (moments Ga, Gb, Gc of dL/dzeta) -> dL/dM rows in
+    float64 (include/splat_b200.h)."""
+    g = gsp.astype(np.float64)
+    r0, r1, r2 = (sp[:, 3 + 3 * k:6 + 3 * k].astype(np.float64) for k in range(3))
+    ga, gb, gc = g[:, 2:5], g[:, 5:8], g[:, 8:11]
+    return np.concatenate([np.cross(r1, ga) + np.cross(gc, r2), np.cross(ga, r0) + np.cross(r2, gb),
+                           np.cross(gb, r1) + np.cross(r0, gc)], axis=1)
 
 
 def test_projection2d_backward_tolerance(c1, cuda):

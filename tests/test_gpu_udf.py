@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 
 IMG_TOL = 1e-4
 GRAD_REL = 1e-4
+GRAD_REL_2DGS = 1e-4
 
 
 @pytest.fixture(scope="module")
@@ -81,7 +82,7 @@ def test_udf_pipeline_matches_oracle(c1, cuda, model):
         if model == "2dgs":
             err[1, 2:] = 0.0  # third scale / pad: unused by surfels (both zero)
         err[1, 3] = 0.0
-        assert (err <= GRAD_REL).all(), err.max()
+        assert (err <= (GRAD_REL_2DGS if model == "2dgs" else GRAD_REL)).all(), err.max()
 
 
 def test_udf_temporal_culling(c1, cuda):
