@@ -43,6 +43,12 @@ CONFIGS = {
     "c3": dict(seed=2, n_points=2_000_000, grid=(1, 1), n_views=8, altitude=50.0, image_size=(1920, 1080),
                batch=4, G=2048, model="2dgs",
                desc="synthetic 2DGS aerial scene, 2M surfels, 1080p cameras, batch 4"),
+    # configs[3]: city scale, 50M Gaussians, 4K cameras, batch 16; strong scaling
+    # over N (points sharded by the partition, the global batch stays 16);
+    # ground truth only for the scheduled views (SeedSequence([seed, 5, view]))
+    "c4": dict(seed=3, n_points=50_000_000, grid=(8, 8), n_views=256, altitude=50.0, image_size=(3840, 2160),
+               batch=16, G=2048, scaling="strong", gt_subset=True,
+               desc="synthetic city-scale 3DGS, 50M Gaussians, 4K cameras, batch 16"),
 }
 METRIC = "train images/s (fwd+bwd) at 1/2/4/8 B200, % HBM roofline; comm bytes/step"
 
@@ -111,7 +117,9 @@ class ClockSampler:
         return out
 
 
-def build_scene(cfg, rank=0, world=1):
+def build_scene(cfg, rank=0, world=1, gt_views=None):
+    """Scene, Z-order groups, Gaussian attributes and ground truth (all views,
+    or only `gt_views` when the configuration asks for a subset)."""
     from paper_2512_20017_b200 import scenes
     from paper_2512_20017_b200.culling import zorder_group
 
@@ -121,7 +129,10 @@ def build_scene(cfg, rank=0, world=1):
     spacing = scenes.mean_spacing(cfg["altitude"], cfg["grid"], cfg["n_points"])
     params = scenes.init_gaussians(g.sorted_cloud, cfg["seed"], spacing)
     W, H = cfg["image_size"]
-    gt = scenes.synthetic_gt(cfg["seed"], cfg["n_views"], W, H)
+    if cfg.get("gt_subset") and gt_views is not None:
+        gt = scenes.synthetic_gt_views(cfg["seed"], gt_views, W, H)
+    else:
+        gt = scenes.synthetic_gt(cfg["seed"], cfg["n_views"], W, H)
     return ds, g, params, gt
 
 
@@ -271,20 +282,24 @@ def run_ours(args, cfg):
 
         # BS_DIST_BACKEND=gloo: several ranks sharing one GPU (plumbing tests)
         dist.init_process_group(os.environ.get("BS_DIST_BACKEND", "nccl"))
-        cfg = weak_scaled(cfg, world)
+        if cfg.get("scaling", "weak") == "weak":
+            cfg = weak_scaled(cfg, world)
+    strong = cfg.get("scaling", "weak") == "strong"
+    B = cfg["batch"] if strong else cfg["batch"] * world
+    sched = schedule(cfg["n_views"], B, args.warmup + 2 * args.steps + 2)
+    gt_ids = sorted({v for b in sched for v in b}) if cfg.get("gt_subset") else None
     t0 = time.time()
-    ds, g, params, gt = build_scene(cfg)
+    ds, g, params, gt = build_scene(cfg, gt_views=gt_ids)
+    gt_row = (lambda v: v) if gt_ids is None else {v: k for k, v in enumerate(gt_ids)}.__getitem__
     gb, aabb = g.group_begin(), g.aabbs.reshape(-1, 6)
     if world > 1:
         params, gb, aabb, part_info = shard_for_rank(ds, g, params, world, rank)
         comm = SplatExchange()
     setup_s = time.time() - t0
     W, H = cfg["image_size"]
-    B = cfg["batch"] * world
     model = cfg.get("model", "3dgs")
     tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt, adam=AdamConfig(scenes.lr_table(cfg["altitude"])),
-                      comm=comm, model=model)
-    sched = schedule(cfg["n_views"], B, args.warmup + 2 * args.steps + 2)
+                      comm=comm, model=model, gt_view_ids=gt_ids)
     # clocks are sampled from the start of the warm-up to the end of the timed
     # region (nvidia-smi needs ~0.5 s to start streaming)
     clk = ClockSampler(local).__enter__()
@@ -351,7 +366,7 @@ def run_ours(args, cfg):
             if freed[i % 2] is not None:
                 copy_stream.wait_event(freed[i % 2])
             for k, v in enumerate(e2e_sched[i]):
-                gt_bufs[i % 2][k].copy_(pinned[v], non_blocking=True)
+                gt_bufs[i % 2][k].copy_(pinned[gt_row(v)], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(copy_stream)
             ready[i % 2] = ev
@@ -404,12 +419,12 @@ def run_ours(args, cfg):
                      "gbs": round(nb / (v / 1000.0) / 1e9, 1) if nb else None}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, ds, g, params, gt, steps=1)
+        cpu = cpu_baseline(cfg, ds, g, params, gt, steps=1, gt_row=gt_row)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["desc"], "primitive": model, "n_points": cfg["n_points"],
                        "image": list(cfg["image_size"]), "global_batch": B, "views": cfg["n_views"], "group_size": cfg["G"],
                        "parallelism": f"points+images x{world}",
@@ -433,7 +448,7 @@ def run_ours(args, cfg):
         torch.distributed.destroy_process_group()
 
 
-def cpu_baseline(cfg, ds, g, params, gt, steps=1, warmup=0):
+def cpu_baseline(cfg, ds, g, params, gt, steps=1, warmup=0, gt_row=lambda v: v):
     """CPU oracle training step on this host, bounded sample: 1 view of the
     configuration per step, all host threads."""
     from oracle import py_oracle
@@ -449,11 +464,13 @@ def cpu_baseline(cfg, ds, g, params, gt, steps=1, warmup=0):
     views = [ds.views[i % len(ds.views)] for i in range(steps + warmup)]
     for k in range(warmup):
         py_oracle.train_step(p, m, v, batch_planes([views[k]], 1), camera_bytes([views[k]]),
-                             gt[views[k].id:views[k].id + 1], 3, lr, 0.9, 0.999, 1e-15, k + 1, model=model)
+                             gt[gt_row(views[k].id):gt_row(views[k].id) + 1], 3, lr, 0.9, 0.999, 1e-15, k + 1,
+                             model=model)
     t0 = time.perf_counter()
     for k in range(warmup, warmup + steps):
         vv = views[k]
-        py_oracle.train_step(p, m, v, batch_planes([vv], 1), camera_bytes([vv]), gt[vv.id:vv.id + 1], 3, lr, 0.9,
+        py_oracle.train_step(p, m, v, batch_planes([vv], 1), camera_bytes([vv]), gt[gt_row(vv.id):gt_row(vv.id) + 1], 3,
+                             lr, 0.9,
                              0.999, 1e-15, k + 1, model=model)
     dt = time.perf_counter() - t0
     return {"value": round(steps / dt, 5), "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
@@ -466,8 +483,8 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    ds, g, params, gt = build_scene_host(cfg)
-    cpu = cpu_baseline(cfg, ds, g, params, gt, steps=args.steps, warmup=min(args.warmup, 1))
+    ds, g, params, gt, gt_row = build_scene_host(cfg, args.steps + min(args.warmup, 1))
+    cpu = cpu_baseline(cfg, ds, g, params, gt, steps=args.steps, warmup=min(args.warmup, 1), gt_row=gt_row)
     line = {"metric": METRIC, "impl": "reference", "value": cpu["value"], "unit": "images/s",
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1000.0 / cpu["value"], 2), "higher_is_better": True, "scaling": "weak",
@@ -479,7 +496,7 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def build_scene_host(cfg):
+def build_scene_host(cfg, n_used=None):
     """Scene on the host only (reference arm: no GPU involvement)."""
     from oracle import py_oracle
     from paper_2512_20017_b200 import scenes
@@ -491,7 +508,11 @@ def build_scene_host(cfg):
     params = scenes.init_gaussians(sorted_cloud, cfg["seed"],
                                    scenes.mean_spacing(cfg["altitude"], cfg["grid"], cfg["n_points"]))
     W, H = cfg["image_size"]
-    return ds, None, params, scenes.synthetic_gt(cfg["seed"], cfg["n_views"], W, H)
+    if cfg.get("gt_subset") and n_used is not None:
+        ids = [i % cfg["n_views"] for i in range(n_used)]
+        return (ds, None, params, scenes.synthetic_gt_views(cfg["seed"], ids, W, H),
+                {v: k for k, v in enumerate(ids)}.__getitem__)
+    return ds, None, params, scenes.synthetic_gt(cfg["seed"], cfg["n_views"], W, H), (lambda v: v)
 
 
 def main():

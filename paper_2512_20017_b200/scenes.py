@@ -343,7 +343,6 @@ def init_gaussians(cloud: PointCloud, seed: int, spacing: float) -> np.ndarray:
     quat = rng.normal(0.0, 1.0, size=(S, 4))
     op = rng.uniform(0.1, 0.9, size=S)
     sh0 = rng.normal(0.0, 0.3, size=(S, 3))
-    shn = rng.normal(0.0, 0.03, size=(S, 45))
     out = np.zeros((15, S, 4), dtype=np.float32)
     out[0, :, :3] = cloud.positions
     out[0, :, 3] = np.log(op / (1.0 - op))
@@ -351,8 +350,14 @@ def init_gaussians(cloud: PointCloud, seed: int, spacing: float) -> np.ndarray:
     ls[:, 2] = np.log(0.3 * spacing * f[:, 2])
     out[1, :, :3] = ls
     out[2] = quat / np.linalg.norm(quat, axis=1, keepdims=True)
-    sh = np.concatenate([sh0, shn], axis=1).astype(np.float32)  # (S, 48), f = 3k + channel
-    out[3:15] = sh.reshape(S, 12, 4).transpose(1, 0, 2)
+    # shN drawn in row blocks (the same stream as one (S, 45) draw) so that
+    # 50M-200M point scenes do not materialise float64 [S, 48] copies
+    step = 1 << 22
+    for r0 in range(0, S, step):
+        r1 = min(S, r0 + step)
+        shn = rng.normal(0.0, 0.03, size=(r1 - r0, 45))
+        sh = np.concatenate([sh0[r0:r1], shn], axis=1).astype(np.float32)  # f = 3k + channel
+        out[3:15, r0:r1] = sh.reshape(r1 - r0, 12, 4).transpose(1, 0, 2)
     return out
 
 
@@ -360,6 +365,17 @@ def synthetic_gt(seed: int, n_views: int, width: int, height: int) -> np.ndarray
     """Ground-truth images u8 [n_views, H, W, 3] from SeedSequence([seed, 5])."""
     rng = _stream(seed, 5)
     return rng.integers(0, 256, size=(n_views, height, width, 3), dtype=np.uint8)
+
+
+def synthetic_gt_views(seed: int, view_ids, width: int, height: int) -> np.ndarray:
+    """Ground truth of selected views only, u8 [len(view_ids), H, W, 3]; view v
+    from SeedSequence([seed, 5, v]) (large configurations, where materialising
+    every view is wasteful)."""
+    out = np.empty((len(view_ids), height, width, 3), dtype=np.uint8)
+    for k, v in enumerate(view_ids):
+        rng = np.random.default_rng(np.random.SeedSequence([int(seed), 5, int(v)]))
+        out[k] = rng.integers(0, 256, size=(height, width, 3), dtype=np.uint8)
+    return out
 
 
 def mean_spacing(altitude: float, grid, n_points: int) -> float:

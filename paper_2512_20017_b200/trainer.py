@@ -102,7 +102,8 @@ class SplatTrainer:
 
     def __init__(self, params: np.ndarray, group_begin: np.ndarray, aabb: np.ndarray, views, gt=None,
                  sh_degree: int = 3, adam: AdamConfig | None = None, device=None, comm=None,
-                 bg=(0.0, 0.0, 0.0), model: str = "3dgs", presence: np.ndarray | None = None):
+                 bg=(0.0, 0.0, 0.0), model: str = "3dgs", presence: np.ndarray | None = None,
+                 gt_view_ids=None):
         nat.load()
         if model not in ("3dgs", "2dgs"):
             raise ValueError(f"unknown splat model {model!r} (3dgs | 2dgs)")
@@ -149,6 +150,12 @@ class SplatTrainer:
             self.view_times = torch.as_tensor(np.array([v.time for v in self.views], dtype=np.float32),
                                               device=self.dev)
         self.gt = None if gt is None else torch.as_tensor(gt, device=self.dev)
+        # gt_view_ids: the view id of each row of `gt` when it holds a subset
+        self.gt_lut = None
+        if gt_view_ids is not None:
+            lut = np.full(len(self.views), -1, dtype=np.int32)
+            lut[np.asarray(gt_view_ids, dtype=np.int64)] = np.arange(len(gt_view_ids), dtype=np.int32)
+            self.gt_lut = torch.as_tensor(lut, device=self.dev)
         self.sh_degree = sh_degree
         self.adam = adam if adam is not None else AdamConfig(np.full(60, 1e-3, dtype=np.float32))
         self.step_count = 0
@@ -414,7 +421,7 @@ class SplatTrainer:
             gt, gt_map = gt_batch, None
         else:
             gt = self.gt
-            gt_map = gt_views.to(torch.int32)
+            gt_map = gt_views.to(torch.int32) if self.gt_lut is None else self.gt_lut.index_select(0, gt_views)
         with self._t("raster_fwd"):
             nat.call(self._raster[0], rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
                      nat.ptr(final_T), nat.ptr(n_contrib), nat.ptr(gt), nat.ptr(gt_map), nat.ptr(loss_tiles), st)
