@@ -283,6 +283,11 @@ typedef struct {
   float bg[3];
   int32_t loss_fused;     /* 1: gt given, fwd writes L1 partials per tile */
   int32_t pixels_per_lane;/* 1: 8x4 pixel region per warp, 2 (default, 0): 8x8 */
+  int32_t patch_P;        /* patches per image side (P > 1 with slot_patches) */
+  const uint64_t* slot_patches; /* device uint64 [n_slots] or NULL: bit
+                           (r P + c) set = this slot renders patch (r, c); the
+                           other pixels are neither rendered nor in the loss
+                           (the view's loss normalisation is unchanged) */
 } bs_raster_desc;
 /* image: f32 [n_slots][H][W][3]; final_T: f32 [n_slots][H][W];
  * n_contrib: int32 [n_slots][H][W] (range-relative end of the blend);
@@ -356,6 +361,38 @@ int32_t bs_project_bwd_adam(const bs_proj_desc* pdesc_host,
                             const int32_t* group_begin, int32_t n_groups,
                             const int32_t* base, const int64_t* view_row0,
                             const bs_camera* cams, const float* g_sp,
+                            void* stream);
+
+/* ---- patch placement (P > 1): render sets and the exchange layout ------
+ * Patch j of view v is rendered by rank patch_owner[v P^2 + j] (W of
+ * hierarchical_place, placement.py:316-361).  Replace the reference's
+ * transfer accounting by the rows actually moved (simulator.py:134-183 counts
+ * the access matrix; the render set adds the splats whose support crosses
+ * a patch border). */
+/* dest_mask[r]: bit d set iff rank d renders a patch the support box of row r
+ * reaches.  Rows view-major from view_row0 (ascending). */
+int32_t bs_row_dest_mask(const float* sp_rows, int32_t model, int64_t n_rows,
+                         const int64_t* view_row0, int32_t n_views, int32_t P,
+                         int32_t width, int32_t height,
+                         const int32_t* patch_owner, uint32_t* dest_mask,
+                         void* stream);
+/* Send layout grouped by destination, then view, rows ascending:
+ * count_only = 1 -> dest_total[d]; then count_only = 0 with dest_base (the
+ * exclusive scan of dest_total) -> send_idx[dest_base[d] + k] = row and
+ * view_counts[d][v] (caller zeroes it). */
+size_t bs_dest_compact_workspace(int64_t n_rows, int32_t n_dest);
+int32_t bs_dest_compact(const uint32_t* dest_mask, int64_t n_rows, int32_t n_dest,
+                        const int64_t* view_row0, int32_t n_views, int32_t count_only,
+                        int64_t* dest_total, const int64_t* dest_base, int64_t* send_idx,
+                        int64_t* view_counts, void* workspace, size_t ws_bytes,
+                        void* stream);
+/* dst[i] = src[idx[i]] (rows of `width` floats, width % 4 == 0) */
+int32_t bs_gather_rows(const float* src, int32_t width, const int64_t* idx, int64_t n,
+                       float* dst, void* stream);
+/* dst[idx[i]][k] += src[i][k], k < used (atomic: rows sent to several ranks);
+ * row strides src_width / dst_width floats */
+int32_t bs_scatter_add_rows(const float* src, int32_t src_width, int32_t used,
+                            const int64_t* idx, int64_t n, float* dst, int32_t dst_width,
                             void* stream);
 
 #ifdef __cplusplus

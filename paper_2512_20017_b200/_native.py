@@ -62,7 +62,8 @@ class ProjDesc(C.Structure):
 class RasterDesc(C.Structure):
     _fields_ = [("n_slots", C.c_int32), ("tiles_per_slot", C.c_int32),
                 ("width", C.c_int32), ("height", C.c_int32),
-                ("bg", C.c_float * 3), ("loss_fused", C.c_int32), ("pixels_per_lane", C.c_int32)]
+                ("bg", C.c_float * 3), ("loss_fused", C.c_int32), ("pixels_per_lane", C.c_int32),
+                ("patch_P", C.c_int32), ("slot_patches", C.c_void_p)]
 
 
 class AdamDesc(C.Structure):
@@ -114,6 +115,11 @@ _SIGS = {
     "bs_adam_step": (_I32, [C.POINTER(AdamDesc), _P, _P, _P, _P, _I64, _P, _P]),
     "bs_project_bwd_adam": (_I32, [C.POINTER(ProjDesc), C.POINTER(AdamDesc), _P, _P, _P, _I64, _P, _P,
                                    _I32, _P, _P, _P, _P, _P]),
+    "bs_row_dest_mask": (_I32, [_P, _I32, _I64, _P, _I32, _I32, _I32, _I32, _P, _P, _P]),
+    "bs_dest_compact_workspace": (_SZ, [_I64, _I32]),
+    "bs_dest_compact": (_I32, [_P, _I64, _I32, _P, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
+    "bs_gather_rows": (_I32, [_P, _I32, _P, _I64, _P, _P]),
+    "bs_scatter_add_rows": (_I32, [_P, _I32, _I32, _P, _I64, _P, _I32, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

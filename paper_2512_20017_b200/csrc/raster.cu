@@ -60,8 +60,20 @@ struct RastArgs {
   int n_slots, tiles_per_slot, W, H, tiles_x;
   float bg[3];
   int loss_fused;
-  float inv_norm;  // 1 / (H * W * 3)
+  float inv_norm;
+  int patch_P;
+  const uint64_t* slot_patches;  // NULL: every pixel  // 1 / (H * W * 3)
 };
+
+// Patch restriction (P > 1): does this slot render pixel (x, y)?  Patch c of
+// an image side spans [floor(c W / P), floor((c + 1) W / P)).
+__device__ __forceinline__ bool slot_pixel(const uint64_t* slot_patches, int P, int W, int H, int slot, int x, int y) {
+  if (x >= W || y >= H) return false;
+  if (slot_patches == nullptr) return true;
+  const int pc = ((x + 1) * P - 1) / W, pr = ((y + 1) * P - 1) / H;
+  return (slot_patches[slot] >> (pr * P + pc)) & 1ull;
+}
+
 
 // Packed FP32 pairs (sm_100 FADD2 / FMUL2 / FFMA2: one issue slot for two
 // lanes' worth of FP32 work; a scalar operand is broadcast for free).
@@ -236,7 +248,8 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
   PixelFwd p[PPL];
 #pragma unroll
-  for (int k = 0; k < PPL; ++k) p[k] = PixelFwd{f2(0.f, 0.f), 1.f, 0.f, 0, !(q.px < a.W && q.py0 + k < a.H)};
+  for (int k = 0; k < PPL; ++k)
+    p[k] = PixelFwd{f2(0.f, 0.f), 1.f, 0.f, 0, !slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, q.px, q.py0 + k)};
   Splat f;
   fetch_splat(f, sp, inst_rows, rg.x + lane, rg.x + lane < rg.y);
   uint32_t row_next = fetch_row(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
@@ -264,7 +277,7 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
   float l = 0.f;
 #pragma unroll
   for (int k = 0; k < PPL; ++k) {
-    if (!(q.px < a.W && q.py0 + k < a.H)) continue;
+    if (!slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, q.px, q.py0 + k)) continue;
     const int64_t pix = ((int64_t)slot * a.H + q.py0 + k) * a.W + q.px;
     const float2 c01 = unf2(p[k].c01);
     const float o0 = c01.x + p[k].T * a.bg[0], o1 = c01.y + p[k].T * a.bg[1], o2 = p[k].c2 + p[k].T * a.bg[2];
@@ -447,7 +460,8 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
   int warp_n = 0;
 #pragma unroll
   for (int k = 0; k < PPL; ++k) {
-    init_pixel_bwd(p[k], a, slot, q.px, q.py0 + k, q.px < a.W && q.py0 + k < a.H, image, final_T, n_contrib,
+    init_pixel_bwd(p[k], a, slot, q.px, q.py0 + k,
+                   slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, q.px, q.py0 + k), image, final_T, n_contrib,
                    grad_image, gt, gt_view);
     warp_n = max(warp_n, p[k].n);
   }
@@ -571,6 +585,10 @@ int32_t make_args(const bs_raster_desc* d, RastArgs& a) {
   a.bg[2] = d->bg[2];
   a.loss_fused = d->loss_fused;
   a.inv_norm = (float)(1.0 / (3.0 * (double)d->width * (double)d->height));
+  a.patch_P = d->patch_P > 0 ? d->patch_P : 1;
+  a.slot_patches = d->slot_patches;
+  BS_REQUIRE(a.slot_patches == nullptr || (a.patch_P >= 1 && a.patch_P <= 8 && a.W >= a.patch_P && a.H >= a.patch_P),
+             BS_ERR_PARAMETER, "patch_P must be in [1, 8] with slot_patches");
   return BS_OK;
 }
 

@@ -52,7 +52,19 @@ struct R2Args {
   float bg[3];
   int loss_fused;
   float inv_norm;
+  int patch_P;
+  const uint64_t* slot_patches;  // NULL: every pixel
 };
+
+// Patch restriction (P > 1): does this slot render pixel (x, y)?  Patch c of
+// an image side spans [floor(c W / P), floor((c + 1) W / P)).
+__device__ __forceinline__ bool slot_pixel(const uint64_t* slot_patches, int P, int W, int H, int slot, int x, int y) {
+  if (x >= W || y >= H) return false;
+  if (slot_patches == nullptr) return true;
+  const int pc = ((x + 1) * P - 1) / W, pr = ((y + 1) * P - 1) / H;
+  return (slot_patches[slot] >> (pr * P + pc)) & 1ull;
+}
+
 
 // staged splat: a = (u, v, opac, M0), b = (M1..M4), c = (M5..M8), d = (r, g, b, -)
 struct Warp2 {
@@ -203,7 +215,7 @@ __global__ void __launch_bounds__(kT2) raster2d_fwd_kernel(R2Args a, const float
   const float x0 = rx + 0.5f, x1 = x0 + 7.f, y0 = ry + 0.5f, y1 = y0 + 3.f;
   const float pxf = px + 0.5f, pyf = py + 0.5f;
   const float oxf = (float)(lane & 7), oyf = (float)(lane >> 3);  // offset from the region origin (x0, y0)
-  const bool inside = px < a.W && py < a.H;
+  const bool inside = slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, px, py);
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
   Px2 p{1.f, 0.f, 0.f, 0.f, 0, !inside};
   Splat2 f;
@@ -322,7 +334,7 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
   const float x0 = rx + 0.5f, x1 = x0 + 7.f, y0 = ry + 0.5f, y1 = y0 + 3.f;
   const float pxf = px + 0.5f, pyf = py + 0.5f;
   const float oxf = (float)(lane & 7), oyf = (float)(lane >> 3);  // offset from the region origin (x0, y0)
-  const bool inside = px < a.W && py < a.H;
+  const bool inside = slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, px, py);
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
   PxB2 q;
   q.T = 1.f;
@@ -459,6 +471,10 @@ int32_t make_r2(const bs_raster_desc* d, R2Args& a) {
   a.bg[2] = d->bg[2];
   a.loss_fused = d->loss_fused;
   a.inv_norm = (float)(1.0 / (3.0 * (double)d->width * (double)d->height));
+  a.patch_P = d->patch_P > 0 ? d->patch_P : 1;
+  a.slot_patches = d->slot_patches;
+  BS_REQUIRE(a.slot_patches == nullptr || (a.patch_P >= 1 && a.patch_P <= 8 && a.W >= a.patch_P && a.H >= a.patch_P),
+             BS_ERR_PARAMETER, "patch_P must be in [1, 8] with slot_patches");
   return BS_OK;
 }
 

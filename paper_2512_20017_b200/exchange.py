@@ -159,6 +159,14 @@ class SplatExchange:
             self._ahead.pop(stale)
         self._ahead[key] = self._pool.submit(job)
 
+    def exchange_counts(self, counts: torch.Tensor) -> np.ndarray:
+        """counts int64 [N, K] (row d: values for rank d) -> [N, K] on the host,
+        row s: the values rank s addressed to this rank (one all_to_all)."""
+        src = self._stage(counts.contiguous().view(-1))
+        out = torch.empty_like(src)
+        dist.all_to_all_single(out, src, group=self.group)
+        return out.view(self.world, -1).cpu().numpy().astype(np.int64)
+
     def _a2a(self, send: torch.Tensor, send_rows, recv_rows, width: int) -> torch.Tensor:
         src = self._stage(send.view(-1, width))
         recv = torch.empty((int(sum(recv_rows)), width), dtype=send.dtype, device=src.device)

@@ -103,7 +103,7 @@ class SplatTrainer:
     def __init__(self, params: np.ndarray, group_begin: np.ndarray, aabb: np.ndarray, views, gt=None,
                  sh_degree: int = 3, adam: AdamConfig | None = None, device=None, comm=None,
                  bg=(0.0, 0.0, 0.0), model: str = "3dgs", presence: np.ndarray | None = None,
-                 gt_view_ids=None):
+                 gt_view_ids=None, patches: int = 1):
         nat.load()
         if model not in ("3dgs", "2dgs"):
             raise ValueError(f"unknown splat model {model!r} (3dgs | 2dgs)")
@@ -131,7 +131,14 @@ class SplatTrainer:
         self.tiles_x = (self.W + nat.TILE - 1) // nat.TILE
         self.tiles_y = (self.H + nat.TILE - 1) // nat.TILE
         self.tiles = self.tiles_x * self.tiles_y
-        self.planes_all = torch.as_tensor(np.stack([view_plane_block(v, 1) for v in self.views]), device=self.dev)
+        # patches per image side: with several ranks each of the B P^2 patches
+        # of a batch is placed on its own; one rank renders
+        # whole views whatever P is
+        if not (1 <= int(patches) <= 8):
+            raise ValueError("patches (P) must be in [1, 8]")
+        self.P = int(patches)
+        self.planes_all = torch.as_tensor(np.stack([view_plane_block(v, self.P) for v in self.views]),
+                                          device=self.dev)
         self.cams_all = torch.as_tensor(camera_bytes(self.views), device=self.dev)
         # 4DGS spatio-temporal culling (visibility.py:244-252):
         # point i is a candidate for view v iff presence[i, 0] <= t_v <= presence[i, 1] (f32)
@@ -217,17 +224,17 @@ class SplatTrainer:
         self._ids_ev[k] = ev
         return dst
 
-    def _cull_counts(self, batch_ids, mask, counts, base, view_rows, view_row0, st, bidx=None):
+    def _cull_counts(self, batch_ids, mask, counts, base, view_rows, view_row0, st, bidx=None, patch_counts=None):
         B = len(batch_ids)
         if bidx is None:
             bidx = self._device_ids(batch_ids, "bidx_cull")
         planes = self.planes_all.index_select(0, bidx).contiguous()
         temporal = self.presence is not None
         times = self.view_times.index_select(0, bidx).contiguous() if temporal else None
-        desc = nat.CullDesc(nat.CULL_MASK, B, 1, 1, 1 if temporal else 0, 4)
+        desc = nat.CullDesc(nat.CULL_MASK, B, self.P, 1, 1 if temporal else 0, 4)
         nat.call("bs_cull_count", desc, nat.ptr(self.params), self.S, nat.ptr(self.presence),
                  nat.ptr(self.group_begin), nat.ptr(self.aabb), self.n_groups, nat.ptr(planes), nat.ptr(times),
-                 None, nat.ptr(mask), nat.ptr(counts), None, st)
+                 None, nat.ptr(mask), nat.ptr(counts), nat.ptr(patch_counts), st)
         order = np.arange(B, dtype=np.int32)
         nat.call("bs_scan_counts", nat.ptr(counts), self.n_groups, B, order.ctypes.data, nat.ptr(base),
                  nat.ptr(view_rows), nat.ptr(view_row0), st)
@@ -249,9 +256,14 @@ class SplatTrainer:
         base = self.buf.get("base", self.n_groups * B, torch.int32)
         view_rows = self.buf.get("view_rows", B, torch.int64)
         view_row0 = self.buf.get("view_row0", B, torch.int64)
+        patched = self.comm is not None and self.P > 1
+        patch_counts = self.buf.get("patch_counts", B * self.P * self.P, torch.int64) if patched else None
         with self._t("cull"):
-            self._cull_counts(batch_ids, mask, counts, base, view_rows, view_row0, st, bidx)
-        if self.comm is not None and next_batch is not None:
+            self._cull_counts(batch_ids, mask, counts, base, view_rows, view_row0, st, bidx, patch_counts)
+        if patched:
+            return self._step_patches(batch_ids, gt_batch, bidx, cams, mask, base, view_rows, view_row0,
+                                      patch_counts, st)
+        if self.comm is not None and next_batch is not None and self.P == 1:
             # counts of the next batch on the pre-update positions -> async W
             Bn = len(next_batch)
             nb = self.buf
@@ -347,6 +359,101 @@ class SplatTrainer:
                      nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
         return losses
 
+    def _step_patches(self, batch_ids, gt_batch, bidx, cams, mask, base, view_rows, view_row0, patch_counts, st):
+        """Alg. 1 with P x P patches per view on several ranks (SURVEY.md
+        §8(e)): A over the B P^2 patches -> W; every rank projects its points
+        for all batch views, sends each splat row to the ranks whose patches
+        its support reaches (csrc/patches.cu; the render set, a superset of
+        A), renders only the pixels of its own patches, and the returned
+        gradient rows are summed into the rows they came from."""
+        comm, P = self.comm, self.P
+        B, N, me, PP = len(batch_ids), self.comm.world, self.comm.rank, self.P * self.P
+        dev, S = self.dev, self.S
+        with self._t("assign"):
+            A = comm.gather_access(patch_counts)       # int64 [B P^2, N]
+            W = comm.assign(A)                          # patch -> rank
+        rows_host = view_rows.cpu().numpy()
+        n_rows = int(rows_host.sum())
+        self.last.update(A=A, W=W, rows_per_view=rows_host.copy())
+        sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
+        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group)
+        with self._t("project"):
+            nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask), nat.ptr(self.group_begin),
+                     self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(sp), st)
+        # ---- render sets -> send layout (destination, view, row)
+        owner = torch.as_tensor(np.asarray(W, dtype=np.int32), device=dev)
+        dmask = self.buf.get("dest_mask", max(n_rows, 1), torch.int32)
+        nat.call("bs_row_dest_mask", nat.ptr(sp), self.model_id, n_rows, nat.ptr(view_row0), B, P, self.W, self.H,
+                 nat.ptr(owner), nat.ptr(dmask), st)
+        lib = nat.load()
+        ws = self.buf.get("dest_ws", lib.bs_dest_compact_workspace(max(n_rows, 1), N), torch.uint8)
+        totals = self.buf.get("dest_total", N, torch.int64)
+        nat.call("bs_dest_compact", nat.ptr(dmask), n_rows, N, nat.ptr(view_row0), B, 1, nat.ptr(totals), None, None,
+                 None, nat.ptr(ws), ws.numel(), st)
+        send_rows = [int(x) for x in totals.cpu().tolist()]
+        n_send = sum(send_rows)
+        base_d = torch.as_tensor(np.concatenate([[0], np.cumsum(send_rows)[:-1]]).astype(np.int64), device=dev)
+        send_idx = self.buf.get("send_idx", max(n_send, 1), torch.int64)
+        vcounts = self.buf.get("dest_view_counts", N * B, torch.int64)
+        vcounts.zero_()
+        nat.call("bs_dest_compact", nat.ptr(dmask), n_rows, N, nat.ptr(view_row0), B, 0, nat.ptr(totals),
+                 nat.ptr(base_d), nat.ptr(send_idx), nat.ptr(vcounts), nat.ptr(ws), ws.numel(), st)
+        recv_v = comm.exchange_counts(vcounts.view(N, B))   # [source, view] rows coming here
+        recv_rows = [int(x) for x in recv_v.sum(axis=1)]
+        send_sp = self.buf.get("send_sp", max(n_send, 1) * self.sp_floats, torch.float32)
+        nat.call("bs_gather_rows", nat.ptr(sp), self.sp_floats, nat.ptr(send_idx), n_send, nat.ptr(send_sp), st)
+        with self._t("a2a_fwd"):
+            sp_recv = comm._a2a(send_sp[: n_send * self.sp_floats], send_rows, recv_rows, self.sp_floats)
+        comm.bytes_fwd += (n_send - send_rows[me]) * self.sp_floats * 4
+        # ---- render the own patches of every view that has one here
+        Wm = np.asarray(W, dtype=np.int64).reshape(B, PP)
+        my_views = [v for v in range(B) if (Wm[v] == me).any()]
+        slot_bits = np.array([int(sum(1 << j for j in range(PP) if Wm[v, j] == me)) for v in my_views],
+                             dtype=np.uint64)
+        seg_rows, seg_slot = [], []
+        for s_ in range(N):
+            for k, v in enumerate(my_views):
+                seg_rows.append(int(recv_v[s_, v]))
+                seg_slot.append(k)
+        n_recv = int(sum(recv_rows))
+        self.last.update(my_views=my_views, send_rows=send_rows, recv_rows=recv_rows, n_send=n_send)
+        losses = torch.zeros(0, dtype=torch.float32, device=dev)
+        gsp_recv = self.buf.get("gsp_recv_p", max(n_recv, 1) * self.gsp_floats, torch.float32)
+        if my_views:
+            mine = torch.as_tensor(my_views, dtype=torch.int64, device=dev)
+            seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(seg_rows)[:-1]]).astype(np.int64), device=dev)
+            seg_slot_t = torch.as_tensor(np.asarray(seg_slot, dtype=np.int32), device=dev)
+            bits_t = torch.as_tensor(slot_bits.view(np.int64), device=dev)
+            gt_slots = gt_batch.index_select(0, mine).contiguous() if gt_batch is not None else None
+            losses, gsp_recv = self._render_and_backward(sp_recv.reshape(-1), n_recv, seg_row0, seg_slot_t,
+                                                         len(my_views), cams.index_select(0, mine).contiguous(),
+                                                         bidx.index_select(0, mine), gt_slots, slot_patches=bits_t)
+        # ---- gradient rows back to their sources, summed into the row they left
+        wire = self.gsp_wire_floats
+        g = gsp_recv[: n_recv * self.gsp_floats].view(-1, self.gsp_floats)[:, :wire].contiguous()
+        with self._t("a2a_bwd"):
+            back = comm._a2a(g.reshape(-1), recv_rows, send_rows, wire)
+        comm.bytes_bwd += (n_recv - recv_rows[me]) * wire * 4
+        gsp = self.buf.get("gsp_home", max(n_rows, 1) * self.gsp_floats, torch.float32)
+        gsp.zero_()
+        nat.call("bs_scatter_add_rows", nat.ptr(back), wire, wire, nat.ptr(send_idx), n_send, nat.ptr(gsp),
+                 self.gsp_floats, st)
+        self.step_count += 1
+        ad = self._adam_desc()
+        with self._t("project_bwd_adam"):
+            nat.call("bs_project_bwd_adam", pdesc, ad, nat.ptr(self.params), nat.ptr(self.exp_avg),
+                     nat.ptr(self.exp_avg_sq), S, nat.ptr(mask), nat.ptr(self.group_begin), self.n_groups,
+                     nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
+        return losses
+
+    def _adam_desc(self):
+        ad = nat.AdamDesc()
+        for k in range(60):
+            ad.lr[k] = float(self.adam.lr[k])
+        ad.beta1, ad.beta2, ad.eps = self.adam.beta1, self.adam.beta2, self.adam.eps
+        ad.step, ad.selective = self.step_count, 1 if self.adam.selective else 0
+        return ad
+
     def _slot_ids(self, B):
         t = self.buf.bufs.get("slot_ids")
         if t is None or t.numel() < 32:
@@ -393,7 +500,8 @@ class SplatTrainer:
         nat.call("bs_tile_ranges", nat.ptr(ikeys), None, n_inst, n_slots * self.tiles, nat.ptr(ranges), st)
         return n_inst, irows, ranges
 
-    def _render_and_backward(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, gt_views, gt_batch):
+    def _render_and_backward(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, gt_views, gt_batch,
+                             slot_patches=None):
         dev, st = self.dev, nat.stream_handle()
         lib = nat.load()
         gsp = self.buf.get("gsp", max(n_rows, 1) * self.gsp_floats, torch.float32)
@@ -416,7 +524,7 @@ class SplatTrainer:
         n_contrib = self.buf.get("n_contrib", n_slots * npx, torch.int32)
         loss_tiles = self.buf.get("loss_tiles", n_slots * self.tiles, torch.float32)
         rdesc = nat.RasterDesc(n_slots, self.tiles, self.W, self.H, (ctypes.c_float * 3)(*self.bg), 1,
-                               self.pixels_per_lane)
+                               self.pixels_per_lane, self.P, nat.ptr(slot_patches))
         if gt_batch is not None:
             gt, gt_map = gt_batch, None
         else:

@@ -28,7 +28,7 @@ def _setup():
     return ds, g, params, gt
 
 
-def _worker(rank, world, port, q, prefetch=False):
+def _worker(rank, world, port, q, prefetch=False, patches=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
 
@@ -47,7 +47,7 @@ def _worker(rank, world, port, q, prefetch=False):
         sizes = [g.groups[k].size for k in mine]
         gb = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
         tr = SplatTrainer(np.ascontiguousarray(params[:, pts, :]), gb, g.aabbs.reshape(-1, 6)[mine], ds.views,
-                          gt=gt, adam=AdamConfig(scenes.lr_table(50.0)), comm=SplatExchange())
+                          gt=gt, adam=AdamConfig(scenes.lr_table(50.0)), comm=SplatExchange(), patches=patches)
         if prefetch:
             # step 1 starts the asynchronous placement of step 2 (stale W)
             tr.step(BATCH, next_batch=BATCH2)
@@ -57,10 +57,10 @@ def _worker(rank, world, port, q, prefetch=False):
         else:
             losses = tr.step(BATCH).cpu().numpy()
             batch = BATCH
-        lay = tr.last["layout"]
-        n = len(lay.my_views)
-        img = tr.last["image"][: n * 96 * 160 * 3].cpu().numpy().reshape(n, 96, 160, 3)
-        q.put((rank, pts, tr.params.cpu().numpy(), [batch[v] for v in lay.my_views], img, losses,
+        my_views = tr.last["layout"].my_views if patches == 1 else tr.last["my_views"]
+        n = len(my_views)
+        img = tr.last["image"][: n * 96 * 160 * 3].cpu().numpy().reshape(n, 96, 160, 3) if n else None
+        q.put((rank, pts, tr.params.cpu().numpy(), [batch[v] for v in my_views], img, losses,
                tr.last["A"], tr.last["W"]))
     finally:
         dist.destroy_process_group()
@@ -123,3 +123,60 @@ def test_two_ranks_match_single_rank(cuda, prefetch):
         steps = 2 if prefetch else 1
         assert (diff <= 1e-3 * lr_full + 1e-7).mean() > (0.99 if prefetch else 0.999)
         assert (diff <= 2.0 * steps * lr_full + 1e-6).all()
+
+
+def test_two_ranks_patches_match_single_rank(cuda):
+    """P = 2: the 4 x 4 = 16 patches of the batch are placed on 2 ranks; each
+    rank renders only its patches from the splats whose support reaches them
+    (csrc/patches.cu); the assembled images equal the single-rank render."""
+    import torch.multiprocessing as mp
+
+    from paper_2512_20017_b200 import scenes
+    from paper_2512_20017_b200.trainer import AdamConfig, SplatTrainer
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, False, 2)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        item = q.get(timeout=600)
+        res[item[0]] = item
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ds, g, params, gt = _setup()
+    lr = scenes.lr_table(50.0)
+    tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt, adam=AdamConfig(lr))
+    losses = tr.step(BATCH).cpu().numpy()
+    img_ref = tr.last["image"][: len(BATCH) * 96 * 160 * 3].cpu().numpy().reshape(len(BATCH), 96, 160, 3)
+    after_ref = tr.params.cpu().numpy()
+    A, W = res[0][6], res[0][7]
+    assert A.shape == (len(BATCH) * 4, 2) and np.array_equal(W, res[1][7])
+    assert np.bincount(W, minlength=2).tolist() == [8, 8]
+    # per view: assemble the patches from their renderers
+    P, Wimg, Himg = 2, 160, 96
+    xs = [(c * Wimg) // P for c in range(P + 1)]
+    ys = [(r * Himg) // P for r in range(P + 1)]
+    loss_sum = np.zeros(len(BATCH))
+    for k, v in enumerate(BATCH):
+        img = np.full((Himg, Wimg, 3), np.nan, dtype=np.float32)
+        for j in range(P * P):
+            r_, c_ = divmod(j, P)
+            owner = int(W[k * P * P + j])
+            slot = res[owner][3].index(v)
+            img[ys[r_]:ys[r_ + 1], xs[c_]:xs[c_ + 1]] = res[owner][4][slot][ys[r_]:ys[r_ + 1], xs[c_]:xs[c_ + 1]]
+        assert np.abs(img - img_ref[k]).max() <= 1e-6, f"view {v}"
+        for r in (0, 1):
+            if v in res[r][3]:
+                loss_sum[k] += res[r][5][res[r][3].index(v)]
+    np.testing.assert_allclose(loss_sum, losses, rtol=0, atol=1e-6)  # patch losses add up to the view's
+    for r in (0, 1):
+        pts, after = res[r][1], res[r][2]
+        ref = after_ref[:, pts, :]
+        lr_full = np.broadcast_to(lr.reshape(15, 1, 4), ref.shape)
+        diff = np.abs(after - ref)
+        assert (diff <= 1e-3 * lr_full + 1e-7).mean() > 0.999
+        assert (diff <= 2.0 * lr_full + 1e-6).all()
