@@ -231,7 +231,7 @@ __device__ __forceinline__ bool all_done(const PixelFwd (&p)[PPL]) {
   return d;
 }
 
-template <int PPL>
+template <int PPL, bool kPatches>
 __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
     RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
     float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
@@ -249,7 +249,9 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
   PixelFwd p[PPL];
 #pragma unroll
   for (int k = 0; k < PPL; ++k)
-    p[k] = PixelFwd{f2(0.f, 0.f), 1.f, 0.f, 0, !slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, q.px, q.py0 + k)};
+    p[k] = PixelFwd{f2(0.f, 0.f), 1.f, 0.f, 0,
+                    !(kPatches ? slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, q.px, q.py0 + k)
+                               : (q.px < a.W && q.py0 + k < a.H))};
   Splat f;
   fetch_splat(f, sp, inst_rows, rg.x + lane, rg.x + lane < rg.y);
   uint32_t row_next = fetch_row(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
@@ -277,7 +279,9 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
   float l = 0.f;
 #pragma unroll
   for (int k = 0; k < PPL; ++k) {
-    if (!slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, q.px, q.py0 + k)) continue;
+    if (!(kPatches ? slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, q.px, q.py0 + k)
+                   : (q.px < a.W && q.py0 + k < a.H)))
+      continue;
     const int64_t pix = ((int64_t)slot * a.H + q.py0 + k) * a.W + q.px;
     const float2 c01 = unf2(p[k].c01);
     const float o0 = c01.x + p[k].T * a.bg[0], o1 = c01.y + p[k].T * a.bg[1], o2 = p[k].c2 + p[k].T * a.bg[2];
@@ -606,14 +610,17 @@ extern "C" int32_t bs_raster_fwd(const bs_raster_desc* d, const float* sp_rows, 
   if (st) return st;
   BS_REQUIRE(!a.loss_fused || (gt && loss_tiles), BS_ERR_PARAMETER, "fused loss needs gt and loss_tiles");
   const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
+  auto launch = [&](auto kern, int threads) {
+    kern<<<grid, threads, 0, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image,
+                                                  final_T, n_contrib, gt, gt_slot_view, loss_tiles);
+  };
+  const bool patches = a.slot_patches != nullptr;
   if (d->pixels_per_lane == 1)
-    raster_fwd_kernel<1><<<grid, Region<1>::kThreads, 0, as_stream(stream)>>>(
-        a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image, final_T, n_contrib, gt, gt_slot_view,
-        loss_tiles);
+    patches ? launch(raster_fwd_kernel<1, true>, Region<1>::kThreads)
+            : launch(raster_fwd_kernel<1, false>, Region<1>::kThreads);
   else
-    raster_fwd_kernel<2><<<grid, Region<2>::kThreads, 0, as_stream(stream)>>>(
-        a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image, final_T, n_contrib, gt, gt_slot_view,
-        loss_tiles);
+    patches ? launch(raster_fwd_kernel<2, true>, Region<2>::kThreads)
+            : launch(raster_fwd_kernel<2, false>, Region<2>::kThreads);
   BS_LAUNCH_CHECK("raster_fwd_kernel");
   return BS_OK;
 }
