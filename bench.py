@@ -181,7 +181,7 @@ def shard_for_rank(ds, g, params, world, rank):
     return np.ascontiguousarray(params[:, pts, :]), gb, aabb, info
 
 
-def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps, row_bytes=48, grad_bytes=36):
+def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps, row_bytes=48, grad_bytes=36, P=1):
     """All-to-all bytes per step: moved by NCCL (summed over ranks),
     A-predicted (account_iteration on topology (N, 1)), and the same
     accounting for the RandomStrategy baseline on the same batches."""
@@ -202,13 +202,14 @@ def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps, row_byt
                                np.random.default_rng(np.random.SeedSequence([5, 17])))[g.permutation]
     rnd = []
     for it, b in enumerate(batches):
-        A = build_access_matrix(g, rnd_pg, [ds.views[v] for v in b], 1)
-        sol = random_placement(len(b), world, np.random.default_rng(np.random.SeedSequence([5, 3, it])))
+        A = build_access_matrix(g, rnd_pg, [ds.views[v] for v in b], P)
+        sol = random_placement(len(b) * P * P, world, np.random.default_rng(np.random.SeedSequence([5, 3, it])))
         rnd.append(account_iteration(A, sol, topo, row_bytes).send_inter.sum() * row_bytes)
     rnd = float(np.mean(rnd))
     return {"fwd_bytes_per_step": fwd, "bwd_bytes_per_step": bwd, "fwd_bytes_predicted": float(pred),
             "random_fwd_bytes_per_step": rnd, "reduction_vs_random_pct": 100.0 * (1.0 - fwd / rnd) if rnd else None,
-            "row_bytes": {"fwd": row_bytes, "bwd": grad_bytes}}
+            "row_bytes": {"fwd": row_bytes, "bwd": grad_bytes}, "patches_per_side": P,
+            "note": "moved = render sets (P > 1 adds splats crossing patch borders); predicted/random = access matrix"}
 
 
 _STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_kernel",
@@ -298,8 +299,9 @@ def run_ours(args, cfg):
     setup_s = time.time() - t0
     W, H = cfg["image_size"]
     model = cfg.get("model", "3dgs")
+    P = args.patches or cfg.get("P", 1)
     tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt, adam=AdamConfig(scenes.lr_table(cfg["altitude"])),
-                      comm=comm, model=model, gt_view_ids=gt_ids)
+                      comm=comm, model=model, gt_view_ids=gt_ids, patches=P)
     # clocks are sampled from the start of the warm-up to the end of the timed
     # region (nvidia-smi needs ~0.5 s to start streaming)
     clk = ClockSampler(local).__enter__()
@@ -351,7 +353,7 @@ def run_ours(args, cfg):
                      "step_wait_ms": round(float(np.mean(comm.wait_ms)), 3) if comm.wait_ms else None}
         comm_report = comm_bytes_report(comm, step_AW, sched[args.warmup:args.warmup + args.steps], ds, g,
                                         world, rank, args.steps, row_bytes=4 * tr.sp_floats,
-                                        grad_bytes=4 * tr.gsp_wire_floats)
+                                        grad_bytes=4 * tr.gsp_wire_floats, P=P)
     # ---- e2e: public API with pinned host ground truth, loss read back
     # the step's ground-truth images are copied from pinned host memory on a
     # side stream, double-buffered: step i+1's upload overlaps step i
@@ -427,7 +429,7 @@ def run_ours(args, cfg):
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["desc"], "primitive": model, "n_points": cfg["n_points"],
                        "image": list(cfg["image_size"]), "global_batch": B, "views": cfg["n_views"], "group_size": cfg["G"],
-                       "parallelism": f"points+images x{world}",
+                       "parallelism": f"points+images x{world}", "patches_per_side": P,
                        "l2": "inputs larger than L2 (params+Adam state %.0f MB/rank)" % (3 * tr.params.numel() * 4 / 1e6)},
             "e2e": {"value": round(e2e_value, 3), "unit": "images/s", "h2d_bytes_per_step": B * H * W * 3 * world,
                     "d2h_bytes_per_step": 4 * B},
@@ -523,6 +525,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--patches", type=int, default=0, help="patches per image side P (default: the config's, 1)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

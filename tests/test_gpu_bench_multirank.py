@@ -13,16 +13,19 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_bench_two_ranks_gloo(cuda):
+@pytest.mark.parametrize("patches", [1, 2])
+def test_bench_two_ranks_gloo(cuda, patches):
     env = dict(os.environ, BS_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29611", os.path.join(ROOT, "bench.py"), "--gpus", "2",
-           "--steps", "3", "--warmup", "3", "--config", "c1"]
+           "--master-addr=127.0.0.1", f"--master-port={29611 + patches}", os.path.join(ROOT, "bench.py"), "--gpus",
+           "2", "--steps", "3", "--warmup", "3", "--config", "c1", "--patches", str(patches)]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["global_batch"] == 2
-    assert d["placement"]["async"] and d["placement"]["step_wait_ms"] is not None
+    assert d["config"]["patches_per_side"] == patches
+    if patches == 1:  # the prefetched placement is used at P = 1
+        assert d["placement"]["async"] and d["placement"]["step_wait_ms"] is not None
     assert d["comm"]["fwd_bytes_per_step"] >= 0 and d["comm"]["random_fwd_bytes_per_step"] > 0
