@@ -312,6 +312,22 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const bool ok = i < end;
+    // Prefetches that cost no registers: the block's parameter and moment
+    // planes into L2 by the bulk-copy engine (one contiguous request per
+    // (array, plane)) for the Adam update, and this point's SH planes into
+    // L1 for the per-view math that reads them on use.
+    if (threadIdx.x < 3 * BS_PARAM_PLANES) {
+      const int arr = threadIdx.x / BS_PARAM_PLANES, pl = threadIdx.x % BS_PARAM_PLANES;
+      const float4* base4 = arr == 0 ? params : (arr == 1 ? m : v);
+      const uint32_t bytes = 16u * (uint32_t)min(kProjThreads, end - b0);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base4 + (int64_t)pl * a.S + b0), "r"(bytes)
+                   : "memory");
+    }
+    if (ok) {
+#pragma unroll
+      for (int k = 3; k < BS_PARAM_PLANES; ++k)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(params + (int64_t)k * a.S + i));
+    }
     const uint32_t mask = ok ? a.mask[i] : 0u;
     rk.round(mask, B);
     if (ok && !(c.selective && mask == 0u)) {
