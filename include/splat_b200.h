@@ -267,7 +267,11 @@ int32_t bs_bin_tiles_scatter(const float* sp_rows, int64_t n_rows,
                              const int64_t* seg_row0, const int32_t* seg_slot,
                              int32_t n_segs, const bs_camera* slot_cams,
                              int32_t tiles_per_slot, int32_t* cursor,
-                             uint64_t* inst_keys, int32_t model, void* stream);
+                             uint64_t* inst_keys, int64_t capacity,
+                             int32_t model, void* stream);
+/* (keys at positions >= capacity are dropped, so the key buffer can be
+ * sized before the instance count reaches the host; re-run offsets + scatter
+ * with a larger buffer when the count exceeds it) */
 int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* ranges,
                           int32_t n_buckets, int32_t smem_cap,
                           uint32_t* inst_rows, void* stream);

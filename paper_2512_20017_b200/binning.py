@@ -14,13 +14,14 @@ from . import _native as nat
 
 
 def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, model_id=nat.MODEL_3DGS,
-                sort_cap=4096, before_sync=None):
+                sort_cap=4096, before_sync=None, capacity_hint=None):
     """Atomics into (slot, tile) buckets, then a shared-memory sort of every
     bucket by (depth, row); buckets larger than the in-SM sort go through the
     device radix sort.  `buf` is a grow-only buffer cache with
     get(name, n, dtype).  `before_sync` (optional) queues independent GPU work
     ahead of the host read of the instance count, which it then overlaps.
-    Returns (n_inst, inst_rows, ranges, largest bucket)."""
+    `capacity_hint` overrides the initial key-buffer size (tests of the
+    overflow path).  Returns (n_inst, inst_rows, ranges, largest bucket)."""
     st, lib = nat.stream_handle(), nat.load()
     nb = n_slots * tiles
     counts = buf.get("bucket_counts", nb, torch.int32)
@@ -30,15 +31,41 @@ def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, 
     cursor = buf.get("cursor", nb, torch.int32)
     stats = buf.get("bin_stats", 2, torch.int64)
     ows = buf.get("offsets_ws", lib.bs_bin_tiles_offsets_workspace(nb), torch.uint8)
-    nat.call("bs_bin_tiles_offsets", nat.ptr(counts), nb, nat.ptr(ranges), nat.ptr(cursor), nat.ptr(stats),
-             nat.ptr(ows), ows.numel(), st)
+
+    def offsets():
+        nat.call("bs_bin_tiles_offsets", nat.ptr(counts), nb, nat.ptr(ranges), nat.ptr(cursor), nat.ptr(stats),
+                 nat.ptr(ows), ows.numel(), st)
+
+    offsets()
+    # the instance count travels to the host while the GPU scatters into a
+    # buffer sized from earlier steps (no idle gap at this read); on overflow
+    # the offsets and the scatter run again with a larger buffer
+    pin = getattr(buf, "bin_stats_pin", None)
+    if pin is None:
+        pin = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        buf.bin_stats_pin = pin
+    pin.copy_(stats, non_blocking=True)
+    ready = torch.cuda.Event()
+    ready.record()
     if before_sync is not None:
         before_sync()
-    n_inst, biggest = (int(x) for x in stats.cpu().tolist())  # sizes the instance buffers
-    keys = buf.get("inst_keys", max(n_inst, 1), torch.int64)
+    inst_cap = max(getattr(buf, "inst_cap", 0), 4 * n_rows, 1024) if capacity_hint is None else capacity_hint
+
+    def scatter(capacity):
+        k = buf.get("inst_keys", capacity, torch.int64)
+        nat.call("bs_bin_tiles_scatter", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
+                 nat.ptr(slot_cams), tiles, nat.ptr(cursor), nat.ptr(k), k.numel(), model_id, st)
+        return k
+
+    keys = scatter(inst_cap)
+    ready.synchronize()
+    n_inst, biggest = (int(x) for x in pin.tolist())  # sizes the instance buffers
+    if n_inst > keys.numel():
+        inst_cap = int(n_inst * 1.25) + 1024
+        offsets()
+        keys = scatter(inst_cap)
+    buf.inst_cap = max(getattr(buf, "inst_cap", 0), int(n_inst * 1.25) + 1024)
     irows = buf.get("irows", max(n_inst, 1), torch.int32)
-    nat.call("bs_bin_tiles_scatter", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
-             nat.ptr(slot_cams), tiles, nat.ptr(cursor), nat.ptr(keys), model_id, st)
     cap = min(sort_cap, lib.bs_bin_tiles_max_sort())
     nat.call("bs_bin_tiles_sort", nat.ptr(keys), nat.ptr(ranges), nb, cap, nat.ptr(irows), st)
     if biggest > cap:  # rare: buckets beyond the shared-memory sort

@@ -169,7 +169,10 @@ __global__ void __launch_bounds__(kScanBlock) bucket_ranges_kernel(const int32_t
   }
 }
 
-__global__ void scatter_tiles_kernel(BinGeom g, int32_t* __restrict__ cursor, uint64_t* __restrict__ keys) {
+// Positions at or beyond `capacity` are dropped: the caller sizes the key
+// buffer before it has read the instance count and re-runs on overflow.
+__global__ void scatter_tiles_kernel(BinGeom g, int32_t* __restrict__ cursor, uint64_t* __restrict__ keys,
+                                     int64_t capacity) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -187,7 +190,8 @@ __global__ void scatter_tiles_kernel(BinGeom g, int32_t* __restrict__ cursor, ui
       int pos = 0;
       if (b >= 0 && lane == leader) pos = atomicAdd(cursor + b, __popc(peers));
       pos = __shfl_sync(0xffffffffu, pos, leader);
-      if (b >= 0) keys[pos + __popc(peers & lt)] = key;
+      const int64_t at = (int64_t)pos + __popc(peers & lt);
+      if (b >= 0 && at < capacity) keys[at] = key;
     }
   }
 }
@@ -376,11 +380,11 @@ extern "C" int32_t bs_bin_tiles_offsets(const int32_t* bucket_counts, int32_t n_
 extern "C" int32_t bs_bin_tiles_scatter(const float* sp_rows, int64_t n_rows, const int64_t* seg_row0,
                                         const int32_t* seg_slot, int32_t n_segs, const bs_camera* slot_cams,
                                         int32_t tiles_per_slot, int32_t* cursor, uint64_t* inst_keys,
-                                        int32_t model, void* stream) {
+                                        int64_t capacity, int32_t model, void* stream) {
   BS_REQUIRE(n_segs >= 1, BS_ERR_PARAMETER, "bin: need at least one segment");
   if (n_rows == 0) return BS_OK;
   BinGeom g{sp_rows, n_rows, seg_row0, seg_slot, n_segs, slot_cams, tiles_per_slot, sp_layout(model)};
-  scatter_tiles_kernel<<<grid_for(n_rows, 256), 256, 0, as_stream(stream)>>>(g, cursor, inst_keys);
+  scatter_tiles_kernel<<<grid_for(n_rows, 256), 256, 0, as_stream(stream)>>>(g, cursor, inst_keys, capacity);
   BS_LAUNCH_CHECK("scatter_tiles_kernel");
   return BS_OK;
 }

@@ -173,6 +173,7 @@ class SplatTrainer:
         self.last = {}
         self.binning = "bucket"  # or "radix" (identical lists, see csrc/bin_tiles.cu)
         self.sort_cap = 4096     # bucket sizes sorted in shared memory
+        self.bin_capacity_hint = None  # initial instance-key buffer (tests of the overflow re-run)
         # raster work split: pixels per lane (1 -> 8x4 region per warp, 2 -> 8x8);
         # 1 measured faster on B200 (C2: bwd 3.30 vs 3.52 ms, fwd 1.22 vs 1.24 ms)
         self.pixels_per_lane = int(os.environ.get("BS_RASTER_PPL", "1"))
@@ -464,7 +465,8 @@ class SplatTrainer:
     def _bin_buckets(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, before_sync=None):
         """Bucket pipeline (csrc/bin_tiles.cu), see binning.bin_buckets."""
         n_inst, irows, ranges, biggest = bin_buckets(self.buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams,
-                                                     self.tiles, self.model_id, self.sort_cap, before_sync)
+                                                     self.tiles, self.model_id, self.sort_cap, before_sync,
+                                                     self.bin_capacity_hint)
         self.last["largest_bucket"] = biggest
         return n_inst, irows, ranges
 

@@ -380,12 +380,14 @@ def test_training_sim_report_matches_reference(golden, cuda):
 
 
 def test_binning_pipelines_agree_and_large_bucket_fallback(c1, cuda):
-    """Bucket pipeline (default), radix pipeline and the large-bucket
-    fallback (tiny shared-memory capacity) give identical per-tile lists."""
+    """Bucket pipeline (default), radix pipeline, the large-bucket fallback
+    (tiny shared-memory capacity) and the key-buffer overflow re-run give
+    identical per-tile lists."""
     outs = []
-    for mode, cap in (("bucket", 4096), ("radix", 4096), ("bucket", 8)):
+    for mode, cap, hint in (("bucket", 4096, None), ("radix", 4096, None), ("bucket", 8, None), ("bucket", 4096, 16)):
         tr = _trainer(c1)
         tr.binning, tr.sort_cap = mode, cap
+        tr.bin_capacity_hint = hint  # 16: the key buffer overflows, offsets + scatter re-run
         tr.step([0, 3, 5])
         torch.cuda.synchronize()
         n = tr.last["n_inst"]
