@@ -261,18 +261,22 @@ class SplatTrainer:
         patch_counts = self.buf.get("patch_counts", B * self.P * self.P, torch.int64) if patched else None
         with self._t("cull"):
             self._cull_counts(batch_ids, mask, counts, base, view_rows, view_row0, st, bidx, patch_counts)
-        if patched:
-            return self._step_patches(batch_ids, gt_batch, bidx, cams, mask, base, view_rows, view_row0,
-                                      patch_counts, st)
-        if self.comm is not None and next_batch is not None and self.P == 1:
-            # counts of the next batch on the pre-update positions -> async W
+        if self.comm is not None and next_batch is not None:
+            # counts of the next batch (per view, or per patch when P > 1) on
+            # the pre-update positions -> its W on a host thread (exchange.py)
             Bn = len(next_batch)
             nb = self.buf
+            pc_next = nb.get("patch_counts_next", Bn * self.P * self.P, torch.int64) if patched else None
             self._cull_counts(next_batch, nb.get("mask_next", S, torch.int32),
                               nb.get("counts_next", self.n_groups * Bn, torch.int32),
                               nb.get("base_next", self.n_groups * Bn, torch.int32),
-                              nb.get("view_rows_next", Bn, torch.int64), nb.get("view_row0_next", Bn, torch.int64), st)
-            self.comm.prefetch(nb.get("view_rows_next", Bn, torch.int64), tuple(int(v) for v in next_batch))
+                              nb.get("view_rows_next", Bn, torch.int64), nb.get("view_row0_next", Bn, torch.int64), st,
+                              patch_counts=pc_next)
+            self.comm.prefetch(pc_next if patched else nb.get("view_rows_next", Bn, torch.int64),
+                               tuple(int(v) for v in next_batch))
+        if patched:
+            return self._step_patches(batch_ids, gt_batch, bidx, cams, mask, base, view_rows, view_row0,
+                                      patch_counts, st)
         lay = None
         pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group)
         early = self.comm is None and S * B * self.sp_floats * 4 <= self.sp_capacity_bytes
@@ -372,7 +376,7 @@ class SplatTrainer:
         dev, S = self.dev, self.S
         with self._t("assign"):
             A = comm.gather_access(patch_counts)       # int64 [B P^2, N]
-            W = comm.assign(A)                          # patch -> rank
+            W = comm.assign(A, key=tuple(int(v) for v in batch_ids))  # patch -> rank (prefetched when given)
         rows_host = view_rows.cpu().numpy()
         n_rows = int(rows_host.sum())
         self.last.update(A=A, W=W, rows_per_view=rows_host.copy())

@@ -26,6 +26,5 @@ def test_bench_two_ranks_gloo(cuda, patches):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["global_batch"] == 2
     assert d["config"]["patches_per_side"] == patches
-    if patches == 1:  # the prefetched placement is used at P = 1
-        assert d["placement"]["async"] and d["placement"]["step_wait_ms"] is not None
+    assert d["placement"]["async"] and d["placement"]["step_wait_ms"] is not None  # prefetched W used
     assert d["comm"]["fwd_bytes_per_step"] >= 0 and d["comm"]["random_fwd_bytes_per_step"] > 0
