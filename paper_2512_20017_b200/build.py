@@ -26,7 +26,7 @@ NVCC_FLAGS = ARCH + [
     "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
 ]
 SOURCES = ["abi.cu", "cull.cu", "sort.cu", "project.cu", "bin.cu", "bin_tiles.cu", "raster.cu", "raster2d.cu", "patches.cu"]
-HEADERS = ["common.cuh", "splat_math.cuh", "splat2d_math.cuh", "tile.cuh"]
+HEADERS = ["common.cuh", "splat_math.cuh", "splat2d_math.cuh", "tile.cuh", "packed.cuh"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -29,6 +29,7 @@
 // into the 16-byte aligned G_SP row); otherwise the warp reduce-scatters the
 // 9 sums in 12 shuffles and 9 lanes issue one RED each.
 #include "common.cuh"
+#include "packed.cuh"
 
 namespace bs {
 namespace {
@@ -75,37 +76,7 @@ __device__ __forceinline__ bool slot_pixel(const uint64_t* slot_patches, int P, 
 }
 
 
-// Packed FP32 pairs (sm_100 FADD2 / FMUL2 / FFMA2: one issue slot for two
-// lanes' worth of FP32 work; a scalar operand is broadcast for free).
-struct F2 {
-  unsigned long long v;
-};
-__device__ __forceinline__ F2 f2(float a, float b) {
-  F2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float2 unf2(F2 x) {
-  float2 r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(x.v));
-  return r;
-}
-__device__ __forceinline__ F2 add2(F2 a, F2 b) {
-  F2 r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-  return r;
-}
-__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
-  F2 r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-  return r;
-}
-__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
-  F2 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-  return r;
-}
-__device__ __forceinline__ F2 bcast(float s) { return f2(s, s); }
+// packed FP32 pairs: csrc/packed.cuh
 
 // log2(e) * power at a pixel from the pre-scaled conic:
 // uv = (u, v), k = (kA, kC), kb: kA = -log2(e) A / 2, kC = -log2(e) C / 2,

@@ -20,6 +20,7 @@
 // shuffles and one RED per term is issued per (region, splat).  exp is one
 // ex2.approx in both kernels (identical skip / stop decisions).
 #include "splat2d_math.cuh"
+#include "packed.cuh"
 
 namespace bs {
 namespace {
@@ -139,8 +140,9 @@ __device__ __forceinline__ bool reaches2(const Splat2& f, float x0, float x1, fl
 // origin (X, Y) (the per-pixel formula evaluated once, z0 = hx0 x hy0) and
 // the increments zb = hy0 x r2, zc = r2 x hx0 of the origin-shifted rows, so
 // a pixel needs zeta = z0 + zb ox + zc oy with small exact integer offsets.
-// staged: a = (u, v, opac, z0.x), b = (z0.y, z0.z, zb.x, zb.y),
-//         c = (zb.z, zc.x, zc.y, zc.z), d = (r, g, b, -)
+// staged (x/y components in aligned register pairs for packed FP32):
+//   a = (u, v, opac, z0.z), b = (z0.x, z0.y, zb.x, zb.y),
+//   c = (zc.x, zc.y, zb.z, zc.z), d = (r, g, b, -)
 __device__ __forceinline__ void cross3(const float a[3], const float b[3], float o[3]) {
   o[0] = __fsub_rn(__fmul_rn(a[1], b[2]), __fmul_rn(a[2], b[1]));
   o[1] = __fsub_rn(__fmul_rn(a[2], b[0]), __fmul_rn(a[0], b[2]));
@@ -161,9 +163,9 @@ __device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f, floa
   cross3(hx, hy, z0);
   cross3(hy, r2, zb);
   cross3(r2, hx, zc);
-  s.a[lane] = make_float4(f.p[0].x, f.p[0].y, f.p[0].z, z0[0]);
-  s.b[lane] = make_float4(z0[1], z0[2], zb[0], zb[1]);
-  s.c[lane] = make_float4(zb[2], zc[0], zc[1], zc[2]);
+  s.a[lane] = make_float4(f.p[0].x, f.p[0].y, f.p[0].z, z0[2]);
+  s.b[lane] = make_float4(z0[0], z0[1], zb[0], zb[1]);
+  s.c[lane] = make_float4(zc[0], zc[1], zb[2], zc[2]);
   s.d[lane] = f.p[3];  // (r, g, b, depth)
   s.row[lane] = f.row;
 }
@@ -177,17 +179,21 @@ struct Eval2 {
 // (ox, oy): the pixel's offset from the region origin (small integers).
 __device__ __forceinline__ void eval2(const float4& a, const float4& b, const float4& c, float px, float py,
                                       float ox, float oy, Eval2& e) {
-  e.z[0] = __fmaf_rn(c.y, oy, __fmaf_rn(b.z, ox, a.w));
-  e.z[1] = __fmaf_rn(c.z, oy, __fmaf_rn(b.w, ox, b.x));
-  e.z[2] = __fmaf_rn(c.w, oy, __fmaf_rn(c.x, ox, b.y));
+  // (z.x, z.y) as a packed pair; each lane is the same FMA chain as z.z
+  const float2 zxy = unf2(fma2(f2(c.x, c.y), bcast(oy), fma2(f2(b.z, b.w), bcast(ox), f2(b.x, b.y))));
+  e.z[0] = zxy.x;
+  e.z[1] = zxy.y;
+  e.z[2] = __fmaf_rn(c.w, oy, __fmaf_rn(c.z, ox, a.w));
   e.ok = e.z[2] != 0.f;
   if (!e.ok) return;
   e.iz = rcpa(e.z[2]);  // one approximate reciprocal (both kernels evaluate it identically)
-  e.u = __fmul_rn(e.z[0], e.iz);
-  e.v = __fmul_rn(e.z[1], e.iz);
+  const float2 uv = unf2(mul2(f2(e.z[0], e.z[1]), bcast(e.iz)));
+  e.u = uv.x;
+  e.v = uv.y;
   e.g3 = __fmaf_rn(e.u, e.u, __fmul_rn(e.v, e.v));
-  e.dx = __fsub_rn(a.x, px);
-  e.dy = __fsub_rn(a.y, py);
+  const float2 dd = unf2(add2(f2(a.x, a.y), f2(-px, -py)));
+  e.dx = dd.x;
+  e.dy = dd.y;
   e.g2 = __fmul_rn(2.f, __fmaf_rn(e.dx, e.dx, __fmul_rn(e.dy, e.dy)));
   e.power = __fmul_rn(-0.5f, fminf(e.g3, e.g2));
 }
@@ -414,17 +420,22 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
                 // power = -0.5 (u^2 + v^2), (u, v) = zeta.xy / zeta.z; G_SP2
                 // carries the moments sum gz, sum gz px, sum gz py of
                 // dL/dzeta (the projection backward applies the M rows)
-                const float gu = -e.u * dpow, gv = -e.v * dpow;
+                const F2 guv = mul2(f2(e.u, e.v), bcast(-dpow));  // dL/d(u, v)
+                const float2 g_uv = unf2(guv);
                 const float iz = e.iz;
-                const float gz0 = gu * iz, gz1 = gv * iz, gz2 = -(gu * e.u + gv * e.v) * iz;
-                g[2] = gz0;
-                g[3] = gz1;
+                const F2 gz01 = mul2(guv, bcast(iz));
+                const float gz2 = -(g_uv.x * e.u + g_uv.y * e.v) * iz;
+                const float2 z01 = unf2(gz01);
+                const float2 zx = unf2(mul2(gz01, bcast(pxf)));
+                const float2 zy = unf2(mul2(gz01, bcast(pyf)));
+                g[2] = z01.x;
+                g[3] = z01.y;
                 g[4] = gz2;
-                g[5] = gz0 * pxf;
-                g[6] = gz1 * pxf;
+                g[5] = zx.x;
+                g[6] = zx.y;
                 g[7] = gz2 * pxf;
-                g[8] = gz0 * pyf;
-                g[9] = gz1 * pyf;
+                g[8] = zy.x;
+                g[9] = zy.y;
                 g[10] = gz2 * pyf;
               } else {
                 // power = -(dx^2 + dy^2), dx = u - px
