@@ -188,7 +188,9 @@ enum { BS_MODEL_3DGS = 0, BS_MODEL_2DGS = 1 };
 /* 2DGS splat-state row (BS_SP2_FLOATS = 24 floats, 96 B): the 20 elements of
  * PAPER.md Table tab:states-2dgs -- 0 u 1 v 2 opacity 3..11 ray transform M
  * (row-major KWH) 12..14 rgb 15 depth 16 radius_x 17 radius_y 18..20 normal
- * -- + 3 pad.  G_SP row: 16 floats (64-byte aligned for 128-bit REDs):
+ * -- + 21 pad, 22..23 centre of the support box whose half-widths are
+ * radius_x/y (the image of the disk u^2 + v^2 <= k united with the low-pass
+ * circle, k = min(9, 2 ln(255 o)); 0 = never contributes).  G_SP row: 16 floats (64-byte aligned for 128-bit REDs):
  * d u, d v, then the moments Ga = sum dL/dzeta, Gb = sum px dL/dzeta,
  * Gc = sum py dL/dzeta of the per-pixel zeta = r0 x r1 + px (r1 x r2) +
  * py (r2 x r0) (r_i rows of M), d opacity, d rgb, pad.  The projection

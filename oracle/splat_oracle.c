@@ -540,9 +540,10 @@ static int inst_cmp(const void* pa, const void* pb) {
   return a->row < b->row ? -1 : (a->row > b->row);
 }
 
-/* tiles whose span meets [u - r, u + r] (same f32 ops as csrc/bin.cu) */
-static int tile_rect_at(const float* row, int rad, int W, int H, int* x0, int* x1, int* y0, int* y1) {
-  const float u = row[0], v = row[1], rx = row[rad], ry = row[rad + 1];
+/* tiles whose span meets [u - r, u + r] of the support box centred at
+ * (row[ctr], row[ctr + 1]) (same f32 ops as csrc/tile.cuh) */
+static int tile_rect_at(const float* row, int rad, int ctr, int W, int H, int* x0, int* x1, int* y0, int* y1) {
+  const float u = row[ctr], v = row[ctr + 1], rx = row[rad], ry = row[rad + 1];
   if (!(rx > 0.f) || !(ry > 0.f)) return 0;
   const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
   *x0 = (int)fminf(fmaxf(floorf((u - rx) * 0.0625f), 0.f), (float)tx);
@@ -555,21 +556,21 @@ static int tile_rect_at(const float* row, int rad, int W, int H, int* x0, int* x
 
 /* row geometry: 3DGS rows {12 floats, radii at 10, depth at 9}, 2DGS {24, 16, 15} */
 typedef struct {
-  int stride, rad, depth;
+  int stride, rad, depth, ctr;
 } olayout;
-static const olayout LAY3 = {SPF, 10, 9};
-static const olayout LAY2 = {24, 16, 15};
+static const olayout LAY3 = {SPF, 10, 9, 0};
+static const olayout LAY2 = {24, 16, 15, 22};
 
 static oinst* bin_view_l(const float* sp, int64_t m, int W, int H, olayout L, int64_t* n_out, int32_t* ranges) {
   const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
   int64_t total = 0;
   int x0, x1, y0, y1;
-  for (int64_t k = 0; k < m; ++k) total += tile_rect_at(sp + k * L.stride, L.rad, W, H, &x0, &x1, &y0, &y1);
+  for (int64_t k = 0; k < m; ++k) total += tile_rect_at(sp + k * L.stride, L.rad, L.ctr, W, H, &x0, &x1, &y0, &y1);
   oinst* inst = (oinst*)malloc(sizeof(oinst) * (size_t)(total > 0 ? total : 1));
   int64_t o = 0;
   for (int64_t k = 0; k < m; ++k) {
     const float* r = sp + k * L.stride;
-    if (!tile_rect_at(r, L.rad, W, H, &x0, &x1, &y0, &y1)) continue;
+    if (!tile_rect_at(r, L.rad, L.ctr, W, H, &x0, &x1, &y0, &y1)) continue;
     fbits db;
     db.f = r[L.depth];
     for (int y = y0; y < y1; ++y)
@@ -762,7 +763,7 @@ double or_train_step(float* params, float* exp_avg, float* exp_avg_sq, int64_t S
 typedef struct {
   float d[3], qc[3], s[2], qn[4], qnorm, Rq[9], Rc[9];
   float c0[3], c1[3], c2[3];
-  float u, v, depth, radius_x, radius_y, normal[3];
+  float u, v, depth, radius_x, radius_y, box_cx, box_cy, normal[3];
   float len, dir[3], Y[16], col_raw[3], col[3], opac;
   int valid;
 } oproj2;
@@ -828,9 +829,30 @@ static void proj2_fwd(const opoint* pt, const or_camera* c, int n_sh, oproj2* f)
     const float bx = d02 / d22, by = d12 / d22;
     const float ex = bx * bx - d00 / d22, ey = by * by - d11 / d22;
     f->valid = ex >= 0.f && ey >= 0.f;
-    if (f->valid) {
-      f->radius_x = ceilf(fabsf(bx - f->u) + sqrtf(ex));
-      f->radius_y = ceilf(fabsf(by - f->v) + sqrtf(ey));
+  }
+  /* support box (csrc/splat2d_math.cuh): image of the disk u^2 + v^2 <= k
+   * united with the low-pass circle of radius sqrt(k / 2), k = min(9, 2 ln(255 o)) */
+  f->box_cx = f->u;
+  f->box_cy = f->v;
+  {
+    const float o = 1.f / (1.f + or_det_expf(-pt->op));
+    const float k = fminf(9.0f, 2.0f * or_det_logf(255.0f * o));
+    if (f->valid && k > 0.f) {
+      const float k22 = k * (a[2] * a[2] + b[2] * b[2]) - e[2] * e[2];
+      const float k02 = k * (a[0] * a[2] + b[0] * b[2]) - e[0] * e[2];
+      const float k12 = k * (a[1] * a[2] + b[1] * b[2]) - e[1] * e[2];
+      const float k00 = k * (a[0] * a[0] + b[0] * b[0]) - e[0] * e[0];
+      const float k11 = k * (a[1] * a[1] + b[1] * b[1]) - e[1] * e[1];
+      const float bx = k02 / k22, by = k12 / k22;
+      const float hx = sqrtf(fmaxf(bx * bx - k00 / k22, 0.f));
+      const float hy = sqrtf(fmaxf(by * by - k11 / k22, 0.f));
+      const float rc = sqrtf(0.5f * k);
+      const float x0 = fminf(bx - hx, f->u - rc), x1 = fmaxf(bx + hx, f->u + rc);
+      const float y0 = fminf(by - hy, f->v - rc), y1 = fmaxf(by + hy, f->v + rc);
+      f->box_cx = 0.5f * (x0 + x1);
+      f->box_cy = 0.5f * (y0 + y1);
+      f->radius_x = 0.5f * (x1 - x0);
+      f->radius_y = 0.5f * (y1 - y0);
     }
   }
   float n[3] = {f->Rc[2], f->Rc[5], f->Rc[8]};
@@ -871,7 +893,9 @@ void or_project2d(const float* params, int64_t S, const int64_t* idx, int64_t m,
     r[16] = f.valid ? f.radius_x : 0.f;
     r[17] = f.valid ? f.radius_y : 0.f;
     for (int k2 = 0; k2 < 3; ++k2) r[18 + k2] = f.normal[k2];
-    r[21] = r[22] = r[23] = 0.f;
+    r[21] = 0.f;
+    r[22] = f.box_cx;
+    r[23] = f.box_cy;
   }
 }
 
@@ -1095,7 +1119,7 @@ int32_t or_render2d(const float* sp, int64_t m, int32_t W, int32_t H, const floa
           const float* r = sp + (int64_t)inst[i].row * SP2F;
           oeval2 e;
           eval2_o(r, pxf, pyf, &e);
-          if (!e.ok || e.power > 0.f) continue;
+          if (!e.ok || e.power > 0.f || e.power < -4.5f) continue; /* outside the 3-sigma support */
           const float alpha = fminf(0.99f, r[2] * expf(e.power));
           if (alpha < 1.f / 255.f) continue;
           const float nT = T * (1.f - alpha);
@@ -1141,7 +1165,7 @@ int32_t or_render2d_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const 
           const float* r = sp + row * SP2F;
           oeval2 e;
           eval2_o(r, pxf, pyf, &e);
-          if (!e.ok || e.power > 0.f) continue;
+          if (!e.ok || e.power > 0.f || e.power < -4.5f) continue; /* outside the 3-sigma support */
           const float ex = expf(e.power);
           const float raw = r[2] * ex;
           const float alpha = fminf(0.99f, raw);

@@ -49,7 +49,7 @@ struct RowTiles {
     slot = g.seg_slot[segment_of(g.seg_row0, g.n_segs, r)];
     const int W = g.cams[slot].width, H = g.cams[slot].height;
     int y0;
-    if (!tile_rect_at(g.sp + r * g.lay.stride, g.lay.rad_off, W, H, x0, x1, y0, y1)) return;
+    if (!tile_rect_at(g.sp + r * g.lay.stride, g.lay.rad_off, g.lay.ctr_off, W, H, x0, x1, y0, y1)) return;
     tx = (W + BS_TILE - 1) / BS_TILE;
     x = x0;
     y = y0;

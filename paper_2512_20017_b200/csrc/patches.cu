@@ -24,7 +24,7 @@
 namespace bs {
 namespace {
 
-__global__ void row_dest_mask_kernel(const float* __restrict__ sp, int stride, int rad_off, int64_t n_rows,
+__global__ void row_dest_mask_kernel(const float* __restrict__ sp, int stride, int rad_off, int ctr_off, int64_t n_rows,
                                      const int64_t* __restrict__ view_row0, int B, int P, int W, int H,
                                      const int32_t* __restrict__ patch_owner, uint32_t* __restrict__ mask) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
@@ -33,7 +33,7 @@ __global__ void row_dest_mask_kernel(const float* __restrict__ sp, int stride, i
     for (int k = 1; k < B; ++k)
       if (view_row0[k] <= r) v = k;
     const float* row = sp + r * stride;
-    const float u = row[0], vv = row[1], hx = row[rad_off], hy = row[rad_off + 1];
+    const float u = row[ctr_off], vv = row[ctr_off + 1], hx = row[rad_off], hy = row[rad_off + 1];
     uint32_t m = 0u;
     if (hx > 0.f && hy > 0.f) {
       // pixel columns / rows whose centres the support box may reach (padded)
@@ -176,7 +176,7 @@ extern "C" int32_t bs_row_dest_mask(const float* sp_rows, int32_t model, int64_t
   if (n_rows == 0) return BS_OK;
   const SpLayout L = sp_layout(model);
   row_dest_mask_kernel<<<grid_for(n_rows, 256), 256, 0, as_stream(stream)>>>(
-      sp_rows, L.stride, L.rad_off, n_rows, view_row0, n_views, P, width, height, patch_owner, dest_mask);
+      sp_rows, L.stride, L.rad_off, L.ctr_off, n_rows, view_row0, n_views, P, width, height, patch_owner, dest_mask);
   BS_LAUNCH_CHECK("row_dest_mask_kernel");
   return BS_OK;
 }

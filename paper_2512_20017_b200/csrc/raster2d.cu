@@ -8,10 +8,9 @@
 //   h_x = M_row0 - x M_row2, h_y = M_row1 - y M_row2, zeta = h_x x h_y,
 //   (u, v) = zeta.xy / zeta.z,  g3 = u^2 + v^2,  g2 = 2 |mean2d - pixel|^2,
 //   alpha = min(0.99, opacity exp(-0.5 min(g3, g2))) -- same skip / stop
-// rules as 3DGS.  Footprint filter: alpha >= 1/255 needs min(g3, g2) <= L,
-// L = 2 ln(255 o): the union of the bounding box of the image of the disk
-// u^2 + v^2 <= L (dual conic; unbounded -> keep) and the circle
-// |mean2d - pixel| <= sqrt(L / 2), padded by 1%.
+// rules as 3DGS, and (as the 3DGS 3-sigma ellipse) pairs with
+// min(g3, g2) > 9 are skipped.  Footprint filter: the projection's support
+// box (see reaches2).
 // Per pixel zeta is affine in the pixel (staging computes it at the region
 // origin and its two increments), so the backward accumulates the moments of
 // dL/dzeta instead of dL/dM (include/splat_b200.h, 2DGS G_SP row).
@@ -74,7 +73,8 @@ struct Warp2 {
 };
 
 struct Splat2 {
-  float4 p[4];  // SP floats 0..15
+  float4 p[4];   // SP floats 0..15
+  float2 h, c;   // support box half-widths (16, 17) and centre (22, 23)
   uint32_t row;
   bool ok;
 };
@@ -86,6 +86,8 @@ __device__ __forceinline__ void fetch2_row(Splat2& f, const float* __restrict__ 
     const float4* r4 = reinterpret_cast<const float4*>(sp + (int64_t)row * kSP2);
 #pragma unroll
     for (int k = 0; k < 4; ++k) f.p[k] = __ldg(r4 + k);
+    f.h = __ldg(reinterpret_cast<const float2*>(sp + (int64_t)row * kSP2 + 16));
+    f.c = __ldg(reinterpret_cast<const float2*>(sp + (int64_t)row * kSP2 + 22));
   }
 }
 
@@ -107,32 +109,14 @@ __device__ __forceinline__ void m_rows(const float4& a, const float4& b, const f
   r2[0] = c.y; r2[1] = c.z; r2[2] = c.w;
 }
 
+// Can the splat's support box (written by the projection: the union of the
+// image of the disk u^2 + v^2 <= k and the low-pass circle, k = min(9,
+// 2 ln(255 o)); half-widths 0 = never contributes) reach a pixel centre of
+// [x0,x1] x [y0,y1]?  Padded like the 3DGS test.
 __device__ __forceinline__ bool reaches2(const Splat2& f, float x0, float x1, float y0, float y1) {
-  if (!f.ok) return false;
-  const float4 a = make_float4(f.p[0].x, f.p[0].y, f.p[0].z, f.p[0].w);
-  const float4 b = f.p[1], c = f.p[2];
-  const float o = a.z;
-  const float L = 2.f * __logf(255.f * o);
-  if (!(L > 0.f)) return false;
-  // low-pass circle around mean2d
-  const float rc = __fsqrt_rz(0.5f * L) * 1.01f + 1e-3f;
-  const float ecx = fabsf(a.x - fminf(fmaxf(a.x, x0), x1)), ecy = fabsf(a.y - fminf(fmaxf(a.y, y0), y1));
-  if (ecx <= rc && ecy <= rc) return true;
-  // image of the disk u^2 + v^2 <= L
-  float r0[3], r1[3], r2[3];
-  m_rows(a, b, c, r0, r1, r2);
-  // columns: c0 = (r0[0], r1[0], r2[0]), c1 = (r0[1], r1[1], r2[1]), c2 = (r0[2], r1[2], r2[2])
-  const float C22 = L * (r2[0] * r2[0] + r2[1] * r2[1]) - r2[2] * r2[2];
-  if (!(C22 < 0.f)) return true;  // unbounded image: keep (conservative)
-  const float C02 = L * (r0[0] * r2[0] + r0[1] * r2[1]) - r0[2] * r2[2];
-  const float C12 = L * (r1[0] * r2[0] + r1[1] * r2[1]) - r1[2] * r2[2];
-  const float C00 = L * (r0[0] * r0[0] + r0[1] * r0[1]) - r0[2] * r0[2];
-  const float C11 = L * (r1[0] * r1[0] + r1[1] * r1[1]) - r1[2] * r1[2];
-  const float i22 = rcpa(C22);  // approximate: absorbed by the 1% padding
-  const float bx = C02 * i22, by = C12 * i22;
-  const float hx = __fsqrt_rz(fmaxf(bx * bx - C00 * i22, 0.f)) * 1.01f + 1e-3f;
-  const float hy = __fsqrt_rz(fmaxf(by * by - C11 * i22, 0.f)) * 1.01f + 1e-3f;
-  return fabsf(bx - fminf(fmaxf(bx, x0), x1)) <= hx && fabsf(by - fminf(fmaxf(by, y0), y1)) <= hy;
+  if (!f.ok || !(f.h.x > 0.f)) return false;
+  return fabsf(f.c.x - fminf(fmaxf(f.c.x, x0), x1)) <= fmaf(f.h.x, 1.0001f, 1e-3f) &&
+         fabsf(f.c.y - fminf(fmaxf(f.c.y, y0), y1)) <= fmaf(f.h.y, 1.0001f, 1e-3f);
 }
 
 // Staging: zeta = h_x x h_y is affine in the pixel (h_x = r0 - px r2,
@@ -242,7 +226,7 @@ __global__ void __launch_bounds__(kT2) raster2d_fwd_kernel(R2Args a, const float
       Eval2 e;
       const float4 sa = s.a[j];
       eval2(sa, s.b[j], s.c[j], pxf, pyf, oxf, oyf, e);
-      if (!e.ok || e.power > 0.f) continue;
+      if (!e.ok || e.power > 0.f || e.power < -4.5f) continue;  // min(g3, g2) > 9: outside the 3-sigma support
       const float alpha = fminf(kAMax, __fmul_rn(sa.z, ex2a(__fmul_rn(e.power, kLog2e2))));
       if (alpha < kAMin) continue;
       const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
@@ -393,7 +377,7 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
         const float4 sa = s.a[j];
         Eval2 e;
         eval2(sa, s.b[j], s.c[j], pxf, pyf, oxf, oyf, e);
-        if (e.ok && e.power <= 0.f) {
+        if (e.ok && e.power <= 0.f && e.power >= -4.5f) {
           const float ex = ex2a(__fmul_rn(e.power, kLog2e2));
           const float raw = __fmul_rn(sa.z, ex);
           const float alpha = fminf(kAMax, raw);

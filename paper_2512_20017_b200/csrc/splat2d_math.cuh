@@ -24,7 +24,8 @@ namespace bs {
 
 // SP row of a 2DGS splat (24 floats, 96 B):
 //   0 u  1 v  2 opacity  3..11 M (row-major)  12 r 13 g 14 b  15 depth
-//   16 radius_x  17 radius_y  18..20 normal (camera frame)  21..23 pad
+//   16 radius_x  17 radius_y (half-widths of the support box)  18..20 normal
+//   (camera frame)  21 pad  22 box centre x  23 box centre y
 constexpr int kSP2 = 24;
 // G_SP row of a 2DGS splat (16 floats, 64-byte aligned; 15 used): d u, d v,
 // d M[9], d opacity, d rgb, pad
@@ -61,6 +62,7 @@ struct Proj2D {
   float d[3], qc[3], Rc[9];
   float c0[3], c1[3], c2[3];  // M columns
   float u, v, depth, radius_x, radius_y, normal[3];
+  float box_cx, box_cy;  // centre of the support box (half-widths radius_x / radius_y)
   float len, dir[3], Y[16], col_raw[3], col[3], opac;
   bool valid;
 };
@@ -113,10 +115,29 @@ __device__ __forceinline__ void project2d_forward(const PointIn& pt, const Pre2D
     const float ex = fsub(fmul(bx, bx), fdiv(c00, c22));
     const float ey = fsub(fmul(by, by), fdiv(c11, c22));
     f.valid = ex >= 0.f && ey >= 0.f;
-    if (f.valid) {
-      f.radius_x = ceilf(fadd(fabsf(fsub(bx, f.u)), fsqrt(ex)));
-      f.radius_y = ceilf(fadd(fabsf(fsub(by, f.v)), fsqrt(ey)));
-    }
+  }
+  f.box_cx = f.u;
+  f.box_cy = f.v;
+  const float k = support_k(pre.opac);
+  if (f.valid && k > 0.f) {
+    // support {min(g3, g2) <= k}, k = min(9, 2 ln(255 o)): the image of the
+    // disk u^2 + v^2 <= k (dual conic, bounded since the 9-disk's is) united
+    // with the low-pass circle |mean2d - pixel| <= sqrt(k / 2)
+    const float k22 = fsub(fmul(k, fadd(fmul(f.c0[2], f.c0[2]), fmul(f.c1[2], f.c1[2]))), fmul(f.c2[2], f.c2[2]));
+    const float k02 = fsub(fmul(k, fadd(fmul(f.c0[0], f.c0[2]), fmul(f.c1[0], f.c1[2]))), fmul(f.c2[0], f.c2[2]));
+    const float k12 = fsub(fmul(k, fadd(fmul(f.c0[1], f.c0[2]), fmul(f.c1[1], f.c1[2]))), fmul(f.c2[1], f.c2[2]));
+    const float k00 = fsub(fmul(k, fadd(fmul(f.c0[0], f.c0[0]), fmul(f.c1[0], f.c1[0]))), fmul(f.c2[0], f.c2[0]));
+    const float k11 = fsub(fmul(k, fadd(fmul(f.c0[1], f.c0[1]), fmul(f.c1[1], f.c1[1]))), fmul(f.c2[1], f.c2[1]));
+    const float bx = fdiv(k02, k22), by = fdiv(k12, k22);
+    const float hx = fsqrt(fmaxf(fsub(fmul(bx, bx), fdiv(k00, k22)), 0.f));
+    const float hy = fsqrt(fmaxf(fsub(fmul(by, by), fdiv(k11, k22)), 0.f));
+    const float rc = fsqrt(fmul(0.5f, k));
+    const float x0 = fminf(fsub(bx, hx), fsub(f.u, rc)), x1 = fmaxf(fadd(bx, hx), fadd(f.u, rc));
+    const float y0 = fminf(fsub(by, hy), fsub(f.v, rc)), y1 = fmaxf(fadd(by, hy), fadd(f.v, rc));
+    f.box_cx = fmul(0.5f, fadd(x0, x1));
+    f.box_cy = fmul(0.5f, fadd(y0, y1));
+    f.radius_x = fmul(0.5f, fsub(x1, x0));
+    f.radius_y = fmul(0.5f, fsub(y1, y0));
   }
   // camera-frame normal, oriented towards the camera
   float n0 = f.Rc[2], n1 = f.Rc[5], n2 = f.Rc[8];
@@ -154,7 +175,7 @@ __device__ __forceinline__ void write_sp2_row(float* __restrict__ row, const Pro
   r4[2] = make_float4(f.c2[1], f.c0[2], f.c1[2], f.c2[2]);
   r4[3] = make_float4(f.col[0], f.col[1], f.col[2], f.depth);
   r4[4] = make_float4(f.valid ? f.radius_x : 0.f, f.valid ? f.radius_y : 0.f, f.normal[0], f.normal[1]);
-  r4[5] = make_float4(f.normal[2], 0.f, 0.f, 0.f);
+  r4[5] = make_float4(f.normal[2], 0.f, f.box_cx, f.box_cy);
 }
 
 // G_SP2 rows from the rasteriser carry, in entries 2..10, the moments

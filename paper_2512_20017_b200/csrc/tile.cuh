@@ -4,13 +4,13 @@
 
 namespace bs {
 
-// Tile rectangle of a splat (integer-exact on host and device), per-axis
-// radii rx = sp[10], ry = sp[11]:
+// Tile rectangle of a splat (integer-exact on host and device), support box
+// centre (u, v) and half-widths (rx, ry) (3DGS: mean, sp[10], sp[11]):
 //   x0 = clamp(floor((u - rx) / 16), 0, tiles_x), x1 = clamp(floor((u + rx) / 16) + 1, 0, tiles_x)
 // (and the same in y with ry): the tiles whose pixel span meets the box.
-__device__ __forceinline__ int tile_rect_at(const float* __restrict__ row, int rad_off, int W, int H, int& x0,
-                                            int& x1, int& y0, int& y1) {
-  const float u = row[0], v = row[1], rx = row[rad_off], ry = row[rad_off + 1];
+__device__ __forceinline__ int tile_rect_at(const float* __restrict__ row, int rad_off, int ctr_off, int W, int H,
+                                            int& x0, int& x1, int& y0, int& y1) {
+  const float u = row[ctr_off], v = row[ctr_off + 1], rx = row[rad_off], ry = row[rad_off + 1];
   if (!(rx > 0.f) || !(ry > 0.f)) {
     x0 = x1 = y0 = y1 = 0;
     return 0;
@@ -28,15 +28,17 @@ __device__ __forceinline__ int tile_rect_at(const float* __restrict__ row, int r
 // 3DGS rows keep the radii at floats 10, 11 (2DGS rows: 16, 17).
 __device__ __forceinline__ int tile_rect(const float* __restrict__ row, int W, int H, int& x0, int& x1, int& y0,
                                          int& y1) {
-  return tile_rect_at(row, 10, W, H, x0, x1, y0, y1);
+  return tile_rect_at(row, 10, 0, W, H, x0, x1, y0, y1);
 }
 
 // Row geometry of the splat-state layouts (include/splat_b200.h).
+// Support box: centre (row[ctr_off], row[ctr_off + 1]), half-widths
+// (row[rad_off], row[rad_off + 1]); 3DGS centres it on the splat's mean.
 struct SpLayout {
-  int stride, rad_off, depth_off;
+  int stride, rad_off, depth_off, ctr_off;
 };
 __host__ __device__ __forceinline__ SpLayout sp_layout(int model) {
-  return model == BS_MODEL_2DGS ? SpLayout{BS_SP2_FLOATS, 16, 15} : SpLayout{BS_SP_FLOATS, 10, 9};
+  return model == BS_MODEL_2DGS ? SpLayout{BS_SP2_FLOATS, 16, 15, 22} : SpLayout{BS_SP_FLOATS, 10, 9, 0};
 }
 
 // Segment (render slot run) of row r: last s with seg_row0[s] <= r.

@@ -182,7 +182,7 @@ def pts_splatting(view: CameraView, PC: dict, infrustum_ids: torch.Tensor, sh_de
     if model_id == nat.MODEL_2DGS:
         return {"means2d": sp[:, 0:2], "opacities": sp[:, 2], "ray_transforms": sp[:, 3:12],
                 "colors": sp[:, 12:15], "depths": sp[:, 15], "radii": sp[:, 16:18], "normals": sp[:, 18:21],
-                "_model": model}
+                "box_centers": sp[:, 22:24], "_model": model}
     return {"means2d": sp[:, 0:2], "opacities": sp[:, 2], "conics": sp[:, 3:6], "colors": sp[:, 6:9],
             "depths": sp[:, 9], "radii": sp[:, 10:12], "_model": model}
 
@@ -191,9 +191,11 @@ def pack_splats(SP: dict) -> torch.Tensor:
     """Differentiable inverse of the pts_splatting split: rows [V, SP]."""
     if SP.get("_model", "3dgs") == "2dgs":
         V = SP["means2d"].shape[0]
-        pad = SP["means2d"].new_zeros(V, 3)
+        pad = SP["means2d"].new_zeros(V, 1)
+        # radii: half-widths of the support box centred at box_centers (binning, culling)
         cols = [SP["means2d"], SP["opacities"].reshape(-1, 1), SP["ray_transforms"], SP["colors"],
-                SP["depths"].reshape(-1, 1).detach(), SP["radii"].detach(), SP["normals"].detach(), pad]
+                SP["depths"].reshape(-1, 1).detach(), SP["radii"].detach(), SP["normals"].detach(), pad,
+                SP["box_centers"].detach()]
     else:
         cols = [SP["means2d"], SP["opacities"].reshape(-1, 1), SP["conics"], SP["colors"],
                 SP["depths"].reshape(-1, 1).detach(), SP["radii"].detach()]
