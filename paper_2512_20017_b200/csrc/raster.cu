@@ -61,9 +61,9 @@ struct RastArgs {
   int n_slots, tiles_per_slot, W, H, tiles_x;
   float bg[3];
   int loss_fused;
-  float inv_norm;
+  float inv_norm;                // 1 / (H * W * 3)
   int patch_P;
-  const uint64_t* slot_patches;  // NULL: every pixel  // 1 / (H * W * 3)
+  const uint64_t* slot_patches;  // NULL: every pixel
 };
 
 // Patch restriction (P > 1): does this slot render pixel (x, y)?  Patch c of
