@@ -119,6 +119,13 @@ typedef struct {
   int32_t n_gpus;     /* columns of the access matrix (ACCESS modes) */
   int32_t temporal;   /* 1: also test presence[i,0] <= t <= presence[i,1] in f32 */
   int32_t pos_stride; /* floats between consecutive positions: 3 or 4 */
+  int32_t max_chunks; /* BS_CULL_MASK with chunk_prefix: chunks of 256 points
+                         per group slot, ceil(max_group_points / 256) */
+  int32_t* chunk_prefix; /* BS_CULL_MASK, optional: int32 [n_groups][max_chunks][B],
+                            visible points of view v in the group's chunks
+                            before chunk c (the per-point projection kernels
+                            then start each 256-point CTA at its row offset
+                            instead of re-counting the group's earlier chunks) */
 } bs_cull_desc;
 
 /* planes: float64 [B][2 + 2*(P+1)][4]: near, far, x-edges c=0..P,
@@ -210,6 +217,8 @@ typedef struct {
   int32_t gsp_form;  /* 3DGS G_SP rows given to the projection backward:
                         0 = raster moments (bs_raster_bwd output, default),
                         1 = plain dL/dSP (d u, d v, d opacity, d conic, d rgb) */
+  const int32_t* chunk_prefix; /* optional: bs_cull_count's chunk_prefix for the
+                                  same mask, max_chunks = ceil(max_group_points / 256) */
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,

@@ -44,7 +44,8 @@ class Camera(C.Structure):
 
 class CullDesc(C.Structure):
     _fields_ = [("mode", C.c_int32), ("n_views", C.c_int32), ("P", C.c_int32),
-                ("n_gpus", C.c_int32), ("temporal", C.c_int32), ("pos_stride", C.c_int32)]
+                ("n_gpus", C.c_int32), ("temporal", C.c_int32), ("pos_stride", C.c_int32),
+                ("max_chunks", C.c_int32), ("chunk_prefix", C.c_void_p)]
 
 
 MODEL_3DGS = 0
@@ -56,7 +57,7 @@ GSP2_FLOATS = 16
 class ProjDesc(C.Structure):
     _fields_ = [("n_views", C.c_int32), ("sh_degree", C.c_int32),
                 ("tiles_x_max", C.c_int32), ("tiles_y_max", C.c_int32), ("model", C.c_int32),
-                ("max_group_points", C.c_int32), ("gsp_form", C.c_int32)]
+                ("max_group_points", C.c_int32), ("gsp_form", C.c_int32), ("chunk_prefix", C.c_void_p)]
 
 
 class RasterDesc(C.Structure):

@@ -35,7 +35,10 @@ struct CullArgs {
   void* out0;
   void* out1;
   void* out2;
+  int max_chunks;
+  int32_t* chunk_prefix;  // MASK: [n_groups][max_chunks][B] or NULL
 };
+static_assert(kCullThreads == 256, "chunk_prefix counts 256-point chunks (the projection CTA size)");
 
 // Plane indices inside one view's block: 0 near, 1 far, 2..2+P x-edges,
 // 3+P..3+2P y-edges.
@@ -122,6 +125,13 @@ __global__ void __launch_bounds__(kCullThreads) cull_kernel(CullArgs a) {
   } else if (s_any_live || MODE == BS_CULL_MASK) {
     const int lane = tid & 31;
     for (int base = begin; base < end; base += blockDim.x) {
+      if (MODE == BS_CULL_MASK && a.chunk_prefix) {
+        // counts of the chunks before this one (all of them are in s_cnt)
+        __syncthreads();
+        if (tid < B)
+          a.chunk_prefix[((size_t)g * a.max_chunks + (base - begin) / kCullThreads) * B + tid] = s_cnt[tid];
+        __syncthreads();
+      }
       const int i = base + tid;
       const bool valid = i < end;
       double x = 0, y = 0, z = 0;
@@ -372,8 +382,11 @@ extern "C" int32_t bs_cull_count(const bs_cull_desc* d, const float* positions, 
   }
   const size_t smem = sizeof(double) * B * npl * 4 + ((B * PP + 15) & ~15) + sizeof(int) * (size_t)n_cnt;
   BS_REQUIRE(smem <= 200 * 1024, BS_ERR_PARAMETER, "too many views/patches for one launch (%zu B smem)", smem);
+  if (mode == BS_CULL_MASK && d->chunk_prefix)
+    BS_REQUIRE(d->max_chunks >= 1, BS_ERR_PARAMETER, "chunk_prefix needs max_chunks >= 1");
   CullArgs a{mode, B, P, d->n_gpus, d->temporal, d->pos_stride, positions, presence, group_begin,
-             group_aabb, n_groups, planes, view_times, point_gpu, out0, out1, out2};
+             group_aabb, n_groups, planes, view_times, point_gpu, out0, out1, out2,
+             d->max_chunks, mode == BS_CULL_MASK ? d->chunk_prefix : nullptr};
   auto launch = [&](auto kern) -> int32_t {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<n_groups, kCullThreads, smem, s>>>(a);

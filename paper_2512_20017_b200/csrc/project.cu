@@ -54,7 +54,8 @@ struct RowRanker {
 // per-view counts advanced over the group's earlier chunks first.  Returns
 // false (uniformly over the CTA) when the chunk lies past the group's end.
 __device__ __forceinline__ bool chunk_range(const int32_t* __restrict__ group_begin, const uint32_t* __restrict__ mask,
-                                            RowRanker& rk, int g, int B, int& lo, int& hi) {
+                                            const int32_t* __restrict__ chunk_prefix, RowRanker& rk, int g, int B,
+                                            int& lo, int& hi) {
   const int begin = group_begin[g], end = group_begin[g + 1];
   if (gridDim.y == 1) {
     lo = begin;
@@ -64,6 +65,11 @@ __device__ __forceinline__ bool chunk_range(const int32_t* __restrict__ group_be
   lo = begin + (int)blockIdx.y * kProjThreads;
   if (lo >= end) return false;
   hi = min(end, lo + kProjThreads);
+  if (chunk_prefix) {  // counted by the culling kernel
+    if (threadIdx.x < B) rk.s_run[threadIdx.x] = chunk_prefix[((size_t)g * gridDim.y + blockIdx.y) * B + threadIdx.x];
+    __syncthreads();
+    return true;
+  }
   for (int b = begin; b < lo; b += kProjThreads) {
     rk.round(mask[b + threadIdx.x], B);
     rk.advance(B);
@@ -81,6 +87,7 @@ struct ProjArgs {
   const int64_t* view_row0;
   const bs_camera* cams;
   int gsp_standard;  // 3DGS G_SP rows: 0 = raster moments (default), 1 = dL/dSP
+  const int32_t* chunk_prefix;  // [ng][gridDim.y][B] rows before each chunk, or NULL
 };
 
 // Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
   __syncthreads();
   RowRanker rk{s_bal, s_run};
   int lo, end;
-  if (!chunk_range(a.group_begin, a.mask, rk, g, B, lo, end)) return;
+  if (!chunk_range(a.group_begin, a.mask, a.chunk_prefix, rk, g, B, lo, end)) return;
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const uint32_t mask = i < end ? a.mask[i] : 0u;
@@ -211,7 +218,7 @@ __global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, c
   __syncthreads();
   RowRanker rk{s_bal, s_run};
   int lo, end;
-  if (!chunk_range(a.group_begin, a.mask, rk, g, B, lo, end)) return;
+  if (!chunk_range(a.group_begin, a.mask, a.chunk_prefix, rk, g, B, lo, end)) return;
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const uint32_t mask = i < end ? a.mask[i] : 0u;
@@ -308,7 +315,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
   __syncthreads();
   RowRanker rk{s_bal, s_run};
   int lo, end;
-  if (!chunk_range(a.group_begin, a.mask, rk, g, B, lo, end)) return;
+  if (!chunk_range(a.group_begin, a.mask, a.chunk_prefix, rk, g, B, lo, end)) return;
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const bool ok = i < end;
@@ -492,7 +499,7 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
   if (n_groups == 0) return BS_OK;
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams, d->gsp_form};
+             view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr};
   const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
     project_fwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
@@ -511,7 +518,7 @@ extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, in
   if (n_groups == 0) return BS_OK;
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams, d->gsp_form};
+             view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr};
   const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
     project_bwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(
@@ -547,7 +554,7 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   if (n_groups == 0) return BS_OK;
   const int n_sh = (pd->sh_degree + 1) * (pd->sh_degree + 1);
   ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams, pd->gsp_form};
+             view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr};
   AdamConsts c = make_adam(ad);
   const size_t smem = sizeof(float) * 48 * kProjThreads;
   auto launch = [&](auto kern) {

@@ -124,6 +124,7 @@ class SplatTrainer:
         self.n_groups = len(group_begin) - 1
         gsz = np.diff(np.asarray(group_begin, dtype=np.int64))
         self.max_group = int(gsz.max()) if len(gsz) else 0  # per-point kernels: one CTA per 256 points
+        self.max_chunks = max(1, -(-self.max_group // 256))
         self.views = list(views)
         self.W, self.H = self.views[0].width, self.views[0].height
         if any((v.width, v.height) != (self.W, self.H) for v in self.views):
@@ -225,14 +226,15 @@ class SplatTrainer:
         self._ids_ev[k] = ev
         return dst
 
-    def _cull_counts(self, batch_ids, mask, counts, base, view_rows, view_row0, st, bidx=None, patch_counts=None):
+    def _cull_counts(self, batch_ids, mask, counts, base, view_rows, view_row0, st, bidx=None, patch_counts=None,
+                     chunk_prefix=None):
         B = len(batch_ids)
         if bidx is None:
             bidx = self._device_ids(batch_ids, "bidx_cull")
         planes = self.planes_all.index_select(0, bidx).contiguous()
         temporal = self.presence is not None
         times = self.view_times.index_select(0, bidx).contiguous() if temporal else None
-        desc = nat.CullDesc(nat.CULL_MASK, B, self.P, 1, 1 if temporal else 0, 4)
+        desc = nat.CullDesc(nat.CULL_MASK, B, self.P, 1, 1 if temporal else 0, 4, self.max_chunks, nat.ptr(chunk_prefix))
         nat.call("bs_cull_count", desc, nat.ptr(self.params), self.S, nat.ptr(self.presence),
                  nat.ptr(self.group_begin), nat.ptr(self.aabb), self.n_groups, nat.ptr(planes), nat.ptr(times),
                  None, nat.ptr(mask), nat.ptr(counts), nat.ptr(patch_counts), st)
@@ -259,8 +261,11 @@ class SplatTrainer:
         view_row0 = self.buf.get("view_row0", B, torch.int64)
         patched = self.comm is not None and self.P > 1
         patch_counts = self.buf.get("patch_counts", B * self.P * self.P, torch.int64) if patched else None
+        # rows of each (group, 256-point chunk) before the chunk, for the projection kernels
+        chunk_prefix = self.buf.get("chunk_prefix", self.n_groups * self.max_chunks * B, torch.int32)
         with self._t("cull"):
-            self._cull_counts(batch_ids, mask, counts, base, view_rows, view_row0, st, bidx, patch_counts)
+            self._cull_counts(batch_ids, mask, counts, base, view_rows, view_row0, st, bidx, patch_counts,
+                              chunk_prefix)
         if self.comm is not None and next_batch is not None:
             # counts of the next batch (per view, or per patch when P > 1) on
             # the pre-update positions -> its W on a host thread (exchange.py)
@@ -276,9 +281,10 @@ class SplatTrainer:
                                tuple(int(v) for v in next_batch))
         if patched:
             return self._step_patches(batch_ids, gt_batch, bidx, cams, mask, base, view_rows, view_row0,
-                                      patch_counts, st)
+                                      patch_counts, st, chunk_prefix)
         lay = None
-        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group)
+        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group, 0,
+                             nat.ptr(chunk_prefix))
         early = self.comm is None and S * B * self.sp_floats * 4 <= self.sp_capacity_bytes
         if early:
             # the row counts start towards the host before the projection is
@@ -364,7 +370,8 @@ class SplatTrainer:
                      nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
         return losses
 
-    def _step_patches(self, batch_ids, gt_batch, bidx, cams, mask, base, view_rows, view_row0, patch_counts, st):
+    def _step_patches(self, batch_ids, gt_batch, bidx, cams, mask, base, view_rows, view_row0, patch_counts, st,
+                      chunk_prefix=None):
         """Alg. 1 with P x P patches per view on several ranks (SURVEY.md
         §8(e)): A over the B P^2 patches -> W; every rank projects its points
         for all batch views, sends each splat row to the ranks whose patches
@@ -381,7 +388,8 @@ class SplatTrainer:
         n_rows = int(rows_host.sum())
         self.last.update(A=A, W=W, rows_per_view=rows_host.copy())
         sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
-        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group)
+        pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group, 0,
+                             nat.ptr(chunk_prefix))
         with self._t("project"):
             nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask), nat.ptr(self.group_begin),
                      self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(sp), st)

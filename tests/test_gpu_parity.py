@@ -173,6 +173,32 @@ def test_projection_bitexact_and_binning(c1, cuda):
             assert np.array_equal(a, b), f"view {v} tile {t}"
 
 
+def test_groups_of_several_chunks(cuda):
+    """Groups larger than one 256-point projection CTA (G = 1000: 4 chunks, the
+    last ragged): the culling kernel's per-chunk row prefix equals the counts of
+    the mask, and the rows land bit-exactly where the oracle puts them."""
+    ds, params, gb, aabb, gt = c1_setup(G=1000)
+    tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt, sh_degree=3)
+    assert tr.max_chunks == 4
+    batch = [0, 3, 5]
+    B = len(batch)
+    tr.step(batch)
+    torch.cuda.synchronize()
+    mask = tr.buf.bufs["mask"][: tr.S].cpu().numpy().view(np.uint32)
+    pre = tr.buf.bufs["chunk_prefix"][: tr.n_groups * 4 * B].cpu().numpy().reshape(tr.n_groups, 4, B)
+    for g in range(tr.n_groups):
+        for c in range(-(-(gb[g + 1] - gb[g]) // 256)):
+            seg = mask[gb[g]: gb[g] + 256 * c]
+            assert [int(((seg >> v) & 1).sum()) for v in range(B)] == list(pre[g, c])
+    sp = tr.last["sp"][: tr.last["n_rows"] * 12].cpu().numpy().reshape(-1, 12)
+    row0 = np.concatenate([[0], np.cumsum(tr.last["rows_per_view"])])
+    for s, v in enumerate(batch):
+        ref = oracle_view_pipeline(params, gb, aabb, ds.views[v], camera_bytes([ds.views[v]]), gt[v])
+        assert np.array_equal(sp[row0[s]:row0[s + 1]].view(np.uint32), ref["sp"].view(np.uint32))
+        assert np.abs(tr.last["image"][s * tr.H * tr.W * 3:(s + 1) * tr.H * tr.W * 3].cpu().numpy().reshape(
+            tr.H, tr.W, 3) - ref["img"]).max() <= IMG_TOL
+
+
 @pytest.mark.parametrize("bg", [(0.0, 0.0, 0.0), (0.2, 0.5, 0.9)])
 def test_render_forward_and_backward_tolerance(c1, cuda, bg):
     ds, params, gb, aabb, gt = c1
