@@ -381,6 +381,52 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
   return true;
 }
 
+// pixel_grad<true, kBg> without branches (one pixel per lane): every lane
+// runs the whole sequence and the pixels the splat does not touch (or that lie
+// past their last contributor: live == false) keep their state through
+// selects and return zero terms.  The arithmetic of a contributing pixel is
+// the same instruction sequence as pixel_grad's, so the results are identical;
+// what goes is the divergent-branch bookkeeping (BSSY/BSYNC, three branches
+// and their reconvergence stalls) in the hottest loop of the backward.
+template <bool kBg>
+__device__ __forceinline__ bool pixel_grad_sel(PixelBwd& p, const float4& sa, const float4& sb, float cb, F2 npx,
+                                               bool live, float g[9]) {
+  F2 d;
+  const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
+  const float ex = ex2_approx(fminf(power2, 0.f));
+  const float raw = __fmul_rn(sb.y, ex);
+  const float alpha = fminf(kAlphaMax, raw);
+  const bool ok = live && !(power2 > 0.f || power2 < kP2Min) && !(alpha < kAlphaMin);
+  const float ra = rcp_approx(1.f - alpha);  // alpha <= 0.99
+  const float T = p.T * ra;
+  const float fac = alpha * T;
+  const F2 e01 = add2(f2(sb.z, sb.w), f2(-p.acc01.x, -p.acc01.y));
+  const float e2 = cb - p.acc2;
+  const float2 ed = unf2(mul2(e01, p.dC01));
+  float dL_dalpha = T * fmaf(e2, p.dC2, ed.x + ed.y);
+  if (kBg) dL_dalpha -= p.T_final * ra * p.bgdot;
+  const float2 acc01 = unf2(fma2(bcast(alpha), e01, f2(p.acc01.x, p.acc01.y)));
+  const float acc2 = fmaf(alpha, e2, p.acc2);
+  p.T = ok ? T : p.T;
+  p.acc01 = ok ? acc01 : p.acc01;
+  p.acc2 = ok ? acc2 : p.acc2;
+  const bool grad = ok && !(raw > kAlphaMax);
+  const float dpow = grad ? dL_dalpha * alpha : 0.f;  // dL / d power
+  const float2 t01 = unf2(mul2(bcast(dpow), d));
+  const float2 t34 = unf2(mul2(bcast(t01.x), d));
+  const float2 t67 = unf2(mul2(bcast(ok ? fac : 0.f), p.dC01));
+  g[0] = t01.x;
+  g[1] = t01.y;
+  g[2] = grad ? dL_dalpha * ex : 0.f;
+  g[3] = t34.x;
+  g[4] = t34.y;
+  g[5] = t01.y * unf2(d).y;
+  g[6] = t67.x;
+  g[7] = t67.y;
+  g[8] = (ok ? fac : 0.f) * p.dC2;
+  return ok;
+}
+
 __device__ __forceinline__ void init_pixel_bwd(PixelBwd& q, const RastArgs& a, int slot, int px, int py, bool inside,
                                                const float* __restrict__ image, const float* __restrict__ final_T,
                                                const int32_t* __restrict__ n_contrib,
@@ -463,7 +509,7 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
       const float cb = s.c[j];
       bool any = false;
       if constexpr (PPL == 1) {
-        if (rel < p[0].n) any = pixel_grad<true, kBg>(p[0], sa, sb, cb, f2(-pxf, -((float)q.py0 + 0.5f)), g);
+        any = pixel_grad_sel<kBg>(p[0], sa, sb, cb, f2(-pxf, -((float)q.py0 + 0.5f)), rel < p[0].n, g);
       } else {
 #pragma unroll
         for (int k = 0; k < 9; ++k) g[k] = 0.f;
@@ -486,9 +532,7 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
           for (int k = 0; k < 9; ++k) atomicAdd(dst + k, g[k]);
 #endif
         }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) g[k] = any ? g[k] : 0.f;
+      } else {  // g is zero in the lanes without a contribution
         int idx;
         const float r = warp_reduce9(g, idx);
         if (idx >= 0) atomicAdd(dst + idx, r);
