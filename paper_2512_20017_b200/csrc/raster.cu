@@ -194,6 +194,27 @@ __device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float
   p.contrib = rel + 1;
 }
 
+// blend() with one early-out (the support test, mostly warp-uniform) and
+// selects for the rest; same arithmetic as blend().
+__device__ __forceinline__ void blend_sel(PixelFwd& p, const float4& sa, const float4& sb, float cb, F2 npx, int rel) {
+  F2 d;
+  const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
+  if (power2 > 0.f || power2 < kP2Min) return;
+  const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, ex2_approx(power2)));
+  const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
+  const bool ok = !(alpha < kAlphaMin);
+  const bool fin = ok && nT < kTMin;
+  const bool c = ok && !fin;
+  const float w = __fmul_rn(alpha, p.T);
+  const F2 c01 = fma2(f2(sb.z, sb.w), bcast(w), p.c01);
+  const float c2 = __fmaf_rn(cb, w, p.c2);
+  p.done = p.done || fin;
+  p.c01 = c ? c01 : p.c01;
+  p.c2 = c ? c2 : p.c2;
+  p.T = c ? nT : p.T;
+  p.contrib = c ? rel + 1 : p.contrib;
+}
+
 template <int PPL>
 __device__ __forceinline__ bool all_done(const PixelFwd (&p)[PPL]) {
   bool d = true;
@@ -241,9 +262,13 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
       const float4 sb = s.b[j];
       const float cb = s.c[j];
       const int rel = b0 + j - rg.x;
+      if constexpr (PPL == 1) {
+        if (!p[0].done) blend_sel(p[0], sa, sb, cb, f2(-pxf, -((float)q.py0 + 0.5f)), rel);
+      } else {
 #pragma unroll
-      for (int k = 0; k < PPL; ++k)
-        if (!p[k].done) blend(p[k], sa, sb, cb, f2(-pxf, -((float)(q.py0 + k) + 0.5f)), rel);
+        for (int k = 0; k < PPL; ++k)
+          if (!p[k].done) blend(p[k], sa, sb, cb, f2(-pxf, -((float)(q.py0 + k) + 0.5f)), rel);
+      }
     }
     __syncwarp();
   }
