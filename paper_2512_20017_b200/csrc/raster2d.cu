@@ -169,8 +169,9 @@ __device__ __forceinline__ void eval2(const float4& a, const float4& b, const fl
   e.z[1] = zxy.y;
   e.z[2] = __fmaf_rn(c.w, oy, __fmaf_rn(c.z, ox, a.w));
   e.ok = e.z[2] != 0.f;
-  if (!e.ok) return;
-  e.iz = rcpa(e.z[2]);  // one approximate reciprocal (both kernels evaluate it identically)
+  // one approximate reciprocal (both kernels evaluate it identically); the
+  // rest is evaluated for every pixel and discarded when !ok
+  e.iz = rcpa(e.ok ? e.z[2] : 1.f);
   const float2 uv = unf2(mul2(f2(e.z[0], e.z[1]), bcast(e.iz)));
   e.u = uv.x;
   e.v = uv.y;
@@ -227,20 +228,20 @@ __global__ void __launch_bounds__(kT2) raster2d_fwd_kernel(R2Args a, const float
       const float4 sa = s.a[j];
       eval2(sa, s.b[j], s.c[j], pxf, pyf, oxf, oyf, e);
       if (!e.ok || e.power > 0.f || e.power < -4.5f) continue;  // min(g3, g2) > 9: outside the 3-sigma support
+      // past the support test: selects instead of branches
       const float alpha = fminf(kAMax, __fmul_rn(sa.z, ex2a(__fmul_rn(e.power, kLog2e2))));
-      if (alpha < kAMin) continue;
       const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
-      if (nT < kTStop) {
-        p.done = true;
-        continue;
-      }
+      const bool ok = !(alpha < kAMin);
+      const bool fin = ok && nT < kTStop;
+      const bool c = ok && !fin;
       const float wgt = __fmul_rn(alpha, p.T);
       const float4 col = s.d[j];
-      p.c0 = __fmaf_rn(col.x, wgt, p.c0);
-      p.c1 = __fmaf_rn(col.y, wgt, p.c1);
-      p.c2 = __fmaf_rn(col.z, wgt, p.c2);
-      p.T = nT;
-      p.contrib = b0 + j + 1 - rg.x;
+      p.done = p.done || fin;
+      p.c0 = c ? __fmaf_rn(col.x, wgt, p.c0) : p.c0;
+      p.c1 = c ? __fmaf_rn(col.y, wgt, p.c1) : p.c1;
+      p.c2 = c ? __fmaf_rn(col.z, wgt, p.c2) : p.c2;
+      p.T = c ? nT : p.T;
+      p.contrib = c ? b0 + j + 1 - rg.x : p.contrib;
     }
     __syncwarp();
   }
@@ -369,66 +370,62 @@ __global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
       const int j = __ffs(bits) - 1;
       bits &= bits - 1;
       const int rel = cend - 1 - j - rg.x;
+      // every lane runs the whole sequence; pixels without a contribution
+      // keep their state through selects and produce zero terms (same
+      // arithmetic as a branchy version for the contributing ones)
       float g[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) g[k] = 0.f;
-      bool any = false;
-      if (rel < q.n) {
-        const float4 sa = s.a[j];
-        Eval2 e;
-        eval2(sa, s.b[j], s.c[j], pxf, pyf, oxf, oyf, e);
-        if (e.ok && e.power <= 0.f && e.power >= -4.5f) {
-          const float ex = ex2a(__fmul_rn(e.power, kLog2e2));
-          const float raw = __fmul_rn(sa.z, ex);
-          const float alpha = fminf(kAMax, raw);
-          if (alpha >= kAMin) {
-            any = true;
-            const float4 col = s.d[j];
-            const float ra = rcpa(1.f - alpha);  // alpha <= 0.99
-            q.T = q.T * ra;
-            const float fac = alpha * q.T;
-            g[12] = fac * q.dC0;
-            g[13] = fac * q.dC1;
-            g[14] = fac * q.dC2;
-            // acc = colour behind this splat (normalised); acc' = acc + alpha (c - acc)
-            const float e0 = col.x - q.acc0, e1 = col.y - q.acc1, e2 = col.z - q.acc2;
-            float dLda = q.T * (e0 * q.dC0 + e1 * q.dC1 + e2 * q.dC2);
-            if (kBg) dLda -= q.T_final * ra * q.bgdot;
-            q.acc0 = fmaf(alpha, e0, q.acc0);
-            q.acc1 = fmaf(alpha, e1, q.acc1);
-            q.acc2 = fmaf(alpha, e2, q.acc2);
-            if (raw <= kAMax) {
-              const float dpow = dLda * alpha;
-              g[11] = dLda * ex;
-              if (e.g3 <= e.g2) {
-                // power = -0.5 (u^2 + v^2), (u, v) = zeta.xy / zeta.z; G_SP2
-                // carries the moments sum gz, sum gz px, sum gz py of
-                // dL/dzeta (the projection backward applies the M rows)
-                const F2 guv = mul2(f2(e.u, e.v), bcast(-dpow));  // dL/d(u, v)
-                const float2 g_uv = unf2(guv);
-                const float iz = e.iz;
-                const F2 gz01 = mul2(guv, bcast(iz));
-                const float gz2 = -(g_uv.x * e.u + g_uv.y * e.v) * iz;
-                const float2 z01 = unf2(gz01);
-                const float2 zx = unf2(mul2(gz01, bcast(pxf)));
-                const float2 zy = unf2(mul2(gz01, bcast(pyf)));
-                g[2] = z01.x;
-                g[3] = z01.y;
-                g[4] = gz2;
-                g[5] = zx.x;
-                g[6] = zx.y;
-                g[7] = gz2 * pxf;
-                g[8] = zy.x;
-                g[9] = zy.y;
-                g[10] = gz2 * pyf;
-              } else {
-                // power = -(dx^2 + dy^2), dx = u - px
-                g[0] = -2.f * e.dx * dpow;
-                g[1] = -2.f * e.dy * dpow;
-              }
-            }
-          }
-        }
+      const float4 sa = s.a[j];
+      Eval2 e;
+      eval2(sa, s.b[j], s.c[j], pxf, pyf, oxf, oyf, e);
+      const float ex = ex2a(__fmul_rn(fminf(e.power, 0.f), kLog2e2));
+      const float raw = __fmul_rn(sa.z, ex);
+      const float alpha = fminf(kAMax, raw);
+      const bool any = rel < q.n && e.ok && e.power <= 0.f && e.power >= -4.5f && alpha >= kAMin;
+      {
+        const float4 col = s.d[j];
+        const float ra = rcpa(1.f - alpha);  // alpha <= 0.99
+        const float T = q.T * ra;
+        const float fac = any ? alpha * T : 0.f;
+        g[12] = fac * q.dC0;
+        g[13] = fac * q.dC1;
+        g[14] = fac * q.dC2;
+        g[15] = 0.f;
+        // acc = colour behind this splat (normalised); acc' = acc + alpha (c - acc)
+        const float e0 = col.x - q.acc0, e1 = col.y - q.acc1, e2 = col.z - q.acc2;
+        float dLda = T * (e0 * q.dC0 + e1 * q.dC1 + e2 * q.dC2);
+        if (kBg) dLda -= q.T_final * ra * q.bgdot;
+        q.acc0 = any ? fmaf(alpha, e0, q.acc0) : q.acc0;
+        q.acc1 = any ? fmaf(alpha, e1, q.acc1) : q.acc1;
+        q.acc2 = any ? fmaf(alpha, e2, q.acc2) : q.acc2;
+        q.T = any ? T : q.T;
+        const bool grad = any && raw <= kAMax;
+        const float dpow = dLda * alpha;
+        g[11] = grad ? dLda * ex : 0.f;
+        // disk term: power = -0.5 (u^2 + v^2), (u, v) = zeta.xy / zeta.z; G_SP2
+        // carries the moments sum gz, sum gz px, sum gz py of dL/dzeta (the
+        // projection backward applies the M rows)
+        const bool disk = grad && e.g3 <= e.g2;
+        const F2 guv = mul2(f2(e.u, e.v), bcast(-dpow));  // dL/d(u, v)
+        const float2 g_uv = unf2(guv);
+        const float iz = e.iz;
+        const F2 gz01 = mul2(guv, bcast(iz));
+        const float gz2 = -(g_uv.x * e.u + g_uv.y * e.v) * iz;
+        const float2 z01 = unf2(gz01);
+        const float2 zx = unf2(mul2(gz01, bcast(pxf)));
+        const float2 zy = unf2(mul2(gz01, bcast(pyf)));
+        g[2] = disk ? z01.x : 0.f;
+        g[3] = disk ? z01.y : 0.f;
+        g[4] = disk ? gz2 : 0.f;
+        g[5] = disk ? zx.x : 0.f;
+        g[6] = disk ? zx.y : 0.f;
+        g[7] = disk ? gz2 * pxf : 0.f;
+        g[8] = disk ? zy.x : 0.f;
+        g[9] = disk ? zy.y : 0.f;
+        g[10] = disk ? gz2 * pyf : 0.f;
+        // low-pass term: power = -(dx^2 + dy^2), dx = u - px
+        const bool lp = grad && !disk;
+        g[0] = lp ? -2.f * e.dx * dpow : 0.f;
+        g[1] = lp ? -2.f * e.dy * dpow : 0.f;
       }
       const uint32_t who = __ballot_sync(0xffffffffu, any);
       if (who == 0u) continue;
