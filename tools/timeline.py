@@ -22,17 +22,20 @@ from paper_2512_20017_b200.trainer import AdamConfig, SplatTrainer  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--steps", type=int, default=1, help="consecutive steps inside the profile")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     ds, g, params, gt = bench.build_scene(cfg)
     tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt,
                       adam=AdamConfig(scenes.lr_table(cfg["altitude"])), model=cfg.get("model", "3dgs"))
-    sched = bench.schedule(cfg["n_views"], cfg["batch"], 8)
+    sched = bench.schedule(cfg["n_views"], cfg["batch"], 5 + args.steps)
     for i in range(5):
         tr.step(sched[i])
+    assert len(sched) >= 5 + args.steps
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        tr.step(sched[5])
+        for i in range(args.steps):
+            tr.step(sched[5 + i])
         torch.cuda.synchronize()
     ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     ev.sort(key=lambda e: e.time_range.start)
