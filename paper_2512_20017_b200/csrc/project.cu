@@ -100,15 +100,19 @@ struct Model3 {
   using Pre = PointPre;
   static constexpr int kSP = BS_SP_FLOATS, kGSP = BS_GSP_FLOATS, kAcc = 6;
   __device__ static void pre(const PointIn& pt, Pre& r) { point_pre(pt, r); }
+  static constexpr int kGcol = 6;  // colour gradient inside a G_SP row
+  static constexpr bool kFuseWk = false;
   template <class SH>
-  __device__ static void forward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh, F& f) {
-    project_forward_t(pt, r, sh, c, n_sh, f);
+  __device__ static void forward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh, F& f,
+                                 const float* gcol = nullptr, float* wk = nullptr) {
+    project_forward_t(pt, r, sh, c, n_sh, f, gcol, wk);
   }
   __device__ static void write(float* row, const F& f) { write_sp_row(row, f); }
   template <class SH, class A>
   __device__ static void backward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh,
-                                  const F& f, const float* gs, float* g, float* acc, A add) {
-    project_backward_t(pt, r, sh, c, n_sh, f, gs, g, acc, add);
+                                  const F& f, const float* gs, float* g, float* acc, A add,
+                                  const float* wk_pre = nullptr) {
+    project_backward_t(pt, r, sh, c, n_sh, f, gs, g, acc, add, wk_pre);
   }
   __device__ static void finish(const PointIn& pt, const float* acc, float* g) { point_pre_backward(pt, acc, g); }
   // raster moments (M1..M5 of dL/dpower) -> dL/d(u, v, conic a, b, c)
@@ -120,15 +124,19 @@ struct Model2 {
   using Pre = Pre2D;
   static constexpr int kSP = kSP2, kGSP = kGSP2, kAcc = 9;
   __device__ static void pre(const PointIn& pt, Pre& r) { point_pre2(pt, r); }
+  static constexpr int kGcol = 12;
+  static constexpr bool kFuseWk = true;
   template <class SH>
-  __device__ static void forward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh, F& f) {
-    project2d_forward(pt, r, sh, c, n_sh, f);
+  __device__ static void forward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh, F& f,
+                                 const float* gcol = nullptr, float* wk = nullptr) {
+    project2d_forward(pt, r, sh, c, n_sh, f, gcol, wk);
   }
   __device__ static void write(float* row, const F& f) { write_sp2_row(row, f); }
   template <class SH, class A>
   __device__ static void backward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh,
-                                  const F& f, const float* gs, float* g, float* acc, A add) {
-    project2d_backward(pt, r, sh, c, n_sh, f, gs, g, acc, add);
+                                  const F& f, const float* gs, float* g, float* acc, A add,
+                                  const float* wk_pre = nullptr) {
+    project2d_backward(pt, r, sh, c, n_sh, f, gs, g, acc, add, wk_pre);
   }
   __device__ static void finish(const PointIn& pt, const float* acc, float* g) { point_pre2_backward(pt, acc, g); }
   // raster moments of dL/dzeta -> dL/dM rows
@@ -195,9 +203,10 @@ __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camer
 #pragma unroll
     for (int k = 0; k < M::kGSP; ++k) gs[k] = src[k];
     typename M::F f;
-    M::forward(pt, pre, sh, s_cam[v], a.n_sh, f);
+    float wk[16];  // SH direction weights, computed with the colour (one pass over the coefficients)
+    M::forward(pt, pre, sh, s_cam[v], a.n_sh, f, M::kFuseWk ? gs + M::kGcol : nullptr, M::kFuseWk ? wk : nullptr);
     if (!a.gsp_standard) M::from_moments(f, gs);
-    M::backward(pt, pre, sh, s_cam[v], a.n_sh, f, gs, g, acc, sh_add);
+    M::backward(pt, pre, sh, s_cam[v], a.n_sh, f, gs, g, acc, sh_add, M::kFuseWk ? wk : nullptr);
   }
   M::finish(pt, acc, g);
 }

@@ -75,7 +75,8 @@ __device__ __forceinline__ void kmul(const bs_camera& c, const float x[3], float
 
 template <class SH>
 __device__ __forceinline__ void project2d_forward(const PointIn& pt, const Pre2D& pre, const SH& sh,
-                                                  const bs_camera& c, int n_sh, Proj2D& f) {
+                                                  const bs_camera& c, int n_sh, Proj2D& f,
+                                                  const float* gcol = nullptr, float* wk = nullptr) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) f.d[k] = fsub(pt.p[k], c.pos[k]);
   const float* W = c.rot_cw;
@@ -155,15 +156,7 @@ __device__ __forceinline__ void project2d_forward(const PointIn& pt, const Pre2D
 #pragma unroll
   for (int k = 0; k < 3; ++k) f.dir[k] = fdiv(f.d[k], f.len);
   sh_basis(f.dir, n_sh, f.Y);
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    float acc = fmul(f.Y[0], sh(ch));
-#pragma unroll
-    for (int k = 1; k < 16; ++k)
-      if (k < n_sh) acc = fadd(acc, fmul(f.Y[k], sh(3 * k + ch)));
-    f.col_raw[ch] = fadd(acc, 0.5f);
-    f.col[ch] = fmaxf(f.col_raw[ch], 0.f);
-  }
+  sh_colour(sh, n_sh, f.Y, f.col_raw, f.col, gcol, wk);
   f.opac = pre.opac;
 }
 
@@ -215,24 +208,12 @@ __device__ __forceinline__ void gsp2_from_moments(const Proj2D& f, float* gs) {
 template <class SH, class ShAdd>
 __device__ __forceinline__ void project2d_backward(const PointIn& pt, const Pre2D& pre, const SH& sh,
                                                    const bs_camera& c, int n_sh, const Proj2D& f,
-                                                   const float gsp[15], float* g, float GR[9], ShAdd sh_add) {
+                                                   const float gsp[15], float* g, float GR[9], ShAdd sh_add,
+                                                   const float* wk_pre = nullptr) {
   if (!f.valid) return;
   // ---- colour -> sh, dir (as 3DGS)
-  float dc[3];
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) dc[ch] = f.col_raw[ch] >= 0.f ? gsp[12 + ch] : 0.f;
   float wk[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) wk[k] = 0.f;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    if (k >= n_sh) break;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      sh_add(3 * k + ch, f.Y[k] * dc[ch]);
-      wk[k] += dc[ch] * sh(3 * k + ch);
-    }
-  }
+  sh_colour_backward(sh, n_sh, f.Y, f.col_raw, gsp + 12, wk_pre, wk, sh_add);
   float gdir[3];
   sh_dir_grad(f.dir, n_sh, wk, gdir);
   const float dd = f.dir[0] * gdir[0] + f.dir[1] * gdir[1] + f.dir[2] * gdir[2];

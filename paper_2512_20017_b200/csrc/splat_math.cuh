@@ -113,9 +113,13 @@ __device__ __forceinline__ void sh_basis(const float dir[3], int n_sh, float Y[1
 
 // SH coefficient accessors: from the registers of a loaded point, or straight
 // from the plane-major parameters (L1-resident) to keep 48 registers free.
+// load4(q): coefficients 4q .. 4q + 3 (one float4 plane entry).
 struct ShRegs {
   const float* sh;
   __device__ __forceinline__ float operator()(int f) const { return sh[f]; }
+  __device__ __forceinline__ float4 load4(int q) const {
+    return make_float4(sh[4 * q], sh[4 * q + 1], sh[4 * q + 2], sh[4 * q + 3]);
+  }
 };
 struct ShPlanes {
   const float* params;  // plane-major float4 planes as floats
@@ -123,7 +127,69 @@ struct ShPlanes {
   __device__ __forceinline__ float operator()(int f) const {
     return __ldg(params + ((int64_t)(3 + (f >> 2)) * S + i) * 4 + (f & 3));
   }
+  __device__ __forceinline__ float4 load4(int q) const {
+    return __ldg(reinterpret_cast<const float4*>(params) + (int64_t)(3 + q) * S + i);
+  }
 };
+
+// View-dependent colour from the SH coefficients (flat index f = 3k + ch):
+// each channel sums Y_k sh_{k,ch} in k order (round-to-nearest, as the
+// reference); coefficients are read as float4 plane entries.  With gcol
+// (the colour gradient of this view) it also returns the direction weights
+// wk[k] = sum_ch gcol[ch] sh_{k,ch} the backward needs when no channel is
+// clamped, so the backward does not read the coefficients a second time.
+template <class SH>
+__device__ __forceinline__ void sh_colour(const SH& sh, int n_sh, const float Y[16], float col_raw[3], float col[3],
+                                          const float* gcol, float* wk) {
+  float acc[3] = {0.f, 0.f, 0.f};
+  if (wk) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) wk[k] = 0.f;
+  }
+#pragma unroll
+  for (int q = 0; q < 12; ++q) {
+    if (4 * q >= 3 * n_sh) break;
+    const float4 v4 = sh.load4(q);
+    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int f = 4 * q + e, k = f / 3, ch = f % 3;
+      if (k < n_sh) {
+        const float t = fmul(Y[k], v[e]);
+        acc[ch] = k == 0 ? t : fadd(acc[ch], t);
+        if (wk) wk[k] = __fmaf_rn(gcol[ch], v[e], wk[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    col_raw[ch] = fadd(acc[ch], 0.5f);
+    col[ch] = fmaxf(col_raw[ch], 0.f);
+  }
+}
+
+// Backward of the colour clamp into the SH coefficients and the direction
+// weights wk (see sh_colour; wk_pre is used when no channel was clamped).
+template <class SH, class ShAdd>
+__device__ __forceinline__ void sh_colour_backward(const SH& sh, int n_sh, const float Y[16], const float col_raw[3],
+                                                   const float gcol[3], const float* wk_pre, float wk[16],
+                                                   ShAdd sh_add) {
+  float dc[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) dc[ch] = col_raw[ch] >= 0.f ? gcol[ch] : 0.f;
+  const bool fast = wk_pre != nullptr && col_raw[0] >= 0.f && col_raw[1] >= 0.f && col_raw[2] >= 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) wk[k] = fast ? wk_pre[k] : 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (k >= n_sh) break;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      sh_add(3 * k + ch, Y[k] * dc[ch]);
+      if (!fast) wk[k] = __fmaf_rn(dc[ch], sh(3 * k + ch), wk[k]);
+    }
+  }
+}
 
 // Scales, normalised quaternion and its rotation matrix of a point (shared by
 // the 3DGS and 2DGS models; explicit round-to-nearest ops).
@@ -226,7 +292,8 @@ __device__ __forceinline__ void point_pre_backward(const PointIn& pt, const floa
 
 template <class SH>
 __device__ __forceinline__ void project_forward_t(const PointIn& pt, const PointPre& pre, const SH& sh,
-                                                  const bs_camera& c, int n_sh, ProjFwd& f) {
+                                                  const bs_camera& c, int n_sh, ProjFwd& f,
+                                                  const float* gcol = nullptr, float* wk = nullptr) {
   // camera frame: q = Rcw (p - pos)
 #pragma unroll
   for (int k = 0; k < 3; ++k) f.d[k] = fsub(pt.p[k], c.pos[k]);
@@ -299,15 +366,7 @@ __device__ __forceinline__ void project_forward_t(const PointIn& pt, const Point
 #pragma unroll
   for (int k = 0; k < 3; ++k) f.dir[k] = fdiv(f.d[k], f.len);
   sh_basis(f.dir, n_sh, f.Y);
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    float acc = fmul(f.Y[0], sh(ch));
-#pragma unroll
-    for (int k = 1; k < 16; ++k)
-      if (k < n_sh) acc = fadd(acc, fmul(f.Y[k], sh(3 * k + ch)));
-    f.col_raw[ch] = fadd(acc, 0.5f);
-    f.col[ch] = fmaxf(f.col_raw[ch], 0.f);
-  }
+  sh_colour(sh, n_sh, f.Y, f.col_raw, f.col, gcol, wk);
   f.opac = pre.opac;
 }
 
@@ -392,24 +451,12 @@ __device__ __forceinline__ void sh_dir_grad(const float dir[3], int n_sh, const 
 template <class SH, class ShAdd>
 __device__ __forceinline__ void project_backward_t(const PointIn& pt, const PointPre& pre, const SH& sh,
                                                    const bs_camera& c, int n_sh, const ProjFwd& f,
-                                                   const float gsp[9], float* g, float gS[6], ShAdd sh_add) {
+                                                   const float gsp[9], float* g, float gS[6], ShAdd sh_add,
+                                                   const float* wk_pre = nullptr) {
   if (!f.valid) return;
   // ---- colour -> sh, dir
-  float dc[3];
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) dc[ch] = f.col_raw[ch] >= 0.f ? gsp[6 + ch] : 0.f;
   float wk[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) wk[k] = 0.f;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    if (k >= n_sh) break;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      sh_add(3 * k + ch, f.Y[k] * dc[ch]);
-      wk[k] += dc[ch] * sh(3 * k + ch);
-    }
-  }
+  sh_colour_backward(sh, n_sh, f.Y, f.col_raw, gsp + 6, wk_pre, wk, sh_add);
   float gdir[3];
   sh_dir_grad(f.dir, n_sh, wk, gdir);
   const float dd = f.dir[0] * gdir[0] + f.dir[1] * gdir[1] + f.dir[2] * gdir[2];
