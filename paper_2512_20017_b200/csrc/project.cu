@@ -14,6 +14,10 @@ namespace bs {
 namespace {
 
 constexpr int kProjThreads = 256;
+#ifndef BS_ADAM_BATCH
+#define BS_ADAM_BATCH 3
+#endif
+constexpr int kAdamBatch = BS_ADAM_BATCH;  // parameter planes per batch of Adam loads in the fused kernel
 constexpr int kProjWarps = kProjThreads / 32;
 constexpr int kMaxViews = 32;
 
@@ -366,17 +370,17 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
       // Adam over the 15 planes, 3 planes per batch: all 15 loads of a batch
       // are issued before its first store (memory-level parallelism)
 #pragma unroll
-      for (int p0 = 0; p0 < BS_PARAM_PLANES; p0 += 3) {
-        float4 pp[3], mm[3], vv[3];
+      for (int p0 = 0; p0 < BS_PARAM_PLANES; p0 += kAdamBatch) {
+        float4 pp[kAdamBatch], mm[kAdamBatch], vv[kAdamBatch];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
+        for (int k = 0; k < kAdamBatch; ++k) {
           const int64_t t = (p0 + k) * a.S + i;
           pp[k] = params[t];
           mm[k] = m[t];
           vv[k] = v[t];
         }
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
+        for (int k = 0; k < kAdamBatch; ++k) {
           const int p = p0 + k;
           const int64_t t = p * a.S + i;
           const float4 gg = p < 3 ? make_float4(g12[4 * p], g12[4 * p + 1], g12[4 * p + 2], g12[4 * p + 3])
