@@ -217,20 +217,39 @@ _STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_ke
                  "project_bwd_adam": "project_bwd_adam_kernel", "project": "project_fwd_kernel", "cull": "cull_kernel"}
 
 
-def kernel_traffic(stage, model="3dgs"):
-    """DRAM bytes (read + write) of one launch of the stage's kernel from the
-    committed ncu --set full summary of the same configuration, or None."""
+def kernel_profile(stage, model="3dgs"):
+    """Entry of the committed ncu --set full summary (profiles/r1_kernel_traffic.json)
+    for one launch of the stage's kernel in the same configuration, or {}."""
     path = os.path.join(ROOT, "profiles", "r1_kernel_traffic.json")
     try:
         table = json.load(open(path))
     except Exception:
-        return None
+        return {}
     key = stage.replace("raster_", "raster2d_") if model == "2dgs" and stage.startswith("raster_") else stage
     prefix = _STAGE_KERNEL.get(key, key)
-    for k, v in table.items():
-        if k.startswith(prefix):
-            return v.get("dram_traffic_bytes")
-    return None
+    model_tag = "Model2" if model == "2dgs" else "Model3"
+    hits = [v for k, v in table.items() if k.startswith(prefix)]
+    tagged = [v for k, v in table.items() if k.startswith(prefix) and model_tag in k]
+    return (tagged or hits or [{}])[0]
+
+
+def kernel_traffic(stage, model="3dgs"):
+    """DRAM bytes (read + write) of one launch of the stage's kernel, or None."""
+    return kernel_profile(stage, model).get("dram_traffic_bytes")
+
+
+def issue_roofline(stage, ms, sm_mhz, model="3dgs"):
+    """The raster kernels' real bound: warp-instruction issue.  Achieved =
+    the launch's executed warp instructions (ncu, same configuration) over the
+    launch time measured here; peak = 148 SMs x 4 schedulers x 1 issue/clock
+    at the SM clock sampled during the timed region."""
+    n = kernel_profile(stage, model).get("warp_instructions")
+    if not n or not ms or not sm_mhz:
+        return None
+    ach = n / (ms / 1000.0) / 1e9
+    peak = 148 * 4 * sm_mhz * 1e6 / 1e9
+    return {"bound": "issue", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "G warp-instr/s",
+            "frac": round(ach / peak, 4), "warp_instructions": n}
 
 
 def kernel_bytes(stage, last, S, B, model="3dgs"):
@@ -405,6 +424,7 @@ def run_ours(args, cfg):
     last = dict(tr.last, H=H, W=W, n_visible_points=int(tr.last.get("n_visible_points", tr.S)))
     dom = max(stage_ms, key=stage_ms.get) if stage_ms else None
     roof = None
+    clk_summary = clk.summary()
     if dom:
         nbytes = kernel_bytes(dom, dict(last, n_inst=int(np.mean(inst)), n_rows=int(np.mean(rows))), tr.S, B,
                               model)
@@ -412,8 +432,10 @@ def run_ours(args, cfg):
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": (ach / peak) if ach else None, "traffic": kernel_traffic(dom, model), "peak_kind": peak_kind,
                 "bytes_per_launch": nbytes, "ms_per_launch": stage_ms[dom],
-                "note": "raster kernels are FP32/issue-bound (ncu: issue slots ~80-90% busy), not HBM-bound; "
-                        "traffic = ncu dram read+write bytes of one launch (profiles/r1_kernel_traffic.json)"}
+                "issue": issue_roofline(dom, stage_ms[dom], clk_summary.get("sm_mhz"), model),
+                "note": "raster kernels are FP32/issue-bound (ncu: issue slots ~80-90% busy), not HBM-bound: "
+                        "see `issue`; traffic = ncu dram read+write bytes of one launch "
+                        "(profiles/r1_kernel_traffic.json)"}
     stages = {}
     for k, v in stage_ms.items():
         nb = kernel_bytes(k, dict(last, n_inst=int(np.mean(inst)), n_rows=int(np.mean(rows))), tr.S, B, model)
@@ -440,7 +462,7 @@ def run_ours(args, cfg):
             "stages": stages,
             "instances_per_step": int(np.mean(inst)), "splat_rows_per_step": int(np.mean(rows)),
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "clocks": clk_summary,
             "cpu_baseline": cpu,
             "setup_s": round(setup_s, 1),
             "final_loss": None if loss_host is None else [round(float(x), 5) for x in loss_host],
