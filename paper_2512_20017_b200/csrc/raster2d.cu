@@ -33,6 +33,12 @@ constexpr float kLog2e2 = 1.4426950408889634f;
 #ifndef BS_SPARSE2_LANES
 #define BS_SPARSE2_LANES 12  // swept on B200 (C3, 128-bit REDs): 5 5.74, 8 5.53, 12 5.38, 16 5.41 ms
 #endif
+#ifndef BS_R2_FWD_CTAS
+#define BS_R2_FWD_CTAS 1
+#endif
+#ifndef BS_R2_BWD_CTAS
+#define BS_R2_BWD_CTAS 3
+#endif
 constexpr int kSparse2 = BS_SPARSE2_LANES;  // contributing lanes handled with direct REDs
 
 __device__ __forceinline__ float ex2a(float x) {
@@ -189,7 +195,7 @@ struct Px2 {
   bool done;
 };
 
-__global__ void __launch_bounds__(kT2) raster2d_fwd_kernel(R2Args a, const float* __restrict__ sp,
+__global__ void __launch_bounds__(kT2, BS_R2_FWD_CTAS) raster2d_fwd_kernel(R2Args a, const float* __restrict__ sp,
                                                             const uint32_t* __restrict__ inst_rows,
                                                             const int2* __restrict__ ranges, float* __restrict__ image,
                                                             float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
@@ -311,7 +317,7 @@ struct PxB2 {
 };
 
 template <bool kBg>
-__global__ void __launch_bounds__(kT2, 3) raster2d_bwd_kernel(
+__global__ void __launch_bounds__(kT2, BS_R2_BWD_CTAS) raster2d_bwd_kernel(
     R2Args a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
     const float* __restrict__ image, const float* __restrict__ final_T, const int32_t* __restrict__ n_contrib,
     const float* __restrict__ grad_image, const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view,
