@@ -34,7 +34,7 @@ constexpr float kLog2e2 = 1.4426950408889634f;
 #define BS_SPARSE2_LANES 12  // swept on B200 (C3, 128-bit REDs): 5 5.74, 8 5.53, 12 5.38, 16 5.41 ms
 #endif
 #ifndef BS_R2_FWD_CTAS
-#define BS_R2_FWD_CTAS 1
+#define BS_R2_FWD_CTAS 4
 #endif
 #ifndef BS_R2_BWD_CTAS
 #define BS_R2_BWD_CTAS 3
