@@ -8,9 +8,12 @@
 //  3. bs_bin_tiles_scatter per (row, tile): key = (f32bits(depth) << 32) | row
 //                          written at an atomically claimed slot of the bucket
 //                          (arbitrary order inside the bucket)
-//  4. bs_bin_tiles_sort    one CTA per bucket: bitonic sort of the bucket's
-//                          keys in shared memory; the row (low 32 bits) of
-//                          the sorted keys is the tile list
+//  4. bs_bin_tiles_sort    by bucket size: one warp per bucket with a
+//                          register bitonic network (<= 256 and 513..1024
+//                          keys) or a register + shared-memory merge sort
+//                          (257..512, the common class), one CTA per larger
+//                          bucket; the row (low 32 bits) of the sorted keys
+//                          is the tile list
 // Every key is unique (rows are), so the per-tile order -- ascending depth,
 // ties by ascending row -- is a total order: deterministic and identical to
 // a stable depth sort of the rows followed by a stable tile sort (bin.cu),
@@ -261,6 +264,103 @@ __device__ __forceinline__ void sort_bucket_regs(const uint64_t* __restrict__ ke
   }
 }
 
+// Buckets of 257..512 keys (the common class at 1080p): one warp per bucket,
+// merge sort instead of the 45-step bitonic network.  Each lane sorts its 16
+// keys in registers (10-step in-lane network), then five rounds merge runs of
+// 16, 32, ..., 256 through warp-private shared memory: lane l produces merged
+// outputs [16 l, 16 l + 16) of its pair of runs -- the split point by a
+// merge-path binary search, then 16 sequential merge steps.  Padding keys are
+// ~0 (sort last; every real key is unique).  Loads and the row stores go
+// through the same buffer so global accesses stay coalesced.
+constexpr int kMergeE = 16;                       // keys per lane
+constexpr int kMergeM = 32 * kMergeE;             // 512 keys per bucket
+constexpr int kMergeWords = kMergeM + kMergeM / 16;  // + one pad word per 16 (bank skew)
+
+__device__ __forceinline__ int mpad(int i) { return i + (i >> 4); }
+
+__device__ __forceinline__ void cas64(uint64_t& a, uint64_t& b) {
+  const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+  a = lo;
+  b = hi;
+}
+
+__device__ __forceinline__ void warp_merge_sort512(const uint64_t* __restrict__ keys, int start, int n,
+                                                   uint32_t* __restrict__ rows, uint64_t* sm, int lane) {
+  // coalesced load into the buffer, then 16 consecutive keys per lane
+  for (int i = lane; i < kMergeM; i += 32) sm[mpad(i)] = i < n ? __ldg(keys + start + i) : ~0ull;
+  __syncwarp();
+  uint64_t x[kMergeE];
+#pragma unroll
+  for (int e = 0; e < kMergeE; ++e) x[e] = sm[mpad(lane * kMergeE + e)];
+  // in-lane bitonic sort (ascending)
+#pragma unroll
+  for (int k = 2; k <= kMergeE; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int e = 0; e < kMergeE; ++e) {
+        const int p = e ^ j;
+        if (p > e) {
+          if ((e & k) == 0) cas64(x[e], x[p]);
+          else cas64(x[p], x[e]);
+        }
+      }
+  // merge rounds: runs of L -> 2L
+#pragma unroll 1
+  for (int L = kMergeE; L < kMergeM; L <<= 1) {
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < kMergeE; ++e) sm[mpad(lane * kMergeE + e)] = x[e];
+    __syncwarp();
+    const int d0 = lane * kMergeE;
+    const int base = d0 & ~(2 * L - 1);
+    const int d = d0 - base;  // outputs of this pair before this lane's first
+    const int a0 = base, b0 = base + L;
+    int lo = max(0, d - L), hi = min(d, L);
+    while (lo < hi) {  // merge path: A elements among the first d outputs
+      const int mid = (lo + hi) >> 1;
+      if (sm[mpad(a0 + mid)] <= sm[mpad(b0 + d - 1 - mid)]) lo = mid + 1;
+      else hi = mid;
+    }
+    int i = lo, j = d - lo;
+    uint64_t a = i < L ? sm[mpad(a0 + i)] : ~0ull;
+    uint64_t b = j < L ? sm[mpad(b0 + j)] : ~0ull;
+#pragma unroll
+    for (int e = 0; e < kMergeE; ++e) {
+      const bool take_a = j >= L || (i < L && a <= b);
+      x[e] = take_a ? a : b;
+      if (take_a) {
+        ++i;
+        a = i < L ? sm[mpad(a0 + i)] : ~0ull;
+      } else {
+        ++j;
+        b = j < L ? sm[mpad(b0 + j)] : ~0ull;
+      }
+    }
+  }
+  // rows (low 32 bits) out through the buffer, coalesced
+  __syncwarp();
+  uint32_t* sr = reinterpret_cast<uint32_t*>(sm);
+#pragma unroll
+  for (int e = 0; e < kMergeE; ++e) sr[mpad(lane * kMergeE + e)] = (uint32_t)x[e];
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) rows[start + i] = sr[mpad(i)];
+}
+
+__global__ void __launch_bounds__(32 * kSortWarpsPerCta) sort_tiles_merge_kernel(const uint64_t* __restrict__ keys,
+                                                                                  const int2* __restrict__ ranges,
+                                                                                  int nb, int cap,
+                                                                                  uint32_t* __restrict__ rows) {
+  __shared__ uint64_t s_buf[kSortWarpsPerCta][kMergeWords];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kSortWarpsPerCta + w;
+  if (b >= nb) return;
+  const int2 rg = ranges[b];
+  const int n = rg.y - rg.x;
+  if (n <= kMergeM / 2 || n > kMergeM || n > cap) return;
+  warp_merge_sort512(keys, rg.x, n, rows, s_buf[w], lane);
+}
+
 // One launch per size class (n <= 256, <= 512, <= 1024) so that each class
 // is compiled with the registers of its own largest network (the 1024-key
 // network needs 64 key registers per lane; the common 257..512 class half of
@@ -399,8 +499,13 @@ extern "C" int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* r
   const int2* rg = reinterpret_cast<const int2*>(ranges);
   sort_tiles_warp_kernel<8><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
   BS_LAUNCH_CHECK("sort_tiles_warp_kernel<8>");
+#ifdef BS_SORT_BITONIC16
   sort_tiles_warp_kernel<16><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
   BS_LAUNCH_CHECK("sort_tiles_warp_kernel<16>");
+#else
+  sort_tiles_merge_kernel<<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+  BS_LAUNCH_CHECK("sort_tiles_merge_kernel");
+#endif
   sort_tiles_warp_kernel<32><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
   BS_LAUNCH_CHECK("sort_tiles_warp_kernel<32>");
   if (smem_cap > kWarpCap) {
