@@ -9,11 +9,11 @@
 //                          written at an atomically claimed slot of the bucket
 //                          (arbitrary order inside the bucket)
 //  4. bs_bin_tiles_sort    by bucket size: one warp per bucket with a
-//                          register bitonic network (<= 256 and 513..1024
-//                          keys) or a register + shared-memory merge sort
-//                          (257..512, the common class), one CTA per larger
-//                          bucket; the row (low 32 bits) of the sorted keys
-//                          is the tile list
+//                          register bitonic network (<= 256 keys) or a
+//                          register + shared-memory merge sort (257..1024,
+//                          the common classes), one CTA per larger bucket;
+//                          the row (low 32 bits) of the sorted keys is the
+//                          tile list
 // Every key is unique (rows are), so the per-tile order -- ascending depth,
 // ties by ascending row -- is a total order: deterministic and identical to
 // a stable depth sort of the rows followed by a stable tile sort (bin.cu),
@@ -207,6 +207,10 @@ __global__ void scatter_tiles_kernel(BinGeom g, int32_t* __restrict__ cursor, ui
 // no dependent-load chain.
 constexpr int kWarpCap = 1024;
 constexpr int kSortWarpsPerCta = 8;
+#ifndef BS_SORT_BITONIC256
+#define BS_SORT_BITONIC256 1  // measured: 10 us faster on C2 than the E = 8 merge sort
+#endif
+constexpr bool kBitonic256 = BS_SORT_BITONIC256;  // 129..256 keys: bitonic network instead of merge sort
 
 __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
   const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, m);
@@ -264,19 +268,16 @@ __device__ __forceinline__ void sort_bucket_regs(const uint64_t* __restrict__ ke
   }
 }
 
-// Buckets of 257..512 keys (the common class at 1080p): one warp per bucket,
-// merge sort instead of the 45-step bitonic network.  Each lane sorts its 16
-// keys in registers (10-step in-lane network), then five rounds merge runs of
-// 16, 32, ..., 256 through warp-private shared memory: lane l produces merged
-// outputs [16 l, 16 l + 16) of its pair of runs -- the split point by a
-// merge-path binary search, then 16 sequential merge steps.  Padding keys are
-// ~0 (sort last; every real key is unique).  Loads and the row stores go
-// through the same buffer so global accesses stay coalesced.
-constexpr int kMergeE = 16;                       // keys per lane
-constexpr int kMergeM = 32 * kMergeE;             // 512 keys per bucket
-constexpr int kMergeWords = kMergeM + kMergeM / 16;  // + one pad word per 16 (bank skew)
-
-__device__ __forceinline__ int mpad(int i) { return i + (i >> 4); }
+// Buckets of 129..1024 keys (the common classes): one warp per bucket, merge
+// sort instead of a bitonic network (45 steps over 16 keys per lane for 512).
+// Each lane sorts its E keys in registers (in-lane bitonic network), then
+// log2(32) = 5 rounds merge runs of E, 2E, ..., 16E through warp-private
+// shared memory: lane l produces merged outputs [E l, E l + E) of its pair
+// of runs -- the split point by a merge-path binary search, then E
+// sequential merge steps.  Padding keys are ~0 (sort last; every real key is
+// unique).  Loads and the row stores go through the same buffer so global
+// accesses stay coalesced.
+__device__ __forceinline__ int mpad(int i) { return i + (i >> 4); }  // one pad word per 16: bank skew
 
 __device__ __forceinline__ void cas64(uint64_t& a, uint64_t& b) {
   const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
@@ -284,35 +285,34 @@ __device__ __forceinline__ void cas64(uint64_t& a, uint64_t& b) {
   b = hi;
 }
 
-__device__ __forceinline__ void warp_merge_sort512(const uint64_t* __restrict__ keys, int start, int n,
-                                                   uint32_t* __restrict__ rows, uint64_t* sm, int lane) {
-  // coalesced load into the buffer, then 16 consecutive keys per lane
-  for (int i = lane; i < kMergeM; i += 32) sm[mpad(i)] = i < n ? __ldg(keys + start + i) : ~0ull;
+template <int E>
+__device__ __forceinline__ void warp_merge_sort(const uint64_t* __restrict__ keys, int start, int n,
+                                                uint32_t* __restrict__ rows, uint64_t* sm, int lane) {
+  constexpr int M = 32 * E;
+  for (int i = lane; i < M; i += 32) sm[mpad(i)] = i < n ? __ldg(keys + start + i) : ~0ull;
   __syncwarp();
-  uint64_t x[kMergeE];
+  uint64_t x[E];
 #pragma unroll
-  for (int e = 0; e < kMergeE; ++e) x[e] = sm[mpad(lane * kMergeE + e)];
-  // in-lane bitonic sort (ascending)
+  for (int e = 0; e < E; ++e) x[e] = sm[mpad(lane * E + e)];
 #pragma unroll
-  for (int k = 2; k <= kMergeE; k <<= 1)
+  for (int k = 2; k <= E; k <<= 1)
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1)
 #pragma unroll
-      for (int e = 0; e < kMergeE; ++e) {
+      for (int e = 0; e < E; ++e) {
         const int p = e ^ j;
         if (p > e) {
           if ((e & k) == 0) cas64(x[e], x[p]);
           else cas64(x[p], x[e]);
         }
       }
-  // merge rounds: runs of L -> 2L
 #pragma unroll 1
-  for (int L = kMergeE; L < kMergeM; L <<= 1) {
+  for (int L = E; L < M; L <<= 1) {
     __syncwarp();
 #pragma unroll
-    for (int e = 0; e < kMergeE; ++e) sm[mpad(lane * kMergeE + e)] = x[e];
+    for (int e = 0; e < E; ++e) sm[mpad(lane * E + e)] = x[e];
     __syncwarp();
-    const int d0 = lane * kMergeE;
+    const int d0 = lane * E;
     const int base = d0 & ~(2 * L - 1);
     const int d = d0 - base;  // outputs of this pair before this lane's first
     const int a0 = base, b0 = base + L;
@@ -326,7 +326,7 @@ __device__ __forceinline__ void warp_merge_sort512(const uint64_t* __restrict__ 
     uint64_t a = i < L ? sm[mpad(a0 + i)] : ~0ull;
     uint64_t b = j < L ? sm[mpad(b0 + j)] : ~0ull;
 #pragma unroll
-    for (int e = 0; e < kMergeE; ++e) {
+    for (int e = 0; e < E; ++e) {
       const bool take_a = j >= L || (i < L && a <= b);
       x[e] = take_a ? a : b;
       if (take_a) {
@@ -338,27 +338,28 @@ __device__ __forceinline__ void warp_merge_sort512(const uint64_t* __restrict__ 
       }
     }
   }
-  // rows (low 32 bits) out through the buffer, coalesced
   __syncwarp();
   uint32_t* sr = reinterpret_cast<uint32_t*>(sm);
 #pragma unroll
-  for (int e = 0; e < kMergeE; ++e) sr[mpad(lane * kMergeE + e)] = (uint32_t)x[e];
+  for (int e = 0; e < E; ++e) sr[mpad(lane * E + e)] = (uint32_t)x[e];
   __syncwarp();
   for (int i = lane; i < n; i += 32) rows[start + i] = sr[mpad(i)];
 }
 
-__global__ void __launch_bounds__(32 * kSortWarpsPerCta) sort_tiles_merge_kernel(const uint64_t* __restrict__ keys,
-                                                                                  const int2* __restrict__ ranges,
-                                                                                  int nb, int cap,
-                                                                                  uint32_t* __restrict__ rows) {
-  __shared__ uint64_t s_buf[kSortWarpsPerCta][kMergeWords];
+// Size class (16 E, 32 E] -- E = 8: 129..256, 16: 257..512, 32: 513..1024.
+template <int E, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) sort_tiles_merge_kernel(const uint64_t* __restrict__ keys,
+                                                                       const int2* __restrict__ ranges, int nb,
+                                                                       int cap, uint32_t* __restrict__ rows) {
+  constexpr int kWords = 32 * E + 2 * E;  // mpad(32 E - 1) + 1
+  __shared__ uint64_t s_buf[WARPS][kWords];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * kSortWarpsPerCta + w;
+  const int b = blockIdx.x * WARPS + w;
   if (b >= nb) return;
   const int2 rg = ranges[b];
   const int n = rg.y - rg.x;
-  if (n <= kMergeM / 2 || n > kMergeM || n > cap) return;
-  warp_merge_sort512(keys, rg.x, n, rows, s_buf[w], lane);
+  if (n <= 16 * E || n > 32 * E || n > cap) return;
+  warp_merge_sort<E>(keys, rg.x, n, rows, s_buf[w], lane);
 }
 
 // One launch per size class (n <= 256, <= 512, <= 1024) so that each class
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(32 * kSortWarpsPerCta) sort_tiles_merge_kernel
 // network needs 64 key registers per lane; the common 257..512 class half of
 // that), instead of the whole kernel paying for the largest one.
 template <int EMAX>
-__global__ void __launch_bounds__(32 * kSortWarpsPerCta) sort_tiles_warp_kernel(const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(32 * kSortWarpsPerCta, 4) sort_tiles_warp_kernel(const uint64_t* __restrict__ keys,
                                                                                  const int2* __restrict__ ranges,
                                                                                  int nb, int cap,
                                                                                  uint32_t* __restrict__ rows) {
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(32 * kSortWarpsPerCta) sort_tiles_warp_kernel(
     if (n <= 32) sort_bucket_regs<1>(keys, rg.x, n, rows, lane);
     else if (n <= 64) sort_bucket_regs<2>(keys, rg.x, n, rows, lane);
     else if (n <= 128) sort_bucket_regs<4>(keys, rg.x, n, rows, lane);
-    else sort_bucket_regs<8>(keys, rg.x, n, rows, lane);
+    else if constexpr (EMAX >= 8) sort_bucket_regs<8>(keys, rg.x, n, rows, lane);
   } else {
     sort_bucket_regs<EMAX>(keys, rg.x, n, rows, lane);
   }
@@ -497,17 +498,19 @@ extern "C" int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* r
   cudaStream_t s = as_stream(stream);
   const int grid = (n_buckets + kSortWarpsPerCta - 1) / kSortWarpsPerCta;
   const int2* rg = reinterpret_cast<const int2*>(ranges);
-  sort_tiles_warp_kernel<8><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
-  BS_LAUNCH_CHECK("sort_tiles_warp_kernel<8>");
-#ifdef BS_SORT_BITONIC16
-  sort_tiles_warp_kernel<16><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
-  BS_LAUNCH_CHECK("sort_tiles_warp_kernel<16>");
-#else
-  sort_tiles_merge_kernel<<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
-  BS_LAUNCH_CHECK("sort_tiles_merge_kernel");
-#endif
-  sort_tiles_warp_kernel<32><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
-  BS_LAUNCH_CHECK("sort_tiles_warp_kernel<32>");
+  // n <= 128 (and, with kBitonic256, 129..256): register bitonic networks
+  constexpr int kSmallE = kBitonic256 ? 8 : 4;
+  sort_tiles_warp_kernel<kSmallE><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+  BS_LAUNCH_CHECK("sort_tiles_warp_kernel<small>");
+  if (!kBitonic256) {
+    sort_tiles_merge_kernel<8, 8><<<grid, 32 * 8, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+    BS_LAUNCH_CHECK("sort_tiles_merge_kernel<8>");
+  }
+  sort_tiles_merge_kernel<16, 8><<<grid, 32 * 8, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+  BS_LAUNCH_CHECK("sort_tiles_merge_kernel<16>");
+  const int grid4 = (n_buckets + 3) / 4;
+  sort_tiles_merge_kernel<32, 4><<<grid4, 32 * 4, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+  BS_LAUNCH_CHECK("sort_tiles_merge_kernel<32>");
   if (smem_cap > kWarpCap) {
     sort_tiles_kernel<<<n_buckets, kSortThreads, 0, s>>>(inst_keys, reinterpret_cast<const int2*>(ranges), smem_cap,
                                                          inst_rows);

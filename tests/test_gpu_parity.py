@@ -472,3 +472,27 @@ def test_train_step_temporal_culling_4dgs(cuda):
         assert np.array_equal(((mask >> s) & 1).astype(bool), ref), f"view {v}"
         assert rows[s] == ref.sum()
     assert 0 < rows.sum() < len(batch) * tr.S  # the time test actually removes points
+
+
+@pytest.mark.parametrize("sizes", [[0, 1, 2, 31, 32, 33, 255, 256, 257, 300, 511, 512, 513, 1000, 1024, 1025, 4096],
+                                   [257] * 40 + [512] * 40 + [384] * 40])
+def test_bucket_sort_every_size_class(cuda, sizes):
+    """bs_bin_tiles_sort on random unique (depth bits << 32 | row) keys, every
+    size class (empty, single, in-register bitonic, merge sort 257..512,
+    bitonic 513..1024, CTA sort): rows in ascending key order, bucket by bucket."""
+    rng = np.random.default_rng(len(sizes))
+    total = int(sum(sizes))
+    depth = rng.random(total, dtype=np.float32) * 100 + 0.1
+    depth[::7] = depth[0]  # ties in depth: broken by the row
+    rows = rng.permutation(np.arange(total, dtype=np.uint64) + 1000)
+    keys = (depth.view(np.uint32).astype(np.uint64) << np.uint64(32)) | rows
+    starts = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int32)
+    ranges = np.stack([starts, starts + np.asarray(sizes, dtype=np.int32)], axis=1).astype(np.int32)
+    kd = torch.as_tensor(keys.view(np.int64), device="cuda")
+    rd = torch.as_tensor(ranges.reshape(-1), device="cuda")
+    out = torch.full((max(total, 1),), -1, dtype=torch.int32, device="cuda")
+    nat.call("bs_bin_tiles_sort", nat.ptr(kd), nat.ptr(rd), len(sizes), 4096, nat.ptr(out), nat.stream_handle())
+    got = out[:total].cpu().numpy().view(np.uint32)
+    for s0, n in zip(starts, sizes):
+        want = (np.sort(keys[s0:s0 + n]) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+        assert np.array_equal(got[s0:s0 + n], want), n
