@@ -314,7 +314,9 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
                                                                            float4* params,
                                                                            float4* __restrict__ m,
                                                                            float4* __restrict__ v) {
-  extern __shared__ float s_gsh[];  // [48][kProjThreads]
+  // [48][kProjThreads] SH gradients, then [12][kProjThreads] float4 SH values
+  extern __shared__ float s_gsh[];
+  float4* s_sh4 = reinterpret_cast<float4*>(s_gsh + 48 * kProjThreads);
   __shared__ uint32_t s_bal[kProjWarps * kMaxViews];
   __shared__ int s_run[kMaxViews];
   __shared__ bs_camera s_cam[kMaxViews];
@@ -332,10 +334,12 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const bool ok = i < end;
-    // Prefetches that cost no registers: the block's parameter and moment
-    // planes into L2 by the bulk-copy engine (one contiguous request per
-    // (array, plane)) for the Adam update, and this point's SH planes into
-    // L1 for the per-view math that reads them on use.
+    // Copies that cost no registers: the block's parameter and moment planes
+    // into L2 by the bulk-copy engine (one contiguous request per (array,
+    // plane)) for the Adam update, and this point's SH coefficients into its
+    // own shared-memory column (cp.async) for the per-view math, which then
+    // reads them at shared-memory latency instead of one dependent global
+    // load per float4.
     if (threadIdx.x < 3 * BS_PARAM_PLANES) {
       const int arr = threadIdx.x / BS_PARAM_PLANES, pl = threadIdx.x % BS_PARAM_PLANES;
       const float4* base4 = arr == 0 ? params : (arr == 1 ? m : v);
@@ -343,11 +347,15 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base4 + (int64_t)pl * a.S + b0), "r"(bytes)
                    : "memory");
     }
+    const int sh_q = (3 * a.n_sh + 3) / 4;  // float4 entries holding this degree's coefficients
     if (ok) {
-#pragma unroll
-      for (int k = 3; k < BS_PARAM_PLANES; ++k)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(params + (int64_t)k * a.S + i));
+      for (int q = 0; q < sh_q; ++q) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_sh4 + q * kProjThreads + threadIdx.x);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(params + (int64_t)(3 + q) * a.S + i)
+                     : "memory");
+      }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     const uint32_t mask = ok ? a.mask[i] : 0u;
     rk.round(mask, B);
     if (ok && !(c.selective && mask == 0u)) {
@@ -362,8 +370,9 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
       for (int f = 0; f < 48; ++f) my_sh[f * kProjThreads] = 0.f;
       if (mask) {
         PointIn pt;
-        load_point(a.params, a.S, i, 0, pt);  // geometry planes only; SH read from L1 on use
-        const ShPlanes sh{reinterpret_cast<const float*>(a.params), a.S, i};
+        load_point(a.params, a.S, i, 0, pt);  // geometry planes only; SH from shared memory
+        asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own column
+        const ShSmem sh{s_sh4 + threadIdx.x};
         point_backward<M>(a, s_cam, s_row0, rk, mask, pt, sh, gsp, g12,
                        [&](int f, float val) { my_sh[f * kProjThreads] += val; });
       }
@@ -569,7 +578,7 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr};
   AdamConsts c = make_adam(ad);
-  const size_t smem = sizeof(float) * 48 * kProjThreads;
+  const size_t smem = sizeof(float) * 48 * kProjThreads + sizeof(float4) * 12 * kProjThreads;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<proj_grid(pd, n_groups), kProjThreads, smem, as_stream(stream)>>>(a, c, g_sp, reinterpret_cast<float4*>(params),

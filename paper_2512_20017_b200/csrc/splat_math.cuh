@@ -132,6 +132,17 @@ struct ShPlanes {
   }
 };
 
+// SH coefficients of one point staged in shared memory as float4 entries
+// [q][kProjThreads] (s = &entry[0][thread]; stride 256 float4 between q).
+struct ShSmem {
+  const float4* s;
+  __device__ __forceinline__ float4 load4(int q) const { return s[q * 256]; }
+  __device__ __forceinline__ float operator()(int f) const {
+    const float4 v = s[(f >> 2) * 256];
+    return (f & 3) == 0 ? v.x : (f & 3) == 1 ? v.y : (f & 3) == 2 ? v.z : v.w;
+  }
+};
+
 // View-dependent colour from the SH coefficients (flat index f = 3k + ch):
 // each channel sums Y_k sh_{k,ch} in k order (round-to-nearest, as the
 // reference); coefficients are read as float4 plane entries.  With gcol
