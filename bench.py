@@ -217,9 +217,15 @@ _STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_ke
                  "project_bwd_adam": "project_bwd_adam_kernel", "project": "project_fwd_kernel", "cull": "cull_kernel"}
 
 
-def kernel_profile(stage, model="3dgs"):
+_PROFILED = {"3dgs": "c2", "2dgs": "c3"}  # configuration each model's ncu capture ran (tools/gpu_profile.sh)
+
+
+def kernel_profile(stage, model="3dgs", config=None):
     """Entry of the committed ncu --set full summary (profiles/r1_kernel_traffic.json)
-    for one launch of the stage's kernel in the same configuration, or {}."""
+    for one launch of the stage's kernel, or {} when that capture is not of
+    this configuration (counts and bytes are per launch of that workload)."""
+    if config is not None and _PROFILED.get(model) != config:
+        return {}
     path = os.path.join(ROOT, "profiles", "r1_kernel_traffic.json")
     try:
         table = json.load(open(path))
@@ -233,17 +239,17 @@ def kernel_profile(stage, model="3dgs"):
     return (tagged or hits or [{}])[0]
 
 
-def kernel_traffic(stage, model="3dgs"):
+def kernel_traffic(stage, model="3dgs", config=None):
     """DRAM bytes (read + write) of one launch of the stage's kernel, or None."""
-    return kernel_profile(stage, model).get("dram_traffic_bytes")
+    return kernel_profile(stage, model, config).get("dram_traffic_bytes")
 
 
-def issue_roofline(stage, ms, sm_mhz, model="3dgs"):
+def issue_roofline(stage, ms, sm_mhz, model="3dgs", config=None):
     """The raster kernels' real bound: warp-instruction issue.  Achieved =
     the launch's executed warp instructions (ncu, same configuration) over the
     launch time measured here; peak = 148 SMs x 4 schedulers x 1 issue/clock
     at the SM clock sampled during the timed region."""
-    n = kernel_profile(stage, model).get("warp_instructions")
+    n = kernel_profile(stage, model, config).get("warp_instructions")
     if not n or not ms or not sm_mhz:
         return None
     ach = n / (ms / 1000.0) / 1e9
@@ -333,7 +339,7 @@ def run_ours(args, cfg):
     tr.timers = {}
     lc0 = nat.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    inst, rows = [], []
+    inst, rows, big = [], [], []
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -348,6 +354,7 @@ def run_ours(args, cfg):
         tr.step(sched[args.warmup + i], next_batch=nxt(args.warmup + i))
         inst.append(tr.last["n_inst"])
         rows.append(tr.last["n_rows"])
+        big.append(int(tr.last.get("largest_bucket", 0)))
         if comm is not None:
             step_AW.append((tr.last["A"], tr.last["W"]))
     end.record()
@@ -440,9 +447,9 @@ def run_ours(args, cfg):
                               model)
         ach = nbytes / (stage_ms[dom] / 1000.0) / 1e9 if nbytes else None
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": kernel_traffic(dom, model), "peak_kind": peak_kind,
+                "frac": (ach / peak) if ach else None, "traffic": kernel_traffic(dom, model, args.config), "peak_kind": peak_kind,
                 "bytes_per_launch": nbytes, "ms_per_launch": stage_ms[dom],
-                "issue": issue_roofline(dom, stage_ms[dom], clk_summary.get("sm_mhz"), model),
+                "issue": issue_roofline(dom, stage_ms[dom], clk_summary.get("sm_mhz"), model, args.config),
                 "note": "raster kernels are FP32/issue-bound (ncu: issue slots ~80-90% busy), not HBM-bound: "
                         "see `issue`; traffic = ncu dram read+write bytes of one launch "
                         "(profiles/r1_kernel_traffic.json)"}
@@ -472,6 +479,7 @@ def run_ours(args, cfg):
             "roofline": roof,
             "stages": stages,
             "instances_per_step": int(np.mean(inst)), "splat_rows_per_step": int(np.mean(rows)),
+            "largest_tile_bucket": int(max(big)) if big else None,
             "gpu_launches": int(launches),
             "clocks": clk_summary,
             "cpu_baseline": cpu,

@@ -14,7 +14,7 @@ from . import _native as nat
 
 
 def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, model_id=nat.MODEL_3DGS,
-                sort_cap=4096, before_sync=None, capacity_hint=None):
+                sort_cap=16384, before_sync=None, capacity_hint=None):
     """Atomics into (slot, tile) buckets, then a shared-memory sort of every
     bucket by (depth, row); buckets larger than the in-SM sort go through the
     device radix sort.  `buf` is a grow-only buffer cache with

@@ -25,8 +25,8 @@
 namespace bs {
 namespace {
 
-constexpr int kSortThreads = 256;
-constexpr int kSortCap = 4096;  // keys per bucket sorted in shared memory (32 KB)
+constexpr int kSortThreads = 1024;
+constexpr int kSortCap = 16384;  // keys per bucket sorted in shared memory (128 KB, dynamic)
 
 struct BinGeom {
   const float* sp;
@@ -210,7 +210,11 @@ constexpr int kSortWarpsPerCta = 8;
 #ifndef BS_SORT_BITONIC256
 #define BS_SORT_BITONIC256 1  // measured: 10 us faster on C2 than the E = 8 merge sort
 #endif
-constexpr bool kBitonic256 = BS_SORT_BITONIC256;  // 129..256 keys: bitonic network instead of merge sort
+constexpr bool kBitonic256 = BS_SORT_BITONIC256;
+#ifndef BS_SORT_MERGE1024
+#define BS_SORT_MERGE1024 1
+#endif
+constexpr bool kMerge1024 = BS_SORT_MERGE1024;  // 513..1024 keys: merge sort instead of the bitonic network  // 129..256 keys: bitonic network instead of merge sort
 
 __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
   const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, m);
@@ -394,37 +398,54 @@ __global__ void __launch_bounds__(32 * kSortWarpsPerCta, 4) sort_tiles_warp_kern
 }
 
 // Buckets with kWarpCap < n <= cap: one CTA each.
+// Buckets with kWarpCap < n <= cap: a persistent grid (one 1024-thread CTA
+// per SM, 128 KB of shared memory) scans the bucket table 1024 entries at a
+// time, collects the large buckets of each slice and bitonic-sorts them one
+// after the other with the whole CTA -- no CTA per bucket (most buckets are
+// small and a launch over all of them costs more than the sorting).
 __global__ void __launch_bounds__(kSortThreads) sort_tiles_kernel(const uint64_t* __restrict__ keys,
-                                                                  const int2* __restrict__ ranges, int cap,
+                                                                  const int2* __restrict__ ranges, int nb, int cap,
                                                                   uint32_t* __restrict__ rows) {
-  __shared__ uint64_t s[kSortCap];
-  const int2 rg = ranges[blockIdx.x];
-  const int n = rg.y - rg.x;
-  if (n <= kWarpCap || n > cap) return;
-  if (n == 1) {
-    if (threadIdx.x == 0) rows[rg.x] = (uint32_t)keys[rg.x];
-    return;
-  }
-  int m = 2;
-  while (m < n) m <<= 1;
-  for (int i = threadIdx.x; i < m; i += kSortThreads) s[i] = i < n ? keys[rg.x + i] : ~0ull;
-  __syncthreads();
-  for (int k = 2; k <= m; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < m; i += kSortThreads) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t a = s[i], b = s[ixj];
-          if (((i & k) == 0) ? (a > b) : (a < b)) {
-            s[i] = b;
-            s[ixj] = a;
+  extern __shared__ uint64_t s[];  // [cap rounded up to a power of two]
+  __shared__ int s_list[kSortThreads];
+  __shared__ int s_n;
+  for (int base = blockIdx.x * kSortThreads; base < nb; base += gridDim.x * kSortThreads) {
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const int b = base + threadIdx.x;
+    if (b < nb) {
+      const int2 rg = ranges[b];
+      const int n = rg.y - rg.x;
+      if (n > kWarpCap && n <= cap) s_list[atomicAdd(&s_n, 1)] = b;
+    }
+    __syncthreads();
+    const int n_big = s_n;
+    for (int t = 0; t < n_big; ++t) {
+      const int2 rg = ranges[s_list[t]];
+      const int n = rg.y - rg.x;
+      int m = 2;
+      while (m < n) m <<= 1;
+      for (int i = threadIdx.x; i < m; i += kSortThreads) s[i] = i < n ? keys[rg.x + i] : ~0ull;
+      __syncthreads();
+      for (int k = 2; k <= m; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = threadIdx.x; i < m; i += kSortThreads) {
+            const int ixj = i ^ j;
+            if (ixj > i) {
+              const uint64_t a = s[i], c = s[ixj];
+              if (((i & k) == 0) ? (a > c) : (a < c)) {
+                s[i] = c;
+                s[ixj] = a;
+              }
+            }
           }
+          __syncthreads();
         }
       }
+      for (int i = threadIdx.x; i < n; i += kSortThreads) rows[rg.x + i] = (uint32_t)s[i];
       __syncthreads();
     }
   }
-  for (int i = threadIdx.x; i < n; i += kSortThreads) rows[rg.x + i] = (uint32_t)s[i];
 }
 
 __global__ void low32_kernel(const uint64_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ out) {
@@ -508,12 +529,26 @@ extern "C" int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* r
   }
   sort_tiles_merge_kernel<16, 8><<<grid, 32 * 8, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
   BS_LAUNCH_CHECK("sort_tiles_merge_kernel<16>");
-  const int grid4 = (n_buckets + 3) / 4;
-  sort_tiles_merge_kernel<32, 4><<<grid4, 32 * 4, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
-  BS_LAUNCH_CHECK("sort_tiles_merge_kernel<32>");
+  if (kMerge1024) {
+    const int grid4 = (n_buckets + 3) / 4;
+    sort_tiles_merge_kernel<32, 4><<<grid4, 32 * 4, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+    BS_LAUNCH_CHECK("sort_tiles_merge_kernel<32>");
+  } else {
+    sort_tiles_warp_kernel<32><<<grid, 32 * kSortWarpsPerCta, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+    BS_LAUNCH_CHECK("sort_tiles_warp_kernel<32>");
+  }
   if (smem_cap > kWarpCap) {
-    sort_tiles_kernel<<<n_buckets, kSortThreads, 0, s>>>(inst_keys, reinterpret_cast<const int2*>(ranges), smem_cap,
-                                                         inst_rows);
+    {
+      int m = 2;
+      while (m < smem_cap) m <<= 1;
+      const size_t smem = sizeof(uint64_t) * (size_t)m;
+      cudaFuncSetAttribute(sort_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      sort_tiles_kernel<<<sms, kSortThreads, smem, s>>>(inst_keys, reinterpret_cast<const int2*>(ranges), n_buckets,
+                                                        smem_cap, inst_rows);
+    }
     BS_LAUNCH_CHECK("sort_tiles_kernel");
   }
   return BS_OK;

@@ -173,7 +173,7 @@ class SplatTrainer:
         self.timers = None  # optional {stage: [(start_evt, end_evt), ...]}
         self.last = {}
         self.binning = "bucket"  # or "radix" (identical lists, see csrc/bin_tiles.cu)
-        self.sort_cap = 4096     # bucket sizes sorted in shared memory
+        self.sort_cap = 16384    # bucket sizes sorted in shared memory
         self.bin_capacity_hint = None  # initial instance-key buffer (tests of the overflow re-run)
         # raster work split: pixels per lane (1 -> 8x4 region per warp, 2 -> 8x8);
         # 1 measured faster on B200 (C2: bwd 3.30 vs 3.52 ms, fwd 1.22 vs 1.24 ms)

@@ -474,7 +474,8 @@ def test_train_step_temporal_culling_4dgs(cuda):
     assert 0 < rows.sum() < len(batch) * tr.S  # the time test actually removes points
 
 
-@pytest.mark.parametrize("sizes", [[0, 1, 2, 31, 32, 33, 255, 256, 257, 300, 511, 512, 513, 1000, 1024, 1025, 4096],
+@pytest.mark.parametrize("sizes", [[0, 1, 2, 31, 32, 33, 255, 256, 257, 300, 511, 512, 513, 1000, 1024, 1025, 4096,
+                                    5000, 16384],
                                    [257] * 40 + [512] * 40 + [384] * 40])
 def test_bucket_sort_every_size_class(cuda, sizes):
     """bs_bin_tiles_sort on random unique (depth bits << 32 | row) keys, every
@@ -491,7 +492,7 @@ def test_bucket_sort_every_size_class(cuda, sizes):
     kd = torch.as_tensor(keys.view(np.int64), device="cuda")
     rd = torch.as_tensor(ranges.reshape(-1), device="cuda")
     out = torch.full((max(total, 1),), -1, dtype=torch.int32, device="cuda")
-    nat.call("bs_bin_tiles_sort", nat.ptr(kd), nat.ptr(rd), len(sizes), 4096, nat.ptr(out), nat.stream_handle())
+    nat.call("bs_bin_tiles_sort", nat.ptr(kd), nat.ptr(rd), len(sizes), 16384, nat.ptr(out), nat.stream_handle())
     got = out[:total].cpu().numpy().view(np.uint32)
     for s0, n in zip(starts, sizes):
         want = (np.sort(keys[s0:s0 + n]) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
