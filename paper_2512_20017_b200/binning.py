@@ -49,10 +49,15 @@ def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, 
     ready.record()
     if before_sync is not None:
         before_sync()
-    inst_cap = max(getattr(buf, "inst_cap", 0), 4 * n_rows, 1024) if capacity_hint is None else capacity_hint
+    # the key buffer is sized generously (6 tiles per row, or the largest
+    # count seen) and the scatter may fill all of it: an overflow costs a
+    # re-run and a reallocation, which at C4 sizes is milliseconds
+    inst_cap = max(getattr(buf, "inst_cap", 0), 6 * n_rows, 1024) if capacity_hint is None else capacity_hint
 
     def scatter(capacity):
         k = buf.get("inst_keys", capacity, torch.int64)
+        if capacity_hint is None:
+            k = buf.bufs["inst_keys"]  # the whole cached allocation
         nat.call("bs_bin_tiles_scatter", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
                  nat.ptr(slot_cams), tiles, nat.ptr(cursor), nat.ptr(k), k.numel(), model_id, st)
         return k
@@ -65,7 +70,7 @@ def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, 
         offsets()
         keys = scatter(inst_cap)
     buf.inst_cap = max(getattr(buf, "inst_cap", 0), int(n_inst * 1.25) + 1024)
-    irows = buf.get("irows", max(n_inst, 1), torch.int32)
+    irows = buf.get("irows", max(keys.numel(), 1), torch.int32)[: max(n_inst, 1)]
     cap = min(sort_cap, lib.bs_bin_tiles_max_sort())
     nat.call("bs_bin_tiles_sort", nat.ptr(keys), nat.ptr(ranges), nb, cap, nat.ptr(irows), st)
     if biggest > cap:  # rare: buckets beyond the shared-memory sort
