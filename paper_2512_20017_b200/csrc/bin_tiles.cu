@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(32 * WARPS) sort_tiles_merge_kernel(const uint
 // network needs 64 key registers per lane; the common 257..512 class half of
 // that), instead of the whole kernel paying for the largest one.
 template <int EMAX>
-__global__ void __launch_bounds__(32 * kSortWarpsPerCta, 4) sort_tiles_warp_kernel(const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(32 * kSortWarpsPerCta, EMAX >= 32 ? 1 : 4) sort_tiles_warp_kernel(const uint64_t* __restrict__ keys,
                                                                                  const int2* __restrict__ ranges,
                                                                                  int nb, int cap,
                                                                                  uint32_t* __restrict__ rows) {
@@ -527,9 +527,14 @@ extern "C" int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* r
     sort_tiles_merge_kernel<8, 8><<<grid, 32 * 8, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
     BS_LAUNCH_CHECK("sort_tiles_merge_kernel<8>");
   }
-  sort_tiles_merge_kernel<16, 8><<<grid, 32 * 8, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
-  BS_LAUNCH_CHECK("sort_tiles_merge_kernel<16>");
-  if (kMerge1024) {
+  // size classes above smem_cap cannot hold a bucket the caller wants sorted
+  // here (callers pass min(cap, largest bucket)): their launches are skipped
+  if (smem_cap > 256) {
+    sort_tiles_merge_kernel<16, 8><<<grid, 32 * 8, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
+    BS_LAUNCH_CHECK("sort_tiles_merge_kernel<16>");
+  }
+  if (smem_cap <= 512) {
+  } else if (kMerge1024) {
     const int grid4 = (n_buckets + 3) / 4;
     sort_tiles_merge_kernel<32, 4><<<grid4, 32 * 4, 0, s>>>(inst_keys, rg, n_buckets, smem_cap, inst_rows);
     BS_LAUNCH_CHECK("sort_tiles_merge_kernel<32>");
