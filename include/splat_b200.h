@@ -264,7 +264,8 @@ int32_t bs_tile_ranges(const uint32_t* inst_keys, const int64_t* n_dev,
  *   sort    -> inst_rows u32 [total]: per bucket, rows in key order; buckets
  *              with more than smem_cap (<= bs_bin_tiles_max_sort()) keys are
  *              skipped -- sort that slice with bs_radix_sort_u64 and take
- *              bs_keys_low32. */
+ *              bs_keys_low32.  Passing min(cap, largest bucket) (the
+ *              offsets' stats[1]) skips the launches of empty size classes. */
 int32_t bs_bin_tiles_count(const float* sp_rows, int64_t n_rows,
                            const int64_t* seg_row0, const int32_t* seg_slot,
                            int32_t n_segs, const bs_camera* slot_cams,
