@@ -149,6 +149,9 @@ struct Model2 {
 
 template <class M>
 __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, float* __restrict__ sp) {
+  // each thread's SH coefficients, staged by cp.async (no registers held for
+  // them across the view loop): [12][kProjThreads] float4
+  extern __shared__ float4 s_sh4f[];
   __shared__ uint32_t s_bal[kProjWarps * kMaxViews];
   __shared__ int s_run[kMaxViews];
   __shared__ bs_camera s_cam[kMaxViews];
@@ -166,18 +169,29 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const uint32_t mask = i < end ? a.mask[i] : 0u;
+    if (mask) {
+      const int sh_q = (3 * a.n_sh + 3) / 4;
+      for (int q = 0; q < sh_q; ++q) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_sh4f + q * kProjThreads + threadIdx.x);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(a.params + (int64_t)(3 + q) * a.S + i)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     rk.round(mask, B);
     if (mask) {
       PointIn pt;
-      load_point(a.params, a.S, i, a.n_sh, pt);
+      load_point(a.params, a.S, i, 0, pt);  // geometry planes; SH from shared memory
       typename M::Pre pre;
       M::pre(pt, pre);
+      asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own column
+      const ShSmem sh{s_sh4f + threadIdx.x};
       uint32_t m = mask;
       while (m) {
         const int v = __ffs(m) - 1;
         m &= m - 1;
         typename M::F f;
-        M::forward(pt, pre, ShRegs{pt.sh}, s_cam[v], a.n_sh, f);
+        M::forward(pt, pre, sh, s_cam[v], a.n_sh, f);
         const int64_t row = s_row0[v] + rk.row_offset(v);
         M::write(sp + row * M::kSP, f);
       }
@@ -523,10 +537,13 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr};
   const dim3 grid = proj_grid(d, n_groups);
-  if (d->model == BS_MODEL_2DGS)
-    project_fwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
-  else
-    project_fwd_kernel<Model3><<<grid, kProjThreads, 0, as_stream(stream)>>>(a, sp_rows);
+  const size_t smem = sizeof(float4) * 12 * kProjThreads;
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, kProjThreads, smem, as_stream(stream)>>>(a, sp_rows);
+  };
+  if (d->model == BS_MODEL_2DGS) launch(project_fwd_kernel<Model2>);
+  else launch(project_fwd_kernel<Model3>);
   BS_LAUNCH_CHECK("project_fwd_kernel");
   return BS_OK;
 }
