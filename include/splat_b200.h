@@ -219,6 +219,10 @@ typedef struct {
                         1 = plain dL/dSP (d u, d v, d opacity, d conic, d rgb) */
   const int32_t* chunk_prefix; /* optional: bs_cull_count's chunk_prefix for the
                                   same mask, max_chunks = ceil(max_group_points / 256) */
+  float* gsp_zero;             /* optional (bs_project_fwd): G_SP rows (BS_GSP_FLOATS /
+                                  BS_GSP2_FLOATS floats) cleared at the index of every SP
+                                  row written -- the accumulator of a single-rank step,
+                                  cleared without a separate pass */
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,

@@ -57,7 +57,8 @@ GSP2_FLOATS = 16
 class ProjDesc(C.Structure):
     _fields_ = [("n_views", C.c_int32), ("sh_degree", C.c_int32),
                 ("tiles_x_max", C.c_int32), ("tiles_y_max", C.c_int32), ("model", C.c_int32),
-                ("max_group_points", C.c_int32), ("gsp_form", C.c_int32), ("chunk_prefix", C.c_void_p)]
+                ("max_group_points", C.c_int32), ("gsp_form", C.c_int32), ("chunk_prefix", C.c_void_p),
+                ("gsp_zero", C.c_void_p)]
 
 
 class RasterDesc(C.Structure):

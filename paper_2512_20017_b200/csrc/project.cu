@@ -92,6 +92,7 @@ struct ProjArgs {
   const bs_camera* cams;
   int gsp_standard;  // 3DGS G_SP rows: 0 = raster moments (default), 1 = dL/dSP
   const int32_t* chunk_prefix;  // [ng][gridDim.y][B] rows before each chunk, or NULL
+  float* gsp_zero;              // G_SP rows cleared alongside the SP rows (project_fwd), or NULL
 };
 
 // Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
@@ -194,6 +195,11 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
         M::forward(pt, pre, sh, s_cam[v], a.n_sh, f);
         const int64_t row = s_row0[v] + rk.row_offset(v);
         M::write(sp + row * M::kSP, f);
+        if (a.gsp_zero) {
+          float4* z = reinterpret_cast<float4*>(a.gsp_zero + row * M::kGSP);
+#pragma unroll
+          for (int k = 0; k < M::kGSP / 4; ++k) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
     }
     rk.advance(B);
@@ -535,7 +541,7 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
   if (n_groups == 0) return BS_OK;
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr};
+             view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, d->gsp_zero};
   const dim3 grid = proj_grid(d, n_groups);
   const size_t smem = sizeof(float4) * 12 * kProjThreads;
   auto launch = [&](auto kern) {
@@ -557,7 +563,7 @@ extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, in
   if (n_groups == 0) return BS_OK;
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr};
+             view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, d->gsp_zero};
   const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
     project_bwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(
@@ -593,7 +599,7 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   if (n_groups == 0) return BS_OK;
   const int n_sh = (pd->sh_degree + 1) * (pd->sh_degree + 1);
   ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr};
+             view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr, nullptr};
   AdamConsts c = make_adam(ad);
   const size_t smem = sizeof(float) * 48 * kProjThreads + sizeof(float4) * 12 * kProjThreads;
   auto launch = [&](auto kern) {

@@ -67,5 +67,5 @@ def test_host_library_exports_every_declared_symbol():
 
 def test_proj_desc_layout():
     # bs_proj_desc: 7 int32 (n_views, sh_degree, tiles_x_max, tiles_y_max, model, max_group_points, gsp_form)
-    assert ctypes.sizeof(_native.ProjDesc) == 40
+    assert ctypes.sizeof(_native.ProjDesc) == 48
     assert ctypes.sizeof(_native.CullDesc) == 40
