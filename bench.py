@@ -14,6 +14,13 @@ Prints ONE JSON line on rank 0 (contract in the task statement):
   cpu_baseline  the CPU oracle's training step on this host (bounded sample)
 --impl reference times the CPU oracle alone (the reference package has no
 renderer) on the host cores.
+
+--gpus N without a torchrun environment re-launches this script under
+torch.distributed.run with N local ranks (one process per GPU, NCCL; gloo
+when the ranks have to share GPUs or BS_DIST_BACKEND=gloo) and relays the
+rank-0 line.  Rank 0 alone builds the bipartite visibility graph and the
+points-to-rank partition and broadcasts the group owners; every rank then
+materialises only its own shard's Gaussian attributes.
 """
 
 from __future__ import annotations
@@ -51,15 +58,6 @@ CONFIGS = {
                desc="synthetic city-scale 3DGS, 50M Gaussians, 4K cameras, batch 16"),
 }
 METRIC = "train images/s (fwd+bwd) at 1/2/4/8 B200, % HBM roofline; comm bytes/step"
-
-
-def _peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
-    except Exception:
-        return 6650.0, "fallback"
 
 
 class ClockSampler:
@@ -117,9 +115,12 @@ class ClockSampler:
         return out
 
 
-def build_scene(cfg, rank=0, world=1, gt_views=None):
-    """Scene, Z-order groups, Gaussian attributes and ground truth (all views,
-    or only `gt_views` when the configuration asks for a subset)."""
+def build_scene(cfg, gt_views=None, world=1, rank=0):
+    """Scene, Z-order groups, this rank's Gaussian attributes and ground truth
+    (all views, or only `gt_views` when the configuration asks for a subset).
+    N = 1: every point.  N > 1: the shard of `shard_for_rank` only (the
+    attribute stream is drawn in blocks and only the shard's rows are kept).
+    Returns ds, g, params, gt, group_begin, aabb, partition info."""
     from paper_2512_20017_b200 import scenes
     from paper_2512_20017_b200.culling import zorder_group
 
@@ -127,13 +128,19 @@ def build_scene(cfg, rank=0, world=1, gt_views=None):
                                       cfg["image_size"])
     g = zorder_group(ds.cloud, G=cfg["G"])
     spacing = scenes.mean_spacing(cfg["altitude"], cfg["grid"], cfg["n_points"])
-    params = scenes.init_gaussians(g.sorted_cloud, cfg["seed"], spacing)
+    info = {}
+    if world > 1:
+        rows, gb, aabb, info = shard_for_rank(ds, g, world, rank)
+        params = scenes.init_gaussians_rows(g.sorted_cloud, cfg["seed"], spacing, rows)
+    else:
+        params = scenes.init_gaussians(g.sorted_cloud, cfg["seed"], spacing)
+        gb, aabb = g.group_begin(), g.aabbs.reshape(-1, 6)
     W, H = cfg["image_size"]
     if cfg.get("gt_subset") and gt_views is not None:
         gt = scenes.synthetic_gt_views(cfg["seed"], gt_views, W, H)
     else:
         gt = scenes.synthetic_gt(cfg["seed"], cfg["n_views"], W, H)
-    return ds, g, params, gt
+    return ds, g, params, gt, gb, aabb, info
 
 
 def schedule(n_views, batch, steps, seed=9):
@@ -158,27 +165,45 @@ def weak_scaled(cfg, world):
     return c
 
 
-def shard_for_rank(ds, g, params, world, rank):
+def shard_for_rank(ds, g, world, rank):
     """Points-to-rank map of the paper's offline placement: GPU-built
-    bipartite visibility graph -> hierarchical_partition(graph, N, 1)
-    (deterministic, identical on every rank); returns this rank's shard."""
+    bipartite visibility graph -> hierarchical_partition(graph, N, 1), run by
+    rank 0 alone and broadcast as the per-group owner (every rank needs all
+    owners: the random baseline and the comm report replay them).  Returns
+    this rank's point rows (ascending global index, whole groups), its group
+    table and AABBs, and the partition info."""
+    import torch
+    import torch.distributed as dist
+
     from paper_2512_20017_b200.sharding import build_bipartite_graph, hierarchical_partition
 
-    t0 = time.time()
-    graph = build_bipartite_graph(g, ds)
-    t1 = time.time()
-    part = hierarchical_partition(graph, world, 1, eps=0.05, seed=5)
-    t2 = time.time()
-    owner = part.flat_gpus()
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    owner_t = torch.empty(g.n_groups, dtype=torch.int64, device=dev)
+    stats = torch.zeros(4, dtype=torch.float64, device=dev)
+    if rank == 0:
+        t0 = time.time()
+        graph = build_bipartite_graph(g, ds)
+        t1 = time.time()
+        part = hierarchical_partition(graph, world, 1, eps=0.05, seed=5)
+        t2 = time.time()
+        owner_t.copy_(torch.as_tensor(np.asarray(part.flat_gpus(), dtype=np.int64)))
+        stats.copy_(torch.tensor([len(graph.edge_weights), t1 - t0, t2 - t1, 0.0], dtype=torch.float64))
+    dist.broadcast(owner_t, 0)
+    dist.broadcast(stats, 0)
+    owner = owner_t.cpu().numpy()
+    gbeg = g.group_begin().astype(np.int64)
+    sizes_all = np.diff(gbeg)
     mine = np.flatnonzero(owner == rank)
-    sizes = np.array([g.groups[k].size for k in mine], dtype=np.int64)
-    pts = np.concatenate([np.arange(g.groups[k].begin, g.groups[k].end) for k in mine])
+    sizes = sizes_all[mine]
+    rows = np.concatenate([np.arange(gbeg[k], gbeg[k + 1]) for k in mine]) if len(mine) else np.zeros(0, np.int64)
     gb = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
     aabb = g.aabbs.reshape(-1, 6)[mine]
-    info = {"groups": int(g.n_groups), "graph_edges": int(len(graph.edge_weights)),
-            "graph_build_s": round(t1 - t0, 2), "partition_s": round(t2 - t1, 2),
-            "points_per_rank": [int(x) for x in part.per_gpu_weights()], "owner": owner}
-    return np.ascontiguousarray(params[:, pts, :]), gb, aabb, info
+    per_rank = np.bincount(owner, weights=sizes_all, minlength=world).astype(np.int64)
+    e, tg, tp = stats.cpu().tolist()[:3]
+    info = {"groups": int(g.n_groups), "graph_edges": int(e), "graph_build_s": round(tg, 2),
+            "partition_s": round(tp, 2), "points_per_rank": [int(x) for x in per_rank], "built_on": "rank 0",
+            "owner": owner}
+    return rows, gb, aabb, info
 
 
 def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps, row_bytes=48, grad_bytes=36, P=1):
@@ -216,67 +241,32 @@ _STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_ke
                  "raster2d_bwd": "raster2d_bwd_kernel", "raster2d_fwd": "raster2d_fwd_kernel",
                  "project_bwd_adam": "project_bwd_adam_kernel", "project": "project_fwd_kernel", "cull": "cull_kernel"}
 
-
-_PROFILED = {"3dgs": "c2", "2dgs": "c3"}  # configuration each model's ncu capture ran (tools/gpu_profile.sh)
+# committed ncu --set full summaries (newest first); each names the
+# configuration it captured per model (tools/gpu_profile.sh)
+TRAFFIC_FILES = ("r2_kernel_traffic.json", "r1_kernel_traffic.json")
+_PROFILED = {"3dgs": "c2", "2dgs": "c3"}
 
 
 def kernel_profile(stage, model="3dgs", config=None):
-    """Entry of the committed ncu --set full summary (profiles/r1_kernel_traffic.json)
-    for one launch of the stage's kernel, or {} when that capture is not of
-    this configuration (counts and bytes are per launch of that workload)."""
+    """Entry of the newest committed ncu --set full summary (profiles/) for
+    one launch of the stage's kernel, or {} when that capture is not of this
+    configuration (counts and bytes are per launch of that workload)."""
     if config is not None and _PROFILED.get(model) != config:
         return {}
-    path = os.path.join(ROOT, "profiles", "r1_kernel_traffic.json")
-    try:
-        table = json.load(open(path))
-    except Exception:
-        return {}
-    key = stage.replace("raster_", "raster2d_") if model == "2dgs" and stage.startswith("raster_") else stage
-    prefix = _STAGE_KERNEL.get(key, key)
-    model_tag = "Model2" if model == "2dgs" else "Model3"
-    hits = [v for k, v in table.items() if k.startswith(prefix)]
-    tagged = [v for k, v in table.items() if k.startswith(prefix) and model_tag in k]
-    return (tagged or hits or [{}])[0]
-
-
-def kernel_traffic(stage, model="3dgs", config=None):
-    """DRAM bytes (read + write) of one launch of the stage's kernel, or None."""
-    return kernel_profile(stage, model, config).get("dram_traffic_bytes")
-
-
-def issue_roofline(stage, ms, sm_mhz, model="3dgs", config=None):
-    """The raster kernels' real bound: warp-instruction issue.  Achieved =
-    the launch's executed warp instructions (ncu, same configuration) over the
-    launch time measured here; peak = 148 SMs x 4 schedulers x 1 issue/clock
-    at the SM clock sampled during the timed region."""
-    n = kernel_profile(stage, model, config).get("warp_instructions")
-    if not n or not ms or not sm_mhz:
-        return None
-    ach = n / (ms / 1000.0) / 1e9
-    peak = 148 * 4 * sm_mhz * 1e6 / 1e9
-    return {"bound": "issue", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "G warp-instr/s",
-            "frac": round(ach / peak, 4), "warp_instructions": n}
-
-
-def kernel_bytes(stage, last, S, B, model="3dgs"):
-    """Algorithmic (compulsory) bytes of one launch of a stage.
-    Per instance: list entry 4 B + the splat fields the rasteriser gathers
-    (3DGS 36 B: mean, opacity, conic, rgb; 2DGS 64 B: mean, opacity, M, rgb, depth);
-    per row: SP write (48 / 96 B) and the used G_SP floats (36 / 60 B)."""
-    I, V, slots = last["n_inst"], last["n_rows"], last["n_slots"]
-    npx = slots * last["H"] * last["W"]
-    per_inst, sp_row, gsp_row = (68, 96, 60) if model == "2dgs" else (40, 48, 36)
-    if stage == "raster_fwd":   # instance list + gathered splat; image 12 + T 4 + n 4 B/px + gt 3 B/px
-        return per_inst * I + 23 * npx
-    if stage == "raster_bwd":   # same reads + image/gt re-read + one f32 atomic per G_SP term per splat
-        return per_inst * I + 23 * npx + gsp_row * V
-    if stage == "project":      # 240 B params per visible point (once) + mask + SP row
-        return 240 * last["n_visible_points"] + 4 * S + sp_row * V
-    if stage == "project_bwd_adam":  # params/m/v read+write (60 f32 each) + mask + G_SP per row
-        return 6 * 240 * S + 4 * S + gsp_row * V
-    if stage == "cull":
-        return 16 * S + 4 * S
-    return None
+    for name in TRAFFIC_FILES:
+        try:
+            table = json.load(open(os.path.join(ROOT, "profiles", name)))
+        except Exception:
+            continue
+        key = stage.replace("raster_", "raster2d_") if model == "2dgs" and stage.startswith("raster_") else stage
+        prefix = _STAGE_KERNEL.get(key, key)
+        model_tag = "Model2" if model == "2dgs" else "Model3"
+        hits = [v for k, v in table.items() if k.startswith(prefix)]
+        tagged = [v for k, v in table.items() if k.startswith(prefix) and model_tag in k]
+        ent = (tagged or hits or [{}])[0]
+        if ent:
+            return dict(ent, source=f"profiles/{name}")
+    return {}
 
 
 def _max_over_ranks(vals):
@@ -287,6 +277,27 @@ def _max_over_ranks(vals):
     t = torch.tensor(vals, dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(x) for x in t.tolist()]
+
+
+def dist_backend(world: int) -> str:
+    """NCCL when every rank has its own GPU; gloo (host-staged exchanges) when
+    ranks have to share GPUs (NCCL refuses two ranks on one device) or when
+    BS_DIST_BACKEND says so."""
+    import torch
+
+    forced = os.environ.get("BS_DIST_BACKEND")
+    if forced:
+        return forced
+    return "nccl" if torch.cuda.device_count() >= world else "gloo"
+
+
+def config_dict(cfg, B, world, P):
+    """The `config` of the JSON line, identical in both arms."""
+    return {"workload": cfg["desc"], "primitive": cfg.get("model", "3dgs"), "n_points": cfg["n_points"],
+            "image": list(cfg["image_size"]), "global_batch": B, "views": cfg["n_views"], "group_size": cfg["G"],
+            "parallelism": f"points+images x{world}", "patches_per_side": P,
+            "l2": "inputs larger than L2 (params + Adam state %.0f MB over the scene; L2 126 MB)"
+                  % (cfg["n_points"] * 720 / 1e6)}
 
 
 def run_ours(args, cfg):
@@ -300,14 +311,14 @@ def run_ours(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local % torch.cuda.device_count())
-    comm, part_info = None, {}
+    comm, part_info, backend = None, {}, None
     if world > 1:
         import torch.distributed as dist
 
         from paper_2512_20017_b200.exchange import SplatExchange
 
-        # BS_DIST_BACKEND=gloo: several ranks sharing one GPU (plumbing tests)
-        dist.init_process_group(os.environ.get("BS_DIST_BACKEND", "nccl"))
+        backend = dist_backend(world)
+        dist.init_process_group(backend)
         if cfg.get("scaling", "weak") == "weak":
             cfg = weak_scaled(cfg, world)
     strong = cfg.get("scaling", "weak") == "strong"
@@ -315,11 +326,9 @@ def run_ours(args, cfg):
     sched = schedule(cfg["n_views"], B, args.warmup + 2 * args.steps + 2)
     gt_ids = sorted({v for b in sched for v in b}) if cfg.get("gt_subset") else None
     t0 = time.time()
-    ds, g, params, gt = build_scene(cfg, gt_views=gt_ids)
+    ds, g, params, gt, gb, aabb, part_info = build_scene(cfg, gt_views=gt_ids, world=world, rank=rank)
     gt_row = (lambda v: v) if gt_ids is None else {v: k for k, v in enumerate(gt_ids)}.__getitem__
-    gb, aabb = g.group_begin(), g.aabbs.reshape(-1, 6)
     if world > 1:
-        params, gb, aabb, part_info = shard_for_rank(ds, g, params, world, rank)
         comm = SplatExchange()
     setup_s = time.time() - t0
     W, H = cfg["image_size"]
@@ -380,6 +389,8 @@ def run_ours(args, cfg):
         comm_report = comm_bytes_report(comm, step_AW, sched[args.warmup:args.warmup + args.steps], ds, g,
                                         world, rank, args.steps, row_bytes=4 * tr.sp_floats,
                                         grad_bytes=4 * tr.gsp_wire_floats, P=P)
+        comm_report.update(backend=backend, communicator_size=world,
+                           collectives_per_step={"all_gather": 1, "all_to_all_single": 2 if P == 1 else 3})
     # ---- e2e: public API with pinned host ground truth, loss read back
     # the step's ground-truth images are copied from pinned host memory on a
     # side stream, double-buffered: step i+1's upload overlaps step i
@@ -436,28 +447,47 @@ def run_ours(args, cfg):
     if world > 1:
         e2e_ms, e2e_wall = _max_over_ranks([e2e_ms, e2e_wall])
     e2e_value = B * len(e2e_sched) / (max(e2e_ms, e2e_wall) / 1000.0)
-    # ---- roofline of the dominant kernel
-    peak, peak_kind = _peaks()
-    last = dict(tr.last, H=H, W=W, n_visible_points=int(tr.last.get("n_visible_points", tr.S)))
-    dom = max(stage_ms, key=stage_ms.get) if stage_ms else None
-    roof = None
+    # ---- rooflines (paper_2512_20017_b200/roofline.py): every stage's
+    # compulsory bytes vs the measured HBM peak, the step's total, and the
+    # issue rate of the kernels ncu captured
+    from paper_2512_20017_b200 import roofline as rl
+
+    peak, peak_kind = rl.peaks(ROOT)
     clk_summary = clk.summary()
-    if dom:
-        nbytes = kernel_bytes(dom, dict(last, n_inst=int(np.mean(inst)), n_rows=int(np.mean(rows))), tr.S, B,
-                              model)
-        ach = nbytes / (stage_ms[dom] / 1000.0) / 1e9 if nbytes else None
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": kernel_traffic(dom, model, args.config), "peak_kind": peak_kind,
-                "bytes_per_launch": nbytes, "ms_per_launch": stage_ms[dom],
-                "issue": issue_roofline(dom, stage_ms[dom], clk_summary.get("sm_mhz"), model, args.config),
-                "note": "raster kernels are FP32/issue-bound (ncu: issue slots ~80-90% busy), not HBM-bound: "
-                        "see `issue`; traffic = ncu dram read+write bytes of one launch "
-                        "(profiles/r1_kernel_traffic.json)"}
+    counts = {"S": tr.S, "V": int(np.mean(rows)), "Vp": int(tr.last.get("n_visible_points", tr.S)),
+              "I": int(np.mean(inst)), "Np": int(tr.last["n_slots"]) * H * W,
+              "nb": int(tr.last["n_slots"]) * tr.tiles,
+              "gsp_clear": comm is None and model == "3dgs" and tr.binning != "radix"}
     stages = {}
     for k, v in stage_ms.items():
-        nb = kernel_bytes(k, dict(last, n_inst=int(np.mean(inst)), n_rows=int(np.mean(rows))), tr.S, B, model)
+        nb = rl.stage_bytes(k, counts, model)
+        h = rl.hbm(nb, v, peak) if nb else None
+        prof = kernel_profile(k, model, args.config)
+        iss = rl.issue(prof.get("warp_instructions"), v, clk_summary.get("sm_mhz"))
         stages[k] = {"ms": round(v, 4), "share": round(v / ms_per_step, 4),
-                     "gbs": round(nb / (v / 1000.0) / 1e9, 1) if nb else None}
+                     "gbs": round(h["achieved"], 1) if h else None, "hbm_frac": round(h["frac"], 4) if h else None,
+                     "issue_frac": iss["frac"] if iss else None, "binding": rl.binding(h, iss)}
+    dom = max(stage_ms, key=stage_ms.get) if stage_ms else None
+    roof = None
+    if dom:
+        nbytes = rl.stage_bytes(dom, counts, model)
+        h = rl.hbm(nbytes, stage_ms[dom], peak)
+        prof = kernel_profile(dom, model, args.config)
+        iss = rl.issue(prof.get("warp_instructions"), stage_ms[dom], clk_summary.get("sm_mhz"))
+        sb = rl.step_bytes(counts, model)
+        roof = {"kernel": dom, "bound": "hbm", "achieved": h["achieved"], "peak": peak, "unit": "GB/s",
+                "frac": h["frac"], "traffic": prof.get("dram_traffic_bytes"), "peak_kind": peak_kind,
+                "bytes_per_launch": nbytes, "ms_per_launch": stage_ms[dom],
+                "binding": rl.binding(h, iss), "issue": iss,
+                "traffic_source": prof.get("source"),
+                "step_hbm": {"bytes_per_step": sb, "achieved": round(sb / (ms_per_step / 1000.0) / 1e9, 1),
+                             "peak": peak, "frac": round(sb / (ms_per_step / 1000.0) / 1e9 / peak, 4),
+                             "survey_formula_bytes": rl.survey_step_bytes(counts)},
+                "note": "bound/achieved/frac: the contract's HBM roofline of the dominant kernel (algorithmic bytes "
+                        "of roofline.py / CUDA-event launch time); binding: the bound it actually sits at "
+                        "(issue = executed warp instructions of the same launch in the committed ncu capture / "
+                        "launch time vs 148 SMs x 4 schedulers x the sampled SM clock); step_hbm: compulsory "
+                        "bytes of every stage of the step / ms_per_step"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, ds, g, params, gt, steps=1, gt_row=gt_row)
@@ -466,10 +496,7 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": round(value, 3), "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "primitive": model, "n_points": cfg["n_points"],
-                       "image": list(cfg["image_size"]), "global_batch": B, "views": cfg["n_views"], "group_size": cfg["G"],
-                       "parallelism": f"points+images x{world}", "patches_per_side": P,
-                       "l2": "inputs larger than L2 (params+Adam state %.0f MB/rank)" % (3 * tr.params.numel() * 4 / 1e6)},
+            "config": config_dict(cfg, B, world, P),
             "e2e": {"value": round(e2e_value, 3), "unit": "images/s", "device_ms": round(e2e_ms, 3),
                     "wall_ms": round(e2e_wall, 3), "h2d_bytes_per_step": B * H * W * 3 * world,
                     "d2h_bytes_per_step": 4 * B},
@@ -523,19 +550,32 @@ def cpu_baseline(cfg, ds, g, params, gt, steps=1, warmup=0, gt_row=lambda v: v):
 
 
 def run_reference(args, cfg):
+    """The reference arm: the CPU implementation of the path (the oracle port,
+    oracle/splat_oracle.c; the reference package itself has no renderer,
+    SURVEY.md §0) on all host cores, rank 0 only.  Each step is a bounded
+    sample of the workload -- ONE view of the configuration's scene through
+    the full training step (cull, project, bin, blend, L1, backward, Adam) --
+    so images/s compares per image with the GPU arm's batches."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 and cfg.get("scaling", "weak") == "weak":
+        cfg = weak_scaled(cfg, world)
+    strong = cfg.get("scaling", "weak") == "strong"
+    B = cfg["batch"] if strong else cfg["batch"] * world
+    P = args.patches or cfg.get("P", 1)
     ds, g, params, gt, gt_row = build_scene_host(cfg, args.steps + min(args.warmup, 1))
     cpu = cpu_baseline(cfg, ds, g, params, gt, steps=args.steps, warmup=min(args.warmup, 1), gt_row=gt_row)
     line = {"metric": METRIC, "impl": "reference", "value": cpu["value"], "unit": "images/s",
-            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1000.0 / cpu["value"], 2), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "primitive": cfg.get("model", "3dgs"), "n_points": cfg["n_points"],
-                       "image": list(cfg["image_size"]), "global_batch": cfg["batch"]},
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1000.0 / cpu["value"], 2), "higher_is_better": True,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(cfg, B, world, P),
             "cpu_baseline": cpu,
-            "e2e": {"value": cpu["value"], "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": cpu["value"], "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "each reference step is 1 view of the configuration's scene (bounded CPU sample); "
+                    "images/s is per image, like the GPU arm's"}
     print(json.dumps(line), flush=True)
 
 
@@ -558,6 +598,19 @@ def build_scene_host(cfg, n_used=None):
     return ds, None, params, scenes.synthetic_gt(cfg["seed"], cfg["n_views"], W, H), (lambda v: v)
 
 
+def spawn(args) -> int:
+    """--gpus N outside torchrun: re-launch this script as N local ranks
+    (torch.distributed.run, rendezvous on 127.0.0.1); rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -568,6 +621,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--patches", type=int, default=0, help="patches per image side P (default: the config's, 1)")
     args = ap.parse_args()
+    world = os.environ.get("WORLD_SIZE")
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if world is None and args.gpus > 1:
+        sys.exit(spawn(args))
+    if world is not None and int(world) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

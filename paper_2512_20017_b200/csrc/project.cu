@@ -368,7 +368,11 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
                    : "memory");
     }
     const int sh_q = (3 * a.n_sh + 3) / 4;  // float4 entries holding this degree's coefficients
-    if (ok) {
+    const uint32_t mask = ok ? a.mask[i] : 0u;
+    // only visible points stage their coefficients: every copy issued here is
+    // waited for below (cp.async.wait_all inside `if (mask)`), so no copy is
+    // left in flight into the column when the next round reuses it
+    if (mask) {
       for (int q = 0; q < sh_q; ++q) {
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_sh4 + q * kProjThreads + threadIdx.x);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(params + (int64_t)(3 + q) * a.S + i)
@@ -376,7 +380,6 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    const uint32_t mask = ok ? a.mask[i] : 0u;
     rk.round(mask, B);
     if (ok && !(c.selective && mask == 0u)) {
       // geometry gradient in registers, the 48 SH gradients in this thread's

@@ -337,27 +337,49 @@ def init_gaussians(cloud: PointCloud, seed: int, spacing: float) -> np.ndarray:
     opacity U(0.1, 0.9) -> logit; sh0 N(0, 0.3) (S, 3); shN N(0, 0.03) (S, 45).
     log_scale = log(spacing * f) on x, y and log(0.3 * spacing * f) on z.
     """
+    return init_gaussians_rows(cloud, seed, spacing, None)
+
+
+def init_gaussians_rows(cloud: PointCloud, seed: int, spacing: float, rows: np.ndarray | None) -> np.ndarray:
+    """init_gaussians restricted to the points `rows` (ascending indices into
+    `cloud`; None = all): [15, len(rows), 4].  Every draw of the stream is
+    made in row blocks (a block draw continues the stream exactly like one
+    (S, k) draw), and only the selected rows are kept, so a rank of a
+    50M-200M point scene materialises its own shard and no float64 [S, k]
+    array (bench.py, one process per GPU)."""
     S = len(cloud)
     rng = _stream(seed, 4)
-    f = rng.uniform(0.5, 1.5, size=(S, 3))
-    quat = rng.normal(0.0, 1.0, size=(S, 4))
-    op = rng.uniform(0.1, 0.9, size=S)
-    sh0 = rng.normal(0.0, 0.3, size=(S, 3))
-    out = np.zeros((15, S, 4), dtype=np.float32)
-    out[0, :, :3] = cloud.positions
-    out[0, :, 3] = np.log(op / (1.0 - op))
-    ls = np.log(spacing * f)
-    ls[:, 2] = np.log(0.3 * spacing * f[:, 2])
-    out[1, :, :3] = ls
-    out[2] = quat / np.linalg.norm(quat, axis=1, keepdims=True)
-    # shN drawn in row blocks (the same stream as one (S, 45) draw) so that
-    # 50M-200M point scenes do not materialise float64 [S, 48] copies
+    sel = np.arange(S, dtype=np.int64) if rows is None else np.asarray(rows, dtype=np.int64)
+    if len(sel) and (np.any(np.diff(sel) <= 0) or sel[0] < 0 or sel[-1] >= S):
+        raise ParameterError("rows must be ascending unique point indices")
+    n = len(sel)
+    out = np.zeros((15, n, 4), dtype=np.float32)
     step = 1 << 22
-    for r0 in range(0, S, step):
-        r1 = min(S, r0 + step)
-        shn = rng.normal(0.0, 0.03, size=(r1 - r0, 45))
-        sh = np.concatenate([sh0[r0:r1], shn], axis=1).astype(np.float32)  # f = 3k + channel
-        out[3:15, r0:r1] = sh.reshape(r1 - r0, 12, 4).transpose(1, 0, 2)
+    blocks = [(r0, min(S, r0 + step)) for r0 in range(0, S, step)]
+    # output slice of every block: sel[lo:hi] lies in [r0, r1)
+    cuts = np.searchsorted(sel, [b[0] for b in blocks] + [S])
+
+    def each_block(draw):
+        for k, (r0, r1) in enumerate(blocks):
+            vals = draw(r1 - r0)
+            lo, hi = cuts[k], cuts[k + 1]
+            yield lo, hi, (vals if rows is None else vals[sel[lo:hi] - r0])
+
+    out[0, :, :3] = np.asarray(cloud.positions) if rows is None else np.asarray(cloud.positions)[sel]
+    for lo, hi, f in each_block(lambda m: rng.uniform(0.5, 1.5, size=(m, 3))):
+        ls = np.log(spacing * f)
+        ls[:, 2] = np.log(0.3 * spacing * f[:, 2])
+        out[1, lo:hi, :3] = ls
+    for lo, hi, quat in each_block(lambda m: rng.normal(0.0, 1.0, size=(m, 4))):
+        out[2, lo:hi] = quat / np.linalg.norm(quat, axis=1, keepdims=True)
+    for lo, hi, op in each_block(lambda m: rng.uniform(0.1, 0.9, size=m)):
+        out[0, lo:hi, 3] = np.log(op / (1.0 - op))
+    sh0 = np.zeros((n, 3), dtype=np.float64)
+    for lo, hi, v in each_block(lambda m: rng.normal(0.0, 0.3, size=(m, 3))):
+        sh0[lo:hi] = v
+    for lo, hi, shn in each_block(lambda m: rng.normal(0.0, 0.03, size=(m, 45))):
+        sh = np.concatenate([sh0[lo:hi], shn], axis=1).astype(np.float32)  # f = 3k + channel
+        out[3:15, lo:hi] = sh.reshape(hi - lo, 12, 4).transpose(1, 0, 2)
     return out
 
 

@@ -1,4 +1,4 @@
-"""bench.py at --gpus 2 with both ranks on cuda:0 over gloo (the driver runs
+"""bench.py --gpus 2 (self-launched ranks, both on cuda:0, over gloo (the driver runs
 N > 1 under torchrun over NCCL on N GPUs; this checks the plumbing: weak
 scaling, sharding, async placement, comm report, one JSON line)."""
 
@@ -16,9 +16,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("patches", [1, 2])
 def test_bench_two_ranks_gloo(cuda, patches):
     env = dict(os.environ, BS_DIST_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", f"--master-port={29611 + patches}", os.path.join(ROOT, "bench.py"), "--gpus",
-           "2", "--steps", "3", "--warmup", "3", "--config", "c1", "--patches", str(patches)]
+    # no torchrun wrapper: `--gpus 2` launches its own two ranks
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3", "--config",
+           "c1", "--patches", str(patches)]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
@@ -28,3 +28,6 @@ def test_bench_two_ranks_gloo(cuda, patches):
     assert d["config"]["patches_per_side"] == patches
     assert d["placement"]["async"] and d["placement"]["step_wait_ms"] is not None  # prefetched W used
     assert d["comm"]["fwd_bytes_per_step"] >= 0 and d["comm"]["random_fwd_bytes_per_step"] > 0
+    assert d["comm"]["backend"] == "gloo" and d["comm"]["communicator_size"] == 2
+    assert d["partition"]["built_on"] == "rank 0" and sum(d["partition"]["points_per_rank"]) == 2 * 10_000
+    assert d["roofline"]["step_hbm"]["frac"] > 0
