@@ -132,6 +132,7 @@ def build_scene(cfg, gt_views=None, world=1, rank=0):
     if world > 1:
         rows, gb, aabb, info = shard_for_rank(ds, g, world, rank)
         params = scenes.init_gaussians_rows(g.sorted_cloud, cfg["seed"], spacing, rows)
+        info["rows"] = rows
     else:
         params = scenes.init_gaussians(g.sorted_cloud, cfg["seed"], spacing)
         gb, aabb = g.group_begin(), g.aabbs.reshape(-1, 6)
@@ -335,7 +336,7 @@ def run_ours(args, cfg):
     model = cfg.get("model", "3dgs")
     P = args.patches or cfg.get("P", 1)
     tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt, adam=AdamConfig(scenes.lr_table(cfg["altitude"])),
-                      comm=comm, model=model, gt_view_ids=gt_ids, patches=P)
+                      comm=comm, model=model, gt_view_ids=gt_ids, patches=P, global_ids=part_info.get("rows"))
     # clocks are sampled from the start of the warm-up to the end of the timed
     # region (nvidia-smi needs ~0.5 s to start streaming)
     clk = ClockSampler(local).__enter__()
@@ -502,7 +503,7 @@ def run_ours(args, cfg):
                     "d2h_bytes_per_step": 4 * B},
             "comm": comm_report,
             "placement": placement,
-            "partition": {k: v for k, v in part_info.items() if k != "owner"} or None,
+            "partition": {k: v for k, v in part_info.items() if k not in ("owner", "rows")} or None,
             "roofline": roof,
             "stages": stages,
             "instances_per_step": int(np.mean(inst)), "splat_rows_per_step": int(np.mean(rows)),

@@ -223,6 +223,11 @@ typedef struct {
                                   BS_GSP2_FLOATS floats) cleared at the index of every SP
                                   row written -- the accumulator of a single-rank step,
                                   cleared without a separate pass */
+  const int32_t* point_gid;    /* optional (bs_project_fwd): global id of every local
+                                  point (NULL: the local index) */
+  int32_t* row_gid;            /* optional (bs_project_fwd): int32 per SP row, the
+                                  global id of the row's point -- the canonical
+                                  tie order of the receiving rank (bs_canonical_order) */
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,
@@ -406,7 +411,8 @@ int32_t bs_dest_compact(const uint32_t* dest_mask, int64_t n_rows, int32_t n_des
                         int64_t* dest_total, const int64_t* dest_base, int64_t* send_idx,
                         int64_t* view_counts, void* workspace, size_t ws_bytes,
                         void* stream);
-/* dst[i] = src[idx[i]] (rows of `width` floats, width % 4 == 0) */
+/* dst[i] = src[idx[i]] (rows of `width` 32-bit words; float4 copies when
+ * width % 4 == 0) */
 int32_t bs_gather_rows(const float* src, int32_t width, const int64_t* idx, int64_t n,
                        float* dst, void* stream);
 /* dst[idx[i]][k] += src[i][k], k < used (atomic: rows sent to several ranks);
@@ -414,6 +420,22 @@ int32_t bs_gather_rows(const float* src, int32_t width, const int64_t* idx, int6
 int32_t bs_scatter_add_rows(const float* src, int32_t src_width, int32_t used,
                             const int64_t* idx, int64_t n, float* dst, int32_t dst_width,
                             void* stream);
+
+/* Canonical row order of a receiving rank (stable order
+ * contract of visibility.py:122): the rows of every render slot sorted by the
+ * global id of their point, so that the per-tile lists (ties in depth broken
+ * by row) are the same on 1 or N ranks.  Replaces nothing in the reference
+ * (it has no receive side); called by the executor between the splat
+ * all-to-all and the binning.
+ * row_gid[r] (int32 >= 0) of received row r, segments [seg_row0[s], next)
+ * rendered in slot seg_slot[s].  Outputs: order[i] = received row placed at
+ * canonical position i (slot-major, ascending global id), canon_gid[i] (optional)
+ * its global id. */
+size_t bs_canonical_order_workspace(int64_t n_rows);
+int32_t bs_canonical_order(const int32_t* row_gid, int64_t n_rows, const int64_t* seg_row0,
+                           const int32_t* seg_slot, int32_t n_segs, int32_t n_slots,
+                           int64_t* order, int32_t* canon_gid, void* workspace, size_t ws_bytes,
+                           void* stream);
 
 #ifdef __cplusplus
 }

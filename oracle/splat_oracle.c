@@ -596,11 +596,25 @@ static oinst* bin_view(const float* sp, int64_t m, int W, int H, int64_t* n_out,
   return bin_view_l(sp, m, W, H, LAY3, n_out, ranges);
 }
 
-static float splat_power(const float* r, float px, float py, float* dx, float* dy) {
-  *dx = r[0] - px;
-  *dy = r[1] - py;
-  const float q = fmaf(r[3], (*dx) * (*dx), r[5] * ((*dy) * (*dy)));
-  return fmaf(-0.5f, q, -(r[4] * ((*dx) * (*dy))));
+/* Per-pixel exponent in log2 units, in the op order of csrc/raster.cu
+ * (stage + splat_power2): the conic pre-scaled by -log2(e)/2 (B by -log2(e)),
+ * d = (u - px, v - py), p2 = fma(kB, dx dy, kA dx^2) + kC dy^2.  Bit-identical
+ * to the kernels, so every keep/skip decision is the same. */
+#define LOG2E_F 1.4426950408889634f
+static float splat_p2(const float* r, float px, float py, float* dx, float* dy) {
+  const float kA = r[3] * (-0.5f * LOG2E_F), kC = r[5] * (-0.5f * LOG2E_F), kB = r[4] * -LOG2E_F;
+  *dx = r[0] + (-px);
+  *dy = r[1] + (-py);
+  const float tx = ((*dx) * (*dx)) * kA, ty = ((*dy) * (*dy)) * kC;
+  return fmaf(kB, (*dx) * (*dy), tx) + ty;
+}
+
+/* Support of a splat at a pixel: q <= k, k = min(9, 2 ln(255 o)) (the
+ * alpha >= 1/255 test and the 3-sigma cut as one threshold on the exponent,
+ * computed with the shared deterministic log: csrc/raster.cu support_p2) */
+static float support_p2(float o) {
+  const float k = fminf(9.0f, 2.0f * or_det_logf(255.0f * o));
+  return k * (-0.5f * LOG2E_F);
 }
 
 int32_t or_render(const float* sp, int64_t m, int32_t W, int32_t H, const float* bg, float* image, float* final_T,
@@ -633,10 +647,9 @@ int32_t or_render(const float* sp, int64_t m, int32_t W, int32_t H, const float*
         for (int i = ranges[2 * t]; i < ranges[2 * t + 1]; ++i) {
           const float* r = sp + (int64_t)inst[i].row * SPF;
           float dx, dy;
-          const float power = splat_power(r, pxf, pyf, &dx, &dy);
-          if (power > 0.f || power < -4.5f) continue; /* q > 9: outside the 3-sigma ellipse */
-          const float alpha = fminf(0.99f, r[2] * expf(power));
-          if (alpha < 1.f / 255.f) continue;
+          const float p2 = splat_p2(r, pxf, pyf, &dx, &dy);
+          if (p2 > 0.f || p2 < support_p2(r[2])) continue; /* outside the support (q > k) */
+          const float alpha = fminf(0.99f, r[2] * exp2f(p2));
           const float nT = T * (1.f - alpha);
           if (nT < 1e-4f) break;
           const float w = alpha * T;
@@ -680,12 +693,11 @@ int32_t or_render_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const fl
           const int64_t row = inst[i].row;
           const float* r = sp + row * SPF;
           float dx, dy;
-          const float power = splat_power(r, pxf, pyf, &dx, &dy);
-          if (power > 0.f || power < -4.5f) continue; /* q > 9: outside the 3-sigma ellipse */
-          const float ex = expf(power);
+          const float p2 = splat_p2(r, pxf, pyf, &dx, &dy);
+          if (p2 > 0.f || p2 < support_p2(r[2])) continue; /* outside the support (q > k) */
+          const float ex = exp2f(p2);
           const float raw = r[2] * ex;
           const float alpha = fminf(0.99f, raw);
-          if (alpha < 1.f / 255.f) continue;
           const float ra = 1.f / (1.f - alpha);
           T = T * ra;
           float* g = gsp + row * GSPF;
@@ -1049,7 +1061,7 @@ void or_project2d_bwd(const float* params, int64_t S, const int64_t* idx, int64_
 /* ray-splat intersection of pixel centre (px, py) with a 2DGS row */
 typedef struct {
   float hx[3], hy[3], z[3], u, v, g3, dx, dy, g2, power;
-  int ok;
+  int ok, in, disk;
 } oeval2;
 
 static void cross3e(const float* a, const float* b, float* o) {
@@ -1078,14 +1090,22 @@ static void eval2_o(const float* r, float px, float py, oeval2* e) {
   cross3e(M + 6, e->hx, zc);
   for (int k = 0; k < 3; ++k) e->z[k] = fmaf(zc[k], oy, fmaf(zb[k], ox, z0[k]));
   e->ok = e->z[2] != 0.f;
+  e->in = e->disk = 0;
   if (!e->ok) return;
   e->u = e->z[0] / e->z[2];
   e->v = e->z[1] / e->z[2];
   e->g3 = fmaf(e->u, e->u, e->v * e->v);
-  e->dx = r[0] - px;
-  e->dy = r[1] - py;
+  e->dx = r[0] + (-px);
+  e->dy = r[1] + (-py);
   e->g2 = 2.f * fmaf(e->dx, e->dx, e->dy * e->dy);
   e->power = -0.5f * fminf(e->g3, e->g2);
+  /* decisions without the division (csrc/raster2d.cu eval2, bit-identical):
+   * g3 <= k  <=>  zx^2 + zy^2 <= k zz^2, k = min(9, 2 ln(255 o)); the disk
+   * branch of min(g3, g2) iff zx^2 + zy^2 <= g2 zz^2 */
+  const float k = fminf(9.0f, 2.0f * or_det_logf(255.0f * r[2]));
+  const float n3 = fmaf(e->z[0], e->z[0], e->z[1] * e->z[1]), zz = e->z[2] * e->z[2];
+  e->in = (n3 <= k * zz) || (e->g2 <= k);
+  e->disk = n3 <= e->g2 * zz;
 }
 
 int32_t or_render2d(const float* sp, int64_t m, int32_t W, int32_t H, const float* bg, float* image, float* final_T,
@@ -1119,9 +1139,8 @@ int32_t or_render2d(const float* sp, int64_t m, int32_t W, int32_t H, const floa
           const float* r = sp + (int64_t)inst[i].row * SP2F;
           oeval2 e;
           eval2_o(r, pxf, pyf, &e);
-          if (!e.ok || e.power > 0.f || e.power < -4.5f) continue; /* outside the 3-sigma support */
+          if (!e.ok || !e.in) continue; /* outside the support: min(g3, g2) > k */
           const float alpha = fminf(0.99f, r[2] * expf(e.power));
-          if (alpha < 1.f / 255.f) continue;
           const float nT = T * (1.f - alpha);
           if (nT < 1e-4f) break;
           const float w = alpha * T;
@@ -1165,11 +1184,10 @@ int32_t or_render2d_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const 
           const float* r = sp + row * SP2F;
           oeval2 e;
           eval2_o(r, pxf, pyf, &e);
-          if (!e.ok || e.power > 0.f || e.power < -4.5f) continue; /* outside the 3-sigma support */
+          if (!e.ok || !e.in) continue; /* outside the support: min(g3, g2) > k */
           const float ex = expf(e.power);
           const float raw = r[2] * ex;
           const float alpha = fminf(0.99f, raw);
-          if (alpha < 1.f / 255.f) continue;
           const float ra = 1.f / (1.f - alpha);
           T = T * ra;
           float* g = gsp + row * GSP2F;
@@ -1184,7 +1202,7 @@ int32_t or_render2d_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const 
           if (raw > 0.99f) continue;
           const float dpow = dL_da * alpha;
           g[11] += dL_da * ex;
-          if (e.g3 <= e.g2) {
+          if (e.disk) {
             /* power = -(u^2 + v^2) / 2, (u, v) = zeta.xy / zeta.z, zeta = hx x hy */
             const float gu = -e.u * dpow, gv = -e.v * dpow;
             const float gz[3] = {gu / e.z[2], gv / e.z[2], -(gu * e.z[0] + gv * e.z[1]) / (e.z[2] * e.z[2])};

@@ -58,7 +58,7 @@ class ProjDesc(C.Structure):
     _fields_ = [("n_views", C.c_int32), ("sh_degree", C.c_int32),
                 ("tiles_x_max", C.c_int32), ("tiles_y_max", C.c_int32), ("model", C.c_int32),
                 ("max_group_points", C.c_int32), ("gsp_form", C.c_int32), ("chunk_prefix", C.c_void_p),
-                ("gsp_zero", C.c_void_p)]
+                ("gsp_zero", C.c_void_p), ("point_gid", C.c_void_p), ("row_gid", C.c_void_p)]
 
 
 class RasterDesc(C.Structure):
@@ -122,6 +122,8 @@ _SIGS = {
     "bs_dest_compact": (_I32, [_P, _I64, _I32, _P, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "bs_gather_rows": (_I32, [_P, _I32, _P, _I64, _P, _P]),
     "bs_scatter_add_rows": (_I32, [_P, _I32, _I32, _P, _I64, _P, _I32, _P]),
+    "bs_canonical_order_workspace": (_SZ, [_I64]),
+    "bs_canonical_order": (_I32, [_P, _I64, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -153,6 +153,35 @@ __global__ void gather_rows_kernel(const float4* __restrict__ src, int w4, const
   }
 }
 
+__global__ void gather_words_kernel(const uint32_t* __restrict__ src, int w, const int64_t* __restrict__ idx, int64_t n,
+                                    uint32_t* __restrict__ dst) {
+  const int64_t total = n * w;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / w;
+    const int k = (int)(t - i * w);
+    dst[t] = src[idx[i] * w + k];
+  }
+}
+
+// canonical order: key = (slot << 32) | global id, value = received row
+__global__ void order_keys_kernel(const int32_t* __restrict__ row_gid, int64_t n, const int64_t* __restrict__ seg_row0,
+                                  const int32_t* __restrict__ seg_slot, int n_segs, uint64_t* __restrict__ keys,
+                                  uint32_t* __restrict__ vals) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int slot = seg_slot[segment_of(seg_row0, n_segs, r)];
+    keys[r] = ((uint64_t)(uint32_t)slot << 32) | (uint32_t)row_gid[r];
+    vals[r] = (uint32_t)r;
+  }
+}
+
+__global__ void order_out_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t n,
+                                 int64_t* __restrict__ order, int32_t* __restrict__ canon_gid) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    order[i] = (int64_t)vals[i];
+    if (canon_gid) canon_gid[i] = (int32_t)(uint32_t)keys[i];
+  }
+}
+
 __global__ void scatter_add_rows_kernel(const float* __restrict__ src, int src_width, int dst_width, int used,
                                         const int64_t* __restrict__ idx, int64_t n, float* __restrict__ dst) {
   const int64_t total = n * used;
@@ -220,8 +249,14 @@ extern "C" int32_t bs_dest_compact(const uint32_t* dest_mask, int64_t n_rows, in
 
 extern "C" int32_t bs_gather_rows(const float* src, int32_t width, const int64_t* idx, int64_t n, float* dst,
                                   void* stream) {
-  BS_REQUIRE(width > 0 && width % 4 == 0, BS_ERR_PARAMETER, "row width must be a multiple of 4 floats");
+  BS_REQUIRE(width > 0, BS_ERR_PARAMETER, "row width must be >= 1");
   if (n <= 0) return BS_OK;
+  if (width % 4 != 0) {
+    gather_words_kernel<<<grid_for(n * width, 256), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const uint32_t*>(src), width, idx, n, reinterpret_cast<uint32_t*>(dst));
+    BS_LAUNCH_CHECK("gather_words_kernel");
+    return BS_OK;
+  }
   gather_rows_kernel<<<grid_for(n * (width / 4), 256), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4*>(src), width / 4, idx, n, reinterpret_cast<float4*>(dst));
   BS_LAUNCH_CHECK("gather_rows_kernel");
@@ -235,5 +270,39 @@ extern "C" int32_t bs_scatter_add_rows(const float* src, int32_t src_width, int3
   scatter_add_rows_kernel<<<grid_for(n * used, 256), 256, 0, as_stream(stream)>>>(src, src_width, dst_width, used, idx,
                                                                                   n, dst);
   BS_LAUNCH_CHECK("scatter_add_rows_kernel");
+  return BS_OK;
+}
+
+extern "C" size_t bs_canonical_order_workspace(int64_t n_rows) {
+  const int64_t n = n_rows > 0 ? n_rows : 1;
+  const size_t a = ((size_t)n * 8 + 255) & ~(size_t)255, b = ((size_t)n * 4 + 255) & ~(size_t)255;
+  return 2 * a + 2 * b + bs_radix_sort_workspace(n);
+}
+
+extern "C" int32_t bs_canonical_order(const int32_t* row_gid, int64_t n_rows, const int64_t* seg_row0,
+                                      const int32_t* seg_slot, int32_t n_segs, int32_t n_slots, int64_t* order,
+                                      int32_t* canon_gid, void* workspace, size_t ws_bytes, void* stream) {
+  BS_REQUIRE(n_slots >= 1 && n_segs >= 1, BS_ERR_PARAMETER, "canonical_order needs >= 1 slot and segment");
+  BS_REQUIRE(ws_bytes >= bs_canonical_order_workspace(n_rows), BS_ERR_CAPACITY, "canonical_order workspace too small");
+  if (n_rows <= 0) return BS_OK;
+  const int64_t n = n_rows;
+  const size_t a = ((size_t)n * 8 + 255) & ~(size_t)255, b = ((size_t)n * 4 + 255) & ~(size_t)255;
+  char* w = static_cast<char*>(workspace);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(w);
+  uint64_t* keys_alt = reinterpret_cast<uint64_t*>(w + a);
+  uint32_t* vals = reinterpret_cast<uint32_t*>(w + 2 * a);
+  uint32_t* vals_alt = reinterpret_cast<uint32_t*>(w + 2 * a + b);
+  void* sort_ws = w + 2 * a + 2 * b;
+  cudaStream_t s = as_stream(stream);
+  order_keys_kernel<<<grid_for(n, 256), 256, 0, s>>>(row_gid, n, seg_row0, seg_slot, n_segs, keys, vals);
+  BS_LAUNCH_CHECK("order_keys_kernel");
+  int bits = 1;
+  while ((1 << bits) < n_slots) ++bits;
+  // keys sorted stably on [0, 32 + bits): ids are unique within a slot
+  const int32_t st = bs_radix_sort_u64(keys, vals, keys_alt, vals_alt, n, nullptr, 0, 32 + bits, sort_ws,
+                                       bs_radix_sort_workspace(n), stream);
+  if (st) return st;
+  order_out_kernel<<<grid_for(n, 256), 256, 0, s>>>(keys, vals, n, order, canon_gid);
+  BS_LAUNCH_CHECK("order_out_kernel");
   return BS_OK;
 }

@@ -93,6 +93,8 @@ struct ProjArgs {
   int gsp_standard;  // 3DGS G_SP rows: 0 = raster moments (default), 1 = dL/dSP
   const int32_t* chunk_prefix;  // [ng][gridDim.y][B] rows before each chunk, or NULL
   float* gsp_zero;              // G_SP rows cleared alongside the SP rows (project_fwd), or NULL
+  const int32_t* point_gid;     // global id per local point (project_fwd), or NULL (= local index)
+  int32_t* row_gid;             // per SP row: global id of its point (project_fwd), or NULL
 };
 
 // Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
@@ -195,6 +197,7 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
         M::forward(pt, pre, sh, s_cam[v], a.n_sh, f);
         const int64_t row = s_row0[v] + rk.row_offset(v);
         M::write(sp + row * M::kSP, f);
+        if (a.row_gid) a.row_gid[row] = a.point_gid ? a.point_gid[i] : i;
         if (a.gsp_zero) {
           float4* z = reinterpret_cast<float4*>(a.gsp_zero + row * M::kGSP);
 #pragma unroll
@@ -544,7 +547,8 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
   if (n_groups == 0) return BS_OK;
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, d->gsp_zero};
+             view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, d->gsp_zero,
+             d->point_gid, d->row_gid};
   const dim3 grid = proj_grid(d, n_groups);
   const size_t smem = sizeof(float4) * 12 * kProjThreads;
   auto launch = [&](auto kern) {
@@ -566,7 +570,8 @@ extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, in
   if (n_groups == 0) return BS_OK;
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, d->gsp_zero};
+             view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, nullptr,
+             nullptr, nullptr};
   const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
     project_bwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(
@@ -602,7 +607,8 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   if (n_groups == 0) return BS_OK;
   const int n_sh = (pd->sh_degree + 1) * (pd->sh_degree + 1);
   ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
-             view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr, nullptr};
+             view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr, nullptr,
+             nullptr, nullptr};
   AdamConsts c = make_adam(ad);
   const size_t smem = sizeof(float) * 48 * kProjThreads + sizeof(float4) * 12 * kProjThreads;
   auto launch = [&](auto kern) {

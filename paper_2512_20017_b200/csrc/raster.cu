@@ -12,10 +12,14 @@
 // compacts them with a ballot into warp-private shared memory and blends
 // them in depth order.  Per pixel (centre (x + 0.5, y + 0.5)):
 //   power = -0.5 q = -0.5 (A dx^2 + C dy^2) - B dx dy,  dx = u - px
-//   alpha = min(0.99, opacity * exp(power)); skipped if power > 0, q > 9
-//   (outside the 3-sigma ellipse) or alpha < 1/255; a pixel stops before the
-//   splat that would bring its transmittance below 1e-4 (standard 3DGS
-//   conventions).
+//   alpha = min(0.99, opacity * exp(power)); the pair contributes iff
+//   q <= k, k = min(9, 2 ln(255 opacity)) -- the 3-sigma cut and the
+//   alpha >= 1/255 test as ONE threshold on the exponent, per splat from the
+//   shared deterministic log (support_k), so the decision never depends on
+//   the exp approximation and is the oracle's bit for bit; a pixel stops
+//   before the splat that would bring its transmittance below 1e-4
+//   (standard 3DGS conventions; deviations from gsplat
+//   v1.4.0 in DESIGN.md §3).
 // The conic is staged pre-scaled by -log2(e)/2 (B by -log2(e)) so the
 // exponent is one ex2.approx; forward and backward evaluate alpha with the
 // same instructions, so their skip / stop decisions agree exactly.
@@ -34,11 +38,10 @@
 namespace bs {
 namespace {
 
-constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kAlphaMax = 0.99f;
 constexpr float kTMin = 1e-4f;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kP2Min = -4.5f * kLog2e;  // q > 9 (outside the 3-sigma ellipse): no contribution
+constexpr float kHalfLog2e = -0.5f * kLog2e;  // p2 = power * log2(e) = q * kHalfLog2e
 #ifndef BS_SPARSE_LANES
 // swept on B200 (C2, 128-bit REDs): 6 2.18, 8 2.11, 10 2.07, 12 2.06, 16 2.15, 32 3.25 ms
 #define BS_SPARSE_LANES 12
@@ -90,13 +93,17 @@ __device__ __forceinline__ float splat_power2(F2 uv, F2 k, float kb, F2 npx, F2&
   return __fadd_rn(__fmaf_rn(kb, __fmul_rn(dd.x, dd.y), t.x), t.y);
 }
 
-// Warp-private staging: a = (u, v, kA, kC), b = (kB, opacity, r, g), c = b-channel
+// Warp-private staging: a = (u, v, kA, kC), b = (kB, opacity, r, g),
+// c = (b-channel, th2): th2 = the exponent threshold k * (-log2(e) / 2)
 struct WarpSmem {
   float4 a[32];
   float4 b[32];
-  float c[32];
+  float2 c[32];
   uint32_t row[32];
 };
+
+// Lowest log2-exponent of the splat's support: p2 >= th2 <=> q <= k.
+__device__ __forceinline__ float support_p2(float opacity) { return __fmul_rn(support_k(opacity), kHalfLog2e); }
 
 // One gathered splat (register prefetch of the next chunk).
 struct Splat {
@@ -142,9 +149,9 @@ __device__ __forceinline__ bool reaches(const Splat& f, float x0, float x1, floa
 }
 
 __device__ __forceinline__ void stage(WarpSmem& s, int lane, const Splat& f) {
-  s.a[lane] = make_float4(f.p0.x, f.p0.y, f.p0.w * (-0.5f * kLog2e), f.p1.y * (-0.5f * kLog2e));
-  s.b[lane] = make_float4(f.p1.x * -kLog2e, f.p0.z, f.p1.z, f.p1.w);
-  s.c[lane] = f.b;
+  s.a[lane] = make_float4(f.p0.x, f.p0.y, __fmul_rn(f.p0.w, kHalfLog2e), __fmul_rn(f.p1.y, kHalfLog2e));
+  s.b[lane] = make_float4(__fmul_rn(f.p1.x, -kLog2e), f.p0.z, f.p1.z, f.p1.w);
+  s.c[lane] = make_float2(f.b, support_p2(f.p0.z));
   s.row[lane] = f.row;
 }
 
@@ -176,12 +183,12 @@ struct PixelFwd {
   bool done;
 };
 
-__device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float4& sb, float cb, F2 npx, int rel) {
+__device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float4& sb, float cb, float th2, F2 npx,
+                                      int rel) {
   F2 d;
   const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
-  if (power2 > 0.f || power2 < kP2Min) return;
+  if (power2 > 0.f || power2 < th2) return;
   const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, ex2_approx(power2)));
-  if (alpha < kAlphaMin) return;
   const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
   if (nT < kTMin) {
     p.done = true;
@@ -196,15 +203,15 @@ __device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float
 
 // blend() with one early-out (the support test, mostly warp-uniform) and
 // selects for the rest; same arithmetic as blend().
-__device__ __forceinline__ void blend_sel(PixelFwd& p, const float4& sa, const float4& sb, float cb, F2 npx, int rel) {
+__device__ __forceinline__ void blend_sel(PixelFwd& p, const float4& sa, const float4& sb, float cb, float th2, F2 npx,
+                                          int rel) {
   F2 d;
   const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
-  if (power2 > 0.f || power2 < kP2Min) return;
+  if (power2 > 0.f || power2 < th2) return;
   const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, ex2_approx(power2)));
   const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
-  const bool ok = !(alpha < kAlphaMin);
-  const bool fin = ok && nT < kTMin;
-  const bool c = ok && !fin;
+  const bool fin = nT < kTMin;
+  const bool c = !fin;
   const float w = __fmul_rn(alpha, p.T);
   const F2 c01 = fma2(f2(sb.z, sb.w), bcast(w), p.c01);
   const float c2 = __fmaf_rn(cb, w, p.c2);
@@ -260,14 +267,14 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
       bits &= bits - 1;
       const float4 sa = s.a[j];
       const float4 sb = s.b[j];
-      const float cb = s.c[j];
+      const float2 sc = s.c[j];
       const int rel = b0 + j - rg.x;
       if constexpr (PPL == 1) {
-        if (!p[0].done) blend_sel(p[0], sa, sb, cb, f2(-pxf, -((float)q.py0 + 0.5f)), rel);
+        if (!p[0].done) blend_sel(p[0], sa, sb, sc.x, sc.y, f2(-pxf, -((float)q.py0 + 0.5f)), rel);
       } else {
 #pragma unroll
         for (int k = 0; k < PPL; ++k)
-          if (!p[k].done) blend(p[k], sa, sb, cb, f2(-pxf, -((float)(q.py0 + k) + 0.5f)), rel);
+          if (!p[k].done) blend(p[k], sa, sb, sc.x, sc.y, f2(-pxf, -((float)(q.py0 + k) + 0.5f)), rel);
       }
     }
     __syncwarp();
@@ -365,15 +372,14 @@ struct PixelBwd {
 // in front of it: acc' = acc + alpha (c - acc) after the splat.  kBg: the
 // background is not black (adds its transmittance term to dL/dalpha).
 template <bool kAssign, bool kBg>
-__device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const float4& sb, float cb, F2 npx,
+__device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const float4& sb, float cb, float th2, F2 npx,
                                            float g[9]) {
   F2 d;
   const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
-  if (power2 > 0.f || power2 < kP2Min) return false;
+  if (power2 > 0.f || power2 < th2) return false;
   const float ex = ex2_approx(power2);
   const float raw = __fmul_rn(sb.y, ex);
   const float alpha = fminf(kAlphaMax, raw);
-  if (alpha < kAlphaMin) return false;
   const float ra = rcp_approx(1.f - alpha);  // alpha <= 0.99
   p.T = p.T * ra;
   const float fac = alpha * p.T;
@@ -414,14 +420,14 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
 // what goes is the divergent-branch bookkeeping (BSSY/BSYNC, three branches
 // and their reconvergence stalls) in the hottest loop of the backward.
 template <bool kBg>
-__device__ __forceinline__ bool pixel_grad_sel(PixelBwd& p, const float4& sa, const float4& sb, float cb, F2 npx,
-                                               bool live, float g[9]) {
+__device__ __forceinline__ bool pixel_grad_sel(PixelBwd& p, const float4& sa, const float4& sb, float cb, float th2,
+                                               F2 npx, bool live, float g[9]) {
   F2 d;
   const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
   const float ex = ex2_approx(fminf(power2, 0.f));
   const float raw = __fmul_rn(sb.y, ex);
   const float alpha = fminf(kAlphaMax, raw);
-  const bool ok = live && !(power2 > 0.f || power2 < kP2Min) && !(alpha < kAlphaMin);
+  const bool ok = live && !(power2 > 0.f || power2 < th2);
   const float ra = rcp_approx(1.f - alpha);  // alpha <= 0.99
   const float T = p.T * ra;
   const float fac = alpha * T;
@@ -531,16 +537,17 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
       float g[9];
       const float4 sa = s.a[j];
       const float4 sb = s.b[j];
-      const float cb = s.c[j];
+      const float2 sc = s.c[j];
       bool any = false;
       if constexpr (PPL == 1) {
-        any = pixel_grad_sel<kBg>(p[0], sa, sb, cb, f2(-pxf, -((float)q.py0 + 0.5f)), rel < p[0].n, g);
+        any = pixel_grad_sel<kBg>(p[0], sa, sb, sc.x, sc.y, f2(-pxf, -((float)q.py0 + 0.5f)), rel < p[0].n, g);
       } else {
 #pragma unroll
         for (int k = 0; k < 9; ++k) g[k] = 0.f;
 #pragma unroll
         for (int k = 0; k < PPL; ++k)
-          if (rel < p[k].n) any |= pixel_grad<false, kBg>(p[k], sa, sb, cb, f2(-pxf, -((float)(q.py0 + k) + 0.5f)), g);
+          if (rel < p[k].n)
+            any |= pixel_grad<false, kBg>(p[k], sa, sb, sc.x, sc.y, f2(-pxf, -((float)(q.py0 + k) + 0.5f)), g);
       }
       const uint32_t who = __ballot_sync(0xffffffffu, any);
       if (who == 0u) continue;

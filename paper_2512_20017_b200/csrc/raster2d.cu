@@ -7,10 +7,14 @@
 // memory.  Per pixel (centre x + 0.5, y + 0.5):
 //   h_x = M_row0 - x M_row2, h_y = M_row1 - y M_row2, zeta = h_x x h_y,
 //   (u, v) = zeta.xy / zeta.z,  g3 = u^2 + v^2,  g2 = 2 |mean2d - pixel|^2,
-//   alpha = min(0.99, opacity exp(-0.5 min(g3, g2))) -- same skip / stop
-// rules as 3DGS, and (as the 3DGS 3-sigma ellipse) pairs with
-// min(g3, g2) > 9 are skipped.  Footprint filter: the projection's support
-// box (see reaches2).
+//   alpha = min(0.99, opacity exp(-0.5 min(g3, g2))); the pair contributes
+// iff min(g3, g2) <= k, k = min(9, 2 ln(255 opacity)) (the 3-sigma cut and
+// alpha >= 1/255 as one threshold, as in 3DGS), decided WITHOUT the division:
+// g3 <= k <=> zx^2 + zy^2 <= k zz^2, and the disk branch of the min iff
+// zx^2 + zy^2 <= g2 zz^2 -- explicit round-to-nearest ops, so the decisions
+// are the oracle's bit for bit while u, v use one approximate reciprocal.
+// Same stop rule as 3DGS.  Footprint filter: the projection's support box
+// (see reaches2).
 // Per pixel zeta is affine in the pixel (staging computes it at the region
 // origin and its two increments), so the backward accumulates the moments of
 // dL/dzeta instead of dL/dM (include/splat_b200.h, 2DGS G_SP row).
@@ -26,7 +30,6 @@ namespace {
 
 constexpr int kW2 = 8;  // warps per 16x16 tile (8x4 region each)
 constexpr int kT2 = 32 * kW2;
-constexpr float kAMin = 1.0f / 255.0f;
 constexpr float kAMax = 0.99f;
 constexpr float kTStop = 1e-4f;
 constexpr float kLog2e2 = 1.4426950408889634f;
@@ -156,18 +159,18 @@ __device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f, floa
   s.a[lane] = make_float4(f.p[0].x, f.p[0].y, f.p[0].z, z0[2]);
   s.b[lane] = make_float4(z0[0], z0[1], zb[0], zb[1]);
   s.c[lane] = make_float4(zc[0], zc[1], zb[2], zc[2]);
-  s.d[lane] = f.p[3];  // (r, g, b, depth)
+  s.d[lane] = make_float4(f.p[3].x, f.p[3].y, f.p[3].z, support_k(f.p[0].z));  // (r, g, b, k)
   s.row[lane] = f.row;
 }
 
 struct Eval2 {
   float z[3], iz, u, v, g3, dx, dy, g2, power;
-  bool ok;
+  bool ok, in, disk;  // z.z != 0; min(g3, g2) <= k; g3 <= g2 (division-free, exact)
 };
 
 // Bit-identical in forward and backward (explicit round-to-nearest ops).
 // (ox, oy): the pixel's offset from the region origin (small integers).
-__device__ __forceinline__ void eval2(const float4& a, const float4& b, const float4& c, float px, float py,
+__device__ __forceinline__ void eval2(const float4& a, const float4& b, const float4& c, float k, float px, float py,
                                       float ox, float oy, Eval2& e) {
   // (z.x, z.y) as a packed pair; each lane is the same FMA chain as z.z
   const float2 zxy = unf2(fma2(f2(c.x, c.y), bcast(oy), fma2(f2(b.z, b.w), bcast(ox), f2(b.x, b.y))));
@@ -187,6 +190,9 @@ __device__ __forceinline__ void eval2(const float4& a, const float4& b, const fl
   e.dy = dd.y;
   e.g2 = __fmul_rn(2.f, __fmaf_rn(e.dx, e.dx, __fmul_rn(e.dy, e.dy)));
   e.power = __fmul_rn(-0.5f, fminf(e.g3, e.g2));
+  const float n3 = __fmaf_rn(e.z[0], e.z[0], __fmul_rn(e.z[1], e.z[1])), zz = __fmul_rn(e.z[2], e.z[2]);
+  e.in = e.ok && (n3 <= __fmul_rn(k, zz) || e.g2 <= k);
+  e.disk = n3 <= __fmul_rn(e.g2, zz);
 }
 
 struct Px2 {
@@ -232,16 +238,15 @@ __global__ void __launch_bounds__(kT2, BS_R2_FWD_CTAS) raster2d_fwd_kernel(R2Arg
       if (p.done) continue;
       Eval2 e;
       const float4 sa = s.a[j];
-      eval2(sa, s.b[j], s.c[j], pxf, pyf, oxf, oyf, e);
-      if (!e.ok || e.power > 0.f || e.power < -4.5f) continue;  // min(g3, g2) > 9: outside the 3-sigma support
+      const float4 col = s.d[j];
+      eval2(sa, s.b[j], s.c[j], col.w, pxf, pyf, oxf, oyf, e);
+      if (!e.in) continue;  // min(g3, g2) > k: outside the support
       // past the support test: selects instead of branches
       const float alpha = fminf(kAMax, __fmul_rn(sa.z, ex2a(__fmul_rn(e.power, kLog2e2))));
       const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
-      const bool ok = !(alpha < kAMin);
-      const bool fin = ok && nT < kTStop;
-      const bool c = ok && !fin;
+      const bool fin = nT < kTStop;
+      const bool c = !fin;
       const float wgt = __fmul_rn(alpha, p.T);
-      const float4 col = s.d[j];
       p.done = p.done || fin;
       p.c0 = c ? __fmaf_rn(col.x, wgt, p.c0) : p.c0;
       p.c1 = c ? __fmaf_rn(col.y, wgt, p.c1) : p.c1;
@@ -381,14 +386,14 @@ __global__ void __launch_bounds__(kT2, BS_R2_BWD_CTAS) raster2d_bwd_kernel(
       // arithmetic as a branchy version for the contributing ones)
       float g[16];
       const float4 sa = s.a[j];
+      const float4 col = s.d[j];
       Eval2 e;
-      eval2(sa, s.b[j], s.c[j], pxf, pyf, oxf, oyf, e);
+      eval2(sa, s.b[j], s.c[j], col.w, pxf, pyf, oxf, oyf, e);
       const float ex = ex2a(__fmul_rn(fminf(e.power, 0.f), kLog2e2));
       const float raw = __fmul_rn(sa.z, ex);
       const float alpha = fminf(kAMax, raw);
-      const bool any = rel < q.n && e.ok && e.power <= 0.f && e.power >= -4.5f && alpha >= kAMin;
+      const bool any = rel < q.n && e.in;
       {
-        const float4 col = s.d[j];
         const float ra = rcpa(1.f - alpha);  // alpha <= 0.99
         const float T = q.T * ra;
         const float fac = any ? alpha * T : 0.f;
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(kT2, BS_R2_BWD_CTAS) raster2d_bwd_kernel(
         // disk term: power = -0.5 (u^2 + v^2), (u, v) = zeta.xy / zeta.z; G_SP2
         // carries the moments sum gz, sum gz px, sum gz py of dL/dzeta (the
         // projection backward applies the M rows)
-        const bool disk = grad && e.g3 <= e.g2;
+        const bool disk = grad && e.disk;
         const F2 guv = mul2(f2(e.u, e.v), bcast(-dpow));  // dL/d(u, v)
         const float2 g_uv = unf2(guv);
         const float iz = e.iz;

@@ -180,6 +180,13 @@ class SplatExchange:
         self.bytes_fwd += remote * width * sp_send.element_size()
         return self._a2a(sp_send, lay.send_rows, lay.recv_rows, width)
 
+    def forward_ids(self, row_gid: torch.Tensor, lay: StepLayout) -> torch.Tensor:
+        """Global point id (int32) of every row sent by forward(): the
+        receiver's canonical tie order (4 B per row, counted in bytes_fwd)."""
+        remote = sum(r for d, r in enumerate(lay.send_rows) if d != self.rank)
+        self.bytes_fwd += remote * row_gid.element_size()
+        return self._a2a(row_gid, lay.send_rows, lay.recv_rows, 1).view(-1)
+
     def backward(self, g_recv: torch.Tensor, lay: StepLayout, width: int) -> torch.Tensor:
         """Splat-state gradients back to the owners of the points (line 21)."""
         remote = sum(r for s, r in enumerate(lay.recv_rows) if s != self.rank)

@@ -98,12 +98,17 @@ class SplatTrainer:
     [15, S, 4] float32 shard (ascending global point index); `group_begin`
     (int32, n_groups+1) and `aabb` (float32, n_groups x 6) describe its point
     groups; `views` are all dataset views (the batch picks from them);
-    `gt` is u8 [n_views, H, W, 3] (device-resident ground truth)."""
+    `gt` is u8 [n_views, H, W, 3] (device-resident ground truth);
+    `global_ids` (int [S], ascending) the global point index of every shard
+    point (default: the local index, i.e. a single rank holding every point).
+    With several ranks the received splat rows of every rendered view are put
+    in ascending global-id order before binning (bs_canonical_order), so the
+    per-tile lists are the single-rank lists on any number of ranks."""
 
     def __init__(self, params: np.ndarray, group_begin: np.ndarray, aabb: np.ndarray, views, gt=None,
                  sh_degree: int = 3, adam: AdamConfig | None = None, device=None, comm=None,
                  bg=(0.0, 0.0, 0.0), model: str = "3dgs", presence: np.ndarray | None = None,
-                 gt_view_ids=None, patches: int = 1):
+                 gt_view_ids=None, patches: int = 1, global_ids: np.ndarray | None = None):
         nat.load()
         if model not in ("3dgs", "2dgs"):
             raise ValueError(f"unknown splat model {model!r} (3dgs | 2dgs)")
@@ -143,6 +148,13 @@ class SplatTrainer:
         self.cams_all = torch.as_tensor(camera_bytes(self.views), device=self.dev)
         # 4DGS spatio-temporal culling (visibility.py:244-252):
         # point i is a candidate for view v iff presence[i, 0] <= t_v <= presence[i, 1] (f32)
+        self.global_ids = None
+        if global_ids is not None:
+            gid = np.asarray(global_ids, dtype=np.int64)
+            if gid.shape != (self.S,) or (len(gid) and (np.any(np.diff(gid) <= 0) or gid[0] < 0 or gid[-1] >= 2**31)):
+                raise ValueError("global_ids must be ascending int32-range point indices, one per shard point")
+            self.global_ids = torch.as_tensor(gid.astype(np.int32), device=self.dev)
+        self.record_row_gid = False  # single rank: also write the rows' global ids (tests)
         self.presence = self.view_times = None
         if presence is not None:
             pres = np.ascontiguousarray(presence, dtype=np.float32)
@@ -285,7 +297,12 @@ class SplatTrainer:
         lay = None
         pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group, 0,
                              nat.ptr(chunk_prefix))
+        pdesc.point_gid = nat.ptr(self.global_ids)
         early = self.comm is None and S * B * self.sp_floats * 4 <= self.sp_capacity_bytes
+        row_gid = None
+        if self.comm is not None or self.record_row_gid:
+            row_gid = self.buf.get("row_gid", max(S * B, 1), torch.int32)
+            pdesc.row_gid = nat.ptr(row_gid)
         if early:
             # the row counts start towards the host before the projection is
             # queued, so the host resumes while the projection still runs
@@ -332,7 +349,10 @@ class SplatTrainer:
                          nat.ptr(sp), st)
         if lay is None:
             # every batch view is rendered here (N = 1: W[v] = k for all v):
-            # one segment per view, starting at the scan's view_row0
+            # one segment per view, starting at the scan's view_row0; the rows
+            # of a view are in ascending point order, the canonical order
+            if row_gid is not None:
+                self.last["row_gid"] = row_gid[:n_rows]
             seg_row0 = view_row0
             seg_slot = self._slot_ids(B)
             losses, gsp = self._render_and_backward(sp, n_rows, seg_row0, seg_slot, B, cams, bidx, gt_batch,
@@ -341,21 +361,27 @@ class SplatTrainer:
             # SP all-to-all to the rendering ranks (line 9), render, G_SP back (line 21)
             with self._t("a2a_fwd"):
                 sp_recv = self.comm.forward(sp[: n_rows * self.sp_floats], lay, self.sp_floats)
+                gid_recv = self.comm.forward_ids(row_gid[:n_rows], lay)
             mine = torch.as_tensor(lay.my_views, device=dev)
-            seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(lay.seg_rows)[:-1]]).astype(np.int64),
-                                       device=dev)
-            seg_slot = torch.as_tensor(lay.seg_slot, device=dev)
+            n_slots = len(lay.my_views)
+            # received rows in canonical order: per rendered view, ascending global id
+            slot_rows = np.bincount(lay.seg_slot, weights=lay.seg_rows, minlength=n_slots).astype(np.int64)
+            sp_c, order = self._canonical(sp_recv.reshape(-1), gid_recv, lay.n_recv, lay.seg_rows, lay.seg_slot,
+                                          n_slots)
+            seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(slot_rows)[:-1]]).astype(np.int64), device=dev)
+            seg_slot = self._slot_ids(n_slots)
             gt_slots = None
             if gt_batch is not None:
                 gt_slots = gt_batch.index_select(0, mine).contiguous()
-            losses, gsp_recv = self._render_and_backward(sp_recv.reshape(-1), lay.n_recv, seg_row0, seg_slot,
-                                                         len(lay.my_views), cams.index_select(0, mine).contiguous(),
-                                                         bidx.index_select(0, mine), gt_slots)
+            losses, gsp_c = self._render_and_backward(sp_c, lay.n_recv, seg_row0, seg_slot, n_slots,
+                                                      cams.index_select(0, mine).contiguous(),
+                                                      bidx.index_select(0, mine), gt_slots)
             with self._t("a2a_bwd"):
-                # only the used floats of a G_SP row travel (3DGS: 9 of the 12)
+                # back to the received order, only the used floats of a G_SP
+                # row (3DGS: 9 of the 12), then to the owners
                 wire = self.gsp_wire_floats
-                g = gsp_recv[: lay.n_recv * self.gsp_floats].view(-1, self.gsp_floats)
-                back = self.comm.backward(g[:, :wire].contiguous().reshape(-1), lay, wire).view(-1, wire)
+                g = self._uncanonical(gsp_c, order, lay.n_recv, wire)
+                back = self.comm.backward(g, lay, wire).view(-1, wire)
                 if wire != self.gsp_floats:
                     full = self.buf.get("gsp_home", max(back.shape[0], 1) * self.gsp_floats, torch.float32)
                     full = full[: back.shape[0] * self.gsp_floats].view(-1, self.gsp_floats)
@@ -396,6 +422,8 @@ class SplatTrainer:
         sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
         pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group, 0,
                              nat.ptr(chunk_prefix))
+        row_gid = self.buf.get("row_gid", max(n_rows, 1), torch.int32)
+        pdesc.point_gid, pdesc.row_gid = nat.ptr(self.global_ids), nat.ptr(row_gid)
         with self._t("project"):
             nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask), nat.ptr(self.group_begin),
                      self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(sp), st)
@@ -421,9 +449,12 @@ class SplatTrainer:
         recv_rows = [int(x) for x in recv_v.sum(axis=1)]
         send_sp = self.buf.get("send_sp", max(n_send, 1) * self.sp_floats, torch.float32)
         nat.call("bs_gather_rows", nat.ptr(sp), self.sp_floats, nat.ptr(send_idx), n_send, nat.ptr(send_sp), st)
+        send_gid = self.buf.get("send_gid", max(n_send, 1), torch.int32)
+        nat.call("bs_gather_rows", nat.ptr(row_gid), 1, nat.ptr(send_idx), n_send, nat.ptr(send_gid), st)
         with self._t("a2a_fwd"):
             sp_recv = comm._a2a(send_sp[: n_send * self.sp_floats], send_rows, recv_rows, self.sp_floats)
-        comm.bytes_fwd += (n_send - send_rows[me]) * self.sp_floats * 4
+            gid_recv = comm._a2a(send_gid[:n_send], send_rows, recv_rows, 1).view(-1)
+        comm.bytes_fwd += (n_send - send_rows[me]) * (self.sp_floats + 1) * 4
         # ---- render the own patches of every view that has one here
         Wm = np.asarray(W, dtype=np.int64).reshape(B, PP)
         my_views = [v for v in range(B) if (Wm[v] == me).any()]
@@ -437,19 +468,22 @@ class SplatTrainer:
         n_recv = int(sum(recv_rows))
         self.last.update(my_views=my_views, send_rows=send_rows, recv_rows=recv_rows, n_send=n_send)
         losses = torch.zeros(0, dtype=torch.float32, device=dev)
-        gsp_recv = self.buf.get("gsp_recv_p", max(n_recv, 1) * self.gsp_floats, torch.float32)
+        wire = self.gsp_wire_floats
+        g = self.buf.get("gsp_wire", max(n_recv, 1) * wire, torch.float32)[: n_recv * wire]
         if my_views:
+            n_slots = len(my_views)
             mine = torch.as_tensor(my_views, dtype=torch.int64, device=dev)
-            seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(seg_rows)[:-1]]).astype(np.int64), device=dev)
-            seg_slot_t = torch.as_tensor(np.asarray(seg_slot, dtype=np.int32), device=dev)
+            # canonical order of the received rows (per slot, ascending global id)
+            sp_c, order = self._canonical(sp_recv.reshape(-1), gid_recv, n_recv, seg_rows, seg_slot, n_slots)
+            slot_rows = np.bincount(np.asarray(seg_slot), weights=np.asarray(seg_rows), minlength=n_slots)
+            seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(slot_rows)[:-1]]).astype(np.int64), device=dev)
             bits_t = torch.as_tensor(slot_bits.view(np.int64), device=dev)
             gt_slots = gt_batch.index_select(0, mine).contiguous() if gt_batch is not None else None
-            losses, gsp_recv = self._render_and_backward(sp_recv.reshape(-1), n_recv, seg_row0, seg_slot_t,
-                                                         len(my_views), cams.index_select(0, mine).contiguous(),
-                                                         bidx.index_select(0, mine), gt_slots, slot_patches=bits_t)
+            losses, gsp_c = self._render_and_backward(sp_c, n_recv, seg_row0, self._slot_ids(n_slots), n_slots,
+                                                      cams.index_select(0, mine).contiguous(),
+                                                      bidx.index_select(0, mine), gt_slots, slot_patches=bits_t)
+            g = self._uncanonical(gsp_c, order, n_recv, wire)
         # ---- gradient rows back to their sources, summed into the row they left
-        wire = self.gsp_wire_floats
-        g = gsp_recv[: n_recv * self.gsp_floats].view(-1, self.gsp_floats)[:, :wire].contiguous()
         with self._t("a2a_bwd"):
             back = comm._a2a(g.reshape(-1), recv_rows, send_rows, wire)
         comm.bytes_bwd += (n_recv - recv_rows[me]) * wire * 4
@@ -464,6 +498,31 @@ class SplatTrainer:
                      nat.ptr(self.exp_avg_sq), S, nat.ptr(mask), nat.ptr(self.group_begin), self.n_groups,
                      nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
         return losses
+
+    def _canonical(self, sp_recv, gid_recv, n, seg_rows, seg_slot, n_slots):
+        """Received rows -> canonical order (slot-major, ascending global id;
+        bs_canonical_order).  Returns the reordered rows and `order`
+        (canonical position -> received row)."""
+        st, lib = nat.stream_handle(), nat.load()
+        seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(seg_rows)[:-1]]).astype(np.int64), device=self.dev)
+        seg_slot_t = torch.as_tensor(np.asarray(seg_slot, dtype=np.int32), device=self.dev)
+        order = self.buf.get("canon_order", max(n, 1), torch.int64)
+        cgid = self.buf.get("canon_gid", max(n, 1), torch.int32)
+        ws = self.buf.get("canon_ws", lib.bs_canonical_order_workspace(max(n, 1)), torch.uint8)
+        nat.call("bs_canonical_order", nat.ptr(gid_recv), n, nat.ptr(seg_row0), nat.ptr(seg_slot_t), len(seg_slot),
+                 n_slots, nat.ptr(order), nat.ptr(cgid), nat.ptr(ws), ws.numel(), st)
+        sp_c = self.buf.get("sp_canon", max(n, 1) * self.sp_floats, torch.float32)
+        nat.call("bs_gather_rows", nat.ptr(sp_recv), self.sp_floats, nat.ptr(order), n, nat.ptr(sp_c), st)
+        self.last["row_gid"] = cgid[:n]
+        return sp_c, order
+
+    def _uncanonical(self, gsp_c, order, n, wire):
+        """G_SP rows of the canonical order -> received order, `wire` floats each."""
+        g = self.buf.get("gsp_wire", max(n, 1) * wire, torch.float32)[: n * wire]
+        g.zero_()
+        nat.call("bs_scatter_add_rows", nat.ptr(gsp_c), self.gsp_floats, wire, nat.ptr(order), n, nat.ptr(g), wire,
+                 nat.stream_handle())
+        return g
 
     def _adam_desc(self):
         ad = nat.AdamDesc()

@@ -47,7 +47,8 @@ def _worker(rank, world, port, q, prefetch=False, patches=1):
         sizes = [g.groups[k].size for k in mine]
         gb = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
         tr = SplatTrainer(np.ascontiguousarray(params[:, pts, :]), gb, g.aabbs.reshape(-1, 6)[mine], ds.views,
-                          gt=gt, adam=AdamConfig(scenes.lr_table(50.0)), comm=SplatExchange(), patches=patches)
+                          gt=gt, adam=AdamConfig(scenes.lr_table(50.0)), comm=SplatExchange(), patches=patches,
+                          global_ids=pts)
         if prefetch:
             # step 1 starts the asynchronous placement of step 2 (stale W)
             tr.step(BATCH, next_batch=BATCH2)
@@ -61,9 +62,22 @@ def _worker(rank, world, port, q, prefetch=False, patches=1):
         n = len(my_views)
         img = tr.last["image"][: n * 96 * 160 * 3].cpu().numpy().reshape(n, 96, 160, 3) if n else None
         q.put((rank, pts, tr.params.cpu().numpy(), [batch[v] for v in my_views], img, losses,
-               tr.last["A"], tr.last["W"]))
+               tr.last["A"], tr.last["W"], _gid_lists(tr, n) if n else None))
     finally:
         dist.destroy_process_group()
+
+
+def _gid_lists(tr, n_slots):
+    """Per rendered slot and tile: the global ids of the tile's depth-sorted
+    instance list (rows mapped through the canonical row -> global id)."""
+    T = tr.tiles
+    rg = tr.last["ranges"][: n_slots * T * 2].cpu().numpy().reshape(n_slots, T, 2)
+    irows = tr.last["irows"][: tr.last["n_inst"]].cpu().numpy().astype(np.int64)
+    gid = tr.last["row_gid"].cpu().numpy()
+    out = []
+    for s in range(n_slots):
+        out.append([gid[irows[a:b]] if b > a else np.zeros(0, np.int32) for a, b in rg[s]])
+    return out
 
 
 def _port():
@@ -98,10 +112,12 @@ def test_two_ranks_match_single_rank(cuda, prefetch):
     ds, g, params, gt = _setup()
     lr = scenes.lr_table(50.0)
     tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt, adam=AdamConfig(lr))
+    tr.record_row_gid = True
     if prefetch:
         tr.step(BATCH)
     batch = BATCH2 if prefetch else BATCH
     losses = tr.step(batch).cpu().numpy()
+    lists_ref = _gid_lists(tr, len(batch))
     img_ref = tr.last["image"][: len(batch) * 96 * 160 * 3].cpu().numpy().reshape(len(batch), 96, 160, 3)
     after_ref = tr.params.cpu().numpy()
     A = res[0][6]
@@ -111,11 +127,19 @@ def test_two_ranks_match_single_rank(cuda, prefetch):
     for r in (0, 1):
         for slot, v in enumerate(res[r][3]):
             k = batch.index(v)
-            # second step (prefetch case): parameters after step 1 agree to
-            # the Adam tolerance below, so the images to the parity tolerance
-            tol = 1e-4 if prefetch else 1e-6
-            assert np.abs(res[r][4][slot] - img_ref[k]).max() <= tol, f"view {v}"
-            assert abs(res[r][5][slot] - losses[k]) <= tol
+            if not prefetch:
+                # canonical order (bs_canonical_order): the per-tile lists of
+                # global ids are the single-rank lists bit for bit, and so the
+                # forward image is bit-identical
+                for t, (a, b) in enumerate(zip(res[r][8][slot], lists_ref[k])):
+                    assert np.array_equal(a, b), f"view {v} tile {t}"
+                assert np.array_equal(res[r][4][slot], img_ref[k]), f"view {v}"
+                assert res[r][5][slot] == losses[k]
+            else:
+                # second step: parameters after step 1 agree to the Adam
+                # tolerance below, so the images to the parity tolerance
+                assert np.abs(res[r][4][slot] - img_ref[k]).max() <= 1e-4, f"view {v}"
+                assert abs(res[r][5][slot] - losses[k]) <= 1e-4
         pts, after = res[r][1], res[r][2]
         ref = after_ref[:, pts, :]
         lr_full = np.broadcast_to(lr.reshape(15, 1, 4), ref.shape)
@@ -168,7 +192,7 @@ def test_two_ranks_patches_match_single_rank(cuda):
             owner = int(W[k * P * P + j])
             slot = res[owner][3].index(v)
             img[ys[r_]:ys[r_ + 1], xs[c_]:xs[c_ + 1]] = res[owner][4][slot][ys[r_]:ys[r_ + 1], xs[c_]:xs[c_ + 1]]
-        assert np.abs(img - img_ref[k]).max() <= 1e-6, f"view {v}"
+        assert np.array_equal(img, img_ref[k]), f"view {v}"  # canonical order: bit-identical
         for r in (0, 1):
             if v in res[r][3]:
                 loss_sum[k] += res[r][5][res[r][3].index(v)]

@@ -67,5 +67,7 @@ def test_host_library_exports_every_declared_symbol():
 
 def test_proj_desc_layout():
     # bs_proj_desc: 7 int32 (n_views, sh_degree, tiles_x_max, tiles_y_max, model, max_group_points, gsp_form)
-    assert ctypes.sizeof(_native.ProjDesc) == 48
+    # + pad + 4 pointers (chunk_prefix, gsp_zero, point_gid, row_gid)
+    assert ctypes.sizeof(_native.ProjDesc) == 64
+    assert _native.ProjDesc.row_gid.offset == 56
     assert ctypes.sizeof(_native.CullDesc) == 40
