@@ -826,10 +826,21 @@ static void proj2_fwd(const opoint* pt, const or_camera* c, int n_sh, oproj2* f)
   f->depth = f->qc[2];
   f->u = f->c2[0] / f->c2[2];
   f->v = f->c2[1] / f->c2[2];
-  /* bounding box of the image of the disk u^2 + v^2 <= 9 (dual conic) */
-  const float* a = f->c0;
-  const float* b = f->c1;
-  const float* e = f->c2;
+  /* dual conics of the disk images in image coordinates centred on (u, v)
+   * (csrc/splat2d_math.cuh: the columns shifted to c' = (c.x - u c.z,
+   * c.y - v c.z, c.z), which avoids the ~0.1 px float cancellation of the
+   * absolute-coordinate box); same op sequence as the kernel */
+  float a[3], b[3], e[3];
+  a[0] = f->c0[0] - f->u * f->c0[2];
+  a[1] = f->c0[1] - f->v * f->c0[2];
+  a[2] = f->c0[2];
+  b[0] = f->c1[0] - f->u * f->c1[2];
+  b[1] = f->c1[1] - f->v * f->c1[2];
+  b[2] = f->c1[2];
+  e[0] = f->c2[0] - f->u * f->c2[2];
+  e[1] = f->c2[1] - f->v * f->c2[2];
+  e[2] = f->c2[2];
+  /* the image of the disk u^2 + v^2 <= 9 is a bounded ellipse */
   const float d22 = 9.f * (a[2] * a[2] + b[2] * b[2]) - e[2] * e[2];
   const float d02 = 9.f * (a[0] * a[2] + b[0] * b[2]) - e[0] * e[2];
   const float d12 = 9.f * (a[1] * a[2] + b[1] * b[2]) - e[1] * e[2];
@@ -859,10 +870,10 @@ static void proj2_fwd(const opoint* pt, const or_camera* c, int n_sh, oproj2* f)
       const float hx = sqrtf(fmaxf(bx * bx - k00 / k22, 0.f));
       const float hy = sqrtf(fmaxf(by * by - k11 / k22, 0.f));
       const float rc = sqrtf(0.5f * k);
-      const float x0 = fminf(bx - hx, f->u - rc), x1 = fmaxf(bx + hx, f->u + rc);
-      const float y0 = fminf(by - hy, f->v - rc), y1 = fmaxf(by + hy, f->v + rc);
-      f->box_cx = 0.5f * (x0 + x1);
-      f->box_cy = 0.5f * (y0 + y1);
+      const float x0 = fminf(bx - hx, -rc), x1 = fmaxf(bx + hx, rc);
+      const float y0 = fminf(by - hy, -rc), y1 = fmaxf(by + hy, rc);
+      f->box_cx = f->u + 0.5f * (x0 + x1);
+      f->box_cy = f->v + 0.5f * (y0 + y1);
       f->radius_x = 0.5f * (x1 - x0);
       f->radius_y = 0.5f * (y1 - y0);
     }

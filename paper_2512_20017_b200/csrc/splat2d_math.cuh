@@ -103,13 +103,29 @@ __device__ __forceinline__ void project2d_forward(const PointIn& pt, const Pre2D
   f.depth = z;
   f.u = fdiv(f.c2[0], f.c2[2]);
   f.v = fdiv(f.c2[1], f.c2[2]);
-  // dual conic of the 3-sigma disk: C*_ij = 9 (c0_i c0_j + c1_i c1_j) - c2_i c2_j
-  const float c22 = fsub(fmul(9.f, fadd(fmul(f.c0[2], f.c0[2]), fmul(f.c1[2], f.c1[2]))), fmul(f.c2[2], f.c2[2]));
-  const float c02 = fsub(fmul(9.f, fadd(fmul(f.c0[0], f.c0[2]), fmul(f.c1[0], f.c1[2]))), fmul(f.c2[0], f.c2[2]));
-  const float c12 = fsub(fmul(9.f, fadd(fmul(f.c0[1], f.c0[2]), fmul(f.c1[1], f.c1[2]))), fmul(f.c2[1], f.c2[2]));
-  const float c00 = fsub(fmul(9.f, fadd(fmul(f.c0[0], f.c0[0]), fmul(f.c1[0], f.c1[0]))), fmul(f.c2[0], f.c2[0]));
-  const float c11 = fsub(fmul(9.f, fadd(fmul(f.c0[1], f.c0[1]), fmul(f.c1[1], f.c1[1]))), fmul(f.c2[1], f.c2[1]));
-  f.valid = c22 < 0.f;  // the 3-sigma disk images to a bounded ellipse
+  // Dual conics of the disk images, in image coordinates CENTRED on (u, v):
+  // x - u = (p.x - u p.z) / p.z for p = c0 s + c1 t + c2, so the columns are
+  // shifted to c_i' = (c_i.x - u c_i.z, c_i.y - v c_i.z, c_i.z) (c2' ~ (0, 0, z)).
+  // In absolute pixel coordinates the box half-width comes out of
+  // bx^2 - C*00 / C*22 with bx ~ u ~ 10^3 px: a float cancellation of
+  // ~0.1 px.  C*_ij = s (c0'_i c0'_j + c1'_i c1'_j) - c2'_i c2'_j.
+  float a0[3], a1[3], a2[3];
+  a0[0] = fsub(f.c0[0], fmul(f.u, f.c0[2]));
+  a0[1] = fsub(f.c0[1], fmul(f.v, f.c0[2]));
+  a0[2] = f.c0[2];
+  a1[0] = fsub(f.c1[0], fmul(f.u, f.c1[2]));
+  a1[1] = fsub(f.c1[1], fmul(f.v, f.c1[2]));
+  a1[2] = f.c1[2];
+  a2[0] = fsub(f.c2[0], fmul(f.u, f.c2[2]));
+  a2[1] = fsub(f.c2[1], fmul(f.v, f.c2[2]));
+  a2[2] = f.c2[2];
+  // the 3-sigma disk (s = 9) images to a bounded ellipse
+  const float c22 = fsub(fmul(9.f, fadd(fmul(a0[2], a0[2]), fmul(a1[2], a1[2]))), fmul(a2[2], a2[2]));
+  const float c02 = fsub(fmul(9.f, fadd(fmul(a0[0], a0[2]), fmul(a1[0], a1[2]))), fmul(a2[0], a2[2]));
+  const float c12 = fsub(fmul(9.f, fadd(fmul(a0[1], a0[2]), fmul(a1[1], a1[2]))), fmul(a2[1], a2[2]));
+  const float c00 = fsub(fmul(9.f, fadd(fmul(a0[0], a0[0]), fmul(a1[0], a1[0]))), fmul(a2[0], a2[0]));
+  const float c11 = fsub(fmul(9.f, fadd(fmul(a0[1], a0[1]), fmul(a1[1], a1[1]))), fmul(a2[1], a2[1]));
+  f.valid = c22 < 0.f;
   f.radius_x = f.radius_y = 0.f;
   if (f.valid) {
     const float bx = fdiv(c02, c22), by = fdiv(c12, c22);
@@ -124,19 +140,19 @@ __device__ __forceinline__ void project2d_forward(const PointIn& pt, const Pre2D
     // support {min(g3, g2) <= k}, k = min(9, 2 ln(255 o)): the image of the
     // disk u^2 + v^2 <= k (dual conic, bounded since the 9-disk's is) united
     // with the low-pass circle |mean2d - pixel| <= sqrt(k / 2)
-    const float k22 = fsub(fmul(k, fadd(fmul(f.c0[2], f.c0[2]), fmul(f.c1[2], f.c1[2]))), fmul(f.c2[2], f.c2[2]));
-    const float k02 = fsub(fmul(k, fadd(fmul(f.c0[0], f.c0[2]), fmul(f.c1[0], f.c1[2]))), fmul(f.c2[0], f.c2[2]));
-    const float k12 = fsub(fmul(k, fadd(fmul(f.c0[1], f.c0[2]), fmul(f.c1[1], f.c1[2]))), fmul(f.c2[1], f.c2[2]));
-    const float k00 = fsub(fmul(k, fadd(fmul(f.c0[0], f.c0[0]), fmul(f.c1[0], f.c1[0]))), fmul(f.c2[0], f.c2[0]));
-    const float k11 = fsub(fmul(k, fadd(fmul(f.c0[1], f.c0[1]), fmul(f.c1[1], f.c1[1]))), fmul(f.c2[1], f.c2[1]));
-    const float bx = fdiv(k02, k22), by = fdiv(k12, k22);
+    const float k22 = fsub(fmul(k, fadd(fmul(a0[2], a0[2]), fmul(a1[2], a1[2]))), fmul(a2[2], a2[2]));
+    const float k02 = fsub(fmul(k, fadd(fmul(a0[0], a0[2]), fmul(a1[0], a1[2]))), fmul(a2[0], a2[2]));
+    const float k12 = fsub(fmul(k, fadd(fmul(a0[1], a0[2]), fmul(a1[1], a1[2]))), fmul(a2[1], a2[2]));
+    const float k00 = fsub(fmul(k, fadd(fmul(a0[0], a0[0]), fmul(a1[0], a1[0]))), fmul(a2[0], a2[0]));
+    const float k11 = fsub(fmul(k, fadd(fmul(a0[1], a0[1]), fmul(a1[1], a1[1]))), fmul(a2[1], a2[1]));
+    const float bx = fdiv(k02, k22), by = fdiv(k12, k22);  // ellipse centre - (u, v)
     const float hx = fsqrt(fmaxf(fsub(fmul(bx, bx), fdiv(k00, k22)), 0.f));
     const float hy = fsqrt(fmaxf(fsub(fmul(by, by), fdiv(k11, k22)), 0.f));
     const float rc = fsqrt(fmul(0.5f, k));
-    const float x0 = fminf(fsub(bx, hx), fsub(f.u, rc)), x1 = fmaxf(fadd(bx, hx), fadd(f.u, rc));
-    const float y0 = fminf(fsub(by, hy), fsub(f.v, rc)), y1 = fmaxf(fadd(by, hy), fadd(f.v, rc));
-    f.box_cx = fmul(0.5f, fadd(x0, x1));
-    f.box_cy = fmul(0.5f, fadd(y0, y1));
+    const float x0 = fminf(fsub(bx, hx), -rc), x1 = fmaxf(fadd(bx, hx), rc);
+    const float y0 = fminf(fsub(by, hy), -rc), y1 = fmaxf(fadd(by, hy), rc);
+    f.box_cx = fadd(f.u, fmul(0.5f, fadd(x0, x1)));
+    f.box_cy = fadd(f.v, fmul(0.5f, fadd(y0, y1)));
     f.radius_x = fmul(0.5f, fsub(x1, x0));
     f.radius_y = fmul(0.5f, fsub(y1, y0));
   }
