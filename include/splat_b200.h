@@ -228,6 +228,9 @@ typedef struct {
   int32_t* row_gid;            /* optional (bs_project_fwd): int32 per SP row, the
                                   global id of the row's point -- the canonical
                                   tie order of the receiving rank (bs_canonical_order) */
+  float* row_support;          /* optional (bs_project_fwd): f32 per SP row, the
+                                  support threshold the rasterisers test (see
+                                  bs_row_support), computed with the extents */
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,
@@ -313,6 +316,8 @@ typedef struct {
                            (r P + c) set = this slot renders patch (r, c); the
                            other pixels are neither rendered nor in the loss
                            (the view's loss normalisation is unchanged) */
+  const float* row_support; /* optional: f32 per SP row (bs_row_support); NULL =
+                           computed per staged splat (same values) */
 } bs_raster_desc;
 /* image: f32 [n_slots][H][W][3]; final_T: f32 [n_slots][H][W];
  * n_contrib: int32 [n_slots][H][W] (range-relative end of the blend);
@@ -431,6 +436,13 @@ int32_t bs_scatter_add_rows(const float* src, int32_t src_width, int32_t used,
  * rendered in slot seg_slot[s].  Outputs: order[i] = received row placed at
  * canonical position i (slot-major, ascending global id), canon_gid[i] (optional)
  * its global id. */
+/* Per-row support threshold of the rasterisers: a pixel pair contributes
+ * iff q <= k, k = min(9, 2 ln(255 o)) (include/ header notes);
+ * 3DGS rows store k * (-log2(e) / 2) (the threshold on the log2 exponent),
+ * 2DGS rows k.  Computed once per row (the projection writes it through
+ * bs_proj_desc.row_support; this entry recomputes it for received rows)
+ * instead of once per (warp, staged splat). */
+int32_t bs_row_support(const float* sp_rows, int32_t model, int64_t n_rows, float* out, void* stream);
 size_t bs_canonical_order_workspace(int64_t n_rows);
 int32_t bs_canonical_order(const int32_t* row_gid, int64_t n_rows, const int64_t* seg_row0,
                            const int32_t* seg_slot, int32_t n_segs, int32_t n_slots,

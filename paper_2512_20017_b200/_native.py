@@ -58,14 +58,15 @@ class ProjDesc(C.Structure):
     _fields_ = [("n_views", C.c_int32), ("sh_degree", C.c_int32),
                 ("tiles_x_max", C.c_int32), ("tiles_y_max", C.c_int32), ("model", C.c_int32),
                 ("max_group_points", C.c_int32), ("gsp_form", C.c_int32), ("chunk_prefix", C.c_void_p),
-                ("gsp_zero", C.c_void_p), ("point_gid", C.c_void_p), ("row_gid", C.c_void_p)]
+                ("gsp_zero", C.c_void_p), ("point_gid", C.c_void_p), ("row_gid", C.c_void_p),
+                ("row_support", C.c_void_p)]
 
 
 class RasterDesc(C.Structure):
     _fields_ = [("n_slots", C.c_int32), ("tiles_per_slot", C.c_int32),
                 ("width", C.c_int32), ("height", C.c_int32),
                 ("bg", C.c_float * 3), ("loss_fused", C.c_int32), ("pixels_per_lane", C.c_int32),
-                ("patch_P", C.c_int32), ("slot_patches", C.c_void_p)]
+                ("patch_P", C.c_int32), ("slot_patches", C.c_void_p), ("row_support", C.c_void_p)]
 
 
 class AdamDesc(C.Structure):
@@ -122,6 +123,7 @@ _SIGS = {
     "bs_dest_compact": (_I32, [_P, _I64, _I32, _P, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "bs_gather_rows": (_I32, [_P, _I32, _P, _I64, _P, _P]),
     "bs_scatter_add_rows": (_I32, [_P, _I32, _I32, _P, _I64, _P, _I32, _P]),
+    "bs_row_support": (_I32, [_P, _I32, _I64, _P, _P]),
     "bs_canonical_order_workspace": (_SZ, [_I64]),
     "bs_canonical_order": (_I32, [_P, _I64, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
 }

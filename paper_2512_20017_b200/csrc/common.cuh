@@ -112,6 +112,14 @@ __device__ __forceinline__ float support_k(float opac) {
   return fminf(9.0f, fmul(2.0f, det_logf(fmul(255.0f, opac))));
 }
 
+// Rasteriser support threshold of a row with opacity o (bs_row_support):
+// 3DGS the log2-exponent threshold k * (-log2(e) / 2), 2DGS k itself.
+constexpr float kHalfLog2eNeg = -0.5f * 1.4426950408889634f;
+__device__ __forceinline__ float row_support_value(float opac, bool two_d) {
+  const float k = support_k(opac);
+  return two_d ? k : fmul(k, kHalfLog2eNeg);
+}
+
 __device__ __forceinline__ float det_sigmoid(float x) {
   return fdiv(1.0f, fadd(1.0f, det_expf(-x)));
 }

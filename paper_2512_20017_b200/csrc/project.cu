@@ -95,6 +95,7 @@ struct ProjArgs {
   float* gsp_zero;              // G_SP rows cleared alongside the SP rows (project_fwd), or NULL
   const int32_t* point_gid;     // global id per local point (project_fwd), or NULL (= local index)
   int32_t* row_gid;             // per SP row: global id of its point (project_fwd), or NULL
+  float* row_support;           // per SP row: the rasteriser's support threshold (project_fwd), or NULL
 };
 
 // Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
@@ -106,6 +107,7 @@ struct Model3 {
   using F = ProjFwd;
   using Pre = PointPre;
   static constexpr int kSP = BS_SP_FLOATS, kGSP = BS_GSP_FLOATS, kAcc = 6;
+  static constexpr bool k2D = false;
   __device__ static void pre(const PointIn& pt, Pre& r) { point_pre(pt, r); }
   static constexpr int kGcol = 6;  // colour gradient inside a G_SP row
   static constexpr bool kFuseWk = false;
@@ -130,6 +132,7 @@ struct Model2 {
   using F = Proj2D;
   using Pre = Pre2D;
   static constexpr int kSP = kSP2, kGSP = kGSP2, kAcc = 9;
+  static constexpr bool k2D = true;
   __device__ static void pre(const PointIn& pt, Pre& r) { point_pre2(pt, r); }
   static constexpr int kGcol = 12;
   static constexpr bool kFuseWk = true;
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
         const int64_t row = s_row0[v] + rk.row_offset(v);
         M::write(sp + row * M::kSP, f);
         if (a.row_gid) a.row_gid[row] = a.point_gid ? a.point_gid[i] : i;
+        if (a.row_support) a.row_support[row] = row_support_value(f.opac, M::k2D);
         if (a.gsp_zero) {
           float4* z = reinterpret_cast<float4*>(a.gsp_zero + row * M::kGSP);
 #pragma unroll
@@ -482,6 +486,12 @@ __global__ void view_row0_kernel(const int64_t* __restrict__ rows, ViewOrder o, 
   }
 }
 
+__global__ void row_support_kernel(const float* __restrict__ sp, int stride, bool two_d, int64_t n,
+                                   float* __restrict__ out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    out[r] = row_support_value(sp[r * stride + 2], two_d);  // opacity: float 2 of both row layouts
+}
+
 int32_t check_proj(const bs_proj_desc* d) {
   BS_REQUIRE(d != nullptr, BS_ERR_PARAMETER, "null projection descriptor");
   BS_REQUIRE(d->n_views >= 1 && d->n_views <= kMaxViews, BS_ERR_PARAMETER, "projection supports 1..32 views");
@@ -548,7 +558,7 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, d->gsp_zero,
-             d->point_gid, d->row_gid};
+             d->point_gid, d->row_gid, d->row_support};
   const dim3 grid = proj_grid(d, n_groups);
   const size_t smem = sizeof(float4) * 12 * kProjThreads;
   auto launch = [&](auto kern) {
@@ -571,7 +581,7 @@ extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, in
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, nullptr,
-             nullptr, nullptr};
+             nullptr, nullptr, nullptr};
   const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
     project_bwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(
@@ -608,7 +618,7 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   const int n_sh = (pd->sh_degree + 1) * (pd->sh_degree + 1);
   ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr, nullptr,
-             nullptr, nullptr};
+             nullptr, nullptr, nullptr};
   AdamConsts c = make_adam(ad);
   const size_t smem = sizeof(float) * 48 * kProjThreads + sizeof(float4) * 12 * kProjThreads;
   auto launch = [&](auto kern) {
@@ -620,5 +630,15 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   if (pd->model == BS_MODEL_2DGS) launch(project_bwd_adam_kernel<Model2>);
   else launch(project_bwd_adam_kernel<Model3>);
   BS_LAUNCH_CHECK("project_bwd_adam_kernel");
+  return BS_OK;
+}
+
+extern "C" int32_t bs_row_support(const float* sp_rows, int32_t model, int64_t n_rows, float* out, void* stream) {
+  BS_REQUIRE(model == BS_MODEL_3DGS || model == BS_MODEL_2DGS, BS_ERR_PARAMETER, "unknown splat model");
+  if (n_rows <= 0) return BS_OK;
+  const bool two_d = model == BS_MODEL_2DGS;
+  row_support_kernel<<<grid_for(n_rows, 256), 256, 0, as_stream(stream)>>>(sp_rows, two_d ? kSP2 : BS_SP_FLOATS, two_d,
+                                                                          n_rows, out);
+  BS_LAUNCH_CHECK("row_support_kernel");
   return BS_OK;
 }

@@ -67,6 +67,7 @@ struct RastArgs {
   float inv_norm;                // 1 / (H * W * 3)
   int patch_P;
   const uint64_t* slot_patches;  // NULL: every pixel
+  const float* support;          // per-row support threshold (bs_row_support) or NULL
 };
 
 // Patch restriction (P > 1): does this slot render pixel (x, y)?  Patch c of
@@ -110,11 +111,13 @@ struct Splat {
   float4 p0, p1;  // (u v opac A), (B C r g)
   float b;
   float2 h;       // support half-widths (hx, hy) = sp[10], sp[11]
+  float th2;      // support threshold (per-row array; else computed at staging)
   uint32_t row;
   bool ok;
 };
 
-__device__ __forceinline__ void fetch_row_data(Splat& f, const float* __restrict__ sp, uint32_t row, bool ok) {
+__device__ __forceinline__ void fetch_row_data(Splat& f, const float* __restrict__ sp, const float* __restrict__ sup,
+                                               uint32_t row, bool ok) {
   f.ok = ok;
   if (ok) {
     f.row = row;
@@ -123,12 +126,13 @@ __device__ __forceinline__ void fetch_row_data(Splat& f, const float* __restrict
     f.p1 = __ldg(r4 + 1);
     f.b = __ldg(sp + (int64_t)row * BS_SP_FLOATS + 8);
     f.h = __ldg(reinterpret_cast<const float2*>(sp + (int64_t)row * BS_SP_FLOATS + 10));
+    if (sup) f.th2 = __ldg(sup + row);
   }
 }
 
-__device__ __forceinline__ void fetch_splat(Splat& f, const float* __restrict__ sp,
+__device__ __forceinline__ void fetch_splat(Splat& f, const float* __restrict__ sp, const float* __restrict__ sup,
                                             const uint32_t* __restrict__ inst_rows, int idx, bool ok) {
-  fetch_row_data(f, sp, ok ? __ldg(inst_rows + idx) : 0u, ok);
+  fetch_row_data(f, sp, sup, ok ? __ldg(inst_rows + idx) : 0u, ok);
 }
 
 // Row index of instance idx (prefetched one chunk ahead of its SP row so the
@@ -148,10 +152,10 @@ __device__ __forceinline__ bool reaches(const Splat& f, float x0, float x1, floa
          fabsf(v - fminf(fmaxf(v, y0), y1)) <= fmaf(hy, 1.0001f, 1e-3f);
 }
 
-__device__ __forceinline__ void stage(WarpSmem& s, int lane, const Splat& f) {
+__device__ __forceinline__ void stage(WarpSmem& s, int lane, const Splat& f, bool have_support) {
   s.a[lane] = make_float4(f.p0.x, f.p0.y, __fmul_rn(f.p0.w, kHalfLog2e), __fmul_rn(f.p1.y, kHalfLog2e));
   s.b[lane] = make_float4(__fmul_rn(f.p1.x, -kLog2e), f.p0.z, f.p1.z, f.p1.w);
-  s.c[lane] = make_float2(f.b, support_p2(f.p0.z));
+  s.c[lane] = make_float2(f.b, have_support ? f.th2 : support_p2(f.p0.z));
   s.row[lane] = f.row;
 }
 
@@ -252,14 +256,14 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
                     !(kPatches ? slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, q.px, q.py0 + k)
                                : (q.px < a.W && q.py0 + k < a.H))};
   Splat f;
-  fetch_splat(f, sp, inst_rows, rg.x + lane, rg.x + lane < rg.y);
+  fetch_splat(f, sp, a.support, inst_rows, rg.x + lane, rg.x + lane < rg.y);
   uint32_t row_next = fetch_row(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
   for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
     if (__all_sync(0xffffffffu, all_done<PPL>(p))) break;
     const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
-    if (keep) stage(s, lane, f);
-    fetch_row_data(f, sp, row_next, b0 + 32 + lane < rg.y);
+    if (keep) stage(s, lane, f, a.support != nullptr);
+    fetch_row_data(f, sp, a.support, row_next, b0 + 32 + lane < rg.y);
     row_next = fetch_row(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
     __syncwarp();
     while (bits) {
@@ -520,14 +524,14 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
   for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
   const int end = rg.x + warp_n;  // deepest contributor of this warp's pixels
   Splat f;
-  fetch_splat(f, sp, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
+  fetch_splat(f, sp, a.support, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
   uint32_t row_next = fetch_row(inst_rows, end - 33 - lane, end - 33 - lane >= rg.x);
   // chunks back to front; within a chunk lane j holds instance cend - 1 - j
   for (int cend = end; cend > rg.x; cend -= 32) {
     const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
-    if (keep) stage(s, lane, f);
-    fetch_row_data(f, sp, row_next, cend - 33 - lane >= rg.x);
+    if (keep) stage(s, lane, f, a.support != nullptr);
+    fetch_row_data(f, sp, a.support, row_next, cend - 33 - lane >= rg.x);
     row_next = fetch_row(inst_rows, cend - 65 - lane, cend - 65 - lane >= rg.x);
     __syncwarp();
     while (bits) {
@@ -638,6 +642,7 @@ int32_t make_args(const bs_raster_desc* d, RastArgs& a) {
   a.inv_norm = (float)(1.0 / (3.0 * (double)d->width * (double)d->height));
   a.patch_P = d->patch_P > 0 ? d->patch_P : 1;
   a.slot_patches = d->slot_patches;
+  a.support = d->row_support;
   BS_REQUIRE(a.slot_patches == nullptr || (a.patch_P >= 1 && a.patch_P <= 8 && a.W >= a.patch_P && a.H >= a.patch_P),
              BS_ERR_PARAMETER, "patch_P must be in [1, 8] with slot_patches");
   return BS_OK;

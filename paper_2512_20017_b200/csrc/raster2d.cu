@@ -63,6 +63,7 @@ struct R2Args {
   float inv_norm;
   int patch_P;
   const uint64_t* slot_patches;  // NULL: every pixel
+  const float* support;          // per-row support threshold k (bs_row_support) or NULL
 };
 
 // Patch restriction (P > 1): does this slot render pixel (x, y)?  Patch c of
@@ -84,14 +85,17 @@ struct Warp2 {
 struct Splat2 {
   float4 p[4];   // SP floats 0..15
   float2 h, c;   // support box half-widths (16, 17) and centre (22, 23)
+  float k;       // support threshold (per-row array; else computed at staging)
   uint32_t row;
   bool ok;
 };
 
-__device__ __forceinline__ void fetch2_row(Splat2& f, const float* __restrict__ sp, uint32_t row, bool ok) {
+__device__ __forceinline__ void fetch2_row(Splat2& f, const float* __restrict__ sp, const float* __restrict__ sup,
+                                           uint32_t row, bool ok) {
   f.ok = ok;
   if (ok) {
     f.row = row;
+    if (sup) f.k = __ldg(sup + row);
     const float4* r4 = reinterpret_cast<const float4*>(sp + (int64_t)row * kSP2);
 #pragma unroll
     for (int k = 0; k < 4; ++k) f.p[k] = __ldg(r4 + k);
@@ -100,9 +104,9 @@ __device__ __forceinline__ void fetch2_row(Splat2& f, const float* __restrict__ 
   }
 }
 
-__device__ __forceinline__ void fetch2(Splat2& f, const float* __restrict__ sp, const uint32_t* __restrict__ rows,
-                                       int idx, bool ok) {
-  fetch2_row(f, sp, ok ? __ldg(rows + idx) : 0u, ok);
+__device__ __forceinline__ void fetch2(Splat2& f, const float* __restrict__ sp, const float* __restrict__ sup,
+                                       const uint32_t* __restrict__ rows, int idx, bool ok) {
+  fetch2_row(f, sp, sup, ok ? __ldg(rows + idx) : 0u, ok);
 }
 
 // row index prefetched one chunk ahead of its SP row (no back-to-back dependent gathers)
@@ -142,7 +146,7 @@ __device__ __forceinline__ void cross3(const float a[3], const float b[3], float
   o[2] = __fsub_rn(__fmul_rn(a[0], b[1]), __fmul_rn(a[1], b[0]));
 }
 
-__device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f, float X, float Y) {
+__device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f, float X, float Y, bool have_support) {
   float r0[3], r1[3], r2[3];
   m_rows(f.p[0], f.p[1], f.p[2], r0, r1, r2);
   float hx[3], hy[3], z0[3], zb[3], zc[3];
@@ -159,7 +163,7 @@ __device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f, floa
   s.a[lane] = make_float4(f.p[0].x, f.p[0].y, f.p[0].z, z0[2]);
   s.b[lane] = make_float4(z0[0], z0[1], zb[0], zb[1]);
   s.c[lane] = make_float4(zc[0], zc[1], zb[2], zc[2]);
-  s.d[lane] = make_float4(f.p[3].x, f.p[3].y, f.p[3].z, support_k(f.p[0].z));  // (r, g, b, k)
+  s.d[lane] = make_float4(f.p[3].x, f.p[3].y, f.p[3].z, have_support ? f.k : support_k(f.p[0].z));  // (r, g, b, k)
   s.row[lane] = f.row;
 }
 
@@ -222,14 +226,14 @@ __global__ void __launch_bounds__(kT2, BS_R2_FWD_CTAS) raster2d_fwd_kernel(R2Arg
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
   Px2 p{1.f, 0.f, 0.f, 0.f, 0, !inside};
   Splat2 f;
-  fetch2(f, sp, inst_rows, rg.x + lane, rg.x + lane < rg.y);
+  fetch2(f, sp, a.support, inst_rows, rg.x + lane, rg.x + lane < rg.y);
   uint32_t row_next = row2(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
   for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
     if (__all_sync(0xffffffffu, p.done)) break;
     const bool keep = reaches2(f, x0, x1, y0, y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
-    if (keep) stage2(s, lane, f, x0, y0);
-    fetch2_row(f, sp, row_next, b0 + 32 + lane < rg.y);
+    if (keep) stage2(s, lane, f, x0, y0, a.support != nullptr);
+    fetch2_row(f, sp, a.support, row_next, b0 + 32 + lane < rg.y);
     row_next = row2(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
     __syncwarp();
     while (bits) {
@@ -368,13 +372,13 @@ __global__ void __launch_bounds__(kT2, BS_R2_BWD_CTAS) raster2d_bwd_kernel(
   for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
   const int end = rg.x + warp_n;
   Splat2 f;
-  fetch2(f, sp, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
+  fetch2(f, sp, a.support, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
   uint32_t row_next = row2(inst_rows, end - 33 - lane, end - 33 - lane >= rg.x);
   for (int cend = end; cend > rg.x; cend -= 32) {
     const bool keep = reaches2(f, x0, x1, y0, y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
-    if (keep) stage2(s, lane, f, x0, y0);
-    fetch2_row(f, sp, row_next, cend - 33 - lane >= rg.x);
+    if (keep) stage2(s, lane, f, x0, y0, a.support != nullptr);
+    fetch2_row(f, sp, a.support, row_next, cend - 33 - lane >= rg.x);
     row_next = row2(inst_rows, cend - 65 - lane, cend - 65 - lane >= rg.x);
     __syncwarp();
     while (bits) {
@@ -476,6 +480,7 @@ int32_t make_r2(const bs_raster_desc* d, R2Args& a) {
   a.inv_norm = (float)(1.0 / (3.0 * (double)d->width * (double)d->height));
   a.patch_P = d->patch_P > 0 ? d->patch_P : 1;
   a.slot_patches = d->slot_patches;
+  a.support = d->row_support;
   BS_REQUIRE(a.slot_patches == nullptr || (a.patch_P >= 1 && a.patch_P <= 8 && a.W >= a.patch_P && a.H >= a.patch_P),
              BS_ERR_PARAMETER, "patch_P must be in [1, 8] with slot_patches");
   return BS_OK;

@@ -303,6 +303,11 @@ class SplatTrainer:
         if self.comm is not None or self.record_row_gid:
             row_gid = self.buf.get("row_gid", max(S * B, 1), torch.int32)
             pdesc.row_gid = nat.ptr(row_gid)
+        support = None
+        if self.comm is None:
+            # the rasterisers' per-row support threshold, written with the rows
+            support = self.buf.get("row_support", max(S * B, 1), torch.float32)
+            pdesc.row_support = nat.ptr(support)
         if early:
             # the row counts start towards the host before the projection is
             # queued, so the host resumes while the projection still runs
@@ -356,7 +361,7 @@ class SplatTrainer:
             seg_row0 = view_row0
             seg_slot = self._slot_ids(B)
             losses, gsp = self._render_and_backward(sp, n_rows, seg_row0, seg_slot, B, cams, bidx, gt_batch,
-                                                    gsp_cleared=bool(pdesc.gsp_zero))
+                                                    gsp_cleared=bool(pdesc.gsp_zero), support=support)
         else:
             # SP all-to-all to the rendering ranks (line 9), render, G_SP back (line 21)
             with self._t("a2a_fwd"):
@@ -375,7 +380,8 @@ class SplatTrainer:
                 gt_slots = gt_batch.index_select(0, mine).contiguous()
             losses, gsp_c = self._render_and_backward(sp_c, lay.n_recv, seg_row0, seg_slot, n_slots,
                                                       cams.index_select(0, mine).contiguous(),
-                                                      bidx.index_select(0, mine), gt_slots)
+                                                      bidx.index_select(0, mine), gt_slots,
+                                                      support=self._recv_support)
             with self._t("a2a_bwd"):
                 # back to the received order, only the used floats of a G_SP
                 # row (3DGS: 9 of the 12), then to the owners
@@ -481,7 +487,8 @@ class SplatTrainer:
             gt_slots = gt_batch.index_select(0, mine).contiguous() if gt_batch is not None else None
             losses, gsp_c = self._render_and_backward(sp_c, n_recv, seg_row0, self._slot_ids(n_slots), n_slots,
                                                       cams.index_select(0, mine).contiguous(),
-                                                      bidx.index_select(0, mine), gt_slots, slot_patches=bits_t)
+                                                      bidx.index_select(0, mine), gt_slots, slot_patches=bits_t,
+                                                      support=self._recv_support)
             g = self._uncanonical(gsp_c, order, n_recv, wire)
         # ---- gradient rows back to their sources, summed into the row they left
         with self._t("a2a_bwd"):
@@ -513,7 +520,10 @@ class SplatTrainer:
                  n_slots, nat.ptr(order), nat.ptr(cgid), nat.ptr(ws), ws.numel(), st)
         sp_c = self.buf.get("sp_canon", max(n, 1) * self.sp_floats, torch.float32)
         nat.call("bs_gather_rows", nat.ptr(sp_recv), self.sp_floats, nat.ptr(order), n, nat.ptr(sp_c), st)
+        sup = self.buf.get("row_support", max(n, 1), torch.float32)
+        nat.call("bs_row_support", nat.ptr(sp_c), self.model_id, n, nat.ptr(sup), st)
         self.last["row_gid"] = cgid[:n]
+        self._recv_support = sup
         return sp_c, order
 
     def _uncanonical(self, gsp_c, order, n, wire):
@@ -580,7 +590,7 @@ class SplatTrainer:
         return n_inst, irows, ranges
 
     def _render_and_backward(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, gt_views, gt_batch,
-                             slot_patches=None, gsp_cleared=False):
+                             slot_patches=None, gsp_cleared=False, support=None):
         dev, st = self.dev, nat.stream_handle()
         lib = nat.load()
         gsp = self.buf.get("gsp", max(n_rows, 1) * self.gsp_floats, torch.float32)
@@ -603,7 +613,7 @@ class SplatTrainer:
         n_contrib = self.buf.get("n_contrib", n_slots * npx, torch.int32)
         loss_tiles = self.buf.get("loss_tiles", n_slots * self.tiles, torch.float32)
         rdesc = nat.RasterDesc(n_slots, self.tiles, self.W, self.H, (ctypes.c_float * 3)(*self.bg), 1,
-                               self.pixels_per_lane, self.P, nat.ptr(slot_patches))
+                               self.pixels_per_lane, self.P, nat.ptr(slot_patches), nat.ptr(support))
         if gt_batch is not None:
             gt, gt_map = gt_batch, None
         else:
