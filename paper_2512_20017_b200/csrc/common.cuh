@@ -115,9 +115,9 @@ __device__ __forceinline__ float support_k(float opac) {
 // Rasteriser support threshold of a row with opacity o (bs_row_support):
 // 3DGS the log2-exponent threshold k * (-log2(e) / 2), 2DGS k itself.
 constexpr float kHalfLog2eNeg = -0.5f * 1.4426950408889634f;
+__device__ __forceinline__ float row_support_from_k(float k, bool two_d) { return two_d ? k : fmul(k, kHalfLog2eNeg); }
 __device__ __forceinline__ float row_support_value(float opac, bool two_d) {
-  const float k = support_k(opac);
-  return two_d ? k : fmul(k, kHalfLog2eNeg);
+  return row_support_from_k(support_k(opac), two_d);
 }
 
 __device__ __forceinline__ float det_sigmoid(float x) {

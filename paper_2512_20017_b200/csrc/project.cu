@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
         const int64_t row = s_row0[v] + rk.row_offset(v);
         M::write(sp + row * M::kSP, f);
         if (a.row_gid) a.row_gid[row] = a.point_gid ? a.point_gid[i] : i;
-        if (a.row_support) a.row_support[row] = row_support_value(f.opac, M::k2D);
+        if (a.row_support) a.row_support[row] = row_support_from_k(f.support_k, M::k2D);
         if (a.gsp_zero) {
           float4* z = reinterpret_cast<float4*>(a.gsp_zero + row * M::kGSP);
 #pragma unroll

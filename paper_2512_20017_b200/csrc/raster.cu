@@ -234,7 +234,7 @@ __device__ __forceinline__ bool all_done(const PixelFwd (&p)[PPL]) {
   return d;
 }
 
-template <int PPL, bool kPatches>
+template <int PPL, bool kPatches, bool kSup>
 __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
     RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
     float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
@@ -256,14 +256,15 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
                     !(kPatches ? slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, q.px, q.py0 + k)
                                : (q.px < a.W && q.py0 + k < a.H))};
   Splat f;
-  fetch_splat(f, sp, a.support, inst_rows, rg.x + lane, rg.x + lane < rg.y);
+  const float* sup = kSup ? a.support : nullptr;  // kSup: per-row support thresholds given
+  fetch_splat(f, sp, sup, inst_rows, rg.x + lane, rg.x + lane < rg.y);
   uint32_t row_next = fetch_row(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
   for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
     if (__all_sync(0xffffffffu, all_done<PPL>(p))) break;
     const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
-    if (keep) stage(s, lane, f, a.support != nullptr);
-    fetch_row_data(f, sp, a.support, row_next, b0 + 32 + lane < rg.y);
+    if (keep) stage(s, lane, f, kSup);
+    fetch_row_data(f, sp, sup, row_next, b0 + 32 + lane < rg.y);
     row_next = fetch_row(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
     __syncwarp();
     while (bits) {
@@ -497,7 +498,7 @@ __device__ __forceinline__ void init_pixel_bwd(PixelBwd& q, const RastArgs& a, i
   q.acc2 = 0.f;
 }
 
-template <int PPL, bool kBg>
+template <int PPL, bool kBg, bool kSup>
 __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768) / Region<PPL>::kThreads) raster_bwd_kernel(
     RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
     const float* __restrict__ image, const float* __restrict__ final_T, const int32_t* __restrict__ n_contrib,
@@ -524,14 +525,15 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
   for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
   const int end = rg.x + warp_n;  // deepest contributor of this warp's pixels
   Splat f;
-  fetch_splat(f, sp, a.support, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
+  const float* sup = kSup ? a.support : nullptr;  // kSup: per-row support thresholds given
+  fetch_splat(f, sp, sup, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
   uint32_t row_next = fetch_row(inst_rows, end - 33 - lane, end - 33 - lane >= rg.x);
   // chunks back to front; within a chunk lane j holds instance cend - 1 - j
   for (int cend = end; cend > rg.x; cend -= 32) {
     const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
-    if (keep) stage(s, lane, f, a.support != nullptr);
-    fetch_row_data(f, sp, a.support, row_next, cend - 33 - lane >= rg.x);
+    if (keep) stage(s, lane, f, kSup);
+    fetch_row_data(f, sp, sup, row_next, cend - 33 - lane >= rg.x);
     row_next = fetch_row(inst_rows, cend - 65 - lane, cend - 65 - lane >= rg.x);
     __syncwarp();
     while (bits) {
@@ -666,13 +668,18 @@ extern "C" int32_t bs_raster_fwd(const bs_raster_desc* d, const float* sp_rows, 
     kern<<<grid, threads, 0, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image,
                                                   final_T, n_contrib, gt, gt_slot_view, loss_tiles);
   };
-  const bool patches = a.slot_patches != nullptr;
-  if (d->pixels_per_lane == 1)
-    patches ? launch(raster_fwd_kernel<1, true>, Region<1>::kThreads)
-            : launch(raster_fwd_kernel<1, false>, Region<1>::kThreads);
-  else
-    patches ? launch(raster_fwd_kernel<2, true>, Region<2>::kThreads)
-            : launch(raster_fwd_kernel<2, false>, Region<2>::kThreads);
+  const bool patches = a.slot_patches != nullptr, sup = a.support != nullptr;
+  if (d->pixels_per_lane == 1) {
+    if (sup)
+      patches ? launch(raster_fwd_kernel<1, true, true>, Region<1>::kThreads)
+              : launch(raster_fwd_kernel<1, false, true>, Region<1>::kThreads);
+    else
+      patches ? launch(raster_fwd_kernel<1, true, false>, Region<1>::kThreads)
+              : launch(raster_fwd_kernel<1, false, false>, Region<1>::kThreads);
+  } else {
+    patches ? launch(raster_fwd_kernel<2, true, false>, Region<2>::kThreads)
+            : launch(raster_fwd_kernel<2, false, false>, Region<2>::kThreads);
+  }
   BS_LAUNCH_CHECK("raster_fwd_kernel");
   return BS_OK;
 }
@@ -691,10 +698,18 @@ extern "C" int32_t bs_raster_bwd(const bs_raster_desc* d, const float* sp_rows, 
     kern<<<grid, threads, 0, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image,
                                                   final_T, n_contrib, grad_image, gt, gt_slot_view, g_sp);
   };
-  if (d->pixels_per_lane == 1)
-    bg ? launch(raster_bwd_kernel<1, true>, Region<1>::kThreads) : launch(raster_bwd_kernel<1, false>, Region<1>::kThreads);
-  else
-    bg ? launch(raster_bwd_kernel<2, true>, Region<2>::kThreads) : launch(raster_bwd_kernel<2, false>, Region<2>::kThreads);
+  const bool sup = a.support != nullptr;
+  if (d->pixels_per_lane == 1) {
+    if (sup)
+      bg ? launch(raster_bwd_kernel<1, true, true>, Region<1>::kThreads)
+         : launch(raster_bwd_kernel<1, false, true>, Region<1>::kThreads);
+    else
+      bg ? launch(raster_bwd_kernel<1, true, false>, Region<1>::kThreads)
+         : launch(raster_bwd_kernel<1, false, false>, Region<1>::kThreads);
+  } else {
+    bg ? launch(raster_bwd_kernel<2, true, false>, Region<2>::kThreads)
+       : launch(raster_bwd_kernel<2, false, false>, Region<2>::kThreads);
+  }
   BS_LAUNCH_CHECK("raster_bwd_kernel");
   return BS_OK;
 }

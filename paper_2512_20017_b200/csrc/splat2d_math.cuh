@@ -62,6 +62,7 @@ struct Proj2D {
   float d[3], qc[3], Rc[9];
   float c0[3], c1[3], c2[3];  // M columns
   float u, v, depth, radius_x, radius_y, normal[3];
+  float support_k;  // k = min(9, 2 ln(255 o)) of the support (box, rasteriser threshold)
   float box_cx, box_cy;  // centre of the support box (half-widths radius_x / radius_y)
   float len, dir[3], Y[16], col_raw[3], col[3], opac;
   bool valid;
@@ -136,6 +137,7 @@ __device__ __forceinline__ void project2d_forward(const PointIn& pt, const Pre2D
   f.box_cx = f.u;
   f.box_cy = f.v;
   const float k = support_k(pre.opac);
+  f.support_k = k;
   if (f.valid && k > 0.f) {
     // support {min(g3, g2) <= k}, k = min(9, 2 ln(255 o)): the image of the
     // disk u^2 + v^2 <= k (dual conic, bounded since the 9-disk's is) united

@@ -53,6 +53,7 @@ struct ProjFwd {
   float a, b, c, det;  // dilated 2D covariance
   float conic[3];
   float radius_x, radius_y;
+  float support_k;  // k = min(9, 2 ln(255 o)) of the support (extents, rasteriser threshold)
   float u, v, depth;
   float len, dir[3];
   float Y[16];
@@ -356,13 +357,14 @@ __device__ __forceinline__ void project_forward_t(const PointIn& pt, const Point
   f.c = fadd(fadd(fmul(U1[1], f.J11), fmul(U1[2], f.J12)), kDilation);
   f.det = fsub(fmul(f.a, f.c), fmul(f.b, f.b));
   f.valid = f.det > 0.f;
+  f.support_k = support_k(pre.opac);
   if (f.valid) {
     f.conic[0] = fdiv(f.c, f.det);
     f.conic[1] = fdiv(-f.b, f.det);
     f.conic[2] = fdiv(f.a, f.det);
     // per-axis extents = the tight bounding box of the support ellipse
     // q <= k, k = min(9, 2 ln(255 o)) (half-widths sqrt(k cov_xx), sqrt(k cov_yy))
-    const float k = support_k(pre.opac);
+    const float k = f.support_k;
     f.radius_x = k > 0.f ? fsqrt(fmul(k, f.a)) : 0.f;
     f.radius_y = k > 0.f ? fsqrt(fmul(k, f.c)) : 0.f;
   } else {

@@ -39,6 +39,7 @@ from .exchange import layout_for
 from .scenes import CameraView
 
 _CAM_BYTES = ctypes.sizeof(nat.Camera)
+_NVTX = os.environ.get("BS_NVTX", "0") == "1"
 
 
 def camera_struct(view: CameraView) -> nat.Camera:
@@ -202,11 +203,15 @@ class SplatTrainer:
 
     # ------------------------------------------------------------------ utils
     def _t(self, name):
-        """Context manager recording CUDA events around a stage (if enabled)."""
+        """Context manager around a stage: CUDA events (if `timers` is
+        enabled) and an NVTX range named after the stage (if BS_NVTX=1, for
+        nsys / ncu --nvtx; SURVEY.md §5 tracing)."""
         trainer = self
 
         class _T:
             def __enter__(self_):
+                if _NVTX:
+                    torch.cuda.nvtx.range_push(f"bs:{name}")
                 if trainer.timers is not None:
                     self_.s = torch.cuda.Event(enable_timing=True)
                     self_.s.record()
@@ -217,6 +222,8 @@ class SplatTrainer:
                     e = torch.cuda.Event(enable_timing=True)
                     e.record()
                     trainer.timers.setdefault(name, []).append((self_.s, e))
+                if _NVTX:
+                    torch.cuda.nvtx.range_pop()
                 return False
 
         return _T()
@@ -256,7 +263,10 @@ class SplatTrainer:
 
     def step(self, batch_ids, gt_batch: torch.Tensor | None = None, next_batch=None):
         """One training step over `batch_ids` (indices into self.views).
-        Returns the per-view mean-L1 losses as a device tensor [B].
+        Returns the mean-L1 losses of the views rendered on THIS rank as a
+        device tensor, in batch order (N = 1: all B views); their batch
+        positions are in self.last["loss_views"] (with several ranks each
+        rank returns its own views' losses, W of PAPER.md:488).
         With several ranks, `next_batch` (the same on every rank) starts the
         asynchronous placement of the following step (exchange.py)."""
         B = len(batch_ids)
@@ -360,6 +370,7 @@ class SplatTrainer:
                 self.last["row_gid"] = row_gid[:n_rows]
             seg_row0 = view_row0
             seg_slot = self._slot_ids(B)
+            self.last["loss_views"] = list(range(B))
             losses, gsp = self._render_and_backward(sp, n_rows, seg_row0, seg_slot, B, cams, bidx, gt_batch,
                                                     gsp_cleared=bool(pdesc.gsp_zero), support=support)
         else:
@@ -369,6 +380,7 @@ class SplatTrainer:
                 gid_recv = self.comm.forward_ids(row_gid[:n_rows], lay)
             mine = torch.as_tensor(lay.my_views, device=dev)
             n_slots = len(lay.my_views)
+            self.last["loss_views"] = [int(v) for v in lay.my_views]
             # received rows in canonical order: per rendered view, ascending global id
             slot_rows = np.bincount(lay.seg_slot, weights=lay.seg_rows, minlength=n_slots).astype(np.int64)
             sp_c, order = self._canonical(sp_recv.reshape(-1), gid_recv, lay.n_recv, lay.seg_rows, lay.seg_slot,
@@ -472,7 +484,8 @@ class SplatTrainer:
                 seg_rows.append(int(recv_v[s_, v]))
                 seg_slot.append(k)
         n_recv = int(sum(recv_rows))
-        self.last.update(my_views=my_views, send_rows=send_rows, recv_rows=recv_rows, n_send=n_send)
+        self.last.update(my_views=my_views, send_rows=send_rows, recv_rows=recv_rows, n_send=n_send,
+                         loss_views=list(my_views))
         losses = torch.zeros(0, dtype=torch.float32, device=dev)
         wire = self.gsp_wire_floats
         g = self.buf.get("gsp_wire", max(n_recv, 1) * wire, torch.float32)[: n_recv * wire]
