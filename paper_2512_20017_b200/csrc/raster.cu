@@ -28,7 +28,7 @@
 //
 // Backward: each warp walks its own range back to front from the deepest
 // contributor of its pixels (T recovered by division).  Per splat the lanes
-// that contribute are counted with a ballot: up to kSparseLanes (12) of them
+// that contribute are counted with a ballot: up to kSparseLanes (10) of them
 // add their 9 gradient terms with direct REDs (two 128-bit + one 32-bit RED
 // into the 16-byte aligned G_SP row); otherwise the warp reduce-scatters the
 // 9 sums in 12 shuffles and 9 lanes issue one RED each.
@@ -43,8 +43,9 @@ constexpr float kTMin = 1e-4f;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kHalfLog2e = -0.5f * kLog2e;  // p2 = power * log2(e) = q * kHalfLog2e
 #ifndef BS_SPARSE_LANES
-// swept on B200 (C2, 128-bit REDs): 6 2.18, 8 2.11, 10 2.07, 12 2.06, 16 2.15, 32 3.25 ms
-#define BS_SPARSE_LANES 12
+// swept on B200 (C2, 128-bit REDs; round 2, 48-byte staged records): 6 1.974, 8 1.937,
+// 10 1.931, 12 1.958, 16 2.118 ms (round 1, separate arrays: 12 best at 2.06)
+#define BS_SPARSE_LANES 10
 #endif
 constexpr int kSparseLanes = BS_SPARSE_LANES;  // contributing lanes handled with direct REDs
 
@@ -94,13 +95,20 @@ __device__ __forceinline__ float splat_power2(F2 uv, F2 k, float kb, F2 npx, F2&
   return __fadd_rn(__fmaf_rn(kb, __fmul_rn(dd.x, dd.y), t.x), t.y);
 }
 
-// Warp-private staging: a = (u, v, kA, kC), b = (kB, opacity, r, g),
-// c = (b-channel, th2): th2 = the exponent threshold k * (-log2(e) / 2)
+// Warp-private staging, one 48-byte record per splat (one address, three
+// broadcast LDS.128): a = (u, v, kA, kC), b = (kB, opacity, r, g),
+// c = (b-channel, th2, row bits, -): th2 = the exponent threshold k * (-log2(e) / 2)
+struct Staged {
+  float4 a, b, c;
+};
 struct WarpSmem {
+  Staged s[32];
+};
+// forward staging (no row needed): arrays, conflict-free 16-byte stores
+struct WarpSmemF {
   float4 a[32];
   float4 b[32];
   float2 c[32];
-  uint32_t row[32];
 };
 
 // Lowest log2-exponent of the splat's support: p2 >= th2 <=> q <= k.
@@ -152,11 +160,17 @@ __device__ __forceinline__ bool reaches(const Splat& f, float x0, float x1, floa
          fabsf(v - fminf(fmaxf(v, y0), y1)) <= fmaf(hy, 1.0001f, 1e-3f);
 }
 
-__device__ __forceinline__ void stage(WarpSmem& s, int lane, const Splat& f, bool have_support) {
+__device__ __forceinline__ void stage(WarpSmemF& s, int lane, const Splat& f, bool have_support) {
   s.a[lane] = make_float4(f.p0.x, f.p0.y, __fmul_rn(f.p0.w, kHalfLog2e), __fmul_rn(f.p1.y, kHalfLog2e));
   s.b[lane] = make_float4(__fmul_rn(f.p1.x, -kLog2e), f.p0.z, f.p1.z, f.p1.w);
   s.c[lane] = make_float2(f.b, have_support ? f.th2 : support_p2(f.p0.z));
-  s.row[lane] = f.row;
+}
+
+__device__ __forceinline__ void stage(WarpSmem& s, int lane, const Splat& f, bool have_support) {
+  Staged& t = s.s[lane];
+  t.a = make_float4(f.p0.x, f.p0.y, __fmul_rn(f.p0.w, kHalfLog2e), __fmul_rn(f.p1.y, kHalfLog2e));
+  t.b = make_float4(__fmul_rn(f.p1.x, -kLog2e), f.p0.z, f.p1.z, f.p1.w);
+  t.c = make_float4(f.b, have_support ? f.th2 : support_p2(f.p0.z), __uint_as_float(f.row), 0.f);
 }
 
 // Pixel region of a warp: 8 x (4 * PPL) pixels, PPL vertically adjacent
@@ -240,12 +254,12 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
     float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
     const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view, float* __restrict__ loss_tiles) {
   constexpr int kW = Region<PPL>::kWarps;
-  __shared__ WarpSmem smem[kW];
+  __shared__ WarpSmemF smem[kW];
   __shared__ float s_red[kW];
   const int slot = blockIdx.z;
   const int tile = blockIdx.y * a.tiles_x + blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  WarpSmem& s = smem[w];
+  WarpSmemF& s = smem[w];
   const Region<PPL> q(blockIdx.x, blockIdx.y);
   const float pxf = (float)q.px + 0.5f;
   const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
@@ -541,9 +555,9 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
       bits &= bits - 1;
       const int rel = cend - 1 - j - rg.x;  // range-relative index of this splat
       float g[9];
-      const float4 sa = s.a[j];
-      const float4 sb = s.b[j];
-      const float2 sc = s.c[j];
+      const float4 sa = s.s[j].a;
+      const float4 sb = s.s[j].b;
+      const float4 sc = s.s[j].c;
       bool any = false;
       if constexpr (PPL == 1) {
         any = pixel_grad_sel<kBg>(p[0], sa, sb, sc.x, sc.y, f2(-pxf, -((float)q.py0 + 0.5f)), rel < p[0].n, g);
@@ -557,7 +571,7 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
       }
       const uint32_t who = __ballot_sync(0xffffffffu, any);
       if (who == 0u) continue;
-      float* dst = g_sp + (int64_t)s.row[j] * BS_GSP_FLOATS;
+      float* dst = g_sp + (int64_t)__float_as_uint(sc.z) * BS_GSP_FLOATS;
       if (__popc(who) <= kSparseLanes) {
         if (any) {
 #if BS_GSP_FLOATS == 12
