@@ -17,7 +17,10 @@ constexpr int kProjThreads = 256;
 #ifndef BS_ADAM_BATCH
 #define BS_ADAM_BATCH 3
 #endif
-constexpr int kAdamBatch = BS_ADAM_BATCH;  // parameter planes per batch of Adam loads in the fused kernel
+constexpr int kAdamBatch = BS_ADAM_BATCH;
+#ifndef BS_ADAM_SMEM_PARAMS
+#define BS_ADAM_SMEM_PARAMS 1
+#endif  // parameter planes per batch of Adam loads in the fused kernel
 constexpr int kProjWarps = kProjThreads / 32;
 constexpr int kMaxViews = 32;
 
@@ -119,7 +122,7 @@ struct Model3 {
   __device__ static void write(float* row, const F& f) { write_sp_row(row, f); }
   template <class SH, class A>
   __device__ static void backward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh,
-                                  const F& f, const float* gs, float* g, float* acc, A add,
+                                  const F& f, const float* gs, float* g, float* acc, A& add,
                                   const float* wk_pre = nullptr) {
     project_backward_t(pt, r, sh, c, n_sh, f, gs, g, acc, add, wk_pre);
   }
@@ -144,7 +147,7 @@ struct Model2 {
   __device__ static void write(float* row, const F& f) { write_sp2_row(row, f); }
   template <class SH, class A>
   __device__ static void backward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh,
-                                  const F& f, const float* gs, float* g, float* acc, A add,
+                                  const F& f, const float* gs, float* g, float* acc, A& add,
                                   const float* wk_pre = nullptr) {
     project2d_backward(pt, r, sh, c, n_sh, f, gs, g, acc, add, wk_pre);
   }
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, f
 template <class M, class SH, class ShAdd>
 __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camera* s_cam, const int64_t* s_row0,
                                                const RowRanker& rk, uint32_t mask, const PointIn& pt, const SH& sh,
-                                               const float* __restrict__ gsp, float* g, ShAdd sh_add) {
+                                               const float* __restrict__ gsp, float* g, ShAdd& sh_add) {
   typename M::Pre pre;
   M::pre(pt, pre);
   float acc[M::kAcc];
@@ -241,6 +244,29 @@ __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camer
   }
   M::finish(pt, acc, g);
 }
+
+// SH gradient accumulators (sh_colour_backward's add4): registers, or this
+// thread's float4 column of shared memory ([12][kProjThreads] float4)
+struct ShAccRegs {
+  float* g;
+  __device__ __forceinline__ void add4(int q, float4 v) {
+    g[4 * q] += v.x;
+    g[4 * q + 1] += v.y;
+    g[4 * q + 2] += v.z;
+    g[4 * q + 3] += v.w;
+  }
+};
+struct ShAccSmem {
+  float4* col;  // &entry[0][thread]
+  __device__ __forceinline__ void add4(int q, float4 v) {
+    float4 t = col[q * kProjThreads];
+    t.x += v.x;
+    t.y += v.y;
+    t.z += v.z;
+    t.w += v.w;
+    col[q * kProjThreads] = t;
+  }
+};
 
 template <class M>
 __global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, const float* __restrict__ gsp,
@@ -269,8 +295,8 @@ __global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, c
       PointGrad gr;
 #pragma unroll
       for (int k = 0; k < 60; ++k) gr.g[k] = 0.f;
-      point_backward<M>(a, s_cam, s_row0, rk, mask, pt, ShRegs{pt.sh}, gsp, gr.g,
-                        [&](int f, float v) { gr.g[12 + f] += v; });
+      ShAccRegs acc{gr.g + 12};
+      point_backward<M>(a, s_cam, s_row0, rk, mask, pt, ShRegs{pt.sh}, gsp, gr.g, acc);
 #pragma unroll
       for (int p = 0; p < BS_PARAM_PLANES; ++p) {
         float4 acc = gparams[p * a.S + i];
@@ -341,9 +367,9 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
                                                                            float4* params,
                                                                            float4* __restrict__ m,
                                                                            float4* __restrict__ v) {
-  // [48][kProjThreads] SH gradients, then [12][kProjThreads] float4 SH values
-  extern __shared__ float s_gsh[];
-  float4* s_sh4 = reinterpret_cast<float4*>(s_gsh + 48 * kProjThreads);
+  // [12][kProjThreads] float4 SH gradients, then [12][kProjThreads] float4 SH values
+  extern __shared__ float4 s_gsh4[];
+  float4* s_sh4 = s_gsh4 + 12 * kProjThreads;
   __shared__ uint32_t s_bal[kProjWarps * kMaxViews];
   __shared__ int s_run[kMaxViews];
   __shared__ bs_camera s_cam[kMaxViews];
@@ -395,16 +421,16 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
       float g12[12];
 #pragma unroll
       for (int k = 0; k < 12; ++k) g12[k] = 0.f;
-      float* my_sh = s_gsh + threadIdx.x;
+      float4* my_sh = s_gsh4 + threadIdx.x;
 #pragma unroll
-      for (int f = 0; f < 48; ++f) my_sh[f * kProjThreads] = 0.f;
+      for (int q = 0; q < 12; ++q) my_sh[q * kProjThreads] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (mask) {
         PointIn pt;
         load_point(a.params, a.S, i, 0, pt);  // geometry planes only; SH from shared memory
         asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own column
         const ShSmem sh{s_sh4 + threadIdx.x};
-        point_backward<M>(a, s_cam, s_row0, rk, mask, pt, sh, gsp, g12,
-                       [&](int f, float val) { my_sh[f * kProjThreads] += val; });
+        ShAccSmem acc{my_sh};
+        point_backward<M>(a, s_cam, s_row0, rk, mask, pt, sh, gsp, g12, acc);
       }
       // Adam over the 15 planes, 3 planes per batch: all 15 loads of a batch
       // are issued before its first store (memory-level parallelism)
@@ -414,7 +440,13 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
 #pragma unroll
         for (int k = 0; k < kAdamBatch; ++k) {
           const int64_t t = (p0 + k) * a.S + i;
+#if BS_ADAM_SMEM_PARAMS
+          // SH planes of a visible point: already in this thread's shared column
+          const int q = p0 + k - 3;
+          pp[k] = (q >= 0 && q < sh_q && mask) ? s_sh4[q * kProjThreads + threadIdx.x] : params[t];
+#else
           pp[k] = params[t];
+#endif
           mm[k] = m[t];
           vv[k] = v[t];
         }
@@ -423,8 +455,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
           const int p = p0 + k;
           const int64_t t = p * a.S + i;
           const float4 gg = p < 3 ? make_float4(g12[4 * p], g12[4 * p + 1], g12[4 * p + 2], g12[4 * p + 3])
-                                  : make_float4(my_sh[(4 * p - 12) * kProjThreads], my_sh[(4 * p - 11) * kProjThreads],
-                                                my_sh[(4 * p - 10) * kProjThreads], my_sh[(4 * p - 9) * kProjThreads]);
+                                  : my_sh[(p - 3) * kProjThreads];
           adam4(pp[k], gg, mm[k], vv[k], c, p);
           params[t] = pp[k];
           m[t] = mm[k];
@@ -620,7 +651,7 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
              view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr, nullptr,
              nullptr, nullptr, nullptr};
   AdamConsts c = make_adam(ad);
-  const size_t smem = sizeof(float) * 48 * kProjThreads + sizeof(float4) * 12 * kProjThreads;
+  const size_t smem = sizeof(float4) * 24 * kProjThreads;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<proj_grid(pd, n_groups), kProjThreads, smem, as_stream(stream)>>>(a, c, g_sp, reinterpret_cast<float4*>(params),

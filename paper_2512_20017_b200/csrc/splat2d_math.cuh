@@ -226,7 +226,7 @@ __device__ __forceinline__ void gsp2_from_moments(const Proj2D& f, float* gs) {
 template <class SH, class ShAdd>
 __device__ __forceinline__ void project2d_backward(const PointIn& pt, const Pre2D& pre, const SH& sh,
                                                    const bs_camera& c, int n_sh, const Proj2D& f,
-                                                   const float gsp[15], float* g, float GR[9], ShAdd sh_add,
+                                                   const float gsp[15], float* g, float GR[9], ShAdd& sh_add,
                                                    const float* wk_pre = nullptr) {
   if (!f.valid) return;
   // ---- colour -> sh, dir (as 3DGS)

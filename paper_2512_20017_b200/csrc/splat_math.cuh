@@ -182,10 +182,12 @@ __device__ __forceinline__ void sh_colour(const SH& sh, int n_sh, const float Y[
 
 // Backward of the colour clamp into the SH coefficients and the direction
 // weights wk (see sh_colour; wk_pre is used when no channel was clamped).
+// The coefficient gradients go out as float4 plane entries:
+// sh_add.add4(q, (dL/dsh_f for f = 4q .. 4q + 3)), f = 3k + channel.
 template <class SH, class ShAdd>
 __device__ __forceinline__ void sh_colour_backward(const SH& sh, int n_sh, const float Y[16], const float col_raw[3],
                                                    const float gcol[3], const float* wk_pre, float wk[16],
-                                                   ShAdd sh_add) {
+                                                   ShAdd& sh_add) {
   float dc[3];
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) dc[ch] = col_raw[ch] >= 0.f ? gcol[ch] : 0.f;
@@ -193,13 +195,19 @@ __device__ __forceinline__ void sh_colour_backward(const SH& sh, int n_sh, const
 #pragma unroll
   for (int k = 0; k < 16; ++k) wk[k] = fast ? wk_pre[k] : 0.f;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    if (k >= n_sh) break;
+  for (int q = 0; q < 12; ++q) {
+    if (4 * q >= 3 * n_sh) break;
+    float v[4];
+    float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!fast) c4 = sh.load4(q);
+    const float c[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      sh_add(3 * k + ch, Y[k] * dc[ch]);
-      if (!fast) wk[k] = __fmaf_rn(dc[ch], sh(3 * k + ch), wk[k]);
+    for (int e = 0; e < 4; ++e) {
+      const int f = 4 * q + e, k = f / 3, ch = f % 3;
+      v[e] = k < n_sh ? Y[k] * dc[ch] : 0.f;
+      if (!fast && k < n_sh) wk[k] = __fmaf_rn(dc[ch], c[e], wk[k]);
     }
+    sh_add.add4(q, make_float4(v[0], v[1], v[2], v[3]));
   }
 }
 
@@ -464,7 +472,7 @@ __device__ __forceinline__ void sh_dir_grad(const float dir[3], int n_sh, const 
 template <class SH, class ShAdd>
 __device__ __forceinline__ void project_backward_t(const PointIn& pt, const PointPre& pre, const SH& sh,
                                                    const bs_camera& c, int n_sh, const ProjFwd& f,
-                                                   const float gsp[9], float* g, float gS[6], ShAdd sh_add,
+                                                   const float gsp[9], float* g, float gS[6], ShAdd& sh_add,
                                                    const float* wk_pre = nullptr) {
   if (!f.valid) return;
   // ---- colour -> sh, dir
