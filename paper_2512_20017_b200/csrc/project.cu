@@ -157,7 +157,10 @@ struct Model2 {
 };
 
 template <class M>
-__global__ void __launch_bounds__(kProjThreads) project_fwd_kernel(ProjArgs a, float* __restrict__ sp) {
+#ifndef BS_PROJ_FWD_CTAS
+#define BS_PROJ_FWD_CTAS 4  // CTAs per SM the projection's register budget is sized for
+#endif
+__global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_kernel(ProjArgs a, float* __restrict__ sp) {
   // each thread's SH coefficients, staged by cp.async (no registers held for
   // them across the view loop): [12][kProjThreads] float4
   extern __shared__ float4 s_sh4f[];
