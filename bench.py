@@ -462,7 +462,8 @@ def run_ours(args, cfg):
     counts = {"S": tr.S, "V": int(np.mean(rows)), "Vp": int(tr.last.get("n_visible_points", tr.S)),
               "I": int(np.mean(inst)), "Np": int(tr.last["n_slots"]) * H * W,
               "nb": int(tr.last["n_slots"]) * tr.tiles,
-              "gsp_clear": comm is None and model == "3dgs" and tr.binning != "radix"}
+              "gsp_clear": comm is None and model == "3dgs" and tr.binning != "radix",
+              "selective": bool(tr.adam.selective)}
     stages = {}
     for k, v in stage_ms.items():
         nb = rl.stage_bytes(k, counts, model)

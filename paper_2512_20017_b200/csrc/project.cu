@@ -181,6 +181,8 @@ __global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_ke
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const uint32_t mask = i < end ? a.mask[i] : 0u;
+    // a round without a visible point writes no row and advances no count
+    if (!__syncthreads_or(mask != 0u)) continue;
     if (mask) {
       const int sh_q = (3 * a.n_sh + 3) / 4;
       for (int q = 0; q < sh_q; ++q) {
@@ -291,6 +293,7 @@ __global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, c
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const uint32_t mask = i < end ? a.mask[i] : 0u;
+    if (!__syncthreads_or(mask != 0u)) continue;  // no visible point: no row, no gradient
     rk.round(mask, B);
     if (mask) {
       PointIn pt;
@@ -390,6 +393,10 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const bool ok = i < end;
+    const uint32_t mask = ok ? a.mask[i] : 0u;
+    // selective Adam: a round without a visible point updates nothing (and
+    // its rows advance no view's count) -- skip it before any traffic
+    if (c.selective && !__syncthreads_or(mask != 0u)) continue;
     // Copies that cost no registers: the block's parameter and moment planes
     // into L2 by the bulk-copy engine (one contiguous request per (array,
     // plane)) for the Adam update, and this point's SH coefficients into its
@@ -404,7 +411,6 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
                    : "memory");
     }
     const int sh_q = (3 * a.n_sh + 3) / 4;  // float4 entries holding this degree's coefficients
-    const uint32_t mask = ok ? a.mask[i] : 0u;
     // only visible points stage their coefficients: every copy issued here is
     // waited for below (cp.async.wait_all inside `if (mask)`), so no copy is
     // left in flight into the column when the next round reuses it

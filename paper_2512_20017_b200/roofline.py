@@ -22,6 +22,7 @@ blend reads) + 4 B list entry.
 | raster_fwd       | (4 + gather) I + 23 Np (rgb 12, T 4, n 4 written, gt 3 read) |
 | raster_bwd       | (4 + gather) I + 23 Np (image, T, n, gt read) + G_SP V       |
 | project_bwd_adam | 6 x 240 S (p, m, v read + write) + 4 S + G_SP V              |
+|                  | (selective Adam: 6 x 240 Vp + 4 S + G_SP V)                  |
 
 The SURVEY's own formula (§8(d), `survey_step_bytes`) is kept beside it for
 comparison; it assumes 4(K-3) + 44 B per projected row and 44 B per
@@ -49,7 +50,7 @@ MODEL = {
 
 def stage_bytes(stage: str, c: dict, model: str = "3dgs") -> int | None:
     """Compulsory bytes of one launch of `stage` given step counts `c`
-    (keys S, V, Vp, I, Np, nb, gsp_clear)."""
+    (keys S, V, Vp, I, Np, nb, gsp_clear, selective)."""
     m = MODEL[model]
     S, V, I, Np = c["S"], c["V"], c["I"], c["Np"]
     if stage == "cull":
@@ -62,8 +63,9 @@ def stage_bytes(stage: str, c: dict, model: str = "3dgs") -> int | None:
         return (4 + m["gather"]) * I + 23 * Np
     if stage == "raster_bwd":
         return (4 + m["gather"]) * I + 23 * Np + m["gsp"] * V
-    if stage == "project_bwd_adam":
-        return 6 * PARAM_ROW * S + 4 * S + m["gsp"] * V
+    if stage == "project_bwd_adam":  # selective Adam: only the visible points' rows move
+        n_upd = c.get("Vp", S) if c.get("selective") else S
+        return 6 * PARAM_ROW * n_upd + 4 * S + m["gsp"] * V
     return None
 
 
