@@ -319,7 +319,7 @@ def run_ours(args, cfg):
     if world > 1:
         import torch.distributed as dist
 
-        from paper_2512_20017_b200.exchange import SplatExchange
+        from paper_2512_20017_b200.exchange import PeerExchange, SplatExchange
 
         backend = dist_backend(world)
         dist.init_process_group(backend)
@@ -333,7 +333,11 @@ def run_ours(args, cfg):
     ds, g, params, gt, gb, aabb, part_info = build_scene(cfg, gt_views=gt_ids, world=world, rank=rank)
     gt_row = (lambda v: v) if gt_ids is None else {v: k for k, v in enumerate(gt_ids)}.__getitem__
     if world > 1:
-        comm = SplatExchange()
+        # peer: the splat rows / gradients move by loads and stores into the
+        # renderers' / owners' memory (CUDA IPC over NVLink, fused into the
+        # projection and the gradient return); collective: torch.distributed
+        # all_to_all_single (NCCL; host-staged over gloo)
+        comm = PeerExchange() if args.exchange == "peer" else SplatExchange()
     setup_s = time.time() - t0
     W, H = cfg["image_size"]
     model = cfg.get("model", "3dgs")
@@ -394,8 +398,13 @@ def run_ours(args, cfg):
         comm_report = comm_bytes_report(comm, step_AW, sched[args.warmup:args.warmup + args.steps], ds, g,
                                         world, rank, args.steps, row_bytes=4 * tr.sp_floats,
                                         grad_bytes=4 * tr.gsp_wire_floats, P=P)
+        peer = getattr(comm, "peer", False) and P == 1
         comm_report.update(backend=backend, communicator_size=world,
-                           collectives_per_step={"all_gather": 1, "all_to_all_single": 2 if P == 1 else 3})
+                           exchange="peer memory (CUDA IPC: rows written by the projection / gradient return "
+                                    "into the destination's buffer, stream-ordered flags)" if peer
+                           else "torch.distributed all_to_all_single",
+                           collectives_per_step={"all_gather": 1, "all_to_all_single": 0 if peer else
+                                                 (2 if P == 1 else 3)})
     # ---- e2e: public API with pinned host ground truth, loss read back
     # the step's ground-truth images are copied from pinned host memory on a
     # side stream, double-buffered: step i+1's upload overlaps step i
@@ -521,6 +530,8 @@ def run_ours(args, cfg):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        if hasattr(comm, "close"):
+            comm.close()
         torch.distributed.destroy_process_group()
 
 
@@ -626,6 +637,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--patches", type=int, default=0, help="patches per image side P (default: the config's, 1)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "collective"],
+                    help="N > 1: splat-row exchange through peer memory (default) or torch.distributed all-to-alls")
     args = ap.parse_args()
     world = os.environ.get("WORLD_SIZE")
     if args.gpus < 1:

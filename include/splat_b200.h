@@ -231,6 +231,13 @@ typedef struct {
   float* row_support;          /* optional (bs_project_fwd): f32 per SP row, the
                                   support threshold the rasterisers test (see
                                   bs_row_support), computed with the extents */
+  float* const* view_sp;       /* optional (bs_project_fwd): device array [n_views] of
+                                  row-0 pointers -- view v's rows go to
+                                  view_sp[v] + k * row floats instead of sp_rows at
+                                  view_row0[v] + k (peer receive buffers: the forward
+                                  all-to-all fused into the projection) */
+  int32_t* const* view_gid;    /* optional, with view_sp and row_gid semantics: the
+                                  rows' global ids at view_gid[v] + k */
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,
@@ -436,6 +443,29 @@ int32_t bs_scatter_add_rows(const float* src, int32_t src_width, int32_t used,
  * rendered in slot seg_slot[s].  Outputs: order[i] = received row placed at
  * canonical position i (slot-major, ascending global id), canon_gid[i] (optional)
  * its global id. */
+/* ---- peer-memory exchange (csrc/peer.cu; replaces the all-to-alls of
+ * counted by the reference in simulator.py:134-183) ----
+ * One IPC-exported allocation per rank, mapped by the others; completion by
+ * stream-ordered flags.  bs_ipc_alloc: cudaMalloc + handle (bs_ipc_handle_bytes
+ * bytes), zero-filled; bs_ipc_open / close / free.  bs_stream_signal: after
+ * all prior work of `stream`, *flag = value (system-scope fence first);
+ * bs_stream_wait: later work of `stream` waits until *flag >= value. */
+size_t bs_ipc_handle_bytes(void);
+int32_t bs_ipc_alloc(size_t bytes, void** ptr, uint8_t* handle);
+int32_t bs_ipc_open(const uint8_t* handle, void** ptr);
+int32_t bs_ipc_close(void* ptr);
+int32_t bs_ipc_free(void* ptr);
+int32_t bs_stream_signal(void* stream, uint32_t* flag, uint32_t value);
+int32_t bs_stream_wait(void* stream, const uint32_t* flag, uint32_t value);
+/* Gradient rows back to their owners: the first `width` floats of canonical
+ * row i (stride src_width; received row order[i], in segment s = (source
+ * seg_src[s], view), segment start seg_row0[s]) are copied to
+ * dst[seg_src[s]] + (seg_dst0[s] + order[i] - seg_row0[s]) * dst_width
+ * (dst: device array [n_ranks] of the owners' G_SP send-layout buffers). */
+int32_t bs_return_rows(const float* src, int32_t src_width, int32_t width, const int64_t* order, int64_t n,
+                       const int64_t* seg_row0, const int32_t* seg_src, const int64_t* seg_dst0,
+                       int32_t n_segs, float* const* dst, int32_t dst_width, void* stream);
+
 /* Per-row support threshold of the rasterisers: a pixel pair contributes
  * iff q <= k, k = min(9, 2 ln(255 o)) (include/ header notes);
  * 3DGS rows store k * (-log2(e) / 2) (the threshold on the log2 exponent),

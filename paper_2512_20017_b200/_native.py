@@ -59,7 +59,7 @@ class ProjDesc(C.Structure):
                 ("tiles_x_max", C.c_int32), ("tiles_y_max", C.c_int32), ("model", C.c_int32),
                 ("max_group_points", C.c_int32), ("gsp_form", C.c_int32), ("chunk_prefix", C.c_void_p),
                 ("gsp_zero", C.c_void_p), ("point_gid", C.c_void_p), ("row_gid", C.c_void_p),
-                ("row_support", C.c_void_p)]
+                ("row_support", C.c_void_p), ("view_sp", C.c_void_p), ("view_gid", C.c_void_p)]
 
 
 class RasterDesc(C.Structure):
@@ -124,6 +124,14 @@ _SIGS = {
     "bs_gather_rows": (_I32, [_P, _I32, _P, _I64, _P, _P]),
     "bs_scatter_add_rows": (_I32, [_P, _I32, _I32, _P, _I64, _P, _I32, _P]),
     "bs_row_support": (_I32, [_P, _I32, _I64, _P, _P]),
+    "bs_ipc_handle_bytes": (_SZ, []),
+    "bs_ipc_alloc": (_I32, [_SZ, C.POINTER(C.c_void_p), _P]),
+    "bs_ipc_open": (_I32, [_P, C.POINTER(C.c_void_p)]),
+    "bs_ipc_close": (_I32, [_P]),
+    "bs_ipc_free": (_I32, [_P]),
+    "bs_stream_signal": (_I32, [_P, _P, C.c_uint32]),
+    "bs_stream_wait": (_I32, [_P, _P, C.c_uint32]),
+    "bs_return_rows": (_I32, [_P, _I32, _I32, _P, _I64, _P, _P, _P, _I32, _P, _I32, _P]),
     "bs_canonical_order_workspace": (_SZ, [_I64]),
     "bs_canonical_order": (_I32, [_P, _I64, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
 }

@@ -99,6 +99,8 @@ struct ProjArgs {
   const int32_t* point_gid;     // global id per local point (project_fwd), or NULL (= local index)
   int32_t* row_gid;             // per SP row: global id of its point (project_fwd), or NULL
   float* row_support;           // per SP row: the rasteriser's support threshold (project_fwd), or NULL
+  float* const* view_sp;        // per view: row-0 pointer of its rows (peer receive buffers), or NULL
+  int32_t* const* view_gid;     // per view: row-0 pointer of its global ids, or NULL
 };
 
 // Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
@@ -207,8 +209,15 @@ __global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_ke
         typename M::F f;
         M::forward(pt, pre, sh, s_cam[v], a.n_sh, f);
         const int64_t row = s_row0[v] + rk.row_offset(v);
-        M::write(sp + row * M::kSP, f);
-        if (a.row_gid) a.row_gid[row] = a.point_gid ? a.point_gid[i] : i;
+        if (a.view_sp) {
+          // the row of this view lands in its renderer's receive buffer
+          const int64_t k = row - a.view_row0[v];
+          M::write(a.view_sp[v] + k * M::kSP, f);
+          if (a.view_gid) a.view_gid[v][k] = a.point_gid ? a.point_gid[i] : i;
+        } else {
+          M::write(sp + row * M::kSP, f);
+          if (a.row_gid) a.row_gid[row] = a.point_gid ? a.point_gid[i] : i;
+        }
         if (a.row_support) a.row_support[row] = row_support_from_k(f.support_k, M::k2D);
         if (a.gsp_zero) {
           float4* z = reinterpret_cast<float4*>(a.gsp_zero + row * M::kGSP);
@@ -598,7 +607,7 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, d->gsp_zero,
-             d->point_gid, d->row_gid, d->row_support};
+             d->point_gid, d->row_gid, d->row_support, d->view_sp, d->view_gid};
   const dim3 grid = proj_grid(d, n_groups);
   const size_t smem = sizeof(float4) * 12 * kProjThreads;
   auto launch = [&](auto kern) {
@@ -621,7 +630,7 @@ extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, in
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, nullptr,
-             nullptr, nullptr, nullptr};
+             nullptr, nullptr, nullptr, nullptr, nullptr};
   const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
     project_bwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(
@@ -658,7 +667,7 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   const int n_sh = (pd->sh_degree + 1) * (pd->sh_degree + 1);
   ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr, nullptr,
-             nullptr, nullptr, nullptr};
+             nullptr, nullptr, nullptr, nullptr, nullptr};
   AdamConsts c = make_adam(ad);
   const size_t smem = sizeof(float4) * 24 * kProjThreads;
   auto launch = [&](auto kern) {

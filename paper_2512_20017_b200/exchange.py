@@ -192,3 +192,173 @@ class SplatExchange:
         remote = sum(r for s, r in enumerate(lay.recv_rows) if s != self.rank)
         self.bytes_bwd += remote * width * g_recv.element_size()
         return self._a2a(g_recv, lay.recv_rows, lay.send_rows, width)
+
+
+class _Dev:
+    """A raw device pointer where the C ABI wrappers expect a tensor."""
+
+    def __init__(self, p: int):
+        self.p = int(p)
+
+    def data_ptr(self) -> int:
+        return self.p
+
+
+class PeerExchange(SplatExchange):
+    """The two all-to-alls of the step through peer memory (csrc/peer.cu)
+    instead of a collective library: every rank exports one device block
+    (flags, splat-row receive buffer, global-id receive buffer, G_SP home
+    buffer) over CUDA IPC and maps the others' blocks; the projection writes
+    each splat row straight into the renderer's receive buffer
+    (bs_proj_desc.view_sp / view_gid), bs_return_rows writes each gradient
+    row straight into its owner's home buffer, and completion travels as
+    stream-ordered flags (bs_stream_signal / bs_stream_wait, epoch per
+    step).  Between GPUs the loads/stores run over NVLink / NVSwitch; ranks
+    sharing one GPU (tests) map each other's memory the same way.  The host
+    plumbing (access counts, IPC handles) stays on torch.distributed.
+
+    Buffer sizes follow from A and W, which every rank holds, so a
+    reallocation is decided identically everywhere (a collective step)."""
+
+    peer = True
+
+    def __init__(self, *args, **kw):
+        super().__init__(*args, **kw)
+        import ctypes
+
+        from . import _native as nat
+
+        self._nat, self._ct = nat, ctypes
+        self.lib = nat.load()
+        self.epoch = 0
+        self.cap_recv = [0] * self.world   # rows each rank's receive buffer holds
+        self.cap_home = [0] * self.world   # rows each rank's G_SP home buffer holds
+        self.widths = None
+        self.base = None                   # own block
+        self.peers = [None] * self.world   # mapped blocks (own at [rank])
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+
+    # block layout: [fwd flags N u32 | bwd flags N u32 | pad to 256 B] [sp rows] [gid] [gsp home]
+    def _offsets(self, cap_r, cap_h):
+        spf, gspf = self.widths
+        o_sp = 256
+        o_gid = o_sp + ((cap_r * spf * 4 + 255) // 256) * 256
+        o_gsp = o_gid + ((cap_r * 4 + 255) // 256) * 256
+        end = o_gsp + cap_h * gspf * 4
+        return o_sp, o_gid, o_gsp, max(end, 512)
+
+    def _ensure(self, need_recv, need_home, sp_floats, gsp_floats):
+        if (self.widths == (sp_floats, gsp_floats) and all(n <= c for n, c in zip(need_recv, self.cap_recv))
+                and all(n <= c for n, c in zip(need_home, self.cap_home))):
+            return
+        # identical decision on every rank; nobody may still use the old blocks
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        self._release()
+        self.widths = (sp_floats, gsp_floats)
+        self.cap_recv = [max(int(n * 1.25) + 1024, c) for n, c in zip(need_recv, self.cap_recv)]
+        self.cap_home = [max(int(n * 1.25) + 1024, c) for n, c in zip(need_home, self.cap_home)]
+        ct, nat = self._ct, self._nat
+        hb = int(self.lib.bs_ipc_handle_bytes())
+        size = self._offsets(self.cap_recv[self.rank], self.cap_home[self.rank])[3]
+        p = ct.c_void_p()
+        handle = (ct.c_uint8 * hb)()
+        nat.call("bs_ipc_alloc", size, ct.byref(p), handle)
+        self.base = p.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=self.group)
+        for r in range(self.world):
+            if r == self.rank:
+                self.peers[r] = self.base
+            else:
+                q = ct.c_void_p()
+                nat.call("bs_ipc_open", (ct.c_uint8 * hb).from_buffer_copy(handles[r]), ct.byref(q))
+                self.peers[r] = q.value
+        self.epoch = 0  # fresh zeroed flags
+        dist.barrier(group=self.group)
+
+    def _release(self):
+        if self.base is None:
+            return
+        for r, p in enumerate(self.peers):
+            if p is not None and r != self.rank:
+                self._nat.call("bs_ipc_close", p)
+        self._nat.call("bs_ipc_free", self.base)
+        self.base, self.peers = None, [None] * self.world
+
+    def _flag(self, rank, kind, src):
+        return self.peers[rank] + 4 * (kind * self.world + src)
+
+    def plan(self, lay: StepLayout, sp_floats: int, gsp_floats: int):
+        """Per-step plan from A and W: capacities, per-view destination
+        pointers of this rank's rows, the return segments of the rows it
+        renders.  Returns the device arrays the kernels read."""
+        A, W, N, me = lay.A, lay.W, self.world, self.rank
+        B = A.shape[0]
+        need_recv = [int(A[W == d].sum()) for d in range(N)]
+        need_home = [int(A[:, s].sum()) for s in range(N)]
+        self._ensure(need_recv, need_home, sp_floats, gsp_floats)
+        self.epoch += 1
+        offs = [self._offsets(self.cap_recv[r], self.cap_home[r]) for r in range(N)]
+        # receive layout of rank d: sources ascending, then its views ascending
+        view_sp = np.zeros(B, dtype=np.int64)
+        view_gid = np.zeros(B, dtype=np.int64)
+        for v in range(B):
+            d = int(W[v])
+            mine_d = np.flatnonzero(W == d)
+            before = int(A[mine_d, :me].sum()) + int(A[mine_d[mine_d < v], me].sum())
+            view_sp[v] = self.peers[d] + offs[d][0] + before * sp_floats * 4
+            view_gid[v] = self.peers[d] + offs[d][1] + before * 4
+        # send layout of every source s: views ordered by (W, v)
+        order = np.lexsort((np.arange(B), W))
+        row0 = np.zeros((N, B), dtype=np.int64)
+        for s in range(N):
+            acc = 0
+            for v in order:
+                row0[s, v] = acc
+                acc += int(A[v, s])
+        seg_src, seg_dst0 = [], []
+        for s in range(N):
+            for v in lay.my_views:
+                seg_src.append(s)
+                seg_dst0.append(int(row0[s, v]))
+        dst = np.array([self.peers[r] + offs[r][2] for r in range(N)], dtype=np.int64)
+        host = np.concatenate([view_sp, view_gid, dst, np.asarray(seg_dst0, dtype=np.int64),
+                               np.asarray(seg_src, dtype=np.int64)])
+        dev = torch.as_tensor(host, device=self.dev)
+        n_segs = len(seg_src)
+        return {"view_sp": dev[:B], "view_gid": dev[B:2 * B], "dst": dev[2 * B:2 * B + N],
+                "seg_dst0": dev[2 * B + N:2 * B + N + n_segs],
+                "seg_src": dev[2 * B + N + n_segs:].to(torch.int32),
+                "sp_recv": _Dev(self.base + offs[me][0]), "gid_recv": _Dev(self.base + offs[me][1]),
+                "gsp_home": _Dev(self.base + offs[me][2]), "n_segs": n_segs}
+
+    def _signal_all(self, kind, st):
+        for d in range(self.world):
+            if d != self.rank:
+                self._nat.call("bs_stream_signal", st, self._flag(d, kind, self.rank), self.epoch)
+
+    def _wait_all(self, kind, st):
+        for s in range(self.world):
+            if s != self.rank:
+                self._nat.call("bs_stream_wait", st, self._flag(self.rank, kind, s), self.epoch)
+
+    def forward_done(self, lay: StepLayout, sp_floats: int, st) -> None:
+        """After the projection wrote every row into its renderer's buffer:
+        tell every rank, then wait until every rank's rows for this one are in."""
+        remote = sum(r for d, r in enumerate(lay.send_rows) if d != self.rank)
+        self.bytes_fwd += remote * (sp_floats + 1) * 4
+        self._signal_all(0, st)
+        self._wait_all(0, st)
+
+    def backward_done(self, lay: StepLayout, wire: int, st) -> None:
+        remote = sum(r for s, r in enumerate(lay.recv_rows) if s != self.rank)
+        self.bytes_bwd += remote * wire * 4
+        self._signal_all(1, st)
+        self._wait_all(1, st)
+
+    def close(self):
+        if self.base is not None:
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+            self._release()

@@ -355,6 +355,13 @@ class SplatTrainer:
             self.last.update(A=A, W=W, layout=lay)
         n_rows = int(rows_host.sum())
         self.last["rows_per_view"] = rows_host.copy()
+        peer = None
+        if lay is not None and getattr(self.comm, "peer", False):
+            # peer-memory exchange: the projection writes every row straight
+            # into its renderer's receive buffer (exchange.PeerExchange)
+            peer = self.comm.plan(lay, self.sp_floats, self.gsp_floats)
+            pdesc.view_sp, pdesc.view_gid = nat.ptr(peer["view_sp"]), nat.ptr(peer["view_gid"])
+            pdesc.row_gid = None
         if not early:
             # ---- K1: projection into SP rows (send layout)
             sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
@@ -376,15 +383,18 @@ class SplatTrainer:
         else:
             # SP all-to-all to the rendering ranks (line 9), render, G_SP back (line 21)
             with self._t("a2a_fwd"):
-                sp_recv = self.comm.forward(sp[: n_rows * self.sp_floats], lay, self.sp_floats)
-                gid_recv = self.comm.forward_ids(row_gid[:n_rows], lay)
+                if peer is not None:
+                    self.comm.forward_done(lay, self.sp_floats, st)
+                    sp_recv, gid_recv = peer["sp_recv"], peer["gid_recv"]
+                else:
+                    sp_recv = self.comm.forward(sp[: n_rows * self.sp_floats], lay, self.sp_floats).reshape(-1)
+                    gid_recv = self.comm.forward_ids(row_gid[:n_rows], lay)
             mine = torch.as_tensor(lay.my_views, device=dev)
             n_slots = len(lay.my_views)
             self.last["loss_views"] = [int(v) for v in lay.my_views]
             # received rows in canonical order: per rendered view, ascending global id
             slot_rows = np.bincount(lay.seg_slot, weights=lay.seg_rows, minlength=n_slots).astype(np.int64)
-            sp_c, order = self._canonical(sp_recv.reshape(-1), gid_recv, lay.n_recv, lay.seg_rows, lay.seg_slot,
-                                          n_slots)
+            sp_c, order = self._canonical(sp_recv, gid_recv, lay.n_recv, lay.seg_rows, lay.seg_slot, n_slots)
             seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(slot_rows)[:-1]]).astype(np.int64), device=dev)
             seg_slot = self._slot_ids(n_slots)
             gt_slots = None
@@ -395,18 +405,29 @@ class SplatTrainer:
                                                       bidx.index_select(0, mine), gt_slots,
                                                       support=self._recv_support)
             with self._t("a2a_bwd"):
-                # back to the received order, only the used floats of a G_SP
-                # row (3DGS: 9 of the 12), then to the owners
                 wire = self.gsp_wire_floats
-                g = self._uncanonical(gsp_c, order, lay.n_recv, wire)
-                back = self.comm.backward(g, lay, wire).view(-1, wire)
-                if wire != self.gsp_floats:
-                    full = self.buf.get("gsp_home", max(back.shape[0], 1) * self.gsp_floats, torch.float32)
-                    full = full[: back.shape[0] * self.gsp_floats].view(-1, self.gsp_floats)
-                    full.zero_()
-                    full[:, :wire] = back
-                    back = full
-                gsp = back.reshape(-1)
+                if peer is not None:
+                    # each canonical row straight into its owner's send-layout slot
+                    seg_row0_r = torch.as_tensor(np.concatenate([[0], np.cumsum(lay.seg_rows)[:-1]]).astype(np.int64),
+                                                 device=dev)
+                    nat.call("bs_return_rows", nat.ptr(gsp_c), self.gsp_floats, wire, nat.ptr(order), lay.n_recv,
+                             nat.ptr(seg_row0_r), nat.ptr(peer["seg_src"]), nat.ptr(peer["seg_dst0"]), peer["n_segs"],
+                             nat.ptr(peer["dst"]), self.gsp_floats, st)
+                    self.comm.backward_done(lay, wire, st)
+                    gsp = peer["gsp_home"]
+            if peer is None:
+                with self._t("a2a_bwd"):
+                    # back to the received order, only the used floats of a G_SP
+                    # row (3DGS: 9 of the 12), then to the owners
+                    g = self._uncanonical(gsp_c, order, lay.n_recv, wire)
+                    back = self.comm.backward(g, lay, wire).view(-1, wire)
+                    if wire != self.gsp_floats:
+                        full = self.buf.get("gsp_home", max(back.shape[0], 1) * self.gsp_floats, torch.float32)
+                        full = full[: back.shape[0] * self.gsp_floats].view(-1, self.gsp_floats)
+                        full.zero_()
+                        full[:, :wire] = back
+                        back = full
+                    gsp = back.reshape(-1)
         # ---- K1b + K5: projection backward fused with Adam
         self.step_count += 1
         ad = nat.AdamDesc()

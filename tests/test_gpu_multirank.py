@@ -28,12 +28,12 @@ def _setup():
     return ds, g, params, gt
 
 
-def _worker(rank, world, port, q, prefetch=False, patches=1):
+def _worker(rank, world, port, q, prefetch=False, patches=1, peer=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
 
     from paper_2512_20017_b200 import scenes
-    from paper_2512_20017_b200.exchange import SplatExchange
+    from paper_2512_20017_b200.exchange import PeerExchange, SplatExchange
     from paper_2512_20017_b200.sharding import build_bipartite_graph, hierarchical_partition
     from paper_2512_20017_b200.trainer import AdamConfig, SplatTrainer
 
@@ -47,8 +47,8 @@ def _worker(rank, world, port, q, prefetch=False, patches=1):
         sizes = [g.groups[k].size for k in mine]
         gb = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
         tr = SplatTrainer(np.ascontiguousarray(params[:, pts, :]), gb, g.aabbs.reshape(-1, 6)[mine], ds.views,
-                          gt=gt, adam=AdamConfig(scenes.lr_table(50.0)), comm=SplatExchange(), patches=patches,
-                          global_ids=pts)
+                          gt=gt, adam=AdamConfig(scenes.lr_table(50.0)),
+                          comm=PeerExchange() if peer else SplatExchange(), patches=patches, global_ids=pts)
         if prefetch:
             # step 1 starts the asynchronous placement of step 2 (stale W)
             tr.step(BATCH, next_batch=BATCH2)
@@ -62,7 +62,9 @@ def _worker(rank, world, port, q, prefetch=False, patches=1):
         n = len(my_views)
         img = tr.last["image"][: n * 96 * 160 * 3].cpu().numpy().reshape(n, 96, 160, 3) if n else None
         q.put((rank, pts, tr.params.cpu().numpy(), [batch[v] for v in my_views], img, losses,
-               tr.last["A"], tr.last["W"], _gid_lists(tr, n) if n else None))
+               tr.last["A"], tr.last["W"], _gid_lists(tr, n) if n else None, tr.comm.bytes_fwd))
+        if peer:
+            tr.comm.close()
     finally:
         dist.destroy_process_group()
 
@@ -88,8 +90,13 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("prefetch", [False, True])
-def test_two_ranks_match_single_rank(cuda, prefetch):
+@pytest.mark.parametrize("prefetch,peer", [(False, False), (True, False), (False, True), (True, True)])
+def test_two_ranks_match_single_rank(cuda, prefetch, peer):
+    """peer=True: the splat rows and their gradients move through CUDA IPC
+    peer memory (exchange.PeerExchange: the projection writes into the
+    renderer's buffer, bs_return_rows into the owner's, stream-ordered flags)
+    instead of torch.distributed all-to-alls -- both ranks share cuda:0 here,
+    the same loads/stores go over NVLink between GPUs."""
     import torch.multiprocessing as mp
 
     from paper_2512_20017_b200 import scenes
@@ -98,7 +105,7 @@ def test_two_ranks_match_single_rank(cuda, prefetch):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, prefetch)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, prefetch, 1, peer)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
