@@ -238,6 +238,14 @@ typedef struct {
                                   all-to-all fused into the projection) */
   int32_t* const* view_gid;    /* optional, with view_sp and row_gid semantics: the
                                   rows' global ids at view_gid[v] + k */
+  int32_t* bucket_counts;      /* optional (bs_project_fwd, single-pass binning): the
+                                  (view, tile) bucket counters [n_views][tiles_per_slot]
+                                  (zeroed by the caller), incremented per covered tile
+                                  of every row as bs_bin_tiles_count would */
+  int32_t* row_bin;            /* with bucket_counts: int32x4 per SP row, (depth bits,
+                                  x0 | x1 << 16, y0 | y1 << 16, 0) -- the row's tile
+                                  rectangle for bs_bin_tiles_scatter_rec */
+  int32_t tiles_per_slot;      /* bucket stride of bucket_counts */
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,
@@ -303,6 +311,13 @@ int32_t bs_bin_tiles_scatter(const float* sp_rows, int64_t n_rows,
 /* (keys at positions >= capacity are dropped, so the key buffer can be
  * sized before the instance count reaches the host; re-run offsets + scatter
  * with a larger buffer when the count exceeds it) */
+/* Single-pass variant of bs_bin_tiles_scatter: the rows' tile rectangles and
+ * depth bits come from the projection's row_bin records (16 B per row)
+ * instead of a second read of the splat rows; same keys, same positions. */
+int32_t bs_bin_tiles_scatter_rec(const int32_t* row_bin, int64_t n_rows, const int64_t* seg_row0,
+                                 const int32_t* seg_slot, int32_t n_segs, const bs_camera* slot_cams,
+                                 int32_t tiles_per_slot, int32_t* cursor, uint64_t* inst_keys,
+                                 int64_t capacity, void* stream);
 int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* ranges,
                           int32_t n_buckets, int32_t smem_cap,
                           uint32_t* inst_rows, void* stream);

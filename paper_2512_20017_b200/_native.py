@@ -59,7 +59,8 @@ class ProjDesc(C.Structure):
                 ("tiles_x_max", C.c_int32), ("tiles_y_max", C.c_int32), ("model", C.c_int32),
                 ("max_group_points", C.c_int32), ("gsp_form", C.c_int32), ("chunk_prefix", C.c_void_p),
                 ("gsp_zero", C.c_void_p), ("point_gid", C.c_void_p), ("row_gid", C.c_void_p),
-                ("row_support", C.c_void_p), ("view_sp", C.c_void_p), ("view_gid", C.c_void_p)]
+                ("row_support", C.c_void_p), ("view_sp", C.c_void_p), ("view_gid", C.c_void_p),
+                ("bucket_counts", C.c_void_p), ("row_bin", C.c_void_p), ("tiles_per_slot", C.c_int32)]
 
 
 class RasterDesc(C.Structure):
@@ -124,6 +125,7 @@ _SIGS = {
     "bs_gather_rows": (_I32, [_P, _I32, _P, _I64, _P, _P]),
     "bs_scatter_add_rows": (_I32, [_P, _I32, _I32, _P, _I64, _P, _I32, _P]),
     "bs_row_support": (_I32, [_P, _I32, _I64, _P, _P]),
+    "bs_bin_tiles_scatter_rec": (_I32, [_P, _I64, _P, _P, _I32, _P, _I32, _P, _P, _I64, _P]),
     "bs_ipc_handle_bytes": (_SZ, []),
     "bs_ipc_alloc": (_I32, [_SZ, C.POINTER(C.c_void_p), _P]),
     "bs_ipc_open": (_I32, [_P, C.POINTER(C.c_void_p)]),

@@ -14,19 +14,24 @@ from . import _native as nat
 
 
 def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, model_id=nat.MODEL_3DGS,
-                sort_cap=16384, before_sync=None, capacity_hint=None):
+                sort_cap=16384, before_sync=None, capacity_hint=None, records=None):
     """Atomics into (slot, tile) buckets, then a shared-memory sort of every
     bucket by (depth, row); buckets larger than the in-SM sort go through the
     device radix sort.  `buf` is a grow-only buffer cache with
     get(name, n, dtype).  `before_sync` (optional) queues independent GPU work
     ahead of the host read of the instance count, which it then overlaps.
     `capacity_hint` overrides the initial key-buffer size (tests of the
-    overflow path).  Returns (n_inst, inst_rows, ranges, largest bucket)."""
+    overflow path).  `records` (single pass): the projection already counted
+    the buckets into buf "bucket_counts" and wrote each row's tile rectangle
+    (bs_proj_desc.bucket_counts / row_bin); the scatter reads those 16-byte
+    records instead of the splat rows and there is no count pass.
+    Returns (n_inst, inst_rows, ranges, largest bucket)."""
     st, lib = nat.stream_handle(), nat.load()
     nb = n_slots * tiles
     counts = buf.get("bucket_counts", nb, torch.int32)
-    nat.call("bs_bin_tiles_count", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
-             nat.ptr(slot_cams), tiles, nb, nat.ptr(counts), model_id, st)
+    if records is None:
+        nat.call("bs_bin_tiles_count", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
+                 nat.ptr(slot_cams), tiles, nb, nat.ptr(counts), model_id, st)
     ranges = buf.get("ranges", nb * 2, torch.int32)
     cursor = buf.get("cursor", nb, torch.int32)
     stats = buf.get("bin_stats", 2, torch.int64)
@@ -58,8 +63,12 @@ def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, 
         k = buf.get("inst_keys", capacity, torch.int64)
         if capacity_hint is None:
             k = buf.bufs["inst_keys"]  # the whole cached allocation
-        nat.call("bs_bin_tiles_scatter", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot), len(seg_slot),
-                 nat.ptr(slot_cams), tiles, nat.ptr(cursor), nat.ptr(k), k.numel(), model_id, st)
+        if records is None:
+            nat.call("bs_bin_tiles_scatter", nat.ptr(sp), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot),
+                     len(seg_slot), nat.ptr(slot_cams), tiles, nat.ptr(cursor), nat.ptr(k), k.numel(), model_id, st)
+        else:
+            nat.call("bs_bin_tiles_scatter_rec", nat.ptr(records), n_rows, nat.ptr(seg_row0), nat.ptr(seg_slot),
+                     len(seg_slot), nat.ptr(slot_cams), tiles, nat.ptr(cursor), nat.ptr(k), k.numel(), st)
         return k
 
     keys = scatter(inst_cap)

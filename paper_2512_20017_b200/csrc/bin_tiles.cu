@@ -199,6 +199,54 @@ __global__ void scatter_tiles_kernel(BinGeom g, int32_t* __restrict__ cursor, ui
   }
 }
 
+// Single-pass variant: rectangle and depth bits from the projection's row
+// records (int4 per row) -- 16 B per row instead of the splat row.
+__global__ void scatter_rec_kernel(const int4* __restrict__ rec, int64_t n, const int64_t* __restrict__ seg_row0,
+                                   const int32_t* __restrict__ seg_slot, int n_segs, const bs_camera* __restrict__ cams,
+                                   int tiles_per_slot, int32_t* __restrict__ cursor, uint64_t* __restrict__ keys,
+                                   int64_t capacity) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; r0 < n; r0 += stride) {
+    const int64_t r = r0 + lane;
+    int x0 = 0, x1 = 0, y = 0, y1 = 0, x = 0, tx = 1;
+    int64_t bucket0 = 0;
+    uint64_t key = 0ull;
+    bool left = false;
+    if (r < n) {
+      const int4 q = rec[r];
+      x0 = q.y & 0xffff;
+      x1 = (int)((uint32_t)q.y >> 16);
+      y = q.z & 0xffff;
+      y1 = (int)((uint32_t)q.z >> 16);
+      left = x1 > x0 && y1 > y;
+      const int slot = seg_slot[segment_of(seg_row0, n_segs, r)];
+      tx = (cams[slot].width + BS_TILE - 1) / BS_TILE;
+      bucket0 = (int64_t)slot * tiles_per_slot;
+      key = ((uint64_t)(uint32_t)q.x << 32) | (uint64_t)(uint32_t)r;
+      x = x0;
+    }
+    while (__any_sync(0xffffffffu, left)) {
+      int b = -1;
+      if (left) {
+        b = (int)(bucket0 + (int64_t)y * tx + x);
+        if (++x == x1) {
+          x = x0;
+          left = ++y < y1;
+        }
+      }
+      const uint32_t peers = __match_any_sync(0xffffffffu, b);
+      const int leader = __ffs(peers) - 1;
+      int pos = 0;
+      if (b >= 0 && lane == leader) pos = atomicAdd(cursor + b, __popc(peers));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      const int64_t at = (int64_t)pos + __popc(peers & lt);
+      if (b >= 0 && at < capacity) keys[at] = key;
+    }
+  }
+}
+
 // Small buckets (n <= kWarpCap): one warp per bucket, bitonic network held
 // entirely in registers.  Lane l owns elements [l*E, l*E + E) of the padded
 // power of two M = 32*E; partners closer than E are exchanged inside the
@@ -471,6 +519,20 @@ extern "C" int32_t bs_bin_tiles_count(const float* sp_rows, int64_t n_rows, cons
   BinGeom g{sp_rows, n_rows, seg_row0, seg_slot, n_segs, slot_cams, tiles_per_slot, sp_layout(model)};
   count_tiles_kernel<<<grid_for(n_rows, 256), 256, 0, s>>>(g, bucket_counts);
   BS_LAUNCH_CHECK("count_tiles_kernel");
+  return BS_OK;
+}
+
+extern "C" int32_t bs_bin_tiles_scatter_rec(const int32_t* row_bin, int64_t n_rows, const int64_t* seg_row0,
+                                            const int32_t* seg_slot, int32_t n_segs, const bs_camera* slot_cams,
+                                            int32_t tiles_per_slot, int32_t* cursor, uint64_t* inst_keys,
+                                            int64_t capacity, void* stream) {
+  BS_REQUIRE(n_segs >= 1, BS_ERR_PARAMETER, "bin: need at least one segment");
+  BS_REQUIRE(n_rows < (1ll << 32), BS_ERR_PARAMETER, "bin: too many rows for 32-bit row ids");
+  if (n_rows == 0) return BS_OK;
+  scatter_rec_kernel<<<grid_for(n_rows, 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const int4*>(row_bin), n_rows, seg_row0, seg_slot, n_segs, slot_cams, tiles_per_slot, cursor,
+      inst_keys, capacity);
+  BS_LAUNCH_CHECK("scatter_rec_kernel");
   return BS_OK;
 }
 

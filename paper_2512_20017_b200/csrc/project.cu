@@ -9,6 +9,7 @@
 // recomputed identically by every per-point kernel with warp ballots, so no
 // per-(view, point) index table is ever materialised.
 #include "splat2d_math.cuh"
+#include "tile.cuh"
 
 namespace bs {
 namespace {
@@ -101,6 +102,9 @@ struct ProjArgs {
   float* row_support;           // per SP row: the rasteriser's support threshold (project_fwd), or NULL
   float* const* view_sp;        // per view: row-0 pointer of its rows (peer receive buffers), or NULL
   int32_t* const* view_gid;     // per view: row-0 pointer of its global ids, or NULL
+  int32_t* bucket_counts;       // single-pass binning: (view, tile) counters, or NULL
+  int4* row_bin;                // with bucket_counts: per-row (depth bits, x0|x1<<16, y0|y1<<16, 0)
+  int tiles_per_slot;
 };
 
 // Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
@@ -122,6 +126,14 @@ struct Model3 {
     project_forward_t(pt, r, sh, c, n_sh, f, gcol, wk);
   }
   __device__ static void write(float* row, const F& f) { write_sp_row(row, f); }
+  // support box and depth exactly as written into the row (floats 0, 1, 10, 11, 9)
+  __device__ static void box(const F& f, float& u, float& v, float& rx, float& ry, float& depth) {
+    u = f.u;
+    v = f.v;
+    rx = f.valid ? f.radius_x : 0.f;
+    ry = f.valid ? f.radius_y : 0.f;
+    depth = f.depth;
+  }
   template <class SH, class A>
   __device__ static void backward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh,
                                   const F& f, const float* gs, float* g, float* acc, A& add,
@@ -147,6 +159,14 @@ struct Model2 {
     project2d_forward(pt, r, sh, c, n_sh, f, gcol, wk);
   }
   __device__ static void write(float* row, const F& f) { write_sp2_row(row, f); }
+  // support box and depth exactly as written into the row (floats 22, 23, 16, 17, 15)
+  __device__ static void box(const F& f, float& u, float& v, float& rx, float& ry, float& depth) {
+    u = f.box_cx;
+    v = f.box_cy;
+    rx = f.valid ? f.radius_x : 0.f;
+    ry = f.valid ? f.radius_y : 0.f;
+    depth = f.depth;
+  }
   template <class SH, class A>
   __device__ static void backward(const PointIn& pt, const Pre& r, const SH& sh, const bs_camera& c, int n_sh,
                                   const F& f, const float* gs, float* g, float* acc, A& add,
@@ -217,6 +237,17 @@ __global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_ke
         } else {
           M::write(sp + row * M::kSP, f);
           if (a.row_gid) a.row_gid[row] = a.point_gid ? a.point_gid[i] : i;
+        }
+        if (a.bucket_counts) {
+          // single-pass binning: this row's tile rectangle is counted here and
+          // recorded for the scatter, which then never re-reads the row
+          float bu, bv, brx, bry, bd;
+          M::box(f, bu, bv, brx, bry, bd);
+          const int Wv = s_cam[v].width, Hv = s_cam[v].height;
+          int x0, x1, y0, y1;
+          tile_rect_vals(bu, bv, brx, bry, Wv, Hv, x0, x1, y0, y1);
+          a.row_bin[row] = make_int4((int)__float_as_uint(bd), x0 | (x1 << 16), y0 | (y1 << 16), 0);
+          count_rect(a.bucket_counts, (int64_t)v * a.tiles_per_slot, (Wv + BS_TILE - 1) / BS_TILE, x0, x1, y0, y1);
         }
         if (a.row_support) a.row_support[row] = row_support_from_k(f.support_k, M::k2D);
         if (a.gsp_zero) {
@@ -607,7 +638,8 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, d->gsp_zero,
-             d->point_gid, d->row_gid, d->row_support, d->view_sp, d->view_gid};
+             d->point_gid, d->row_gid, d->row_support, d->view_sp, d->view_gid, d->bucket_counts,
+             reinterpret_cast<int4*>(d->row_bin), d->tiles_per_slot};
   const dim3 grid = proj_grid(d, n_groups);
   const size_t smem = sizeof(float4) * 12 * kProjThreads;
   auto launch = [&](auto kern) {
@@ -630,7 +662,7 @@ extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, in
   const int n_sh = (d->sh_degree + 1) * (d->sh_degree + 1);
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, nullptr,
-             nullptr, nullptr, nullptr, nullptr, nullptr};
+             nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
     project_bwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(
@@ -667,7 +699,7 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   const int n_sh = (pd->sh_degree + 1) * (pd->sh_degree + 1);
   ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr, nullptr,
-             nullptr, nullptr, nullptr, nullptr, nullptr};
+             nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   AdamConsts c = make_adam(ad);
   const size_t smem = sizeof(float4) * 24 * kProjThreads;
   auto launch = [&](auto kern) {

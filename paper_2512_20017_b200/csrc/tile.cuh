@@ -8,9 +8,8 @@ namespace bs {
 // centre (u, v) and half-widths (rx, ry) (3DGS: mean, sp[10], sp[11]):
 //   x0 = clamp(floor((u - rx) / 16), 0, tiles_x), x1 = clamp(floor((u + rx) / 16) + 1, 0, tiles_x)
 // (and the same in y with ry): the tiles whose pixel span meets the box.
-__device__ __forceinline__ int tile_rect_at(const float* __restrict__ row, int rad_off, int ctr_off, int W, int H,
-                                            int& x0, int& x1, int& y0, int& y1) {
-  const float u = row[ctr_off], v = row[ctr_off + 1], rx = row[rad_off], ry = row[rad_off + 1];
+__device__ __forceinline__ int tile_rect_vals(float u, float v, float rx, float ry, int W, int H, int& x0, int& x1,
+                                              int& y0, int& y1) {
   if (!(rx > 0.f) || !(ry > 0.f)) {
     x0 = x1 = y0 = y1 = 0;
     return 0;
@@ -23,6 +22,33 @@ __device__ __forceinline__ int tile_rect_at(const float* __restrict__ row, int r
   y1 = (int)fminf(fmaxf(fadd(floorf(fmul(fadd(v, ry), inv)), 1.f), 0.f), (float)ty);
   if (x1 <= x0 || y1 <= y0) return 0;
   return (x1 - x0) * (y1 - y0);
+}
+
+__device__ __forceinline__ int tile_rect_at(const float* __restrict__ row, int rad_off, int ctr_off, int W, int H,
+                                            int& x0, int& x1, int& y0, int& y1) {
+  return tile_rect_vals(row[ctr_off], row[ctr_off + 1], row[rad_off], row[rad_off + 1], W, H, x0, x1, y0, y1);
+}
+
+// Tile counting of one row's rectangle into (slot, tile) buckets,
+// warp-aggregated over the lanes active here (equal buckets -> one atomic).
+__device__ __forceinline__ void count_rect(int32_t* __restrict__ counts, int64_t bucket0, int tx, int x0, int x1,
+                                           int y0, int y1) {
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31;
+  int x = x0, y = y0;
+  bool left = x1 > x0 && y1 > y0;
+  while (__any_sync(act, left)) {
+    int64_t b = -1;
+    if (left) {
+      b = bucket0 + (int64_t)y * tx + x;
+      if (++x == x1) {
+        x = x0;
+        left = ++y < y1;
+      }
+    }
+    const unsigned peers = __match_any_sync(act, (unsigned long long)b);
+    if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(counts + b, __popc(peers));
+  }
 }
 
 // 3DGS rows keep the radii at floats 10, 11 (2DGS rows: 16, 17).

@@ -186,6 +186,8 @@ class SplatTrainer:
         self.timers = None  # optional {stage: [(start_evt, end_evt), ...]}
         self.last = {}
         self.binning = "bucket"  # or "radix" (identical lists, see csrc/bin_tiles.cu)
+        # single rank: the projection counts the tile buckets (no count pass)
+        self.single_pass_bin = os.environ.get("BS_SINGLE_PASS_BIN", "1") == "1"
         self.sort_cap = 16384    # bucket sizes sorted in shared memory
         self.bin_capacity_hint = None  # initial instance-key buffer (tests of the overflow re-run)
         # raster work split: pixels per lane (1 -> 8x4 region per warp, 2 -> 8x8);
@@ -313,11 +315,19 @@ class SplatTrainer:
         if self.comm is not None or self.record_row_gid:
             row_gid = self.buf.get("row_gid", max(S * B, 1), torch.int32)
             pdesc.row_gid = nat.ptr(row_gid)
-        support = None
+        support = records = None
         if self.comm is None:
             # the rasterisers' per-row support threshold, written with the rows
             support = self.buf.get("row_support", max(S * B, 1), torch.float32)
             pdesc.row_support = nat.ptr(support)
+            if early and self.binning != "radix" and self.single_pass_bin:
+                # single-pass binning: the projection counts the (view, tile)
+                # buckets and records each row's tile rectangle
+                counts_b = self.buf.get("bucket_counts", B * self.tiles, torch.int32)
+                counts_b.zero_()
+                records = self.buf.get("row_bin", max(S * B, 1) * 4, torch.int32)
+                pdesc.bucket_counts, pdesc.row_bin, pdesc.tiles_per_slot = nat.ptr(counts_b), nat.ptr(records), \
+                    self.tiles
         if early:
             # the row counts start towards the host before the projection is
             # queued, so the host resumes while the projection still runs
@@ -379,7 +389,8 @@ class SplatTrainer:
             seg_slot = self._slot_ids(B)
             self.last["loss_views"] = list(range(B))
             losses, gsp = self._render_and_backward(sp, n_rows, seg_row0, seg_slot, B, cams, bidx, gt_batch,
-                                                    gsp_cleared=bool(pdesc.gsp_zero), support=support)
+                                                    gsp_cleared=bool(pdesc.gsp_zero), support=support,
+                                                    records=records)
         else:
             # SP all-to-all to the rendering ranks (line 9), render, G_SP back (line 21)
             with self._t("a2a_fwd"):
@@ -583,11 +594,11 @@ class SplatTrainer:
             self.buf.bufs["slot_ids"] = t
         return t[:B]
 
-    def _bin_buckets(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, before_sync=None):
+    def _bin_buckets(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, before_sync=None, records=None):
         """Bucket pipeline (csrc/bin_tiles.cu), see binning.bin_buckets."""
         n_inst, irows, ranges, biggest = bin_buckets(self.buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams,
                                                      self.tiles, self.model_id, self.sort_cap, before_sync,
-                                                     self.bin_capacity_hint)
+                                                     self.bin_capacity_hint, records=records)
         self.last["largest_bucket"] = biggest
         return n_inst, irows, ranges
 
@@ -624,7 +635,7 @@ class SplatTrainer:
         return n_inst, irows, ranges
 
     def _render_and_backward(self, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, gt_views, gt_batch,
-                             slot_patches=None, gsp_cleared=False, support=None):
+                             slot_patches=None, gsp_cleared=False, support=None, records=None):
         dev, st = self.dev, nat.stream_handle()
         lib = nat.load()
         gsp = self.buf.get("gsp", max(n_rows, 1) * self.gsp_floats, torch.float32)
@@ -638,7 +649,8 @@ class SplatTrainer:
             else:
                 # the G_SP accumulator is cleared while the host reads the instance count
                 n_inst, irows, ranges = self._bin_buckets(sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams,
-                                                          before_sync=None if gsp_cleared else gsp.zero_)
+                                                          before_sync=None if gsp_cleared else gsp.zero_,
+                                                          records=records)
         self.last.update(n_rows=n_rows, n_inst=n_inst, n_slots=n_slots)
         # ---- K3: forward + fused L1 partials
         npx = self.H * self.W

@@ -406,13 +406,17 @@ def test_training_sim_report_matches_reference(golden, cuda):
 
 
 def test_binning_pipelines_agree_and_large_bucket_fallback(c1, cuda):
-    """Bucket pipeline (default), radix pipeline, the large-bucket fallback
-    (tiny shared-memory capacity) and the key-buffer overflow re-run give
-    identical per-tile lists."""
+    """Bucket pipeline (default, single pass: the projection counts the
+    buckets), the two-pass bucket pipeline, the radix pipeline, the
+    large-bucket fallback (tiny shared-memory capacity) and the key-buffer
+    overflow re-run give identical per-tile lists."""
     outs = []
-    for mode, cap, hint in (("bucket", 4096, None), ("radix", 4096, None), ("bucket", 8, None), ("bucket", 4096, 16)):
+    for mode, cap, hint, single in (("bucket", 4096, None, True), ("radix", 4096, None, True),
+                                    ("bucket", 8, None, True), ("bucket", 4096, 16, True),
+                                    ("bucket", 4096, None, False), ("bucket", 4096, 16, False)):
         tr = _trainer(c1)
         tr.binning, tr.sort_cap = mode, cap
+        tr.single_pass_bin = single  # counting in the projection vs the count pass
         tr.bin_capacity_hint = hint  # 16: the key buffer overflows, offsets + scatter re-run
         tr.step([0, 3, 5])
         torch.cuda.synchronize()
