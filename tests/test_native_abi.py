@@ -67,8 +67,10 @@ def test_host_library_exports_every_declared_symbol():
 
 def test_proj_desc_layout():
     # bs_proj_desc: 7 int32 (n_views, sh_degree, tiles_x_max, tiles_y_max, model, max_group_points, gsp_form)
-    # + pad + 7 pointers (chunk_prefix, gsp_zero, point_gid, row_gid, row_support, view_sp, view_gid)
-    assert ctypes.sizeof(_native.ProjDesc) == 88 and _native.ProjDesc.view_gid.offset == 80
+    # + pad + 9 pointers (chunk_prefix, gsp_zero, point_gid, row_gid, row_support, view_sp, view_gid,
+    # bucket_counts, row_bin) + int32 tiles_per_slot + pad
+    assert _native.ProjDesc.view_gid.offset == 80 and _native.ProjDesc.row_bin.offset == 96
+    assert _native.ProjDesc.tiles_per_slot.offset == 104 and ctypes.sizeof(_native.ProjDesc) == 112
     assert _native.ProjDesc.row_gid.offset == 56 and _native.ProjDesc.row_support.offset == 64
     # bs_raster_desc: 4 int32, 3 f32, 3 int32, slot_patches, row_support
     assert _native.RasterDesc.slot_patches.offset == 40 and ctypes.sizeof(_native.RasterDesc) == 56
