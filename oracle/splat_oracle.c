@@ -617,6 +617,18 @@ static float support_p2(float o) {
   return k * (-0.5f * LOG2E_F);
 }
 
+/* the support threshold of every row, computed once (bs_row_support):
+ * 3DGS the log2-exponent threshold, 2DGS k; opacity is float 2 of both rows */
+static float* row_support(const float* sp, int64_t m, int stride, int two_d) {
+  float* out = (float*)malloc(sizeof(float) * (size_t)(m > 0 ? m : 1));
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < m; ++k) {
+    const float o = sp[k * stride + 2];
+    out[k] = two_d ? fminf(9.0f, 2.0f * or_det_logf(255.0f * o)) : support_p2(o);
+  }
+  return out;
+}
+
 int32_t or_render(const float* sp, int64_t m, int32_t W, int32_t H, const float* bg, float* image, float* final_T,
                   int32_t* n_contrib, uint32_t* tile_lists, int64_t* n_inst, int32_t* tile_ranges) {
   const int tx = (W + TILE - 1) / TILE, ty = (H + TILE - 1) / TILE;
@@ -634,6 +646,7 @@ int32_t or_render(const float* sp, int64_t m, int32_t W, int32_t H, const float*
     memcpy(tile_ranges, ranges, sizeof(int32_t) * 2 * (size_t)tx * ty);
   }
   if (n_inst) *n_inst = total;
+  float* sup = row_support(sp, m, SPF, 0);
 #pragma omp parallel for schedule(dynamic, 4)
   for (int t = 0; t < tx * ty; ++t) {
     const int bx = t % tx, by = t / tx;
@@ -648,7 +661,7 @@ int32_t or_render(const float* sp, int64_t m, int32_t W, int32_t H, const float*
           const float* r = sp + (int64_t)inst[i].row * SPF;
           float dx, dy;
           const float p2 = splat_p2(r, pxf, pyf, &dx, &dy);
-          if (p2 > 0.f || p2 < support_p2(r[2])) continue; /* outside the support (q > k) */
+          if (p2 > 0.f || p2 < sup[inst[i].row]) continue; /* outside the support (q > k) */
           const float alpha = fminf(0.99f, r[2] * exp2f(p2));
           const float nT = T * (1.f - alpha);
           if (nT < 1e-4f) break;
@@ -664,6 +677,7 @@ int32_t or_render(const float* sp, int64_t m, int32_t W, int32_t H, const float*
       }
   }
   free(inst);
+  free(sup);
   free(ranges);
   return 0;
 }
@@ -674,6 +688,7 @@ int32_t or_render_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const fl
   int32_t* ranges = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)tx * ty);
   int64_t total = 0;
   oinst* inst = bin_view(sp, m, W, H, &total, ranges);
+  float* sup = row_support(sp, m, SPF, 0);
   memset(gsp, 0, sizeof(float) * GSPF * (size_t)m);
   /* serial over tiles: gradient sums are order-sensitive only at fp32 level */
   for (int t = 0; t < tx * ty; ++t) {
@@ -694,7 +709,7 @@ int32_t or_render_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const fl
           const float* r = sp + row * SPF;
           float dx, dy;
           const float p2 = splat_p2(r, pxf, pyf, &dx, &dy);
-          if (p2 > 0.f || p2 < support_p2(r[2])) continue; /* outside the support (q > k) */
+          if (p2 > 0.f || p2 < sup[row]) continue; /* outside the support (q > k) */
           const float ex = exp2f(p2);
           const float raw = r[2] * ex;
           const float alpha = fminf(0.99f, raw);
@@ -722,6 +737,7 @@ int32_t or_render_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const fl
       }
   }
   free(inst);
+  free(sup);
   free(ranges);
   return 0;
 }
@@ -1086,7 +1102,7 @@ static void cross3e(const float* a, const float* b, float* o) {
  * zeta = z0 + ox (hy0 x r2) + oy (r2 x hx0), z0 = hx0 x hy0, with the
  * origin-shifted rows hx0 = r0 - X r2, hy0 = r1 - Y r2 and the pixel's integer
  * offsets (ox, oy) from the origin. */
-static void eval2_o(const float* r, float px, float py, oeval2* e) {
+static void eval2_o(const float* r, float k, float px, float py, oeval2* e) {
   const float* M = r + 3;
   const int x = (int)px, y = (int)py; /* pixel centre = integer + 0.5 */
   const int rx = (x / 8) * 8, ry = (y / 4) * 4;
@@ -1113,7 +1129,6 @@ static void eval2_o(const float* r, float px, float py, oeval2* e) {
   /* decisions without the division (csrc/raster2d.cu eval2, bit-identical):
    * g3 <= k  <=>  zx^2 + zy^2 <= k zz^2, k = min(9, 2 ln(255 o)); the disk
    * branch of min(g3, g2) iff zx^2 + zy^2 <= g2 zz^2 */
-  const float k = fminf(9.0f, 2.0f * or_det_logf(255.0f * r[2]));
   const float n3 = fmaf(e->z[0], e->z[0], e->z[1] * e->z[1]), zz = e->z[2] * e->z[2];
   e->in = (n3 <= k * zz) || (e->g2 <= k);
   e->disk = n3 <= e->g2 * zz;
@@ -1125,10 +1140,12 @@ int32_t or_render2d(const float* sp, int64_t m, int32_t W, int32_t H, const floa
   int32_t* ranges = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)tx * ty);
   int64_t total = 0;
   oinst* inst = bin_view_l(sp, m, W, H, LAY2, &total, ranges);
+  float* sup = row_support(sp, m, SP2F, 1);
   if (tile_lists) {
     if (*n_inst < total) {
       *n_inst = total;
       free(inst);
+      free(sup);
       free(ranges);
       return 1;
     }
@@ -1149,7 +1166,7 @@ int32_t or_render2d(const float* sp, int64_t m, int32_t W, int32_t H, const floa
         for (int i = ranges[2 * t]; i < ranges[2 * t + 1]; ++i) {
           const float* r = sp + (int64_t)inst[i].row * SP2F;
           oeval2 e;
-          eval2_o(r, pxf, pyf, &e);
+          eval2_o(r, sup[inst[i].row], pxf, pyf, &e);
           if (!e.ok || !e.in) continue; /* outside the support: min(g3, g2) > k */
           const float alpha = fminf(0.99f, r[2] * expf(e.power));
           const float nT = T * (1.f - alpha);
@@ -1166,6 +1183,7 @@ int32_t or_render2d(const float* sp, int64_t m, int32_t W, int32_t H, const floa
       }
   }
   free(inst);
+  free(sup);
   free(ranges);
   return 0;
 }
@@ -1176,6 +1194,7 @@ int32_t or_render2d_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const 
   int32_t* ranges = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)tx * ty);
   int64_t total = 0;
   oinst* inst = bin_view_l(sp, m, W, H, LAY2, &total, ranges);
+  float* sup = row_support(sp, m, SP2F, 1);
   memset(gsp, 0, sizeof(float) * GSP2F * (size_t)m);
   for (int t = 0; t < tx * ty; ++t) {
     const int bx = t % tx, by = t / tx;
@@ -1194,7 +1213,7 @@ int32_t or_render2d_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const 
           const int64_t row = inst[i].row;
           const float* r = sp + row * SP2F;
           oeval2 e;
-          eval2_o(r, pxf, pyf, &e);
+          eval2_o(r, sup[inst[i].row], pxf, pyf, &e);
           if (!e.ok || !e.in) continue; /* outside the support: min(g3, g2) > k */
           const float ex = expf(e.power);
           const float raw = r[2] * ex;
@@ -1233,6 +1252,7 @@ int32_t or_render2d_bwd(const float* sp, int64_t m, int32_t W, int32_t H, const 
       }
   }
   free(inst);
+  free(sup);
   free(ranges);
   return 0;
 }
