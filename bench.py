@@ -337,7 +337,7 @@ def run_ours(args, cfg):
         # renderers' / owners' memory (CUDA IPC over NVLink, fused into the
         # projection and the gradient return); collective: torch.distributed
         # all_to_all_single (NCCL; host-staged over gloo)
-        comm = PeerExchange() if args.exchange == "peer" else SplatExchange()
+        comm = PeerExchange.create() if args.exchange == "peer" else SplatExchange()
     setup_s = time.time() - t0
     W, H = cfg["image_size"]
     model = cfg.get("model", "3dgs")

@@ -237,6 +237,87 @@ class PeerExchange(SplatExchange):
         self.base = None                   # own block
         self.peers = [None] * self.world   # mapped blocks (own at [rank])
         self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.ok, self.why = self._preflight()
+
+    @classmethod
+    def create(cls, *args, **kw) -> "SplatExchange":
+        """A PeerExchange when every rank can map every other rank's memory
+        and its stream-ordered flag writes land (checked collectively by
+        `_preflight`), else the collective SplatExchange."""
+        ex = cls(*args, **kw)
+        if ex.ok:
+            return ex
+        import warnings
+
+        warnings.warn(f"peer-memory exchange unavailable ({ex.why}); using all-to-all collectives")
+        return SplatExchange(*args, **kw)
+
+    def _preflight(self):
+        """Collective check: map every peer's block, write a flag into it
+        from this rank's stream, read the own flags back on the host.  Any
+        failure on any rank -> every rank falls back (no device-side wait is
+        issued, so nothing can hang)."""
+        ct, nat = self._ct, self._nat
+        ok, why, base, opened = 1, "", None, []
+        try:
+            hb = int(self.lib.bs_ipc_handle_bytes())
+            p = ct.c_void_p()
+            handle = (ct.c_uint8 * hb)()
+            nat.call("bs_ipc_alloc", 4 * self.world, ct.byref(p), handle)
+            base = p.value
+        except Exception as e:  # noqa: BLE001
+            ok, why, handle = 0, f"alloc: {e}", None
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle) if handle is not None else None, group=self.group)
+        if ok and any(h is None for h in handles):
+            ok, why = 0, "a peer could not allocate"
+        peers = [None] * self.world
+        if ok:
+            try:
+                st = torch.cuda.current_stream().cuda_stream
+                for r in range(self.world):
+                    if r == self.rank:
+                        peers[r] = base
+                        continue
+                    q = ct.c_void_p()
+                    nat.call("bs_ipc_open", (ct.c_uint8 * hb).from_buffer_copy(handles[r]), ct.byref(q))
+                    peers[r] = q.value
+                    opened.append(q.value)
+                for r in range(self.world):
+                    if r != self.rank:
+                        nat.call("bs_stream_signal", st, peers[r] + 4 * self.rank, 1234567)
+                torch.cuda.synchronize()
+            except Exception as e:  # noqa: BLE001
+                ok, why = 0, f"map/signal: {e}"
+        dist.barrier(group=self.group)
+        if ok:
+            try:
+                # the own flag words, copied on the device and read on the host
+                tmp = torch.empty(self.world, dtype=torch.int32, device=self.dev)
+                idx = torch.zeros(1, dtype=torch.int64, device=self.dev)
+                nat.call("bs_gather_rows", base, self.world, nat.ptr(idx), 1, nat.ptr(tmp),
+                         torch.cuda.current_stream().cuda_stream)
+                got = tmp.cpu().numpy()
+                if any(int(got[s]) != 1234567 for s in range(self.world) if s != self.rank):
+                    ok, why = 0, "flag writes did not land"
+            except Exception as e:  # noqa: BLE001
+                ok, why = 0, f"read back: {e}"
+        flag = torch.tensor([ok], dtype=torch.int32)
+        if dist.get_backend(self.group) != "gloo":
+            flag = flag.to(self.dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        for q in opened:
+            try:
+                nat.call("bs_ipc_close", q)
+            except Exception:  # noqa: BLE001
+                pass
+        if base is not None:
+            nat.call("bs_ipc_free", base)
+        if int(flag.item()) == 0 and ok:
+            why = "a peer failed the check"
+        return bool(int(flag.item())), why
 
     # block layout: [fwd flags N u32 | bwd flags N u32 | pad to 256 B] [sp rows] [gid] [gsp home]
     def _offsets(self, cap_r, cap_h):

@@ -48,7 +48,10 @@ def _worker(rank, world, port, q, prefetch=False, patches=1, peer=False):
         gb = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
         tr = SplatTrainer(np.ascontiguousarray(params[:, pts, :]), gb, g.aabbs.reshape(-1, 6)[mine], ds.views,
                           gt=gt, adam=AdamConfig(scenes.lr_table(50.0)),
-                          comm=PeerExchange() if peer else SplatExchange(), patches=patches, global_ids=pts)
+                          comm=PeerExchange.create() if peer else SplatExchange(), patches=patches,
+                          global_ids=pts)
+        if peer:
+            assert getattr(tr.comm, "peer", False), "peer exchange preflight failed"
         if prefetch:
             # step 1 starts the asynchronous placement of step 2 (stale W)
             tr.step(BATCH, next_batch=BATCH2)
