@@ -237,7 +237,8 @@ def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps, row_byt
     return {"fwd_bytes_per_step": fwd, "bwd_bytes_per_step": bwd, "fwd_bytes_predicted": float(pred),
             "random_fwd_bytes_per_step": rnd, "reduction_vs_random_pct": 100.0 * (1.0 - fwd / rnd) if rnd else None,
             "row_bytes": {"fwd": row_bytes, "bwd": grad_bytes}, "patches_per_side": P,
-            "note": "moved = render sets (P > 1 adds splats crossing patch borders); predicted/random = access matrix"}
+            "note": "moved = render sets (P > 1 adds splats crossing patch borders); predicted/random = access "
+                    "matrix (account_iteration, topology (N, 1)); forward bytes per row = splat state + 4-byte id"}
 
 
 _STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_kernel",
@@ -395,8 +396,9 @@ def run_ours(args, cfg):
     if comm is not None:
         placement = {"async": True, "stale_steps": 1, "host_place_ms": round(float(np.mean(comm.place_ms)), 3),
                      "step_wait_ms": round(float(np.mean(comm.wait_ms)), 3) if comm.wait_ms else None}
+        # forward rows travel with their point's 4-byte global id (canonical order)
         comm_report = comm_bytes_report(comm, step_AW, sched[args.warmup:args.warmup + args.steps], ds, g,
-                                        world, rank, args.steps, row_bytes=4 * tr.sp_floats,
+                                        world, rank, args.steps, row_bytes=4 * (tr.sp_floats + 1),
                                         grad_bytes=4 * tr.gsp_wire_floats, P=P)
         peer = getattr(comm, "peer", False) and P == 1
         comm_report.update(backend=backend, communicator_size=world,

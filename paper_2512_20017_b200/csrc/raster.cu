@@ -47,7 +47,10 @@ constexpr float kHalfLog2e = -0.5f * kLog2e;  // p2 = power * log2(e) = q * kHal
 // 10 1.931, 12 1.958, 16 2.118 ms (round 1, separate arrays: 12 best at 2.06)
 #define BS_SPARSE_LANES 10
 #endif
-constexpr int kSparseLanes = BS_SPARSE_LANES;  // contributing lanes handled with direct REDs
+constexpr int kSparseLanes = BS_SPARSE_LANES;
+#ifndef BS_BWD_EARLY_OUT
+#define BS_BWD_EARLY_OUT 0
+#endif  // contributing lanes handled with direct REDs
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float r;
@@ -443,10 +446,14 @@ __device__ __forceinline__ bool pixel_grad_sel(PixelBwd& p, const float4& sa, co
                                                F2 npx, bool live, float g[9]) {
   F2 d;
   const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
+  const bool ok = live && !(power2 > 0.f || power2 < th2);
+#if BS_BWD_EARLY_OUT
+  // no pixel of the warp inside the support: skip the gradient math (warp-uniform)
+  if (!__any_sync(0xffffffffu, ok)) return false;
+#endif
   const float ex = ex2_approx(fminf(power2, 0.f));
   const float raw = __fmul_rn(sb.y, ex);
   const float alpha = fminf(kAlphaMax, raw);
-  const bool ok = live && !(power2 > 0.f || power2 < th2);
   const float ra = rcp_approx(1.f - alpha);  // alpha <= 0.99
   const float T = p.T * ra;
   const float fac = alpha * T;

@@ -168,7 +168,7 @@ __device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f, floa
 }
 
 struct Eval2 {
-  float z[3], iz, u, v, g3, dx, dy, g2, power;
+  float z[3], iz, u, v, g3, dx, dy, g2, pw2;
   bool ok, in, disk;  // z.z != 0; min(g3, g2) <= k; g3 <= g2 (division-free, exact)
 };
 
@@ -193,7 +193,9 @@ __device__ __forceinline__ void eval2(const float4& a, const float4& b, const fl
   e.dx = dd.x;
   e.dy = dd.y;
   e.g2 = __fmul_rn(2.f, __fmaf_rn(e.dx, e.dx, __fmul_rn(e.dy, e.dy)));
-  e.power = __fmul_rn(-0.5f, fminf(e.g3, e.g2));
+  // log2 exponent -0.5 log2(e) min(g3, g2): one rounding, the same value as
+  // (-0.5 min) * log2(e) (the 0.5 scaling is exact)
+  e.pw2 = __fmul_rn(fminf(e.g3, e.g2), -0.5f * kLog2e2);
   const float n3 = __fmaf_rn(e.z[0], e.z[0], __fmul_rn(e.z[1], e.z[1])), zz = __fmul_rn(e.z[2], e.z[2]);
   e.in = e.ok && (n3 <= __fmul_rn(k, zz) || e.g2 <= k);
   e.disk = n3 <= __fmul_rn(e.g2, zz);
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(kT2, BS_R2_FWD_CTAS) raster2d_fwd_kernel(R2Arg
       eval2(sa, s.b[j], s.c[j], col.w, pxf, pyf, oxf, oyf, e);
       if (!e.in) continue;  // min(g3, g2) > k: outside the support
       // past the support test: selects instead of branches
-      const float alpha = fminf(kAMax, __fmul_rn(sa.z, ex2a(__fmul_rn(e.power, kLog2e2))));
+      const float alpha = fminf(kAMax, __fmul_rn(sa.z, ex2a(e.pw2)));
       const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
       const bool fin = nT < kTStop;
       const bool c = !fin;
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(kT2, BS_R2_BWD_CTAS) raster2d_bwd_kernel(
       const float4 col = s.d[j];
       Eval2 e;
       eval2(sa, s.b[j], s.c[j], col.w, pxf, pyf, oxf, oyf, e);
-      const float ex = ex2a(__fmul_rn(fminf(e.power, 0.f), kLog2e2));
+      const float ex = ex2a(fminf(e.pw2, 0.f));
       const float raw = __fmul_rn(sa.z, ex);
       const float alpha = fminf(kAMax, raw);
       const bool any = rel < q.n && e.in;
