@@ -214,3 +214,100 @@ def test_two_ranks_patches_match_single_rank(cuda):
         diff = np.abs(after - ref)
         assert (diff <= 1e-3 * lr_full + 1e-7).mean() > 0.999
         assert (diff <= 2.0 * lr_full + 1e-6).all()
+
+
+def _c2_worker(rank, world, port, q):
+    """One rank of the C2 configuration (1M Gaussians, 1080p, batch 4) over
+    the peer-memory exchange."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_2512_20017_b200 import scenes
+    from paper_2512_20017_b200.culling import zorder_group
+    from paper_2512_20017_b200.exchange import PeerExchange
+    from paper_2512_20017_b200.sharding import build_bipartite_graph, hierarchical_partition
+    from paper_2512_20017_b200.trainer import AdamConfig, SplatTrainer
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ds = scenes.generate_aerial_scene(1, 1_000_000, (1, 1), 8, 50.0, (1920, 1080))
+        g = zorder_group(ds.cloud, G=2048)
+        part = hierarchical_partition(build_bipartite_graph(g, ds), world, 1, eps=0.05, seed=5)
+        mine = np.flatnonzero(part.flat_gpus() == rank)
+        pts = np.concatenate([np.arange(g.groups[k].begin, g.groups[k].end) for k in mine])
+        gb = np.concatenate([[0], np.cumsum([g.groups[k].size for k in mine])]).astype(np.int32)
+        params = scenes.init_gaussians_rows(g.sorted_cloud, 1, scenes.mean_spacing(50.0, (1, 1), 1_000_000), pts)
+        gt = scenes.synthetic_gt(1, 8, 1920, 1080)
+        tr = SplatTrainer(params, gb, g.aabbs.reshape(-1, 6)[mine], ds.views, gt=gt,
+                          adam=AdamConfig(scenes.lr_table(50.0)), comm=PeerExchange.create(), global_ids=pts)
+        assert getattr(tr.comm, "peer", False)
+        tr.step(C2_BATCH)
+        torch.cuda.synchronize()
+        views = [C2_BATCH[v] for v in tr.last["layout"].my_views]
+        n = len(views)
+        T = tr.tiles
+        rg = tr.last["ranges"][: n * T * 2].cpu().numpy().reshape(n, T, 2)
+        irows = tr.last["irows"][: tr.last["n_inst"]].cpu().numpy().astype(np.int64)
+        gid = tr.last["row_gid"].cpu().numpy()
+        lists = [(rg[s, :, 1] - rg[s, :, 0], np.concatenate([gid[irows[a:b]] for a, b in rg[s] if b > a]))
+                 for s in range(n)]
+        img = tr.last["image"][: n * 1080 * 1920 * 3].cpu().numpy().reshape(n, 1080, 1920, 3)
+        q.put((rank, views, lists, img, tr.comm.bytes_fwd))
+        tr.comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+C2_BATCH = [0, 3, 4, 7]
+
+
+def test_two_ranks_c2_scale_lists_bit_identical(cuda):
+    """BASELINE configs[1] size (1M Gaussians, 1080p, batch 4) on 2 ranks over
+    the peer exchange: every rendered view's per-tile lists (as global point
+    ids) and its image are bit-identical to the single-rank step's -- the
+    canonical order at the scale the throughput is quoted on."""
+    import torch.multiprocessing as mp
+
+    from paper_2512_20017_b200 import scenes
+    from paper_2512_20017_b200.culling import zorder_group
+    from paper_2512_20017_b200.trainer import SplatTrainer
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_c2_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        item = q.get(timeout=900)
+        res[item[0]] = item
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ds = scenes.generate_aerial_scene(1, 1_000_000, (1, 1), 8, 50.0, (1920, 1080))
+    g = zorder_group(ds.cloud, G=2048)
+    params = scenes.init_gaussians(g.sorted_cloud, 1, scenes.mean_spacing(50.0, (1, 1), 1_000_000))
+    gt = scenes.synthetic_gt(1, 8, 1920, 1080)
+    tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt)
+    tr.record_row_gid = True
+    tr.step(C2_BATCH)
+    torch.cuda.synchronize()
+    T = tr.tiles
+    rg = tr.last["ranges"][: 4 * T * 2].cpu().numpy().reshape(4, T, 2)
+    irows = tr.last["irows"][: tr.last["n_inst"]].cpu().numpy().astype(np.int64)
+    gid = tr.last["row_gid"].cpu().numpy()
+    img = tr.last["image"][: 4 * 1080 * 1920 * 3].cpu().numpy().reshape(4, 1080, 1920, 3)
+    seen = []
+    for r in (0, 1):
+        assert res[r][4] > 0  # rows really crossed between the ranks
+        for slot, v in enumerate(res[r][1]):
+            k = C2_BATCH.index(v)
+            lens, flat = res[r][2][slot]
+            assert np.array_equal(lens, rg[k, :, 1] - rg[k, :, 0]), f"view {v}: list lengths"
+            ref = np.concatenate([gid[irows[a:b]] for a, b in rg[k] if b > a])
+            assert np.array_equal(flat, ref), f"view {v}: per-tile lists"
+            assert np.array_equal(res[r][3][slot], img[k]), f"view {v}: image"
+            seen.append(v)
+    assert sorted(seen) == sorted(C2_BATCH)
