@@ -31,8 +31,16 @@ __device__ __forceinline__ int tile_rect_at(const float* __restrict__ row, int r
 
 // Tile counting of one row's rectangle into (slot, tile) buckets,
 // warp-aggregated over the lanes active here (equal buckets -> one atomic).
+#ifndef BS_COUNT_PLAIN_ATOMICS
+#define BS_COUNT_PLAIN_ATOMICS 0
+#endif
 __device__ __forceinline__ void count_rect(int32_t* __restrict__ counts, int64_t bucket0, int tx, int x0, int x1,
                                            int y0, int y1) {
+#if BS_COUNT_PLAIN_ATOMICS
+  for (int y = y0; y < y1; ++y)
+    for (int x = x0; x < x1; ++x) atomicAdd(counts + bucket0 + (int64_t)y * tx + x, 1);
+  return;
+#endif
   const unsigned act = __activemask();
   const int lane = threadIdx.x & 31;
   int x = x0, y = y0;

@@ -323,11 +323,7 @@ class SplatTrainer:
             if early and self.binning != "radix" and self.single_pass_bin:
                 # single-pass binning: the projection counts the (view, tile)
                 # buckets and records each row's tile rectangle
-                counts_b = self.buf.get("bucket_counts", B * self.tiles, torch.int32)
-                counts_b.zero_()
-                records = self.buf.get("row_bin", max(S * B, 1) * 4, torch.int32)
-                pdesc.bucket_counts, pdesc.row_bin, pdesc.tiles_per_slot = nat.ptr(counts_b), nat.ptr(records), \
-                    self.tiles
+                records = self._single_pass_bin(pdesc, B, S * B)
         if early:
             # the row counts start towards the host before the projection is
             # queued, so the host resumes while the projection still runs
@@ -374,6 +370,8 @@ class SplatTrainer:
             pdesc.row_gid = None
         if not early:
             # ---- K1: projection into SP rows (send layout)
+            if self.comm is None and self.binning != "radix" and self.single_pass_bin:
+                records = self._single_pass_bin(pdesc, B, n_rows)  # sized by the row counts just read
             sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
             with self._t("project"):
                 nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask),
@@ -550,6 +548,15 @@ class SplatTrainer:
                      nat.ptr(self.exp_avg_sq), S, nat.ptr(mask), nat.ptr(self.group_begin), self.n_groups,
                      nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
         return losses
+
+    def _single_pass_bin(self, pdesc, B, n_rows):
+        """Zeroed (view, tile) bucket counters and the per-row tile records the
+        projection fills (bs_proj_desc.bucket_counts / row_bin)."""
+        counts_b = self.buf.get("bucket_counts", B * self.tiles, torch.int32)
+        counts_b.zero_()
+        records = self.buf.get("row_bin", max(n_rows, 1) * 4, torch.int32)
+        pdesc.bucket_counts, pdesc.row_bin, pdesc.tiles_per_slot = nat.ptr(counts_b), nat.ptr(records), self.tiles
+        return records
 
     def _canonical(self, sp_recv, gid_recv, n, seg_rows, seg_slot, n_slots):
         """Received rows -> canonical order (slot-major, ascending global id;
