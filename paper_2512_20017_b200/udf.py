@@ -236,9 +236,9 @@ class _RenderFn(torch.autograd.Function):
         g_sp = torch.zeros((rows.shape[0], gw), dtype=torch.float32, device=rows.device)
         desc = nat.RasterDesc(1, tiles, W, H, (ctypes.c_float * 3)(*bg), 0, 1)
         _, bwd = _raster_names(model_id)
+        gimg = grad_image.float().contiguous()  # held until the launch is queued
         nat.call(bwd, desc, nat.ptr(rows), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image), nat.ptr(final_T),
-                 nat.ptr(n_contrib), nat.ptr(grad_image.float().contiguous()), None, None, nat.ptr(g_sp),
-                 nat.stream_handle())
+                 nat.ptr(n_contrib), nat.ptr(gimg), None, None, nat.ptr(g_sp), nat.stream_handle())
         grad_rows = torch.zeros_like(rows)
         if model_id == nat.MODEL_2DGS:
             grad_rows[:, 0:2] = g_sp[:, 0:2]
