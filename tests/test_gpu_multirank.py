@@ -311,3 +311,42 @@ def test_two_ranks_c2_scale_lists_bit_identical(cuda):
             assert np.array_equal(res[r][3][slot], img[k]), f"view {v}: image"
             seen.append(v)
     assert sorted(seen) == sorted(C2_BATCH)
+
+
+def test_four_ranks_peer_match_single_rank(cuda):
+    """4 ranks (one view each) over the peer-memory exchange: per-tile lists of
+    global ids and images bit-identical to the single-rank step."""
+    import torch.multiprocessing as mp
+
+    from paper_2512_20017_b200.trainer import SplatTrainer
+
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, False, 1, True)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        item = q.get(timeout=600)
+        res[item[0]] = item
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ds, g, params, gt = _setup()
+    tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt)
+    tr.record_row_gid = True
+    tr.step(BATCH)
+    lists_ref = _gid_lists(tr, len(BATCH))
+    img_ref = tr.last["image"][: len(BATCH) * 96 * 160 * 3].cpu().numpy().reshape(len(BATCH), 96, 160, 3)
+    seen = []
+    for r in range(world):
+        assert np.array_equal(res[r][6], res[0][6]) and np.array_equal(res[r][7], res[0][7])
+        for slot, v in enumerate(res[r][3]):
+            k = BATCH.index(v)
+            for t, (a, b) in enumerate(zip(res[r][8][slot], lists_ref[k])):
+                assert np.array_equal(a, b), f"rank {r} view {v} tile {t}"
+            assert np.array_equal(res[r][4][slot], img_ref[k]), f"rank {r} view {v}"
+            seen.append(v)
+    assert sorted(seen) == sorted(BATCH)
