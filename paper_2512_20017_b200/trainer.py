@@ -549,6 +549,23 @@ class SplatTrainer:
                      nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
         return losses
 
+    # ------------------------------------------------------------------ checkpoint
+    def state_dict(self) -> dict:
+        """The rank's training state (shard parameters, Adam moments, step
+        counter; SURVEY.md §5 checkpoint/resume): `torch.save` it per rank."""
+        return {"params": self.params.detach().clone(), "exp_avg": self.exp_avg.detach().clone(),
+                "exp_avg_sq": self.exp_avg_sq.detach().clone(), "step": int(self.step_count),
+                "model": self.model, "n_points": int(self.S)}
+
+    def load_state_dict(self, sd: dict) -> None:
+        from .status import ConsistencyError
+
+        if sd.get("model") != self.model or int(sd.get("n_points", -1)) != self.S:
+            raise ConsistencyError("checkpoint is of a different model or shard")
+        for name in ("params", "exp_avg", "exp_avg_sq"):
+            getattr(self, name).copy_(sd[name].to(self.dev))
+        self.step_count = int(sd["step"])
+
     def _single_pass_bin(self, pdesc, B, n_rows):
         """Zeroed (view, tile) bucket counters and the per-row tile records the
         projection fills (bs_proj_desc.bucket_counts / row_bin)."""

@@ -142,3 +142,29 @@ def test_gsp_cleared_by_projection_over_three_steps(cuda):
     assert (np.abs(pa - pb) <= 1e-3 * lr_full + 4 * np.spacing(np.abs(pa))).all()
     mscale = np.abs(mb).reshape(15, -1, 4).max(axis=1, keepdims=True) + 1e-30
     assert (np.abs(ma - mb) / mscale).max() <= 1e-3
+
+
+def test_checkpoint_resume(cuda, tmp_path):
+    """state_dict / load_state_dict: resuming a saved shard (parameters, Adam
+    moments, step counter) continues training exactly like the uninterrupted
+    run (same kernels, same inputs; tolerance for atomic order only)."""
+    ds, params, gb, aabb, gt = c1_setup()
+    lr = scenes.lr_table(50.0)
+    a = SplatTrainer(params, gb, aabb, ds.views, gt=gt, adam=AdamConfig(lr))
+    a.step([0, 2, 5])
+    a.step([1, 3, 6])
+    torch.save(a.state_dict(), tmp_path / "ckpt.pt")
+    b = SplatTrainer(params, gb, aabb, ds.views, gt=gt, adam=AdamConfig(lr))
+    b.load_state_dict(torch.load(tmp_path / "ckpt.pt"))
+    assert b.step_count == 2
+    a.step([0, 4, 7])
+    b.step([0, 4, 7])
+    torch.cuda.synchronize()
+    pa, pb = a.params.cpu().numpy(), b.params.cpu().numpy()
+    lr_full = np.broadcast_to(lr.reshape(15, 1, 4), pa.shape)
+    assert (np.abs(pa - pb) <= 1e-3 * lr_full + 4 * np.spacing(np.abs(pa))).all()
+    from paper_2512_20017_b200.status import ConsistencyError
+
+    c = SplatTrainer(params[:, :100], np.array([0, 100], dtype=np.int32), aabb[:1], ds.views, gt=gt)
+    with pytest.raises(ConsistencyError):
+        c.load_state_dict(a.state_dict())
