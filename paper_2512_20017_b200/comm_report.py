@@ -12,7 +12,8 @@ LocalityAwareStrategy (GPU-built bipartite graph, native multilevel
 partitioner, per-step hierarchical_place) and once with RandomStrategy, on
 the same batch schedule.  Bytes are reported for the reference's accounting
 unit (profile bytes per point, 44 B) and for the rows this framework's
-exchange actually moves (SP 48 B forward, G_SP 36 B backward).  The access
+exchange actually moves (SP 48 B + the point's 4-byte global id forward,
+G_SP 36 B backward).  The access
 matrices come from the sm_100a culling kernel; no training step runs.
 """
 
@@ -40,7 +41,7 @@ CONFIGS = {
     "tiny": dict(seed=0, n_points=200_000, grid=(4, 4), n_views=32, image_size=(640, 360), batch=8, P=1, G=2048,
                  desc="200k-point aerial scene, batch 8"),
 }
-SP_BYTES, GSP_BYTES = 48, 36
+SP_BYTES, GSP_BYTES = 48 + 4, 36  # forward rows travel with their global id (canonical order)
 
 
 def run(cfg: dict, gpus, epochs: int = 1, log=print) -> dict:
