@@ -17,4 +17,4 @@ def test_comm_report_tiny(cuda):
         loc, rnd = row["fwd_points_per_step"]["locality"], row["fwd_points_per_step"]["random"]
         assert 0 <= loc < rnd
         assert row["reduction_pct"] == pytest.approx(100.0 * (1.0 - loc / rnd))
-        assert row["fwd_bytes_per_step"]["locality"] == loc * 48
+        assert row["fwd_bytes_per_step"]["locality"] == loc * comm_report.SP_BYTES  # 48-byte row + 4-byte id
