@@ -168,6 +168,9 @@ _HOST_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "l
 _host = None
 _HOST_SIGS = {
     "bs_partition_multilevel": (_I32, [_I64, _P, _I64, _P, _P, _P, _I32, C.c_double, _P, _P]),
+    "bs_local_search": (_I32, [_I64, _I32, _P, _P, C.c_double, C.c_double, C.c_double, C.c_double, _I32,
+                               C.c_double, _P, _I32, _P, _P]),
+    "bs_array_pow": (_I32, [_P, C.c_double, _P, _I64, _P]),
 }
 HOST_EXPORTED = tuple(_HOST_SIGS)
 

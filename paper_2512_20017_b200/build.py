@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libsplat_b200.so")
 HOST_LIB = os.path.join(LIBDIR, "libsplat_host.so")
-HOST_SOURCES = ["host/partition.cpp"]
+HOST_SOURCES = ["host/partition.cpp", "host/placement.cpp"]
 ORACLE_DIR = os.path.join(ROOT, "oracle")
 ORACLE_LIB = os.path.join(ORACLE_DIR, "build", "libsplat_oracle.so")
 
@@ -72,7 +72,8 @@ def build_host(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in HOST_SOURCES]
     hdr = os.path.join(ROOT, "include", "splat_host.h")
     if force or not _newer(HOST_LIB, srcs + [hdr]):
-        _run(["g++", "-O3", "-std=c++17", "-fPIC", "-shared", "-fopenmp", "-Wall", "-o", HOST_LIB, *srcs], verbose)
+        _run(["g++", "-O3", "-std=c++17", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off", "-Wall", "-o", HOST_LIB,
+              *srcs], verbose)
     return HOST_LIB
 
 

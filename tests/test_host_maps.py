@@ -61,9 +61,10 @@ def test_placement_matches_reference(golden, ci):
     mat = golden[f"place_mat_{ci}"]
     B, N = mat.shape
     assert np.array_equal(asg.lsa_assign(mat, B // N).assignment, golden[f"place_lsa_{ci}"])
-    sol, info = asg.local_search(mat, asg.lsa_assign(mat, B // N), asg.CostCoefficients())
-    assert np.array_equal(sol.assignment, golden[f"place_ls_{ci}"])
-    assert np.array_equal(np.array(info["relaxed_history"]), golden[f"place_ls_hist_{ci}"])
+    for native in (False, True):  # numpy restatement and the C++/OpenMP search (csrc/host/placement.cpp)
+        sol, info = asg.local_search(mat, asg.lsa_assign(mat, B // N), asg.CostCoefficients(), native=native)
+        assert np.array_equal(sol.assignment, golden[f"place_ls_{ci}"])
+        assert np.array_equal(np.array(info["relaxed_history"]), golden[f"place_ls_hist_{ci}"])
     flat = asg.hierarchical_place(mat, 1, N, INTER, INTRA)
     assert np.array_equal(flat.assignment, golden[f"place_flat_{ci}"])
     if N % 2 == 0:
@@ -117,3 +118,54 @@ def test_comm_reduction_schedule_check():
     r2 = acc.EpochReport("b", 0, 1, 1, 1, topo, [], [[1]])
     with pytest.raises(acc.ComparisonError):
         acc.comm_reduction(r1, r2)
+
+
+def test_native_local_search_swap_for_swap():
+    """bs_local_search (C++/OpenMP, numpy's power kernel passed in) against
+    the numpy restatement of placement.py:182-281 on random instances: the
+    same final W and the same relaxed history bit for bit (so the same swap
+    sequence), over p = 1, 2, 3, 4, inf, tied columns, LSA and random starts,
+    and up to B = 128 patches (C5: 32 views x 2^2 patches, N = 8)."""
+    rng = np.random.default_rng(2024)
+    swaps = 0
+    for trial in range(160):
+        N = int(rng.choice([2, 3, 4, 8]))
+        B = 128 if trial % 40 == 0 else N * int(rng.integers(1, 9))
+        if B % N:
+            B = N * (B // N)
+        A = rng.integers(0, 10 ** int(rng.integers(2, 8)), size=(B, N))
+        if trial % 3 == 0 and N > 1:
+            A[:, 0] = A[:, 1]  # ties between candidate swaps
+        p = float([1.0, 2.0, 3.0, 4.0, np.inf][trial % 5])
+        co = asg.CostCoefficients(alpha=0.0, beta=float(rng.random()), gamma=float(rng.random()),
+                                  delta=float(rng.random()) + 0.1, p=p)
+        if trial % 2:
+            init = asg.lsa_assign(A, B // N)
+        else:
+            init = asg.PlacementSolution(np.repeat(np.arange(N), B // N)[rng.permutation(B)], N)
+        s1, i1 = asg.local_search(A, init, co, native=False)
+        s2, i2 = asg.local_search(A, init, co, native=True)
+        assert np.array_equal(s1.assignment, s2.assignment)
+        assert i1["relaxed_history"] == i2["relaxed_history"]
+        assert np.array_equal(init.assignment, s1.assignment) or i1["n_swaps"] > 0
+        swaps += i1["n_swaps"]
+    assert swaps > 500
+
+
+def test_native_local_search_limits():
+    """max_sweeps and errors: the native search stops after max_sweeps swaps
+    like the numpy one, and rejects a W outside [0, N)."""
+    rng = np.random.default_rng(5)
+    A = rng.integers(0, 10**6, size=(64, 8))
+    init = asg.PlacementSolution(np.repeat(np.arange(8), 8)[rng.permutation(64)], 8)
+    for k in (0, 1, 3):
+        s1, i1 = asg.local_search(A, init, INTER, max_sweeps=k, native=False)
+        s2, i2 = asg.local_search(A, init, INTER, max_sweeps=k, native=True)
+        assert i2["n_swaps"] == i1["n_swaps"] <= k and np.array_equal(s1.assignment, s2.assignment)
+    from paper_2512_20017_b200 import _native as nat
+    W = np.full(64, 9, dtype=np.int64)
+    hist = np.empty(2)
+    n = np.zeros(1, dtype=np.int64)
+    with pytest.raises(asg.ParameterError):
+        nat.host_call("bs_local_search", 64, 8, np.ascontiguousarray(A).ctypes.data, W.ctypes.data, 0.25, 0.25, 0.5,
+                      4.0, 1, -1.0, None, 1, hist.ctypes.data, n.ctypes.data)
