@@ -52,6 +52,15 @@ constexpr int kSparseLanes = BS_SPARSE_LANES;
 #define BS_BWD_EARLY_OUT 0
 #endif  // contributing lanes handled with direct REDs
 
+#ifdef BS_RASTER_STATS
+// tuning instrumentation (never in the product build; tools/raster_stats.py):
+// [0] bwd warp-chunks, [1] bwd kept iterations, [2] of them with no
+// contributing lane, [3] sparse, [4] dense, [5] sum of contributing lanes,
+// [6] sum of live lanes, [8..40] histogram of contributing lanes; [48] fwd
+// warp-chunks, [49] fwd kept iterations, [50] fwd lanes past the support test
+__device__ unsigned long long g_rstats[64];
+#endif
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -276,10 +285,17 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
   const float* sup = kSup ? a.support : nullptr;  // kSup: per-row support thresholds given
   fetch_splat(f, sp, sup, inst_rows, rg.x + lane, rg.x + lane < rg.y);
   uint32_t row_next = fetch_row(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
+#ifdef BS_RASTER_STATS
+  unsigned long long fst[3] = {0, 0, 0};
+#endif
   for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
     if (__all_sync(0xffffffffu, all_done<PPL>(p))) break;
     const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
+#ifdef BS_RASTER_STATS
+    fst[0]++;
+    fst[1] += __popc(bits);
+#endif
     if (keep) stage(s, lane, f, kSup);
     fetch_row_data(f, sp, sup, row_next, b0 + 32 + lane < rg.y);
     row_next = fetch_row(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
@@ -292,6 +308,13 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
       const float2 sc = s.c[j];
       const int rel = b0 + j - rg.x;
       if constexpr (PPL == 1) {
+#ifdef BS_RASTER_STATS
+        {
+          F2 dd;
+          const float pw = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, f2(-pxf, -((float)q.py0 + 0.5f)), dd);
+          fst[2] += __popc(__ballot_sync(__activemask(), !p[0].done && !(pw > 0.f || pw < sc.y)));
+        }
+#endif
         if (!p[0].done) blend_sel(p[0], sa, sb, sc.x, sc.y, f2(-pxf, -((float)q.py0 + 0.5f)), rel);
       } else {
 #pragma unroll
@@ -301,6 +324,10 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads) raster_fwd_kernel(
     }
     __syncwarp();
   }
+#ifdef BS_RASTER_STATS
+  if (lane == 0)
+    for (int k = 0; k < 3; ++k) atomicAdd(&g_rstats[48 + k], fst[k]);
+#endif
   float l = 0.f;
 #pragma unroll
   for (int k = 0; k < PPL; ++k) {
@@ -550,9 +577,18 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
   fetch_splat(f, sp, sup, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
   uint32_t row_next = fetch_row(inst_rows, end - 33 - lane, end - 33 - lane >= rg.x);
   // chunks back to front; within a chunk lane j holds instance cend - 1 - j
+#ifdef BS_RASTER_STATS
+  unsigned long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long hist[33];
+  for (int k = 0; k < 33; ++k) hist[k] = 0;
+#endif
   for (int cend = end; cend > rg.x; cend -= 32) {
     const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
     uint32_t bits = __ballot_sync(0xffffffffu, keep);
+#ifdef BS_RASTER_STATS
+    st[0]++;
+    st[1] += __popc(bits);
+#endif
     if (keep) stage(s, lane, f, kSup);
     fetch_row_data(f, sp, sup, row_next, cend - 33 - lane >= rg.x);
     row_next = fetch_row(inst_rows, cend - 65 - lane, cend - 65 - lane >= rg.x);
@@ -577,8 +613,22 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
             any |= pixel_grad<false, kBg>(p[k], sa, sb, sc.x, sc.y, f2(-pxf, -((float)(q.py0 + k) + 0.5f)), g);
       }
       const uint32_t who = __ballot_sync(0xffffffffu, any);
+#ifdef BS_RASTER_STATS
+      st[2] += who == 0u;
+      st[3] += who != 0u && __popc(who) <= kSparseLanes;
+      st[4] += __popc(who) > kSparseLanes;
+      st[5] += __popc(who);
+      st[6] += __popc(__ballot_sync(0xffffffffu, rel < p[0].n));
+      hist[__popc(who)]++;
+#endif
       if (who == 0u) continue;
       float* dst = g_sp + (int64_t)__float_as_uint(sc.z) * BS_GSP_FLOATS;
+#ifdef BS_BWD_NO_REDUCE
+      // tuning probe only (tools/gpu_probe_reduce.sh): the gradient terms are
+      // computed but not reduced -- the upper bound of any reduction scheme
+      if (g[0] + g[1] + g[2] + g[3] + g[4] + g[5] + g[6] + g[7] + g[8] == 1.2345e-30f) atomicAdd(dst, 1.f);
+      continue;
+#endif
       if (__popc(who) <= kSparseLanes) {
         if (any) {
 #if BS_GSP_FLOATS == 12
@@ -599,6 +649,13 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
     }
     __syncwarp();
   }
+#ifdef BS_RASTER_STATS
+  if (lane == 0) {
+    for (int k = 0; k < 7; ++k) atomicAdd(&g_rstats[k], st[k]);
+    for (int k = 0; k < 33; ++k)
+      if (hist[k]) atomicAdd(&g_rstats[8 + k], hist[k]);
+  }
+#endif
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -734,6 +791,17 @@ extern "C" int32_t bs_raster_bwd(const bs_raster_desc* d, const float* sp_rows, 
   BS_LAUNCH_CHECK("raster_bwd_kernel");
   return BS_OK;
 }
+
+#ifdef BS_RASTER_STATS
+extern "C" int32_t bs_debug_raster_stats(unsigned long long* out, int32_t reset) {
+  cudaMemcpyFromSymbol(out, g_rstats, sizeof(g_rstats));
+  if (reset) {
+    unsigned long long z[64] = {0};
+    cudaMemcpyToSymbol(g_rstats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 extern "C" size_t bs_l1_loss_workspace(int32_t n_slots) { return sizeof(float) * 64 * (size_t)n_slots; }
 
