@@ -246,6 +246,10 @@ typedef struct {
                                   x0 | x1 << 16, y0 | y1 << 16, 0) -- the row's tile
                                   rectangle for bs_bin_tiles_scatter_rec */
   int32_t tiles_per_slot;      /* bucket stride of bucket_counts */
+  float* densify_stats;        /* optional (bs_project_bwd_adam, 3DGS): float2 per local
+                                  point, (sum over views of |dL/d mean2d| in NDC units,
+                                  number of views with a valid splat) ACCUMULATED --
+                                  the densification statistic (bs_densify_mark) */
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,
@@ -385,6 +389,53 @@ int32_t bs_raster2d_bwd(const bs_raster_desc* desc_host, const float* sp_rows,
                         const int32_t* n_contrib, const float* grad_image,
                         const uint8_t* gt, const int32_t* gt_slot_view,
                         float* g_sp, void* stream);
+
+/* ---- densification ("periodic densification"; standard 3DGS
+ * clone / split / prune) ------------------------------- */
+/* Per point (3DGS): o = sigmoid(opacity logit), smax = max_k exp(log_scale_k),
+ * avg = stats.x / stats.y (0 when stats.y == 0):
+ *   PRUNE (0 outputs)  o < min_opacity, or max_scale > 0 and smax > max_scale
+ *   SPLIT (2 outputs)  else avg >= grad_threshold and smax >  split_scale
+ *   CLONE (2 outputs)  else avg >= grad_threshold (and smax <= split_scale)
+ *   KEEP  (1 output)   otherwise
+ * Outputs stay in the point's group, in point order: KEEP copies the point
+ * and its Adam moments; CLONE writes the point (with its moments) then an
+ * exact copy with zero moments; SPLIT writes two children with zero moments,
+ * log scales minus ln(1.6) and means mu + R(q) (s * eps), eps ~ N(0, 1) per
+ * axis by the Irwin-Hall sum of 12 uniforms from splitmix64(seed, global id,
+ * child, axis) -- every op a round-to-nearest float op, so the outputs are
+ * bit-exact against the CPU oracle (oracle/splat_oracle.c so_densify). */
+#define BS_DENSIFY_PRUNE 0
+#define BS_DENSIFY_KEEP 1
+#define BS_DENSIFY_CLONE 2
+#define BS_DENSIFY_SPLIT 3
+typedef struct {
+  int32_t model;          /* BS_MODEL_3DGS */
+  float grad_threshold;   /* on the mean NDC-space |dL/d mean2d| (3DGS: 2e-4) */
+  float split_scale;      /* split above / clone at or below this max world scale */
+  float min_opacity;      /* prune below (3DGS: 0.005) */
+  float max_scale;        /* prune above this max world scale; <= 0: off */
+  uint32_t seed;          /* split samples */
+} bs_densify_desc;
+/* action: int32 [n_points] (BS_DENSIFY_*); group_out: int32 [n_groups], the
+ * number of output points of each group (its new size). */
+int32_t bs_densify_mark(const bs_densify_desc* desc_host, const float* params, int64_t n_points,
+                        const float* stats, const int32_t* group_begin, int32_t n_groups,
+                        int32_t* action, int32_t* group_out, void* stream);
+/* new_group_begin: int32 [n_groups + 1], the exclusive scan of group_out;
+ * point_gid: global id per old point (NULL = local index) for the split
+ * samples; outputs params_new / exp_avg_new / exp_avg_sq_new (plane layout,
+ * n_new points) and src_index int32 [n_new] (the old point each new point
+ * comes from). */
+int32_t bs_densify_apply(const bs_densify_desc* desc_host, const float* params, const float* exp_avg,
+                         const float* exp_avg_sq, int64_t n_points, const int32_t* action,
+                         const int32_t* group_begin, const int32_t* new_group_begin, int32_t n_groups,
+                         const int32_t* point_gid, float* params_new, float* exp_avg_new,
+                         float* exp_avg_sq_new, int64_t n_new, int32_t* src_index, void* stream);
+/* aabb_out f32 [n_groups][6] (min xyz, max xyz) of each group's means --
+ * visibility.py:127-133 for groups of any size. */
+int32_t bs_group_aabb_ranges(const float* params, int64_t n_points, const int32_t* group_begin,
+                             int32_t n_groups, float* aabb_out, void* stream);
 
 /* ---- K1b + K5 ---------------------------------------------------------- */
 /* grad_params: plane layout like params, ACCUMULATED (caller zeroes). */

@@ -51,6 +51,9 @@ def lib():
             "or_render2d": (I32, [P, I64, I32, I32, P, P, P, P, P, P, P]),
             "or_render2d_bwd": (I32, [P, I64, I32, I32, P, P, P, P, P]),
             "or_train_step_model": (D, [P, P, P, I64, P, P, I32, P, I32, P, F, F, F, I32, I32, I32]),
+            "so_densify_mark": (None, [P, I64, P, P, I32, F, F, F, F, P, P]),
+            "so_densify_apply": (None, [P, P, P, I64, P, P, P, I32, P, C.c_uint32, P, P, P, I64, P]),
+            "so_group_aabb_ranges": (None, [P, P, I32, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -213,3 +216,34 @@ def zorder_layout(positions, G):
     gb = np.concatenate([np.arange(0, n, G), [n]]).astype(np.int32)
     aabb = np.stack([np.concatenate([spos[b:e].min(0), spos[b:e].max(0)]) for b, e in zip(gb[:-1], gb[1:])])
     return perm, gb, aabb.astype(np.float32)
+
+
+def densify(params, m, v, stats, group_begin, grad_threshold, split_scale, min_opacity, max_scale=0.0, seed=0,
+            gid=None):
+    """Clone / split / prune of a 3DGS shard (csrc/densify.cu semantics).
+    params, m, v: float32 [15, S, 4]; stats float32 [S, 2] or None.
+    Returns (action, group_out, new_group_begin, params', m', v', src_index, aabb')."""
+    L = lib()
+    params, m, v = (_c(a, np.float32) for a in (params, m, v))
+    S = params.shape[1]
+    gb = _c(group_begin, np.int32)
+    ng = len(gb) - 1
+    st = None if stats is None else _c(stats, np.float32)
+    action = np.zeros(S, np.int32)
+    gout = np.zeros(ng, np.int32)
+    L.so_densify_mark(params.ctypes.data, S, _p(st), gb.ctypes.data, ng, grad_threshold, split_scale, min_opacity,
+                      max_scale, action.ctypes.data, gout.ctypes.data)
+    nb = np.zeros(ng + 1, np.int32)
+    nb[1:] = np.cumsum(gout)
+    Sn = int(nb[-1])
+    pn = np.zeros((15, Sn, 4), np.float32)
+    mn = np.zeros_like(pn)
+    vn = np.zeros_like(pn)
+    src = np.zeros(Sn, np.int32)
+    g = None if gid is None else _c(gid, np.int32)
+    L.so_densify_apply(params.ctypes.data, m.ctypes.data, v.ctypes.data, S, action.ctypes.data, gb.ctypes.data,
+                       nb.ctypes.data, ng, _p(g), int(seed) & 0xFFFFFFFF, pn.ctypes.data, mn.ctypes.data,
+                       vn.ctypes.data, Sn, src.ctypes.data)
+    aabb = np.zeros((ng, 6), np.float32)
+    L.so_group_aabb_ranges(pn.ctypes.data, nb.ctypes.data, ng, aabb.ctypes.data)
+    return action, gout, nb, pn, mn, vn, src, aabb

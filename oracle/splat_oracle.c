@@ -1314,3 +1314,116 @@ double or_train_step_model(float* params, float* exp_avg, float* exp_avg_sq, int
   return loss;
 }
 
+
+/* ---- densification (restates csrc/densify.cu; include/splat_b200.h
+ * bs_densify_* semantics: 3DGS clone / split / prune) ------ */
+static uint64_t so_splitmix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+static float so_split_normal(uint64_t base, int child, int axis) {
+  uint32_t sum = 0;
+  for (int j = 0; j < 12; ++j) sum += (uint32_t)(so_splitmix64(base + (uint64_t)(child * 36 + axis * 12 + j + 1)) >> 40);
+  return (float)sum * 0x1p-24f - 6.0f;
+}
+
+/* action per point (0 prune, 1 keep, 2 clone, 3 split) and output count per
+ * group; stats float2 per point or NULL */
+void so_densify_mark(const float* params, int64_t S, const float* stats, const int32_t* group_begin, int32_t ng,
+                     float grad_threshold, float split_scale, float min_opacity, float max_scale, int32_t* action,
+                     int32_t* group_out) {
+  for (int32_t g = 0; g < ng; ++g) {
+    int32_t cnt = 0;
+    for (int32_t i = group_begin[g]; i < group_begin[g + 1]; ++i) {
+      const float* p0 = params + 4 * i;
+      const float* p1 = params + 4 * (S + i);
+      const float o = 1.f / (1.f + or_det_expf(-p0[3]));
+      const float smax = fmaxf(fmaxf(or_det_expf(p1[0]), or_det_expf(p1[1])), or_det_expf(p1[2]));
+      const float sx = stats ? stats[2 * i] : 0.f, sy = stats ? stats[2 * i + 1] : 0.f;
+      int a;
+      if (o < min_opacity || (max_scale > 0.f && smax > max_scale)) {
+        a = 0;
+      } else {
+        const float avg = sy > 0.f ? sx / sy : 0.f;
+        a = (sy > 0.f && avg >= grad_threshold) ? (smax > split_scale ? 3 : 2) : 1;
+      }
+      action[i] = a;
+      cnt += a == 0 ? 0 : (a == 1 ? 1 : 2);
+    }
+    group_out[g] = cnt;
+  }
+}
+
+/* new shard (plane layout [15][S_new][4]) from the actions; new_begin the
+ * exclusive scan of group_out; gid NULL = local index */
+void so_densify_apply(const float* params, const float* m, const float* v, int64_t S, const int32_t* action,
+                      const int32_t* group_begin, const int32_t* new_begin, int32_t ng, const int32_t* gid,
+                      uint32_t seed, float* params_new, float* m_new, float* v_new, int64_t S_new,
+                      int32_t* src_index) {
+  const float kLogSplit = 0x1.e148a2p-2f;
+  for (int32_t g = 0; g < ng; ++g) {
+    int64_t j = new_begin[g];
+    for (int32_t i = group_begin[g]; i < group_begin[g + 1]; ++i) {
+      const int a = action[i];
+      if (a == 0) continue;
+      if (a == 3) {
+        const float* p0 = params + 4 * i;
+        const float* p1 = params + 4 * (S + i);
+        const float* q = params + 4 * (2 * S + i);
+        float s[3], qn[4], R[9];
+        for (int k = 0; k < 3; ++k) s[k] = or_det_expf(p1[k]);
+        const float nn = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+        const float qnorm = sqrtf(nn);
+        for (int k = 0; k < 4; ++k) qn[k] = q[k] / qnorm;
+        quat_rot(qn, R);
+        const uint32_t id = gid ? (uint32_t)gid[i] : (uint32_t)i;
+        const uint64_t base = so_splitmix64(((uint64_t)seed << 32) | id);
+        for (int ch = 0; ch < 2; ++ch, ++j) {
+          float l[3];
+          for (int k = 0; k < 3; ++k) l[k] = s[k] * so_split_normal(base, ch, k);
+          float* o0 = params_new + 4 * j;
+          for (int r = 0; r < 3; ++r) o0[r] = p0[r] + ((R[3 * r] * l[0] + R[3 * r + 1] * l[1]) + R[3 * r + 2] * l[2]);
+          o0[3] = p0[3];
+          float* o1 = params_new + 4 * (S_new + j);
+          for (int k = 0; k < 3; ++k) o1[k] = p1[k] - kLogSplit;
+          o1[3] = p1[3];
+          for (int pl = 2; pl < 15; ++pl)
+            for (int e = 0; e < 4; ++e) params_new[4 * (pl * S_new + j) + e] = params[4 * (pl * S + i) + e];
+          for (int pl = 0; pl < 15; ++pl)
+            for (int e = 0; e < 4; ++e) m_new[4 * (pl * S_new + j) + e] = v_new[4 * (pl * S_new + j) + e] = 0.f;
+          src_index[j] = i;
+        }
+      } else {
+        for (int rep = 0; rep < (a == 2 ? 2 : 1); ++rep, ++j) {
+          for (int pl = 0; pl < 15; ++pl)
+            for (int e = 0; e < 4; ++e) {
+              params_new[4 * (pl * S_new + j) + e] = params[4 * (pl * S + i) + e];
+              m_new[4 * (pl * S_new + j) + e] = rep ? 0.f : m[4 * (pl * S + i) + e];
+              v_new[4 * (pl * S_new + j) + e] = rep ? 0.f : v[4 * (pl * S + i) + e];
+            }
+          src_index[j] = i;
+        }
+      }
+    }
+  }
+}
+
+/* min/max of the means of each group (empty group: zeros) */
+void so_group_aabb_ranges(const float* params, const int32_t* group_begin, int32_t ng, float* aabb) {
+  for (int32_t g = 0; g < ng; ++g) {
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int32_t i = group_begin[g]; i < group_begin[g + 1]; ++i)
+      for (int k = 0; k < 3; ++k) {
+        mn[k] = fminf(mn[k], params[4 * i + k]);
+        mx[k] = fmaxf(mx[k], params[4 * i + k]);
+      }
+    const int empty = group_begin[g + 1] <= group_begin[g];
+    for (int k = 0; k < 3; ++k) {
+      aabb[6 * g + k] = empty ? 0.f : mn[k];
+      aabb[6 * g + 3 + k] = empty ? 0.f : mx[k];
+    }
+  }
+}

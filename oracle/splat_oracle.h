@@ -103,4 +103,16 @@ double or_train_step_model(float* params, float* exp_avg, float* exp_avg_sq,
                            float beta2, float eps, int32_t step,
                            int32_t n_threads, int32_t model);
 
+/* densification (csrc/densify.cu semantics, include/splat_b200.h
+ * bs_densify_*): actions + per-group output counts, the new shard, and the
+ * AABBs of variable-size groups. */
+void so_densify_mark(const float* params, int64_t S, const float* stats, const int32_t* group_begin, int32_t ng,
+                     float grad_threshold, float split_scale, float min_opacity, float max_scale, int32_t* action,
+                     int32_t* group_out);
+void so_densify_apply(const float* params, const float* m, const float* v, int64_t S, const int32_t* action,
+                      const int32_t* group_begin, const int32_t* new_begin, int32_t ng, const int32_t* gid,
+                      uint32_t seed, float* params_new, float* m_new, float* v_new, int64_t S_new,
+                      int32_t* src_index);
+void so_group_aabb_ranges(const float* params, const int32_t* group_begin, int32_t ng, float* aabb);
+
 #endif

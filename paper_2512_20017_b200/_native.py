@@ -48,6 +48,7 @@ class CullDesc(C.Structure):
                 ("max_chunks", C.c_int32), ("chunk_prefix", C.c_void_p)]
 
 
+DENSIFY_PRUNE, DENSIFY_KEEP, DENSIFY_CLONE, DENSIFY_SPLIT = 0, 1, 2, 3
 MODEL_3DGS = 0
 MODEL_2DGS = 1
 SP2_FLOATS = 24
@@ -60,7 +61,13 @@ class ProjDesc(C.Structure):
                 ("max_group_points", C.c_int32), ("gsp_form", C.c_int32), ("chunk_prefix", C.c_void_p),
                 ("gsp_zero", C.c_void_p), ("point_gid", C.c_void_p), ("row_gid", C.c_void_p),
                 ("row_support", C.c_void_p), ("view_sp", C.c_void_p), ("view_gid", C.c_void_p),
-                ("bucket_counts", C.c_void_p), ("row_bin", C.c_void_p), ("tiles_per_slot", C.c_int32)]
+                ("bucket_counts", C.c_void_p), ("row_bin", C.c_void_p), ("tiles_per_slot", C.c_int32),
+                ("densify_stats", C.c_void_p)]
+
+
+class DensifyDesc(C.Structure):
+    _fields_ = [("model", C.c_int32), ("grad_threshold", C.c_float), ("split_scale", C.c_float),
+                ("min_opacity", C.c_float), ("max_scale", C.c_float), ("seed", C.c_uint32)]
 
 
 class RasterDesc(C.Structure):
@@ -136,6 +143,10 @@ _SIGS = {
     "bs_return_rows": (_I32, [_P, _I32, _I32, _P, _I64, _P, _P, _P, _I32, _P, _I32, _P]),
     "bs_canonical_order_workspace": (_SZ, [_I64]),
     "bs_canonical_order": (_I32, [_P, _I64, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
+    "bs_densify_mark": (_I32, [C.POINTER(DensifyDesc), _P, _I64, _P, _P, _I32, _P, _P, _P]),
+    "bs_densify_apply": (_I32, [C.POINTER(DensifyDesc), _P, _P, _P, _I64, _P, _P, _P, _I32, _P, _P, _P, _P,
+                                _I64, _P, _P]),
+    "bs_group_aabb_ranges": (_I32, [_P, _I64, _P, _I32, _P, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

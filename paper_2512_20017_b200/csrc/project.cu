@@ -105,6 +105,7 @@ struct ProjArgs {
   int32_t* bucket_counts;       // single-pass binning: (view, tile) counters, or NULL
   int4* row_bin;                // with bucket_counts: per-row (depth bits, x0|x1<<16, y0|y1<<16, 0)
   int tiles_per_slot;
+  float2* densify_stats;        // (bs_project_bwd_adam, 3DGS): per point (sum |dL/d mean2d| NDC, views), or NULL
 };
 
 // Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
@@ -266,7 +267,8 @@ __global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_ke
 template <class M, class SH, class ShAdd>
 __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camera* s_cam, const int64_t* s_row0,
                                                const RowRanker& rk, uint32_t mask, const PointIn& pt, const SH& sh,
-                                               const float* __restrict__ gsp, float* g, ShAdd& sh_add) {
+                                               const float* __restrict__ gsp, float* g, ShAdd& sh_add,
+                                               float2* dstat = nullptr) {
   typename M::Pre pre;
   M::pre(pt, pre);
   float acc[M::kAcc];
@@ -285,6 +287,14 @@ __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camer
     float wk[16];  // SH direction weights, computed with the colour (one pass over the coefficients)
     M::forward(pt, pre, sh, s_cam[v], a.n_sh, f, M::kFuseWk ? gs + M::kGcol : nullptr, M::kFuseWk ? wk : nullptr);
     if (!a.gsp_standard) M::from_moments(f, gs);
+    if constexpr (!M::k2D) {
+      // densification statistic: |dL/d mean2d| in NDC units (u = (x_ndc + 1) W / 2), views with a valid splat
+      if (dstat && f.valid) {
+        const float gx = gs[0] * (0.5f * (float)s_cam[v].width), gy = gs[1] * (0.5f * (float)s_cam[v].height);
+        dstat->x += sqrtf(gx * gx + gy * gy);
+        dstat->y += 1.f;
+      }
+    }
     M::backward(pt, pre, sh, s_cam[v], a.n_sh, f, gs, g, acc, sh_add, M::kFuseWk ? wk : nullptr);
   }
   M::finish(pt, acc, g);
@@ -479,7 +489,14 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
         asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own column
         const ShSmem sh{s_sh4 + threadIdx.x};
         ShAccSmem acc{my_sh};
-        point_backward<M>(a, s_cam, s_row0, rk, mask, pt, sh, gsp, g12, acc);
+        if (a.densify_stats != nullptr && !M::k2D) {
+          float2 ds = make_float2(0.f, 0.f);
+          point_backward<M>(a, s_cam, s_row0, rk, mask, pt, sh, gsp, g12, acc, &ds);
+          float2 t = a.densify_stats[i];
+          a.densify_stats[i] = make_float2(t.x + ds.x, t.y + ds.y);
+        } else {
+          point_backward<M>(a, s_cam, s_row0, rk, mask, pt, sh, gsp, g12, acc);
+        }
       }
       // Adam over the 15 planes, 3 planes per batch: all 15 loads of a batch
       // are issued before its first store (memory-level parallelism)
@@ -699,7 +716,8 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
   const int n_sh = (pd->sh_degree + 1) * (pd->sh_degree + 1);
   ProjArgs a{pd->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, pd->gsp_form, pd->max_group_points > 0 ? pd->chunk_prefix : nullptr, nullptr,
-             nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+             nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+             reinterpret_cast<float2*>(pd->densify_stats)};
   AdamConsts c = make_adam(ad);
   const size_t smem = sizeof(float4) * 24 * kProjThreads;
   auto launch = [&](auto kern) {

@@ -74,6 +74,23 @@ class AdamConfig:
     selective: bool = False
 
 
+@dataclass
+class DensifyConfig:
+    """Periodic densification (standard 3DGS clone / split /
+    prune, include/splat_b200.h bs_densify_*).  grad_threshold: on the mean
+    NDC-space |dL/d mean2d| since the last densification (3DGS: 2e-4);
+    split_scale: points whose largest world scale exceeds it are split in
+    two, the others cloned (3DGS: 0.01 x the scene extent); min_opacity:
+    prune below (3DGS: 0.005); max_scale: also prune points larger than this
+    (0: off); seed: the split samples (keyed by global point id)."""
+
+    grad_threshold: float = 2e-4
+    split_scale: float = 0.01
+    min_opacity: float = 0.005
+    max_scale: float = 0.0
+    seed: int = 0
+
+
 class _Grow:
     """Grow-only cache of device buffers keyed by name."""
 
@@ -193,6 +210,16 @@ class SplatTrainer:
         # raster work split: pixels per lane (1 -> 8x4 region per warp, 2 -> 8x8);
         # 1 measured faster on B200 (C2: bwd 3.30 vs 3.52 ms, fwd 1.22 vs 1.24 ms)
         self.pixels_per_lane = int(os.environ.get("BS_RASTER_PPL", "1"))
+        # densification statistic (track_densify_stats): float2 per point
+        self.densify_stats = None
+        # a stable global key per local group (first global id at construction):
+        # orders the groups of all ranks when densification renumbers the points
+        gb0 = np.asarray(group_begin, dtype=np.int64)[:-1]
+        if self.global_ids is not None and self.S:
+            keys = np.asarray(global_ids, dtype=np.int64)[np.minimum(gb0, self.S - 1)]
+        else:
+            keys = gb0.copy()
+        self.group_keys = keys
         # batch indices reach the GPU by asynchronous copies from a pinned ring
         self._ids_pin = [torch.empty(64, dtype=torch.int64, pin_memory=True) for _ in range(2)]
         self._ids_ev = [None, None]
@@ -310,6 +337,7 @@ class SplatTrainer:
         pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group, 0,
                              nat.ptr(chunk_prefix))
         pdesc.point_gid = nat.ptr(self.global_ids)
+        pdesc.densify_stats = nat.ptr(self.densify_stats)
         early = self.comm is None and S * B * self.sp_floats * 4 <= self.sp_capacity_bytes
         row_gid = None
         if self.comm is not None or self.record_row_gid:
@@ -470,6 +498,7 @@ class SplatTrainer:
         sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
         pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group, 0,
                              nat.ptr(chunk_prefix))
+        pdesc.densify_stats = nat.ptr(self.densify_stats)
         row_gid = self.buf.get("row_gid", max(n_rows, 1), torch.int32)
         pdesc.point_gid, pdesc.row_gid = nat.ptr(self.global_ids), nat.ptr(row_gid)
         with self._t("project"):
@@ -548,6 +577,96 @@ class SplatTrainer:
                      nat.ptr(self.exp_avg_sq), S, nat.ptr(mask), nat.ptr(self.group_begin), self.n_groups,
                      nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
         return losses
+
+    # ------------------------------------------------------------------ densification
+    def track_densify_stats(self, on: bool = True) -> None:
+        """Accumulate the densification statistic in every step's fused
+        projection backward (3DGS): per point, the NDC-space |dL/d mean2d| of
+        each batch view with a valid splat, and the number of such views."""
+        if on and self.model != "3dgs":
+            from .status import ParameterError
+
+            raise ParameterError("densification is implemented for the 3DGS model")
+        self.densify_stats = torch.zeros(max(self.S, 1), 2, dtype=torch.float32, device=self.dev) if on else None
+
+    def densify(self, cfg: DensifyConfig | None = None) -> dict:
+        """Clone / split / prune this rank's shard on the GPU (bs_densify_mark
+        -> scan -> bs_densify_apply -> bs_group_aabb_ranges) from the
+        statistic accumulated since the last call, then reset it.  Points stay
+        in their groups, so the partition and the culling structures keep
+        working; with several ranks (collective) the points are renumbered in
+        global group order so the global ids -- and the canonical per-tile
+        order -- are the single-rank ones.  Returns the action counts."""
+        from .status import ParameterError
+
+        if self.model != "3dgs":
+            raise ParameterError("densification is implemented for the 3DGS model")
+        cfg = cfg if cfg is not None else DensifyConfig()
+        st = nat.stream_handle()
+        S, ng, dev = self.S, self.n_groups, self.dev
+        desc = nat.DensifyDesc(nat.MODEL_3DGS, float(cfg.grad_threshold), float(cfg.split_scale),
+                               float(cfg.min_opacity), float(cfg.max_scale), int(cfg.seed) & 0xFFFFFFFF)
+        action = torch.empty(max(S, 1), dtype=torch.int32, device=dev)
+        gout = torch.zeros(max(ng, 1), dtype=torch.int32, device=dev)
+        stats = self.densify_stats if self.densify_stats is not None and self.densify_stats.shape[0] >= S else None
+        nat.call("bs_densify_mark", desc, nat.ptr(self.params), S, nat.ptr(stats), nat.ptr(self.group_begin), ng,
+                 nat.ptr(action), nat.ptr(gout), st)
+        new_begin = torch.zeros(ng + 1, dtype=torch.int32, device=dev)
+        new_begin[1:] = torch.cumsum(gout[:ng], 0, dtype=torch.int32)
+        S_new = int(new_begin[-1].item())
+        params = torch.empty(nat.PARAM_PLANES, max(S_new, 1), 4, dtype=torch.float32, device=dev)
+        m = torch.empty_like(params)
+        v = torch.empty_like(params)
+        src = torch.empty(max(S_new, 1), dtype=torch.int32, device=dev)
+        nat.call("bs_densify_apply", desc, nat.ptr(self.params), nat.ptr(self.exp_avg), nat.ptr(self.exp_avg_sq), S,
+                 nat.ptr(action), nat.ptr(self.group_begin), nat.ptr(new_begin), ng, nat.ptr(self.global_ids),
+                 nat.ptr(params), nat.ptr(m), nat.ptr(v), S_new, nat.ptr(src), st)
+        aabb = torch.empty(max(ng, 1), 6, dtype=torch.float32, device=dev)
+        nat.call("bs_group_aabb_ranges", nat.ptr(params), S_new, nat.ptr(new_begin), ng, nat.ptr(aabb), st)
+        counts = torch.bincount(action[:S].long(), minlength=4).cpu().numpy()
+        sizes = np.diff(new_begin.cpu().numpy().astype(np.int64))
+        # the new shard
+        self.params, self.exp_avg, self.exp_avg_sq = params[:, :S_new], m[:, :S_new], v[:, :S_new]
+        self.S = S_new
+        self.group_begin = new_begin
+        self.aabb = aabb[:ng]
+        self.max_group = int(sizes.max()) if len(sizes) else 0
+        self.max_chunks = max(1, -(-self.max_group // 256))
+        if self.presence is not None:
+            self.presence = self.presence.index_select(0, src[:S_new].long())
+        if self.comm is not None or self.global_ids is not None:
+            self.global_ids = torch.as_tensor(self._renumber(sizes), device=dev)
+        if self.densify_stats is not None:
+            self.densify_stats = torch.zeros(max(S_new, 1), 2, dtype=torch.float32, device=dev)
+        self.last = {}
+        return {"n_before": int(S), "n_after": int(S_new), "pruned": int(counts[nat.DENSIFY_PRUNE]),
+                "kept": int(counts[nat.DENSIFY_KEEP]), "cloned": int(counts[nat.DENSIFY_CLONE]),
+                "split": int(counts[nat.DENSIFY_SPLIT]), "src_index": src[:S_new]}
+
+    def _renumber(self, sizes: np.ndarray) -> np.ndarray:
+        """Global ids after densification: groups of all ranks in global key
+        order, points consecutively inside each group (the single-rank
+        numbering for any number of ranks)."""
+        keys, sizes = np.asarray(self.group_keys, dtype=np.int64), np.asarray(sizes, dtype=np.int64)
+        if self.comm is not None:
+            import torch.distributed as dist
+
+            grp = getattr(self.comm, "group", None)
+            parts = [None] * dist.get_world_size(grp)
+            dist.all_gather_object(parts, (keys.tolist(), sizes.tolist()), group=grp)
+            all_keys = np.concatenate([np.asarray(k, dtype=np.int64) for k, _ in parts])
+            all_sizes = np.concatenate([np.asarray(z, dtype=np.int64) for _, z in parts])
+        else:
+            all_keys, all_sizes = keys, sizes
+        order = np.argsort(all_keys, kind="stable")
+        start = np.zeros(len(all_keys), dtype=np.int64)
+        start[order] = np.concatenate([[0], np.cumsum(all_sizes[order])[:-1]]) if len(order) else []
+        lut = dict(zip(all_keys.tolist(), start.tolist()))
+        ids = np.concatenate([lut[int(k)] + np.arange(n, dtype=np.int64) for k, n in zip(keys, sizes)]) \
+            if len(keys) else np.zeros(0, dtype=np.int64)
+        if len(ids) and ids[-1] >= 2**31:
+            raise ValueError("global ids exceed int32 after densification")
+        return ids.astype(np.int32)
 
     # ------------------------------------------------------------------ checkpoint
     def state_dict(self) -> dict:
