@@ -671,19 +671,48 @@ class SplatTrainer:
     # ------------------------------------------------------------------ checkpoint
     def state_dict(self) -> dict:
         """The rank's training state (shard parameters, Adam moments, step
-        counter; SURVEY.md §5 checkpoint/resume): `torch.save` it per rank."""
-        return {"params": self.params.detach().clone(), "exp_avg": self.exp_avg.detach().clone(),
-                "exp_avg_sq": self.exp_avg_sq.detach().clone(), "step": int(self.step_count),
-                "model": self.model, "n_points": int(self.S)}
+        counter; SURVEY.md §5 checkpoint/resume): `torch.save` it per rank.
+        It carries the shard layout too (group table, AABBs, global ids,
+        densification statistic), which densification changes."""
+        sd = {"params": self.params.detach().clone(), "exp_avg": self.exp_avg.detach().clone(),
+              "exp_avg_sq": self.exp_avg_sq.detach().clone(), "step": int(self.step_count),
+              "model": self.model, "n_points": int(self.S),
+              "group_begin": self.group_begin.detach().clone(), "aabb": self.aabb.detach().clone(),
+              "group_keys": torch.as_tensor(np.asarray(self.group_keys, dtype=np.int64))}
+        for name in ("global_ids", "presence", "densify_stats"):
+            t = getattr(self, name)
+            sd[name] = None if t is None else t.detach().clone()
+        return sd
 
     def load_state_dict(self, sd: dict) -> None:
+        """Resume from state_dict(); a checkpoint taken after densification
+        (another point count, same groups) replaces the shard layout."""
         from .status import ConsistencyError
 
-        if sd.get("model") != self.model or int(sd.get("n_points", -1)) != self.S:
-            raise ConsistencyError("checkpoint is of a different model or shard")
-        for name in ("params", "exp_avg", "exp_avg_sq"):
-            getattr(self, name).copy_(sd[name].to(self.dev))
+        n = int(sd.get("n_points", -1))
+        if sd.get("model") != self.model:
+            raise ConsistencyError("checkpoint is of a different model")
+        if n != self.S and ("group_begin" not in sd or len(sd["group_begin"]) != self.n_groups + 1):
+            raise ConsistencyError("checkpoint is of a different shard")
+        if n != self.S:
+            for name in ("params", "exp_avg", "exp_avg_sq"):
+                setattr(self, name, sd[name].to(self.dev).clone())
+        else:
+            for name in ("params", "exp_avg", "exp_avg_sq"):
+                getattr(self, name).copy_(sd[name].to(self.dev))
+        if "group_begin" in sd:
+            self.S = n
+            self.group_begin = sd["group_begin"].to(self.dev).clone()
+            self.aabb = sd["aabb"].to(self.dev).clone()
+            self.group_keys = np.asarray(sd["group_keys"].cpu().numpy(), dtype=np.int64)
+            sizes = np.diff(self.group_begin.cpu().numpy().astype(np.int64))
+            self.max_group = int(sizes.max()) if len(sizes) else 0
+            self.max_chunks = max(1, -(-self.max_group // 256))
+            for name in ("global_ids", "presence", "densify_stats"):
+                t = sd.get(name)
+                setattr(self, name, None if t is None else t.to(self.dev).clone())
         self.step_count = int(sd["step"])
+        self.last = {}
 
     def _single_pass_bin(self, pdesc, B, n_rows):
         """Zeroed (view, tile) bucket counters and the per-row tile records the

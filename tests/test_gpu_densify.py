@@ -159,3 +159,29 @@ def test_densify_then_train_matches_oracle(c1_trainer):
     # and training goes on
     for batch in ([0, 3], [2, 5, 7]):
         assert np.isfinite(tr.step(batch).cpu().numpy()).all()
+
+
+def test_densified_checkpoint_resumes(c1_trainer, tmp_path):
+    """state_dict after densification carries the new shard layout; a trainer
+    built on the original shard resumes from it and steps exactly like the
+    densified one (same kernels, same inputs)."""
+    from _scene import c1_setup
+
+    tr = c1_trainer
+    tr.track_densify_stats(True)
+    tr.step([0, 2, 5, 7])
+    st = tr.densify_stats.cpu().numpy()
+    thr = float(np.quantile(st[:, 0] / np.maximum(st[:, 1], 1), 0.7))
+    tr.densify(DensifyConfig(grad_threshold=thr, split_scale=1.0, min_opacity=0.05, seed=2))
+    tr.step([1, 3])
+    torch.save(tr.state_dict(), tmp_path / "ckpt.pt")
+    ds, params, gb, aabb, gt = c1_setup()
+    b = SplatTrainer(params, gb, aabb, ds.views, gt=gt, sh_degree=3)
+    b.load_state_dict(torch.load(tmp_path / "ckpt.pt"))
+    assert b.S == tr.S != params.shape[1] and b.step_count == tr.step_count
+    assert b.densify_stats is not None and torch.equal(b.densify_stats, tr.densify_stats)
+    la = tr.step([4, 6]).cpu().numpy()
+    lb = b.step([4, 6]).cpu().numpy()
+    assert np.array_equal(la, lb)
+    n = tr.last["n_rows"]
+    assert torch.equal(tr.last["sp"][: n * 12], b.last["sp"][: n * 12])
