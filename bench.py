@@ -241,7 +241,7 @@ def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps, row_byt
                     "matrix (account_iteration, topology (N, 1)); forward bytes per row = splat state + 4-byte id"}
 
 
-_STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_kernel",
+_STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_kernel", "raster": "raster_fused_kernel",
                  "raster2d_bwd": "raster2d_bwd_kernel", "raster2d_fwd": "raster2d_fwd_kernel",
                  "project_bwd_adam": "project_bwd_adam_kernel", "project": "project_fwd_kernel", "cull": "cull_kernel"}
 
@@ -491,7 +491,7 @@ def run_ours(args, cfg):
         h = rl.hbm(nbytes, stage_ms[dom], peak)
         prof = kernel_profile(dom, model, args.config)
         iss = rl.issue(prof.get("warp_instructions"), stage_ms[dom], clk_summary.get("sm_mhz"))
-        sb = rl.step_bytes(counts, model)
+        sb = rl.step_bytes(counts, model, stages=tuple(stage_ms))
         roof = {"kernel": dom, "bound": "hbm", "achieved": h["achieved"], "peak": peak, "unit": "GB/s",
                 "frac": h["frac"], "traffic": prof.get("dram_traffic_bytes"), "peak_kind": peak_kind,
                 "bytes_per_launch": nbytes, "ms_per_launch": stage_ms[dom],

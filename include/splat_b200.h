@@ -374,6 +374,17 @@ int32_t bs_raster_bwd(const bs_raster_desc* desc_host, const float* sp_rows,
                       const uint8_t* gt, const int32_t* gt_slot_view,
                       float* g_sp, void* stream);
 
+/* K3 + L + K4 of the mean-L1 training step in one launch (1 pixel per lane):
+ * the forward's outputs and loss partials of bs_raster_fwd (loss fused, gt
+ * required) and the G_SP of bs_raster_bwd with grad_image == NULL, without
+ * re-walking the tile lists from global memory (each warp keeps its
+ * forward's filtered splat list in shared memory; see csrc/raster.cu). */
+int32_t bs_raster_fwd_bwd(const bs_raster_desc* desc_host, const float* sp_rows,
+                          const uint32_t* inst_rows, const int32_t* ranges,
+                          float* image, float* final_T, int32_t* n_contrib,
+                          const uint8_t* gt, const int32_t* gt_slot_view,
+                          float* loss_tiles, float* g_sp, void* stream);
+
 /* 2DGS (surfel) variants: same arguments, BS_SP2_FLOATS rows in, BS_GSP2_FLOATS
  * gradient rows out (config 3; reference: the 2DGS state of PAPER.md:1217-1226,
  * the paper's 2DGS renderer is gsplat's and absent from /root/reference).  Pixel weight exp(-0.5 min(u^2+v^2,

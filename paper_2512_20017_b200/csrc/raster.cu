@@ -658,6 +658,201 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
 #endif
 }
 
+// ---- K3 + L + K4 in one kernel (the mean-L1 training step) ----------------
+//
+// raster_fwd_kernel and raster_bwd_kernel walk the same depth-sorted tile
+// list with the same per-warp support filter; the backward repeats the
+// forward's chunk work (row gathers, support test, ballot, staging) and
+// re-reads every pixel's T, n_contrib, colour and ground truth.  Fused, each
+// warp appends the forward's kept splats (48-byte records with their
+// range-relative index) to a warp-private shared-memory list, turns its
+// pixels' final colours straight into dL/dC (L1 sign), and walks the list
+// back to front: no gathers, no support tests, no per-pixel reloads.  A warp
+// that keeps more than kKeep splats (the list wraps) falls back to the
+// backward's own chunked walk over global memory.  Per pair the arithmetic
+// is raster_fwd_kernel's / raster_bwd_kernel's, so the image is identical
+// and the gradients differ only by atomic order.
+#ifndef BS_FUSED_KEEP
+#define BS_FUSED_KEEP 128
+#endif
+#ifndef BS_FUSED_CTAS
+#define BS_FUSED_CTAS 4
+#endif
+#ifndef BS_FUSED_NOBAR
+#define BS_FUSED_NOBAR 1
+#endif
+constexpr int kKeep = BS_FUSED_KEEP;  // kept-splat records per warp (48 B each; a power of two)
+
+struct KeptRec {
+  float4 a, b, c;  // as Staged; c.w = range-relative index (int bits)
+};
+
+// one splat of the backward for one warp: pixel gradient + warp reduction + REDs
+template <bool kBg>
+__device__ __forceinline__ void bwd_splat(PixelBwd& p, const float4& sa, const float4& sb, const float4& sc, int rel,
+                                          F2 npx, float* __restrict__ g_sp) {
+  float g[9];
+  const bool any = pixel_grad_sel<kBg>(p, sa, sb, sc.x, sc.y, npx, rel < p.n, g);
+  const uint32_t who = __ballot_sync(0xffffffffu, any);
+  if (who == 0u) return;
+  float* dst = g_sp + (int64_t)__float_as_uint(sc.z) * BS_GSP_FLOATS;
+  if (__popc(who) <= kSparseLanes) {
+    if (any) {
+      atomicAdd(reinterpret_cast<float4*>(dst), make_float4(g[0], g[1], g[2], g[3]));
+      atomicAdd(reinterpret_cast<float4*>(dst + 4), make_float4(g[4], g[5], g[6], g[7]));
+      atomicAdd(dst + 8, g[8]);
+    }
+  } else {
+    int idx;
+    const float r = warp_reduce9(g, idx);
+    if (idx >= 0) atomicAdd(dst + idx, r);
+  }
+}
+
+template <bool kBg, bool kSup>
+__global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
+    RastArgs a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
+    float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
+    const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view, float* __restrict__ loss_tiles,
+    float* __restrict__ g_sp) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  __shared__ float s_red[8];
+  const int slot = blockIdx.z;
+  const int tile = blockIdx.y * a.tiles_x + blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  KeptRec* kept = reinterpret_cast<KeptRec*>(s_dyn) + w * kKeep;
+#if BS_FUSED_NOBAR
+  __shared__ int s_arrived;
+  if (threadIdx.x == 0) s_arrived = 0;
+  __syncthreads();
+#endif
+  const Region<1> q(blockIdx.x, blockIdx.y);
+  const float pxf = (float)q.px + 0.5f;
+  const F2 npx = f2(-pxf, -((float)q.py0 + 0.5f));
+  const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
+  const bool inside = slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, q.px, q.py0);
+  // ---------------- forward: blend front to back, appending the kept splats
+  PixelFwd pf{f2(0.f, 0.f), 1.f, 0.f, 0, !inside};
+  Splat f;
+  const float* sup = kSup ? a.support : nullptr;
+  fetch_splat(f, sp, sup, inst_rows, rg.x + lane, rg.x + lane < rg.y);
+  uint32_t row_next = fetch_row(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
+  int nk = 0;  // kept records appended (warp-uniform)
+  for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
+    if (__all_sync(0xffffffffu, pf.done)) break;
+    const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
+    const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      KeptRec& r = kept[(nk + __popc(bits & ((1u << lane) - 1u))) & (kKeep - 1)];
+      r.a = make_float4(f.p0.x, f.p0.y, __fmul_rn(f.p0.w, kHalfLog2e), __fmul_rn(f.p1.y, kHalfLog2e));
+      r.b = make_float4(__fmul_rn(f.p1.x, -kLog2e), f.p0.z, f.p1.z, f.p1.w);
+      r.c = make_float4(f.b, kSup ? f.th2 : support_p2(f.p0.z), __uint_as_float(f.row),
+                        __int_as_float(b0 + lane - rg.x));
+    }
+    fetch_row_data(f, sp, sup, row_next, b0 + 32 + lane < rg.y);
+    row_next = fetch_row(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
+    __syncwarp();
+    const int nb = __popc(bits);
+    for (int k = 0; k < nb; ++k) {
+      const KeptRec& r = kept[(nk + k) & (kKeep - 1)];
+      const float4 sa = r.a, sb = r.b;
+      const float2 sc = make_float2(r.c.x, r.c.y);
+      if (!pf.done) blend_sel(pf, sa, sb, sc.x, sc.y, npx, __float_as_int(r.c.w));
+    }
+    nk += nb;
+    __syncwarp();
+  }
+  // outputs + loss partial + this pixel's L1 gradient
+  float l = 0.f;
+  PixelBwd p;
+  p.T = 1.f;
+  p.n = 0;
+  float dC0 = 0.f, dC1 = 0.f;
+  p.dC2 = 0.f;
+  if (inside) {
+    const int64_t pix = ((int64_t)slot * a.H + q.py0) * a.W + q.px;
+    const float2 c01 = unf2(pf.c01);
+    const float o0 = c01.x + pf.T * a.bg[0], o1 = c01.y + pf.T * a.bg[1], o2 = pf.c2 + pf.T * a.bg[2];
+    image[3 * pix] = o0;
+    image[3 * pix + 1] = o1;
+    image[3 * pix + 2] = o2;
+    final_T[pix] = pf.T;
+    n_contrib[pix] = pf.contrib;
+    const int gv = gt_view ? gt_view[slot] : slot;
+    const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + q.py0) * a.W + q.px);
+    const float d0 = o0 - gp[0] * (1.f / 255.f), d1 = o1 - gp[1] * (1.f / 255.f), d2 = o2 - gp[2] * (1.f / 255.f);
+    l = fabsf(d0) + fabsf(d1) + fabsf(d2);
+    dC0 = (d0 > 0.f ? 1.f : (d0 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+    dC1 = (d1 > 0.f ? 1.f : (d1 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+    p.dC2 = (d2 > 0.f ? 1.f : (d2 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+    p.T = pf.T;
+    p.n = pf.contrib;
+  }
+  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+#if BS_FUSED_NOBAR
+  // the tile's loss partial without a CTA barrier (warps go on to their
+  // backward): the last warp to arrive sums the 8 warp partials in warp order
+  if (lane == 0) {
+    reinterpret_cast<volatile float*>(s_red)[w] = l;
+    // release the partial / acquire the others' (CTA scope; __threadfence_block
+    // is a fence.sc, which stalls the warp far longer)
+    int prev;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.s32 %0, [%1], 1;" : "=r"(prev)
+                 : "r"((uint32_t)__cvta_generic_to_shared(&s_arrived)) : "memory");
+    if (prev == 7) {
+      float t = 0.f;
+      for (int k = 0; k < 8; ++k) t += reinterpret_cast<volatile float*>(s_red)[k];
+      loss_tiles[(int64_t)slot * a.tiles_per_slot + tile] = t;
+    }
+  }
+#else
+  if (lane == 0) s_red[w] = l;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += s_red[k];
+    loss_tiles[(int64_t)slot * a.tiles_per_slot + tile] = t;
+  }
+#endif
+  p.T_final = p.T;
+  p.dC01 = f2(dC0, dC1);
+  p.bgdot = a.bg[0] * dC0 + a.bg[1] * dC1 + a.bg[2] * p.dC2;
+  p.acc01 = make_float2(0.f, 0.f);
+  p.acc2 = 0.f;
+  int warp_n = p.n;
+  for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
+  // ---------------- backward: back to front from the deepest contributor
+  if (nk <= kKeep) {
+    for (int k = nk - 1; k >= 0; --k) {
+      const KeptRec& r = kept[k];
+      const int rel = __float_as_int(r.c.w);
+      if (rel >= warp_n) continue;  // past every pixel's last contributor (warp-uniform)
+      bwd_splat<kBg>(p, r.a, r.b, r.c, rel, npx, g_sp);
+    }
+    return;
+  }
+  // the list wrapped: the backward's own chunked walk over global memory
+  WarpSmem& s = *reinterpret_cast<WarpSmem*>(kept);
+  __syncwarp();
+  const int end = rg.x + warp_n;
+  fetch_splat(f, sp, sup, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
+  row_next = fetch_row(inst_rows, end - 33 - lane, end - 33 - lane >= rg.x);
+  for (int cend = end; cend > rg.x; cend -= 32) {
+    const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
+    uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if (keep) stage(s, lane, f, kSup);
+    fetch_row_data(f, sp, sup, row_next, cend - 33 - lane >= rg.x);
+    row_next = fetch_row(inst_rows, cend - 65 - lane, cend - 65 - lane >= rg.x);
+    __syncwarp();
+    while (bits) {
+      const int j = __ffs(bits) - 1;
+      bits &= bits - 1;
+      bwd_splat<kBg>(p, s.s[j].a, s.s[j].b, s.s[j].c, cend - 1 - j - rg.x, npx, g_sp);
+    }
+    __syncwarp();
+  }
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -802,6 +997,32 @@ extern "C" int32_t bs_debug_raster_stats(unsigned long long* out, int32_t reset)
   return 0;
 }
 #endif
+
+extern "C" int32_t bs_raster_fwd_bwd(const bs_raster_desc* d, const float* sp_rows, const uint32_t* inst_rows,
+                                     const int32_t* ranges, float* image, float* final_T, int32_t* n_contrib,
+                                     const uint8_t* gt, const int32_t* gt_slot_view, float* loss_tiles, float* g_sp,
+                                     void* stream) {
+  RastArgs a;
+  int32_t st = make_args(d, a);
+  if (st) return st;
+  BS_REQUIRE(gt && loss_tiles && g_sp, BS_ERR_PARAMETER, "raster_fwd_bwd needs gt, loss_tiles and g_sp");
+  BS_REQUIRE(d->pixels_per_lane == 1, BS_ERR_PARAMETER, "raster_fwd_bwd: 1 pixel per lane");
+  const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
+  const bool bg = a.bg[0] != 0.f || a.bg[1] != 0.f || a.bg[2] != 0.f;
+  const size_t smem = sizeof(KeptRec) * kKeep * 8;
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 256, smem, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image,
+                                                 final_T, n_contrib, gt, gt_slot_view, loss_tiles, g_sp);
+  };
+  const bool sup = a.support != nullptr;
+  if (sup)
+    bg ? launch(raster_fused_kernel<true, true>) : launch(raster_fused_kernel<false, true>);
+  else
+    bg ? launch(raster_fused_kernel<true, false>) : launch(raster_fused_kernel<false, false>);
+  BS_LAUNCH_CHECK("raster_fused_kernel");
+  return BS_OK;
+}
 
 extern "C" size_t bs_l1_loss_workspace(int32_t n_slots) { return sizeof(float) * 64 * (size_t)n_slots; }
 

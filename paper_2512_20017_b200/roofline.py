@@ -21,6 +21,9 @@ blend reads) + 4 B list entry.
 |                  | read) + 4 I (list write) + 8 nb (ranges)                     |
 | raster_fwd       | (4 + gather) I + 23 Np (rgb 12, T 4, n 4 written, gt 3 read) |
 | raster_bwd       | (4 + gather) I + 23 Np (image, T, n, gt read) + G_SP V       |
+| raster (fused)   | (4 + gather) I + 23 Np (rgb, T, n written, gt read) + G_SP V |
+|                  | (K3 + L + K4 in one kernel: the list and the pixel state are |
+|                  | read once)                                                   |
 | project_bwd_adam | 6 x 240 S (p, m, v read + write) + 4 S + G_SP V              |
 |                  | (selective Adam: 6 x 240 Vp + 4 S + G_SP V)                  |
 
@@ -62,6 +65,8 @@ def stage_bytes(stage: str, c: dict, model: str = "3dgs") -> int | None:
     if stage == "raster_fwd":
         return (4 + m["gather"]) * I + 23 * Np
     if stage == "raster_bwd":
+        return (4 + m["gather"]) * I + 23 * Np + m["gsp"] * V
+    if stage == "raster":  # fused forward + loss + backward (bs_raster_fwd_bwd)
         return (4 + m["gather"]) * I + 23 * Np + m["gsp"] * V
     if stage == "project_bwd_adam":  # selective Adam: only the visible points' rows move
         n_upd = c.get("Vp", S) if c.get("selective") else S

@@ -15,6 +15,8 @@ of views runs, all on the GPU through the C ABI:
   K2  depth keys + radix sort + tile count/emit + radix sort + ranges
   K3  bs_raster_fwd (+ fused mean-L1 loss partials)     (lines 11-15)
   K4  bs_raster_bwd (L1 gradient recomputed in-kernel)  (lines 17-19)
+      3DGS: K3 + L + K4 as one kernel, bs_raster_fwd_bwd (each warp keeps
+      its forward's splat list in shared memory for the backward)
   [N>1] reverse all_to_all_single G_SP                  (line 21)
   K1b+K5 bs_project_bwd_adam      (lines 22-27), fused per point
 
@@ -210,6 +212,8 @@ class SplatTrainer:
         # raster work split: pixels per lane (1 -> 8x4 region per warp, 2 -> 8x8);
         # 1 measured faster on B200 (C2: bwd 3.30 vs 3.52 ms, fwd 1.22 vs 1.24 ms)
         self.pixels_per_lane = int(os.environ.get("BS_RASTER_PPL", "1"))
+        # 3DGS mean-L1 step: forward + loss + backward in one kernel (bs_raster_fwd_bwd)
+        self.raster_fused = os.environ.get("BS_RASTER_FUSED", "1") == "1"
         # densification statistic (track_densify_stats): float2 per point
         self.densify_stats = None
         # a stable global key per local group (first global id at construction):
@@ -837,15 +841,25 @@ class SplatTrainer:
         else:
             gt = self.gt
             gt_map = gt_views.to(torch.int32) if self.gt_lut is None else self.gt_lut.index_select(0, gt_views)
-        with self._t("raster_fwd"):
-            nat.call(self._raster[0], rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
-                     nat.ptr(final_T), nat.ptr(n_contrib), nat.ptr(gt), nat.ptr(gt_map), nat.ptr(loss_tiles), st)
         losses = self.buf.get("losses", n_slots, torch.float32)
-        nat.call("bs_reduce_loss_tiles", nat.ptr(loss_tiles), n_slots, self.tiles, self.H, self.W, nat.ptr(losses), st)
-        # ---- K4: backward
-        with self._t("raster_bwd"):
-            nat.call(self._raster[1], rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
-                     nat.ptr(final_T), nat.ptr(n_contrib), None, nat.ptr(gt), nat.ptr(gt_map), nat.ptr(gsp), st)
+        if self.raster_fused and self.model == "3dgs" and self.pixels_per_lane == 1:
+            # K3 + L + K4 in one launch: each warp keeps its forward's splat list in shared memory
+            with self._t("raster"):
+                nat.call("bs_raster_fwd_bwd", rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
+                         nat.ptr(final_T), nat.ptr(n_contrib), nat.ptr(gt), nat.ptr(gt_map), nat.ptr(loss_tiles),
+                         nat.ptr(gsp), st)
+            nat.call("bs_reduce_loss_tiles", nat.ptr(loss_tiles), n_slots, self.tiles, self.H, self.W,
+                     nat.ptr(losses), st)
+        else:
+            with self._t("raster_fwd"):
+                nat.call(self._raster[0], rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
+                         nat.ptr(final_T), nat.ptr(n_contrib), nat.ptr(gt), nat.ptr(gt_map), nat.ptr(loss_tiles), st)
+            nat.call("bs_reduce_loss_tiles", nat.ptr(loss_tiles), n_slots, self.tiles, self.H, self.W,
+                     nat.ptr(losses), st)
+            # ---- K4: backward
+            with self._t("raster_bwd"):
+                nat.call(self._raster[1], rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
+                         nat.ptr(final_T), nat.ptr(n_contrib), None, nat.ptr(gt), nat.ptr(gt_map), nat.ptr(gsp), st)
         self.last.update(image=image, final_T=final_T, n_contrib=n_contrib, ranges=ranges, irows=irows,
                          sp=sp, gsp=gsp)
         return losses, gsp

@@ -2,7 +2,9 @@
 (racecheck / memcheck / synccheck): 3DGS and 2DGS training
 steps with multi-chunk groups (cp.async SH staging, G_SP clearing in the
 projection), the radix binning pipeline, the tile-bucket sorts of every size
-class, the standalone projection backward and Adam, selective Adam."""
+class, the standalone projection backward and Adam, selective Adam, the
+fused raster kernel (kept lists in shared memory and their wrap-around
+fallback) beside the separate forward / backward kernels, densification."""
 import os
 import sys
 
@@ -29,6 +31,26 @@ for model in ("3dgs", "2dgs"):
             tr.step(b)
         torch.cuda.synchronize()
         print(model, "selective" if selective else "dense", "ok", tr.last["n_rows"], tr.last["n_inst"], flush=True)
+# separate raster kernels (the default 3DGS step runs the fused one), and the
+# fused kernel's wrap-around fallback (large splats: > 128 kept per warp)
+tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt, adam=AdamConfig(lr))
+tr.raster_fused = False
+tr.step([0, 3, 5])
+big = params.copy()
+big[1, :, :3] += np.float32(1.5)
+tr = SplatTrainer(big, gb, aabb, ds.views, gt=gt, adam=AdamConfig(lr), bg=(0.1, 0.2, 0.3))
+tr.step([2, 6])
+# densification (statistic in the fused backward, mark / apply / AABBs)
+tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt, adam=AdamConfig(lr))
+tr.track_densify_stats(True)
+tr.step([0, 3, 5])
+from paper_2512_20017_b200.trainer import DensifyConfig
+st = tr.densify_stats.cpu().numpy()
+rep = tr.densify(DensifyConfig(grad_threshold=float(np.median(st[:, 0] / np.maximum(st[:, 1], 1))), split_scale=1.0,
+                               min_opacity=0.05))
+tr.step([1, 4])
+torch.cuda.synchronize()
+print("separate raster, fused fallback, densify ok", rep["n_before"], rep["n_after"], flush=True)
 tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt, adam=AdamConfig(lr))
 tr.binning = "radix"
 tr.step([0, 4])
