@@ -241,7 +241,7 @@ def comm_bytes_report(comm, step_AW, batches, ds, g, world, rank, steps, row_byt
                     "matrix (account_iteration, topology (N, 1)); forward bytes per row = splat state + 4-byte id"}
 
 
-_STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_kernel", "raster": "raster_fused_kernel",
+_STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_kernel", "raster": "raster_fused_kernel", "raster2d": "raster2d_fused_kernel",
                  "raster2d_bwd": "raster2d_bwd_kernel", "raster2d_fwd": "raster2d_fwd_kernel",
                  "project_bwd_adam": "project_bwd_adam_kernel", "project": "project_fwd_kernel", "cull": "cull_kernel"}
 
@@ -263,6 +263,8 @@ def kernel_profile(stage, model="3dgs", config=None):
         except Exception:
             continue
         key = stage.replace("raster_", "raster2d_") if model == "2dgs" and stage.startswith("raster_") else stage
+        if model == "2dgs" and stage == "raster":
+            key = "raster2d"
         prefix = _STAGE_KERNEL.get(key, key)
         model_tag = "Model2" if model == "2dgs" else "Model3"
         hits = [v for k, v in table.items() if k.startswith(prefix)]

@@ -400,6 +400,12 @@ int32_t bs_raster2d_bwd(const bs_raster_desc* desc_host, const float* sp_rows,
                         const int32_t* n_contrib, const float* grad_image,
                         const uint8_t* gt, const int32_t* gt_slot_view,
                         float* g_sp, void* stream);
+/* 2DGS K3 + L + K4 in one launch (bs_raster_fwd_bwd semantics). */
+int32_t bs_raster2d_fwd_bwd(const bs_raster_desc* desc_host, const float* sp_rows,
+                            const uint32_t* inst_rows, const int32_t* ranges,
+                            float* image, float* final_T, int32_t* n_contrib,
+                            const uint8_t* gt, const int32_t* gt_slot_view,
+                            float* loss_tiles, float* g_sp, void* stream);
 
 /* ---- densification ("periodic densification"; standard 3DGS
  * clone / split / prune) ------------------------------- */

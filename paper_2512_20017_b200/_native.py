@@ -121,6 +121,7 @@ _SIGS = {
     "bs_reduce_loss_tiles": (_I32, [_P, _I32, _I32, _I32, _I32, _P, _P]),
     "bs_raster_bwd": (_I32, [C.POINTER(RasterDesc), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bs_raster_fwd_bwd": (_I32, [C.POINTER(RasterDesc), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "bs_raster2d_fwd_bwd": (_I32, [C.POINTER(RasterDesc), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bs_raster2d_fwd": (_I32, [C.POINTER(RasterDesc), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bs_raster2d_bwd": (_I32, [C.POINTER(RasterDesc), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bs_project_bwd": (_I32, [C.POINTER(ProjDesc), _P, _I64, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),

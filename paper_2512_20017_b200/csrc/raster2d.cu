@@ -146,6 +146,25 @@ __device__ __forceinline__ void cross3(const float a[3], const float b[3], float
   o[2] = __fsub_rn(__fmul_rn(a[0], b[1]), __fmul_rn(a[1], b[0]));
 }
 
+// stage2's record as four float4 (the fused kernel's kept list)
+__device__ __forceinline__ void stage2_rec(const Splat2& f, float X, float Y, bool have_support, float4 (&r)[4]) {
+  float r0[3], r1[3], r2[3];
+  m_rows(f.p[0], f.p[1], f.p[2], r0, r1, r2);
+  float hx[3], hy[3], z0[3], zb[3], zc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    hx[k] = __fsub_rn(r0[k], __fmul_rn(X, r2[k]));
+    hy[k] = __fsub_rn(r1[k], __fmul_rn(Y, r2[k]));
+  }
+  cross3(hx, hy, z0);
+  cross3(hy, r2, zb);
+  cross3(r2, hx, zc);
+  r[0] = make_float4(f.p[0].x, f.p[0].y, f.p[0].z, z0[2]);
+  r[1] = make_float4(z0[0], z0[1], zb[0], zb[1]);
+  r[2] = make_float4(zc[0], zc[1], zb[2], zc[2]);
+  r[3] = make_float4(f.p[3].x, f.p[3].y, f.p[3].z, have_support ? f.k : support_k(f.p[0].z));
+}
+
 __device__ __forceinline__ void stage2(Warp2& s, int lane, const Splat2& f, float X, float Y, bool have_support) {
   float r0[3], r1[3], r2[3];
   m_rows(f.p[0], f.p[1], f.p[2], r0, r1, r2);
@@ -327,6 +346,85 @@ struct PxB2 {
   int n;
 };
 
+// One splat of the 2DGS backward for one warp: the pixel's gradient terms
+// (selects instead of branches), then the per-splat reduction and REDs.
+template <bool kBg>
+__device__ __forceinline__ void bwd2_splat(PxB2& q, const float4& sa, const float4& sb, const float4& sc,
+                                           const float4& col, uint32_t row, int rel, float pxf, float pyf, float oxf,
+                                           float oyf, float* __restrict__ g_sp) {
+  const int lane = threadIdx.x & 31;
+  // every lane runs the whole sequence; pixels without a contribution
+  // keep their state through selects and produce zero terms (same
+  // arithmetic as a branchy version for the contributing ones)
+  float g[16];
+  Eval2 e;
+  eval2(sa, sb, sc, col.w, pxf, pyf, oxf, oyf, e);
+  const float ex = ex2a(fminf(e.pw2, 0.f));
+  const float raw = __fmul_rn(sa.z, ex);
+  const float alpha = fminf(kAMax, raw);
+  const bool any = rel < q.n && e.in;
+  {
+    const float ra = rcpa(1.f - alpha);  // alpha <= 0.99
+    const float T = q.T * ra;
+    const float fac = any ? alpha * T : 0.f;
+    g[12] = fac * q.dC0;
+    g[13] = fac * q.dC1;
+    g[14] = fac * q.dC2;
+    g[15] = 0.f;
+    // acc = colour behind this splat (normalised); acc' = acc + alpha (c - acc)
+    const float e0 = col.x - q.acc0, e1 = col.y - q.acc1, e2 = col.z - q.acc2;
+    float dLda = T * (e0 * q.dC0 + e1 * q.dC1 + e2 * q.dC2);
+    if (kBg) dLda -= q.T_final * ra * q.bgdot;
+    q.acc0 = any ? fmaf(alpha, e0, q.acc0) : q.acc0;
+    q.acc1 = any ? fmaf(alpha, e1, q.acc1) : q.acc1;
+    q.acc2 = any ? fmaf(alpha, e2, q.acc2) : q.acc2;
+    q.T = any ? T : q.T;
+    const bool grad = any && raw <= kAMax;
+    const float dpow = dLda * alpha;
+    g[11] = grad ? dLda * ex : 0.f;
+    // disk term: power = -0.5 (u^2 + v^2), (u, v) = zeta.xy / zeta.z; G_SP2
+    // carries the moments sum gz, sum gz px, sum gz py of dL/dzeta (the
+    // projection backward applies the M rows)
+    const bool disk = grad && e.disk;
+    const F2 guv = mul2(f2(e.u, e.v), bcast(-dpow));  // dL/d(u, v)
+    const float2 g_uv = unf2(guv);
+    const float iz = e.iz;
+    const F2 gz01 = mul2(guv, bcast(iz));
+    const float gz2 = -(g_uv.x * e.u + g_uv.y * e.v) * iz;
+    const float2 z01 = unf2(gz01);
+    const float2 zx = unf2(mul2(gz01, bcast(pxf)));
+    const float2 zy = unf2(mul2(gz01, bcast(pyf)));
+    g[2] = disk ? z01.x : 0.f;
+    g[3] = disk ? z01.y : 0.f;
+    g[4] = disk ? gz2 : 0.f;
+    g[5] = disk ? zx.x : 0.f;
+    g[6] = disk ? zx.y : 0.f;
+    g[7] = disk ? gz2 * pxf : 0.f;
+    g[8] = disk ? zy.x : 0.f;
+    g[9] = disk ? zy.y : 0.f;
+    g[10] = disk ? gz2 * pyf : 0.f;
+    // low-pass term: power = -(dx^2 + dy^2), dx = u - px
+    const bool lp = grad && !disk;
+    g[0] = lp ? -2.f * e.dx * dpow : 0.f;
+    g[1] = lp ? -2.f * e.dy * dpow : 0.f;
+  }
+  const uint32_t who = __ballot_sync(0xffffffffu, any);
+  if (who == 0u) return;
+  float* dst = g_sp + (int64_t)row * kGSP2;
+  if (__popc(who) <= kSparse2) {
+    if (any) {
+      // 64-byte aligned rows: four 128-bit REDs (the 16th float is padding, g[15] = 0)
+#pragma unroll
+      for (int k = 0; k < 16; k += 4)
+        atomicAdd(reinterpret_cast<float4*>(dst + k), make_float4(g[k], g[k + 1], g[k + 2], g[k + 3]));
+    }
+  } else {
+    const float r = warp_reduce16(g);
+    const int idx = lane >> 1;
+    if ((lane & 1) == 0 && idx < kGSP2Used) atomicAdd(dst + idx, r);
+  }
+}
+
 template <bool kBg>
 __global__ void __launch_bounds__(kT2, BS_R2_BWD_CTAS) raster2d_bwd_kernel(
     R2Args a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
@@ -387,78 +485,157 @@ __global__ void __launch_bounds__(kT2, BS_R2_BWD_CTAS) raster2d_bwd_kernel(
       const int j = __ffs(bits) - 1;
       bits &= bits - 1;
       const int rel = cend - 1 - j - rg.x;
-      // every lane runs the whole sequence; pixels without a contribution
-      // keep their state through selects and produce zero terms (same
-      // arithmetic as a branchy version for the contributing ones)
-      float g[16];
-      const float4 sa = s.a[j];
-      const float4 col = s.d[j];
+      bwd2_splat<kBg>(q, s.a[j], s.b[j], s.c[j], s.d[j], s.row[j], rel, pxf, pyf, oxf, oyf, g_sp);
+    }
+    __syncwarp();
+  }
+}
+
+// ---- K3 + L + K4 in one kernel (2DGS; see raster_fused_kernel in raster.cu)
+#ifndef BS_FUSED2_KEEP
+#define BS_FUSED2_KEEP 128  // swept on B200 (C3 raster ms): 32 (4 CTAs) 7.80, 64 7.29, 128 7.16; separate kernels 7.32
+#endif
+#ifndef BS_FUSED2_CTAS
+#define BS_FUSED2_CTAS 3
+#endif
+constexpr int kKeep2 = BS_FUSED2_KEEP;  // kept-splat records per warp (a power of two)
+
+struct Kept2 {
+  float4 rec[kKeep2][4];  // staged a, b, c, d (stage2 layout)
+  int2 idx[kKeep2];       // (G_SP row, range-relative index)
+};
+
+template <bool kBg>
+__global__ void __launch_bounds__(kT2, BS_FUSED2_CTAS) raster2d_fused_kernel(
+    R2Args a, const float* __restrict__ sp, const uint32_t* __restrict__ inst_rows, const int2* __restrict__ ranges,
+    float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
+    const uint8_t* __restrict__ gt, const int32_t* __restrict__ gt_view, float* __restrict__ loss_tiles,
+    float* __restrict__ g_sp) {
+  extern __shared__ __align__(16) unsigned char s_dyn2[];
+  __shared__ float s_red[kW2];
+  __shared__ int s_arrived;
+  const int slot = blockIdx.z, tile = blockIdx.y * a.tiles_x + blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Kept2& kp = reinterpret_cast<Kept2*>(s_dyn2)[w];
+  if (threadIdx.x == 0) s_arrived = 0;
+  __syncthreads();
+  const int rx = blockIdx.x * BS_TILE + (w & 1) * 8, ry = blockIdx.y * BS_TILE + (w >> 1) * 4;
+  const int px = rx + (lane & 7), py = ry + (lane >> 3);
+  const float x0 = rx + 0.5f, x1 = x0 + 7.f, y0 = ry + 0.5f, y1 = y0 + 3.f;
+  const float pxf = px + 0.5f, pyf = py + 0.5f;
+  const float oxf = (float)(lane & 7), oyf = (float)(lane >> 3);
+  const bool inside = slot_pixel(a.slot_patches, a.patch_P, a.W, a.H, slot, px, py);
+  const int2 rg = ranges[(int64_t)slot * a.tiles_per_slot + tile];
+  // ---------------- forward (raster2d_fwd_kernel's blend), appending the kept splats
+  Px2 p{1.f, 0.f, 0.f, 0.f, 0, !inside};
+  Splat2 f;
+  fetch2(f, sp, a.support, inst_rows, rg.x + lane, rg.x + lane < rg.y);
+  uint32_t row_next = row2(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
+  int nk = 0;
+  for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
+    if (__all_sync(0xffffffffu, p.done)) break;
+    const bool keep = reaches2(f, x0, x1, y0, y1);
+    const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int pos = (nk + __popc(bits & ((1u << lane) - 1u))) & (kKeep2 - 1);
+      stage2_rec(f, x0, y0, a.support != nullptr, kp.rec[pos]);
+      kp.idx[pos] = make_int2((int)f.row, b0 + lane - rg.x);
+    }
+    fetch2_row(f, sp, a.support, row_next, b0 + 32 + lane < rg.y);
+    row_next = row2(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
+    __syncwarp();
+    const int nb = __popc(bits);
+    for (int k = 0; k < nb; ++k) {
+      const int pos = (nk + k) & (kKeep2 - 1);
+      if (p.done) continue;
       Eval2 e;
-      eval2(sa, s.b[j], s.c[j], col.w, pxf, pyf, oxf, oyf, e);
-      const float ex = ex2a(fminf(e.pw2, 0.f));
-      const float raw = __fmul_rn(sa.z, ex);
-      const float alpha = fminf(kAMax, raw);
-      const bool any = rel < q.n && e.in;
-      {
-        const float ra = rcpa(1.f - alpha);  // alpha <= 0.99
-        const float T = q.T * ra;
-        const float fac = any ? alpha * T : 0.f;
-        g[12] = fac * q.dC0;
-        g[13] = fac * q.dC1;
-        g[14] = fac * q.dC2;
-        g[15] = 0.f;
-        // acc = colour behind this splat (normalised); acc' = acc + alpha (c - acc)
-        const float e0 = col.x - q.acc0, e1 = col.y - q.acc1, e2 = col.z - q.acc2;
-        float dLda = T * (e0 * q.dC0 + e1 * q.dC1 + e2 * q.dC2);
-        if (kBg) dLda -= q.T_final * ra * q.bgdot;
-        q.acc0 = any ? fmaf(alpha, e0, q.acc0) : q.acc0;
-        q.acc1 = any ? fmaf(alpha, e1, q.acc1) : q.acc1;
-        q.acc2 = any ? fmaf(alpha, e2, q.acc2) : q.acc2;
-        q.T = any ? T : q.T;
-        const bool grad = any && raw <= kAMax;
-        const float dpow = dLda * alpha;
-        g[11] = grad ? dLda * ex : 0.f;
-        // disk term: power = -0.5 (u^2 + v^2), (u, v) = zeta.xy / zeta.z; G_SP2
-        // carries the moments sum gz, sum gz px, sum gz py of dL/dzeta (the
-        // projection backward applies the M rows)
-        const bool disk = grad && e.disk;
-        const F2 guv = mul2(f2(e.u, e.v), bcast(-dpow));  // dL/d(u, v)
-        const float2 g_uv = unf2(guv);
-        const float iz = e.iz;
-        const F2 gz01 = mul2(guv, bcast(iz));
-        const float gz2 = -(g_uv.x * e.u + g_uv.y * e.v) * iz;
-        const float2 z01 = unf2(gz01);
-        const float2 zx = unf2(mul2(gz01, bcast(pxf)));
-        const float2 zy = unf2(mul2(gz01, bcast(pyf)));
-        g[2] = disk ? z01.x : 0.f;
-        g[3] = disk ? z01.y : 0.f;
-        g[4] = disk ? gz2 : 0.f;
-        g[5] = disk ? zx.x : 0.f;
-        g[6] = disk ? zx.y : 0.f;
-        g[7] = disk ? gz2 * pxf : 0.f;
-        g[8] = disk ? zy.x : 0.f;
-        g[9] = disk ? zy.y : 0.f;
-        g[10] = disk ? gz2 * pyf : 0.f;
-        // low-pass term: power = -(dx^2 + dy^2), dx = u - px
-        const bool lp = grad && !disk;
-        g[0] = lp ? -2.f * e.dx * dpow : 0.f;
-        g[1] = lp ? -2.f * e.dy * dpow : 0.f;
-      }
-      const uint32_t who = __ballot_sync(0xffffffffu, any);
-      if (who == 0u) continue;
-      float* dst = g_sp + (int64_t)s.row[j] * kGSP2;
-      if (__popc(who) <= kSparse2) {
-        if (any) {
-          // 64-byte aligned rows: four 128-bit REDs (the 16th float is padding, g[15] = 0)
-#pragma unroll
-          for (int k = 0; k < 16; k += 4)
-            atomicAdd(reinterpret_cast<float4*>(dst + k), make_float4(g[k], g[k + 1], g[k + 2], g[k + 3]));
-        }
-      } else {
-        const float r = warp_reduce16(g);
-        const int idx = lane >> 1;
-        if ((lane & 1) == 0 && idx < kGSP2Used) atomicAdd(dst + idx, r);
-      }
+      const float4 sa = kp.rec[pos][0];
+      const float4 col = kp.rec[pos][3];
+      eval2(sa, kp.rec[pos][1], kp.rec[pos][2], col.w, pxf, pyf, oxf, oyf, e);
+      if (!e.in) continue;
+      const float alpha = fminf(kAMax, __fmul_rn(sa.z, ex2a(e.pw2)));
+      const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
+      const bool fin = nT < kTStop;
+      const bool c = !fin;
+      const float wgt = __fmul_rn(alpha, p.T);
+      p.done = p.done || fin;
+      p.c0 = c ? __fmaf_rn(col.x, wgt, p.c0) : p.c0;
+      p.c1 = c ? __fmaf_rn(col.y, wgt, p.c1) : p.c1;
+      p.c2 = c ? __fmaf_rn(col.z, wgt, p.c2) : p.c2;
+      p.T = c ? nT : p.T;
+      p.contrib = c ? kp.idx[pos].y + 1 : p.contrib;
+    }
+    nk += nb;
+    __syncwarp();
+  }
+  // outputs, loss partial, this pixel's L1 gradient
+  float l = 0.f;
+  PxB2 q;
+  q.T = 1.f;
+  q.n = 0;
+  q.dC0 = q.dC1 = q.dC2 = 0.f;
+  if (inside) {
+    const int64_t pix = ((int64_t)slot * a.H + py) * a.W + px;
+    const float o0 = p.c0 + p.T * a.bg[0], o1 = p.c1 + p.T * a.bg[1], o2 = p.c2 + p.T * a.bg[2];
+    image[3 * pix] = o0;
+    image[3 * pix + 1] = o1;
+    image[3 * pix + 2] = o2;
+    final_T[pix] = p.T;
+    n_contrib[pix] = p.contrib;
+    const int gv = gt_view ? gt_view[slot] : slot;
+    const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py) * a.W + px);
+    const float d0 = o0 - gp[0] * (1.f / 255.f), d1 = o1 - gp[1] * (1.f / 255.f), d2 = o2 - gp[2] * (1.f / 255.f);
+    l = fabsf(d0) + fabsf(d1) + fabsf(d2);
+    q.dC0 = (d0 > 0.f ? 1.f : (d0 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+    q.dC1 = (d1 > 0.f ? 1.f : (d1 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+    q.dC2 = (d2 > 0.f ? 1.f : (d2 < 0.f ? -1.f : 0.f)) * a.inv_norm;
+    q.T = p.T;
+    q.n = p.contrib;
+  }
+  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  if (lane == 0) {  // the last warp to arrive sums the partials in warp order (no CTA barrier)
+    reinterpret_cast<volatile float*>(s_red)[w] = l;
+    int prev;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.s32 %0, [%1], 1;" : "=r"(prev)
+                 : "r"((uint32_t)__cvta_generic_to_shared(&s_arrived)) : "memory");
+    if (prev == kW2 - 1) {
+      float t = 0.f;
+      for (int k = 0; k < kW2; ++k) t += reinterpret_cast<volatile float*>(s_red)[k];
+      loss_tiles[(int64_t)slot * a.tiles_per_slot + tile] = t;
+    }
+  }
+  q.T_final = q.T;
+  q.bgdot = a.bg[0] * q.dC0 + a.bg[1] * q.dC1 + a.bg[2] * q.dC2;
+  q.acc0 = q.acc1 = q.acc2 = 0.f;
+  int warp_n = q.n;
+  for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
+  // ---------------- backward: the kept list back to front
+  if (nk <= kKeep2) {
+    for (int k = nk - 1; k >= 0; --k) {
+      const int2 id = kp.idx[k];
+      if (id.y >= warp_n) continue;  // warp-uniform
+      bwd2_splat<kBg>(q, kp.rec[k][0], kp.rec[k][1], kp.rec[k][2], kp.rec[k][3], (uint32_t)id.x, id.y, pxf, pyf, oxf,
+                      oyf, g_sp);
+    }
+    return;
+  }
+  // the list wrapped: chunked walk over global memory (raster2d_bwd_kernel's)
+  Warp2& s = *reinterpret_cast<Warp2*>(&kp);
+  __syncwarp();
+  const int end = rg.x + warp_n;
+  fetch2(f, sp, a.support, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
+  row_next = row2(inst_rows, end - 33 - lane, end - 33 - lane >= rg.x);
+  for (int cend = end; cend > rg.x; cend -= 32) {
+    const bool keep = reaches2(f, x0, x1, y0, y1);
+    uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if (keep) stage2(s, lane, f, x0, y0, a.support != nullptr);
+    fetch2_row(f, sp, a.support, row_next, cend - 33 - lane >= rg.x);
+    row_next = row2(inst_rows, cend - 65 - lane, cend - 65 - lane >= rg.x);
+    __syncwarp();
+    while (bits) {
+      const int j = __ffs(bits) - 1;
+      bits &= bits - 1;
+      bwd2_splat<kBg>(q, s.a[j], s.b[j], s.c[j], s.d[j], s.row[j], cend - 1 - j - rg.x, pxf, pyf, oxf, oyf, g_sp);
     }
     __syncwarp();
   }
@@ -504,6 +681,25 @@ extern "C" int32_t bs_raster2d_fwd(const bs_raster_desc* d, const float* sp_rows
   raster2d_fwd_kernel<<<grid, kT2, 0, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges),
                                                           image, final_T, n_contrib, gt, gt_slot_view, loss_tiles);
   BS_LAUNCH_CHECK("raster2d_fwd_kernel");
+  return BS_OK;
+}
+
+extern "C" int32_t bs_raster2d_fwd_bwd(const bs_raster_desc* d, const float* sp_rows, const uint32_t* inst_rows,
+                                       const int32_t* ranges, float* image, float* final_T, int32_t* n_contrib,
+                                       const uint8_t* gt, const int32_t* gt_slot_view, float* loss_tiles,
+                                       float* g_sp, void* stream) {
+  R2Args a;
+  int32_t st = make_r2(d, a);
+  if (st) return st;
+  BS_REQUIRE(gt && loss_tiles && g_sp, BS_ERR_PARAMETER, "raster2d_fwd_bwd needs gt, loss_tiles and g_sp");
+  const dim3 grid(a.tiles_x, (a.H + BS_TILE - 1) / BS_TILE, a.n_slots);
+  const bool bg = a.bg[0] != 0.f || a.bg[1] != 0.f || a.bg[2] != 0.f;
+  auto kern = bg ? raster2d_fused_kernel<true> : raster2d_fused_kernel<false>;
+  const size_t smem = sizeof(Kept2) * kW2;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, kT2, smem, as_stream(stream)>>>(a, sp_rows, inst_rows, reinterpret_cast<const int2*>(ranges), image,
+                                               final_T, n_contrib, gt, gt_slot_view, loss_tiles, g_sp);
+  BS_LAUNCH_CHECK("raster2d_fused_kernel");
   return BS_OK;
 }
 

@@ -842,10 +842,10 @@ class SplatTrainer:
             gt = self.gt
             gt_map = gt_views.to(torch.int32) if self.gt_lut is None else self.gt_lut.index_select(0, gt_views)
         losses = self.buf.get("losses", n_slots, torch.float32)
-        if self.raster_fused and self.model == "3dgs" and self.pixels_per_lane == 1:
+        if self.raster_fused and (self.model == "2dgs" or self.pixels_per_lane == 1):
             # K3 + L + K4 in one launch: each warp keeps its forward's splat list in shared memory
             with self._t("raster"):
-                nat.call("bs_raster_fwd_bwd", rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
+                nat.call("bs_raster2d_fwd_bwd" if self.model == "2dgs" else "bs_raster_fwd_bwd", rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
                          nat.ptr(final_T), nat.ptr(n_contrib), nat.ptr(gt), nat.ptr(gt_map), nat.ptr(loss_tiles),
                          nat.ptr(gsp), st)
             nat.call("bs_reduce_loss_tiles", nat.ptr(loss_tiles), n_slots, self.tiles, self.H, self.W,

@@ -25,8 +25,10 @@ def _run(make, batch, fused):
     losses = tr.step(batch).cpu().numpy()
     n = tr.last["n_rows"]
     npx = len(batch) * tr.H * tr.W
+    gf = tr.gsp_floats
     return (losses, tr.last["image"][: npx * 3].cpu().numpy(), tr.last["final_T"][:npx].cpu().numpy(),
-            tr.last["n_contrib"][:npx].cpu().numpy(), tr.last["gsp"][: n * 12].cpu().numpy().reshape(-1, 12))
+            tr.last["n_contrib"][:npx].cpu().numpy(), tr.last["gsp"][: n * gf].cpu().numpy().reshape(-1, gf),
+            tr.gsp_wire_floats)
 
 
 def _compare(make, batch):
@@ -34,26 +36,29 @@ def _compare(make, batch):
     b = _run(make, batch, False)
     for x, y in zip(a[:4], b[:4]):
         assert np.array_equal(x, y)
-    assert not a[4][:, 9:].any()
-    scale = np.abs(b[4][:, :9]).max(axis=0) + 1e-30
-    err = (np.abs(a[4][:, :9] - b[4][:, :9]) / scale).max(axis=0)
+    wire = a[5]
+    assert not a[4][:, wire:].any()
+    scale = np.abs(b[4][:, :wire]).max(axis=0) + 1e-30
+    err = (np.abs(a[4][:, :wire] - b[4][:, :wire]) / scale).max(axis=0)
     assert (err <= REL).all(), err
     return err
 
 
+@pytest.mark.parametrize("model", ["3dgs", "2dgs"])
 @pytest.mark.parametrize("bg", [(0.0, 0.0, 0.0), (0.2, 0.5, 0.9)])
-def test_fused_matches_two_kernels_c1(cuda, bg):
+def test_fused_matches_two_kernels_c1(cuda, bg, model):
     ds, params, gb, aabb, gt = c1_setup()
-    _compare(lambda: SplatTrainer(params, gb, aabb, ds.views, gt=gt, sh_degree=3, bg=bg), [0, 2, 5, 7])
+    _compare(lambda: SplatTrainer(params, gb, aabb, ds.views, gt=gt, sh_degree=3, bg=bg, model=model), [0, 2, 5, 7])
 
 
-def test_fused_wrapped_lists_fall_back(cuda):
-    """Large splats: every warp keeps far more than 128 splats, so the fused
-    kernel's backward takes the chunked global walk."""
+@pytest.mark.parametrize("model", ["3dgs", "2dgs"])
+def test_fused_wrapped_lists_fall_back(cuda, model):
+    """Large splats: every warp keeps far more splats than its shared-memory
+    list holds, so the fused kernel's backward takes the chunked global walk."""
     ds, params, gb, aabb, gt = c1_setup()
     params = params.copy()
     params[1, :, :3] += np.float32(1.5)
-    _compare(lambda: SplatTrainer(params, gb, aabb, ds.views, gt=gt, sh_degree=3), [1, 6])
+    _compare(lambda: SplatTrainer(params, gb, aabb, ds.views, gt=gt, sh_degree=3, model=model), [1, 6])
 
 
 def test_fused_matches_two_kernels_c2(cuda):
@@ -64,3 +69,13 @@ def test_fused_matches_two_kernels_c2(cuda):
     err = _compare(lambda: SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt),
                    [0, 3, 4, 7])
     print("C2 G_SP max rel diff per component", err)
+
+
+def test_fused_matches_two_kernels_c3(cuda):
+    ds = scenes.generate_aerial_scene(2, 2_000_000, (1, 1), 8, 50.0, (1920, 1080))
+    g = zorder_group(ds.cloud, G=2048)
+    params = scenes.init_gaussians(g.sorted_cloud, 2, scenes.mean_spacing(50.0, (1, 1), 2_000_000))
+    gt = scenes.synthetic_gt(2, 8, 1920, 1080)
+    err = _compare(lambda: SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt,
+                                        model="2dgs"), [1, 2, 5, 6])
+    print("C3 G_SP max rel diff per component", err.max())
