@@ -821,6 +821,15 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
   p.acc2 = 0.f;
   int warp_n = p.n;
   for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
+#ifdef BS_RASTER_STATS
+  if (lane == 0) {  // [56] lists that wrapped, [57] warps, [58] kept records, [59] > 192, [60] > 256
+    atomicAdd(&g_rstats[56], (unsigned long long)(nk > kKeep));
+    atomicAdd(&g_rstats[57], 1ull);
+    atomicAdd(&g_rstats[58], (unsigned long long)nk);
+    atomicAdd(&g_rstats[59], (unsigned long long)(nk > 192));
+    atomicAdd(&g_rstats[60], (unsigned long long)(nk > 256));
+  }
+#endif
   // ---------------- backward: back to front from the deepest contributor
   if (nk <= kKeep) {
     for (int k = nk - 1; k >= 0; --k) {

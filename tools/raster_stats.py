@@ -36,3 +36,5 @@ print(f"  zero {s[2]/s[1]:.3f} sparse {s[3]/s[1]:.3f} dense {s[4]/s[1]:.3f} mean
 h = s[8:41]
 print("  hist contributing lanes:", " ".join(f"{i}:{h[i]/s[1]:.3f}" for i in range(33)))
 print(f"fwd warp-chunks {s[48]:.0f} kept iterations {s[49]:.0f}, lanes in support per kept iteration {s[50]/max(s[49],1):.2f}")
+print(f"fused: warps {s[57]:.0f}, kept per warp {s[58]/max(s[57],1):.1f}, lists wrapped (> 128) {s[56]/max(s[57],1):.4f}, "
+      f"> 192 {s[59]/max(s[57],1):.4f}, > 256 {s[60]/max(s[57],1):.4f}")
