@@ -678,9 +678,6 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
 #ifndef BS_FUSED_CTAS
 #define BS_FUSED_CTAS 4
 #endif
-#ifndef BS_FUSED_NOBAR
-#define BS_FUSED_NOBAR 1
-#endif
 constexpr int kKeep = BS_FUSED_KEEP;  // kept-splat records per warp (48 B each; a power of two)
 
 struct KeptRec {
@@ -721,11 +718,6 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
   const int tile = blockIdx.y * a.tiles_x + blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   KeptRec* kept = reinterpret_cast<KeptRec*>(s_dyn) + w * kKeep;
-#if BS_FUSED_NOBAR
-  __shared__ int s_arrived;
-  if (threadIdx.x == 0) s_arrived = 0;
-  __syncthreads();
-#endif
   const Region<1> q(blockIdx.x, blockIdx.y);
   const float pxf = (float)q.px + 0.5f;
   const F2 npx = f2(-pxf, -((float)q.py0 + 0.5f));
@@ -789,23 +781,6 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
     p.n = pf.contrib;
   }
   for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-#if BS_FUSED_NOBAR
-  // the tile's loss partial without a CTA barrier (warps go on to their
-  // backward): the last warp to arrive sums the 8 warp partials in warp order
-  if (lane == 0) {
-    reinterpret_cast<volatile float*>(s_red)[w] = l;
-    // release the partial / acquire the others' (CTA scope; __threadfence_block
-    // is a fence.sc, which stalls the warp far longer)
-    int prev;
-    asm volatile("atom.acq_rel.cta.shared::cta.add.s32 %0, [%1], 1;" : "=r"(prev)
-                 : "r"((uint32_t)__cvta_generic_to_shared(&s_arrived)) : "memory");
-    if (prev == 7) {
-      float t = 0.f;
-      for (int k = 0; k < 8; ++k) t += reinterpret_cast<volatile float*>(s_red)[k];
-      loss_tiles[(int64_t)slot * a.tiles_per_slot + tile] = t;
-    }
-  }
-#else
   if (lane == 0) s_red[w] = l;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -813,7 +788,6 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
     for (int k = 0; k < 8; ++k) t += s_red[k];
     loss_tiles[(int64_t)slot * a.tiles_per_slot + tile] = t;
   }
-#endif
   p.T_final = p.T;
   p.dC01 = f2(dC0, dC1);
   p.bgdot = a.bg[0] * dC0 + a.bg[1] * dC1 + a.bg[2] * p.dC2;

@@ -8,6 +8,10 @@
         key counters of every captured kernel from a `--set full` capture:
         duration, DRAM bytes (traffic), SM/memory throughput, IPC, issue
         slots, occupancy, registers, executed instructions, top stall reasons
+    python profiles/summarize_ncu.py traffic <full1.json,full2.json,...> <out.json>
+        per kernel (first launch): DRAM bytes, duration and executed warp
+        instructions -- the table bench.py reads for `roofline.traffic` and
+        `roofline.issue`
 """
 
 from __future__ import annotations
@@ -87,9 +91,22 @@ def full(path: str) -> dict:
     return out
 
 
+def traffic(paths: str) -> dict:
+    out = {}
+    for p in paths.split(","):
+        table = json.load(open(p))
+        for name, recs in table.items():
+            if name in out or not recs:
+                continue
+            r = recs[0]
+            out[name] = {"dram_traffic_bytes": r.get("dram_traffic_bytes"), "duration_ns": r.get("duration_ns"),
+                         "warp_instructions": r.get("warp_instructions"), "capture": p.split("/")[-1]}
+    return out
+
+
 if __name__ == "__main__":
     mode, src, dst = sys.argv[1:4]
-    res = launches(src) if mode == "launches" else full(src)
+    res = launches(src) if mode == "launches" else (traffic(src) if mode == "traffic" else full(src))
     with open(dst, "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1)[:3000])
