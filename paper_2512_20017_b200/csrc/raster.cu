@@ -233,11 +233,11 @@ __device__ __forceinline__ void blend(PixelFwd& p, const float4& sa, const float
 
 // blend() with one early-out (the support test, mostly warp-uniform) and
 // selects for the rest; same arithmetic as blend().
-__device__ __forceinline__ void blend_sel(PixelFwd& p, const float4& sa, const float4& sb, float cb, float th2, F2 npx,
+__device__ __forceinline__ bool blend_sel(PixelFwd& p, const float4& sa, const float4& sb, float cb, float th2, F2 npx,
                                           int rel) {
   F2 d;
   const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
-  if (power2 > 0.f || power2 < th2) return;
+  if (power2 > 0.f || power2 < th2) return false;
   const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, ex2_approx(power2)));
   const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
   const bool fin = nT < kTMin;
@@ -250,6 +250,7 @@ __device__ __forceinline__ void blend_sel(PixelFwd& p, const float4& sa, const f
   p.c2 = c ? c2 : p.c2;
   p.T = c ? nT : p.T;
   p.contrib = c ? rel + 1 : p.contrib;
+  return c;
 }
 
 template <int PPL>
@@ -468,12 +469,14 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
 // the same instruction sequence as pixel_grad's, so the results are identical;
 // what goes is the divergent-branch bookkeeping (BSSY/BSYNC, three branches
 // and their reconvergence stalls) in the hottest loop of the backward.
-template <bool kBg>
+// kExact: `live` is the forward's own contribution decision for this pair
+// (the fused kernel's recorded mask), so the support test is not repeated.
+template <bool kBg, bool kExact = false>
 __device__ __forceinline__ bool pixel_grad_sel(PixelBwd& p, const float4& sa, const float4& sb, float cb, float th2,
                                                F2 npx, bool live, float g[9]) {
   F2 d;
   const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
-  const bool ok = live && !(power2 > 0.f || power2 < th2);
+  const bool ok = kExact ? live : live && !(power2 > 0.f || power2 < th2);
 #if BS_BWD_EARLY_OUT
   // no pixel of the warp inside the support: skip the gradient math (warp-uniform)
   if (!__any_sync(0xffffffffu, ok)) return false;
@@ -680,9 +683,41 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
 #endif
 constexpr int kKeep = BS_FUSED_KEEP;  // kept-splat records per warp (48 B each; a power of two)
 
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 struct KeptRec {
   float4 a, b, c;  // as Staged; c.w = range-relative index (int bits)
 };
+
+// one kept splat of the fused backward: `who` = the lanes whose pixel the
+// forward blended it into (recorded by the forward, never 0 here)
+template <bool kBg>
+__device__ __forceinline__ void bwd_splat_mask(PixelBwd& p, const float4& sa, const float4& sb, const float4& sc,
+                                               uint32_t who, F2 npx, float* __restrict__ g_sp) {
+  float g[9];
+  const bool any = (who >> (threadIdx.x & 31)) & 1u;
+  pixel_grad_sel<kBg, true>(p, sa, sb, sc.x, sc.y, npx, any, g);
+  float* dst = g_sp + (int64_t)__float_as_uint(sc.z) * BS_GSP_FLOATS;
+  if (__popc(who) <= kSparseLanes) {
+    if (any) {
+      atomicAdd(reinterpret_cast<float4*>(dst), make_float4(g[0], g[1], g[2], g[3]));
+      atomicAdd(reinterpret_cast<float4*>(dst + 4), make_float4(g[4], g[5], g[6], g[7]));
+      atomicAdd(dst + 8, g[8]);
+    }
+  } else {
+    int idx;
+    const float r = warp_reduce9(g, idx);
+    if (idx >= 0) atomicAdd(dst + idx, r);
+  }
+}
 
 // one splat of the backward for one warp: pixel gradient + warp reduction + REDs
 template <bool kBg>
@@ -734,8 +769,12 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
     if (__all_sync(0xffffffffu, pf.done)) break;
     const bool keep = reaches(f, q.x0, q.x1, q.y0, q.y1);
     const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    const int nb = __popc(bits);
+    // records of a chunk are contiguous: a list that would run past kKeep is
+    // abandoned (the backward falls back) and its chunks are staged at 0
+    KeptRec* const rk = kept + (nk + nb <= kKeep ? nk : 0);
     if (keep) {
-      KeptRec& r = kept[(nk + __popc(bits & ((1u << lane) - 1u))) & (kKeep - 1)];
+      KeptRec& r = rk[__popc(bits & ((1u << lane) - 1u))];
       r.a = make_float4(f.p0.x, f.p0.y, __fmul_rn(f.p0.w, kHalfLog2e), __fmul_rn(f.p1.y, kHalfLog2e));
       r.b = make_float4(__fmul_rn(f.p1.x, -kLog2e), f.p0.z, f.p1.z, f.p1.w);
       r.c = make_float4(f.b, kSup ? f.th2 : support_p2(f.p0.z), __uint_as_float(f.row),
@@ -744,12 +783,17 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
     fetch_row_data(f, sp, sup, row_next, b0 + 32 + lane < rg.y);
     row_next = fetch_row(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
     __syncwarp();
-    const int nb = __popc(bits);
-    for (int k = 0; k < nb; ++k) {
-      const KeptRec& r = kept[(nk + k) & (kKeep - 1)];
-      const float4 sa = r.a, sb = r.b;
-      const float2 sc = make_float2(r.c.x, r.c.y);
-      if (!pf.done) blend_sel(pf, sa, sb, sc.x, sc.y, npx, __float_as_int(r.c.w));
+    // explicit shared-space addresses: the three record loads stay together
+    // ahead of the per-pixel branch, and the address is one add per splat
+    uint32_t ra = (uint32_t)__cvta_generic_to_shared(rk);
+    for (int k = 0; k < nb; ++k, ra += (uint32_t)sizeof(KeptRec)) {
+      const float4 sa = lds128(ra), sb = lds128(ra + 16), sc = lds128(ra + 32);
+      bool blended = false;
+      if (!pf.done) blended = blend_sel(pf, sa, sb, sc.x, sc.y, npx, __float_as_int(sc.w));
+      // the pixels this splat was blended into: exactly the pairs the backward
+      // differentiates (rel < n_contrib and inside the support)
+      const uint32_t who = __ballot_sync(0xffffffffu, blended);
+      if (lane == 0) sts32(ra + 44, who);
     }
     nk += nb;
     __syncwarp();
@@ -793,8 +837,6 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
   p.bgdot = a.bg[0] * dC0 + a.bg[1] * dC1 + a.bg[2] * p.dC2;
   p.acc01 = make_float2(0.f, 0.f);
   p.acc2 = 0.f;
-  int warp_n = p.n;
-  for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
 #ifdef BS_RASTER_STATS
   if (lane == 0) {  // [56] lists that wrapped, [57] warps, [58] kept records, [59] > 192, [60] > 256
     atomicAdd(&g_rstats[56], (unsigned long long)(nk > kKeep));
@@ -808,15 +850,17 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
   if (nk <= kKeep) {
     for (int k = nk - 1; k >= 0; --k) {
       const KeptRec& r = kept[k];
-      const int rel = __float_as_int(r.c.w);
-      if (rel >= warp_n) continue;  // past every pixel's last contributor (warp-uniform)
-      bwd_splat<kBg>(p, r.a, r.b, r.c, rel, npx, g_sp);
+      const uint32_t who = __float_as_uint(r.c.w);
+      if (who == 0u) continue;  // blended into none of the warp's pixels (warp-uniform)
+      bwd_splat_mask<kBg>(p, r.a, r.b, r.c, who, npx, g_sp);
     }
     return;
   }
   // the list wrapped: the backward's own chunked walk over global memory
   WarpSmem& s = *reinterpret_cast<WarpSmem*>(kept);
   __syncwarp();
+  int warp_n = p.n;
+  for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
   const int end = rg.x + warp_n;
   fetch_splat(f, sp, sup, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
   row_next = fetch_row(inst_rows, end - 33 - lane, end - 33 - lane >= rg.x);
