@@ -48,9 +48,6 @@ constexpr float kHalfLog2e = -0.5f * kLog2e;  // p2 = power * log2(e) = q * kHal
 #define BS_SPARSE_LANES 10
 #endif
 constexpr int kSparseLanes = BS_SPARSE_LANES;
-#ifndef BS_BWD_EARLY_OUT
-#define BS_BWD_EARLY_OUT 0
-#endif  // contributing lanes handled with direct REDs
 
 #ifdef BS_RASTER_STATS
 // tuning instrumentation (never in the product build; tools/raster_stats.py):
@@ -246,6 +243,28 @@ __device__ __forceinline__ bool blend_sel(PixelFwd& p, const float4& sa, const f
   const F2 c01 = fma2(f2(sb.z, sb.w), bcast(w), p.c01);
   const float c2 = __fmaf_rn(cb, w, p.c2);
   p.done = p.done || fin;
+  p.c01 = c ? c01 : p.c01;
+  p.c2 = c ? c2 : p.c2;
+  p.T = c ? nT : p.T;
+  p.contrib = c ? rel + 1 : p.contrib;
+  return c;
+}
+
+// blend_sel without any branch (done pixels and pairs outside the support
+// keep their state through selects); same arithmetic for a blended pair.
+__device__ __forceinline__ bool blend_pred(PixelFwd& p, const float4& sa, const float4& sb, float cb, float th2, F2 npx,
+                                           int rel) {
+  F2 d;
+  const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
+  const bool in = !p.done && !(power2 > 0.f || power2 < th2);
+  const float alpha = fminf(kAlphaMax, __fmul_rn(sb.y, ex2_approx(fminf(power2, 0.f))));
+  const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
+  const bool fin = nT < kTMin;
+  const bool c = in && !fin;
+  const float w = __fmul_rn(alpha, p.T);
+  const F2 c01 = fma2(f2(sb.z, sb.w), bcast(w), p.c01);
+  const float c2 = __fmaf_rn(cb, w, p.c2);
+  p.done = p.done || (in && fin);
   p.c01 = c ? c01 : p.c01;
   p.c2 = c ? c2 : p.c2;
   p.T = c ? nT : p.T;
@@ -469,48 +488,62 @@ __device__ __forceinline__ bool pixel_grad(PixelBwd& p, const float4& sa, const 
 // the same instruction sequence as pixel_grad's, so the results are identical;
 // what goes is the divergent-branch bookkeeping (BSSY/BSYNC, three branches
 // and their reconvergence stalls) in the hottest loop of the backward.
-// kExact: `live` is the forward's own contribution decision for this pair
-// (the fused kernel's recorded mask), so the support test is not repeated.
-template <bool kBg, bool kExact = false>
-__device__ __forceinline__ bool pixel_grad_sel(PixelBwd& p, const float4& sa, const float4& sb, float cb, float th2,
-                                               F2 npx, bool live, float g[9]) {
+// The per-pair math in two halves: pair_front depends only on the splat
+// and the pixel (independent of the back-to-front recurrence, so a loop can
+// evaluate the next splat's front while the current one's tail and
+// reduction run); pair_back advances the pixel's T / acc and writes the 9
+// gradient terms.  pixel_grad_sel = front + support test + back.
+struct PairFront {
   F2 d;
-  const float power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, d);
-  const bool ok = kExact ? live : live && !(power2 > 0.f || power2 < th2);
-#if BS_BWD_EARLY_OUT
-  // no pixel of the warp inside the support: skip the gradient math (warp-uniform)
-  if (!__any_sync(0xffffffffu, ok)) return false;
-#endif
-  const float ex = ex2_approx(fminf(power2, 0.f));
-  const float raw = __fmul_rn(sb.y, ex);
-  const float alpha = fminf(kAlphaMax, raw);
-  const float ra = rcp_approx(1.f - alpha);  // alpha <= 0.99
-  const float T = p.T * ra;
-  const float fac = alpha * T;
+  float power2, ex, raw, alpha, ra;
+};
+
+__device__ __forceinline__ void pair_front(PairFront& f, const float4& sa, const float4& sb, F2 npx) {
+  f.power2 = splat_power2(f2(sa.x, sa.y), f2(sa.z, sa.w), sb.x, npx, f.d);
+  f.ex = ex2_approx(fminf(f.power2, 0.f));
+  f.raw = __fmul_rn(sb.y, f.ex);
+  f.alpha = fminf(kAlphaMax, f.raw);
+  f.ra = rcp_approx(1.f - f.alpha);  // alpha <= 0.99
+}
+
+template <bool kBg>
+__device__ __forceinline__ void pair_back(PixelBwd& p, const PairFront& f, const float4& sb, float cb, bool ok,
+                                          float g[9]) {
+  const float T = p.T * f.ra;
+  const float fac = f.alpha * T;
   const F2 e01 = add2(f2(sb.z, sb.w), f2(-p.acc01.x, -p.acc01.y));
   const float e2 = cb - p.acc2;
   const float2 ed = unf2(mul2(e01, p.dC01));
   float dL_dalpha = T * fmaf(e2, p.dC2, ed.x + ed.y);
-  if (kBg) dL_dalpha -= p.T_final * ra * p.bgdot;
-  const float2 acc01 = unf2(fma2(bcast(alpha), e01, f2(p.acc01.x, p.acc01.y)));
-  const float acc2 = fmaf(alpha, e2, p.acc2);
+  if (kBg) dL_dalpha -= p.T_final * f.ra * p.bgdot;
+  const float2 acc01 = unf2(fma2(bcast(f.alpha), e01, f2(p.acc01.x, p.acc01.y)));
+  const float acc2 = fmaf(f.alpha, e2, p.acc2);
   p.T = ok ? T : p.T;
   p.acc01 = ok ? acc01 : p.acc01;
   p.acc2 = ok ? acc2 : p.acc2;
-  const bool grad = ok && !(raw > kAlphaMax);
-  const float dpow = grad ? dL_dalpha * alpha : 0.f;  // dL / d power
-  const float2 t01 = unf2(mul2(bcast(dpow), d));
-  const float2 t34 = unf2(mul2(bcast(t01.x), d));
+  const bool grad = ok && !(f.raw > kAlphaMax);
+  const float dpow = grad ? dL_dalpha * f.alpha : 0.f;  // dL / d power
+  const float2 t01 = unf2(mul2(bcast(dpow), f.d));
+  const float2 t34 = unf2(mul2(bcast(t01.x), f.d));
   const float2 t67 = unf2(mul2(bcast(ok ? fac : 0.f), p.dC01));
   g[0] = t01.x;
   g[1] = t01.y;
-  g[2] = grad ? dL_dalpha * ex : 0.f;
+  g[2] = grad ? dL_dalpha * f.ex : 0.f;
   g[3] = t34.x;
   g[4] = t34.y;
-  g[5] = t01.y * unf2(d).y;
+  g[5] = t01.y * unf2(f.d).y;
   g[6] = t67.x;
   g[7] = t67.y;
   g[8] = (ok ? fac : 0.f) * p.dC2;
+}
+
+template <bool kBg>
+__device__ __forceinline__ bool pixel_grad_sel(PixelBwd& p, const float4& sa, const float4& sb, float cb, float th2,
+                                               F2 npx, bool live, float g[9]) {
+  PairFront f;
+  pair_front(f, sa, sb, npx);
+  const bool ok = live && !(f.power2 > 0.f || f.power2 < th2);
+  pair_back<kBg>(p, f, sb, cb, ok, g);
   return ok;
 }
 
@@ -681,7 +714,10 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
 #ifndef BS_FUSED_CTAS
 #define BS_FUSED_CTAS 4
 #endif
-constexpr int kKeep = BS_FUSED_KEEP;  // kept-splat records per warp (48 B each; a power of two)
+#ifndef BS_FUSED_FWD_SEL
+#define BS_FUSED_FWD_SEL 1  // A/B on B200 (C2 raster): branchy 2.545, predicated 2.484 ms
+#endif
+constexpr int kKeep = BS_FUSED_KEEP;  // kept-splat records per warp (48 B each)
 
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
   float4 v;
@@ -697,15 +733,9 @@ struct KeptRec {
   float4 a, b, c;  // as Staged; c.w = range-relative index (int bits)
 };
 
-// one kept splat of the fused backward: `who` = the lanes whose pixel the
-// forward blended it into (recorded by the forward, never 0 here)
-template <bool kBg>
-__device__ __forceinline__ void bwd_splat_mask(PixelBwd& p, const float4& sa, const float4& sb, const float4& sc,
-                                               uint32_t who, F2 npx, float* __restrict__ g_sp) {
-  float g[9];
-  const bool any = (who >> (threadIdx.x & 31)) & 1u;
-  pixel_grad_sel<kBg, true>(p, sa, sb, sc.x, sc.y, npx, any, g);
-  float* dst = g_sp + (int64_t)__float_as_uint(sc.z) * BS_GSP_FLOATS;
+// the reduction of one splat's 9 terms over the warp into its G_SP row:
+// `who` = the contributing lanes (non-zero), `any` = this lane's bit
+__device__ __forceinline__ void reduce_splat(const float g[9], uint32_t who, bool any, float* __restrict__ dst) {
   if (__popc(who) <= kSparseLanes) {
     if (any) {
       atomicAdd(reinterpret_cast<float4*>(dst), make_float4(g[0], g[1], g[2], g[3]));
@@ -717,6 +747,18 @@ __device__ __forceinline__ void bwd_splat_mask(PixelBwd& p, const float4& sa, co
     const float r = warp_reduce9(g, idx);
     if (idx >= 0) atomicAdd(dst + idx, r);
   }
+}
+
+// one kept splat of the fused backward from its record (c.w = the lanes the
+// forward blended it into, never 0 in the compacted list)
+template <bool kBg>
+__device__ __forceinline__ void bwd_rec(PixelBwd& p, const PairFront& fr, const float4& sb, const float4& sc,
+                                        float* __restrict__ g_sp) {
+  const uint32_t who = __float_as_uint(sc.w);
+  const bool any = (who >> (threadIdx.x & 31)) & 1u;
+  float g[9];
+  pair_back<kBg>(p, fr, sb, sc.x, any, g);
+  reduce_splat(g, who, any, g_sp + (int64_t)__float_as_uint(sc.z) * BS_GSP_FLOATS);
 }
 
 // one splat of the backward for one warp: pixel gradient + warp reduction + REDs
@@ -788,15 +830,33 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
     uint32_t ra = (uint32_t)__cvta_generic_to_shared(rk);
     for (int k = 0; k < nb; ++k, ra += (uint32_t)sizeof(KeptRec)) {
       const float4 sa = lds128(ra), sb = lds128(ra + 16), sc = lds128(ra + 32);
+#if BS_FUSED_FWD_SEL
+      const bool blended = blend_pred(pf, sa, sb, sc.x, sc.y, npx, __float_as_int(sc.w));
+#else
       bool blended = false;
       if (!pf.done) blended = blend_sel(pf, sa, sb, sc.x, sc.y, npx, __float_as_int(sc.w));
+#endif
       // the pixels this splat was blended into: exactly the pairs the backward
-      // differentiates (rel < n_contrib and inside the support)
+      // differentiates (rel < n_contrib and inside the support).  (Keeping
+      // the masks in registers until the chunk ends measured slower: spills.)
       const uint32_t who = __ballot_sync(0xffffffffu, blended);
       if (lane == 0) sts32(ra + 44, who);
     }
-    nk += nb;
     __syncwarp();
+    if (nk + nb <= kKeep) {
+      // drop the chunk's records blended into no pixel: the backward's list
+      // holds contributing splats only (lane j moves record j)
+      KeptRec r;
+      if (lane < nb) r = rk[lane];
+      const bool live = lane < nb && __float_as_uint(r.c.w) != 0u;
+      const uint32_t lb = __ballot_sync(0xffffffffu, live);
+      __syncwarp();
+      if (live) rk[__popc(lb & ((1u << lane) - 1u))] = r;
+      nk += __popc(lb);
+      __syncwarp();
+    } else {
+      nk = kKeep + 1;  // the list overflowed: the backward takes the chunked walk
+    }
   }
   // outputs + loss partial + this pixel's L1 gradient
   float l = 0.f;
@@ -848,11 +908,27 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
 #endif
   // ---------------- backward: back to front from the deepest contributor
   if (nk <= kKeep) {
-    for (int k = nk - 1; k >= 0; --k) {
-      const KeptRec& r = kept[k];
-      const uint32_t who = __float_as_uint(r.c.w);
-      if (who == 0u) continue;  // blended into none of the warp's pixels (warp-uniform)
-      bwd_splat_mask<kBg>(p, r.a, r.b, r.c, who, npx, g_sp);
+    // two records per iteration: the front half of the shallower splat's
+    // pair math does not depend on the deeper one's, so it overlaps the
+    // deeper splat's tail and reduction
+    int k = nk - 1;
+    for (; k >= 1; k -= 2) {
+      const KeptRec& r1 = kept[k];
+      const KeptRec& r0 = kept[k - 1];
+      const float4 a1 = r1.a, b1 = r1.b, c1 = r1.c;
+      const float4 a0 = r0.a, b0 = r0.b;
+      PairFront f1, f0;
+      pair_front(f1, a1, b1, npx);
+      pair_front(f0, a0, b0, npx);
+      bwd_rec<kBg>(p, f1, b1, c1, g_sp);
+      bwd_rec<kBg>(p, f0, b0, r0.c, g_sp);
+    }
+    if (k == 0) {
+      const KeptRec& r = kept[0];
+      const float4 a0 = r.a, b0 = r.b;
+      PairFront f0;
+      pair_front(f0, a0, b0, npx);
+      bwd_rec<kBg>(p, f0, b0, r.c, g_sp);
     }
     return;
   }
