@@ -346,51 +346,58 @@ struct PxB2 {
   int n;
 };
 
-// One splat of the 2DGS backward for one warp: the pixel's gradient terms
-// (selects instead of branches), then the per-splat reduction and REDs.
-template <bool kBg>
-__device__ __forceinline__ void bwd2_splat(PxB2& q, const float4& sa, const float4& sb, const float4& sc,
-                                           const float4& col, uint32_t row, int rel, float pxf, float pyf, float oxf,
-                                           float oyf, float* __restrict__ g_sp) {
-  const int lane = threadIdx.x & 31;
-  // every lane runs the whole sequence; pixels without a contribution
-  // keep their state through selects and produce zero terms (same
-  // arithmetic as a branchy version for the contributing ones)
-  float g[16];
+// One splat of the 2DGS backward for one warp, in two halves: bwd2_front
+// depends only on the splat and the pixel (a loop can evaluate the next
+// splat's front while the current one's tail and reduction run);
+// bwd2_back advances the pixel's T / acc and writes the 16 gradient terms
+// (selects instead of branches: every lane runs the whole sequence, pixels
+// without a contribution keep their state and produce zero terms -- the same
+// arithmetic as a branchy version for the contributing ones).
+struct Front2 {
   Eval2 e;
-  eval2(sa, sb, sc, col.w, pxf, pyf, oxf, oyf, e);
-  const float ex = ex2a(fminf(e.pw2, 0.f));
-  const float raw = __fmul_rn(sa.z, ex);
-  const float alpha = fminf(kAMax, raw);
-  const bool any = rel < q.n && e.in;
+  float ex, raw, alpha, ra;
+};
+
+__device__ __forceinline__ void bwd2_front(Front2& f, const float4& sa, const float4& sb, const float4& sc, float k,
+                                           float pxf, float pyf, float oxf, float oyf) {
+  eval2(sa, sb, sc, k, pxf, pyf, oxf, oyf, f.e);
+  f.ex = ex2a(fminf(f.e.pw2, 0.f));
+  f.raw = __fmul_rn(sa.z, f.ex);
+  f.alpha = fminf(kAMax, f.raw);
+  f.ra = rcpa(1.f - f.alpha);  // alpha <= 0.99
+}
+
+template <bool kBg>
+__device__ __forceinline__ void bwd2_back(PxB2& q, const Front2& f, const float4& col, bool any, float pxf, float pyf,
+                                          float g[16]) {
   {
-    const float ra = rcpa(1.f - alpha);  // alpha <= 0.99
+    const float ra = f.ra;
     const float T = q.T * ra;
-    const float fac = any ? alpha * T : 0.f;
+    const float fac = any ? f.alpha * T : 0.f;
     g[12] = fac * q.dC0;
     g[13] = fac * q.dC1;
     g[14] = fac * q.dC2;
     g[15] = 0.f;
-    // acc = colour behind this splat (normalised); acc' = acc + alpha (c - acc)
+    // acc = colour behind this splat (normalised); acc' = acc + f.alpha (c - acc)
     const float e0 = col.x - q.acc0, e1 = col.y - q.acc1, e2 = col.z - q.acc2;
     float dLda = T * (e0 * q.dC0 + e1 * q.dC1 + e2 * q.dC2);
     if (kBg) dLda -= q.T_final * ra * q.bgdot;
-    q.acc0 = any ? fmaf(alpha, e0, q.acc0) : q.acc0;
-    q.acc1 = any ? fmaf(alpha, e1, q.acc1) : q.acc1;
-    q.acc2 = any ? fmaf(alpha, e2, q.acc2) : q.acc2;
+    q.acc0 = any ? fmaf(f.alpha, e0, q.acc0) : q.acc0;
+    q.acc1 = any ? fmaf(f.alpha, e1, q.acc1) : q.acc1;
+    q.acc2 = any ? fmaf(f.alpha, e2, q.acc2) : q.acc2;
     q.T = any ? T : q.T;
-    const bool grad = any && raw <= kAMax;
-    const float dpow = dLda * alpha;
-    g[11] = grad ? dLda * ex : 0.f;
+    const bool grad = any && f.raw <= kAMax;
+    const float dpow = dLda * f.alpha;
+    g[11] = grad ? dLda * f.ex : 0.f;
     // disk term: power = -0.5 (u^2 + v^2), (u, v) = zeta.xy / zeta.z; G_SP2
     // carries the moments sum gz, sum gz px, sum gz py of dL/dzeta (the
     // projection backward applies the M rows)
-    const bool disk = grad && e.disk;
-    const F2 guv = mul2(f2(e.u, e.v), bcast(-dpow));  // dL/d(u, v)
+    const bool disk = grad && f.e.disk;
+    const F2 guv = mul2(f2(f.e.u, f.e.v), bcast(-dpow));  // dL/d(u, v)
     const float2 g_uv = unf2(guv);
-    const float iz = e.iz;
+    const float iz = f.e.iz;
     const F2 gz01 = mul2(guv, bcast(iz));
-    const float gz2 = -(g_uv.x * e.u + g_uv.y * e.v) * iz;
+    const float gz2 = -(g_uv.x * f.e.u + g_uv.y * f.e.v) * iz;
     const float2 z01 = unf2(gz01);
     const float2 zx = unf2(mul2(gz01, bcast(pxf)));
     const float2 zy = unf2(mul2(gz01, bcast(pyf)));
@@ -405,12 +412,14 @@ __device__ __forceinline__ void bwd2_splat(PxB2& q, const float4& sa, const floa
     g[10] = disk ? gz2 * pyf : 0.f;
     // low-pass term: power = -(dx^2 + dy^2), dx = u - px
     const bool lp = grad && !disk;
-    g[0] = lp ? -2.f * e.dx * dpow : 0.f;
-    g[1] = lp ? -2.f * e.dy * dpow : 0.f;
+    g[0] = lp ? -2.f * f.e.dx * dpow : 0.f;
+    g[1] = lp ? -2.f * f.e.dy * dpow : 0.f;
   }
-  const uint32_t who = __ballot_sync(0xffffffffu, any);
-  if (who == 0u) return;
-  float* dst = g_sp + (int64_t)row * kGSP2;
+}
+
+// the reduction of one splat's 15 terms into its G_SP row (`who` non-zero)
+__device__ __forceinline__ void reduce2(const float g[16], uint32_t who, bool any, float* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
   if (__popc(who) <= kSparse2) {
     if (any) {
       // 64-byte aligned rows: four 128-bit REDs (the 16th float is padding, g[15] = 0)
@@ -419,10 +428,24 @@ __device__ __forceinline__ void bwd2_splat(PxB2& q, const float4& sa, const floa
         atomicAdd(reinterpret_cast<float4*>(dst + k), make_float4(g[k], g[k + 1], g[k + 2], g[k + 3]));
     }
   } else {
-    const float r = warp_reduce16(g);
+    const float r = warp_reduce16(const_cast<float*>(g));
     const int idx = lane >> 1;
     if ((lane & 1) == 0 && idx < kGSP2Used) atomicAdd(dst + idx, r);
   }
+}
+
+template <bool kBg>
+__device__ __forceinline__ void bwd2_splat(PxB2& q, const float4& sa, const float4& sb, const float4& sc,
+                                           const float4& col, uint32_t row, int rel, float pxf, float pyf, float oxf,
+                                           float oyf, float* __restrict__ g_sp) {
+  Front2 f;
+  bwd2_front(f, sa, sb, sc, col.w, pxf, pyf, oxf, oyf);
+  const bool any = rel < q.n && f.e.in;
+  float g[16];
+  bwd2_back<kBg>(q, f, col, any, pxf, pyf, g);
+  const uint32_t who = __ballot_sync(0xffffffffu, any);
+  if (who == 0u) return;
+  reduce2(g, who, any, g_sp + (int64_t)row * kGSP2);
 }
 
 template <bool kBg>
@@ -493,12 +516,12 @@ __global__ void __launch_bounds__(kT2, BS_R2_BWD_CTAS) raster2d_bwd_kernel(
 
 // ---- K3 + L + K4 in one kernel (2DGS; see raster_fused_kernel in raster.cu)
 #ifndef BS_FUSED2_KEEP
-#define BS_FUSED2_KEEP 128  // swept on B200 (C3 raster ms): 32 (4 CTAs) 7.80, 64 7.29, 128 7.16; separate kernels 7.32
+#define BS_FUSED2_KEEP 128  // swept on B200 (C3 raster ms, before the list compaction): 32 (4 CTAs) 7.80, 64 7.29, 128 7.16; separate kernels 7.32
 #endif
 #ifndef BS_FUSED2_CTAS
 #define BS_FUSED2_CTAS 3
 #endif
-constexpr int kKeep2 = BS_FUSED2_KEEP;  // kept-splat records per warp (a power of two)
+constexpr int kKeep2 = BS_FUSED2_KEEP;  // kept-splat records per warp
 
 struct Kept2 {
   float4 rec[kKeep2][4];  // staged a, b, c, d (stage2 layout)
@@ -528,42 +551,71 @@ __global__ void __launch_bounds__(kT2, BS_FUSED2_CTAS) raster2d_fused_kernel(
   Splat2 f;
   fetch2(f, sp, a.support, inst_rows, rg.x + lane, rg.x + lane < rg.y);
   uint32_t row_next = row2(inst_rows, rg.x + 32 + lane, rg.x + 32 + lane < rg.y);
-  int nk = 0;
+  int nk = 0;  // kept records (warp-uniform); kKeep2 + 1 once the list overflowed
   for (int b0 = rg.x; b0 < rg.y; b0 += 32) {
     if (__all_sync(0xffffffffu, p.done)) break;
     const bool keep = reaches2(f, x0, x1, y0, y1);
     const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    const int nb = __popc(bits);
+    // a chunk's records are contiguous; a chunk that does not fit is staged
+    // at 0 and the backward takes the chunked walk
+    const int base = nk + nb <= kKeep2 ? nk : 0;
     if (keep) {
-      const int pos = (nk + __popc(bits & ((1u << lane) - 1u))) & (kKeep2 - 1);
+      const int pos = base + __popc(bits & ((1u << lane) - 1u));
       stage2_rec(f, x0, y0, a.support != nullptr, kp.rec[pos]);
       kp.idx[pos] = make_int2((int)f.row, b0 + lane - rg.x);
     }
     fetch2_row(f, sp, a.support, row_next, b0 + 32 + lane < rg.y);
     row_next = row2(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
     __syncwarp();
-    const int nb = __popc(bits);
     for (int k = 0; k < nb; ++k) {
-      const int pos = (nk + k) & (kKeep2 - 1);
-      if (p.done) continue;
+      const int pos = base + k;
       Eval2 e;
       const float4 sa = kp.rec[pos][0];
       const float4 col = kp.rec[pos][3];
       eval2(sa, kp.rec[pos][1], kp.rec[pos][2], col.w, pxf, pyf, oxf, oyf, e);
-      if (!e.in) continue;
-      const float alpha = fminf(kAMax, __fmul_rn(sa.z, ex2a(e.pw2)));
+      // predicated (no branch): pixels done or outside the support keep their state
+      const bool in = !p.done && e.in;
+      const float alpha = fminf(kAMax, __fmul_rn(sa.z, ex2a(fminf(e.pw2, 0.f))));
       const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
       const bool fin = nT < kTStop;
-      const bool c = !fin;
+      const bool c = in && !fin;
       const float wgt = __fmul_rn(alpha, p.T);
-      p.done = p.done || fin;
+      p.done = p.done || (in && fin);
       p.c0 = c ? __fmaf_rn(col.x, wgt, p.c0) : p.c0;
       p.c1 = c ? __fmaf_rn(col.y, wgt, p.c1) : p.c1;
       p.c2 = c ? __fmaf_rn(col.z, wgt, p.c2) : p.c2;
       p.T = c ? nT : p.T;
       p.contrib = c ? kp.idx[pos].y + 1 : p.contrib;
+      // the lanes this splat was blended into = the pairs the backward
+      // differentiates; replaces the range-relative index in the record
+      const uint32_t who = __ballot_sync(0xffffffffu, c);
+      if (lane == 0) kp.idx[pos].y = (int)who;
     }
-    nk += nb;
     __syncwarp();
+    if (nk + nb <= kKeep2) {
+      // keep only the records blended into some pixel (lane j moves record j)
+      float4 r[4];
+      int2 id = make_int2(0, 0);
+      if (lane < nb) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) r[q4] = kp.rec[base + lane][q4];
+        id = kp.idx[base + lane];
+      }
+      const bool live = lane < nb && id.y != 0;
+      const uint32_t lb = __ballot_sync(0xffffffffu, live);
+      __syncwarp();
+      if (live) {
+        const int dst = base + __popc(lb & ((1u << lane) - 1u));
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) kp.rec[dst][q4] = r[q4];
+        kp.idx[dst] = id;
+      }
+      nk += __popc(lb);
+      __syncwarp();
+    } else {
+      nk = kKeep2 + 1;
+    }
   }
   // outputs, loss partial, this pixel's L1 gradient
   float l = 0.f;
@@ -600,21 +652,42 @@ __global__ void __launch_bounds__(kT2, BS_FUSED2_CTAS) raster2d_fused_kernel(
   q.T_final = q.T;
   q.bgdot = a.bg[0] * q.dC0 + a.bg[1] * q.dC1 + a.bg[2] * q.dC2;
   q.acc0 = q.acc1 = q.acc2 = 0.f;
-  int warp_n = q.n;
-  for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
-  // ---------------- backward: the kept list back to front
+  // ---------------- backward: the kept list back to front, two records per
+  // iteration (the shallower splat's front half overlaps the deeper one's
+  // tail and reduction)
   if (nk <= kKeep2) {
-    for (int k = nk - 1; k >= 0; --k) {
-      const int2 id = kp.idx[k];
-      if (id.y >= warp_n) continue;  // warp-uniform
-      bwd2_splat<kBg>(q, kp.rec[k][0], kp.rec[k][1], kp.rec[k][2], kp.rec[k][3], (uint32_t)id.x, id.y, pxf, pyf, oxf,
-                      oyf, g_sp);
+    int k = nk - 1;
+    for (; k >= 1; k -= 2) {
+      const int2 id1 = kp.idx[k], id0 = kp.idx[k - 1];
+      const float4 c1 = kp.rec[k][3], c0 = kp.rec[k - 1][3];
+      Front2 f1, f0;
+      bwd2_front(f1, kp.rec[k][0], kp.rec[k][1], kp.rec[k][2], c1.w, pxf, pyf, oxf, oyf);
+      bwd2_front(f0, kp.rec[k - 1][0], kp.rec[k - 1][1], kp.rec[k - 1][2], c0.w, pxf, pyf, oxf, oyf);
+      float g[16];
+      const bool any1 = ((uint32_t)id1.y >> lane) & 1u;
+      bwd2_back<kBg>(q, f1, c1, any1, pxf, pyf, g);
+      reduce2(g, (uint32_t)id1.y, any1, g_sp + (int64_t)(uint32_t)id1.x * kGSP2);
+      const bool any0 = ((uint32_t)id0.y >> lane) & 1u;
+      bwd2_back<kBg>(q, f0, c0, any0, pxf, pyf, g);
+      reduce2(g, (uint32_t)id0.y, any0, g_sp + (int64_t)(uint32_t)id0.x * kGSP2);
+    }
+    if (k == 0) {
+      const int2 id = kp.idx[0];
+      const float4 c0 = kp.rec[0][3];
+      Front2 f0;
+      bwd2_front(f0, kp.rec[0][0], kp.rec[0][1], kp.rec[0][2], c0.w, pxf, pyf, oxf, oyf);
+      float g[16];
+      const bool any = ((uint32_t)id.y >> lane) & 1u;
+      bwd2_back<kBg>(q, f0, c0, any, pxf, pyf, g);
+      reduce2(g, (uint32_t)id.y, any, g_sp + (int64_t)(uint32_t)id.x * kGSP2);
     }
     return;
   }
   // the list wrapped: chunked walk over global memory (raster2d_bwd_kernel's)
   Warp2& s = *reinterpret_cast<Warp2*>(&kp);
   __syncwarp();
+  int warp_n = q.n;
+  for (int o = 16; o > 0; o >>= 1) warp_n = max(warp_n, __shfl_xor_sync(0xffffffffu, warp_n, o));
   const int end = rg.x + warp_n;
   fetch2(f, sp, a.support, inst_rows, end - 1 - lane, end - 1 - lane >= rg.x);
   row_next = row2(inst_rows, end - 33 - lane, end - 33 - lane >= rg.x);
