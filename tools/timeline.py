@@ -25,7 +25,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1, help="consecutive steps inside the profile")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
-    ds, g, params, gt = bench.build_scene(cfg)
+    ds, g, params, gt = bench.build_scene(cfg)[:4]
     tr = SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt,
                       adam=AdamConfig(scenes.lr_table(cfg["altitude"])), model=cfg.get("model", "3dgs"))
     sched = bench.schedule(cfg["n_views"], cfg["batch"], 5 + args.steps)
