@@ -447,14 +447,18 @@ def run_ours(args, cfg):
         e_start.record()
         upload(0)
         for i, b in enumerate(batches):
-            if i + 1 < len(batches):
-                upload(i + 1)
-            torch.cuda.current_stream().wait_event(ready[i % 2])
-            losses = tr.step(b, gt_batch=gt_bufs[i % 2],
+            # the step waits for its upload only at the first read of the
+            # ground truth (the raster): culling, projection and binning overlap it
+            losses = tr.step(b, gt_batch=gt_bufs[i % 2], gt_ready=ready[i % 2],
                              next_batch=batches[i + 1] if comm is not None and i + 1 < len(batches) else None)
             ev = torch.cuda.Event()
             ev.record()
             freed[i % 2] = ev
+            if i + 1 < len(batches):
+                # queued once the host is back from step i (which returns while
+                # its raster runs): the next upload overlaps the compute-bound
+                # raster rather than the memory-bound front of the step
+                upload(i + 1)
             loss_pinned[i][: losses.numel()].copy_(losses, non_blocking=True)
         e_end.record()
         torch.cuda.synchronize()

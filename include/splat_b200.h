@@ -102,6 +102,22 @@ typedef struct {
   int32_t width, height;
 } bs_camera;
 
+/* ---- per-step view rows and small host transfers (csrc/views.cu) -------
+ * The batch's per-view rows (cameras, frustum planes, view times, ground-truth
+ * indices; the reference selects views by index, visibility.py:308-358) are
+ * gathered with the view ids passed as kernel parameters (`ids` is a HOST
+ * array, n <= 32), and the step's few host-bound integers are stored by a
+ * kernel into mapped pinned memory: neither waits on the copy engines behind
+ * the caller's bulk uploads.  dst[k] = src[ids[k]], rows of row_bytes (a
+ * multiple of 4). */
+int32_t bs_select_rows(const int32_t* ids, int32_t n, const void* src,
+                       int64_t n_src_rows, int64_t row_bytes, void* dst,
+                       void* stream);
+/* n_bytes (a multiple of 4) from device memory into pinned host memory
+ * (cudaHostAlloc / torch pin_memory), stream-ordered */
+int32_t bs_copy_to_host(const void* src, int64_t n_bytes, void* dst_pinned,
+                        void* stream);
+
 /* ---- K0: culling / access counts --------------------------------------- */
 enum {
   BS_CULL_ACCESS_EXACT = 0,  /* out0: int64 [B*P*P, n_gpus] (build_access_matrix EXACT) */

@@ -92,6 +92,8 @@ _SIGS = {
     "bs_last_error": (C.c_char_p, []),
     "bs_abi_version": (_I32, []),
     "bs_launch_count": (_I64, []),
+    "bs_select_rows": (_I32, [_P, _I32, _P, _I64, _I64, _P, _P]),
+    "bs_copy_to_host": (_I32, [_P, _I64, _P, _P]),
     "bs_cull_count": (_I32, [C.POINTER(CullDesc), _P, _I64, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "bs_bbox": (_I32, [_P, _I64, _I32, _P, _P, _SZ, _P]),
     "bs_bbox_workspace": (_SZ, [_I64]),

@@ -49,7 +49,7 @@ def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, 
     if pin is None:
         pin = torch.empty(2, dtype=torch.int64, pin_memory=True)
         buf.bin_stats_pin = pin
-    pin.copy_(stats, non_blocking=True)
+    nat.call("bs_copy_to_host", nat.ptr(stats), 16, pin.data_ptr(), st)  # by a kernel: no copy-engine queue
     ready = torch.cuda.Event()
     ready.record()
     if before_sync is not None:

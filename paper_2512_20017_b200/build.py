@@ -25,7 +25,7 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
     "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
 ]
-SOURCES = ["abi.cu", "cull.cu", "sort.cu", "project.cu", "bin.cu", "bin_tiles.cu", "raster.cu", "raster2d.cu", "patches.cu", "peer.cu", "densify.cu"]
+SOURCES = ["abi.cu", "cull.cu", "sort.cu", "project.cu", "bin.cu", "bin_tiles.cu", "raster.cu", "raster2d.cu", "patches.cu", "peer.cu", "densify.cu", "views.cu"]
 HEADERS = ["common.cuh", "splat_math.cuh", "splat2d_math.cuh", "tile.cuh", "packed.cuh"]
 
 

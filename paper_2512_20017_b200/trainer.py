@@ -224,10 +224,11 @@ class SplatTrainer:
         else:
             keys = gb0.copy()
         self.group_keys = keys
-        # batch indices reach the GPU by asynchronous copies from a pinned ring
-        self._ids_pin = [torch.empty(64, dtype=torch.int64, pin_memory=True) for _ in range(2)]
-        self._ids_ev = [None, None]
-        self._ids_k = 0
+        # per-view device tables the batch's rows are selected from (the view
+        # ids travel as kernel parameters: csrc/views.cu)
+        self._view_iota = torch.arange(len(self.views), dtype=torch.int64, device=self.dev)
+        self._gt_index = (self.gt_lut if self.gt_lut is not None
+                          else torch.arange(len(self.views), dtype=torch.int32, device=self.dev))
         # N = 1: the splat buffer is sized for every point in every batch view
         # when that fits this budget, so the projection is launched before the
         # host reads the row counts (the read then overlaps the projection)
@@ -262,30 +263,35 @@ class SplatTrainer:
         return _T()
 
     # ------------------------------------------------------------------ step
-    def _device_ids(self, ids, name):
-        """Batch indices on the device through a pinned, event-guarded ring
-        (a pageable copy would stall the host until the GPU caught up)."""
-        k = self._ids_k = (self._ids_k + 1) % 2
-        if self._ids_ev[k] is not None:
-            self._ids_ev[k].synchronize()
-        n = len(ids)
-        pin = self._ids_pin[k]
-        pin[:n] = torch.as_tensor(np.asarray(ids, dtype=np.int64))
-        dst = self.buf.get(name, 64, torch.int64)[:n]
-        dst.copy_(pin[:n], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        self._ids_ev[k] = ev
-        return dst
+    def _wait_gt(self):
+        """The compute stream waits for the caller's ground-truth upload (once)."""
+        if getattr(self, "_gt_ready", None) is not None:
+            torch.cuda.current_stream().wait_event(self._gt_ready)
+            self._gt_ready = None
 
-    def _cull_counts(self, batch_ids, mask, counts, base, view_rows, view_row0, st, bidx=None, patch_counts=None,
-                     chunk_prefix=None):
+    def _select_views(self, ids, table, name):
+        """Rows `ids` (host view indices, <= 32) of a per-view device table,
+        into a reused device buffer: bs_select_rows passes the ids as kernel
+        parameters, so nothing waits on a copy engine (csrc/views.cu)."""
+        n = len(ids)
+        row = table[0].numel()
+        out = self.buf.get(name, max(n, 1) * row, table.dtype)[: n * row].view(n, *table.shape[1:])
+        ids32 = np.ascontiguousarray(ids, dtype=np.int32)
+        nat.call("bs_select_rows", ids32.ctypes.data, n, nat.ptr(table), table.shape[0], row * table.element_size(),
+                 nat.ptr(out), nat.stream_handle())
+        return out
+
+    def _device_ids(self, ids, name):
+        """Batch indices as a device int64 tensor (selected from an identity
+        table: no host-to-device copy)."""
+        return self._select_views(ids, self._view_iota, name)
+
+    def _cull_counts(self, batch_ids, mask, counts, base, view_rows, view_row0, st, patch_counts=None,
+                     chunk_prefix=None, tag=""):
         B = len(batch_ids)
-        if bidx is None:
-            bidx = self._device_ids(batch_ids, "bidx_cull")
-        planes = self.planes_all.index_select(0, bidx).contiguous()
+        planes = self._select_views(batch_ids, self.planes_all, "planes_sel" + tag)
         temporal = self.presence is not None
-        times = self.view_times.index_select(0, bidx).contiguous() if temporal else None
+        times = self._select_views(batch_ids, self.view_times, "times_sel" + tag) if temporal else None
         desc = nat.CullDesc(nat.CULL_MASK, B, self.P, 1, 1 if temporal else 0, 4, self.max_chunks, nat.ptr(chunk_prefix))
         nat.call("bs_cull_count", desc, nat.ptr(self.params), self.S, nat.ptr(self.presence),
                  nat.ptr(self.group_begin), nat.ptr(self.aabb), self.n_groups, nat.ptr(planes), nat.ptr(times),
@@ -294,20 +300,24 @@ class SplatTrainer:
         nat.call("bs_scan_counts", nat.ptr(counts), self.n_groups, B, order.ctypes.data, nat.ptr(base),
                  nat.ptr(view_rows), nat.ptr(view_row0), st)
 
-    def step(self, batch_ids, gt_batch: torch.Tensor | None = None, next_batch=None):
+    def step(self, batch_ids, gt_batch: torch.Tensor | None = None, next_batch=None, gt_ready=None):
         """One training step over `batch_ids` (indices into self.views).
         Returns the mean-L1 losses of the views rendered on THIS rank as a
         device tensor, in batch order (N = 1: all B views); their batch
         positions are in self.last["loss_views"] (with several ranks each
         rank returns its own views' losses, W of PAPER.md:488).
         With several ranks, `next_batch` (the same on every rank) starts the
-        asynchronous placement of the following step (exchange.py)."""
+        asynchronous placement of the following step (exchange.py).
+        `gt_ready` (optional CUDA event): `gt_batch` is being uploaded on
+        another stream; the step waits for it only where the ground truth is
+        first read (the raster), so the upload overlaps culling, projection
+        and binning."""
         B = len(batch_ids)
+        self._gt_ready = gt_ready
         if not (1 <= B <= 32):
             raise ValueError("batch must hold 1..32 views")
         dev, S, st = self.dev, self.S, nat.stream_handle()
-        bidx = self._device_ids(batch_ids, "bidx")
-        cams = self.cams_all.index_select(0, bidx).contiguous()
+        cams = self._select_views(batch_ids, self.cams_all, "cams_sel")
         # ---- K0: culling -> visibility masks + per-(group, view) counts
         mask = self.buf.get("mask", S, torch.int32)
         counts = self.buf.get("counts", self.n_groups * B, torch.int32)
@@ -319,7 +329,7 @@ class SplatTrainer:
         # rows of each (group, 256-point chunk) before the chunk, for the projection kernels
         chunk_prefix = self.buf.get("chunk_prefix", self.n_groups * self.max_chunks * B, torch.int32)
         with self._t("cull"):
-            self._cull_counts(batch_ids, mask, counts, base, view_rows, view_row0, st, bidx, patch_counts,
+            self._cull_counts(batch_ids, mask, counts, base, view_rows, view_row0, st, patch_counts,
                               chunk_prefix)
         if self.comm is not None and next_batch is not None:
             # counts of the next batch (per view, or per patch when P > 1) on
@@ -331,11 +341,11 @@ class SplatTrainer:
                               nb.get("counts_next", self.n_groups * Bn, torch.int32),
                               nb.get("base_next", self.n_groups * Bn, torch.int32),
                               nb.get("view_rows_next", Bn, torch.int64), nb.get("view_row0_next", Bn, torch.int64), st,
-                              patch_counts=pc_next)
+                              patch_counts=pc_next, tag="_next")
             self.comm.prefetch(pc_next if patched else nb.get("view_rows_next", Bn, torch.int64),
                                tuple(int(v) for v in next_batch))
         if patched:
-            return self._step_patches(batch_ids, gt_batch, bidx, cams, mask, base, view_rows, view_row0,
+            return self._step_patches(batch_ids, gt_batch, cams, mask, base, view_rows, view_row0,
                                       patch_counts, st, chunk_prefix)
         lay = None
         pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group, 0,
@@ -360,7 +370,7 @@ class SplatTrainer:
             # the row counts start towards the host before the projection is
             # queued, so the host resumes while the projection still runs
             rows_pin = self._rows_pin[:B]
-            rows_pin.copy_(view_rows, non_blocking=True)
+            nat.call("bs_copy_to_host", nat.ptr(view_rows), 8 * B, rows_pin.data_ptr(), st)
             rows_ready = torch.cuda.Event()
             rows_ready.record()
             # ---- K1 first (rows land at view_row0 from the scan), then the
@@ -418,7 +428,7 @@ class SplatTrainer:
             seg_row0 = view_row0
             seg_slot = self._slot_ids(B)
             self.last["loss_views"] = list(range(B))
-            losses, gsp = self._render_and_backward(sp, n_rows, seg_row0, seg_slot, B, cams, bidx, gt_batch,
+            losses, gsp = self._render_and_backward(sp, n_rows, seg_row0, seg_slot, B, cams, batch_ids, gt_batch,
                                                     gsp_cleared=bool(pdesc.gsp_zero), support=support,
                                                     records=records)
         else:
@@ -440,10 +450,11 @@ class SplatTrainer:
             seg_slot = self._slot_ids(n_slots)
             gt_slots = None
             if gt_batch is not None:
+                self._wait_gt()
                 gt_slots = gt_batch.index_select(0, mine).contiguous()
             losses, gsp_c = self._render_and_backward(sp_c, lay.n_recv, seg_row0, seg_slot, n_slots,
                                                       cams.index_select(0, mine).contiguous(),
-                                                      bidx.index_select(0, mine), gt_slots,
+                                                      [batch_ids[int(m)] for m in lay.my_views], gt_slots,
                                                       support=self._recv_support)
             with self._t("a2a_bwd"):
                 wire = self.gsp_wire_floats
@@ -482,7 +493,7 @@ class SplatTrainer:
                      nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(gsp), st)
         return losses
 
-    def _step_patches(self, batch_ids, gt_batch, bidx, cams, mask, base, view_rows, view_row0, patch_counts, st,
+    def _step_patches(self, batch_ids, gt_batch, cams, mask, base, view_rows, view_row0, patch_counts, st,
                       chunk_prefix=None):
         """Alg. 1 with P x P patches per view on several ranks (SURVEY.md
         §8(e)): A over the B P^2 patches -> W; every rank projects its points
@@ -560,10 +571,13 @@ class SplatTrainer:
             slot_rows = np.bincount(np.asarray(seg_slot), weights=np.asarray(seg_rows), minlength=n_slots)
             seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(slot_rows)[:-1]]).astype(np.int64), device=dev)
             bits_t = torch.as_tensor(slot_bits.view(np.int64), device=dev)
+            if gt_batch is not None:
+                self._wait_gt()
             gt_slots = gt_batch.index_select(0, mine).contiguous() if gt_batch is not None else None
             losses, gsp_c = self._render_and_backward(sp_c, n_recv, seg_row0, self._slot_ids(n_slots), n_slots,
                                                       cams.index_select(0, mine).contiguous(),
-                                                      bidx.index_select(0, mine), gt_slots, slot_patches=bits_t,
+                                                      [batch_ids[int(m)] for m in my_views], gt_slots,
+                                                      slot_patches=bits_t,
                                                       support=self._recv_support)
             g = self._uncanonical(gsp_c, order, n_recv, wire)
         # ---- gradient rows back to their sources, summed into the row they left
@@ -837,10 +851,11 @@ class SplatTrainer:
         rdesc = nat.RasterDesc(n_slots, self.tiles, self.W, self.H, (ctypes.c_float * 3)(*self.bg), 1,
                                self.pixels_per_lane, self.P, nat.ptr(slot_patches), nat.ptr(support))
         if gt_batch is not None:
+            self._wait_gt()
             gt, gt_map = gt_batch, None
         else:
             gt = self.gt
-            gt_map = gt_views.to(torch.int32) if self.gt_lut is None else self.gt_lut.index_select(0, gt_views)
+            gt_map = self._select_views(gt_views, self._gt_index, "gt_map")  # host view ids -> gt rows
         losses = self.buf.get("losses", n_slots, torch.float32)
         if self.raster_fused and (self.model == "2dgs" or self.pixels_per_lane == 1):
             # K3 + L + K4 in one launch: each warp keeps its forward's splat list in shared memory

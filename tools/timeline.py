@@ -23,6 +23,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--steps", type=int, default=1, help="consecutive steps inside the profile")
+    ap.add_argument("--e2e", action="store_true",
+                    help="bench.py's e2e loop: ground truth H2D on a side stream (double-buffered), losses D2H")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     ds, g, params, gt = bench.build_scene(cfg)[:4]
@@ -33,9 +35,39 @@ def main():
         tr.step(sched[i])
     assert len(sched) >= 5 + args.steps
     torch.cuda.synchronize()
+    W, H = cfg["image_size"]
+    B = cfg["batch"]
+    pinned = torch.from_numpy(gt).pin_memory()
+    gt_bufs = [torch.empty((B, H, W, 3), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    copy_stream = torch.cuda.Stream()
+    ready, freed = [None, None], [None, None]
+    batches = sched[5:5 + args.steps]
+
+    def upload(i):
+        with torch.cuda.stream(copy_stream):
+            if freed[i % 2] is not None:
+                copy_stream.wait_event(freed[i % 2])
+            for k, v in enumerate(batches[i]):
+                gt_bufs[i % 2][k].copy_(pinned[v], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+            ready[i % 2] = ev
+
+    loss_pinned = torch.empty(B, dtype=torch.float32, pin_memory=True)
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+        if args.e2e:
+            upload(0)
         for i in range(args.steps):
-            tr.step(sched[5 + i])
+            if not args.e2e:
+                tr.step(batches[i])
+                continue
+            losses = tr.step(batches[i], gt_batch=gt_bufs[i % 2], gt_ready=ready[i % 2])
+            ev = torch.cuda.Event()
+            ev.record()
+            freed[i % 2] = ev
+            if i + 1 < args.steps:
+                upload(i + 1)
+            loss_pinned.copy_(losses, non_blocking=True)
         torch.cuda.synchronize()
     ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     ev.sort(key=lambda e: e.time_range.start)
