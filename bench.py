@@ -247,7 +247,7 @@ _STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_ke
 
 # committed ncu --set full summaries (newest first); each names the
 # configuration it captured per model (tools/gpu_profile.sh)
-TRAFFIC_FILES = ("r2_kernel_traffic.json", "r1_kernel_traffic.json")
+TRAFFIC_FILES = ("r2g_kernel_traffic.json", "r2_kernel_traffic.json", "r1_kernel_traffic.json")
 _PROFILED = {"3dgs": "c2", "2dgs": "c3"}
 
 

@@ -111,6 +111,12 @@ __global__ void __launch_bounds__(kCullThreads) cull_kernel(CullArgs a) {
     s_view_live[v] = any;
   }
   __syncthreads();
+  // MASK mode (B <= 32): the group's live views as a bit set, so the
+  // per-point loop visits only them (a group is usually live in 1-3 of the
+  // batch's views)
+  uint32_t live_bits = 0;
+  if (MODE == BS_CULL_MASK)
+    for (int v = 0; v < B && v < 32; ++v) live_bits |= (uint32_t)s_view_live[v] << v;
 
   if (MODE == BS_CULL_ACCESS_GROUP) {
     // Every point of a non-culled group counts (GROUP_APPROX).
@@ -158,7 +164,12 @@ __global__ void __launch_bounds__(kCullThreads) cull_kernel(CullArgs a) {
         if (MODE == BS_CULL_ACCESS_EXACT && a.point_gpu) gpu = a.point_gpu[i];
       }
       uint32_t mask = 0;
-      for (int v = 0; v < B; ++v) {
+      uint32_t todo = live_bits;
+      for (int v = 0; MODE == BS_CULL_MASK ? todo != 0u : v < B; ++v) {
+        if (MODE == BS_CULL_MASK) {  // next live view (CTA-uniform)
+          v = __ffs(todo) - 1;
+          todo &= todo - 1;
+        }
         bool vis_view = false;
         // any live patch for this view? (uniform across the CTA)
         if (s_view_live[v] && valid) {

@@ -25,10 +25,17 @@ import sys
 
 
 def _short(name: str) -> str:
-    n = name.split("(")[0].replace("void ", "")
-    for p in ("bs::(anonymous namespace)::", "bs::<unnamed>::"):
+    n = name.replace("void ", "")
+    for p in ("bs::(anonymous namespace)::", "bs::<unnamed>::", "(anonymous namespace)::", "unnamed>::"):
         n = n.replace(p, "")
-    return n
+    depth, cut = 0, len(n)  # drop the parameter list (the first '(' outside template brackets)
+    for i, ch in enumerate(n):
+        depth += ch == "<"
+        depth -= ch == ">"
+        if ch == "(" and depth == 0:
+            cut = i
+            break
+    return n[:cut]
 
 
 def launches(path: str) -> dict:
