@@ -144,6 +144,17 @@ typedef struct {
                             instead of re-counting the group's earlier chunks) */
 } bs_cull_desc;
 
+/* Visible-chunk work list from a BS_CULL_MASK launch's counts (out1) and
+ * chunk_prefix: work_list (int32 [n_groups * max_chunks]) receives
+ * g * max_chunks + c for every 256-point chunk with a visible point, in no
+ * particular order, and *work_count their number; the projection kernels
+ * then visit only those chunks (bs_proj_desc.work_list). */
+int32_t bs_list_chunks(const int32_t* counts, const int32_t* chunk_prefix,
+                       const int32_t* group_begin, int32_t n_groups,
+                       int32_t max_chunks, int32_t n_views,
+                       int32_t* work_list, int32_t* work_count,
+                       void* stream);
+
 /* planes: float64 [B][2 + 2*(P+1)][4]: near, far, x-edges c=0..P,
  *   y-edges r=0..P, each (nx, ny, nz, offset) exactly as numpy computes
  *   them in frustum_from_view (visibility.py:168-217).  Patch (r,c) of a
@@ -266,6 +277,15 @@ typedef struct {
                                   point, (sum over views of |dL/d mean2d| in NDC units,
                                   number of views with a valid splat) ACCUMULATED --
                                   the densification statistic (bs_densify_mark) */
+  const int32_t* work_list;    /* optional, with chunk_prefix: bs_list_chunks' list of
+                                  the chunks with a visible point and its device count
+                                  (work_count); bs_project_fwd, and bs_project_bwd_adam
+                                  with selective Adam, then run a grid-stride loop over
+                                  those chunks instead of one CTA per (group, chunk) --
+                                  at C4 (~2 % of the points visible per view) the empty
+                                  CTAs cost more than the work.  Same results (rows are
+                                  placed by chunk_prefix, points update independently) */
+  const int32_t* work_count;
 } bs_proj_desc;
 int32_t bs_project_fwd(const bs_proj_desc* desc_host, const float* params,
                        int64_t n_points, const uint32_t* vis_mask,

@@ -62,7 +62,7 @@ class ProjDesc(C.Structure):
                 ("gsp_zero", C.c_void_p), ("point_gid", C.c_void_p), ("row_gid", C.c_void_p),
                 ("row_support", C.c_void_p), ("view_sp", C.c_void_p), ("view_gid", C.c_void_p),
                 ("bucket_counts", C.c_void_p), ("row_bin", C.c_void_p), ("tiles_per_slot", C.c_int32),
-                ("densify_stats", C.c_void_p)]
+                ("densify_stats", C.c_void_p), ("work_list", C.c_void_p), ("work_count", C.c_void_p)]
 
 
 class DensifyDesc(C.Structure):
@@ -93,6 +93,7 @@ _SIGS = {
     "bs_abi_version": (_I32, []),
     "bs_launch_count": (_I64, []),
     "bs_select_rows": (_I32, [_P, _I32, _P, _I64, _I64, _P, _P]),
+    "bs_list_chunks": (_I32, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
     "bs_copy_to_host": (_I32, [_P, _I64, _P, _P]),
     "bs_cull_count": (_I32, [C.POINTER(CullDesc), _P, _I64, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "bs_bbox": (_I32, [_P, _I64, _I32, _P, _P, _SZ, _P]),

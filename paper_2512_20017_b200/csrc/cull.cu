@@ -464,3 +464,60 @@ extern "C" int32_t bs_gather_planes(const float* in, int64_t n_in, const int64_t
   BS_LAUNCH_CHECK("gather_planes_kernel");
   return BS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Visible-chunk work list from the culling's counts: chunk c of group g has a
+// visible point iff some view's running count grows over it (chunk_prefix
+// of chunk c + 1, or the group's total for the last chunk, minus chunk c's).
+// The projection kernels then loop over the listed chunks only (at C4 ~2 %
+// of the points are visible per view; one CTA per (group, chunk) would mostly
+// launch empty CTAs).  Warp-aggregated appends, in no particular order.
+
+namespace bs {
+namespace {
+
+__global__ void list_chunks_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ chunk_prefix,
+                                   const int32_t* __restrict__ group_begin, int n_groups, int max_chunks, int B,
+                                   int32_t* __restrict__ work_list, int32_t* __restrict__ work_count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)n_groups * max_chunks;
+  for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < total; t0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = t0 + threadIdx.x;
+    bool vis = false;
+    if (t < total) {
+      const int g = (int)(t / max_chunks), c = (int)(t - (int64_t)g * max_chunks);
+      const int size = group_begin[g + 1] - group_begin[g];
+      if (c * kCullThreads < size) {
+        const bool last = (c + 1) * kCullThreads >= size;
+        const int32_t* p0 = chunk_prefix + ((int64_t)g * max_chunks + c) * B;
+        const int32_t* p1 = last ? counts + (int64_t)g * B : p0 + B;
+        for (int v = 0; v < B && !vis; ++v) vis = p1[v] > p0[v];
+      }
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, vis);
+    if (bal == 0u) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(work_count, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (vis) work_list[base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)t;
+  }
+}
+
+}  // namespace
+}  // namespace bs
+
+extern "C" int32_t bs_list_chunks(const int32_t* counts, const int32_t* chunk_prefix, const int32_t* group_begin,
+                                  int32_t n_groups, int32_t max_chunks, int32_t n_views, int32_t* work_list,
+                                  int32_t* work_count, void* stream) {
+  BS_REQUIRE(max_chunks >= 1 && n_views >= 1 && n_groups >= 0, BS_ERR_PARAMETER, "list_chunks: bad sizes");
+  BS_REQUIRE((int64_t)n_groups * max_chunks < (1ll << 31), BS_ERR_PARAMETER, "list_chunks: too many chunks");
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(work_count, 0, sizeof(int32_t), s) != cudaSuccess)
+    return set_error(BS_ERR_CUDA, "list_chunks: memset failed");
+  const int64_t total = (int64_t)n_groups * max_chunks;
+  if (total == 0) return BS_OK;
+  list_chunks_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 2048), 256, 0, s>>>(
+      counts, chunk_prefix, group_begin, n_groups, max_chunks, n_views, work_list, work_count);
+  BS_LAUNCH_CHECK("list_chunks_kernel");
+  return BS_OK;
+}

@@ -62,19 +62,19 @@ struct RowRanker {
 // per-view counts advanced over the group's earlier chunks first.  Returns
 // false (uniformly over the CTA) when the chunk lies past the group's end.
 __device__ __forceinline__ bool chunk_range(const int32_t* __restrict__ group_begin, const uint32_t* __restrict__ mask,
-                                            const int32_t* __restrict__ chunk_prefix, RowRanker& rk, int g, int B,
-                                            int& lo, int& hi) {
+                                            const int32_t* __restrict__ chunk_prefix, RowRanker& rk, int g, int cy,
+                                            int ny, int B, int& lo, int& hi) {
   const int begin = group_begin[g], end = group_begin[g + 1];
-  if (gridDim.y == 1) {
+  if (ny == 1) {
     lo = begin;
     hi = end;
     return true;
   }
-  lo = begin + (int)blockIdx.y * kProjThreads;
+  lo = begin + cy * kProjThreads;
   if (lo >= end) return false;
   hi = min(end, lo + kProjThreads);
   if (chunk_prefix) {  // counted by the culling kernel
-    if (threadIdx.x < B) rk.s_run[threadIdx.x] = chunk_prefix[((size_t)g * gridDim.y + blockIdx.y) * B + threadIdx.x];
+    if (threadIdx.x < B) rk.s_run[threadIdx.x] = chunk_prefix[((size_t)g * ny + cy) * B + threadIdx.x];
     __syncthreads();
     return true;
   }
@@ -106,6 +106,10 @@ struct ProjArgs {
   int4* row_bin;                // with bucket_counts: per-row (depth bits, x0|x1<<16, y0|y1<<16, 0)
   int tiles_per_slot;
   float2* densify_stats;        // (bs_project_bwd_adam, 3DGS): per point (sum |dL/d mean2d| NDC, views), or NULL
+  // visible-chunk work list (bs_cull_count): g * max_chunks + c per entry, or NULL
+  const int32_t* work_list;
+  const int32_t* work_count;
+  int max_chunks;
 };
 
 // Splat models: 3DGS (EWA Gaussians, 12-float SP rows) and 2DGS (surfels,
@@ -183,7 +187,7 @@ template <class M>
 #ifndef BS_PROJ_FWD_CTAS
 #define BS_PROJ_FWD_CTAS 4  // CTAs per SM the projection's register budget is sized for
 #endif
-__global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_kernel(ProjArgs a, float* __restrict__ sp) {
+__device__ __forceinline__ void project_fwd_chunk(const ProjArgs& a, float* __restrict__ sp, int g, int cy, int ny) {
   // each thread's SH coefficients, staged by cp.async (no registers held for
   // them across the view loop): [12][kProjThreads] float4
   extern __shared__ float4 s_sh4f[];
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_ke
   __shared__ int s_run[kMaxViews];
   __shared__ bs_camera s_cam[kMaxViews];
   __shared__ int64_t s_row0[kMaxViews];
-  const int g = blockIdx.x, B = a.B;
+  const int B = a.B;
   if (threadIdx.x < B) {
     s_run[threadIdx.x] = 0;
     s_cam[threadIdx.x] = a.cams[threadIdx.x];
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_ke
   __syncthreads();
   RowRanker rk{s_bal, s_run};
   int lo, end;
-  if (!chunk_range(a.group_begin, a.mask, a.chunk_prefix, rk, g, B, lo, end)) return;
+  if (!chunk_range(a.group_begin, a.mask, a.chunk_prefix, rk, g, cy, ny, B, lo, end)) return;
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const uint32_t mask = i < end ? a.mask[i] : 0u;
@@ -259,6 +263,24 @@ __global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_ke
       }
     }
     rk.advance(B);
+  }
+}
+
+// One CTA per (group, chunk), or -- with a visible-chunk work list -- a
+// grid-stride loop over the listed chunks (empty chunks cost no CTA).
+// (kWork: separate instantiations, so the one-CTA-per-chunk kernel keeps
+// its own register allocation)
+template <class M, bool kWork>
+__global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_kernel(ProjArgs a, float* __restrict__ sp) {
+  if constexpr (!kWork) {
+    project_fwd_chunk<M>(a, sp, blockIdx.x, blockIdx.y, gridDim.y);
+    return;
+  }
+  const int n = *a.work_count;
+  for (int w = blockIdx.x; w < n; w += gridDim.x) {
+    const int item = __ldg(a.work_list + w);
+    project_fwd_chunk<M>(a, sp, item / a.max_chunks, item % a.max_chunks, a.max_chunks);
+    __syncthreads();  // the chunk's shared-memory state is rebuilt by the next
   }
 }
 
@@ -339,7 +361,7 @@ __global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, c
   __syncthreads();
   RowRanker rk{s_bal, s_run};
   int lo, end;
-  if (!chunk_range(a.group_begin, a.mask, a.chunk_prefix, rk, g, B, lo, end)) return;
+  if (!chunk_range(a.group_begin, a.mask, a.chunk_prefix, rk, g, blockIdx.y, gridDim.y, B, lo, end)) return;
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const uint32_t mask = i < end ? a.mask[i] : 0u;
@@ -418,11 +440,10 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamConsts c, float4* __restr
 }
 
 template <class M>
-__global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjArgs a, AdamConsts c,
-                                                                           const float* __restrict__ gsp,
-                                                                           float4* params,
-                                                                           float4* __restrict__ m,
-                                                                           float4* __restrict__ v) {
+__device__ __forceinline__ void project_bwd_adam_chunk(const ProjArgs& a, const AdamConsts& c,
+                                                       const float* __restrict__ gsp, float4* params,
+                                                       float4* __restrict__ m, float4* __restrict__ v, int g, int cy,
+                                                       int ny) {
   // [12][kProjThreads] float4 SH gradients, then [12][kProjThreads] float4 SH values
   extern __shared__ float4 s_gsh4[];
   float4* s_sh4 = s_gsh4 + 12 * kProjThreads;
@@ -430,7 +451,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
   __shared__ int s_run[kMaxViews];
   __shared__ bs_camera s_cam[kMaxViews];
   __shared__ int64_t s_row0[kMaxViews];
-  const int g = blockIdx.x, B = a.B;
+  const int B = a.B;
   if (threadIdx.x < B) {
     s_run[threadIdx.x] = 0;
     s_cam[threadIdx.x] = a.cams[threadIdx.x];
@@ -439,7 +460,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
   __syncthreads();
   RowRanker rk{s_bal, s_run};
   int lo, end;
-  if (!chunk_range(a.group_begin, a.mask, a.chunk_prefix, rk, g, B, lo, end)) return;
+  if (!chunk_range(a.group_begin, a.mask, a.chunk_prefix, rk, g, cy, ny, B, lo, end)) return;
   for (int b0 = lo; b0 < end; b0 += kProjThreads) {
     const int i = b0 + threadIdx.x;
     const bool ok = i < end;
@@ -533,6 +554,26 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
   }
 }
 
+template <class M, bool kWork>
+__global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjArgs a, AdamConsts c,
+                                                                           const float* __restrict__ gsp,
+                                                                           float4* params,
+                                                                           float4* __restrict__ m,
+                                                                           float4* __restrict__ v) {
+  if constexpr (!kWork) {
+    project_bwd_adam_chunk<M>(a, c, gsp, params, m, v, blockIdx.x, blockIdx.y, gridDim.y);
+    return;
+  }
+  // selective Adam over the visible chunks only (the launcher passes the list
+  // only then: dense Adam updates every point)
+  const int n = *a.work_count;
+  for (int w = blockIdx.x; w < n; w += gridDim.x) {
+    const int item = __ldg(a.work_list + w);
+    project_bwd_adam_chunk<M>(a, c, gsp, params, m, v, item / a.max_chunks, item % a.max_chunks, a.max_chunks);
+    __syncthreads();
+  }
+}
+
 // ---- row layout ------------------------------------------------------------
 
 __global__ void __launch_bounds__(1024) scan_counts_kernel(const int32_t* __restrict__ counts, int ng, int B,
@@ -603,6 +644,26 @@ dim3 proj_grid(const bs_proj_desc* d, int n_groups) {
   return dim3(n_groups, chunks);
 }
 
+// The visible-chunk work list applies when the chunk prefixes it indexes are
+// given; the grid-stride launch then uses up to 8 x `ctas_per_sm` CTAs per
+// SM (so a step whose chunks are all visible keeps one CTA per chunk).
+bool use_work(const bs_proj_desc* d) { return d->work_list && d->max_group_points > 0 && d->chunk_prefix; }
+
+void set_work(ProjArgs& a, const bs_proj_desc* d, int n_groups, bool on) {
+  a.max_chunks = (int)proj_grid(d, n_groups).y;
+  a.work_list = on ? d->work_list : nullptr;
+  a.work_count = on ? d->work_count : nullptr;
+}
+
+dim3 work_grid(const bs_proj_desc* d, int n_groups, int ctas_per_sm) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const dim3 full = proj_grid(d, n_groups);
+  const long long total = (long long)full.x * full.y;
+  return dim3((unsigned)std::min<long long>(total, 8ll * ctas_per_sm * sms), 1);
+}
+
 AdamConsts make_adam(const bs_adam_desc* d) {
   AdamConsts c;
   const double bc1 = 1.0 - pow((double)d->beta1, (double)d->step);
@@ -657,14 +718,16 @@ extern "C" int32_t bs_project_fwd(const bs_proj_desc* d, const float* params, in
              view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, d->gsp_zero,
              d->point_gid, d->row_gid, d->row_support, d->view_sp, d->view_gid, d->bucket_counts,
              reinterpret_cast<int4*>(d->row_bin), d->tiles_per_slot};
-  const dim3 grid = proj_grid(d, n_groups);
+  const bool work = use_work(d);
+  set_work(a, d, n_groups, work);
+  const dim3 grid = work ? work_grid(d, n_groups, BS_PROJ_FWD_CTAS) : proj_grid(d, n_groups);
   const size_t smem = sizeof(float4) * 12 * kProjThreads;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, kProjThreads, smem, as_stream(stream)>>>(a, sp_rows);
   };
-  if (d->model == BS_MODEL_2DGS) launch(project_fwd_kernel<Model2>);
-  else launch(project_fwd_kernel<Model3>);
+  if (d->model == BS_MODEL_2DGS) work ? launch(project_fwd_kernel<Model2, true>) : launch(project_fwd_kernel<Model2, false>);
+  else work ? launch(project_fwd_kernel<Model3, true>) : launch(project_fwd_kernel<Model3, false>);
   BS_LAUNCH_CHECK("project_fwd_kernel");
   return BS_OK;
 }
@@ -680,6 +743,7 @@ extern "C" int32_t bs_project_bwd(const bs_proj_desc* d, const float* params, in
   ProjArgs a{d->n_views, n_sh, reinterpret_cast<const float4*>(params), n_points, vis_mask, group_begin, base,
              view_row0, cams, d->gsp_form, d->max_group_points > 0 ? d->chunk_prefix : nullptr, nullptr,
              nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  set_work(a, d, n_groups, false);
   const dim3 grid = proj_grid(d, n_groups);
   if (d->model == BS_MODEL_2DGS)
     project_bwd_kernel<Model2><<<grid, kProjThreads, 0, as_stream(stream)>>>(
@@ -719,15 +783,20 @@ extern "C" int32_t bs_project_bwd_adam(const bs_proj_desc* pd, const bs_adam_des
              nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
              reinterpret_cast<float2*>(pd->densify_stats)};
   AdamConsts c = make_adam(ad);
+  // dense Adam updates every point: the visible-chunk list only with selective Adam
+  const bool work = use_work(pd) && c.selective;
+  set_work(a, pd, n_groups, work);
+  const dim3 grid = work ? work_grid(pd, n_groups, 2) : proj_grid(pd, n_groups);
   const size_t smem = sizeof(float4) * 24 * kProjThreads;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<proj_grid(pd, n_groups), kProjThreads, smem, as_stream(stream)>>>(a, c, g_sp, reinterpret_cast<float4*>(params),
+    kern<<<grid, kProjThreads, smem, as_stream(stream)>>>(a, c, g_sp, reinterpret_cast<float4*>(params),
                                                              reinterpret_cast<float4*>(exp_avg),
                                                              reinterpret_cast<float4*>(exp_avg_sq));
   };
-  if (pd->model == BS_MODEL_2DGS) launch(project_bwd_adam_kernel<Model2>);
-  else launch(project_bwd_adam_kernel<Model3>);
+  if (pd->model == BS_MODEL_2DGS)
+    work ? launch(project_bwd_adam_kernel<Model2, true>) : launch(project_bwd_adam_kernel<Model2, false>);
+  else work ? launch(project_bwd_adam_kernel<Model3, true>) : launch(project_bwd_adam_kernel<Model3, false>);
   BS_LAUNCH_CHECK("project_bwd_adam_kernel");
   return BS_OK;
 }

@@ -175,6 +175,9 @@ class SplatTrainer:
                 raise ValueError("global_ids must be ascending int32-range point indices, one per shard point")
             self.global_ids = torch.as_tensor(gid.astype(np.int32), device=self.dev)
         self.record_row_gid = False  # single rank: also write the rows' global ids (tests)
+        # see _use_work (BS_CHUNK_LIST=0/1 forces it: tuning experiments)
+        self.visible_chunk_list = {"0": False, "1": True}.get(os.environ.get("BS_CHUNK_LIST", ""), "auto")
+        self._last_fill, self._work_on = 0.0, False
         self.presence = self.view_times = None
         if presence is not None:
             pres = np.ascontiguousarray(presence, dtype=np.float32)
@@ -263,6 +266,28 @@ class SplatTrainer:
         return _T()
 
     # ------------------------------------------------------------------ step
+    def _work_list(self):
+        return self.buf.get("work_list", max(self.n_groups * self.max_chunks, 1), torch.int32)
+
+    def _work_count(self):
+        return self.buf.get("work_count", 1, torch.int32)
+
+    def _use_work(self):
+        """Visible-chunk work list (culling -> projection kernels): on when the
+        previous step projected under half of its (point, view) pairs -- a
+        sparse step (C4: ~2 %), where one CTA per (group, chunk) mostly
+        launches empty CTAs; off for dense steps (C2: every point in every
+        view), where the listing and the shuffled chunk order cost ~20 us.
+        `visible_chunk_list` = True / False forces it.  Same results."""
+        if self.visible_chunk_list != "auto":
+            return bool(self.visible_chunk_list)
+        return self._last_fill < 0.5
+
+    def _set_work(self, pdesc):
+        """Projection descriptor: visit only the chunks the step's culling listed."""
+        if self.max_group > 0 and self._work_on:
+            pdesc.work_list, pdesc.work_count = nat.ptr(self._work_list()), nat.ptr(self._work_count())
+
     def _wait_gt(self):
         """The compute stream waits for the caller's ground-truth upload (once)."""
         if getattr(self, "_gt_ready", None) is not None:
@@ -293,12 +318,19 @@ class SplatTrainer:
         temporal = self.presence is not None
         times = self._select_views(batch_ids, self.view_times, "times_sel" + tag) if temporal else None
         desc = nat.CullDesc(nat.CULL_MASK, B, self.P, 1, 1 if temporal else 0, 4, self.max_chunks, nat.ptr(chunk_prefix))
+        if not tag:
+            self._work_on = chunk_prefix is not None and self.max_group > 0 and self._use_work()
         nat.call("bs_cull_count", desc, nat.ptr(self.params), self.S, nat.ptr(self.presence),
                  nat.ptr(self.group_begin), nat.ptr(self.aabb), self.n_groups, nat.ptr(planes), nat.ptr(times),
                  None, nat.ptr(mask), nat.ptr(counts), nat.ptr(patch_counts), st)
         order = np.arange(B, dtype=np.int32)
         nat.call("bs_scan_counts", nat.ptr(counts), self.n_groups, B, order.ctypes.data, nat.ptr(base),
                  nat.ptr(view_rows), nat.ptr(view_row0), st)
+        if not tag and self._work_on:
+            # the chunks with a visible point, for the projection kernels'
+            # grid-stride loops (bs_proj_desc.work_list)
+            nat.call("bs_list_chunks", nat.ptr(counts), nat.ptr(chunk_prefix), nat.ptr(self.group_begin),
+                     self.n_groups, self.max_chunks, B, nat.ptr(self._work_list()), nat.ptr(self._work_count()), st)
 
     def step(self, batch_ids, gt_batch: torch.Tensor | None = None, next_batch=None, gt_ready=None):
         """One training step over `batch_ids` (indices into self.views).
@@ -352,6 +384,7 @@ class SplatTrainer:
                              nat.ptr(chunk_prefix))
         pdesc.point_gid = nat.ptr(self.global_ids)
         pdesc.densify_stats = nat.ptr(self.densify_stats)
+        self._set_work(pdesc)
         early = self.comm is None and S * B * self.sp_floats * 4 <= self.sp_capacity_bytes
         row_gid = None
         if self.comm is not None or self.record_row_gid:
@@ -402,6 +435,7 @@ class SplatTrainer:
                 view_row0.copy_(torch.as_tensor(row0))
             self.last.update(A=A, W=W, layout=lay)
         n_rows = int(rows_host.sum())
+        self._last_fill = n_rows / max(1, S * B)
         self.last["rows_per_view"] = rows_host.copy()
         peer = None
         if lay is not None and getattr(self.comm, "peer", False):
@@ -509,11 +543,13 @@ class SplatTrainer:
             W = comm.assign(A, key=tuple(int(v) for v in batch_ids))  # patch -> rank (prefetched when given)
         rows_host = view_rows.cpu().numpy()
         n_rows = int(rows_host.sum())
+        self._last_fill = n_rows / max(1, S * B)
         self.last.update(A=A, W=W, rows_per_view=rows_host.copy())
         sp = self.buf.get("sp", max(n_rows, 1) * self.sp_floats, torch.float32)
         pdesc = nat.ProjDesc(B, self.sh_degree, self.tiles_x, self.tiles_y, self.model_id, self.max_group, 0,
                              nat.ptr(chunk_prefix))
         pdesc.densify_stats = nat.ptr(self.densify_stats)
+        self._set_work(pdesc)
         row_gid = self.buf.get("row_gid", max(n_rows, 1), torch.int32)
         pdesc.point_gid, pdesc.row_gid = nat.ptr(self.global_ids), nat.ptr(row_gid)
         with self._t("project"):

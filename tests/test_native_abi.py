@@ -68,10 +68,11 @@ def test_host_library_exports_every_declared_symbol():
 def test_proj_desc_layout():
     # bs_proj_desc: 7 int32 (n_views, sh_degree, tiles_x_max, tiles_y_max, model, max_group_points, gsp_form)
     # + pad + 9 pointers (chunk_prefix, gsp_zero, point_gid, row_gid, row_support, view_sp, view_gid,
-    # bucket_counts, row_bin) + int32 tiles_per_slot + pad + densify_stats
+    # bucket_counts, row_bin) + int32 tiles_per_slot + pad + densify_stats, work_list, work_count
     assert _native.ProjDesc.view_gid.offset == 80 and _native.ProjDesc.row_bin.offset == 96
     assert _native.ProjDesc.tiles_per_slot.offset == 104 and _native.ProjDesc.densify_stats.offset == 112
-    assert ctypes.sizeof(_native.ProjDesc) == 120
+    assert _native.ProjDesc.work_list.offset == 120 and _native.ProjDesc.work_count.offset == 128
+    assert ctypes.sizeof(_native.ProjDesc) == 136
     # bs_densify_desc: int32 model, 4 f32, uint32 seed
     assert ctypes.sizeof(_native.DensifyDesc) == 24 and _native.DensifyDesc.seed.offset == 20
     assert _native.ProjDesc.row_gid.offset == 56 and _native.ProjDesc.row_support.offset == 64
