@@ -414,7 +414,9 @@ int32_t bs_raster_bwd(const bs_raster_desc* desc_host, const float* sp_rows,
  * the forward's outputs and loss partials of bs_raster_fwd (loss fused, gt
  * required) and the G_SP of bs_raster_bwd with grad_image == NULL, without
  * re-walking the tile lists from global memory (each warp keeps its
- * forward's filtered splat list in shared memory; see csrc/raster.cu). */
+ * forward's filtered splat list in shared memory; see csrc/raster.cu).
+ * final_T and n_contrib may be NULL (the fused backward does not read them;
+ * the training step skips their 8 B per pixel unless asked to keep them). */
 int32_t bs_raster_fwd_bwd(const bs_raster_desc* desc_host, const float* sp_rows,
                           const uint32_t* inst_rows, const int32_t* ranges,
                           float* image, float* final_T, int32_t* n_contrib,

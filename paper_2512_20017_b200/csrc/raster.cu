@@ -725,12 +725,17 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
                : "memory");
   return v;
 }
+__device__ __forceinline__ float2 lds64(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+  return v;
+}
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 struct KeptRec {
-  float4 a, b, c;  // as Staged; c.w = range-relative index (int bits)
+  float4 a, b, c;  // as Staged; c.w = the lanes the forward blended the splat into (written after its blend)
 };
 
 // the reduction of one splat's 9 terms over the warp into its G_SP row:
@@ -819,8 +824,7 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
       KeptRec& r = rk[__popc(bits & ((1u << lane) - 1u))];
       r.a = make_float4(f.p0.x, f.p0.y, __fmul_rn(f.p0.w, kHalfLog2e), __fmul_rn(f.p1.y, kHalfLog2e));
       r.b = make_float4(__fmul_rn(f.p1.x, -kLog2e), f.p0.z, f.p1.z, f.p1.w);
-      r.c = make_float4(f.b, kSup ? f.th2 : support_p2(f.p0.z), __uint_as_float(f.row),
-                        __int_as_float(b0 + lane - rg.x));
+      r.c = make_float4(f.b, kSup ? f.th2 : support_p2(f.p0.z), __uint_as_float(f.row), 0.f);  // c.w: the mask
     }
     fetch_row_data(f, sp, sup, row_next, b0 + 32 + lane < rg.y);
     row_next = fetch_row(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
@@ -828,13 +832,18 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
     // explicit shared-space addresses: the three record loads stay together
     // ahead of the per-pixel branch, and the address is one add per splat
     uint32_t ra = (uint32_t)__cvta_generic_to_shared(rk);
+    uint32_t rest = bits;  // staging lanes of the records still to blend: record k came from lane ffs(rest) - 1
     for (int k = 0; k < nb; ++k, ra += (uint32_t)sizeof(KeptRec)) {
-      const float4 sa = lds128(ra), sb = lds128(ra + 16), sc = lds128(ra + 32);
+      // c.w is not read here: lane 0 writes the record's mask into it below
+      const float4 sa = lds128(ra), sb = lds128(ra + 16);
+      const float2 sc = lds64(ra + 32);
+      const int rel = b0 + __ffs(rest) - 1 - rg.x;  // range-relative index of the splat
+      rest &= rest - 1u;
 #if BS_FUSED_FWD_SEL
-      const bool blended = blend_pred(pf, sa, sb, sc.x, sc.y, npx, __float_as_int(sc.w));
+      const bool blended = blend_pred(pf, sa, sb, sc.x, sc.y, npx, rel);
 #else
       bool blended = false;
-      if (!pf.done) blended = blend_sel(pf, sa, sb, sc.x, sc.y, npx, __float_as_int(sc.w));
+      if (!pf.done) blended = blend_sel(pf, sa, sb, sc.x, sc.y, npx, rel);
 #endif
       // the pixels this splat was blended into: exactly the pairs the backward
       // differentiates (rel < n_contrib and inside the support).  (Keeping
@@ -872,8 +881,8 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
     image[3 * pix] = o0;
     image[3 * pix + 1] = o1;
     image[3 * pix + 2] = o2;
-    final_T[pix] = pf.T;
-    n_contrib[pix] = pf.contrib;
+    if (final_T) final_T[pix] = pf.T;
+    if (n_contrib) n_contrib[pix] = pf.contrib;
     const int gv = gt_view ? gt_view[slot] : slot;
     const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + q.py0) * a.W + q.px);
     const float d0 = o0 - gp[0] * (1.f / 255.f), d1 = o1 - gp[1] * (1.f / 255.f), d2 = o2 - gp[2] * (1.f / 255.f);

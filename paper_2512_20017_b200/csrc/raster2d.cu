@@ -563,13 +563,16 @@ __global__ void __launch_bounds__(kT2, BS_FUSED2_CTAS) raster2d_fused_kernel(
     if (keep) {
       const int pos = base + __popc(bits & ((1u << lane) - 1u));
       stage2_rec(f, x0, y0, a.support != nullptr, kp.rec[pos]);
-      kp.idx[pos] = make_int2((int)f.row, b0 + lane - rg.x);
+      kp.idx[pos] = make_int2((int)f.row, 0);  // .y: the mask, written after the blend
     }
     fetch2_row(f, sp, a.support, row_next, b0 + 32 + lane < rg.y);
     row_next = row2(inst_rows, b0 + 64 + lane, b0 + 64 + lane < rg.y);
     __syncwarp();
+    uint32_t rest = bits;  // staging lanes of the records still to blend
     for (int k = 0; k < nb; ++k) {
       const int pos = base + k;
+      const int rel = b0 + __ffs(rest) - 1 - rg.x;  // range-relative index (idx.y is not read here)
+      rest &= rest - 1u;
       Eval2 e;
       const float4 sa = kp.rec[pos][0];
       const float4 col = kp.rec[pos][3];
@@ -586,7 +589,7 @@ __global__ void __launch_bounds__(kT2, BS_FUSED2_CTAS) raster2d_fused_kernel(
       p.c1 = c ? __fmaf_rn(col.y, wgt, p.c1) : p.c1;
       p.c2 = c ? __fmaf_rn(col.z, wgt, p.c2) : p.c2;
       p.T = c ? nT : p.T;
-      p.contrib = c ? kp.idx[pos].y + 1 : p.contrib;
+      p.contrib = c ? rel + 1 : p.contrib;
       // the lanes this splat was blended into = the pairs the backward
       // differentiates; replaces the range-relative index in the record
       const uint32_t who = __ballot_sync(0xffffffffu, c);
@@ -629,8 +632,8 @@ __global__ void __launch_bounds__(kT2, BS_FUSED2_CTAS) raster2d_fused_kernel(
     image[3 * pix] = o0;
     image[3 * pix + 1] = o1;
     image[3 * pix + 2] = o2;
-    final_T[pix] = p.T;
-    n_contrib[pix] = p.contrib;
+    if (final_T) final_T[pix] = p.T;
+    if (n_contrib) n_contrib[pix] = p.contrib;
     const int gv = gt_view ? gt_view[slot] : slot;
     const uint8_t* gp = gt + 3 * (((int64_t)gv * a.H + py) * a.W + px);
     const float d0 = o0 - gp[0] * (1.f / 255.f), d1 = o1 - gp[1] * (1.f / 255.f), d2 = o2 - gp[2] * (1.f / 255.f);

@@ -177,6 +177,10 @@ class SplatTrainer:
         self.record_row_gid = False  # single rank: also write the rows' global ids (tests)
         # see _use_work (BS_CHUNK_LIST=0/1 forces it: tuning experiments)
         self.visible_chunk_list = {"0": False, "1": True}.get(os.environ.get("BS_CHUNK_LIST", ""), "auto")
+        # the fused raster's per-pixel transmittance / contributor count
+        # (last["final_T"], last["n_contrib"]): not needed by the step, written
+        # only when asked for (8 B per pixel; the separate kernels always write them)
+        self.keep_raster_aux = False
         self._last_fill, self._work_on = 0.0, False
         self.presence = self.view_times = None
         if presence is not None:
@@ -896,8 +900,10 @@ class SplatTrainer:
         if self.raster_fused and (self.model == "2dgs" or self.pixels_per_lane == 1):
             # K3 + L + K4 in one launch: each warp keeps its forward's splat list in shared memory
             with self._t("raster"):
-                nat.call("bs_raster2d_fwd_bwd" if self.model == "2dgs" else "bs_raster_fwd_bwd", rdesc, nat.ptr(sp), nat.ptr(irows), nat.ptr(ranges), nat.ptr(image),
-                         nat.ptr(final_T), nat.ptr(n_contrib), nat.ptr(gt), nat.ptr(gt_map), nat.ptr(loss_tiles),
+                aux = self.keep_raster_aux
+                nat.call("bs_raster2d_fwd_bwd" if self.model == "2dgs" else "bs_raster_fwd_bwd", rdesc, nat.ptr(sp),
+                         nat.ptr(irows), nat.ptr(ranges), nat.ptr(image), nat.ptr(final_T) if aux else None,
+                         nat.ptr(n_contrib) if aux else None, nat.ptr(gt), nat.ptr(gt_map), nat.ptr(loss_tiles),
                          nat.ptr(gsp), st)
             nat.call("bs_reduce_loss_tiles", nat.ptr(loss_tiles), n_slots, self.tiles, self.H, self.W,
                      nat.ptr(losses), st)

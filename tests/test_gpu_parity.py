@@ -342,6 +342,7 @@ def test_c2_scale_properties(cuda):
     gt = scenes.synthetic_gt(1, 8, 1920, 1080)
     gb = g.group_begin()
     tr = SplatTrainer(params, gb, g.aabbs.reshape(-1, 6), ds.views, gt=gt)
+    tr.keep_raster_aux = True  # the fused raster's T is read below
     batch = [0, 3, 4, 7]
     losses = tr.step(batch).cpu().numpy()
     n, I = tr.last["n_rows"], tr.last["n_inst"]

@@ -22,6 +22,7 @@ REL = 1e-5
 def _run(make, batch, fused):
     tr = make()
     tr.raster_fused = fused
+    tr.keep_raster_aux = True  # T and n_contrib compared below
     losses = tr.step(batch).cpu().numpy()
     n = tr.last["n_rows"]
     npx = len(batch) * tr.H * tr.W
@@ -79,3 +80,20 @@ def test_fused_matches_two_kernels_c3(cuda):
     err = _compare(lambda: SplatTrainer(params, g.group_begin(), g.aabbs.reshape(-1, 6), ds.views, gt=gt,
                                         model="2dgs"), [1, 2, 5, 6])
     print("C3 G_SP max rel diff per component", err.max())
+
+
+def test_fused_without_aux_outputs_c1(cuda):
+    """The training step's default skips the fused kernel's T / n_contrib
+    stores (8 B per pixel); image, losses and G_SP are unaffected."""
+    ds, params, gb, aabb, gt = c1_setup()
+    outs = []
+    for aux in (True, False):
+        tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt, sh_degree=3)
+        tr.keep_raster_aux = aux
+        losses = tr.step([0, 2, 5, 7]).cpu().numpy()
+        n, npx = tr.last["n_rows"], 4 * tr.H * tr.W
+        outs.append((losses, tr.last["image"][: npx * 3].cpu().numpy(),
+                     tr.last["gsp"][: n * tr.gsp_floats].cpu().numpy().reshape(n, -1)))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    scale = np.abs(outs[0][2]).max(axis=0) + 1e-30
+    assert ((np.abs(outs[0][2] - outs[1][2]) / scale).max() <= REL)

@@ -214,6 +214,7 @@ def _gpu_step(points, bg=(0.0, 0.0, 0.0)):
     gt = np.zeros((1, H, W, 3), dtype=np.uint8)
     tr = SplatTrainer(params, np.array([0, n], dtype=np.int32), aabb, [_view()], gt=gt, bg=bg,
                       adam=AdamConfig(np.zeros(60, dtype=np.float32)))
+    tr.keep_raster_aux = True  # T is checked against the closed form
     losses = tr.step([0]).cpu().numpy()
     return tr, losses
 
