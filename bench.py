@@ -245,19 +245,22 @@ _STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_ke
                  "raster2d_bwd": "raster2d_bwd_kernel", "raster2d_fwd": "raster2d_fwd_kernel",
                  "project_bwd_adam": "project_bwd_adam_kernel", "project": "project_fwd_kernel", "cull": "cull_kernel"}
 
-# committed ncu --set full summaries (newest first); each names the
-# configuration it captured per model (tools/gpu_profile.sh)
-TRAFFIC_FILES = ("r2g_kernel_traffic.json", "r2_kernel_traffic.json", "r1_kernel_traffic.json")
+# committed ncu --set full summaries (newest first) per (model, configuration)
+# they captured (per launch of that workload: counts and bytes do not transfer)
+TRAFFIC_FILES = {("3dgs", "c2"): ("r2y_kernel_traffic.json", "r2g_kernel_traffic.json", "r2_kernel_traffic.json",
+                                  "r1_kernel_traffic.json"),
+                 ("2dgs", "c3"): ("r2y_kernel_traffic.json", "r2g_kernel_traffic.json", "r2_kernel_traffic.json",
+                                  "r1_kernel_traffic.json"),
+                 ("3dgs", "c4"): ("r2y_kernel_traffic_c4.json",)}
 _PROFILED = {"3dgs": "c2", "2dgs": "c3"}
 
 
 def kernel_profile(stage, model="3dgs", config=None):
     """Entry of the newest committed ncu --set full summary (profiles/) for
-    one launch of the stage's kernel, or {} when that capture is not of this
-    configuration (counts and bytes are per launch of that workload)."""
-    if config is not None and _PROFILED.get(model) != config:
-        return {}
-    for name in TRAFFIC_FILES:
+    one launch of the stage's kernel, or {} when no capture of this
+    configuration is committed (counts and bytes are per launch of that workload)."""
+    files = TRAFFIC_FILES.get((model, config if config is not None else _PROFILED.get(model)), ())
+    for name in files:
         try:
             table = json.load(open(os.path.join(ROOT, "profiles", name)))
         except Exception:

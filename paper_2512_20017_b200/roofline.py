@@ -111,11 +111,14 @@ def issue(warp_instructions: float | None, ms: float, sm_mhz: float | None) -> d
             "frac": round(ach / peak, 4), "warp_instructions": warp_instructions}
 
 
-def binding(h: dict | None, i: dict | None) -> str:
-    """The bound a kernel actually sits against: the larger fraction."""
+def binding(h: dict | None, i: dict | None) -> str | None:
+    """The bound a kernel actually sits against: the larger fraction (None when
+    the issue rate was not captured for this workload and the HBM fraction is
+    too low to call the kernel memory-bound)."""
     hf = (h or {}).get("frac") or 0.0
-    if_ = (i or {}).get("frac") or 0.0
-    return "issue" if if_ > hf else "hbm"
+    if i is None or i.get("frac") is None:
+        return "hbm" if hf >= 0.5 else None
+    return "issue" if i["frac"] > hf else "hbm"
 
 
 def peaks(root: str) -> tuple[float, str]:

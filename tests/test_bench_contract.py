@@ -69,3 +69,4 @@ def test_roofline_model():
     h = rl.hbm(parts["raster_bwd"], 1.9, 6539.5)
     i = rl.issue(1.6e9, 1.9, 1965.0)
     assert rl.binding(h, i) == "issue" and rl.binding(rl.hbm(1.5e9, 0.3, 6539.5), None) == "hbm"
+    assert rl.binding(h, None) is None  # issue rate not captured and far from the HBM bound: not called
