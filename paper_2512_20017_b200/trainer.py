@@ -233,7 +233,6 @@ class SplatTrainer:
         self.group_keys = keys
         # per-view device tables the batch's rows are selected from (the view
         # ids travel as kernel parameters: csrc/views.cu)
-        self._view_iota = torch.arange(len(self.views), dtype=torch.int64, device=self.dev)
         self._gt_index = (self.gt_lut if self.gt_lut is not None
                           else torch.arange(len(self.views), dtype=torch.int32, device=self.dev))
         # N = 1: the splat buffer is sized for every point in every batch view
@@ -310,10 +309,6 @@ class SplatTrainer:
                  nat.ptr(out), nat.stream_handle())
         return out
 
-    def _device_ids(self, ids, name):
-        """Batch indices as a device int64 tensor (selected from an identity
-        table: no host-to-device copy)."""
-        return self._select_views(ids, self._view_iota, name)
 
     def _cull_counts(self, batch_ids, mask, counts, base, view_rows, view_row0, st, patch_counts=None,
                      chunk_prefix=None, tag=""):
