@@ -55,3 +55,47 @@ def test_work_list_matches_one_cta_per_chunk(cuda, model, selective, G, batch):
         for p_after, m_after in ((a[1], a[2]), (b[1], b[2])):
             assert np.array_equal(p_after[:, hidden], a[3][:, hidden])
             assert not m_after[:, hidden].any()
+
+
+def test_list_chunks_matches_counts(cuda):
+    """bs_list_chunks: exactly the (group, chunk) pairs whose chunk holds a
+    point visible in some view, from the culling's counts / chunk prefixes."""
+    ds, params, gb, aabb, gt = c1_setup(G=1000)
+    tr = SplatTrainer(params, gb, aabb, ds.views, gt=gt)
+    tr.visible_chunk_list = True
+    tr.step([0, 5])
+    torch.cuda.synchronize()
+    mask = tr.buf.bufs["mask"][: tr.S].cpu().numpy()
+    gbh = np.asarray(gb, dtype=np.int64)
+    want = set()
+    for g in range(len(gbh) - 1):
+        for c in range(tr.max_chunks):
+            lo, hi = gbh[g] + 256 * c, min(gbh[g + 1], gbh[g] + 256 * (c + 1))
+            if lo < hi and mask[lo:hi].any():
+                want.add(g * tr.max_chunks + c)
+    n = int(tr.buf.bufs["work_count"].cpu().numpy()[0])
+    got = tr.buf.bufs["work_list"][:n].cpu().numpy()
+    assert len(got) == len(set(got.tolist())) and set(got.tolist()) == want
+
+
+def test_select_rows_and_copy_to_host(cuda):
+    """bs_select_rows (view ids as kernel parameters) and bs_copy_to_host (a
+    kernel store into mapped pinned memory) against torch."""
+    from paper_2512_20017_b200 import _native as nat
+
+    table = torch.arange(40 * 7, dtype=torch.float32, device="cuda").reshape(40, 7)
+    ids = np.array([3, 39, 0, 3, 17], dtype=np.int32)
+    out = torch.empty((5, 7), dtype=torch.float32, device="cuda")
+    nat.call("bs_select_rows", ids.ctypes.data, 5, nat.ptr(table), 40, 28, nat.ptr(out), nat.stream_handle())
+    assert torch.equal(out, table[torch.as_tensor(ids.astype(np.int64), device="cuda")])
+    with pytest.raises(Exception):
+        bad = np.array([40], dtype=np.int32)
+        nat.call("bs_select_rows", bad.ctypes.data, 1, nat.ptr(table), 40, 28, nat.ptr(out), nat.stream_handle())
+    src = torch.arange(9, dtype=torch.int64, device="cuda") * 1000003
+    pin = torch.zeros(9, dtype=torch.int64, pin_memory=True)
+    nat.call("bs_copy_to_host", nat.ptr(src), 72, pin.data_ptr(), nat.stream_handle())
+    torch.cuda.synchronize()
+    assert torch.equal(pin, src.cpu())
+    with pytest.raises(Exception):  # pageable host memory is refused
+        nat.call("bs_copy_to_host", nat.ptr(src), 72, torch.zeros(9, dtype=torch.int64).data_ptr(),
+                 nat.stream_handle())
