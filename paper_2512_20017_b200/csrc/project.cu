@@ -262,7 +262,7 @@ __device__ __forceinline__ void project_fwd_chunk(const ProjArgs& a, float* __re
         }
       }
     }
-    rk.advance(B);
+    if (b0 + kProjThreads < end) rk.advance(B);  // (a chunk's single round needs no advance)
   }
 }
 
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kProjThreads) project_bwd_kernel(ProjArgs a, c
         gparams[p * a.S + i] = acc;
       }
     }
-    rk.advance(B);
+    if (b0 + kProjThreads < end) rk.advance(B);  // (a chunk's single round needs no advance)
   }
 }
 
@@ -550,7 +550,7 @@ __device__ __forceinline__ void project_bwd_adam_chunk(const ProjArgs& a, const 
         }
       }
     }
-    rk.advance(B);
+    if (b0 + kProjThreads < end) rk.advance(B);  // (a chunk's single round needs no advance)
   }
 }
 
