@@ -34,7 +34,7 @@ constexpr float kAMax = 0.99f;
 constexpr float kTStop = 1e-4f;
 constexpr float kLog2e2 = 1.4426950408889634f;
 #ifndef BS_SPARSE2_LANES
-#define BS_SPARSE2_LANES 12  // swept on B200 (C3, 128-bit REDs): 5 5.74, 8 5.53, 12 5.38, 16 5.41 ms
+#define BS_SPARSE2_LANES 9  // re-swept on the fused kernel (C3 raster ms): 5 6.73, 7 6.53, 9 6.50, 12 6.57, 16 6.84
 #endif
 #ifndef BS_R2_FWD_CTAS
 #define BS_R2_FWD_CTAS 4
