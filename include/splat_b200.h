@@ -113,6 +113,11 @@ typedef struct {
 int32_t bs_select_rows(const int32_t* ids, int32_t n, const void* src,
                        int64_t n_src_rows, int64_t row_bytes, void* dst,
                        void* stream);
+/* n_bytes (a multiple of 4) of host memory (any: read at the call) into
+ * device memory, as kernel parameters, stream-ordered: the step's small
+ * per-step tables (row offsets, slot lists, owners) without a copy engine
+ * or a stream synchronisation */
+int32_t bs_upload(const void* host, int64_t n_bytes, void* dst, void* stream);
 /* n_bytes (a multiple of 4) from device memory into pinned host memory
  * (cudaHostAlloc / torch pin_memory), stream-ordered */
 int32_t bs_copy_to_host(const void* src, int64_t n_bytes, void* dst_pinned,

@@ -95,6 +95,7 @@ _SIGS = {
     "bs_select_rows": (_I32, [_P, _I32, _P, _I64, _I64, _P, _P]),
     "bs_list_chunks": (_I32, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
     "bs_copy_to_host": (_I32, [_P, _I64, _P, _P]),
+    "bs_upload": (_I32, [_P, _I64, _P, _P]),
     "bs_cull_count": (_I32, [C.POINTER(CullDesc), _P, _I64, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "bs_bbox": (_I32, [_P, _I64, _I32, _P, _P, _SZ, _P]),
     "bs_bbox_workspace": (_SZ, [_I64]),
@@ -223,6 +224,18 @@ def call(name: str, *args) -> None:
     st = getattr(lib, name)(*args)
     if st != 0:
         raise_for_status(st, lib.bs_last_error().decode(errors="replace"))
+
+
+def upload(arr, out) -> "object":
+    """Small host array -> device tensor `out` (its first arr.nbytes bytes) by
+    bs_upload: kernel parameters, stream-ordered, no copy engine and no stream
+    synchronisation (a pageable torch copy synchronises).  Returns `out`."""
+    import numpy as np
+
+    a = np.ascontiguousarray(arr)
+    if a.nbytes:
+        call("bs_upload", a.ctypes.data, a.nbytes, out.data_ptr(), stream_handle())
+    return out
 
 
 def ptr(t) -> int | None:

@@ -1,5 +1,6 @@
 // Per-step view selection and the step's small host transfers, without the
-// copy engines.  A step needs a handful of per-view rows on the device (the
+// copy engines (and without the stream synchronisation a pageable
+// host-to-device copy implies).  A step needs a handful of per-view rows on the device (the
 // batch's cameras, frustum planes, view times, ground-truth indices; Alg. 1
 // line 3) and returns a few integers to the host (the per-view
 // row counts C[v]_k that size the render buffers, the instance count).  As
@@ -29,6 +30,16 @@ __global__ void select_rows_kernel(SelIds s, const uint32_t* __restrict__ src, i
     const int64_t k = t / row_words, w = t - k * row_words;
     dst[t] = src[(int64_t)s.ids[k] * row_words + w];
   }
+}
+
+// A small host array as a kernel parameter (kUploadWords words per launch).
+constexpr int kUploadWords = 512;  // 2 KB: inside the classic 4 KB parameter limit
+struct UploadBlob {
+  uint32_t w[kUploadWords];
+};
+
+__global__ void upload_kernel(UploadBlob b, int n_words, uint32_t* __restrict__ dst) {
+  for (int t = threadIdx.x; t < n_words; t += blockDim.x) dst[t] = b.w[t];
 }
 
 __global__ void copy_words_kernel(const uint32_t* __restrict__ src, int64_t n_words, uint32_t* dst) {
@@ -72,5 +83,20 @@ extern "C" int32_t bs_copy_to_host(const void* src, int64_t n_bytes, void* dst_p
   copy_words_kernel<<<(int)std::min<int64_t>((words + 255) / 256, 1024), 256, 0, as_stream(stream)>>>(
       static_cast<const uint32_t*>(src), words, static_cast<uint32_t*>(at.devicePointer));
   BS_LAUNCH_CHECK("copy_words_kernel");
+  return BS_OK;
+}
+
+extern "C" int32_t bs_upload(const void* host, int64_t n_bytes, void* dst, void* stream) {
+  BS_REQUIRE(n_bytes >= 0 && n_bytes % 4 == 0, BS_ERR_PARAMETER, "upload: size must be a multiple of 4");
+  BS_REQUIRE(n_bytes == 0 || (host != nullptr && dst != nullptr), BS_ERR_PARAMETER, "upload: null pointer");
+  const uint32_t* src = static_cast<const uint32_t*>(host);
+  uint32_t* out = static_cast<uint32_t*>(dst);
+  for (int64_t w0 = 0; w0 < n_bytes / 4; w0 += kUploadWords) {
+    const int n = (int)std::min<int64_t>(kUploadWords, n_bytes / 4 - w0);
+    UploadBlob b;
+    memcpy(b.w, src + w0, sizeof(uint32_t) * n);
+    upload_kernel<<<1, 256, 0, as_stream(stream)>>>(b, n, out + w0);
+    BS_LAUNCH_CHECK("upload_kernel");
+  }
   return BS_OK;
 }

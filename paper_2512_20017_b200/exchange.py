@@ -406,7 +406,15 @@ class PeerExchange(SplatExchange):
         dst = np.array([self.peers[r] + offs[r][2] for r in range(N)], dtype=np.int64)
         host = np.concatenate([view_sp, view_gid, dst, np.asarray(seg_dst0, dtype=np.int64),
                                np.asarray(seg_src, dtype=np.int64)])
-        dev = torch.as_tensor(host, device=self.dev)
+        # kernel-parameter upload (bs_upload): no stream synchronisation per
+        # step; two alternating buffers, as a step's plan may still be read
+        # by the previous step's kernels when the next one is queued
+        self._plan_k = 1 - getattr(self, "_plan_k", 0)
+        bufs = getattr(self, "_plan_bufs", [None, None])
+        if bufs[self._plan_k] is None or bufs[self._plan_k].numel() < host.size:
+            bufs[self._plan_k] = torch.empty(max(host.size, 256), dtype=torch.int64, device=self.dev)
+        self._plan_bufs = bufs
+        dev = self._nat.upload(host.astype(np.int64), bufs[self._plan_k][: host.size])
         n_segs = len(seg_src)
         return {"view_sp": dev[:B], "view_gid": dev[B:2 * B], "dst": dev[2 * B:2 * B + N],
                 "seg_dst0": dev[2 * B + N:2 * B + N + n_segs],

@@ -291,6 +291,12 @@ class SplatTrainer:
         if self.max_group > 0 and self._work_on:
             pdesc.work_list, pdesc.work_count = nat.ptr(self._work_list()), nat.ptr(self._work_count())
 
+    def _up(self, arr, name, dtype):
+        """Small per-step host table -> reused device buffer (bs_upload: no
+        copy engine, no stream synchronisation)."""
+        a = np.ascontiguousarray(arr, dtype={torch.int64: np.int64, torch.int32: np.int32}[dtype])
+        return nat.upload(a, self.buf.get(name, max(a.size, 1), dtype)[: a.size])
+
     def _wait_gt(self):
         """The compute stream waits for the caller's ground-truth upload (once)."""
         if getattr(self, "_gt_ready", None) is not None:
@@ -431,7 +437,7 @@ class SplatTrainer:
                 rows_host = A[:, self.comm.rank].copy()
                 row0 = np.zeros(B, dtype=np.int64)
                 row0[lay.order] = np.concatenate([[0], np.cumsum(rows_host[lay.order])[:-1]])
-                view_row0.copy_(torch.as_tensor(row0))
+                nat.upload(row0, view_row0)
             self.last.update(A=A, W=W, layout=lay)
         n_rows = int(rows_host.sum())
         self._last_fill = n_rows / max(1, S * B)
@@ -473,13 +479,13 @@ class SplatTrainer:
                 else:
                     sp_recv = self.comm.forward(sp[: n_rows * self.sp_floats], lay, self.sp_floats).reshape(-1)
                     gid_recv = self.comm.forward_ids(row_gid[:n_rows], lay)
-            mine = torch.as_tensor(lay.my_views, device=dev)
+            mine = self._up(lay.my_views, "mine", torch.int64)
             n_slots = len(lay.my_views)
             self.last["loss_views"] = [int(v) for v in lay.my_views]
             # received rows in canonical order: per rendered view, ascending global id
             slot_rows = np.bincount(lay.seg_slot, weights=lay.seg_rows, minlength=n_slots).astype(np.int64)
             sp_c, order = self._canonical(sp_recv, gid_recv, lay.n_recv, lay.seg_rows, lay.seg_slot, n_slots)
-            seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(slot_rows)[:-1]]).astype(np.int64), device=dev)
+            seg_row0 = self._up(np.concatenate([[0], np.cumsum(slot_rows)[:-1]]), "seg_row0", torch.int64)
             seg_slot = self._slot_ids(n_slots)
             gt_slots = None
             if gt_batch is not None:
@@ -493,8 +499,8 @@ class SplatTrainer:
                 wire = self.gsp_wire_floats
                 if peer is not None:
                     # each canonical row straight into its owner's send-layout slot
-                    seg_row0_r = torch.as_tensor(np.concatenate([[0], np.cumsum(lay.seg_rows)[:-1]]).astype(np.int64),
-                                                 device=dev)
+                    seg_row0_r = self._up(np.concatenate([[0], np.cumsum(lay.seg_rows)[:-1]]), "seg_row0_r",
+                                          torch.int64)
                     nat.call("bs_return_rows", nat.ptr(gsp_c), self.gsp_floats, wire, nat.ptr(order), lay.n_recv,
                              nat.ptr(seg_row0_r), nat.ptr(peer["seg_src"]), nat.ptr(peer["seg_dst0"]), peer["n_segs"],
                              nat.ptr(peer["dst"]), self.gsp_floats, st)
@@ -555,7 +561,7 @@ class SplatTrainer:
             nat.call("bs_project_fwd", pdesc, nat.ptr(self.params), S, nat.ptr(mask), nat.ptr(self.group_begin),
                      self.n_groups, nat.ptr(base), nat.ptr(view_row0), nat.ptr(cams), nat.ptr(sp), st)
         # ---- render sets -> send layout (destination, view, row)
-        owner = torch.as_tensor(np.asarray(W, dtype=np.int32), device=dev)
+        owner = self._up(W, "owner", torch.int32)
         dmask = self.buf.get("dest_mask", max(n_rows, 1), torch.int32)
         nat.call("bs_row_dest_mask", nat.ptr(sp), self.model_id, n_rows, nat.ptr(view_row0), B, P, self.W, self.H,
                  nat.ptr(owner), nat.ptr(dmask), st)
@@ -566,7 +572,7 @@ class SplatTrainer:
                  None, nat.ptr(ws), ws.numel(), st)
         send_rows = [int(x) for x in totals.cpu().tolist()]
         n_send = sum(send_rows)
-        base_d = torch.as_tensor(np.concatenate([[0], np.cumsum(send_rows)[:-1]]).astype(np.int64), device=dev)
+        base_d = self._up(np.concatenate([[0], np.cumsum(send_rows)[:-1]]), "base_d", torch.int64)
         send_idx = self.buf.get("send_idx", max(n_send, 1), torch.int64)
         vcounts = self.buf.get("dest_view_counts", N * B, torch.int64)
         vcounts.zero_()
@@ -600,12 +606,12 @@ class SplatTrainer:
         g = self.buf.get("gsp_wire", max(n_recv, 1) * wire, torch.float32)[: n_recv * wire]
         if my_views:
             n_slots = len(my_views)
-            mine = torch.as_tensor(my_views, dtype=torch.int64, device=dev)
+            mine = self._up(my_views, "mine", torch.int64)
             # canonical order of the received rows (per slot, ascending global id)
             sp_c, order = self._canonical(sp_recv.reshape(-1), gid_recv, n_recv, seg_rows, seg_slot, n_slots)
             slot_rows = np.bincount(np.asarray(seg_slot), weights=np.asarray(seg_rows), minlength=n_slots)
-            seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(slot_rows)[:-1]]).astype(np.int64), device=dev)
-            bits_t = torch.as_tensor(slot_bits.view(np.int64), device=dev)
+            seg_row0 = self._up(np.concatenate([[0], np.cumsum(slot_rows)[:-1]]), "seg_row0", torch.int64)
+            bits_t = self._up(slot_bits.view(np.int64), "slot_bits", torch.int64)
             if gt_batch is not None:
                 self._wait_gt()
             gt_slots = gt_batch.index_select(0, mine).contiguous() if gt_batch is not None else None
@@ -781,8 +787,8 @@ class SplatTrainer:
         bs_canonical_order).  Returns the reordered rows and `order`
         (canonical position -> received row)."""
         st, lib = nat.stream_handle(), nat.load()
-        seg_row0 = torch.as_tensor(np.concatenate([[0], np.cumsum(seg_rows)[:-1]]).astype(np.int64), device=self.dev)
-        seg_slot_t = torch.as_tensor(np.asarray(seg_slot, dtype=np.int32), device=self.dev)
+        seg_row0 = self._up(np.concatenate([[0], np.cumsum(seg_rows)[:-1]]), "canon_seg_row0", torch.int64)
+        seg_slot_t = self._up(seg_slot, "canon_seg_slot", torch.int32)
         order = self.buf.get("canon_order", max(n, 1), torch.int64)
         cgid = self.buf.get("canon_gid", max(n, 1), torch.int32)
         ws = self.buf.get("canon_ws", lib.bs_canonical_order_workspace(max(n, 1)), torch.uint8)

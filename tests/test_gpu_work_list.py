@@ -79,8 +79,9 @@ def test_list_chunks_matches_counts(cuda):
 
 
 def test_select_rows_and_copy_to_host(cuda):
-    """bs_select_rows (view ids as kernel parameters) and bs_copy_to_host (a
-    kernel store into mapped pinned memory) against torch."""
+    """bs_select_rows (view ids as kernel parameters), bs_upload (a host array
+    as kernel parameters) and bs_copy_to_host (a kernel store into mapped
+    pinned memory) against torch."""
     from paper_2512_20017_b200 import _native as nat
 
     table = torch.arange(40 * 7, dtype=torch.float32, device="cuda").reshape(40, 7)
@@ -96,6 +97,10 @@ def test_select_rows_and_copy_to_host(cuda):
     nat.call("bs_copy_to_host", nat.ptr(src), 72, pin.data_ptr(), nat.stream_handle())
     torch.cuda.synchronize()
     assert torch.equal(pin, src.cpu())
+    host = (np.arange(1300, dtype=np.int64) * 7919) % 104729  # > one 2 KB kernel-parameter chunk
+    dev = torch.full((1300,), -1, dtype=torch.int64, device="cuda")
+    nat.upload(host, dev)
+    assert np.array_equal(dev.cpu().numpy(), host)
     with pytest.raises(Exception):  # pageable host memory is refused
         nat.call("bs_copy_to_host", nat.ptr(src), 72, torch.zeros(9, dtype=torch.int64).data_ptr(),
                  nat.stream_handle())
