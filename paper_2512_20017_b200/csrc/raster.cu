@@ -700,14 +700,17 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
 // list with the same per-warp support filter; the backward repeats the
 // forward's chunk work (row gathers, support test, ballot, staging) and
 // re-reads every pixel's T, n_contrib, colour and ground truth.  Fused, each
-// warp appends the forward's kept splats (48-byte records with their
-// range-relative index) to a warp-private shared-memory list, turns its
-// pixels' final colours straight into dL/dC (L1 sign), and walks the list
-// back to front: no gathers, no support tests, no per-pixel reloads.  A warp
-// that keeps more than kKeep splats (the list wraps) falls back to the
-// backward's own chunked walk over global memory.  Per pair the arithmetic
-// is raster_fwd_kernel's / raster_bwd_kernel's, so the image is identical
-// and the gradients differ only by atomic order.
+// warp stages the forward's kept splats as 48-byte records in a warp-private
+// shared-memory list, blends them (predicated, no branch per pair), stores
+// in each record the ballot of the lanes it was blended into, drops the
+// records blended into no pixel after every chunk, turns its pixels' final
+// colours straight into dL/dC (L1 sign), and walks the list back to front,
+// two records per iteration, the mask standing in for the support and
+// contributor tests: no gathers, no per-pixel reloads.  A warp that keeps
+// more than kKeep splats (the list overflows) falls back to the backward's
+// own chunked walk over global memory.  Per pair the arithmetic is
+// raster_fwd_kernel's / raster_bwd_kernel's, so the image is identical and
+// the gradients differ only by atomic order.
 #ifndef BS_FUSED_KEEP
 #define BS_FUSED_KEEP 128  // swept on B200 (C2 raster ms): 64 2.93, 128 2.61, 256 (2 CTAs) 5.5; separate kernels 2.93
 #endif

@@ -525,7 +525,7 @@ constexpr int kKeep2 = BS_FUSED2_KEEP;  // kept-splat records per warp
 
 struct Kept2 {
   float4 rec[kKeep2][4];  // staged a, b, c, d (stage2 layout)
-  int2 idx[kKeep2];       // (G_SP row, range-relative index)
+  int2 idx[kKeep2];       // (G_SP row, mask of the lanes the splat was blended into)
 };
 
 template <bool kBg>
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(kT2, BS_FUSED2_CTAS) raster2d_fused_kernel(
       p.T = c ? nT : p.T;
       p.contrib = c ? rel + 1 : p.contrib;
       // the lanes this splat was blended into = the pairs the backward
-      // differentiates; replaces the range-relative index in the record
+      // differentiates (written after every lane's last read of the record)
       const uint32_t who = __ballot_sync(0xffffffffu, c);
       if (lane == 0) kp.idx[pos].y = (int)who;
     }
