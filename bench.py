@@ -26,6 +26,7 @@ materialises only its own shard's Gaussian attributes.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -370,6 +371,10 @@ def run_ours(args, cfg):
     step_AW = []
     if comm is not None:
         comm.bytes_fwd = comm.bytes_bwd = 0
+    # no Python garbage collection inside the timed loops: a collection pass
+    # stalls the host between two launches and leaves the GPU idle
+    gc.collect()
+    gc.disable()
     start.record()
     if comm is not None:
         comm.place_ms.clear()
@@ -386,6 +391,7 @@ def run_ours(args, cfg):
     if world > 1:
         torch.distributed.barrier()
     clk.__exit__(None, None, None)
+    gc.enable()
     launches = nat.launch_count() - lc0
     tr.last["n_visible_points"] = int((tr.buf.bufs["mask"][: tr.S] != 0).sum().item())
     ms = start.elapsed_time(end)
@@ -468,7 +474,10 @@ def run_ours(args, cfg):
         return e_start.elapsed_time(e_end), (time.perf_counter() - t0) * 1000.0, loss_pinned[-1]
 
     e2e_run(sched[:max(1, min(args.warmup, 3))])  # warm-up of the e2e path (untimed)
+    gc.collect()
+    gc.disable()
     e2e_ms, e2e_wall, loss_host = e2e_run(e2e_sched)
+    gc.enable()
     if world > 1:
         e2e_ms, e2e_wall = _max_over_ranks([e2e_ms, e2e_wall])
     e2e_value = B * len(e2e_sched) / (max(e2e_ms, e2e_wall) / 1000.0)

@@ -366,6 +366,12 @@ int32_t bs_bin_tiles_scatter_rec(const int32_t* row_bin, int64_t n_rows, const i
 int32_t bs_bin_tiles_sort(const uint64_t* inst_keys, const int32_t* ranges,
                           int32_t n_buckets, int32_t smem_cap,
                           uint32_t* inst_rows, void* stream);
+/* bs_bin_tiles_sort choosing the 129..256-key method from the average bucket
+ * occupancy n_inst / n_buckets (the register bitonic network for full
+ * buckets, the warp merge sort for sparse ones); same lists. */
+int32_t bs_bin_tiles_sort_n(const uint64_t* inst_keys, const int32_t* ranges,
+                            int32_t n_buckets, int32_t smem_cap, int64_t n_inst,
+                            uint32_t* inst_rows, void* stream);
 int32_t bs_bin_tiles_max_sort(void);
 int32_t bs_keys_low32(const uint64_t* keys, int64_t n, uint32_t* out,
                       void* stream);

@@ -117,6 +117,7 @@ _SIGS = {
     "bs_bin_tiles_offsets_workspace": (_SZ, [_I32]),
     "bs_bin_tiles_scatter": (_I32, [_P, _I64, _P, _P, _I32, _P, _I32, _P, _P, _I64, _I32, _P]),
     "bs_bin_tiles_sort": (_I32, [_P, _P, _I32, _I32, _P, _P]),
+    "bs_bin_tiles_sort_n": (_I32, [_P, _P, _I32, _I32, _I64, _P, _P]),
     "bs_bin_tiles_max_sort": (_I32, []),
     "bs_keys_low32": (_I32, [_P, _I64, _P, _P]),
     "bs_raster_fwd": (_I32, [C.POINTER(RasterDesc), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -82,7 +82,8 @@ def bin_buckets(buf, sp, n_rows, seg_row0, seg_slot, n_slots, slot_cams, tiles, 
     irows = buf.get("irows", max(keys.numel(), 1), torch.int32)[: max(n_inst, 1)]
     cap = min(sort_cap, lib.bs_bin_tiles_max_sort())
     # no bucket exceeds `biggest`: size classes above it are not launched
-    nat.call("bs_bin_tiles_sort", nat.ptr(keys), nat.ptr(ranges), nb, max(1, min(cap, biggest)), nat.ptr(irows), st)
+    nat.call("bs_bin_tiles_sort_n", nat.ptr(keys), nat.ptr(ranges), nb, max(1, min(cap, biggest)), n_inst,
+             nat.ptr(irows), st)
     if biggest > cap:  # rare: buckets beyond the shared-memory sort
         from .culling import radix_sort_u64
 

@@ -502,3 +502,9 @@ def test_bucket_sort_every_size_class(cuda, sizes):
     for s0, n in zip(starts, sizes):
         want = (np.sort(keys[s0:s0 + n]) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
         assert np.array_equal(got[s0:s0 + n], want), n
+    # the occupancy-driven variant, both methods for 129..256 keys: same lists
+    for n_inst in (0, 1 << 40):
+        out2 = torch.full((max(total, 1),), -1, dtype=torch.int32, device="cuda")
+        nat.call("bs_bin_tiles_sort_n", nat.ptr(kd), nat.ptr(rd), len(sizes), 16384, n_inst, nat.ptr(out2),
+                 nat.stream_handle())
+        assert torch.equal(out2, out)
