@@ -32,11 +32,25 @@ struct RowRanker {
 
   // Call with all threads of the CTA.  Returns nothing; rows are obtained by
   // row_of() for set bits until the next advance().
+  // kSparse (the visible-chunk kernels): ballots only for the views some
+  // lane of the warp sees (a sparse step's chunk is usually visible in one
+  // or two of the batch's views); the other views' entries are zero
+  template <bool kSparse = false>
   __device__ void round(uint32_t mask, int B) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int v = 0; v < B; ++v) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, (mask >> v) & 1u);
-      if (lane == 0) s_bal[w * kMaxViews + v] = bal;
+    if constexpr (kSparse) {
+      const uint32_t seen = __reduce_or_sync(0xffffffffu, mask);
+      if (lane < B && !((seen >> lane) & 1u)) s_bal[w * kMaxViews + lane] = 0u;
+      for (uint32_t rest = seen; rest; rest &= rest - 1u) {
+        const int v = __ffs(rest) - 1;
+        const uint32_t bal = __ballot_sync(0xffffffffu, (mask >> v) & 1u);
+        if (lane == 0) s_bal[w * kMaxViews + v] = bal;
+      }
+    } else {
+      for (int v = 0; v < B; ++v) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (mask >> v) & 1u);
+        if (lane == 0) s_bal[w * kMaxViews + v] = bal;
+      }
     }
     __syncthreads();
   }
@@ -183,7 +197,7 @@ struct Model2 {
   __device__ static void from_moments(const F& f, float* gs) { gsp2_from_moments(f, gs); }
 };
 
-template <class M>
+template <class M, bool kWork>
 #ifndef BS_PROJ_FWD_CTAS
 #define BS_PROJ_FWD_CTAS 4  // CTAs per SM the projection's register budget is sized for
 #endif
@@ -219,7 +233,7 @@ __device__ __forceinline__ void project_fwd_chunk(const ProjArgs& a, float* __re
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    rk.round(mask, B);
+    rk.template round<kWork>(mask, B);
     if (mask) {
       PointIn pt;
       load_point(a.params, a.S, i, 0, pt);  // geometry planes; SH from shared memory
@@ -273,13 +287,13 @@ __device__ __forceinline__ void project_fwd_chunk(const ProjArgs& a, float* __re
 template <class M, bool kWork>
 __global__ void __launch_bounds__(kProjThreads, BS_PROJ_FWD_CTAS) project_fwd_kernel(ProjArgs a, float* __restrict__ sp) {
   if constexpr (!kWork) {
-    project_fwd_chunk<M>(a, sp, blockIdx.x, blockIdx.y, gridDim.y);
+    project_fwd_chunk<M, false>(a, sp, blockIdx.x, blockIdx.y, gridDim.y);
     return;
   }
   const int n = *a.work_count;
   for (int w = blockIdx.x; w < n; w += gridDim.x) {
     const int item = __ldg(a.work_list + w);
-    project_fwd_chunk<M>(a, sp, item / a.max_chunks, item % a.max_chunks, a.max_chunks);
+    project_fwd_chunk<M, true>(a, sp, item / a.max_chunks, item % a.max_chunks, a.max_chunks);
     __syncthreads();  // the chunk's shared-memory state is rebuilt by the next
   }
 }
@@ -439,7 +453,7 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamConsts c, float4* __restr
   }
 }
 
-template <class M>
+template <class M, bool kWork>
 __device__ __forceinline__ void project_bwd_adam_chunk(const ProjArgs& a, const AdamConsts& c,
                                                        const float* __restrict__ gsp, float4* params,
                                                        float4* __restrict__ m, float4* __restrict__ v, int g, int cy,
@@ -493,7 +507,7 @@ __device__ __forceinline__ void project_bwd_adam_chunk(const ProjArgs& a, const 
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    rk.round(mask, B);
+    rk.template round<kWork>(mask, B);
     if (ok && !(c.selective && mask == 0u)) {
       // geometry gradient in registers, the 48 SH gradients in this thread's
       // shared-memory column (keeps the register peak below the
@@ -561,7 +575,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
                                                                            float4* __restrict__ m,
                                                                            float4* __restrict__ v) {
   if constexpr (!kWork) {
-    project_bwd_adam_chunk<M>(a, c, gsp, params, m, v, blockIdx.x, blockIdx.y, gridDim.y);
+    project_bwd_adam_chunk<M, false>(a, c, gsp, params, m, v, blockIdx.x, blockIdx.y, gridDim.y);
     return;
   }
   // selective Adam over the visible chunks only (the launcher passes the list
@@ -569,7 +583,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) project_bwd_adam_kernel(ProjA
   const int n = *a.work_count;
   for (int w = blockIdx.x; w < n; w += gridDim.x) {
     const int item = __ldg(a.work_list + w);
-    project_bwd_adam_chunk<M>(a, c, gsp, params, m, v, item / a.max_chunks, item % a.max_chunks, a.max_chunks);
+    project_bwd_adam_chunk<M, true>(a, c, gsp, params, m, v, item / a.max_chunks, item % a.max_chunks, a.max_chunks);
     __syncthreads();
   }
 }
