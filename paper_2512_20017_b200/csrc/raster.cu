@@ -717,6 +717,9 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
 #ifndef BS_FUSED_CTAS
 #define BS_FUSED_CTAS 4
 #endif
+#ifndef BS_FUSED_PAIR_MERGE
+#define BS_FUSED_PAIR_MERGE 1  // A/B on B200 (C2 raster): 0 2.474, 1 (sparse pairs) 2.443, 2 (all disjoint pairs) 2.456 ms
+#endif
 #ifndef BS_FUSED_FWD_SEL
 #define BS_FUSED_FWD_SEL 1  // A/B on B200 (C2 raster): branchy 2.545, predicated 2.484 ms
 #endif
@@ -928,12 +931,54 @@ __global__ void __launch_bounds__(256, BS_FUSED_CTAS) raster_fused_kernel(
       const KeptRec& r1 = kept[k];
       const KeptRec& r0 = kept[k - 1];
       const float4 a1 = r1.a, b1 = r1.b, c1 = r1.c;
-      const float4 a0 = r0.a, b0 = r0.b;
+      const float4 a0 = r0.a, b0 = r0.b, c0 = r0.c;
+#if BS_FUSED_PAIR_MERGE
+      const uint32_t m1 = __float_as_uint(c1.w), m0 = __float_as_uint(c0.w);
+#if BS_FUSED_PAIR_MERGE >= 2
+      if ((m1 & m0) == 0u) {
+#else
+      if ((m1 & m0) == 0u && __popc(m1) <= kSparseLanes && __popc(m0) <= kSparseLanes) {
+#endif
+        // two splats on disjoint pixels: one pass of the pair math, each
+        // lane on the splat that covers its pixel (the other does not touch
+        // the pixel, so their order does not matter for it)
+        const bool in1 = (m1 >> lane) & 1u, in0 = (m0 >> lane) & 1u;
+        const bool any = in1 || in0;
+        const float4 a = in1 ? a1 : a0, b = in1 ? b1 : b0;
+        const float cb = in1 ? c1.x : c0.x;
+        PairFront f;
+        pair_front(f, a, b, npx);
+        float g[9];
+        pair_back<kBg>(p, f, b, cb, any, g);
+#if BS_FUSED_PAIR_MERGE >= 2
+        if (__popc(m1) <= kSparseLanes && __popc(m0) <= kSparseLanes) {
+#endif
+          if (any) {
+            float* dst = g_sp + (int64_t)__float_as_uint(in1 ? c1.z : c0.z) * BS_GSP_FLOATS;
+            atomicAdd(reinterpret_cast<float4*>(dst), make_float4(g[0], g[1], g[2], g[3]));
+            atomicAdd(reinterpret_cast<float4*>(dst + 4), make_float4(g[4], g[5], g[6], g[7]));
+            atomicAdd(dst + 8, g[8]);
+          }
+#if BS_FUSED_PAIR_MERGE >= 2
+        } else {
+          // each splat's own lanes (a dense one reduces the others' as zero)
+          float gm[9];
+#pragma unroll
+          for (int t = 0; t < 9; ++t) gm[t] = in1 ? g[t] : 0.f;
+          reduce_splat(gm, m1, in1, g_sp + (int64_t)__float_as_uint(c1.z) * BS_GSP_FLOATS);
+#pragma unroll
+          for (int t = 0; t < 9; ++t) gm[t] = in0 ? g[t] : 0.f;
+          reduce_splat(gm, m0, in0, g_sp + (int64_t)__float_as_uint(c0.z) * BS_GSP_FLOATS);
+        }
+#endif
+        continue;
+      }
+#endif
       PairFront f1, f0;
       pair_front(f1, a1, b1, npx);
       pair_front(f0, a0, b0, npx);
       bwd_rec<kBg>(p, f1, b1, c1, g_sp);
-      bwd_rec<kBg>(p, f0, b0, r0.c, g_sp);
+      bwd_rec<kBg>(p, f0, b0, c0, g_sp);
     }
     if (k == 0) {
       const KeptRec& r = kept[0];
