@@ -718,7 +718,8 @@ __global__ void __launch_bounds__(Region<PPL>::kThreads, (PPL == 1 ? 1024 : 768)
 #define BS_FUSED_CTAS 4
 #endif
 #ifndef BS_FUSED_PAIR_MERGE
-#define BS_FUSED_PAIR_MERGE 1  // A/B on B200 (C2 raster): 0 2.474, 1 (sparse pairs) 2.443, 2 (all disjoint pairs) 2.456 ms
+#define BS_FUSED_PAIR_MERGE 1  // A/B on B200 (C2 raster): 0 2.474, 1 (sparse pairs) 2.443, 2 (all disjoint pairs) 2.456 ms;
+                               // the record of each lane's splat re-read per lane instead of selected: 2.464
 #endif
 #ifndef BS_FUSED_FWD_SEL
 #define BS_FUSED_FWD_SEL 1  // A/B on B200 (C2 raster): branchy 2.545, predicated 2.484 ms
