@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kT2, BS_R2_BWD_CTAS) raster2d_bwd_kernel(
 #define BS_FUSED2_CTAS 3
 #endif
 #ifndef BS_FUSED2_PAIR_MERGE
-#define BS_FUSED2_PAIR_MERGE 1  // A/B on B200 (C3 raster): 0 6.500, 1 6.300 ms
+#define BS_FUSED2_PAIR_MERGE 2  // A/B on B200 (C3 raster): 0 6.500, 1 (sparse pairs) 6.303, 2 (all disjoint pairs) 6.242 ms
 #endif
 constexpr int kKeep2 = BS_FUSED2_KEEP;  // kept-splat records per warp
 
@@ -667,6 +667,26 @@ __global__ void __launch_bounds__(kT2, BS_FUSED2_CTAS) raster2d_fused_kernel(
       const int2 id1 = kp.idx[k], id0 = kp.idx[k - 1];
 #if BS_FUSED2_PAIR_MERGE
       const uint32_t m1 = (uint32_t)id1.y, m0 = (uint32_t)id0.y;
+#if BS_FUSED2_PAIR_MERGE >= 2
+      if ((m1 & m0) == 0u && (__popc(m1) > kSparse2 || __popc(m0) > kSparse2)) {
+        // disjoint with a dense one: one pass, then each surfel's own lanes
+        // reduced (the other surfel's lanes as zero)
+        const bool in1 = (m1 >> lane) & 1u, in0 = (m0 >> lane) & 1u;
+        const int kk = in1 ? k : k - 1;
+        const float4 cc = kp.rec[kk][3];
+        Front2 f;
+        bwd2_front(f, kp.rec[kk][0], kp.rec[kk][1], kp.rec[kk][2], cc.w, pxf, pyf, oxf, oyf);
+        float g[16], gm[16];
+        bwd2_back<kBg>(q, f, cc, in1 || in0, pxf, pyf, g);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) gm[t] = in1 ? g[t] : 0.f;
+        reduce2(gm, m1, in1, g_sp + (int64_t)(uint32_t)id1.x * kGSP2);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) gm[t] = in0 ? g[t] : 0.f;
+        reduce2(gm, m0, in0, g_sp + (int64_t)(uint32_t)id0.x * kGSP2);
+        continue;
+      }
+#endif
       if ((m1 & m0) == 0u && __popc(m1) <= kSparse2 && __popc(m0) <= kSparse2) {
         // two sparse surfels on disjoint pixels: one pass, each lane reading
         // the record of the surfel that covers its pixel (see raster.cu)
