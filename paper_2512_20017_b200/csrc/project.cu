@@ -22,6 +22,11 @@ constexpr int kAdamBatch = BS_ADAM_BATCH;
 #ifndef BS_ADAM_SMEM_PARAMS
 #define BS_ADAM_SMEM_PARAMS 1
 #endif  // parameter planes per batch of Adam loads in the fused kernel
+#ifndef BS_GSP_LDCS
+#define BS_GSP_LDCS 1
+#endif  // 1: G_SP rows read evict-first (ld.global.cs) by the projection backward: their
+        // last use before the next step's projection clears them (C2 0.366 -> 0.360 ms,
+        // DRAM reads 1.025 -> 0.982 GB; C3 0.787 -> 0.755 ms)
 #ifndef BS_ADAM_STREAM
 #define BS_ADAM_STREAM 2
 #endif  // 2: parameters and moments written evict-first (st.global.cs): the lines are
@@ -323,8 +328,17 @@ __device__ __forceinline__ void point_backward(const ProjArgs& a, const bs_camer
     const int64_t row = s_row0[v] + rk.row_offset(v);
     float gs[M::kGSP];
     const float* src = gsp + row * M::kGSP;
+#if BS_GSP_LDCS
+    // the row's last use before the next step's projection clears it: evict-first
+#pragma unroll
+    for (int k = 0; k < M::kGSP / 4; ++k) {
+      const float4 t = __ldcs(reinterpret_cast<const float4*>(src) + k);
+      gs[4 * k] = t.x, gs[4 * k + 1] = t.y, gs[4 * k + 2] = t.z, gs[4 * k + 3] = t.w;
+    }
+#else
 #pragma unroll
     for (int k = 0; k < M::kGSP; ++k) gs[k] = src[k];
+#endif
     typename M::F f;
     float wk[16];  // SH direction weights, computed with the colour (one pass over the coefficients)
     M::forward(pt, pre, sh, s_cam[v], a.n_sh, f, M::kFuseWk ? gs + M::kGcol : nullptr, M::kFuseWk ? wk : nullptr);
