@@ -34,6 +34,28 @@ constexpr int kAdamBatch = BS_ADAM_BATCH;
         // the planes still to come (C2: 0.376 -> 0.366 ms, C3: 0.787 -> 0.779 ms);
         // 1: also the moment loads (ld.global.cs; 0.368 ms); 0: no hints
 constexpr int kProjWarps = kProjThreads / 32;
+#ifndef BS_SH_EVICT_FIRST
+#define BS_SH_EVICT_FIRST 1
+#endif  // 1: the projection kernels stage SH coefficients with an L2 evict-first policy
+        // (with BS_GSP_ZERO_CS: C2 projection 0.167 -> 0.165 ms, fused Adam 0.362 -> 0.356 ms;
+        // C3 fused Adam 0.759 -> 0.748 ms; profiles/r2z_ab_proj_hints.txt)
+#ifndef BS_GSP_ZERO_CS
+#define BS_GSP_ZERO_CS 1
+#endif  // 1: the projection clears G_SP rows with evict-first stores
+
+// 16-byte global -> shared copy of one SH float4 (L2::cache_hint with an
+// evict-first policy when BS_SH_EVICT_FIRST: the coefficients are read once
+// per kernel, so their lines should not displace the kernel's outputs in L2)
+__device__ __forceinline__ void sh_copy16(uint32_t dst, const void* src) {
+#if BS_SH_EVICT_FIRST
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+#else
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#endif
+}
+
 constexpr int kMaxViews = 32;
 
 // Per-round in-group ranks of the set view bits of every thread.
@@ -239,8 +261,7 @@ __device__ __forceinline__ void project_fwd_chunk(const ProjArgs& a, float* __re
       const int sh_q = (3 * a.n_sh + 3) / 4;
       for (int q = 0; q < sh_q; ++q) {
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_sh4f + q * kProjThreads + threadIdx.x);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(a.params + (int64_t)(3 + q) * a.S + i)
-                     : "memory");
+        sh_copy16(dst, a.params + (int64_t)(3 + q) * a.S + i);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -283,7 +304,13 @@ __device__ __forceinline__ void project_fwd_chunk(const ProjArgs& a, float* __re
         if (a.gsp_zero) {
           float4* z = reinterpret_cast<float4*>(a.gsp_zero + row * M::kGSP);
 #pragma unroll
-          for (int k = 0; k < M::kGSP / 4; ++k) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int k = 0; k < M::kGSP / 4; ++k) {
+#if BS_GSP_ZERO_CS
+            __stcs(z + k, make_float4(0.f, 0.f, 0.f, 0.f));
+#else
+            z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
+          }
         }
       }
     }
@@ -522,8 +549,7 @@ __device__ __forceinline__ void project_bwd_adam_chunk(const ProjArgs& a, const 
     if (mask) {
       for (int q = 0; q < sh_q; ++q) {
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_sh4 + q * kProjThreads + threadIdx.x);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(params + (int64_t)(3 + q) * a.S + i)
-                     : "memory");
+        sh_copy16(dst, params + (int64_t)(3 + q) * a.S + i);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
