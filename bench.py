@@ -248,9 +248,9 @@ _STAGE_KERNEL = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_ke
 
 # committed ncu --set full summaries (newest first) per (model, configuration)
 # they captured (per launch of that workload: counts and bytes do not transfer)
-TRAFFIC_FILES = {("3dgs", "c2"): ("r2u_kernel_traffic.json", "r2v_kernel_traffic.json", "r2y_kernel_traffic.json", "r2g_kernel_traffic.json",
+TRAFFIC_FILES = {("3dgs", "c2"): ("r2z_kernel_traffic.json", "r2u_kernel_traffic.json", "r2v_kernel_traffic.json", "r2y_kernel_traffic.json", "r2g_kernel_traffic.json",
                                   "r2_kernel_traffic.json", "r1_kernel_traffic.json"),
-                 ("2dgs", "c3"): ("r2u_kernel_traffic.json", "r2v_kernel_traffic.json", "r2y_kernel_traffic.json", "r2g_kernel_traffic.json",
+                 ("2dgs", "c3"): ("r2z_kernel_traffic.json", "r2u_kernel_traffic.json", "r2v_kernel_traffic.json", "r2y_kernel_traffic.json", "r2g_kernel_traffic.json",
                                   "r2_kernel_traffic.json", "r1_kernel_traffic.json"),
                  ("3dgs", "c4"): ("r2v_kernel_traffic_c4.json", "r2y_kernel_traffic_c4.json")}
 _PROFILED = {"3dgs": "c2", "2dgs": "c3"}
