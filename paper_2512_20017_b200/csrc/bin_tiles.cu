@@ -329,6 +329,19 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&x)[E], int lane) {
   }
 }
 
+#ifndef BS_SORT_LDCS
+#define BS_SORT_LDCS 1  // C2 bin 0.2255 -> 0.2236 ms, C3 0.547 -> 0.541 ms (profiles/r2z_ab_sort_ldcs.txt)
+#endif
+// A bucket sort reads each instance key once (its last use): evict-first
+// when BS_SORT_LDCS, so the sorted row lists the raster reads next keep L2.
+__device__ __forceinline__ uint64_t sort_key_load(const uint64_t* p) {
+#if BS_SORT_LDCS
+  return __ldcs(reinterpret_cast<const unsigned long long*>(p));
+#else
+  return __ldg(p);
+#endif
+}
+
 template <int E>
 __device__ __forceinline__ void sort_bucket_regs(const uint64_t* __restrict__ keys, int start, int n,
                                                  uint32_t* __restrict__ rows, int lane) {
@@ -336,7 +349,7 @@ __device__ __forceinline__ void sort_bucket_regs(const uint64_t* __restrict__ ke
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = lane * E + e;
-    x[e] = i < n ? keys[start + i] : ~0ull;
+    x[e] = i < n ? sort_key_load(keys + start + i) : ~0ull;
   }
   warp_bitonic<E>(x, lane);
 #pragma unroll
@@ -367,7 +380,7 @@ template <int E>
 __device__ __forceinline__ void warp_merge_sort(const uint64_t* __restrict__ keys, int start, int n,
                                                 uint32_t* __restrict__ rows, uint64_t* sm, int lane) {
   constexpr int M = 32 * E;
-  for (int i = lane; i < M; i += 32) sm[mpad(i)] = i < n ? __ldg(keys + start + i) : ~0ull;
+  for (int i = lane; i < M; i += 32) sm[mpad(i)] = i < n ? sort_key_load(keys + start + i) : ~0ull;
   __syncwarp();
   uint64_t x[E];
 #pragma unroll
